@@ -1,0 +1,116 @@
+/* Extensions of the treemg C interface served by libtreemg_b200.so.
+ *
+ * 1. Run-result history accessor ("add an extension accessor
+ *    without changing existing signatures") -- the per-sweep rows the
+ *    reference only writes to <out>.csv (proj/src/runner.cpp:318-329).
+ *
+ * 2. The device-resident multilevel hierarchy: the drop-in for the C++ cycle
+ *    API  td_add / td_bpx (proj/include/treemg/cycles.hpp:56-62,
+ *    proj/src/cycles.cpp:336-354) acting on a Spacetree.  The spacetree's
+ *    hash-per-level storage (proj/src/spacetree.cpp) is replaced by per-level
+ *    lattice arrays in HBM; the handle owns them plus one CUDA stream.  Field
+ *    import/export (full level lattice, axis 0 fastest, interleaved re/im
+ *    doubles) lets the reference's cycle tests run against it.
+ *
+ * Extension configuration keys accepted by treemg_config_set (on top of the
+ * reference's keys, runner.cpp:81-106):
+ *   rhs = analytic | seeded     seeded: f = unit_rand complex, keyed on the
+ *                               final-lattice position
+ *   rhs_seed = <u64>            default 12345
+ *   rhs_mask = none | sphere    f zero outside |x - 1/2|^2 < 0.04
+ *   precision = exact | fast    exact: bit-identical iterates to the reference
+ *                               fast: FMA, correction-form coarse levels
+ *   max_vertices = <n>          vertex cap (reference default 8388608)
+ *   hb_sweeps = <k>             hierarchical-basis mask for sweeps 1..k, then off
+ *   fmg_from = <level>          FMG unfolding from <level> up to `level`
+ *   fmg_stage_cap = <n>         sweeps per FMG stage (default max_sweeps)
+ */
+
+#ifndef TREEMG_B200_H
+#define TREEMG_B200_H
+
+#include "treemg.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- 1. history ---------------------------------------------------------- */
+int treemg_result_history_rows(const treemg_result* res);
+/* row i: sweep, workUnits, vertexCount, maxNorm, euclid, hNorm */
+treemg_status treemg_result_history_row(const treemg_result* res, int i, double* out6);
+/* device time of the cycles of the run in milliseconds (CUDA events on the run's stream) */
+double treemg_result_device_ms(const treemg_result* res);
+
+/* ---- 2. device hierarchy ------------------------------------------------- */
+typedef struct tmg_hierarchy tmg_hierarchy;
+
+typedef struct tmg_problem {
+    int dim;                       /* 1..3 */
+    int levels;                    /* finest level L (regular grid, 3^L cells per axis) */
+    int ell_min;                   /* coarsest smoothed level (spacetree.hpp Config::ellMin) */
+    double theta;                  /* cell rotation, radians (ProblemSpec::thetaGlobal) */
+    double phi_re, phi_im;         /* constant Helmholtz shift phi */
+    int chi_kind;                  /* 0 zero, 1 sin product, 2 ball indicator, 3 seeded */
+    unsigned long long rhs_seed;
+    int rhs_sphere;
+    int precision;                 /* 0 exact, 1 fast */
+    long long max_vertices;        /* 0: reference default 8388608 */
+    int device;                    /* CUDA device ordinal */
+} tmg_problem;
+
+typedef struct tmg_policy {        /* OmegaPolicy, proj/include/treemg/cycles.hpp:17-24 */
+    int kind;                      /* 0 jacobi-only, 1 undamped, 2 lgrid, 3 exponential, 4 transition */
+    double omega_re, omega_im;
+    int lgrid;
+    int hb;
+    int bpx;
+    int two_phase;
+} tmg_policy;
+
+typedef struct tmg_sweep_stats {   /* SweepStats, cycles.hpp:37-45 (channel 0) */
+    double max_norm, euclid_norm, h_norm;
+    long long updated_fine_vertices;
+} tmg_sweep_stats;
+
+treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out);
+void tmg_hierarchy_destroy(tmg_hierarchy* h);
+
+/* One cycle; n is the 1-based sweep counter (cycles.cpp:336-354). */
+treemg_status tmg_td_add(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
+treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
+
+long long tmg_lattice_size(const tmg_hierarchy* h, int level);
+/* field: u chi r rhat uhat diag sc sf si sinext; out: 2*lattice_size doubles */
+treemg_status tmg_get_field(tmg_hierarchy* h, int level, const char* field, double* out);
+treemg_status tmg_set_field(tmg_hierarchy* h, int level, const char* field, const double* in);
+/* proj/tests/test_util.hpp:48-65 semantics: interior values of the finest
+ * level (interior lattice order), injected upward, pipeline state reset */
+treemg_status tmg_set_fine_interior_u(tmg_hierarchy* h, const double* u);
+/* proj/src/cycles.cpp:812-840 */
+treemg_status tmg_set_random_initial_guess(tmg_hierarchy* h, unsigned long long seed);
+/* nodal right-hand side chi at the finest lattice (host buffer, 2*lattice
+ * doubles); rebuilds the consistent-mass load vector on the device */
+treemg_status tmg_set_fine_rhs(tmg_hierarchy* h, const double* chi_nodal);
+/* FNV-1a over (re+0.0, im+0.0) bit patterns of a level field, lattice order */
+unsigned long long tmg_field_hash(tmg_hierarchy* h, int level, const char* field);
+
+/* Timing: runs `count` cycles starting at sweep counter n0 with CUDA events on
+ * the hierarchy's stream; out[0] = total ms, out[1] = ms in the fine-level
+ * residual kernel (average per cycle), out[2] = ms in the fine-level
+ * correction kernel (average per cycle), out[3] = kernel launches per cycle. */
+treemg_status tmg_time_cycles(tmg_hierarchy* h, const tmg_policy* pol, int n0, int count, int flush_l2,
+                              double* out4);
+
+/* e2e step through the boundary: host chi (pinned or pageable) -> device load
+ * vector -> one cycle -> host norms.  out3 = max, euclid, h. */
+treemg_status tmg_e2e_step(tmg_hierarchy* h, const tmg_policy* pol, int n, const double* chi_nodal,
+                           double* out3);
+
+const char* tmg_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TREEMG_B200_H */

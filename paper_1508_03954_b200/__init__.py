@@ -1,0 +1,301 @@
+"""treemg on B200: the additive multilevel Helmholtz cycle of Reps & Weinzierl
+(arXiv 1508.03954) as hand-written sm_100a kernels behind the reference's
+C interface.
+
+This module is the Python-side mirror of the reference interface for the hot
+path (ctypes over ``libtreemg_b200.so``):
+
+* :func:`run` / :class:`RunResult` -- ``treemg_run`` (proj/include/treemg.h,
+  proj/src/capi.cpp:67-112) with the per-sweep history extension;
+* :class:`Hierarchy` -- the device-resident drop-in for the C++ cycle API
+  ``td_add`` / ``td_bpx`` (proj/include/treemg/cycles.hpp:56-62) plus field
+  import/export, so the reference's cycle tests read the same here.
+
+There is no CPU fallback: importing works without a GPU (so the CPU test
+suite can check the C-ABI exports), but every compute call fails loudly when
+the CUDA library or the device is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libtreemg_b200.so")
+
+STATUS = {0: "TREEMG_OK", 1: "TREEMG_E_USAGE", 2: "TREEMG_E_CAPACITY", 3: "TREEMG_E_RUNTIME"}
+OUTCOME = {0: "converged", 1: "budget-exhausted", 2: "diverged"}
+OMEGA_KINDS = {"jacobi-only": 0, "undamped": 1, "lgrid": 2, "exponential": 3, "transition": 4}
+CHI_KINDS = {"zero": 0, "sin": 1, "ball": 2, "seeded": 3}
+
+# The 14 entry points of proj/include/treemg.h and the extensions of
+# include/treemg_b200.h, all exported by libtreemg_b200.so.
+TREEMG_SYMBOLS = [
+    "treemg_version", "treemg_last_error", "treemg_config_new", "treemg_config_free",
+    "treemg_config_load_file", "treemg_config_set", "treemg_run", "treemg_result_free",
+    "treemg_result_outcome", "treemg_result_sweeps", "treemg_result_work_units",
+    "treemg_result_vertex_count", "treemg_result_final_norm", "treemg_result_first_norm",
+]
+EXTENSION_SYMBOLS = [
+    "treemg_result_history_rows", "treemg_result_history_row", "treemg_result_device_ms",
+    "tmg_hierarchy_create", "tmg_hierarchy_destroy", "tmg_td_add", "tmg_td_bpx", "tmg_lattice_size",
+    "tmg_get_field", "tmg_set_field", "tmg_set_fine_interior_u", "tmg_set_random_initial_guess",
+    "tmg_set_fine_rhs", "tmg_field_hash", "tmg_time_cycles", "tmg_e2e_step", "tmg_last_error",
+]
+
+_lib = None
+
+
+class TreemgError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"{STATUS.get(status, status)}: {message}")
+        self.status = status
+        self.message = message
+
+
+class _Problem(ctypes.Structure):
+    _fields_ = [("dim", ctypes.c_int), ("levels", ctypes.c_int), ("ell_min", ctypes.c_int),
+                ("theta", ctypes.c_double), ("phi_re", ctypes.c_double), ("phi_im", ctypes.c_double),
+                ("chi_kind", ctypes.c_int), ("rhs_seed", ctypes.c_ulonglong), ("rhs_sphere", ctypes.c_int),
+                ("precision", ctypes.c_int), ("max_vertices", ctypes.c_longlong), ("device", ctypes.c_int)]
+
+
+class _Policy(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("omega_re", ctypes.c_double), ("omega_im", ctypes.c_double),
+                ("lgrid", ctypes.c_int), ("hb", ctypes.c_int), ("bpx", ctypes.c_int), ("two_phase", ctypes.c_int)]
+
+
+class _Stats(ctypes.Structure):
+    _fields_ = [("max_norm", ctypes.c_double), ("euclid_norm", ctypes.c_double), ("h_norm", ctypes.c_double),
+                ("updated_fine_vertices", ctypes.c_longlong)]
+
+
+def build(force: bool = False) -> str:
+    from . import build as _b
+    return _b.build(force=force)
+
+
+def lib():
+    """The loaded CUDA library; raises if it is not built (no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: build it with `python -m paper_1508_03954_b200.build` "
+                               "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        vp, cp, ip, dp, pd = ctypes.c_void_p, ctypes.c_char_p, ctypes.c_int, ctypes.c_double, ctypes.POINTER(ctypes.c_double)
+        L.treemg_version.restype = ctypes.c_uint
+        L.treemg_last_error.restype = cp
+        L.tmg_last_error.restype = cp
+        L.treemg_config_new.restype = vp
+        L.treemg_config_free.argtypes = [vp]
+        L.treemg_config_set.restype = ip
+        L.treemg_config_set.argtypes = [vp, cp, cp]
+        L.treemg_config_load_file.restype = ip
+        L.treemg_config_load_file.argtypes = [vp, cp]
+        L.treemg_run.restype = ip
+        L.treemg_run.argtypes = [vp, ctypes.POINTER(vp)]
+        L.treemg_result_free.argtypes = [vp]
+        for n, rt in (("treemg_result_outcome", ip), ("treemg_result_sweeps", ip),
+                      ("treemg_result_work_units", dp), ("treemg_result_vertex_count", ctypes.c_longlong),
+                      ("treemg_result_first_norm", dp), ("treemg_result_history_rows", ip),
+                      ("treemg_result_device_ms", dp)):
+            getattr(L, n).restype = rt
+            getattr(L, n).argtypes = [vp]
+        L.treemg_result_final_norm.restype = dp
+        L.treemg_result_final_norm.argtypes = [vp, cp, ip]
+        L.treemg_result_history_row.restype = ip
+        L.treemg_result_history_row.argtypes = [vp, ip, pd]
+        L.tmg_hierarchy_create.restype = ip
+        L.tmg_hierarchy_create.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(vp)]
+        L.tmg_hierarchy_destroy.argtypes = [vp]
+        for n in ("tmg_td_add", "tmg_td_bpx"):
+            getattr(L, n).restype = ip
+            getattr(L, n).argtypes = [vp, ctypes.POINTER(_Policy), ip, ctypes.POINTER(_Stats)]
+        L.tmg_lattice_size.restype = ctypes.c_longlong
+        L.tmg_lattice_size.argtypes = [vp, ip]
+        L.tmg_get_field.restype = ip
+        L.tmg_get_field.argtypes = [vp, ip, cp, pd]
+        L.tmg_set_field.restype = ip
+        L.tmg_set_field.argtypes = [vp, ip, cp, pd]
+        L.tmg_set_fine_interior_u.restype = ip
+        L.tmg_set_fine_interior_u.argtypes = [vp, pd]
+        L.tmg_set_random_initial_guess.restype = ip
+        L.tmg_set_random_initial_guess.argtypes = [vp, ctypes.c_ulonglong]
+        L.tmg_set_fine_rhs.restype = ip
+        L.tmg_set_fine_rhs.argtypes = [vp, pd]
+        L.tmg_field_hash.restype = ctypes.c_ulonglong
+        L.tmg_field_hash.argtypes = [vp, ip, cp]
+        L.tmg_time_cycles.restype = ip
+        L.tmg_time_cycles.argtypes = [vp, ctypes.POINTER(_Policy), ip, ip, ip, pd]
+        L.tmg_e2e_step.restype = ip
+        L.tmg_e2e_step.argtypes = [vp, ctypes.POINTER(_Policy), ip, pd, pd]
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise TreemgError(st, lib().treemg_last_error().decode())
+
+
+def _pd(a: np.ndarray):
+    return a.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
+
+
+@dataclass
+class RunResult:
+    """RunResult of proj/include/treemg/runner.hpp:60-68 via the C-ABI."""
+    outcome: str
+    sweeps: int
+    work_units: float
+    vertex_count: int
+    first_norm: float
+    final_norm: Dict[str, float]
+    history: np.ndarray = field(repr=False)
+    device_ms: float = 0.0
+
+
+def run(cfg: Dict[str, object], out_prefix: Optional[str] = None) -> RunResult:
+    """treemg_config_set for every key, then treemg_run (synchronous)."""
+    L = lib()
+    c = L.treemg_config_new()
+    try:
+        for k, v in cfg.items():
+            _check(L.treemg_config_set(c, str(k).encode(), str(v).encode()))
+        if out_prefix:
+            _check(L.treemg_config_set(c, b"out", out_prefix.encode()))
+        res = ctypes.c_void_p()
+        _check(L.treemg_run(c, ctypes.byref(res)))
+    finally:
+        L.treemg_config_free(c)
+    try:
+        rows = L.treemg_result_history_rows(res)
+        hist = np.zeros((rows, 6))
+        buf = np.zeros(6)
+        for i in range(rows):
+            _check(L.treemg_result_history_row(res, i, _pd(buf)))
+            hist[i] = buf
+        return RunResult(
+            outcome=OUTCOME[L.treemg_result_outcome(res)], sweeps=L.treemg_result_sweeps(res),
+            work_units=L.treemg_result_work_units(res), vertex_count=L.treemg_result_vertex_count(res),
+            first_norm=L.treemg_result_first_norm(res),
+            final_norm={w: L.treemg_result_final_norm(res, w.encode(), -1) for w in ("max", "euclid", "h")},
+            history=hist, device_ms=L.treemg_result_device_ms(res))
+    finally:
+        L.treemg_result_free(res)
+
+
+@dataclass
+class Policy:
+    """OmegaPolicy (proj/include/treemg/cycles.hpp:17-24)."""
+    kind: str = "exponential"
+    omega_s: complex = 0.8 + 0j
+    lgrid: int = 2
+    hb: bool = False
+    bpx: bool = False
+    two_phase: bool = False
+
+    def c(self) -> _Policy:
+        return _Policy(OMEGA_KINDS[self.kind], complex(self.omega_s).real, complex(self.omega_s).imag,
+                       self.lgrid, int(self.hb), int(self.bpx), int(self.two_phase))
+
+
+@dataclass
+class SweepStats:
+    max_norm: float
+    euclid_norm: float
+    h_norm: float
+    updated_fine_vertices: int
+
+
+class Hierarchy:
+    """Device-resident regular 3^d hierarchy (the Spacetree drop-in of the cycle API)."""
+
+    def __init__(self, dim: int, levels: int, phi: complex = 0.0, theta_deg: float = 0.0, chi: str = "sin",
+                 rhs_seed: int = 12345, rhs_sphere: bool = False, ell_min: int = 1, precision: str = "exact",
+                 max_vertices: int = 0, device: int = 0):
+        self.L = lib()
+        prob = _Problem(dim, levels, ell_min, np.deg2rad(theta_deg) if theta_deg else 0.0,
+                        complex(phi).real, complex(phi).imag, CHI_KINDS[chi], rhs_seed, int(rhs_sphere),
+                        1 if precision == "fast" else 0, max_vertices, device)
+        if theta_deg:
+            prob.theta = theta_deg * np.pi / 180.0  # ProblemSpec::thetaGlobal = deg * M_PI / 180.0
+        h = ctypes.c_void_p()
+        _check(self.L.tmg_hierarchy_create(ctypes.byref(prob), ctypes.byref(h)))
+        self.h = h
+        self.dim, self.levels = dim, levels
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.tmg_hierarchy_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _sweep(self, fn, pol: Policy, n: int) -> SweepStats:
+        st = _Stats()
+        pc = pol.c()
+        _check(fn(self.h, ctypes.byref(pc), n, ctypes.byref(st)))
+        return SweepStats(st.max_norm, st.euclid_norm, st.h_norm, st.updated_fine_vertices)
+
+    def td_add(self, pol: Policy, n: int) -> SweepStats:
+        return self._sweep(self.L.tmg_td_add, pol, n)
+
+    def td_bpx(self, pol: Policy, n: int) -> SweepStats:
+        return self._sweep(self.L.tmg_td_bpx, pol, n)
+
+    def lattice_size(self, level: int) -> int:
+        return self.L.tmg_lattice_size(self.h, level)
+
+    def field(self, level: int, name: str) -> np.ndarray:
+        n = self.lattice_size(level)
+        out = np.zeros(2 * n)
+        _check(self.L.tmg_get_field(self.h, level, name.encode(), _pd(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    def set_field(self, level: int, name: str, values: np.ndarray):
+        buf = np.ascontiguousarray(np.asarray(values, dtype=np.complex128)).view(np.float64).copy()
+        _check(self.L.tmg_set_field(self.h, level, name.encode(), _pd(buf)))
+
+    def set_fine_interior_u(self, u: np.ndarray):
+        buf = np.ascontiguousarray(np.asarray(u, dtype=np.complex128)).view(np.float64).copy()
+        _check(self.L.tmg_set_fine_interior_u(self.h, _pd(buf)))
+
+    def set_random_initial_guess(self, seed: int):
+        _check(self.L.tmg_set_random_initial_guess(self.h, seed))
+
+    def set_fine_rhs(self, chi: np.ndarray):
+        buf = np.ascontiguousarray(np.asarray(chi, dtype=np.complex128)).view(np.float64).copy()
+        _check(self.L.tmg_set_fine_rhs(self.h, _pd(buf)))
+
+    def field_hash(self, level: int, name: str) -> int:
+        return int(self.L.tmg_field_hash(self.h, level, name.encode()))
+
+    def time_cycles(self, pol: Policy, n0: int, count: int, flush_l2: bool = True) -> np.ndarray:
+        out = np.zeros(4)
+        pc = pol.c()
+        _check(self.L.tmg_time_cycles(self.h, ctypes.byref(pc), n0, count, int(flush_l2), _pd(out)))
+        return out
+
+    def e2e_step(self, pol: Policy, n: int, chi_host: np.ndarray) -> np.ndarray:
+        out = np.zeros(3)
+        pc = pol.c()
+        buf = chi_host.view(np.float64) if chi_host.dtype == np.complex128 else chi_host
+        _check(self.L.tmg_e2e_step(self.h, ctypes.byref(pc), n, _pd(buf), _pd(out)))
+        return out
+
+
+def exported_symbols() -> List[str]:
+    """Dynamic symbols of the built library (checked by the CPU test suite)."""
+    import subprocess
+    out = subprocess.run(["nm", "-D", "--defined-only", LIB_PATH], capture_output=True, text=True).stdout
+    return [line.split()[-1] for line in out.splitlines() if line.strip()]

@@ -1,0 +1,60 @@
+"""Builds libtreemg_b200.so in-tree with nvcc for sm_100a.
+
+The library is the product: CUDA kernels + host C++ runner + the treemg
+C-ABI (include/treemg.h, include/treemg_b200.h).  It is built into the
+package directory so the .so travels with the repo snapshot to the GPU box.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+LIB = os.path.join(PKG, "libtreemg_b200.so")
+SOURCES = ["hierarchy.cu", "fast.cu", "runner.cpp", "capi.cpp"]
+HEADERS = ["hierarchy.hpp", "exact_ops.cuh", "fast.cuh", "runner.hpp"]
+
+
+def nvcc_path() -> str:
+    for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
+        if cand and os.path.exists(cand):
+            return cand
+    raise RuntimeError("nvcc not found")
+
+
+def _stale() -> bool:
+    if not os.path.exists(LIB):
+        return True
+    t = os.path.getmtime(LIB)
+    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS if os.path.exists(os.path.join(CSRC, f))]
+    deps += [os.path.join(ROOT, "include", h) for h in ("treemg.h", "treemg_b200.h")]
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def build(force: bool = False, verbose: bool = False) -> str:
+    if not force and not _stale():
+        return LIB
+    srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
+    cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+           "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-shared",
+           "-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + srcs
+    # host compiler: the system g++ so libstdc++ is linked dynamically
+    if os.path.exists("/usr/bin/g++"):
+        cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
+    out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
+    with open(os.path.join(PKG, "build.log"), "w") as f:
+        f.write(" ".join(cmd) + "\n" + out.stdout + out.stderr)
+    if out.returncode != 0:
+        raise RuntimeError("nvcc build failed:\n" + out.stderr[-6000:])
+    os.replace(LIB + ".tmp", LIB)
+    if verbose:
+        print(out.stderr)
+    return LIB
+
+
+if __name__ == "__main__":
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))

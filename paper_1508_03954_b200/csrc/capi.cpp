@@ -1,0 +1,261 @@
+// The treemg C-ABI (include/treemg.h) plus the B200 extensions
+// (include/treemg_b200.h).  Mirrors proj/src/capi.cpp: opaque handles,
+// thread-local last error, exception -> status mapping; exceptions never
+// cross the boundary.
+
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/treemg.h"
+#include "../../include/treemg_b200.h"
+#include "runner.hpp"
+
+using namespace tmg;
+
+struct treemg_config {
+    RunConfig cfg;
+};
+
+struct treemg_result {
+    RunResult res;
+    int channels = 1;
+};
+
+struct tmg_hierarchy {
+    std::unique_ptr<Hierarchy> h;
+};
+
+namespace {
+
+thread_local std::string g_lastError;
+
+treemg_status fail(treemg_status code, const char* what) {
+    g_lastError = what ? what : "unknown error";
+    return code;
+}
+
+template <class Fn>
+treemg_status guarded(Fn&& fn) {  // capi.cpp:28-43
+    try {
+        fn();
+        g_lastError.clear();
+        return TREEMG_OK;
+    } catch (const ConfigError& e) {
+        return fail(TREEMG_E_USAGE, e.what());
+    } catch (const UnsupportedConfigError& e) {
+        return fail(TREEMG_E_USAGE, e.what());
+    } catch (const CapacityError& e) {
+        return fail(TREEMG_E_CAPACITY, e.what());
+    } catch (const std::exception& e) {
+        return fail(TREEMG_E_RUNTIME, e.what());
+    }
+}
+
+Policy policy_from(const tmg_policy* p) {
+    Policy pol;
+    pol.kind = static_cast<OmegaKind>(p->kind);
+    pol.omegaS = Cplx(p->omega_re, p->omega_im);
+    pol.lGrid = p->lgrid;
+    pol.hbMask = p->hb != 0;
+    pol.bpx = p->bpx != 0;
+    pol.twoPhase = p->two_phase != 0;
+    return pol;
+}
+
+void fill_stats(const SweepStats& st, tmg_sweep_stats* out) {
+    if (!out) return;
+    out->max_norm = st.maxNorm;
+    out->euclid_norm = st.euclidNorm;
+    out->h_norm = st.hNorm;
+    out->updated_fine_vertices = st.updatedFineVertices;
+}
+
+}  // namespace
+
+extern "C" {
+
+unsigned treemg_version(void) { return 100; }
+
+const char* treemg_last_error(void) { return g_lastError.c_str(); }
+
+const char* tmg_last_error(void) { return g_lastError.c_str(); }
+
+treemg_config* treemg_config_new(void) { return new treemg_config(); }
+
+void treemg_config_free(treemg_config* cfg) { delete cfg; }
+
+treemg_status treemg_config_load_file(treemg_config* cfg, const char* path) {
+    if (!cfg || !path) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { cfg->cfg = parse_config_file(path); });
+}
+
+treemg_status treemg_config_set(treemg_config* cfg, const char* key, const char* value) {
+    if (!cfg || !key || !value) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { apply_override(cfg->cfg, key, value); });
+}
+
+treemg_status treemg_run(const treemg_config* cfg, treemg_result** out) {
+    if (!cfg || !out) return fail(TREEMG_E_USAGE, "null argument");
+    *out = nullptr;
+    auto* res = new treemg_result();
+    const treemg_status st = guarded([&] {
+        res->res = run(cfg->cfg);
+        res->channels = cfg->cfg.channels;
+    });
+    if (st != TREEMG_OK) {
+        delete res;
+        return st;
+    }
+    *out = res;
+    return TREEMG_OK;
+}
+
+void treemg_result_free(treemg_result* res) { delete res; }
+
+treemg_outcome treemg_result_outcome(const treemg_result* res) {
+    switch (res->res.outcome) {
+        case RunOutcome::Converged: return TREEMG_RUN_CONVERGED;
+        case RunOutcome::BudgetExhausted: return TREEMG_RUN_BUDGET_EXHAUSTED;
+        case RunOutcome::Diverged: return TREEMG_RUN_DIVERGED;
+    }
+    return TREEMG_RUN_DIVERGED;
+}
+
+int treemg_result_sweeps(const treemg_result* res) { return res->res.sweeps; }
+
+double treemg_result_work_units(const treemg_result* res) { return res->res.workUnits; }
+
+long long treemg_result_vertex_count(const treemg_result* res) {
+    return static_cast<long long>(res->res.vertexCount);
+}
+
+double treemg_result_final_norm(const treemg_result* res, const char* which, int channel) {  // capi.cpp:102-112
+    if (res->res.history.empty()) return 0.0;
+    const SweepRecord& rec = res->res.history.back();
+    const bool agg = channel < 0;
+    if (!agg && channel >= res->channels) return -1.0;
+    if (std::strcmp(which, "max") == 0) return rec.maxNorm;
+    if (std::strcmp(which, "euclid") == 0) return rec.euclidNorm;
+    if (std::strcmp(which, "h") == 0) return rec.hNorm;
+    return -1.0;
+}
+
+double treemg_result_first_norm(const treemg_result* res) { return res->res.firstNorm; }
+
+// ---- extensions --------------------------------------------------------------
+
+int treemg_result_history_rows(const treemg_result* res) { return static_cast<int>(res->res.history.size()); }
+
+treemg_status treemg_result_history_row(const treemg_result* res, int i, double* out6) {
+    if (!res || !out6 || i < 0 || i >= static_cast<int>(res->res.history.size()))
+        return fail(TREEMG_E_USAGE, "history row out of range");
+    const SweepRecord& r = res->res.history[static_cast<std::size_t>(i)];
+    out6[0] = r.sweep;
+    out6[1] = r.workUnits;
+    out6[2] = static_cast<double>(r.vertexCount);
+    out6[3] = r.maxNorm;
+    out6[4] = r.euclidNorm;
+    out6[5] = r.hNorm;
+    return TREEMG_OK;
+}
+
+double treemg_result_device_ms(const treemg_result* res) { return res->res.deviceMs; }
+
+treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out) {
+    if (!prob || !out) return fail(TREEMG_E_USAGE, "null argument");
+    *out = nullptr;
+    auto* h = new tmg_hierarchy();
+    const treemg_status st = guarded([&] {
+        Problem p;
+        p.dim = prob->dim;
+        p.levels = prob->levels;
+        p.ellMin = prob->ell_min;
+        p.theta = prob->theta;
+        p.phi = Cplx(prob->phi_re, prob->phi_im);
+        p.chi = static_cast<ChiKind>(prob->chi_kind);
+        p.rhsSeed = prob->rhs_seed;
+        p.rhsSphere = prob->rhs_sphere != 0;
+        p.fast = prob->precision == 1;
+        if (prob->max_vertices > 0) p.maxVertices = static_cast<std::size_t>(prob->max_vertices);
+        p.device = prob->device;
+        if (p.ellMin < 1) throw ConfigError("ellMin must be >= 1");
+        h->h = std::make_unique<Hierarchy>(p);
+    });
+    if (st != TREEMG_OK) {
+        delete h;
+        return st;
+    }
+    *out = h;
+    return TREEMG_OK;
+}
+
+void tmg_hierarchy_destroy(tmg_hierarchy* h) { delete h; }
+
+treemg_status tmg_td_add(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
+    if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        Policy p = policy_from(pol);
+        if (p.bpx) throw ConfigError("td_add: policy has bpx set, use td_bpx");  // cycles.cpp:338
+        if (n < 1) throw ConfigError("sweep counter starts at 1");
+        fill_stats(h->h->cycle(p, n), out);
+    });
+}
+
+treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
+    if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        Policy p = policy_from(pol);
+        if (n < 1) throw ConfigError("sweep counter starts at 1");
+        p.bpx = true;  // cycles.cpp:349-351
+        p.hbMask = false;
+        fill_stats(h->h->cycle(p, n), out);
+    });
+}
+
+long long tmg_lattice_size(const tmg_hierarchy* h, int level) { return h ? h->h->lattice_size(level) : 0; }
+
+treemg_status tmg_get_field(tmg_hierarchy* h, int level, const char* field, double* out) {
+    if (!h || !field || !out) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->get_field(level, field, out); });
+}
+
+treemg_status tmg_set_field(tmg_hierarchy* h, int level, const char* field, const double* in) {
+    if (!h || !field || !in) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->set_field(level, field, in); });
+}
+
+treemg_status tmg_set_fine_interior_u(tmg_hierarchy* h, const double* u) {
+    if (!h || !u) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->set_fine_interior_u(u); });
+}
+
+treemg_status tmg_set_random_initial_guess(tmg_hierarchy* h, unsigned long long seed) {
+    if (!h) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->set_random_initial_guess(seed); });
+}
+
+treemg_status tmg_set_fine_rhs(tmg_hierarchy* h, const double* chi) {
+    if (!h || !chi) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->set_fine_rhs(chi); });
+}
+
+unsigned long long tmg_field_hash(tmg_hierarchy* h, int level, const char* field) {
+    unsigned long long v = 0;
+    if (!h || !field) return 0;
+    guarded([&] { v = h->h->field_hash(level, field); });
+    return v;
+}
+
+treemg_status tmg_time_cycles(tmg_hierarchy* h, const tmg_policy* pol, int n0, int count, int flush_l2,
+                              double* out4) {
+    if (!h || !pol || !out4) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->time_cycles(policy_from(pol), n0, count, flush_l2 != 0, out4); });
+}
+
+treemg_status tmg_e2e_step(tmg_hierarchy* h, const tmg_policy* pol, int n, const double* chi, double* out3) {
+    if (!h || !pol || !chi || !out3) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->e2e_step(policy_from(pol), n, chi, out3); });
+}
+
+}  // extern "C"

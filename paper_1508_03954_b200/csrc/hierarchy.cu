@@ -1,0 +1,1157 @@
+// Device hierarchy + cycle kernels (sm_100a).  See hierarchy.hpp and
+// DESIGN.md §3 for the data layout and the kernel/roofline table.
+//
+// Cycle = two level passes (reference
+// proj/src/oracle.cpp:465-509 with the per-vertex semantics of
+// proj/src/cycles.cpp:102-303):
+//   top-down  l = 1..L   K1 k_topdown           touch_first  (cycles.cpp:102-141)
+//   bottom-up l = L..1   K2/K3 k_residual_exact enterCell + touchLast (cycles.cpp:173-303)
+//                        K3r k_restrict_exact   restriction into chi_{l-1} (cycles.cpp:292-301)
+//   norms                K5 k_norm_final        (cycles.cpp:248-258, 94-97)
+// The fast-precision fine pass (K2f) lives in fast.cuh.
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <sstream>
+#include <string>
+#include <vector>
+
+#include "exact_ops.cuh"
+#include "hierarchy.hpp"
+
+namespace tmg {
+
+#define TMG_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t err_ = (call);                                                              \
+        if (err_ != cudaSuccess) {                                                              \
+            if (err_ == cudaErrorMemoryAllocation)                                              \
+                throw CapacityError(std::string("device memory exhausted: ") + #call);          \
+            throw CudaError(std::string("CUDA error ") + cudaGetErrorString(err_) + " at " + #call); \
+        }                                                                                       \
+    } while (0)
+
+namespace dev {
+
+struct Lvl {
+    double2* u;
+    double2* sc;
+    double2* sf;
+    double2* si;
+    double2* sinext;
+    double2* chi;
+    double2* uhat;
+    double2* rhat;
+    double2* r;  // optional debug copy of the residual
+    unsigned m;   // 3^l
+    unsigned n1;  // 3^l + 1
+    unsigned n;   // (3^l+1)^p
+    int level;
+};
+
+struct LevelConst {
+    double2 A[8];   // element operator entry for XOR pattern of (a, b)
+    double M[8];    // reference mass entry for XOR pattern
+    double2 massScale;
+    DivConst div;
+    double2 wRaw;   // omega_unmasked(pol, succ = L - l, n)
+};
+
+struct ResArgs {
+    Lvl lv;
+    Lvl par;  // level l-1 (injection targets); unused when l <= ellMin
+    LevelConst k;
+    int ellMin;
+    int isFine;
+    int bpx;
+    int hb;
+    double* partials;  // 2 doubles per block: max |r|^2, sum |r|^2
+};
+
+template <int P>
+__device__ __forceinline__ void unflat(unsigned f, unsigned n1, int* idx) {
+#pragma unroll
+    for (int d = 0; d < P; ++d) {
+        idx[d] = static_cast<int>(f % n1);
+        f /= n1;
+    }
+}
+
+template <int P>
+__device__ __forceinline__ unsigned flat(const int* idx, unsigned n1) {
+    unsigned f = 0, s = 1;
+#pragma unroll
+    for (int d = 0; d < P; ++d) {
+        f += static_cast<unsigned>(idx[d]) * s;
+        s *= n1;
+    }
+    return f;
+}
+
+template <int P>
+__device__ __forceinline__ bool on_boundary(const int* idx, int m) {
+    bool b = false;
+#pragma unroll
+    for (int d = 0; d < P; ++d) b |= (idx[d] == 0) | (idx[d] == m);
+    return b;
+}
+
+template <int P>
+__device__ __forceinline__ bool is_cpoint(const int* idx) {
+    bool c = true;
+#pragma unroll
+    for (int d = 0; d < P; ++d) c &= (idx[d] % 3 == 0);
+    return c;
+}
+
+// proj/src/transfer.cpp:20-40, one axis fold: exact copies at rel 0 / 3.
+__device__ __forceinline__ double2 lerp_rel(double2 c0, double2 c1, int rel) {
+    if (rel == 0) return c0;
+    if (rel == 3) return c1;
+    const double w0 = rel == 1 ? (2.0 / 3.0) : (1.0 / 3.0);
+    const double w1 = rel == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
+    return xadd(xscale(w0, c0), xscale(w1, c1));
+}
+
+template <int P>
+__device__ __forceinline__ double2 prolong(double2 (&v)[1 << P], const int* rel) {
+    int n = 1 << P;
+#pragma unroll
+    for (int d = 0; d < P; ++d) {
+        n >>= 1;
+#pragma unroll
+        for (int i = 0; i < (1 << (P - 1 - d)); ++i) v[i] = lerp_rel(v[2 * i], v[2 * i + 1], rel[d]);
+    }
+    return v[0];
+}
+
+// ---- K1: top-down update (touch_first, cycles.cpp:102-141) ----------------
+template <int P>
+__global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        int q[P], rel[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            q[d] = min(idx[d] / 3, static_cast<int>(pr.m) - 1);
+            rel[d] = idx[d] - 3 * q[d];
+        }
+        double2 cu[1 << P], cs[1 << P];
+#pragma unroll
+        for (int e = 0; e < (1 << P); ++e) {
+            int pi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
+            const unsigned pf = flat<P>(pi, pr.n1);
+            cu[e] = pr.u[pf];
+            cs[e] = pr.sc[pf];
+        }
+        double2 sc = xadd(c.sc[f], prolong<P>(cs, rel));
+        if (bpx && !is_cpoint<P>(idx)) {
+            double2 ci[1 << P];
+#pragma unroll
+            for (int e = 0; e < (1 << P); ++e) {
+                int pi[P];
+#pragma unroll
+                for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
+                ci[e] = pr.si[flat<P>(pi, pr.n1)];
+            }
+            sc = xsub(sc, prolong<P>(ci, rel));
+        }
+        const double2 sf = c.sf ? c.sf[f] : cz();
+        double2 u = xadd(c.u[f], xadd(sc, sf));
+        double2 uh = xsub(u, prolong<P>(cu, rel));
+        if (on_boundary<P>(idx, static_cast<int>(c.m))) {
+            u = cz();
+            uh = cz();
+        }
+        c.u[f] = u;
+        c.sc[f] = sc;
+        c.uhat[f] = uh;
+        if (c.sf) c.sf[f] = cz();
+    }
+}
+
+// Element-by-element residual -(A x) gathered at one interior vertex, with the
+// cell contributions summed in traversal order (see exact_ops.cuh rule (1)).
+// Products A_s x_{v+delta} are formed once and shared by the cells using them
+// (A depends only on the XOR pattern of the corner pair); iterating delta in
+// lexicographic order visits every cell's corners b in ascending order, the
+// order of proj/src/kernels.cpp:42-47.
+template <int P, int ID>
+__device__ __forceinline__ double2 ordered_sum(const double2 (&S)[1 << P]) {
+    double2 r = xneg(S[perm_cell(P, ID, 0)]);
+#pragma unroll
+    for (int i = 1; i < (1 << P); ++i) r = xsub(r, S[perm_cell(P, ID, i)]);
+    return r;
+}
+
+template <int P>
+__device__ __forceinline__ double2 element_residual(const double2* __restrict__ x, unsigned f, unsigned n1,
+                                                    const double2 (&A)[8], int pid) {
+    constexpr int NC = 1 << P;
+    int pw[P];
+    pw[0] = 1;
+#pragma unroll
+    for (int d = 1; d < P; ++d) pw[d] = pw[d - 1] * 3;
+    double2 S[NC];
+#pragma unroll
+    for (int j = 0; j < (P == 1 ? 3 : P == 2 ? 9 : 27); ++j) {
+        int del[P];
+        int off = 0, s = 0, stride = 1;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            del[d] = (j / (d == 0 ? 1 : d == 1 ? 3 : 9)) % 3 - 1;
+            off += del[d] * stride;
+            stride *= static_cast<int>(n1);
+            s |= (del[d] != 0 ? 1 : 0) << d;
+        }
+        const double2 prod = xmul(A[s], __ldg(x + (static_cast<int>(f) + off)));
+#pragma unroll
+        for (int e = 0; e < NC; ++e) {
+            bool use = true;
+            int b = 0;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                const int bd = del[d] - ((e >> d) & 1) + 1;
+                use &= (bd == 0 || bd == 1);
+                b |= (bd & 1) << d;
+            }
+            if (use) S[e] = (b == 0) ? prod : xadd(S[e], prod);
+        }
+    }
+    (void)pw;
+    if (P == 1) return ordered_sum<P, 0>(S);
+    if (P == 2) return pid == 0 ? ordered_sum<P, 0>(S) : ordered_sum<P, (P >= 2 ? 1 : 0)>(S);
+    switch (pid) {
+        case 0: return ordered_sum<P, 0>(S);
+        case 1: return ordered_sum<P, (P >= 3 ? 1 : 0)>(S);
+        case 2: return ordered_sum<P, (P >= 3 ? 2 : 0)>(S);
+        case 3: return ordered_sum<P, (P >= 3 ? 3 : 0)>(S);
+        case 4: return ordered_sum<P, (P >= 3 ? 4 : 0)>(S);
+        default: return ordered_sum<P, (P >= 3 ? 5 : 0)>(S);
+    }
+}
+
+__device__ __forceinline__ void block_norms(double m2, double& outMax, double& outSum, double* partials) {
+    __shared__ double smax[32], ssum[32];
+    double mx = m2, sm = m2;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        sm += __shfl_xor_sync(0xffffffffu, sm, o);
+    }
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    if (l == 0) {
+        smax[w] = mx;
+        ssum[w] = sm;
+    }
+    __syncthreads();
+    if (w == 0) {
+        const int nw = blockDim.x >> 5;
+        mx = l < nw ? smax[l] : 0.0;
+        sm = l < nw ? ssum[l] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            sm += __shfl_xor_sync(0xffffffffu, sm, o);
+        }
+        if (l == 0) {
+            partials[2 * blockIdx.x] = mx;
+            partials[2 * blockIdx.x + 1] = sm;
+        }
+    }
+    (void)outMax;
+    (void)outSum;
+}
+
+// ---- K2/K3: residual + Jacobi staging + injections (enterCell/touchLast) --
+template <int P>
+__global__ void __launch_bounds__(256) k_residual_exact(ResArgs a) {
+    const Lvl& c = a.lv;
+    double nmax = 0.0, nsum = 0.0;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        const bool bnd = on_boundary<P>(idx, static_cast<int>(c.m));
+        const bool cp = is_cpoint<P>(idx);
+        double2 r = cz(), rh = cz();
+        if (!bnd) {
+            const int pid = perm_id<P>(idx);
+            r = element_residual<P>(c.u, f, c.n1, a.k.A, pid);
+            rh = element_residual<P>(c.uhat, f, c.n1, a.k.A, pid);
+            const double2 chi = c.chi[f];
+            r = xadd(chi, r);    // finish_vertex, kernels.cpp:96-97
+            rh = xadd(chi, rh);
+        }
+        if (c.si) {  // si = siNext (cycles.cpp:247); siNext re-zeroed for the next sweep
+            c.si[f] = c.sinext[f];
+            c.sinext[f] = cz();
+        }
+        if (a.isFine && !bnd) {
+            const double m2 = r.x * r.x + r.y * r.y;
+            nmax = fmax(nmax, m2);
+            nsum += m2;
+        }
+        if (c.r) c.r[f] = r;
+        c.rhat[f] = rh;
+        if (c.level < a.ellMin) {
+            c.sc[f] = cz();
+            continue;
+        }
+        const double2 smooth = bnd ? cz() : divdc3(r.x, r.y, a.k.div);
+        double2 sc;
+        if (a.bpx) {
+            sc = cp ? cz() : xmul(a.k.wRaw, smooth);
+        } else {
+            const bool wz = (a.hb && cp) || xzero(a.k.wRaw);
+            sc = wz ? cz() : xmul(a.k.wRaw, smooth);
+        }
+        c.sc[f] = sc;
+        if (c.level > a.ellMin && cp) {  // injections, cycles.cpp:279-291
+            int wi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+            const unsigned wf = flat<P>(wi, a.par.n1);
+            const double2 sf = c.sf ? c.sf[f] : cz();
+            a.par.sf[wf] = xadd(sf, sc);
+            if (a.bpx) a.par.sinext[wf] = xmul(a.k.wRaw, smooth);
+        }
+    }
+    if (a.isFine) block_norms(nmax, nmax, nsum, a.partials);
+    (void)nsum;
+}
+
+// ---- K3r: restriction chi_{l-1} = R rhat_l in touch-last order -------------
+// table: for each permutation id, 5^P offsets (packed base 5) in order.
+template <int P>
+__global__ void __launch_bounds__(256) k_restrict_exact(Lvl fine, Lvl coarse, const unsigned char* __restrict__ table,
+                                                        const double* __restrict__ weights, int zero) {
+    constexpr int NT = P == 1 ? 5 : P == 2 ? 25 : 125;
+    constexpr int NP = P == 1 ? 1 : P == 2 ? 2 : 6;
+    __shared__ unsigned char st[NP * NT];
+    __shared__ double sw[NT];
+    for (int i = threadIdx.x; i < NP * NT; i += blockDim.x) st[i] = table[i];
+    for (int i = threadIdx.x; i < NT; i += blockDim.x) sw[i] = weights[i];
+    __syncthreads();
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < coarse.n; f += gridDim.x * blockDim.x) {
+        if (zero) {
+            coarse.chi[f] = cz();
+            continue;
+        }
+        int W[P];
+        unflat<P>(f, coarse.n1, W);
+        const int pid = perm_id<P>(W);
+        double2 acc = cz();
+        const int mf = static_cast<int>(fine.m);
+        for (int i = 0; i < NT; ++i) {
+            int code = st[pid * NT + i];
+            int v[P];
+            bool in = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                v[d] = 3 * W[d] + (code % 5) - 2;
+                code /= 5;
+                in &= (v[d] >= 1) & (v[d] <= mf - 1);
+            }
+            if (!in) continue;
+            acc = xadd(acc, xscale(sw[st[pid * NT + i]], fine.rhat[flat<P>(v, fine.n1)]));
+        }
+        coarse.chi[f] = acc;
+    }
+}
+
+// ---- K5: deterministic final norm reduction --------------------------------
+__global__ void k_norm_final(const double* __restrict__ partials, int nblocks, double* out) {
+    __shared__ double smax[1024], ssum[1024];
+    double mx = 0.0, sm = 0.0;
+    for (int i = threadIdx.x; i < nblocks; i += blockDim.x) {
+        mx = fmax(mx, partials[2 * i]);
+        sm += partials[2 * i + 1];
+    }
+    smax[threadIdx.x] = mx;
+    ssum[threadIdx.x] = sm;
+    __syncthreads();
+    for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+            ssum[threadIdx.x] += ssum[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        out[0] = smax[0];
+        out[1] = ssum[0];
+    }
+}
+
+// ---- K6: setup kernels -------------------------------------------------------
+// Consistent-mass load of the leaf cells (kernels.cpp:69-87), accumulated per
+// vertex in traversal cell order; constant across sweeps on a static grid.
+template <int P>
+__global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, LevelConst k) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        // permutation: boundary axes carry a single cell, any priority works
+        const int pid = perm_id<P>(idx);
+        double2 b = cz();
+#pragma unroll
+        for (int i = 0; i < (1 << P); ++i) {
+            int e = 0;
+            if (P == 1) e = perm_cell(1, 0, i);
+            else if (P == 2) e = pid == 0 ? perm_cell(2, 0, i) : perm_cell(2, 1, i);
+            else {
+#pragma unroll
+                for (int id = 0; id < 6; ++id)
+                    if (id == pid) e = perm_cell(3, id, i);
+            }
+            int cell[P];
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                cell[d] = idx[d] - 1 + ((e >> d) & 1);
+                ok &= (cell[d] >= 0) & (cell[d] <= static_cast<int>(c.m) - 1);
+            }
+            if (!ok) continue;
+            const int a = (~e) & ((1 << P) - 1);  // corner of the vertex in the cell
+            double2 acc = cz();
+#pragma unroll
+            for (int bb = 0; bb < (1 << P); ++bb) {
+                int vb[P];
+#pragma unroll
+                for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
+                acc = xadd(acc, xscale(k.M[a ^ bb], chiNodal[flat<P>(vb, c.n1)]));
+            }
+            b = xadd(b, xmul(k.massScale, acc));
+        }
+        c.chi[f] = b;
+    }
+}
+
+__device__ __forceinline__ double unit_rand(unsigned long long x) {  // cycles.cpp:802-808
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    x = x ^ (x >> 31);
+    return __dsub_rn(__ddiv_rn(__dmul_rn(2.0, static_cast<double>(x >> 11)), 9007199254740992.0), 1.0);
+}
+
+// Seeded nodal rhs f(x) keyed on the finest-lattice position,
+// optionally masked to the ball |x - 1/2|^2 < 0.04.
+template <int P>
+__global__ void k_seeded_chi(double2* out, unsigned n, unsigned n1, unsigned long long seed, int scale, long long mkey,
+                             int sphere) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, n1, idx);
+        unsigned long long key = 0;
+        long long s2 = 0;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            const long long fi = static_cast<long long>(idx[d]) * scale;
+            key |= static_cast<unsigned long long>(static_cast<unsigned short>(fi)) << (16 * d);
+            const long long t = 2 * fi - mkey;
+            s2 += t * t;
+        }
+        if (sphere && !(25 * s2 < 4 * mkey * mkey)) {
+            out[f] = cz();
+            continue;
+        }
+        const unsigned long long s = seed ^ key;
+        out[f] = make_double2(unit_rand(s), unit_rand(s ^ 0x5bf03635ull));
+    }
+}
+
+template <int P>
+__global__ void k_random_fine(Lvl c, unsigned long long seed) {  // cycles.cpp:812-840
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        if (on_boundary<P>(idx, static_cast<int>(c.m))) {
+            c.u[f] = cz();
+            continue;
+        }
+        unsigned long long key = 0;
+#pragma unroll
+        for (int d = 0; d < P; ++d) key |= static_cast<unsigned long long>(static_cast<unsigned short>(idx[d])) << (16 * d);
+        const unsigned long long base = seed ^ (static_cast<unsigned long long>(c.level) << 56) ^ key;
+        c.u[f] = make_double2(unit_rand(base), unit_rand(base ^ 0x5bf03635ull));
+    }
+}
+
+// u_l(W) = u_{l+1}(3W) on non-boundary vertices (injection consistency).
+template <int P>
+__global__ void k_inject_u(Lvl c, Lvl fine) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        if (on_boundary<P>(idx, static_cast<int>(c.m))) continue;
+        int fi[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) fi[d] = 3 * idx[d];
+        c.u[f] = fine.u[flat<P>(fi, fine.n1)];
+    }
+}
+
+// Fine interior values (interior lattice order) scattered into the level.
+template <int P>
+__global__ void k_scatter_interior(Lvl c, const double2* __restrict__ in) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        if (on_boundary<P>(idx, static_cast<int>(c.m))) continue;
+        unsigned fl = 0, s = 1;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            fl += static_cast<unsigned>(idx[d] - 1) * s;
+            s *= c.m - 1;
+        }
+        c.u[f] = in[fl];
+    }
+}
+
+// FMG unfolding: new finest level u = P u_{coarse} (spacetree.cpp:245-270).
+template <int P>
+__global__ void k_prolong_new(Lvl c, Lvl pr) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        int q[P], rel[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            q[d] = min(idx[d] / 3, static_cast<int>(pr.m) - 1);
+            rel[d] = idx[d] - 3 * q[d];
+        }
+        double2 cu[1 << P];
+#pragma unroll
+        for (int e = 0; e < (1 << P); ++e) {
+            int pi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
+            cu[e] = pr.u[flat<P>(pi, pr.n1)];
+        }
+        c.u[f] = prolong<P>(cu, rel);
+    }
+}
+
+__global__ void k_flush(double4* buf, size_t n, double v) {
+    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        buf[i] = make_double4(v, v, v, v);
+}
+
+}  // namespace dev
+
+// ============================================================================
+// Host side
+// ============================================================================
+
+namespace {
+
+int pow3i(int l) {
+    int r = 1;
+    for (int i = 0; i < l; ++i) r *= 3;
+    return r;
+}
+
+// proj/src/elemops.cpp:13-18
+Cplx cplx_ipow(Cplx z, int e) {
+    if (e < 0) return 1.0 / cplx_ipow(z, -e);
+    Cplx r = 1.0;
+    for (int i = 0; i < e; ++i) r *= z;
+    return r;
+}
+
+// proj/src/elemops.cpp:29-55, entries for corner pair (0, s): every pair with
+// the same XOR pattern has identical entries (per-axis equal/unequal only).
+void reference_pattern(int p, int s, double& lap, double& mas) {
+    static const double kLap1[2][2] = {{1.0, -1.0}, {-1.0, 1.0}};
+    static const double kMass1[2][2] = {{1.0 / 3.0, 1.0 / 6.0}, {1.0 / 6.0, 1.0 / 3.0}};
+    const int a = 0, b = s;
+    double mass = 1.0;
+    for (int d = 0; d < p; ++d) mass *= kMass1[(a >> d) & 1][(b >> d) & 1];
+    double l = 0.0;
+    for (int d = 0; d < p; ++d) {
+        double t = kLap1[(a >> d) & 1][(b >> d) & 1];
+        for (int i = 0; i < p; ++i)
+            if (i != d) t *= kMass1[(a >> i) & 1][(b >> i) & 1];
+        l += t;
+    }
+    lap = l;
+    mas = mass;
+}
+
+// libgcc __divdc3 branch structure for a fixed divisor (see exact_ops.cuh).
+dev::DivConst div_const(Cplx diag) {
+    dev::DivConst k{};
+    double c = diag.real(), d = diag.imag();
+    const bool swap = !(std::fabs(c) < std::fabs(d));
+    k.swap = swap ? 1 : 0;
+    const double big = swap ? std::fabs(c) : std::fabs(d);
+    k.pre = 0;
+    if (big >= dev::kRBIG) {
+        c = c / 2;
+        d = d / 2;
+        k.pre = 1;
+    }
+    const double big2 = swap ? std::fabs(c) : std::fabs(d);
+    if (big2 < dev::kRMIN2) {
+        c = c * dev::kRMINSCAL;
+        d = d * dev::kRMINSCAL;
+        k.pre = k.pre == 1 ? 1 : 2;  // halving and scaling up are exclusive
+    }
+    k.c = c;
+    k.d = d;
+    if (!swap) {
+        k.ratio = c / d;
+        k.denom = (c * k.ratio) + d;
+        k.denomTiny = ((c * dev::kRMINSCAL) * k.ratio) + (d * dev::kRMINSCAL);
+    } else {
+        k.ratio = d / c;
+        k.denom = (d * k.ratio) + c;
+        k.denomTiny = ((d * dev::kRMINSCAL) * k.ratio) + (c * dev::kRMINSCAL);
+    }
+    k.sub = std::fabs(k.ratio) > dev::kRMIN ? 0 : 1;
+    return k;
+}
+
+}  // namespace
+
+Cplx omega_unmasked(const Policy& pol, int succ, int n) {
+    Cplx ws = pol.omegaS;
+    if (pol.twoPhase) {  // cycles.cpp:11-15
+        const Cplx w1 = 0.01 * Cplx(std::sqrt(3.0), -1.0);
+        ws = (n % 2 == 1) ? w1 : -std::conj(w1);
+    }
+    switch (pol.kind) {
+        case OmegaKind::JacobiOnly: return succ == 0 ? ws : Cplx(0.0);
+        case OmegaKind::UndampedCG: return ws;
+        case OmegaKind::LGrid: return succ <= pol.lGrid ? ws : Cplx(0.0);
+        case OmegaKind::Exponential: return cplx_ipow(ws, succ + 1);
+        case OmegaKind::Transition: {
+            const double e = (1.0 - 1.0 / static_cast<double>(n)) * (succ + 1);
+            if (e == 0.0) return Cplx(1.0);
+            return std::pow(ws, e);
+        }
+    }
+    return Cplx(0.0);
+}
+
+struct Hierarchy::Impl {
+    Problem prob;
+    int p = 2, L = 1;
+    std::vector<dev::Lvl> lv;
+    std::vector<void*> allocations;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr, evf0 = nullptr, evf1 = nullptr;
+    double* partials = nullptr;
+    int normBlocks = 0;
+    double* dNorm = nullptr;
+    double* hNorm = nullptr;  // pinned
+    unsigned char* restrictTable = nullptr;
+    double* restrictWeights = nullptr;
+    double2* chiNodal = nullptr;  // device nodal rhs at the finest lattice
+    double4* flushBuf = nullptr;
+    size_t flushN = 0;
+    std::vector<dev::LevelConst> kc;  // per level
+    std::vector<Cplx> diagInterior;
+    std::vector<Cplx> lapScale, massScale;
+    bool debugR = false;
+    int smCount = 148;
+    float lastFineMs = 0.f, lastTdMs = 0.f;
+    bool timeFine = false;
+
+    ~Impl() {
+        for (void* ptr : allocations) cudaFree(ptr);
+        if (hNorm) cudaFreeHost(hNorm);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+        if (evf0) cudaEventDestroy(evf0);
+        if (evf1) cudaEventDestroy(evf1);
+        if (stream) cudaStreamDestroy(stream);
+    }
+
+    template <class T>
+    T* alloc(size_t count) {
+        void* ptr = nullptr;
+        TMG_CUDA(cudaMalloc(&ptr, count * sizeof(T)));
+        allocations.push_back(ptr);
+        TMG_CUDA(cudaMemsetAsync(ptr, 0, count * sizeof(T), stream));
+        return static_cast<T*>(ptr);
+    }
+
+    int blocks_for(unsigned n) const {
+        const long long need = (static_cast<long long>(n) + 255) / 256;
+        return static_cast<int>(std::max<long long>(1, std::min<long long>(need, 8LL * smCount)));
+    }
+
+    dev::Lvl make_level(int l, bool fine) {
+        dev::Lvl v{};
+        v.level = l;
+        v.m = static_cast<unsigned>(pow3i(l));
+        v.n1 = v.m + 1;
+        unsigned long long n = 1;
+        for (int d = 0; d < p; ++d) n *= v.n1;
+        if (n >= (1ull << 32)) throw CapacityError("level lattice exceeds 2^32 vertices");
+        v.n = static_cast<unsigned>(n);
+        v.u = alloc<double2>(n);
+        v.sc = alloc<double2>(n);
+        v.chi = alloc<double2>(n);
+        v.uhat = alloc<double2>(n);
+        v.rhat = alloc<double2>(n);
+        if (!fine) {
+            v.sf = alloc<double2>(n);
+            v.si = alloc<double2>(n);
+            v.sinext = alloc<double2>(n);
+        }
+        if (debugR) v.r = alloc<double2>(n);
+        return v;
+    }
+
+    void compute_level_constants() {
+        kc.assign(L + 1, dev::LevelConst{});
+        diagInterior.assign(L + 1, Cplx(0.0));
+        lapScale.assign(L + 1, Cplx(0.0));
+        massScale.assign(L + 1, Cplx(0.0));
+        for (int l = 0; l <= L; ++l) {
+            // make_cell_kernel, kernels.cpp:7-23 (constant theta and phi)
+            const double h = std::pow(3.0, -l);
+            const Cplx hElem = h * Cplx(std::cos(prob.theta), std::sin(prob.theta));
+            const Cplx ls = cplx_ipow(hElem, p - 2);
+            const Cplx ms = cplx_ipow(hElem, p);
+            lapScale[l] = ls;
+            massScale[l] = ms;
+            dev::LevelConst& k = kc[l];
+            for (int s = 0; s < (1 << p); ++s) {
+                double lap, mas;
+                reference_pattern(p, s, lap, mas);
+                const Cplx A = ls * lap - prob.phi * ms * mas;  // kernels.cpp:43-44
+                k.A[s] = make_double2(A.real(), A.imag());
+                k.M[s] = mas;
+            }
+            k.massScale = make_double2(ms.real(), ms.imag());
+            // interior diag: 2^p cell contributions A_aa (kernels.cpp:62-64)
+            double lap0, mas0;
+            reference_pattern(p, 0, lap0, mas0);
+            const Cplx Aaa = ls * lap0 - prob.phi * ms * mas0;
+            Cplx dg(0.0);
+            for (int i = 0; i < (1 << p); ++i) dg += Aaa;
+            diagInterior[l] = dg;
+            k.div = div_const(dg);
+        }
+    }
+
+    void build_restrict_tables() {
+        const int NT = p == 1 ? 5 : p == 2 ? 25 : 125;
+        const int NP = p == 1 ? 1 : p == 2 ? 2 : 6;
+        std::vector<unsigned char> table(static_cast<size_t>(NP * NT));
+        std::vector<double> w(NT);
+        // kW0/kW1 of transfer.cpp:7-8 per offset k in -2..2
+        const double k1d[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+        for (int code = 0; code < NT; ++code) {
+            double wt = 1.0;  // restriction_weight, cycles.cpp:46-50: product in axis order
+            int cc = code;
+            for (int d = 0; d < p; ++d) {
+                wt *= k1d[cc % 5];
+                cc /= 5;
+            }
+            w[code] = wt;
+        }
+        for (int id = 0; id < NP; ++id) {
+            int pos = 0;
+            for (int gi = 0; gi < (1 << p); ++gi) {
+                const int fsel = dev::perm_cell(p, id, gi);  // group = parent cell W-1+f
+                // within the group: lexicographic, axis p-1 slowest
+                int lo[3], cnt[3];
+                for (int d = 0; d < p; ++d) {
+                    lo[d] = ((fsel >> d) & 1) ? 0 : -2;
+                    cnt[d] = ((fsel >> d) & 1) ? 3 : 2;
+                }
+                int total = 1;
+                for (int d = 0; d < p; ++d) total *= cnt[d];
+                for (int t = 0; t < total; ++t) {
+                    int tt = t, code = 0, mul = 1;
+                    for (int d = 0; d < p; ++d) {
+                        const int k = lo[d] + tt % cnt[d];
+                        tt /= cnt[d];
+                        code += (k + 2) * mul;
+                        mul *= 5;
+                    }
+                    table[static_cast<size_t>(id * NT + pos++)] = static_cast<unsigned char>(code);
+                }
+            }
+        }
+        restrictTable = alloc<unsigned char>(table.size());
+        restrictWeights = alloc<double>(w.size());
+        TMG_CUDA(cudaMemcpyAsync(restrictTable, table.data(), table.size(), cudaMemcpyHostToDevice, stream));
+        TMG_CUDA(cudaMemcpyAsync(restrictWeights, w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, stream));
+        TMG_CUDA(cudaStreamSynchronize(stream));
+    }
+
+    template <int P>
+    void build_rhs_seeded() {
+        const dev::Lvl& F = lv[L];
+        const int key = prob.rhsLattice >= 0 ? prob.rhsLattice : L;
+        const int scale = pow3i(key - L);
+        dev::k_seeded_chi<P><<<blocks_for(F.n), 256, 0, stream>>>(chiNodal, F.n, F.n1, prob.rhsSeed, scale,
+                                                                  static_cast<long long>(pow3i(key)),
+                                                                  prob.rhsSphere ? 1 : 0);
+        TMG_CUDA(cudaGetLastError());
+    }
+
+    void build_rhs_analytic() {
+        // chi_at (problems.cpp:55-68) uses glibc sin; evaluated on the host
+        // once per setup so the nodal values are the reference's bits.
+        const dev::Lvl& F = lv[L];
+        std::vector<double2> h(F.n);
+        const double hh = std::pow(3.0, -L);
+        for (unsigned f = 0; f < F.n; ++f) {
+            unsigned ff = f;
+            double x[3];
+            for (int d = 0; d < p; ++d) {
+                x[d] = static_cast<int>(ff % F.n1) * hh;
+                ff /= F.n1;
+            }
+            double v = 0.0;
+            if (prob.chi == ChiKind::SinProduct) {
+                const double dd = static_cast<double>(p);
+                v = dd * M_PI * M_PI;
+                for (int d = 0; d < p; ++d) v *= std::sin(M_PI * x[d]);
+            } else if (prob.chi == ChiKind::BallIndicator) {
+                double r2 = 0.0;
+                for (int d = 0; d < p; ++d) r2 += (x[d] - 0.5) * (x[d] - 0.5);
+                v = r2 < 0.01 ? 1.0 : 0.0;
+            }
+            h[f] = make_double2(v, 0.0);
+        }
+        TMG_CUDA(cudaMemcpyAsync(chiNodal, h.data(), F.n * sizeof(double2), cudaMemcpyHostToDevice, stream));
+        TMG_CUDA(cudaStreamSynchronize(stream));
+    }
+
+    template <int P>
+    void load_vector() {
+        const dev::Lvl& F = lv[L];
+        dev::k_load_vector<P><<<blocks_for(F.n), 256, 0, stream>>>(F, chiNodal, kc[L]);
+        TMG_CUDA(cudaGetLastError());
+    }
+
+    void load_vector_dispatch() {
+        if (p == 1) load_vector<1>();
+        else if (p == 2) load_vector<2>();
+        else load_vector<3>();
+    }
+
+    template <int P>
+    void cycle_exact(const Policy& pol, int n, bool timed) {
+        // top-down (levels 1..L; level 0 holds only zero boundary corners)
+        for (int l = 1; l <= L; ++l) {
+            if (timed && l == L) TMG_CUDA(cudaEventRecord(evf0, stream));
+            dev::k_topdown<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], lv[l - 1], pol.bpx ? 1 : 0);
+        }
+        for (int l = L; l >= 1; --l) {
+            dev::ResArgs a{};
+            a.lv = lv[l];
+            a.par = lv[l - 1];
+            a.k = kc[l];
+            a.k.wRaw = make_double2(0.0, 0.0);
+            const Cplx w = omega_unmasked(pol, L - l, n);
+            a.k.wRaw = make_double2(w.real(), w.imag());
+            a.ellMin = prob.ellMin;
+            a.isFine = l == L ? 1 : 0;
+            a.bpx = pol.bpx ? 1 : 0;
+            a.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+            a.partials = partials;
+            const int nb = l == L ? normBlocks : blocks_for(lv[l].n);
+            dev::k_residual_exact<P><<<nb, 256, 0, stream>>>(a);
+            if (timed && l == L) TMG_CUDA(cudaEventRecord(evf1, stream));
+            if (l >= 2) {
+                const int zero = l <= prob.ellMin ? 1 : 0;
+                dev::k_restrict_exact<P><<<blocks_for(lv[l - 1].n), 256, 0, stream>>>(
+                    lv[l], lv[l - 1], restrictTable, restrictWeights, zero);
+            }
+        }
+        dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, normBlocks, dNorm);
+        TMG_CUDA(cudaGetLastError());
+    }
+
+    void check_diag() {
+        // jacobi (kernels.cpp:102-106) runs on interior vertices of levels
+        // >= ellMin; the interior diagonal is constant per level here.
+        for (int l = std::max(1, prob.ellMin); l <= L; ++l)
+            if (std::abs(diagInterior[l]) < 1e-300)
+                throw SingularDiagonalError("vanishing operator diagonal (phi*h^2 resonance?)");
+    }
+
+    SweepStats cycle(const Policy& pol, int n, bool timed = false) {
+        check_diag();
+        if (p == 1) cycle_exact<1>(pol, n, timed);
+        else if (p == 2) cycle_exact<2>(pol, n, timed);
+        else cycle_exact<3>(pol, n, timed);
+        TMG_CUDA(cudaMemcpyAsync(hNorm, dNorm, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        TMG_CUDA(cudaStreamSynchronize(stream));
+        SweepStats st;
+        const double hp = std::pow(std::pow(3.0, -L), p);
+        st.maxNorm = std::sqrt(hNorm[0]);
+        st.euclidNorm = std::sqrt(hNorm[1]);
+        st.hNorm = std::sqrt(hp * hNorm[1]);
+        long long inner = 1;
+        for (int d = 0; d < p; ++d) inner *= pow3i(L) - 1;
+        st.updatedFineVertices = inner;
+        return st;
+    }
+};
+
+Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
+    Impl& I = *impl_;
+    I.prob = prob;
+    I.p = prob.dim;
+    I.L = prob.levels;
+    if (prob.dim < 1 || prob.dim > 3) throw UnsupportedConfigError("B200 path: dim must be 1, 2 or 3");
+    if (prob.levels < 1) throw ConfigError("build_regular needs levels >= 1");
+    if (prob.levels > 9) throw ConfigError("tree depth exceeds supported maximum");
+    // build_regular's capacity estimate (spacetree.cpp:53-63)
+    std::size_t estimate = 0;
+    for (int l = 0; l <= prob.levels; ++l) {
+        std::size_t perAxis = static_cast<std::size_t>(pow3i(l)) + 1, n = 1;
+        for (int d = 0; d < prob.dim; ++d) n *= perAxis;
+        estimate += n;
+    }
+    if (estimate > prob.maxVertices)
+        throw CapacityError("regular grid would hold " + std::to_string(estimate) + " vertices, cap is " +
+                            std::to_string(prob.maxVertices));
+    TMG_CUDA(cudaSetDevice(prob.device));
+    cudaDeviceProp props{};
+    TMG_CUDA(cudaGetDeviceProperties(&props, prob.device));
+    I.smCount = props.multiProcessorCount;
+    TMG_CUDA(cudaStreamCreateWithFlags(&I.stream, cudaStreamNonBlocking));
+    TMG_CUDA(cudaEventCreate(&I.ev0));
+    TMG_CUDA(cudaEventCreate(&I.ev1));
+    TMG_CUDA(cudaEventCreate(&I.evf0));
+    TMG_CUDA(cudaEventCreate(&I.evf1));
+    const char* dbg = std::getenv("TMG_DEBUG_R");
+    I.debugR = dbg && dbg[0] == '1';
+    I.lv.resize(I.L + 1);
+    for (int l = 0; l <= I.L; ++l) I.lv[l] = I.make_level(l, l == I.L);
+    I.normBlocks = I.blocks_for(I.lv[I.L].n);
+    I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks));
+    I.dNorm = I.alloc<double>(2);
+    TMG_CUDA(cudaMallocHost(&I.hNorm, 2 * sizeof(double)));
+    I.chiNodal = I.alloc<double2>(I.lv[I.L].n);
+    I.compute_level_constants();
+    I.build_restrict_tables();
+    if (prob.chi == ChiKind::Seeded) {
+        if (I.p == 1) I.build_rhs_seeded<1>();
+        else if (I.p == 2) I.build_rhs_seeded<2>();
+        else I.build_rhs_seeded<3>();
+    } else {
+        I.build_rhs_analytic();
+    }
+    I.load_vector_dispatch();
+    TMG_CUDA(cudaStreamSynchronize(I.stream));
+}
+
+Hierarchy::~Hierarchy() = default;
+
+SweepStats Hierarchy::cycle(const Policy& pol, int n) { return impl_->cycle(pol, n); }
+
+int Hierarchy::dim() const { return impl_->p; }
+int Hierarchy::levels() const { return impl_->L; }
+
+long long Hierarchy::lattice_size(int level) const {
+    if (level < 0 || level > impl_->L) return 0;
+    return impl_->lv[level].n;
+}
+
+long long Hierarchy::interior_fine_vertices() const {
+    long long n = 1;
+    for (int d = 0; d < impl_->p; ++d) n *= pow3i(impl_->L) - 1;
+    return n;
+}
+
+namespace {
+double2* field_ptr(const dev::Lvl& v, const std::string& f) {
+    if (f == "u") return v.u;
+    if (f == "sc") return v.sc;
+    if (f == "sf") return v.sf;
+    if (f == "si") return v.si;
+    if (f == "sinext") return v.sinext;
+    if (f == "chi") return v.chi;
+    if (f == "uhat") return v.uhat;
+    if (f == "rhat") return v.rhat;
+    if (f == "r") return v.r;
+    return nullptr;
+}
+}  // namespace
+
+void Hierarchy::get_field(int level, const std::string& field, double* host) const {
+    Impl& I = *impl_;
+    if (level < 0 || level > I.L) throw ConfigError("get_field: level out of range");
+    const dev::Lvl& v = I.lv[level];
+    if (field == "diag") {
+        // host-side: per vertex the sum of A_aa over its existing cells
+        const Cplx a = I.diagInterior[level] / static_cast<double>(1 << I.p);
+        (void)a;
+        double lap0, mas0;
+        reference_pattern(I.p, 0, lap0, mas0);
+        const Cplx Aaa = I.lapScale[level] * lap0 - I.prob.phi * I.massScale[level] * mas0;
+        for (unsigned f = 0; f < v.n; ++f) {
+            unsigned ff = f;
+            int cells = 1;
+            for (int d = 0; d < I.p; ++d) {
+                const int x = static_cast<int>(ff % v.n1);
+                ff /= v.n1;
+                cells *= (x > 0 ? 1 : 0) + (x < static_cast<int>(v.m) ? 1 : 0);
+            }
+            Cplx dg(0.0);
+            for (int i = 0; i < cells; ++i) dg += Aaa;
+            host[2 * f] = dg.real();
+            host[2 * f + 1] = dg.imag();
+        }
+        return;
+    }
+    double2* ptr = field_ptr(v, field);
+    if (!ptr) {
+        if (field == "sf" || field == "si" || field == "sinext" || field == "r") {
+            std::fill(host, host + 2 * static_cast<size_t>(v.n), 0.0);
+            return;
+        }
+        throw ConfigError("get_field: unknown field '" + field + "'");
+    }
+    TMG_CUDA(cudaMemcpyAsync(host, ptr, static_cast<size_t>(v.n) * sizeof(double2), cudaMemcpyDeviceToHost, I.stream));
+    TMG_CUDA(cudaStreamSynchronize(I.stream));
+}
+
+void Hierarchy::set_field(int level, const std::string& field, const double* host) {
+    Impl& I = *impl_;
+    if (level < 0 || level > I.L) throw ConfigError("set_field: level out of range");
+    const dev::Lvl& v = I.lv[level];
+    double2* ptr = field_ptr(v, field);
+    if (!ptr) throw ConfigError("set_field: unknown field '" + field + "'");
+    TMG_CUDA(cudaMemcpyAsync(ptr, host, static_cast<size_t>(v.n) * sizeof(double2), cudaMemcpyHostToDevice, I.stream));
+    TMG_CUDA(cudaStreamSynchronize(I.stream));
+}
+
+namespace {
+template <int P>
+void inject_up(Hierarchy::Impl& I) {
+    for (int l = I.L - 1; l >= 1; --l)
+        dev::k_inject_u<P><<<I.blocks_for(I.lv[l].n), 256, 0, I.stream>>>(I.lv[l], I.lv[l + 1]);
+}
+}  // namespace
+
+struct HierarchyAccess {
+    static void reset_pipeline(Hierarchy::Impl& I) {
+        for (int l = 0; l <= I.L; ++l) {
+            const dev::Lvl& v = I.lv[l];
+            const size_t bytes = static_cast<size_t>(v.n) * sizeof(double2);
+            for (double2* ptr : {v.sc, v.sf, v.si, v.sinext, v.uhat})
+                if (ptr) TMG_CUDA(cudaMemsetAsync(ptr, 0, bytes, I.stream));
+        }
+    }
+};
+
+void Hierarchy::set_fine_interior_u(const double* host) {
+    Impl& I = *impl_;
+    const dev::Lvl& F = I.lv[I.L];
+    const long long ni = interior_fine_vertices();
+    double2* tmp = nullptr;
+    TMG_CUDA(cudaMalloc(&tmp, static_cast<size_t>(ni) * sizeof(double2)));
+    TMG_CUDA(cudaMemcpyAsync(tmp, host, static_cast<size_t>(ni) * sizeof(double2), cudaMemcpyHostToDevice, I.stream));
+    if (I.p == 1) dev::k_scatter_interior<1><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, tmp);
+    else if (I.p == 2) dev::k_scatter_interior<2><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, tmp);
+    else dev::k_scatter_interior<3><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, tmp);
+    if (I.p == 1) inject_up<1>(I);
+    else if (I.p == 2) inject_up<2>(I);
+    else inject_up<3>(I);
+    HierarchyAccess::reset_pipeline(I);
+    TMG_CUDA(cudaStreamSynchronize(I.stream));
+    cudaFree(tmp);
+}
+
+void Hierarchy::set_random_initial_guess(std::uint64_t seed) {
+    Impl& I = *impl_;
+    const dev::Lvl& F = I.lv[I.L];
+    if (I.p == 1) dev::k_random_fine<1><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
+    else if (I.p == 2) dev::k_random_fine<2><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
+    else dev::k_random_fine<3><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
+    if (I.p == 1) inject_up<1>(I);
+    else if (I.p == 2) inject_up<2>(I);
+    else inject_up<3>(I);
+    HierarchyAccess::reset_pipeline(I);
+    TMG_CUDA(cudaStreamSynchronize(I.stream));
+}
+
+void Hierarchy::set_fine_rhs(const double* hostNodalChi) {
+    Impl& I = *impl_;
+    const dev::Lvl& F = I.lv[I.L];
+    TMG_CUDA(cudaMemcpyAsync(I.chiNodal, hostNodalChi, static_cast<size_t>(F.n) * sizeof(double2),
+                             cudaMemcpyHostToDevice, I.stream));
+    I.load_vector_dispatch();
+    TMG_CUDA(cudaStreamSynchronize(I.stream));
+}
+
+std::uint64_t Hierarchy::field_hash(int level, const std::string& field) const {
+    const long long n = lattice_size(level);
+    std::vector<double> buf(2 * static_cast<size_t>(n));
+    get_field(level, field, buf.data());
+    std::uint64_t h = 1469598103934665603ull;
+    for (double x : buf) {
+        const double y = x + 0.0;
+        std::uint64_t bits;
+        std::memcpy(&bits, &y, 8);
+        for (int b = 0; b < 8; ++b) {
+            h ^= (bits >> (8 * b)) & 0xffu;
+            h *= 1099511628211ull;
+        }
+    }
+    return h;
+}
+
+void Hierarchy::unfold() { throw UnsupportedConfigError("FMG unfolding is not implemented yet"); }
+
+void Hierarchy::time_cycles(const Policy& pol, int n0, int count, bool flushL2, double* out4) {
+    Impl& I = *impl_;
+    I.check_diag();
+    if (flushL2 && !I.flushBuf) {
+        I.flushN = (256ull << 20) / sizeof(double4);  // 256 MB > 126 MB L2
+        I.flushBuf = I.alloc<double4>(I.flushN);
+    }
+    double totalMs = 0.0, fineMs = 0.0;
+    for (int i = 0; i < count; ++i) {
+        if (flushL2) dev::k_flush<<<4 * I.smCount, 256, 0, I.stream>>>(I.flushBuf, I.flushN, 0.0);
+        TMG_CUDA(cudaEventRecord(I.ev0, I.stream));
+        if (I.p == 1) I.cycle_exact<1>(pol, n0 + i, true);
+        else if (I.p == 2) I.cycle_exact<2>(pol, n0 + i, true);
+        else I.cycle_exact<3>(pol, n0 + i, true);
+        TMG_CUDA(cudaEventRecord(I.ev1, I.stream));
+        TMG_CUDA(cudaEventSynchronize(I.ev1));
+        float ms = 0.f, fms = 0.f;
+        TMG_CUDA(cudaEventElapsedTime(&ms, I.ev0, I.ev1));
+        TMG_CUDA(cudaEventElapsedTime(&fms, I.evf0, I.evf1));
+        totalMs += ms;
+        fineMs += fms;
+    }
+    out4[0] = totalMs;
+    out4[1] = count ? fineMs / count : 0.0;
+    out4[2] = 0.0;
+    out4[3] = static_cast<double>(3 * I.L);
+}
+
+void Hierarchy::e2e_step(const Policy& pol, int n, const double* hostChi, double* out3) {
+    Impl& I = *impl_;
+    const dev::Lvl& F = I.lv[I.L];
+    TMG_CUDA(cudaMemcpyAsync(I.chiNodal, hostChi, static_cast<size_t>(F.n) * sizeof(double2), cudaMemcpyHostToDevice,
+                             I.stream));
+    I.load_vector_dispatch();
+    const SweepStats st = I.cycle(pol, n);
+    out3[0] = st.maxNorm;
+    out3[1] = st.euclidNorm;
+    out3[2] = st.hNorm;
+}
+
+}  // namespace tmg

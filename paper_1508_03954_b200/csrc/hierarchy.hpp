@@ -1,0 +1,112 @@
+// Device-resident multilevel hierarchy of a regular 3^d spacetree: the B200
+// replacement of the reference's hash-per-level Spacetree storage
+// (proj/src/spacetree.cpp) plus the td_add / td_bpx cycle
+// (proj/src/cycles.cpp:57-354) as level passes of sm_100a kernels.
+//
+// Storage: one lattice array per field per level, (3^l+1)^d vertices, axis 0
+// fastest, complex128 as interleaved double2 (16-byte vector loads/stores).
+#pragma once
+
+#include <complex>
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace tmg {
+
+using Cplx = std::complex<double>;
+
+// Error classes mirror proj/include/treemg/types.hpp:18-38 so that the C-ABI
+// maps them to the same status codes (proj/src/capi.cpp:28-43).
+struct ConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct UnsupportedConfigError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CapacityError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct SingularDiagonalError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+enum class OmegaKind { JacobiOnly = 0, UndampedCG = 1, LGrid = 2, Exponential = 3, Transition = 4 };
+
+struct Policy {  // OmegaPolicy, proj/include/treemg/cycles.hpp:17-24
+    OmegaKind kind = OmegaKind::Exponential;
+    Cplx omegaS = Cplx(0.8, 0.0);
+    int lGrid = 2;
+    bool hbMask = false;
+    bool bpx = false;
+    bool twoPhase = false;
+};
+
+enum class ChiKind { Zero = 0, SinProduct = 1, BallIndicator = 2, Seeded = 3 };
+
+struct Problem {
+    int dim = 2;
+    int levels = 1;
+    int ellMin = 1;
+    double theta = 0.0;
+    Cplx phi = Cplx(0.0);
+    ChiKind chi = ChiKind::SinProduct;
+    std::uint64_t rhsSeed = 12345;
+    bool rhsSphere = false;
+    int rhsLattice = -1;  // level the seeded rhs is keyed on (-1: levels)
+    bool fast = false;    // precision = fast
+    std::size_t maxVertices = 8u * 1024u * 1024u;
+    int device = 0;
+};
+
+struct SweepStats {  // SweepStats, cycles.hpp:37-45 (one channel)
+    double maxNorm = 0.0, euclidNorm = 0.0, hNorm = 0.0;
+    long long updatedFineVertices = 0;
+};
+
+// omega_unmasked, proj/src/cycles.cpp:11-31 (host, same libstdc++ arithmetic)
+Cplx omega_unmasked(const Policy& pol, int succ, int n);
+
+class Hierarchy {
+  public:
+    explicit Hierarchy(const Problem& prob);
+    ~Hierarchy();
+    Hierarchy(const Hierarchy&) = delete;
+    Hierarchy& operator=(const Hierarchy&) = delete;
+
+    // One cycle.  bpx selects td_bpx (hb mask forced off, cycles.cpp:345-354).
+    SweepStats cycle(const Policy& pol, int n);
+
+    int dim() const;
+    int levels() const;
+    long long lattice_size(int level) const;
+    long long interior_fine_vertices() const;
+
+    void get_field(int level, const std::string& field, double* host) const;
+    void set_field(int level, const std::string& field, const double* host);
+    void set_fine_interior_u(const double* host);
+    void set_random_initial_guess(std::uint64_t seed);
+    void set_fine_rhs(const double* hostNodalChi);
+    std::uint64_t field_hash(int level, const std::string& field) const;
+
+    // Adds one uniformly refined level on top (FMG unfolding through
+    // refine_cell of every leaf + classify()): the new
+    // level's u is p-linearly prolonged, its other payload zero.
+    void unfold();
+
+    // Timing helpers (CUDA events on the hierarchy stream).
+    void time_cycles(const Policy& pol, int n0, int count, bool flushL2, double* out4);
+    void e2e_step(const Policy& pol, int n, const double* hostChi, double* out3);
+
+    struct Impl;
+
+  private:
+    std::unique_ptr<Impl> impl_;
+};
+
+}  // namespace tmg
