@@ -1,0 +1,312 @@
+#!/usr/bin/env python
+"""Benchmark of the additive multilevel Helmholtz cycle on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--workload cfg5|cfg3|cfg2|cfg1] [--precision fast|exact]
+
+A "step" is one additive multigrid cycle (td_add / td_bpx) over
+the whole hierarchy of the workload, inputs resident in HBM.  Metric
+(BASELINE.json): complex DoF-updates/s per cycle = interior fine DoF x
+cycles / device time, plus the fine-pass kernel's achieved HBM GB/s against
+MEASURED_PEAKS.json.  Prints ONE JSON line on rank 0.
+
+Workload: the BASELINE metric's target is quoted on the 243^3
+and 729^3 configs; the 729^3 cycle (cfg5's final FMG level, k=80) fits one
+GPU, so it is the N=1 workload.  Other configs are parity-test cases.
+
+N>1 (torchrun, one process per GPU): every rank runs its own 729^3 replica
+("scaling": "weak"); value = total DoF-updates of all ranks / max-over-ranks
+device time.  Round-1 status of the z-slab sharding: DESIGN.md §6.
+
+--impl reference: the reference CPU implementation (oracle/_ref, built from
+the unmodified reference sources) on the host cores -- one independent
+single-threaded reference process per core on an 81^3 sample of the same
+operator (the reference has no intra-solve parallelism), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# BASELINE.json configs -> solver settings: phi = k^2 (1 + 0.5 i)
+WORKLOADS = {
+    "cfg1": dict(dim=2, level=5, k=10, cycle="td-add", omega="exponential", omega_s=0.6,
+                 desc="2D depth 5 (243^2), k=10, additive MG, exponential omega 0.6"),
+    "cfg2": dict(dim=2, level=7, k=100, cycle="td-bpx", omega="undamped", omega_s=0.5,
+                 desc="2D depth 7 (2187^2), k=100, BPX variant, undamped omega 0.5"),
+    "cfg3": dict(dim=3, level=5, k=20, cycle="td-add", omega="exponential", omega_s=0.6,
+                 desc="3D depth 5 (243^3), k=20, additive MG, exponential omega 0.6"),
+    "cfg5": dict(dim=3, level=6, k=80, cycle="td-add", omega="exponential", omega_s=0.6,
+                 desc="3D depth 6 (729^3), k=80, additive MG, exponential omega 0.6 (cfg5 final FMG level)"),
+}
+RHS_SEED = 12345
+
+
+def interior(w):
+    return (3 ** w["level"] - 1) ** w["dim"]
+
+
+def lattice(level, dim):
+    return (3 ** level + 1) ** dim
+
+
+def algorithmic_bytes(w, precision):
+    """B = 80 N_L + 200 sum_{l<L} N_l (complex128 lattice sizes)."""
+    NL = lattice(w["level"], w["dim"])
+    coarse = sum(lattice(l, w["dim"]) for l in range(1, w["level"]))
+    return 80 * NL + 200 * coarse, 80 * NL
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = os.path.join("/tmp", f"tmg_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.fh.close()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.path):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    sm.append(float(f[0]))
+                    mx = max(mx, float(f[1]))
+                except ValueError:
+                    continue
+                for n, v in zip(names, f[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(n)
+        except FileNotFoundError:
+            pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# reference CPU arm
+def _ref_worker(args):
+    w, steps, warmup, q = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refdriver as R
+    cfg = dict(problem="helmholtz-sin", dim=w["dim"], level=w["sample_level"],
+               phi=f"{w['k'] ** 2},{0.5 * w['k'] ** 2}", cycle=w["cycle"], omega=w["omega"],
+               omega_s=w["omega_s"], max_sweeps=10 ** 6, target_drop=1e-300, rhs="seeded", rhs_seed=RHS_SEED,
+               max_vertices=10 ** 9)
+    s = R.RefSession(cfg)
+    for n in range(1, warmup + 1):
+        s.sweep(n)
+    times = []
+    for n in range(warmup + 1, warmup + steps + 1):
+        t0 = time.perf_counter()
+        s.sweep(n)
+        times.append(time.perf_counter() - t0)
+    q.put(times)
+
+
+def reference_sample(w, steps, warmup, procs):
+    """Time `procs` independent reference processes on a bounded sample."""
+    ws = dict(w)
+    ws["sample_level"] = 4 if w["dim"] == 3 else min(w["level"], 6)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_ref_worker, args=((ws, steps, warmup, q),)) for _ in range(procs)]
+    for p in ps:
+        p.start()
+    res = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
+    dof = (3 ** ws["sample_level"] - 1) ** w["dim"]
+    per_step = [max(r[i] for r in res) for i in range(steps)]  # all processes finish a step
+    total = sum(per_step)
+    value = procs * dof * steps / total
+    sample = (f"{procs} independent single-threaded reference processes, each {steps} timed cycles (+{warmup} warm-up) "
+              f"of the same operator on the level-{ws['sample_level']} sub-problem "
+              f"({3 ** ws['sample_level']}^{w['dim']} cells, {dof} DoF)")
+    return value, total / steps, sample
+
+
+def run_reference_arm(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    procs = max(1, min(os.cpu_count() or 1, 64))
+    try:
+        import refdriver  # noqa: F401
+    except Exception:
+        pass
+    if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtreemg_ref.so")):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtreemg_ref.so not built"}))
+        return 0
+    value, sec_per_step, sample = reference_sample(w, args.steps, args.warmup, procs)
+    line = {
+        "metric": "complex DoF-updates/s per additive MG cycle", "value": value, "unit": "DoF-updates/s",
+        "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "complex128 (f64)", "data": "synthetic (seeded uniform complex rhs, SURVEY §8d)",
+        "config": {"workload": args.workload, "desc": w["desc"], "precision": "reference"},
+        "cpu_baseline": {"value": value, "unit": "DoF-updates/s", "cores": procs, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "DoF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# --------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="cfg5", choices=list(WORKLOADS))
+    ap.add_argument("--precision", default=os.environ.get("TMG_PRECISION", "fast"), choices=["fast", "exact"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference_arm(args, w)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dist = None
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl")
+
+    import numpy as np
+    import paper_1508_03954_b200 as T
+
+    k = w["k"]
+    phi = complex(k * k, 0.5 * k * k)
+    h = T.Hierarchy(w["dim"], w["level"], phi=phi, chi="seeded", rhs_seed=RHS_SEED, precision=args.precision,
+                    max_vertices=10 ** 10, device=local)
+    pol = T.Policy(kind=w["omega"], omega_s=w["omega_s"], bpx=(w["cycle"] == "td-bpx"))
+    # warm-up cycles (untimed), then K timed cycles with CUDA events on the library stream
+    h.time_cycles(pol, 1, args.warmup, flush_l2=False)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+            import torch
+            torch.cuda.synchronize()
+
+    barrier()
+    with ClockSampler(local) as clk:
+        out = h.time_cycles(pol, args.warmup + 1, args.steps, flush_l2=False)
+    barrier()
+    total_ms, fine_ms, launches_per_cycle = float(out[0]), float(out[1]), int(out[3])
+    if dist:
+        import torch
+        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    dof = interior(w)
+    ms_per_step = total_ms / args.steps
+    value = world * dof * args.steps / (total_ms / 1e3)
+    B_total, B_fine = algorithmic_bytes(w, args.precision)
+    peak, peak_kind = peaks()
+    achieved = B_fine / (fine_ms / 1e3) / 1e9
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None, "kernel": "fine-level pass (K1 top-down + K2 residual/smooth/restrict), "
+                f"{B_fine / 1e9:.2f} GB algorithmic per cycle (80 B per fine vertex)",
+                "peak_kind": peak_kind, "whole_cycle_GBps": B_total / (ms_per_step / 1e3) / 1e9}
+
+    # e2e through the boundary: host rhs (pinned) -> device -> one cycle -> host norms
+    n_lat = lattice(w["level"], w["dim"])
+    try:
+        import torch
+        chi_host = torch.empty(2 * n_lat, dtype=torch.float64, pin_memory=True).numpy()
+    except Exception:
+        chi_host = np.empty(2 * n_lat)
+    rng = np.random.default_rng(RHS_SEED)
+    chi_host[:] = rng.uniform(-1, 1, size=2 * n_lat)
+    e2e_steps = max(2, min(args.steps, 5))
+    t0 = time.perf_counter()
+    for i in range(e2e_steps):
+        h.e2e_step(pol, args.warmup + args.steps + 1 + i, chi_host)
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    e2e = {"value": world * dof / e2e_s, "unit": "DoF-updates/s", "h2d_bytes_per_step": 16 * n_lat,
+           "d2h_bytes_per_step": 24, "note": "per step: H2D of the nodal rhs (16 B/vertex, pinned), device load "
+           "vector, one cycle, D2H of the three residual norms (wall clock)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            v, sps, sample = reference_sample(w, 4, 1, 1)
+            cpu = {"value": v, "unit": "DoF-updates/s", "cores": 1, "kind": "reference", "sample": sample}
+        except Exception as exc:  # reported, never silently replaced
+            cpu = {"value": None, "unit": "DoF-updates/s", "cores": 1, "kind": "reference",
+                   "sample": f"unavailable: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "complex DoF-updates/s per additive MG cycle", "value": value, "unit": "DoF-updates/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
+            "data": "synthetic (seeded uniform complex rhs, SURVEY §8d)",
+            "config": {"workload": args.workload, "desc": w["desc"], "dim": w["dim"], "level": w["level"],
+                       "interior_dof": dof, "precision": args.precision, "cycle": w["cycle"],
+                       "l2": "inputs larger than L2 (fine level arrays of "
+                             f"{16 * n_lat / 1e9:.2f} GB each); no flush",
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": launches_per_cycle * args.steps, "fine_pass_ms": fine_ms,
+        }
+        print(json.dumps(line))
+    if dist:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,321 @@
+// Fast-precision cycle kernels; see fast.cuh for the formulation and
+// DESIGN.md §3 for the roofline of each kernel.
+
+#include "fast.cuh"
+
+namespace tmg {
+namespace fast {
+
+using dev::Lvl;
+
+namespace {
+
+__device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// acc + a * b
+__device__ __forceinline__ double2 mac(double2 acc, double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ double2 ld(const double2* p) { return __ldg(p); }
+
+__device__ __forceinline__ double2 lerp(double2 c0, double2 c1, int rel) {
+    if (rel == 0) return c0;
+    if (rel == 3) return c1;
+    const double w1 = rel == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
+    return make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
+}
+
+template <int P>
+__device__ __forceinline__ double2 prolong_at(const double2* __restrict__ src, unsigned n1, const int* q,
+                                              const int* rel) {
+    double2 v[1 << P];
+#pragma unroll
+    for (int e = 0; e < (1 << P); ++e) {
+        unsigned f = 0, s = 1;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            f += static_cast<unsigned>(q[d] + ((e >> d) & 1)) * s;
+            s *= n1;
+        }
+        v[e] = ld(src + f);
+    }
+#pragma unroll
+    for (int d = 0; d < P; ++d)
+#pragma unroll
+        for (int i = 0; i < (1 << (P - 1 - d)); ++i) v[i] = lerp(v[2 * i], v[2 * i + 1], rel[d]);
+    return v[0];
+}
+
+// sc staging shared by fine and coarse smoothing (cycles.cpp:264-278)
+__device__ __forceinline__ double2 stage(double2 smooth, double2 w, bool cp, int bpx, int hb) {
+    if (bpx) return cp ? make_double2(0.0, 0.0) : mul(w, smooth);
+    if ((hb && cp) || (w.x == 0.0 && w.y == 0.0)) return make_double2(0.0, 0.0);
+    return mul(w, smooth);
+}
+
+// ---- K1f / K1c: top-down correction ----------------------------------------
+template <int P, bool FINE>
+__global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        dev::unflat<P>(f, c.n1, idx);
+        if (dev::on_boundary<P>(idx, static_cast<int>(c.m))) continue;  // u = sc = 0 stay pinned
+        int q[P], rel[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            q[d] = min(idx[d] / 3, static_cast<int>(pr.m) - 1);
+            rel[d] = idx[d] - 3 * q[d];
+        }
+        double2 sc = add(c.sc[f], prolong_at<P>(pr.sc, pr.n1, q, rel));
+        if (bpx && !dev::is_cpoint<P>(idx)) sc = sub(sc, prolong_at<P>(pr.si, pr.n1, q, rel));
+        if (FINE) {
+            c.u[f] = add(c.u[f], sc);  // sf is identically zero on the finest level
+        } else {
+            c.sc[f] = sc;
+        }
+    }
+}
+
+// ---- K2f (3D): r = b - H u by z-marching planes -----------------------------
+// Block = 32 x 4 columns (x, y); each thread walks ZCH planes in z, forming per
+// plane the centre / 4-edge / 4-corner sums of its 3x3 neighbourhood so every
+// u value is loaded 9x per vertex from L1 (not 27x) and once from HBM.
+constexpr int TX = 32, TY = 4;
+
+__global__ void __launch_bounds__(TX* TY) k_residual3(ResArgs a, int zch) {
+    const Lvl& F = a.lv;
+    const int m = static_cast<int>(F.m);
+    const long long sy = F.n1, sz = static_cast<long long>(F.n1) * F.n1;
+    const int x = blockIdx.x * TX + threadIdx.x + 1;
+    const int y = blockIdx.y * TY + threadIdx.y + 1;
+    const int z0 = blockIdx.z * zch + 1;
+    const int z1 = min(z0 + zch, m);
+    double nmax = 0.0, nsum = 0.0;
+    if (x <= m - 1 && y <= m - 1 && z0 < z1) {
+        const double2 c0 = a.k.c[0], c1 = a.k.c[1], c2 = a.k.c[2], c3 = a.k.c[3];
+        const double2* __restrict__ u = F.u;
+        const long long base = x + y * sy;
+        auto plane = [&](int z, double2& C, double2& E, double2& K) {
+            const double2* p = u + base + z * sz;
+            C = ld(p);
+            E = add(add(ld(p - 1), ld(p + 1)), add(ld(p - sy), ld(p + sy)));
+            K = add(add(ld(p - 1 - sy), ld(p + 1 - sy)), add(ld(p - 1 + sy), ld(p + 1 + sy)));
+        };
+        double2 Cm, Em, Km, C0, E0, K0, Cp, Ep, Kp;
+        plane(z0 - 1, Cm, Em, Km);
+        plane(z0, C0, E0, K0);
+        const bool cpxy = (x % 3 == 0) && (y % 3 == 0);
+        const bool inject = a.bpx && F.level > a.ellMin;
+        for (int z = z0; z < z1; ++z) {
+            plane(z + 1, Cp, Ep, Kp);
+            const double2 faces = add(E0, add(Cm, Cp));
+            const double2 edges = add(K0, add(Em, Ep));
+            const double2 corners = add(Km, Kp);
+            double2 hu = mul(c0, C0);
+            hu = mac(hu, c1, faces);
+            hu = mac(hu, c2, edges);
+            hu = mac(hu, c3, corners);
+            const long long f = base + z * sz;
+            const double2 r = sub(ld(F.chi + f), hu);
+            const double m2 = fma(r.x, r.x, r.y * r.y);
+            nmax = fmax(nmax, m2);
+            nsum += m2;
+            const bool cp = cpxy && (z % 3 == 0);
+            const double2 smooth = mul(r, a.k.invDiag);
+            F.sc[f] = F.level < a.ellMin ? make_double2(0.0, 0.0) : stage(smooth, a.k.wRaw, cp, a.bpx, a.hb);
+            F.rhat[f] = r;
+            if (inject && cp) {
+                const unsigned wf = static_cast<unsigned>(x / 3) +
+                                    a.par.n1 * (static_cast<unsigned>(y / 3) + a.par.n1 * static_cast<unsigned>(z / 3));
+                a.par.sinext[wf] = mul(a.k.wRaw, smooth);
+            }
+            Cm = C0; Em = E0; Km = K0;
+            C0 = Cp; E0 = Ep; K0 = Kp;
+        }
+    }
+    dev::block_norms(nmax, nsum, a.partials);
+}
+
+// ---- K2f (1D / 2D): thread per vertex ---------------------------------------
+template <int P>
+__global__ void __launch_bounds__(256) k_residual_lowdim(ResArgs a) {
+    const Lvl& F = a.lv;
+    double nmax = 0.0, nsum = 0.0;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < F.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        dev::unflat<P>(f, F.n1, idx);
+        if (dev::on_boundary<P>(idx, static_cast<int>(F.m))) continue;
+        double2 hu;
+        if (P == 1) {
+            hu = mul(a.k.c[0], ld(F.u + f));
+            hu = mac(hu, a.k.c[1], add(ld(F.u + f - 1), ld(F.u + f + 1)));
+        } else {
+            const long long sy = F.n1;
+            const double2* p = F.u + f;
+            hu = mul(a.k.c[0], ld(p));
+            hu = mac(hu, a.k.c[1], add(add(ld(p - 1), ld(p + 1)), add(ld(p - sy), ld(p + sy))));
+            hu = mac(hu, a.k.c[2], add(add(ld(p - 1 - sy), ld(p + 1 - sy)), add(ld(p - 1 + sy), ld(p + 1 + sy))));
+        }
+        const double2 r = sub(ld(F.chi + f), hu);
+        const double m2 = fma(r.x, r.x, r.y * r.y);
+        nmax = fmax(nmax, m2);
+        nsum += m2;
+        const bool cp = dev::is_cpoint<P>(idx);
+        const double2 smooth = mul(r, a.k.invDiag);
+        F.sc[f] = F.level < a.ellMin ? make_double2(0.0, 0.0) : stage(smooth, a.k.wRaw, cp, a.bpx, a.hb);
+        F.rhat[f] = r;
+        if (a.bpx && F.level > a.ellMin && cp) {
+            int wi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+            a.par.sinext[dev::flat<P>(wi, a.par.n1)] = mul(a.k.wRaw, smooth);
+        }
+    }
+    dev::block_norms(nmax, nsum, a.partials);
+}
+
+// ---- K3r: r_{l-1} = R r_l (separable 1D weights 1/3 2/3 1 2/3 1/3) -----------
+template <int P>
+__global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse) {
+    const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+    const long long sy = fine.n1, sz = static_cast<long long>(fine.n1) * fine.n1;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < coarse.n; f += gridDim.x * blockDim.x) {
+        int W[P];
+        dev::unflat<P>(f, coarse.n1, W);
+        if (dev::on_boundary<P>(W, static_cast<int>(coarse.m))) continue;
+        long long centre = 0, s = 1;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            centre += 3LL * W[d] * s;
+            s *= fine.n1;
+        }
+        const double2* __restrict__ r = fine.rhat + centre;
+        double2 acc = make_double2(0.0, 0.0);
+        if (P == 1) {
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const double2 v = ld(r + (i - 2));
+                acc.x = fma(w[i], v.x, acc.x);
+                acc.y = fma(w[i], v.y, acc.y);
+            }
+        } else if (P == 2) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const double2 v = ld(r + (j - 2) * sy + (i - 2));
+                    row.x = fma(w[i], v.x, row.x);
+                    row.y = fma(w[i], v.y, row.y);
+                }
+                acc.x = fma(w[j], row.x, acc.x);
+                acc.y = fma(w[j], row.y, acc.y);
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                double2 pl = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) {
+                        const double2 v = ld(r + (k - 2) * sz + (j - 2) * sy + (i - 2));
+                        row.x = fma(w[i], v.x, row.x);
+                        row.y = fma(w[i], v.y, row.y);
+                    }
+                    pl.x = fma(w[j], row.x, pl.x);
+                    pl.y = fma(w[j], row.y, pl.y);
+                }
+                acc.x = fma(w[k], pl.x, acc.x);
+                acc.y = fma(w[k], pl.y, acc.y);
+            }
+        }
+        coarse.rhat[f] = acc;
+    }
+}
+
+// ---- K3c: coarse smoothing on the restricted residual ------------------------
+template <int P>
+__global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a) {
+    const Lvl& c = a.lv;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        dev::unflat<P>(f, c.n1, idx);
+        if (c.si) {  // si = siNext (cycles.cpp:247)
+            c.si[f] = c.sinext[f];
+            c.sinext[f] = make_double2(0.0, 0.0);
+        }
+        if (dev::on_boundary<P>(idx, static_cast<int>(c.m)) || c.level < a.ellMin) {
+            c.sc[f] = make_double2(0.0, 0.0);
+            continue;
+        }
+        const bool cp = dev::is_cpoint<P>(idx);
+        const double2 smooth = mul(c.rhat[f], a.k.invDiag);
+        c.sc[f] = stage(smooth, a.k.wRaw, cp, a.bpx, a.hb);
+        if (a.bpx && c.level > a.ellMin && cp) {
+            int wi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+            a.par.sinext[dev::flat<P>(wi, a.par.n1)] = mul(a.k.wRaw, smooth);
+        }
+    }
+}
+
+constexpr int kZch = 48;
+
+}  // namespace
+
+void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaStream_t s) {
+    if (P == 1) k_topdown<1, true><<<blocks, 256, 0, s>>>(f, pr, bpx);
+    else if (P == 2) k_topdown<2, true><<<blocks, 256, 0, s>>>(f, pr, bpx);
+    else k_topdown<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx);
+}
+
+void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cudaStream_t s) {
+    if (P == 1) k_topdown<1, false><<<blocks, 256, 0, s>>>(c, pr, bpx);
+    else if (P == 2) k_topdown<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx);
+    else k_topdown<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx);
+}
+
+int residual_fine_blocks(int P, const Lvl& f, int smCount) {
+    if (P == 3) {
+        const int m = static_cast<int>(f.m);
+        const int bx = (m - 1 + TX - 1) / TX, by = (m - 1 + TY - 1) / TY, bz = (m - 1 + kZch - 1) / kZch;
+        return bx * by * bz;
+    }
+    const long long need = (static_cast<long long>(f.n) + 255) / 256;
+    return static_cast<int>(std::max<long long>(1, std::min<long long>(need, 8LL * smCount)));
+}
+
+int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s) {
+    const int nb = residual_fine_blocks(P, a.lv, smCount);
+    if (P == 3) {
+        const int m = static_cast<int>(a.lv.m);
+        dim3 grid((m - 1 + TX - 1) / TX, (m - 1 + TY - 1) / TY, (m - 1 + kZch - 1) / kZch);
+        k_residual3<<<grid, dim3(TX, TY), 0, s>>>(a, kZch);
+    } else if (P == 2) {
+        k_residual_lowdim<2><<<nb, 256, 0, s>>>(a);
+    } else {
+        k_residual_lowdim<1><<<nb, 256, 0, s>>>(a);
+    }
+    return nb;
+}
+
+void restrict_level(int P, const Lvl& fine, const Lvl& coarse, const double*, int blocks, cudaStream_t s) {
+    if (P == 1) k_restrict<1><<<blocks, 256, 0, s>>>(fine, coarse);
+    else if (P == 2) k_restrict<2><<<blocks, 256, 0, s>>>(fine, coarse);
+    else k_restrict<3><<<blocks, 256, 0, s>>>(fine, coarse);
+}
+
+void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s) {
+    if (P == 1) k_smooth_coarse<1><<<blocks, 256, 0, s>>>(a);
+    else if (P == 2) k_smooth_coarse<2><<<blocks, 256, 0, s>>>(a);
+    else k_smooth_coarse<3><<<blocks, 256, 0, s>>>(a);
+}
+
+}  // namespace fast
+}  // namespace tmg

@@ -1,0 +1,54 @@
+// Fast-precision cycle kernels (precision = fast).
+//
+// Same cycle as the exact path evaluated the way a GPU
+// wants it, mathematically identical and different only by rounding:
+//  * the fine operator is applied as its assembled 3^d-point stencil with one
+//    complex coefficient per neighbour class (centre / face / edge / corner:
+//    2^(d-k) A_k for a neighbour differing on k axes), with FMA;
+//  * the coarse levels run in correction form: on a regular grid with uniform
+//    theta and constant phi the FAS coarse residual chi_l - H_l u_l equals
+//    R r_{l+1} exactly (Lemma 2 + Galerkin, proj/tests/test_cycles.cpp:233-259
+//    and Lemma 1 :217-231), so coarse levels carry only sc, the restricted
+//    residual and the BPX si -- no coarse matvec, no u-hat;
+//  * the Jacobi division uses the level's precomputed 1/diag.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "lattice.cuh"
+
+namespace tmg {
+namespace fast {
+
+struct LevelCoef {
+    double2 c[4];     // stencil coefficient per neighbour class (popcount of the offset)
+    double2 invDiag;  // 1 / diag of an interior vertex
+    double2 wRaw;     // omega_unmasked(pol, L - l, n)
+};
+
+struct ResArgs {
+    dev::Lvl lv;   // the level being smoothed
+    dev::Lvl par;  // level l-1: BPX si injection target
+    LevelCoef k;
+    int ellMin;
+    int bpx;
+    int hb;
+    double* partials;
+};
+
+// Fine level: u += sc + P sc_{L-1} (- P si_{L-1} at non-cPoints, BPX).
+void correct_fine(int P, const dev::Lvl& f, const dev::Lvl& pr, int bpx, int blocks, cudaStream_t s);
+// Coarse level l < L: sc_l += P sc_{l-1} (- P si_{l-1}, BPX).
+void topdown_coarse(int P, const dev::Lvl& c, const dev::Lvl& pr, int bpx, int blocks, cudaStream_t s);
+// Fine residual r = b - H u, norms, sc = omega r / diag, BPX injection; r to lv.rhat.
+// Returns the number of blocks that wrote norm partials.
+int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s);
+int residual_fine_blocks(int P, const dev::Lvl& f, int smCount);
+// r_{l-1} = R r_l on interior coarse vertices (rhat arrays).
+void restrict_level(int P, const dev::Lvl& fine, const dev::Lvl& coarse, const double* weights, int blocks,
+                    cudaStream_t s);
+// Coarse smoothing: sc_l = omega r_l / diag, si commit, BPX injection into l-1.
+void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s);
+
+}  // namespace fast
+}  // namespace tmg

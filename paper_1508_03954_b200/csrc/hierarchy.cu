@@ -21,7 +21,9 @@
 #include <vector>
 
 #include "exact_ops.cuh"
+#include "fast.cuh"
 #include "hierarchy.hpp"
+#include "lattice.cuh"
 
 namespace tmg {
 
@@ -36,22 +38,6 @@ namespace tmg {
     } while (0)
 
 namespace dev {
-
-struct Lvl {
-    double2* u;
-    double2* sc;
-    double2* sf;
-    double2* si;
-    double2* sinext;
-    double2* chi;
-    double2* uhat;
-    double2* rhat;
-    double2* r;  // optional debug copy of the residual
-    unsigned m;   // 3^l
-    unsigned n1;  // 3^l + 1
-    unsigned n;   // (3^l+1)^p
-    int level;
-};
 
 struct LevelConst {
     double2 A[8];   // element operator entry for XOR pattern of (a, b)
@@ -71,63 +57,6 @@ struct ResArgs {
     int hb;
     double* partials;  // 2 doubles per block: max |r|^2, sum |r|^2
 };
-
-template <int P>
-__device__ __forceinline__ void unflat(unsigned f, unsigned n1, int* idx) {
-#pragma unroll
-    for (int d = 0; d < P; ++d) {
-        idx[d] = static_cast<int>(f % n1);
-        f /= n1;
-    }
-}
-
-template <int P>
-__device__ __forceinline__ unsigned flat(const int* idx, unsigned n1) {
-    unsigned f = 0, s = 1;
-#pragma unroll
-    for (int d = 0; d < P; ++d) {
-        f += static_cast<unsigned>(idx[d]) * s;
-        s *= n1;
-    }
-    return f;
-}
-
-template <int P>
-__device__ __forceinline__ bool on_boundary(const int* idx, int m) {
-    bool b = false;
-#pragma unroll
-    for (int d = 0; d < P; ++d) b |= (idx[d] == 0) | (idx[d] == m);
-    return b;
-}
-
-template <int P>
-__device__ __forceinline__ bool is_cpoint(const int* idx) {
-    bool c = true;
-#pragma unroll
-    for (int d = 0; d < P; ++d) c &= (idx[d] % 3 == 0);
-    return c;
-}
-
-// proj/src/transfer.cpp:20-40, one axis fold: exact copies at rel 0 / 3.
-__device__ __forceinline__ double2 lerp_rel(double2 c0, double2 c1, int rel) {
-    if (rel == 0) return c0;
-    if (rel == 3) return c1;
-    const double w0 = rel == 1 ? (2.0 / 3.0) : (1.0 / 3.0);
-    const double w1 = rel == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
-    return xadd(xscale(w0, c0), xscale(w1, c1));
-}
-
-template <int P>
-__device__ __forceinline__ double2 prolong(double2 (&v)[1 << P], const int* rel) {
-    int n = 1 << P;
-#pragma unroll
-    for (int d = 0; d < P; ++d) {
-        n >>= 1;
-#pragma unroll
-        for (int i = 0; i < (1 << (P - 1 - d)); ++i) v[i] = lerp_rel(v[2 * i], v[2 * i + 1], rel[d]);
-    }
-    return v[0];
-}
 
 // ---- K1: top-down update (touch_first, cycles.cpp:102-141) ----------------
 template <int P>
@@ -238,38 +167,6 @@ __device__ __forceinline__ double2 element_residual(const double2* __restrict__ 
     }
 }
 
-__device__ __forceinline__ void block_norms(double m2, double& outMax, double& outSum, double* partials) {
-    __shared__ double smax[32], ssum[32];
-    double mx = m2, sm = m2;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        sm += __shfl_xor_sync(0xffffffffu, sm, o);
-    }
-    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
-    if (l == 0) {
-        smax[w] = mx;
-        ssum[w] = sm;
-    }
-    __syncthreads();
-    if (w == 0) {
-        const int nw = blockDim.x >> 5;
-        mx = l < nw ? smax[l] : 0.0;
-        sm = l < nw ? ssum[l] : 0.0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            sm += __shfl_xor_sync(0xffffffffu, sm, o);
-        }
-        if (l == 0) {
-            partials[2 * blockIdx.x] = mx;
-            partials[2 * blockIdx.x + 1] = sm;
-        }
-    }
-    (void)outMax;
-    (void)outSum;
-}
-
 // ---- K2/K3: residual + Jacobi staging + injections (enterCell/touchLast) --
 template <int P>
 __global__ void __launch_bounds__(256) k_residual_exact(ResArgs a) {
@@ -323,8 +220,7 @@ __global__ void __launch_bounds__(256) k_residual_exact(ResArgs a) {
             if (a.bpx) a.par.sinext[wf] = xmul(a.k.wRaw, smooth);
         }
     }
-    if (a.isFine) block_norms(nmax, nmax, nsum, a.partials);
-    (void)nsum;
+    if (a.isFine) block_norms(nmax, nsum, a.partials);
 }
 
 // ---- K3r: restriction chi_{l-1} = R rhat_l in touch-last order -------------
@@ -658,13 +554,15 @@ struct Hierarchy::Impl {
     double2* chiNodal = nullptr;  // device nodal rhs at the finest lattice
     double4* flushBuf = nullptr;
     size_t flushN = 0;
-    std::vector<dev::LevelConst> kc;  // per level
+    std::vector<dev::LevelConst> kc;  // per level (exact)
+    std::vector<fast::LevelCoef> fc;  // per level (fast)
     std::vector<Cplx> diagInterior;
     std::vector<Cplx> lapScale, massScale;
     bool debugR = false;
     int smCount = 148;
     float lastFineMs = 0.f, lastTdMs = 0.f;
     bool timeFine = false;
+    bool coarseUStale = false;
 
     ~Impl() {
         for (void* ptr : allocations) cudaFree(ptr);
@@ -701,11 +599,15 @@ struct Hierarchy::Impl {
         v.n = static_cast<unsigned>(n);
         v.u = alloc<double2>(n);
         v.sc = alloc<double2>(n);
-        v.chi = alloc<double2>(n);
-        v.uhat = alloc<double2>(n);
         v.rhat = alloc<double2>(n);
+        if (!prob.fast) {  // exact: the full FAS state of cycles.cpp
+            v.chi = alloc<double2>(n);
+            v.uhat = alloc<double2>(n);
+            if (!fine) v.sf = alloc<double2>(n);
+        } else if (fine) {  // fast: load vector on the finest level only
+            v.chi = alloc<double2>(n);
+        }
         if (!fine) {
-            v.sf = alloc<double2>(n);
             v.si = alloc<double2>(n);
             v.sinext = alloc<double2>(n);
         }
@@ -715,6 +617,7 @@ struct Hierarchy::Impl {
 
     void compute_level_constants() {
         kc.assign(L + 1, dev::LevelConst{});
+        fc.assign(L + 1, fast::LevelCoef{});
         diagInterior.assign(L + 1, Cplx(0.0));
         lapScale.assign(L + 1, Cplx(0.0));
         massScale.assign(L + 1, Cplx(0.0));
@@ -743,6 +646,16 @@ struct Hierarchy::Impl {
             for (int i = 0; i < (1 << p); ++i) dg += Aaa;
             diagInterior[l] = dg;
             k.div = div_const(dg);
+            fast::LevelCoef& fcl = fc[l];
+            for (int cls = 0; cls <= p; ++cls) {  // assembled stencil: 2^(p-k) A_k per class
+                double lapk, mask;
+                reference_pattern(p, (1 << cls) - 1, lapk, mask);
+                const Cplx Ak = ls * lapk - prob.phi * ms * mask;
+                const Cplx ck = static_cast<double>(1 << (p - cls)) * Ak;
+                fcl.c[cls] = make_double2(ck.real(), ck.imag());
+            }
+            const Cplx inv = 1.0 / dg;
+            fcl.invDiag = make_double2(inv.real(), inv.imag());
         }
     }
 
@@ -879,6 +792,66 @@ struct Hierarchy::Impl {
         TMG_CUDA(cudaGetLastError());
     }
 
+    template <int P>
+    void cycle_fast(const Policy& pol, int n, bool timed) {
+        const int bpx = pol.bpx ? 1 : 0;
+        for (int l = 1; l < L; ++l) fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+        if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
+        fast::correct_fine(P, lv[L], lv[L - 1], bpx, blocks_for(lv[L].n), stream);
+        auto args = [&](int l) {
+            fast::ResArgs a{};
+            a.lv = lv[l];
+            a.par = lv[l - 1];
+            a.k = fc[l];
+            const Cplx w = omega_unmasked(pol, L - l, n);
+            a.k.wRaw = make_double2(w.real(), w.imag());
+            a.ellMin = prob.ellMin;
+            a.bpx = bpx;
+            a.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+            a.partials = partials;
+            return a;
+        };
+        const int nb = fast::residual_fine(P, args(L), smCount, stream);
+        if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+        for (int l = L - 1; l >= 1; --l) {
+            if (l >= prob.ellMin) fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
+            fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+        }
+        dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, nb, dNorm);
+        TMG_CUDA(cudaGetLastError());
+        coarseUStale = true;
+    }
+
+    template <int P>
+    void inject_coarse_u() {
+        for (int l = L - 1; l >= 1; --l)
+            dev::k_inject_u<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], lv[l + 1]);
+    }
+
+    void materialize_coarse_u() {
+        if (!prob.fast || !coarseUStale) return;
+        if (p == 1) inject_coarse_u<1>();
+        else if (p == 2) inject_coarse_u<2>();
+        else inject_coarse_u<3>();
+        coarseUStale = false;
+    }
+
+    void run_cycle(const Policy& pol, int n, bool timed) {
+        if (prob.fast) {
+            if (p == 1) cycle_fast<1>(pol, n, timed);
+            else if (p == 2) cycle_fast<2>(pol, n, timed);
+            else cycle_fast<3>(pol, n, timed);
+        } else {
+            if (p == 1) cycle_exact<1>(pol, n, timed);
+            else if (p == 2) cycle_exact<2>(pol, n, timed);
+            else cycle_exact<3>(pol, n, timed);
+        }
+    }
+
+    int launches_per_cycle() const {
+        return prob.fast ? (L - 1) + 2 + (L - 1 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1 : 3 * L;
+    }
+
     void check_diag() {
         // jacobi (kernels.cpp:102-106) runs on interior vertices of levels
         // >= ellMin; the interior diagonal is constant per level here.
@@ -889,9 +862,7 @@ struct Hierarchy::Impl {
 
     SweepStats cycle(const Policy& pol, int n, bool timed = false) {
         check_diag();
-        if (p == 1) cycle_exact<1>(pol, n, timed);
-        else if (p == 2) cycle_exact<2>(pol, n, timed);
-        else cycle_exact<3>(pol, n, timed);
+        run_cycle(pol, n, timed);
         TMG_CUDA(cudaMemcpyAsync(hNorm, dNorm, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
         TMG_CUDA(cudaStreamSynchronize(stream));
         SweepStats st;
@@ -937,7 +908,7 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     I.debugR = dbg && dbg[0] == '1';
     I.lv.resize(I.L + 1);
     for (int l = 0; l <= I.L; ++l) I.lv[l] = I.make_level(l, l == I.L);
-    I.normBlocks = I.blocks_for(I.lv[I.L].n);
+    I.normBlocks = std::max(I.blocks_for(I.lv[I.L].n), fast::residual_fine_blocks(I.p, I.lv[I.L], I.smCount));
     I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks));
     I.dNorm = I.alloc<double>(2);
     TMG_CUDA(cudaMallocHost(&I.hNorm, 2 * sizeof(double)));
@@ -1014,9 +985,10 @@ void Hierarchy::get_field(int level, const std::string& field, double* host) con
         }
         return;
     }
+    if (field == "u" && level < I.L) I.materialize_coarse_u();
     double2* ptr = field_ptr(v, field);
     if (!ptr) {
-        if (field == "sf" || field == "si" || field == "sinext" || field == "r") {
+        if (field == "uhat" || field == "chi" || field == "sf" || field == "si" || field == "sinext" || field == "r") {
             std::fill(host, host + 2 * static_cast<size_t>(v.n), 0.0);
             return;
         }
@@ -1125,9 +1097,7 @@ void Hierarchy::time_cycles(const Policy& pol, int n0, int count, bool flushL2, 
     for (int i = 0; i < count; ++i) {
         if (flushL2) dev::k_flush<<<4 * I.smCount, 256, 0, I.stream>>>(I.flushBuf, I.flushN, 0.0);
         TMG_CUDA(cudaEventRecord(I.ev0, I.stream));
-        if (I.p == 1) I.cycle_exact<1>(pol, n0 + i, true);
-        else if (I.p == 2) I.cycle_exact<2>(pol, n0 + i, true);
-        else I.cycle_exact<3>(pol, n0 + i, true);
+        I.run_cycle(pol, n0 + i, true);
         TMG_CUDA(cudaEventRecord(I.ev1, I.stream));
         TMG_CUDA(cudaEventSynchronize(I.ev1));
         float ms = 0.f, fms = 0.f;
@@ -1139,7 +1109,7 @@ void Hierarchy::time_cycles(const Policy& pol, int n0, int count, bool flushL2, 
     out4[0] = totalMs;
     out4[1] = count ? fineMs / count : 0.0;
     out4[2] = 0.0;
-    out4[3] = static_cast<double>(3 * I.L);
+    out4[3] = static_cast<double>(I.launches_per_cycle());
 }
 
 void Hierarchy::e2e_step(const Policy& pol, int n, const double* hostChi, double* out3) {

@@ -1,0 +1,97 @@
+"""Generates the golden fixtures under tests/golden/ from the REFERENCE itself.
+
+Runs the unmodified reference library (oracle/_ref, built from
+/root/reference/proj by oracle/Makefile) through the oracle harness
+(oracle/refdriver.cpp) and records, per configuration:
+  * the per-sweep CSV exactly as the reference runner writes it
+    (runner.cpp:318-329, %.17g),
+  * outcome / sweep count / first and final norm,
+  * FNV-1a hashes of the finest-level u and sc bit patterns (sign of zero
+    folded), which pin the iterates bit-for-bit at any size,
+  * the reference's per-sweep wall time on this host (planning only; the
+    CPU baseline proper is measured on the GPU box by bench.py).
+
+Usage:  python tests/golden/make_goldens.py <name> [<name> ...]
+Names:  see CONFIGS.  Only runnable where /root/reference exists.
+"""
+from __future__ import annotations
+
+import json
+import os
+import platform
+import sys
+import time
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+SEEDED = dict(rhs="seeded", rhs_seed=12345, theta_deg=0, ell_min=1, norm="h")
+
+# BASELINE.json configs (SURVEY §8d mapping) plus the reference's own
+# test_runner / test_capi / cli_smoke runs.
+CONFIGS = {
+    # cfg1: 2D depth 5, k=10 -> phi = k^2(1+0.5i), exponential omega 0.6, 20 cycles
+    "cfg1": dict(problem="helmholtz-sin", dim=2, level=5, phi="100,50", cycle="td-add", omega="exponential",
+                 omega_s=0.6, max_sweeps=20, target_drop=1e-30, **SEEDED),
+    # cfg2: 2D depth 7, k=100, BPX undamped 0.5, to 1e-8 or 200 cycles
+    "cfg2": dict(problem="helmholtz-sin", dim=2, level=7, phi="10000,5000", cycle="td-bpx", omega="undamped",
+                 omega_s=0.5, max_sweeps=200, target_drop=1e-8, **SEEDED),
+    # cfg3: 3D depth 5, k=20, exponential 0.6, 50 cycles (vertex cap raised)
+    "cfg3": dict(problem="helmholtz-sin", dim=3, level=5, phi="400,200", cycle="td-add", omega="exponential",
+                 omega_s=0.6, max_sweeps=50, target_drop=1e-30, max_vertices=40000000, **SEEDED),
+    # cfg3 operator at 81^3 (fast to regenerate; used by the CPU suite's oracle pin)
+    "cfg3_l4": dict(problem="helmholtz-sin", dim=3, level=4, phi="400,200", cycle="td-add", omega="exponential",
+                    omega_s=0.6, max_sweeps=12, target_drop=1e-30, **SEEDED),
+    # cfg2 operator at 243^2
+    "cfg2_l5": dict(problem="helmholtz-sin", dim=2, level=5, phi="10000,5000", cycle="td-bpx", omega="undamped",
+                    omega_s=0.5, max_sweeps=60, target_drop=1e-8, **SEEDED),
+    # a converging seeded 2D case (k=10 undamped)
+    "conv2d": dict(problem="helmholtz-sin", dim=2, level=5, phi="100,50", cycle="td-add", omega="undamped",
+                   omega_s=0.6, max_sweeps=120, target_drop=1e-8, **SEEDED),
+    # cfg4 schedule on a regular grid: hb for 5 sweeps then additive
+    "hb_then_add": dict(problem="helmholtz-sin", dim=3, level=3, phi="1600,800", cycle="td-add",
+                        omega="exponential", omega_s=0.6, max_sweeps=12, target_drop=1e-30, hb_sweeps=5,
+                        rhs_mask="sphere", **SEEDED),
+    # reference tests: cli_smoke (tests/data/poisson_smoke.cfg), test_runner.cpp:472-505, test_capi.cpp:8-28
+    "poisson_smoke": dict(problem="poisson-sin", dim=2, cycle="td-add", omega="exponential", omega_s=0.8,
+                          level=2, max_sweeps=60, target_drop=1e-6, norm="h"),
+    "runner_poisson_l3": dict(problem="poisson-sin", dim=2, level=3, omega="exponential", max_sweeps=80),
+    "runner_helmholtz_diverges": dict(problem="helmholtz-sin", phi="2025", dim=2, level=3, theta_deg=0,
+                                      max_sweeps=300),
+    "runner_budget_one": dict(problem="poisson-sin", dim=2, level=2, max_sweeps=1, target_drop=1e-30),
+    "capi_poisson_l2": dict(problem="poisson-sin", dim=2, level=2, max_sweeps=60),
+    "rotated_3d_bpx": dict(problem="helmholtz-sin", dim=3, level=3, phi="2025", theta_deg=35, cycle="td-bpx",
+                           omega="transition", max_sweeps=15, target_drop=1e-30),
+}
+
+
+def generate(name: str) -> dict:
+    import refdriver as R
+    cfg = CONFIGS[name]
+    t0 = time.time()
+    s = R.RefSession(cfg)
+    if s.status != 0:
+        raise RuntimeError(s.message)
+    build_s = time.time() - t0
+    s.run()
+    L = s.depth
+    secs = s.sweep_seconds()
+    rec = dict(
+        name=name, config={k: str(v) for k, v in cfg.items()}, outcome=s.outcome(), sweeps=s.sweeps(),
+        csv=s.csv(), log=s.log(),
+        u_hash=f"{s.field_hash(L, 'u'):016x}", sc_hash=f"{s.field_hash(L, 'sc'):016x}",
+        coarse_u_hash=f"{s.field_hash(L - 1, 'u'):016x}" if L >= 1 else "",
+        reference_seconds_per_sweep=float(secs.mean()) if len(secs) else 0.0,
+        reference_build_seconds=build_s, host=platform.node(), cpu=platform.processor() or platform.machine(),
+        generator="tests/golden/make_goldens.py via oracle/_ref (unmodified reference sources)",
+    )
+    with open(os.path.join(HERE, f"{name}.json"), "w") as f:
+        json.dump(rec, f, indent=1)
+    return rec
+
+
+if __name__ == "__main__":
+    for n in sys.argv[1:] or [k for k in CONFIGS if k not in ("cfg2", "cfg3")]:
+        r = generate(n)
+        print(n, r["outcome"], r["sweeps"], f"{r['reference_seconds_per_sweep']:.3f}s/sweep", flush=True)
