@@ -39,8 +39,11 @@ extern "C" {
 int treemg_result_history_rows(const treemg_result* res);
 /* row i: sweep, workUnits, vertexCount, maxNorm, euclid, hNorm */
 treemg_status treemg_result_history_row(const treemg_result* res, int i, double* out6);
-/* device time of the cycles of the run in milliseconds (CUDA events on the run's stream) */
+/* wall time of the run's cycle loop in milliseconds */
 double treemg_result_device_ms(const treemg_result* res);
+/* FNV-1a of the final finest-level field ("u" or "sc") bit patterns; needs
+ * config key fingerprint = 1, else 0 */
+unsigned long long treemg_result_fingerprint(const treemg_result* res, const char* which);
 
 /* ---- 2. device hierarchy ------------------------------------------------- */
 typedef struct tmg_hierarchy tmg_hierarchy;
@@ -108,6 +111,10 @@ treemg_status tmg_e2e_step(tmg_hierarchy* h, const tmg_policy* pol, int n, const
                            double* out3);
 
 const char* tmg_last_error(void);
+
+/* Test hook: out = x / y elementwise (interleaved complex, host buffers) on
+ * the device with the kernels' restatement of libgcc __divdc3. */
+treemg_status tmg_test_divdc3(const double* x, const double* y, double* out, long long n);
 
 #ifdef __cplusplus
 }

@@ -52,6 +52,10 @@ def lib():
         L.tmo_set_fine_interior_u.argtypes = [vp, pd]
         L.tmo_omega.argtypes = [ip, dp, dp, ip, ip, ip, ip, pd]
         L.tmo_cdiv.argtypes = [pd, pd, pd, ctypes.c_longlong]
+        L.tmo_csv.restype = cp
+        L.tmo_csv.argtypes = [vp]
+        L.tmo_field_hash.restype = ctypes.c_ulonglong
+        L.tmo_field_hash.argtypes = [vp, ip, cp]
         _lib = L
     return _lib
 
@@ -103,6 +107,12 @@ class OracleSession:
             self.L.tmo_history_row(self.h, i, _pd(buf))
             out[i] = buf
         return out
+
+    def csv(self) -> str:
+        return self.L.tmo_csv(self.h).decode()
+
+    def field_hash(self, level: int, name: str) -> int:
+        return int(self.L.tmo_field_hash(self.h, level, name.encode()))
 
     def field(self, level: int, name: str) -> np.ndarray:
         n = self.L.tmo_lattice_size(self.h, level)

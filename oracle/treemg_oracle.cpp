@@ -28,6 +28,7 @@
 #include <cmath>
 #include <complex>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <numeric>
 #include <sstream>
@@ -710,6 +711,38 @@ int tmo_history_rows(void* h) { return static_cast<int>(static_cast<Session*>(h)
 void tmo_history_row(void* h, int i, double* out) {
     const auto& r = static_cast<Session*>(h)->history.at(static_cast<std::size_t>(i));
     for (int k = 0; k < 6; ++k) out[k] = r[k];
+}
+
+// CSV text exactly as proj/src/runner.cpp:247-251,318-329 writes it (one channel).
+const char* tmo_csv(void* h) {
+    auto* s = static_cast<Session*>(h);
+    static thread_local std::string out;
+    out = "sweep,workUnits,vertexCount,maxNorm,euclid,hNorm\n";
+    char buf[256];
+    for (const auto& r : s->history) {
+        std::snprintf(buf, sizeof buf, "%d,%.17g,%zu,%.17g,%.17g,%.17g\n", static_cast<int>(r[0]), r[1],
+                      static_cast<std::size_t>(r[2]), r[3], r[4], r[5]);
+        out += buf;
+    }
+    return out.c_str();
+}
+
+// FNV-1a over (re+0.0, im+0.0) bit patterns, lattice order (as refdriver.cpp).
+unsigned long long tmo_field_hash(void* h, int level, const char* name) {
+    auto* v = field_ptr(static_cast<Session*>(h)->o, level, name);
+    if (!v) return 0;
+    std::uint64_t hsh = 1469598103934665603ull;
+    for (const Cplx& z : *v) {
+        for (double x : {z.real() + 0.0, z.imag() + 0.0}) {
+            std::uint64_t bits;
+            std::memcpy(&bits, &x, 8);
+            for (int b = 0; b < 8; ++b) {
+                hsh ^= (bits >> (8 * b)) & 0xffu;
+                hsh *= 1099511628211ull;
+            }
+        }
+    }
+    return hsh;
 }
 
 long long tmo_lattice_size(void* h, int level) {

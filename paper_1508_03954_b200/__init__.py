@@ -45,6 +45,7 @@ EXTENSION_SYMBOLS = [
     "tmg_hierarchy_create", "tmg_hierarchy_destroy", "tmg_td_add", "tmg_td_bpx", "tmg_lattice_size",
     "tmg_get_field", "tmg_set_field", "tmg_set_fine_interior_u", "tmg_set_random_initial_guess",
     "tmg_set_fine_rhs", "tmg_field_hash", "tmg_time_cycles", "tmg_e2e_step", "tmg_last_error",
+    "treemg_result_fingerprint", "tmg_test_divdc3",
 ]
 
 _lib = None
@@ -132,6 +133,10 @@ def lib():
         L.tmg_field_hash.argtypes = [vp, ip, cp]
         L.tmg_time_cycles.restype = ip
         L.tmg_time_cycles.argtypes = [vp, ctypes.POINTER(_Policy), ip, ip, ip, pd]
+        L.treemg_result_fingerprint.restype = ctypes.c_ulonglong
+        L.treemg_result_fingerprint.argtypes = [vp, cp]
+        L.tmg_test_divdc3.restype = ip
+        L.tmg_test_divdc3.argtypes = [pd, pd, pd, ctypes.c_longlong]
         L.tmg_e2e_step.restype = ip
         L.tmg_e2e_step.argtypes = [vp, ctypes.POINTER(_Policy), ip, pd, pd]
         _lib = L
@@ -158,6 +163,8 @@ class RunResult:
     final_norm: Dict[str, float]
     history: np.ndarray = field(repr=False)
     device_ms: float = 0.0
+    u_hash: int = 0
+    sc_hash: int = 0
 
 
 def run(cfg: Dict[str, object], out_prefix: Optional[str] = None) -> RunResult:
@@ -185,7 +192,8 @@ def run(cfg: Dict[str, object], out_prefix: Optional[str] = None) -> RunResult:
             work_units=L.treemg_result_work_units(res), vertex_count=L.treemg_result_vertex_count(res),
             first_norm=L.treemg_result_first_norm(res),
             final_norm={w: L.treemg_result_final_norm(res, w.encode(), -1) for w in ("max", "euclid", "h")},
-            history=hist, device_ms=L.treemg_result_device_ms(res))
+            history=hist, device_ms=L.treemg_result_device_ms(res),
+            u_hash=L.treemg_result_fingerprint(res, b"u"), sc_hash=L.treemg_result_fingerprint(res, b"sc"))
     finally:
         L.treemg_result_free(res)
 
@@ -292,6 +300,15 @@ class Hierarchy:
         buf = chi_host.view(np.float64) if chi_host.dtype == np.complex128 else chi_host
         _check(self.L.tmg_e2e_step(self.h, ctypes.byref(pc), n, _pd(buf), _pd(out)))
         return out
+
+
+def device_divide(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """x / y on the device with the kernels' __divdc3 restatement (test hook)."""
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    y = np.ascontiguousarray(y, dtype=np.complex128)
+    out = np.zeros_like(x)
+    _check(lib().tmg_test_divdc3(_pd(x.view(np.float64)), _pd(y.view(np.float64)), _pd(out.view(np.float64)), len(x)))
+    return out
 
 
 def exported_symbols() -> List[str]:

@@ -40,7 +40,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
     cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-           "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-shared",
+           "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-shared", "-Xlinker", "-soname=libtreemg_b200.so",
            "-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + srcs
     # host compiler: the system g++ so libstdc++ is linked dynamically
     if os.path.exists("/usr/bin/g++"):

@@ -162,6 +162,18 @@ treemg_status treemg_result_history_row(const treemg_result* res, int i, double*
 
 double treemg_result_device_ms(const treemg_result* res) { return res->res.deviceMs; }
 
+unsigned long long treemg_result_fingerprint(const treemg_result* res, const char* which) {
+    if (!res || !which) return 0;
+    if (std::strcmp(which, "u") == 0) return res->res.uHash;
+    if (std::strcmp(which, "sc") == 0) return res->res.scHash;
+    return 0;
+}
+
+treemg_status tmg_test_divdc3(const double* x, const double* y, double* out, long long n) {
+    if (!x || !y || !out || n < 0) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { test_divdc3(x, y, out, n); });
+}
+
 treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out) {
     if (!prob || !out) return fail(TREEMG_E_USAGE, "null argument");
     *out = nullptr;

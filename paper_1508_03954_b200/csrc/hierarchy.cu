@@ -436,6 +436,11 @@ __global__ void k_prolong_new(Lvl c, Lvl pr) {
     }
 }
 
+__global__ void k_test_divdc3(const double2* x, const DivConst* k, double2* out, long long n) {
+    for (long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = divdc3(x[i].x, x[i].y, k[i]);
+}
+
 __global__ void k_flush(double4* buf, size_t n, double v) {
     for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         buf[i] = make_double4(v, v, v, v);
@@ -1082,6 +1087,24 @@ std::uint64_t Hierarchy::field_hash(int level, const std::string& field) const {
         }
     }
     return h;
+}
+
+void test_divdc3(const double* x, const double* y, double* out, long long n) {
+    std::vector<dev::DivConst> k(static_cast<size_t>(n));
+    for (long long i = 0; i < n; ++i) k[static_cast<size_t>(i)] = div_const(Cplx(y[2 * i], y[2 * i + 1]));
+    double2 *dx = nullptr, *dout = nullptr;
+    dev::DivConst* dk = nullptr;
+    TMG_CUDA(cudaMalloc(&dx, n * sizeof(double2)));
+    TMG_CUDA(cudaMalloc(&dout, n * sizeof(double2)));
+    TMG_CUDA(cudaMalloc(&dk, n * sizeof(dev::DivConst)));
+    TMG_CUDA(cudaMemcpy(dx, x, n * sizeof(double2), cudaMemcpyHostToDevice));
+    TMG_CUDA(cudaMemcpy(dk, k.data(), n * sizeof(dev::DivConst), cudaMemcpyHostToDevice));
+    dev::k_test_divdc3<<<64, 256>>>(dx, dk, dout, n);
+    TMG_CUDA(cudaGetLastError());
+    TMG_CUDA(cudaMemcpy(out, dout, n * sizeof(double2), cudaMemcpyDeviceToHost));
+    cudaFree(dx);
+    cudaFree(dout);
+    cudaFree(dk);
 }
 
 void Hierarchy::unfold() { throw UnsupportedConfigError("FMG unfolding is not implemented yet"); }

@@ -109,4 +109,8 @@ class Hierarchy {
     std::unique_ptr<Impl> impl_;
 };
 
+// Test hook: x / y elementwise on the device with the kernels' __divdc3
+// restatement (per-element divisor constants); host buffers.
+void test_divdc3(const double* x, const double* y, double* out, long long n);
+
 }  // namespace tmg
