@@ -24,6 +24,11 @@
  *   hb_sweeps = <k>             hierarchical-basis mask for sweeps 1..k, then off
  *   fmg_from = <level>          FMG unfolding from <level> up to `level`
  *   fmg_stage_cap = <n>         sweeps per FMG stage (default max_sweeps)
+ *   norms = device | host       host (exact precision only): |r| downloaded and
+ *                               summed on the host in the reference's traversal
+ *                               order, so CSV/log bytes match the reference
+ *   fingerprint = 0 | 1         hash the final fine u / sc (treemg_result_fingerprint)
+ *   device = <ordinal>          CUDA device
  */
 
 #ifndef TREEMG_B200_H

@@ -865,6 +865,60 @@ struct Hierarchy::Impl {
                 throw SingularDiagonalError("vanishing operator diagonal (phi*h^2 resonance?)");
     }
 
+    // Morton (DFS) order of the interior fine vertices = their touch-last order
+    // (exact_ops.cuh rule (2)); the reference sums norms in this order.
+    std::vector<unsigned> finishOrder;
+
+    void build_finish_order() {
+        const dev::Lvl& F = lv[L];
+        std::vector<std::pair<unsigned long long, unsigned>> keys;
+        for (unsigned f = 0; f < F.n; ++f) {
+            unsigned ff = f;
+            int idx[3];
+            bool interior = true;
+            for (int d = 0; d < p; ++d) {
+                idx[d] = static_cast<int>(ff % F.n1);
+                ff /= F.n1;
+                interior &= idx[d] > 0 && idx[d] < static_cast<int>(F.m);
+            }
+            if (!interior) continue;
+            unsigned long long key = 0;
+            for (int k = L - 1; k >= 0; --k) {
+                int slot = 0, mul = 1;
+                for (int d = 0; d < p; ++d) {
+                    slot += ((idx[d] / pow3i(k)) % 3) * mul;
+                    mul *= 3;
+                }
+                key = key * static_cast<unsigned long long>(pow3i(p)) + static_cast<unsigned long long>(slot);
+            }
+            keys.emplace_back(key, f);
+        }
+        std::sort(keys.begin(), keys.end());
+        finishOrder.resize(keys.size());
+        for (size_t i = 0; i < keys.size(); ++i) finishOrder[i] = keys[i].second;
+    }
+
+    // proj/src/cycles.cpp:248-258 + 94-97 on the host, bit-for-bit.
+    void host_norms(SweepStats& st) {
+        if (finishOrder.empty()) build_finish_order();
+        const dev::Lvl& F = lv[L];
+        std::vector<Cplx> r(F.n);
+        TMG_CUDA(cudaMemcpyAsync(r.data(), F.r, static_cast<size_t>(F.n) * sizeof(double2), cudaMemcpyDeviceToHost,
+                                 stream));
+        TMG_CUDA(cudaStreamSynchronize(stream));
+        const double hp = std::pow(std::pow(3.0, -L), p);
+        double mx = 0.0, eu = 0.0, hn = 0.0;
+        for (unsigned f : finishOrder) {
+            const double m = std::abs(r[f]);
+            mx = std::max(mx, m);
+            eu += m * m;
+            hn += hp * m * m;
+        }
+        st.maxNorm = mx;
+        st.euclidNorm = std::sqrt(eu);
+        st.hNorm = std::sqrt(hn);
+    }
+
     SweepStats cycle(const Policy& pol, int n, bool timed = false) {
         check_diag();
         run_cycle(pol, n, timed);
@@ -878,6 +932,7 @@ struct Hierarchy::Impl {
         long long inner = 1;
         for (int d = 0; d < p; ++d) inner *= pow3i(L) - 1;
         st.updatedFineVertices = inner;
+        if (prob.hostNorms && !prob.fast) host_norms(st);
         return st;
     }
 };
@@ -910,7 +965,7 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     TMG_CUDA(cudaEventCreate(&I.evf0));
     TMG_CUDA(cudaEventCreate(&I.evf1));
     const char* dbg = std::getenv("TMG_DEBUG_R");
-    I.debugR = dbg && dbg[0] == '1';
+    I.debugR = (dbg && dbg[0] == '1') || (prob.hostNorms && !prob.fast);
     I.lv.resize(I.L + 1);
     for (int l = 0; l <= I.L; ++l) I.lv[l] = I.make_level(l, l == I.L);
     I.normBlocks = std::max(I.blocks_for(I.lv[I.L].n), fast::residual_fine_blocks(I.p, I.lv[I.L], I.smCount));

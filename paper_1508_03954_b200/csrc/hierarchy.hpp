@@ -60,6 +60,7 @@ struct Problem {
     bool rhsSphere = false;
     int rhsLattice = -1;  // level the seeded rhs is keyed on (-1: levels)
     bool fast = false;    // precision = fast
+    bool hostNorms = false;  // norms = host: reference-order sums of |r| on the host (exact mode)
     std::size_t maxVertices = 8u * 1024u * 1024u;
     int device = 0;
 };

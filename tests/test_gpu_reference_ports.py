@@ -207,6 +207,6 @@ def test_reference_cli_runs_on_the_b200_library(tmg, tmp_path):
     if not os.path.exists(exe):
         pytest.skip("solve_b200 not built (needs the reference sources at build time)")
     out = subprocess.run([exe, os.path.join(ROOT, "tests", "data", "poisson_smoke.cfg"), "--out",
-                          str(tmp_path / "smoke")], capture_output=True, text=True)
+                          str(tmp_path / "smoke"), "--norms", "host"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert (tmp_path / "smoke.csv").read_text() == load_golden("poisson_smoke")["csv"]
