@@ -1,0 +1,74 @@
+// Fused fine pass for 3D, precision = fast (K2F in DESIGN.md §3).
+//
+// One kernel does, per fine vertex, everything the cycle needs on the finest
+// level: the top-down correction u += sc + P sc_{L-1} (- P si_{L-1}, BPX),
+// the residual r = b - H u of the corrected iterate, the norm partials, the
+// Jacobi staging sc = omega r / diag, the BPX injection into si_{L-1} and
+// the restriction R r into the coarse residual.  HBM traffic is the
+// algorithmic minimum of SURVEY §8d: u, sc, b read once, u, sc written once
+// (80 B per fine vertex); u and sc are double-buffered so halo reads never
+// race with the owner's writes.
+//
+// Structure: 2D tiles (32 x 12 columns) marching in z over a chunk of planes.
+// The halo'd (34 x 14) u_old / sc_old planes arrive by TMA
+// (cp.async.bulk.tensor.3d) into a 4-stage mbarrier ring; the block forms
+// the corrected plane in shared memory, every column keeps its centre /
+// edge / corner plane sums in registers (z-marching), and the restriction is
+// evaluated separably (x, then y, then z accumulators) into per-tile partial
+// sums that a small combine kernel adds in a fixed order, so the coarse
+// residual is deterministic without atomics.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "fast.cuh"
+#include "lattice.cuh"
+
+namespace tmg {
+namespace fused3 {
+
+constexpr int TX = 32, TY = 12, STAGES = 3;
+constexpr int HX = TX + 2, HY = TY + 2;
+constexpr int SX = TX / 3 + 3, SY = TY / 3 + 3;  // restriction slots per tile (upper bounds)
+constexpr int CX = (TX + 1) / 3 + 2, CY = (TY + 1) / 3 + 2;  // coarse tile feeding the prolongation
+
+struct Geometry {
+    int m;      // fine cells per axis (3^L)
+    int mc;     // coarse cells per axis
+    int nbx, nby, nbz;
+    int zc;     // planes per z-chunk (multiple of 3)
+    int sz;     // z slots per chunk
+};
+
+struct Args {
+    double2* uNew;
+    double2* scNew;
+    const double2* b;
+    const double2* scC;   // coarse sc (after the coarse top-down)
+    const double2* siC;   // coarse si (BPX)
+    double2* sinextC;     // coarse si next (BPX injection)
+    double2* partial;     // restriction partials
+    double* norms;        // 2 doubles per block
+    unsigned n1, n1c;
+    Geometry g;
+    fast::LevelCoef k;
+    int bpx, hb, ellMin, level;
+};
+
+Geometry geometry(int m, int mc);
+size_t partial_count(const Geometry& g);
+size_t smem_bytes();
+int blocks(const Geometry& g);
+
+// TMA descriptor for one lattice array (double2 viewed as float64 pairs).
+// kind 0: fine u / sc halo'd tile, 1: fine b tile, 2: two coarse planes.
+bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind);
+
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapB,
+            const CUtensorMap& mapC, const CUtensorMap& mapI, cudaStream_t s);
+// r_{L-1}(W) = sum of the tile partials covering W, fixed order.
+void combine(const Args& a, double2* rCoarse, int blocks, cudaStream_t s);
+
+}  // namespace fused3
+}  // namespace tmg

@@ -22,6 +22,7 @@
 
 #include "exact_ops.cuh"
 #include "fast.cuh"
+#include "fused3.cuh"
 #include "hierarchy.hpp"
 #include "lattice.cuh"
 
@@ -568,6 +569,14 @@ struct Hierarchy::Impl {
     float lastFineMs = 0.f, lastTdMs = 0.f;
     bool timeFine = false;
     bool coarseUStale = false;
+    // fused 3D fine pass (fast precision): double-buffered fine u / sc
+    bool fused = false;
+    double2* uAlt = nullptr;
+    double2* scAlt = nullptr;
+    CUtensorMap mapU[2], mapS[2];  // [0]: current buffers, [1]: alternates
+    CUtensorMap mapB, mapC, mapI;
+    fused3::Geometry geo{};
+    double2* partial3 = nullptr;
 
     ~Impl() {
         for (void* ptr : allocations) cudaFree(ptr);
@@ -800,9 +809,6 @@ struct Hierarchy::Impl {
     template <int P>
     void cycle_fast(const Policy& pol, int n, bool timed) {
         const int bpx = pol.bpx ? 1 : 0;
-        for (int l = 1; l < L; ++l) fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
-        if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
-        fast::correct_fine(P, lv[L], lv[L - 1], bpx, blocks_for(lv[L].n), stream);
         auto args = [&](int l) {
             fast::ResArgs a{};
             a.lv = lv[l];
@@ -816,6 +822,47 @@ struct Hierarchy::Impl {
             a.partials = partials;
             return a;
         };
+        for (int l = 1; l < L; ++l) fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+        if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
+        if (P == 3 && fused) {
+            fused3::Args fa{};
+            dev::Lvl& F = lv[L];
+            fa.uNew = uAlt;
+            fa.scNew = scAlt;
+            fa.b = F.chi;
+            fa.scC = lv[L - 1].sc;
+            fa.siC = lv[L - 1].si;
+            fa.sinextC = lv[L - 1].sinext;
+            fa.partial = partial3;
+            fa.norms = partials;
+            fa.n1 = F.n1;
+            fa.n1c = lv[L - 1].n1;
+            fa.g = geo;
+            fa.k = fc[L];
+            const Cplx w = omega_unmasked(pol, 0, n);
+            fa.k.wRaw = make_double2(w.real(), w.imag());
+            fa.bpx = bpx;
+            fa.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+            fa.ellMin = prob.ellMin;
+            fa.level = L;
+            fused3::launch(fa, mapU[0], mapS[0], mapB, mapC, mapI, stream);
+            if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+            fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream);
+            std::swap(F.u, uAlt);
+            std::swap(F.sc, scAlt);
+            std::swap(mapU[0], mapU[1]);
+            std::swap(mapS[0], mapS[1]);
+            for (int l = L - 1; l >= 1; --l) {
+                if (l < L - 1 && l >= prob.ellMin)
+                    fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
+                fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+            }
+            dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused3::blocks(geo), dNorm);
+            TMG_CUDA(cudaGetLastError());
+            coarseUStale = true;
+            return;
+        }
+        fast::correct_fine(P, lv[L], lv[L - 1], bpx, blocks_for(lv[L].n), stream);
         const int nb = fast::residual_fine(P, args(L), smCount, stream);
         if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
         for (int l = L - 1; l >= 1; --l) {
@@ -854,6 +901,7 @@ struct Hierarchy::Impl {
     }
 
     int launches_per_cycle() const {
+        if (prob.fast && fused) return (L - 1) + 2 + std::max(0, L - 2 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1;
         return prob.fast ? (L - 1) + 2 + (L - 1 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1 : 3 * L;
     }
 
@@ -969,12 +1017,32 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     I.lv.resize(I.L + 1);
     for (int l = 0; l <= I.L; ++l) I.lv[l] = I.make_level(l, l == I.L);
     I.normBlocks = std::max(I.blocks_for(I.lv[I.L].n), fast::residual_fine_blocks(I.p, I.lv[I.L], I.smCount));
+    if (prob.fast && I.p == 3 && I.L >= 2)
+        I.normBlocks = std::max(I.normBlocks, fused3::blocks(fused3::geometry(static_cast<int>(I.lv[I.L].m),
+                                                                              static_cast<int>(I.lv[I.L - 1].m))));
     I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks));
     I.dNorm = I.alloc<double>(2);
     TMG_CUDA(cudaMallocHost(&I.hNorm, 2 * sizeof(double)));
     I.chiNodal = I.alloc<double2>(I.lv[I.L].n);
     I.compute_level_constants();
     I.build_restrict_tables();
+    {
+        const char* fz = std::getenv("TMG_FUSED");
+        if (prob.fast && I.p == 3 && I.L >= 2 && fz && fz[0] == '1') {
+            const dev::Lvl& F = I.lv[I.L];
+            I.uAlt = I.alloc<double2>(F.n);
+            I.scAlt = I.alloc<double2>(F.n);
+            I.geo = fused3::geometry(static_cast<int>(F.m), static_cast<int>(I.lv[I.L - 1].m));
+            I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
+            const dev::Lvl& C = I.lv[I.L - 1];
+            bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0) && fused3::encode_map(&I.mapS[0], F.sc, F.n1, 0) &&
+                      fused3::encode_map(&I.mapU[1], I.uAlt, F.n1, 0) &&
+                      fused3::encode_map(&I.mapS[1], I.scAlt, F.n1, 0) && fused3::encode_map(&I.mapB, F.chi, F.n1, 1) &&
+                      fused3::encode_map(&I.mapC, C.sc, C.n1, 2) && fused3::encode_map(&I.mapI, C.si, C.n1, 2);
+            if (!ok) throw CudaError("cuTensorMapEncodeTiled failed for the fused fine pass");
+            I.fused = true;
+        }
+    }
     if (prob.chi == ChiKind::Seeded) {
         if (I.p == 1) I.build_rhs_seeded<1>();
         else if (I.p == 2) I.build_rhs_seeded<2>();
