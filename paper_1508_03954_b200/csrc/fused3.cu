@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 namespace tmg {
 namespace fused3 {
@@ -45,6 +46,10 @@ __device__ __forceinline__ double2 prolong3(const double2* __restrict__ src, uns
     const double2 c = lerp(ld(p + sz), ld(p + sz + 1), rx);
     const double2 d = lerp(ld(p + sz + sy), ld(p + sz + sy + 1), rx);
     return lerp(lerp(a, b, ry), lerp(c, d, ry), rz);
+}
+
+__device__ __forceinline__ double2 lerpw(double2 c0, double2 c1, double w1) {
+    return make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
 }
 
 __device__ __forceinline__ double2 stage_sc(double2 smooth, double2 w, bool cp, int bpx, int hb) {
@@ -88,28 +93,25 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
 
 constexpr int kPlane = (HX * HY + 7) / 8 * 8;  // stage strides: TMA destinations are 128-byte aligned
 constexpr unsigned kTileBytes = HX * HY * sizeof(double2);
-constexpr int kB = TX * TY;                      // b tile (no halo)
-constexpr unsigned kBBytes = kB * sizeof(double2);
-constexpr int kC = (CX * CY * 2 + 7) / 8 * 8;     // two coarse planes
+constexpr int kC = (CX * CY * 2 + 7) / 8 * 8;     // two coarse planes (box {2*CX, CY, 2})
 constexpr unsigned kCBytes = CX * CY * 2 * sizeof(double2);
+constexpr int kV = (HY * CX + 7) / 8 * 8;         // z- and y-interpolated coarse rows
+constexpr int NT = TX * TY;
 
-__device__ __forceinline__ double2 shfl2(double2 v, int src) {
-    return make_double2(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
-}
+template <bool BPX>
+__host__ __device__ constexpr int stage_elems() { return 2 * kPlane + (BPX ? 2 : 1) * kC; }
 
-__global__ void __launch_bounds__(TX* TY, 2)
+template <bool BPX>
+__global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
     k_fused3(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapS,
-             const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapC,
-             const __grid_constant__ CUtensorMap mapI, const Args a) {
+             const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
-    double2* bufU = reinterpret_cast<double2*>(smem);
-    double2* bufS = bufU + STAGES * kPlane;
-    double2* bufB = bufS + STAGES * kPlane;
-    double2* bufC = bufB + STAGES * kB;
-    double2* bufI = bufC + STAGES * kC;             // BPX si planes (only when a.bpx)
-    double2* plane = bufI + STAGES * kC;
-    double2* xs = plane + 2 * kPlane;               // [TY][SX] x-restricted rows
-    uint64_t* bar = reinterpret_cast<uint64_t*>(xs + TY * SX);
+    constexpr int SE = stage_elems<BPX>();
+    double2* ring = reinterpret_cast<double2*>(smem);          // STAGES x {U, S, C[, I]}
+    double2* Vb = ring + STAGES * SE;                           // [2][kV] (+[2][kV] si)
+    double2* Pb = Vb + (BPX ? 4 : 2) * kV;                      // [2][kPlane] corrected planes
+    double2* tb = Pb + 2 * kPlane;                              // [TY][TX] z-restricted columns
+    uint64_t* bar = reinterpret_cast<uint64_t*>(tb + NT);
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int m = a.g.m, mc = a.g.mc;
@@ -118,16 +120,16 @@ __global__ void __launch_bounds__(TX* TY, 2)
     const int nplanes = z1 - z0 + 2;
     const long long sy = a.n1, sz = static_cast<long long>(a.n1) * a.n1;
     const int cx0 = (x0 - 1) / 3, cy0 = (y0 - 1) / 3;
-    const unsigned stageBytes = 2 * kTileBytes + kBBytes + kCBytes * (a.bpx ? 2u : 1u);
+    constexpr unsigned stageBytes = 2 * kTileBytes + (BPX ? 2 : 1) * kCBytes;
 
     auto issue = [&](int stage, int zz) {
+        double2* st = ring + stage * SE;
         const int cz = min(zz / 3, mc - 1);
         mbar_expect_tx(&bar[stage], stageBytes);
-        tma_load3(bufU + stage * kPlane, &mapU, 2 * (x0 - 1), y0 - 1, zz, &bar[stage]);
-        tma_load3(bufS + stage * kPlane, &mapS, 2 * (x0 - 1), y0 - 1, zz, &bar[stage]);
-        tma_load3(bufB + stage * kB, &mapB, 2 * x0, y0, zz, &bar[stage]);
-        tma_load3(bufC + stage * kC, &mapC, 2 * cx0, cy0, cz, &bar[stage]);
-        if (a.bpx) tma_load3(bufI + stage * kC, &mapI, 2 * cx0, cy0, cz, &bar[stage]);
+        tma_load3(st, &mapU, 2 * (x0 - 1), y0 - 1, zz, &bar[stage]);
+        tma_load3(st + kPlane, &mapS, 2 * (x0 - 1), y0 - 1, zz, &bar[stage]);
+        tma_load3(st + 2 * kPlane, &mapC, 2 * cx0, cy0, cz, &bar[stage]);
+        if (BPX) tma_load3(st + 2 * kPlane + kC, &mapI, 2 * cx0, cy0, cz, &bar[stage]);
     };
 
     if (tid == 0) {
@@ -138,13 +140,72 @@ __global__ void __launch_bounds__(TX* TY, 2)
     if (tid == 0)
         for (int s = 0; s < STAGES && s < nplanes; ++s) issue(s, z0 - 1 + s);
 
+    // ---- per-thread constants ----
+    // Phase B: every thread corrects its own column's point; threads [0, RING)
+    // also one halo-ring point, threads [RING, RING + HY*CX) one row of the
+    // z/y-interpolated coarse plane of the next fine plane.
+    constexpr int RING = 2 * HX + 2 * TY;
     const int x = x0 + tx, y = y0 + ty;
-    const bool owned = x < xe && y < ye;
+    const bool owned = x < xe && y < ye;  // == own point inside [1, m-1]^2
     const bool cpxy = (x % 3 == 0) && (y % 3 == 0);
-    double2 Cm = zero2(), Em = zero2(), Km = zero2(), C0 = zero2(), E0 = zero2(), K0 = zero2();
-    double nmax = 0.0, nsum = 0.0;
+    const int po = (ty + 1) * HX + (tx + 1);
+    int vo;
+    double wxo;
+    {
+        const int qx = min(x / 3, mc - 1);
+        vo = (ty + 1) * CX + (qx - cx0);
+        const int rx = x - 3 * qx;
+        wxo = rx == 1 ? (1.0 / 3.0) : rx == 2 ? (2.0 / 3.0) : (rx == 3 ? 1.0 : 0.0);
+    }
+    const int task = tid < RING ? 1 : (tid < RING + HY * CX ? 2 : 0);  // warp-uniform except one warp
+    int pr = 0, vr = 0;
+    double wxr = 0.0;
+    bool pinr = false, cpr = false;
+    int vcOff = 0;
+    double w1y = 0.0;
+    const int vt = tid - RING;
+    if (task == 1) {
+        const int k = tid;
+        int lx, ly;
+        if (k < HX) { lx = k; ly = 0; }
+        else if (k < 2 * HX) { lx = k - HX; ly = HY - 1; }
+        else if (k < 2 * HX + TY) { lx = 0; ly = 1 + (k - 2 * HX); }
+        else { lx = HX - 1; ly = 1 + (k - 2 * HX - TY); }
+        const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+        pinr = gx >= 1 && gx <= m - 1 && gy >= 1 && gy <= m - 1;
+        const int qx = min(max(gx, 0) / 3, mc - 1);
+        const int rx = gx - 3 * qx;
+        pr = ly * HX + lx;
+        vr = ly * CX + (qx - cx0);
+        wxr = rx == 1 ? (1.0 / 3.0) : rx == 2 ? (2.0 / 3.0) : (rx == 3 ? 1.0 : 0.0);
+        cpr = (gx % 3 == 0) && (gy % 3 == 0);
+    } else if (task == 2) {
+        const int ly = vt / CX, ci = vt % CX;
+        const int gy = y0 - 1 + ly;
+        const int qy = min(max(gy, 0) / 3, mc - 1);
+        const int ry = gy - 3 * qy;
+        vcOff = (qy - cy0) * CX + ci;
+        w1y = ry == 1 ? (1.0 / 3.0) : ry == 2 ? (2.0 / 3.0) : (ry == 3 ? 1.0 : 0.0);
+    }
+    auto computeV = [&](int stage, int zz, int vb) {
+        const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
+        const double w1z = rz == 1 ? (1.0 / 3.0) : rz == 2 ? (2.0 / 3.0) : (rz == 3 ? 1.0 : 0.0);
+        const double2* C = ring + stage * SE + 2 * kPlane;
+        const double2 a0 = lerpw(C[vcOff], C[vcOff + CX], w1y);
+        const double2 a1 = lerpw(C[vcOff + CX * CY], C[vcOff + CX * CY + CX], w1y);
+        Vb[vb * kV + vt] = lerpw(a0, a1, w1z);
+        if (BPX) {
+            const double2* I = C + kC;
+            const double2 b0 = lerpw(I[vcOff], I[vcOff + CX], w1y);
+            const double2 b1 = lerpw(I[vcOff + CX * CY], I[vcOff + CX * CY + CX], w1y);
+            Vb[(2 + vb) * kV + vt] = lerpw(b0, b1, w1z);
+        }
+    };
 
-    // restriction slots of this tile
+    double nmax = 0.0, nsum = 0.0;
+    double2 accLo = zero2(), accHi = zero2();
+
+    // restriction slots of this tile (xy); z handled by the column accumulators
     const int Xa = x0 / 3, Xb = (xe + 1) / 3, Ya = y0 / 3, Yb = (ye + 1) / 3;
     const int nsx = Xb - Xa + 1, nsy = Yb - Ya + 1;
     const long long blockLin =
@@ -152,129 +213,152 @@ __global__ void __launch_bounds__(TX* TY, 2)
     double2* part = a.partial + blockLin * static_cast<long long>(a.g.sz * SY * SX);
     const int zBase = (z0 - 1) / 3;
     int zLow = zBase;
-    double2 accLo = zero2(), accHi = zero2();
     const bool slotThread = tid < nsx * nsy;
     const int sxi = slotThread ? tid % nsx : 0, syi = slotThread ? tid / nsx : 0;
-
-    for (int it = 0; it < nplanes; ++it) {
-        const int zz = z0 - 1 + it;
-        const int s = it % STAGES;
-        mbar_wait(&bar[s], static_cast<unsigned>((it / STAGES) & 1));
-        double2* P = plane + (it & 1) * kPlane;
-        {
-            const double2* U = bufU + s * kPlane;
-            const double2* Sc = bufS + s * kPlane;
-            const double2* Cc = bufC + s * kC;
-            const double2* Ci = bufI + s * kC;
-            const bool zin = zz >= 1 && zz <= m - 1;
-            const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
-            for (int p = tid; p < HX * HY; p += TX * TY) {
-                const int lx = p % HX, ly = p / HX;
-                const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
-                double2 v = zero2();
-                if (zin && gx >= 1 && gx <= m - 1 && gy >= 1 && gy <= m - 1) {
-                    const int qx = min(gx / 3, mc - 1), qy = min(gy / 3, mc - 1);
-                    const int rx = gx - 3 * qx, ry = gy - 3 * qy;
-                    const int o = (qx - cx0) + CX * (qy - cy0);
-                    auto tri = [&](const double2* C) {
-                        const double2 a0 = lerp(C[o], C[o + 1], rx), a1 = lerp(C[o + CX], C[o + CX + 1], rx);
-                        const double2 b0 = lerp(C[o + CX * CY], C[o + CX * CY + 1], rx);
-                        const double2 b1 = lerp(C[o + CX * CY + CX], C[o + CX * CY + CX + 1], rx);
-                        return lerp(lerp(a0, a1, ry), lerp(b0, b1, ry), rz);
-                    };
-                    double2 scv = add(Sc[p], tri(Cc));
-                    if (a.bpx && !((gx % 3 == 0) && (gy % 3 == 0) && (zz % 3 == 0))) scv = sub(scv, tri(Ci));
-                    v = add(U[p], scv);
+    auto flushSlots = [&](int zi) {
+        __syncthreads();
+        if (slotThread) {
+            const int X = Xa + sxi, Y = Ya + syi;
+            double2 acc = zero2();
+#pragma unroll
+            for (int ky = -2; ky <= 2; ++ky) {
+                const int fy = 3 * Y + ky;
+                if (fy < y0 || fy >= ye) continue;
+                const double wy = ky == 0 ? 1.0 : (ky == 1 || ky == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
+                double2 row = zero2();
+#pragma unroll
+                for (int kx = -2; kx <= 2; ++kx) {
+                    const int fx = 3 * X + kx;
+                    if (fx < x0 || fx >= xe) continue;
+                    const double wx = kx == 0 ? 1.0 : (kx == 1 || kx == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
+                    row = axpy(wx, tb[(fy - y0) * TX + (fx - x0)], row);
                 }
-                P[p] = v;
+                acc = axpy(wy, row, acc);
             }
+            part[(zi * SY + syi) * SX + sxi] = acc;
+        }
+    };
+
+    const long long colBase = x + y * sy;
+    const double2* bPtr = a.b + colBase + static_cast<long long>(z0) * sz;
+    double2* uPtr = a.uNew + colBase + static_cast<long long>(z0) * sz;
+    double2* sPtr = a.scNew + colBase + static_cast<long long>(z0) * sz;
+    double2* siPtr = a.sinextC + (x / 3) + a.n1c * (static_cast<long long>(y / 3) + static_cast<long long>(a.n1c) * ((z0 + 2) / 3));
+    double2 bq0 = (owned && z0 < z1) ? ld(bPtr) : zero2();
+    const bool zeroSc = a.level < a.ellMin;
+    const bool injectOK = BPX && a.level > a.ellMin && cpxy && owned;
+    const double2 k0 = a.k.c[0], k1 = a.k.c[1], k2 = a.k.c[2], k3 = a.k.c[3];
+
+    mbar_wait(&bar[0], 0);
+    if (task == 2) computeV(0, z0 - 1, 0);
+    __syncthreads();
+
+    // running stencil accumulators: Aprev = H u at plane p-1 minus its plane-p terms, Acur = plane p's so far
+    double2 Aprev = zero2(), Acur = zero2();
+    int stage = 0;
+    unsigned parity = 0;
+
+    auto step = [&](int it, auto U3) {
+        constexpr int u = decltype(U3)::value;  // zz % 3 == u
+        const int zz = z0 - 1 + it;
+        const bool hasNext = it + 1 < nplanes;
+        const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
+        const unsigned nparity = stage + 1 == STAGES ? parity ^ 1u : parity;
+        mbar_wait(&bar[stage], parity);
+        if (hasNext) mbar_wait(&bar[nstage], nparity);
+        const bool zin = zz >= 1 && zz <= m - 1;
+        const double2* Ut = ring + stage * SE;
+        const double2* Sc = Ut + kPlane;
+        const double2* V = Vb + (it & 1) * kV;
+        double2* P = Pb + (it & 1) * kPlane;
+        // ---- phase B ----
+        double2 cOwn;
+        {
+            double2 scv = add(Sc[po], lerpw(V[vo], V[vo + 1], wxo));
+            if (BPX && !(cpxy && u == 0)) {
+                const double2* Vi = Vb + (2 + (it & 1)) * kV;
+                scv = sub(scv, lerpw(Vi[vo], Vi[vo + 1], wxo));
+            }
+            cOwn = (zin && owned) ? add(Ut[po], scv) : zero2();
+            P[po] = cOwn;
+        }
+        if (task == 1) {
+            double2 scv = add(Sc[pr], lerpw(V[vr], V[vr + 1], wxr));
+            if (BPX && !(cpr && u == 0)) {
+                const double2* Vi = Vb + (2 + (it & 1)) * kV;
+                scv = sub(scv, lerpw(Vi[vr], Vi[vr + 1], wxr));
+            }
+            P[pr] = (zin && pinr) ? add(Ut[pr], scv) : zero2();
+        } else if (task == 2 && hasNext) {
+            computeV(nstage, zz + 1, (it + 1) & 1);
         }
         __syncthreads();
-        double2 Cp = zero2(), Ep = zero2(), Kp = zero2();
-        if (owned) {
-            const double2* c = P + (ty + 1) * HX + (tx + 1);
-            Cp = c[0];
-            Ep = add(add(c[-1], c[1]), add(c[-HX], c[HX]));
-            Kp = add(add(c[-1 - HX], c[1 - HX]), add(c[-1 + HX], c[1 + HX]));
-            if (zz >= z0 && zz < z1) a.uNew[x + y * sy + zz * sz] = Cp;
-        }
+        if (tid == 0 && it + STAGES < nplanes) issue(stage, zz + STAGES);
+        stage = nstage;
+        parity = nparity;
+        // ---- phase C ----
+        const double2* c = P + po;
+        const double2 E = add(add(c[-1], c[1]), add(c[-HX], c[HX]));
+        const double2 K = add(add(c[-1 - HX], c[1 - HX]), add(c[-1 + HX], c[1 + HX]));
+        double2 T = mul(k1, cOwn);
+        T = mac(T, k2, E);
+        T = mac(T, k3, K);
+        double2 Uo = mul(k0, cOwn);
+        Uo = mac(Uo, k1, E);
+        Uo = mac(Uo, k2, K);
+        if (owned && zz >= z0 && zz < z1) *uPtr = cOwn;
+        if (zz >= z0) uPtr += sz;
         if (it >= 2) {
-            const int z = zz - 1;
-            const int sb = (it - 1) % STAGES;
-            double2 r = zero2();
-            if (owned) {
-                const double2 faces = add(E0, add(Cm, Cp));
-                const double2 edges = add(K0, add(Em, Ep));
-                const double2 corners = add(Km, Kp);
-                double2 hu = mul(a.k.c[0], C0);
-                hu = mac(hu, a.k.c[1], faces);
-                hu = mac(hu, a.k.c[2], edges);
-                hu = mac(hu, a.k.c[3], corners);
-                r = sub(bufB[sb * kB + ty * TX + tx], hu);
-                const double m2 = fma(r.x, r.x, r.y * r.y);
-                nmax = fmax(nmax, m2);
-                nsum += m2;
-                const bool cp = cpxy && (z % 3 == 0);
-                const double2 smooth = mul(r, a.k.invDiag);
-                const long long f = x + y * sy + z * sz;
-                a.scNew[f] = a.level < a.ellMin ? zero2() : stage_sc(smooth, a.k.wRaw, cp, a.bpx, a.hb);
-                if (a.bpx && cp && a.level > a.ellMin)
-                    a.sinextC[(x / 3) + a.n1c * (static_cast<long long>(y / 3) + static_cast<long long>(a.n1c) * (z / 3))] =
-                        mul(a.k.wRaw, smooth);
+            constexpr int kz = (u + 2) % 3;  // plane z = zz - 1
+            const double2 hu = add(Aprev, T);
+            const double2 r = owned ? sub(bq0, hu) : zero2();
+            bPtr += sz;
+            if (owned && zz < z1) bq0 = ld(bPtr);
+            const double m2 = fma(r.x, r.x, r.y * r.y);
+            nmax = fmax(nmax, m2);
+            nsum += m2;
+            const double2 smooth = mul(r, a.k.invDiag);
+            if (owned) *sPtr = zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpxy && kz == 0, BPX ? 1 : 0, a.hb);
+            sPtr += sz;
+            if (BPX && kz == 0 && injectOK) {
+                *siPtr = mul(a.k.wRaw, smooth);
+                siPtr += static_cast<long long>(a.n1c) * a.n1c;
             }
-            // restriction, x direction, inside the row's warp (lane j -> slot X = Xa + j)
-            {
-                const int X = Xa + tx;
-                double2 acc = zero2();
-#pragma unroll
-                for (int k = -2; k <= 2; ++k) {
-                    const int lane = 3 * X + k - x0;
-                    const double2 v = shfl2(r, lane & 31);
-                    const double w = (k == 0) ? 1.0 : ((k == -1 || k == 1) ? 2.0 / 3.0 : 1.0 / 3.0);
-                    if (lane >= 0 && lane < 32 && tx < nsx) acc = axpy(w, v, acc);
-                }
-                if (tx < nsx) xs[ty * SX + tx] = acc;
+            if (kz == 0) {
+                accLo = add(accLo, r);
+            } else if (kz == 1) {
+                accLo = axpy(2.0 / 3.0, r, accLo);
+                accHi = axpy(1.0 / 3.0, r, accHi);
+            } else {
+                accLo = axpy(1.0 / 3.0, r, accLo);
+                accHi = axpy(2.0 / 3.0, r, accHi);
+                tb[ty * TX + tx] = accLo;
+                accLo = accHi;
+                accHi = zero2();
+                flushSlots(zLow - zBase);
+                ++zLow;
             }
-            __syncthreads();
-            if (tid == 0 && it - 1 + STAGES < nplanes) issue(sb, zz - 1 + STAGES);
-            if (slotThread) {
-                const int Y = Ya + syi;
-                double2 val = zero2();
-#pragma unroll
-                for (int k = -2; k <= 2; ++k) {
-                    const int fy = 3 * Y + k;
-                    const double w = (k == 0) ? 1.0 : ((k == -1 || k == 1) ? 2.0 / 3.0 : 1.0 / 3.0);
-                    if (fy >= y0 && fy < ye) val = axpy(w, xs[(fy - y0) * SX + sxi], val);
-                }
-                const int kz = z % 3;
-                if (kz == 0) {
-                    accLo = add(accLo, val);
-                } else if (kz == 1) {
-                    accLo = axpy(2.0 / 3.0, val, accLo);
-                    accHi = axpy(1.0 / 3.0, val, accHi);
-                } else {
-                    accLo = axpy(1.0 / 3.0, val, accLo);
-                    accHi = axpy(2.0 / 3.0, val, accHi);
-                    part[((zLow - zBase) * SY + syi) * SX + sxi] = accLo;
-                    ++zLow;
-                    accLo = accHi;
-                    accHi = zero2();
-                }
-            }
-        } else if (it == 1 && tid == 0 && STAGES < nplanes) {
-            issue(0, z0 - 1 + STAGES);  // plane z0-1 is halo only: its stage is free after the sync
         }
-        Cm = C0;
-        Em = E0;
-        Km = K0;
-        C0 = Cp;
-        E0 = Ep;
-        K0 = Kp;
+        Aprev = add(Acur, Uo);
+        Acur = T;
+    };
+    using U0 = std::integral_constant<int, 0>;
+    using U1 = std::integral_constant<int, 1>;
+    using U2 = std::integral_constant<int, 2>;
+    // zz = z0 - 1 + it and z0 = 1 (mod 3): zz % 3 == it % 3
+    for (int it = 0; it < nplanes; it += 3) {
+        step(it, U0{});
+        if (it + 1 >= nplanes) break;
+        step(it + 1, U1{});
+        if (it + 2 >= nplanes) break;
+        step(it + 2, U2{});
     }
-    if (slotThread) {
-        part[((zLow - zBase) * SY + syi) * SX + sxi] = accLo;
-        part[((zLow + 1 - zBase) * SY + syi) * SX + sxi] = accHi;
-    }
+    __syncthreads();
+    tb[ty * TX + tx] = accLo;
+    flushSlots(zLow - zBase);
+    __syncthreads();
+    tb[ty * TX + tx] = accHi;
+    flushSlots(zLow + 1 - zBase);
     dev::block_norms(nmax, nsum, a.norms);
 }
 
@@ -328,9 +412,9 @@ size_t partial_count(const Geometry& g) {
 
 int blocks(const Geometry& g) { return g.nbx * g.nby * g.nbz; }
 
-size_t smem_bytes() {
-    return (2 * STAGES * kPlane + STAGES * kB + 2 * STAGES * kC + 2 * kPlane + TY * SX) * sizeof(double2) +
-           STAGES * sizeof(uint64_t);
+size_t smem_bytes(bool bpx) {
+    const int se = bpx ? stage_elems<true>() : stage_elems<false>();
+    return (STAGES * se + (bpx ? 4 : 2) * kV + 2 * kPlane + NT) * sizeof(double2) + STAGES * sizeof(uint64_t);
 }
 
 bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind) {
@@ -354,16 +438,25 @@ bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind) {
     return r == CUDA_SUCCESS;
 }
 
-void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapB,
-            const CUtensorMap& mapC, const CUtensorMap& mapI, cudaStream_t s) {
-    static bool configured = false;
-    const size_t smem = smem_bytes();
-    if (!configured) {
-        cudaFuncSetAttribute(k_fused3, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        configured = true;
-    }
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapC,
+            const CUtensorMap& mapI, cudaStream_t s) {
+    static bool configured[2] = {false, false};
+    const bool bpx = a.bpx != 0;
+    const size_t smem = smem_bytes(bpx);
     dim3 grid(a.g.nbx, a.g.nby, a.g.nbz);
-    k_fused3<<<grid, dim3(TX, TY), smem, s>>>(mapU, mapS, mapB, mapC, mapI, a);
+    if (bpx) {
+        if (!configured[1]) {
+            cudaFuncSetAttribute(k_fused3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            configured[1] = true;
+        }
+        k_fused3<true><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapS, mapC, mapI, a);
+    } else {
+        if (!configured[0]) {
+            cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+            configured[0] = true;
+        }
+        k_fused3<false><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapS, mapC, mapI, a);
+    }
 }
 
 void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s) {

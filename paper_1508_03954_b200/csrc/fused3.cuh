@@ -28,7 +28,10 @@
 namespace tmg {
 namespace fused3 {
 
-constexpr int TX = 32, TY = 12, STAGES = 3;
+#ifndef TMG_FUSED_TY
+#define TMG_FUSED_TY 8
+#endif
+constexpr int TX = 32, TY = TMG_FUSED_TY, STAGES = 4;
 constexpr int HX = TX + 2, HY = TY + 2;
 constexpr int SX = TX / 3 + 3, SY = TY / 3 + 3;  // restriction slots per tile (upper bounds)
 constexpr int CX = (TX + 1) / 3 + 2, CY = (TY + 1) / 3 + 2;  // coarse tile feeding the prolongation
@@ -58,15 +61,15 @@ struct Args {
 
 Geometry geometry(int m, int mc);
 size_t partial_count(const Geometry& g);
-size_t smem_bytes();
+size_t smem_bytes(bool bpx);
 int blocks(const Geometry& g);
 
 // TMA descriptor for one lattice array (double2 viewed as float64 pairs).
 // kind 0: fine u / sc halo'd tile, 1: fine b tile, 2: two coarse planes.
 bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind);
 
-void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapB,
-            const CUtensorMap& mapC, const CUtensorMap& mapI, cudaStream_t s);
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapC,
+            const CUtensorMap& mapI, cudaStream_t s);
 // r_{L-1}(W) = sum of the tile partials covering W, fixed order.
 void combine(const Args& a, double2* rCoarse, int blocks, cudaStream_t s);
 

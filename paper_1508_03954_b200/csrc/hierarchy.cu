@@ -845,7 +845,7 @@ struct Hierarchy::Impl {
             fa.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
             fa.ellMin = prob.ellMin;
             fa.level = L;
-            fused3::launch(fa, mapU[0], mapS[0], mapB, mapC, mapI, stream);
+            fused3::launch(fa, mapU[0], mapS[0], mapC, mapI, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream);
             std::swap(F.u, uAlt);
@@ -1028,7 +1028,7 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     I.build_restrict_tables();
     {
         const char* fz = std::getenv("TMG_FUSED");
-        if (prob.fast && I.p == 3 && I.L >= 2 && fz && fz[0] == '1') {
+        if (prob.fast && I.p == 3 && I.L >= 2 && !(fz && fz[0] == '0')) {
             const dev::Lvl& F = I.lv[I.L];
             I.uAlt = I.alloc<double2>(F.n);
             I.scAlt = I.alloc<double2>(F.n);
