@@ -1230,7 +1230,43 @@ void test_divdc3(const double* x, const double* y, double* out, long long n) {
     cudaFree(dk);
 }
 
-void Hierarchy::unfold() { throw UnsupportedConfigError("FMG unfolding is not implemented yet"); }
+// FMG unfolding: the reference refines every leaf cell in
+// sorted key order (spacetree.cpp:272-329), giving new vertices p-linearly
+// prolonged u (create_vertex_if_missing, :245-270) and zero payload, keeps the
+// existing levels' u / sc / sf / si, and re-classifies (succ = L+1-l).  The
+// canonical-parent prolongation used here equals the creating cell's for
+// every vertex (coinciding components are exact copies, transfer.cpp:26-38).
+void Hierarchy::unfold() {
+    Impl& old = *impl_;
+    Problem p2 = old.prob;
+    p2.levels = old.L + 1;
+    if (p2.rhsLattice < 0) p2.rhsLattice = p2.levels;
+    TMG_CUDA(cudaStreamSynchronize(old.stream));
+    Hierarchy deeper(p2);
+    Impl& nw = *deeper.impl_;
+    const int L = old.L;
+    for (int l = 0; l <= L; ++l) {
+        const dev::Lvl& a = old.lv[l];
+        const dev::Lvl& b = nw.lv[l];
+        const size_t bytes = static_cast<size_t>(a.n) * sizeof(double2);
+        auto copy = [&](double2* dst, const double2* src) {
+            if (dst && src) TMG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, nw.stream));
+        };
+        copy(b.u, a.u);
+        copy(b.sc, a.sc);
+        copy(b.sf, a.sf);
+        copy(b.si, a.si);
+        copy(b.sinext, a.sinext);
+    }
+    const dev::Lvl& F = nw.lv[L + 1];
+    if (nw.p == 1) dev::k_prolong_new<1><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L]);
+    else if (nw.p == 2) dev::k_prolong_new<2><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L]);
+    else dev::k_prolong_new<3><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L]);
+    TMG_CUDA(cudaGetLastError());
+    nw.coarseUStale = nw.prob.fast;
+    TMG_CUDA(cudaStreamSynchronize(nw.stream));
+    std::swap(impl_, deeper.impl_);
+}
 
 void Hierarchy::time_cycles(const Policy& pol, int n0, int count, bool flushL2, double* out4) {
     Impl& I = *impl_;

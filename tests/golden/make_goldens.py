@@ -61,6 +61,21 @@ CONFIGS = {
                                       max_sweeps=300),
     "runner_budget_one": dict(problem="poisson-sin", dim=2, level=2, max_sweeps=1, target_drop=1e-30),
     "capi_poisson_l2": dict(problem="poisson-sin", dim=2, level=2, max_sweeps=60),
+    # cfg5 schedule (FMG unfolding) at reduced depth: 3D 2 -> 4 with the cfg5 operator, and converging variants
+    "fmg3d_cfg5op": dict(problem="helmholtz-sin", dim=3, level=4, fmg_from=2, phi="6400,3200", cycle="td-add",
+                         omega="exponential", omega_s=0.6, max_sweeps=40, fmg_stage_cap=40, target_drop=1e-8,
+                         **SEEDED),
+    "fmg3d_k20": dict(problem="helmholtz-sin", dim=3, level=4, fmg_from=2, phi="400,200", cycle="td-add",
+                      omega="undamped", omega_s=0.6, max_sweeps=60, fmg_stage_cap=60, target_drop=1e-6, **SEEDED),
+    "fmg3d_poisson": dict(problem="poisson-sin", dim=3, level=4, fmg_from=2, cycle="td-add", omega="exponential",
+                          omega_s=0.8, max_sweeps=60, fmg_stage_cap=60, target_drop=1e-6, norm="h"),
+    "fmg3d_seeded_k3": dict(problem="helmholtz-sin", dim=3, level=4, fmg_from=2, phi="9,4.5", cycle="td-add",
+                            omega="undamped", omega_s=0.6, max_sweeps=60, fmg_stage_cap=60, target_drop=1e-6,
+                            **SEEDED),
+    "fmg2d_k10": dict(problem="helmholtz-sin", dim=2, level=5, fmg_from=2, phi="100,50", cycle="td-add",
+                      omega="undamped", omega_s=0.6, max_sweeps=80, fmg_stage_cap=80, target_drop=1e-8, **SEEDED),
+    "fmg2d_bpx": dict(problem="helmholtz-sin", dim=2, level=4, fmg_from=2, phi="100,50", cycle="td-bpx",
+                      omega="undamped", omega_s=0.5, max_sweeps=50, fmg_stage_cap=50, target_drop=1e-6, **SEEDED),
     "rotated_3d_bpx": dict(problem="helmholtz-sin", dim=3, level=3, phi="2025", theta_deg=35, cycle="td-bpx",
                            omega="transition", max_sweeps=15, target_drop=1e-30),
 }
