@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a) {
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
         int idx[P];
         dev::unflat<P>(f, c.n1, idx);
-        if (c.si) {  // si = siNext (cycles.cpp:247)
+        if (a.bpx && c.si) {  // si = siNext (cycles.cpp:247); identically zero unless BPX
             c.si[f] = c.sinext[f];
             c.sinext[f] = make_double2(0.0, 0.0);
         }
