@@ -14,9 +14,12 @@ Workload: the BASELINE metric's target is quoted on the 243^3
 and 729^3 configs; the 729^3 cycle (cfg5's final FMG level, k=80) fits one
 GPU, so it is the N=1 workload.  Other configs are parity-test cases.
 
-N>1 (torchrun, one process per GPU): every rank runs its own 729^3 replica
-("scaling": "weak"); value = total DoF-updates of all ranks / max-over-ranks
-device time.  Round-1 status of the z-slab sharding: DESIGN.md §6.
+N>1 (torchrun, one process per GPU): 3D workloads run the z-slab
+decomposition: each rank owns a slab of the fine level and of
+level L-1, halos / restriction partials / the replicated level's residual
+move over NCCL; the problem size is fixed ("scaling": "strong") and value =
+DoF x cycles / max-over-ranks device time.  2D workloads run one replica
+per GPU ("scaling": "weak").  --mode replicas forces replicas.
 
 --impl reference: the reference CPU implementation (oracle/_ref, built from
 the unmodified reference sources) on the host cores -- one independent
@@ -207,6 +210,7 @@ def main():
     ap.add_argument("--workload", default="cfg5", choices=list(WORKLOADS))
     ap.add_argument("--precision", default=os.environ.get("TMG_PRECISION", "fast"), choices=["fast", "exact"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default=None, choices=["single", "slabs", "replicas"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     w = WORKLOADS[args.workload]
@@ -228,11 +232,23 @@ def main():
 
     k = w["k"]
     phi = complex(k * k, 0.5 * k * k)
-    h = T.Hierarchy(w["dim"], w["level"], phi=phi, chi="seeded", rhs_seed=RHS_SEED, precision=args.precision,
-                    max_vertices=10 ** 10, device=local)
+    mode = args.mode or ("slabs" if (world > 1 and w["dim"] == 3 and args.precision == "fast") else
+                         ("replicas" if world > 1 else "single"))
     pol = T.Policy(kind=w["omega"], omega_s=w["omega_s"], bpx=(w["cycle"] == "td-bpx"))
-    # warm-up cycles (untimed), then K timed cycles with CUDA events on the library stream
-    h.time_cycles(pol, 1, args.warmup, flush_l2=False)
+    if mode == "slabs":
+        uid = T.nccl_unique_id() if rank == 0 else None
+        if dist:
+            box = [uid]
+            dist.broadcast_object_list(box, src=0)
+            uid = box[0]
+        h = T.Slabs(w["level"], phi, chi="seeded", rhs_seed=RHS_SEED, rank=rank, world=world, nccl_id=uid,
+                    device=local)
+        h.time_cycles(pol, 1, args.warmup)
+    else:
+        h = T.Hierarchy(w["dim"], w["level"], phi=phi, chi="seeded", rhs_seed=RHS_SEED, precision=args.precision,
+                        max_vertices=10 ** 10, device=local)
+        # warm-up cycles (untimed), then K timed cycles with CUDA events on the library stream
+        h.time_cycles(pol, 1, args.warmup, flush_l2=False)
 
     def barrier():
         if dist:
@@ -242,7 +258,10 @@ def main():
 
     barrier()
     with ClockSampler(local) as clk:
-        out = h.time_cycles(pol, args.warmup + 1, args.steps, flush_l2=False)
+        if mode == "slabs":
+            out = h.time_cycles(pol, args.warmup + 1, args.steps)
+        else:
+            out = h.time_cycles(pol, args.warmup + 1, args.steps, flush_l2=False)
     barrier()
     total_ms, fine_ms, launches_per_cycle = float(out[0]), float(out[1]), int(out[3])
     if dist:
@@ -252,8 +271,14 @@ def main():
         total_ms = float(t.item())
     dof = interior(w)
     ms_per_step = total_ms / args.steps
-    value = world * dof * args.steps / (total_ms / 1e3)
+    copies = 1 if mode == "slabs" else world
+    value = copies * dof * args.steps / (total_ms / 1e3)
     B_total, B_fine = algorithmic_bytes(w, args.precision)
+    if mode == "slabs":  # this rank's share of the fine level
+        z0, z1 = h.owned_planes()
+        B_fine = 80 * (z1 - z0) * (3 ** w["level"] + 1) ** 2
+        B_total = B_total * (z1 - z0) / (3 ** w["level"] - 1)
+        launches_per_cycle = 2 * w["level"] + 6
     peak, peak_kind = peaks()
     achieved = B_fine / (fine_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
@@ -271,13 +296,23 @@ def main():
     rng = np.random.default_rng(RHS_SEED)
     chi_host[:] = rng.uniform(-1, 1, size=2 * n_lat)
     e2e_steps = max(2, min(args.steps, 5))
+    h2d = 16 * n_lat
+    barrier()
     t0 = time.perf_counter()
     for i in range(e2e_steps):
-        h.e2e_step(pol, args.warmup + args.steps + 1 + i, chi_host)
+        if mode == "slabs":
+            _, h2d = h.e2e_step(pol, args.warmup + args.steps + 1 + i, chi_host)
+        else:
+            h.e2e_step(pol, args.warmup + args.steps + 1 + i, chi_host)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e = {"value": world * dof / e2e_s, "unit": "DoF-updates/s", "h2d_bytes_per_step": 16 * n_lat,
-           "d2h_bytes_per_step": 24, "note": "per step: H2D of the nodal rhs (16 B/vertex, pinned), device load "
-           "vector, one cycle, D2H of the three residual norms (wall clock)"}
+    if dist:
+        import torch
+        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": copies * dof / e2e_s, "unit": "DoF-updates/s", "h2d_bytes_per_step": int(h2d),
+           "d2h_bytes_per_step": 24, "note": "per step: H2D of the nodal rhs (16 B/vertex, pinned; slabs: the "
+           "rank's planes), device load vector, one cycle, D2H of the three residual norms (wall clock, max over ranks)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -292,13 +327,15 @@ def main():
         line = {
             "metric": "complex DoF-updates/s per additive MG cycle", "value": value, "unit": "DoF-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "complex128 (f64)",
+            "higher_is_better": True, "scaling": "strong" if mode == "slabs" else "weak", "vs_baseline": None,
+            "dtype": "complex128 (f64)",
             "data": "synthetic (seeded uniform complex rhs, SURVEY §8d)",
             "config": {"workload": args.workload, "desc": w["desc"], "dim": w["dim"], "level": w["level"],
                        "interior_dof": dof, "precision": args.precision, "cycle": w["cycle"],
                        "l2": "inputs larger than L2 (fine level arrays of "
                              f"{16 * n_lat / 1e9:.2f} GB each); no flush",
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU"},
+                       "parallelism": {"slabs": f"z-slabs x{world} (NCCL)", "replicas": f"replicas x{world}",
+                                       "single": "single GPU"}[mode]},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_cycle * args.steps, "fine_pass_ms": fine_ms,
         }

@@ -117,6 +117,32 @@ treemg_status tmg_e2e_step(tmg_hierarchy* h, const tmg_policy* pol, int n, const
 
 const char* tmg_last_error(void);
 
+/* ---- 3. z-slab multi-GPU cycle ---------------------------
+ * The fine level and level L-1 are split into z-slabs (whole z-chunks of the
+ * fused fine pass), coarser levels are replicated; halos, restriction
+ * partials and the replicated level's residual move over NCCL (dlopen'd
+ * libnccl.so.2), one slab per process/GPU.  With nccl_id == NULL, `local`
+ * virtual slabs run in this process on one device with device-copy
+ * transfers (the single-GPU test mode of the same code path).  3D, fast
+ * precision; iterates are bitwise identical for every slab count. */
+typedef struct tmg_slabs tmg_slabs;
+treemg_status tmg_nccl_unique_id(unsigned char* out128);
+treemg_status tmg_slabs_create(const tmg_problem* prob, int local, int rank, int world,
+                               const unsigned char* nccl_id, tmg_slabs** out);
+void tmg_slabs_destroy(tmg_slabs* h);
+treemg_status tmg_slabs_cycle(tmg_slabs* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
+/* owned fine planes of the local slabs into a full-lattice host buffer */
+treemg_status tmg_slabs_get_fine_u(tmg_slabs* h, double* out);
+treemg_status tmg_slabs_time_cycles(tmg_slabs* h, const tmg_policy* pol, int n0, int count, double* out4);
+int tmg_slabs_owned_planes(tmg_slabs* h, int* z0, int* z1);
+/* e2e step: owned (+halo) planes of a full-lattice host rhs -> device load
+ * vector -> one cycle -> host norms (out3); *h2d_bytes = bytes uploaded */
+treemg_status tmg_slabs_e2e_step(tmg_slabs* h, const tmg_policy* pol, int n, const double* chi, double* out3,
+                                 long long* h2d_bytes);
+/* host-only slab plan: per slab {cb, ce, z0, z1, Zs, Ze, Ws, We} (fused
+ * z-chunks, fine planes, level L-1 planes, level L-2 planes); out: 8*world */
+treemg_status tmg_slab_plan(int levels, int world, int* out8);
+
 /* Test hook: out = x / y elementwise (interleaved complex, host buffers) on
  * the device with the kernels' restatement of libgcc __divdc3. */
 treemg_status tmg_test_divdc3(const double* x, const double* y, double* out, long long n);

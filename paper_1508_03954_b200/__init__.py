@@ -45,7 +45,9 @@ EXTENSION_SYMBOLS = [
     "tmg_hierarchy_create", "tmg_hierarchy_destroy", "tmg_td_add", "tmg_td_bpx", "tmg_lattice_size",
     "tmg_get_field", "tmg_set_field", "tmg_set_fine_interior_u", "tmg_set_random_initial_guess",
     "tmg_set_fine_rhs", "tmg_field_hash", "tmg_time_cycles", "tmg_e2e_step", "tmg_last_error",
-    "treemg_result_fingerprint", "tmg_test_divdc3",
+    "treemg_result_fingerprint", "tmg_test_divdc3", "tmg_nccl_unique_id", "tmg_slabs_create", "tmg_slabs_destroy",
+    "tmg_slabs_cycle", "tmg_slabs_get_fine_u", "tmg_slabs_time_cycles", "tmg_slabs_owned_planes", "tmg_slab_plan",
+    "tmg_slabs_e2e_step",
 ]
 
 _lib = None
@@ -137,6 +139,23 @@ def lib():
         L.treemg_result_fingerprint.argtypes = [vp, cp]
         L.tmg_test_divdc3.restype = ip
         L.tmg_test_divdc3.argtypes = [pd, pd, pd, ctypes.c_longlong]
+        L.tmg_nccl_unique_id.restype = ip
+        L.tmg_nccl_unique_id.argtypes = [ctypes.c_char_p]
+        L.tmg_slabs_create.restype = ip
+        L.tmg_slabs_create.argtypes = [ctypes.POINTER(_Problem), ip, ip, ip, ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.tmg_slabs_destroy.argtypes = [vp]
+        L.tmg_slabs_cycle.restype = ip
+        L.tmg_slabs_cycle.argtypes = [vp, ctypes.POINTER(_Policy), ip, ctypes.POINTER(_Stats)]
+        L.tmg_slabs_get_fine_u.restype = ip
+        L.tmg_slabs_get_fine_u.argtypes = [vp, pd]
+        L.tmg_slabs_time_cycles.restype = ip
+        L.tmg_slabs_time_cycles.argtypes = [vp, ctypes.POINTER(_Policy), ip, ip, pd]
+        L.tmg_slabs_owned_planes.restype = ip
+        L.tmg_slabs_owned_planes.argtypes = [vp, ctypes.POINTER(ip), ctypes.POINTER(ip)]
+        L.tmg_slabs_e2e_step.restype = ip
+        L.tmg_slabs_e2e_step.argtypes = [vp, ctypes.POINTER(_Policy), ip, pd, pd, ctypes.POINTER(ctypes.c_longlong)]
+        L.tmg_slab_plan.restype = ip
+        L.tmg_slab_plan.argtypes = [ip, ip, ctypes.POINTER(ip)]
         L.tmg_e2e_step.restype = ip
         L.tmg_e2e_step.argtypes = [vp, ctypes.POINTER(_Policy), ip, pd, pd]
         _lib = L
@@ -300,6 +319,78 @@ class Hierarchy:
         buf = chi_host.view(np.float64) if chi_host.dtype == np.complex128 else chi_host
         _check(self.L.tmg_e2e_step(self.h, ctypes.byref(pc), n, _pd(buf), _pd(out)))
         return out
+
+
+def nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().tmg_nccl_unique_id(buf))
+    return buf.raw
+
+
+def slab_plan(levels: int, world: int) -> np.ndarray:
+    """Per slab (cb, ce, z0, z1, Zs, Ze, Ws, We), host-only."""
+    out = (ctypes.c_int * (8 * world))()
+    _check(lib().tmg_slab_plan(levels, world, out))
+    return np.array(list(out)).reshape(world, 8)
+
+
+class Slabs:
+    """z-slab decomposition of a 3D fast-precision hierarchy.
+
+    nccl_id=None: `local` virtual slabs on this process's device (test mode);
+    else one slab for `rank` of `world` over NCCL."""
+
+    def __init__(self, levels: int, phi: complex, chi: str = "seeded", rhs_seed: int = 12345, ell_min: int = 1,
+                 local: int = 1, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, device: int = 0):
+        self.L = lib()
+        prob = _Problem(3, levels, ell_min, 0.0, complex(phi).real, complex(phi).imag, CHI_KINDS[chi], rhs_seed, 0, 1,
+                        10 ** 12, device)
+        h = ctypes.c_void_p()
+        _check(self.L.tmg_slabs_create(ctypes.byref(prob), local, rank, world, nccl_id, ctypes.byref(h)))
+        self.h = h
+        self.levels = levels
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.tmg_slabs_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def cycle(self, pol: "Policy", n: int) -> "SweepStats":
+        st = _Stats()
+        pc = pol.c()
+        _check(self.L.tmg_slabs_cycle(self.h, ctypes.byref(pc), n, ctypes.byref(st)))
+        return SweepStats(st.max_norm, st.euclid_norm, st.h_norm, st.updated_fine_vertices)
+
+    def fine_u(self) -> np.ndarray:
+        n = (3 ** self.levels + 1) ** 3
+        out = np.zeros(2 * n)
+        _check(self.L.tmg_slabs_get_fine_u(self.h, _pd(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    def owned_planes(self):
+        z0, z1 = ctypes.c_int(), ctypes.c_int()
+        self.L.tmg_slabs_owned_planes(self.h, ctypes.byref(z0), ctypes.byref(z1))
+        return z0.value, z1.value
+
+    def time_cycles(self, pol: "Policy", n0: int, count: int) -> np.ndarray:
+        out = np.zeros(4)
+        pc = pol.c()
+        _check(self.L.tmg_slabs_time_cycles(self.h, ctypes.byref(pc), n0, count, _pd(out)))
+        return out
+
+    def e2e_step(self, pol: "Policy", n: int, chi_host: np.ndarray):
+        out = np.zeros(3)
+        nb = ctypes.c_longlong()
+        pc = pol.c()
+        buf = chi_host.view(np.float64) if chi_host.dtype == np.complex128 else chi_host
+        _check(self.L.tmg_slabs_e2e_step(self.h, ctypes.byref(pc), n, _pd(buf), _pd(out), ctypes.byref(nb)))
+        return out, nb.value
 
 
 def device_divide(x: np.ndarray, y: np.ndarray) -> np.ndarray:

@@ -26,6 +26,10 @@ struct tmg_hierarchy {
     std::unique_ptr<Hierarchy> h;
 };
 
+struct tmg_slabs {
+    std::unique_ptr<SlabGroup> g;
+};
+
 namespace {
 
 thread_local std::string g_lastError;
@@ -172,6 +176,96 @@ unsigned long long treemg_result_fingerprint(const treemg_result* res, const cha
 treemg_status tmg_test_divdc3(const double* x, const double* y, double* out, long long n) {
     if (!x || !y || !out || n < 0) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] { test_divdc3(x, y, out, n); });
+}
+
+namespace {
+Problem problem_from(const tmg_problem* prob) {
+    Problem p;
+    p.dim = prob->dim;
+    p.levels = prob->levels;
+    p.ellMin = prob->ell_min;
+    p.theta = prob->theta;
+    p.phi = Cplx(prob->phi_re, prob->phi_im);
+    p.chi = static_cast<ChiKind>(prob->chi_kind);
+    p.rhsSeed = prob->rhs_seed;
+    p.rhsSphere = prob->rhs_sphere != 0;
+    p.fast = prob->precision == 1;
+    if (prob->max_vertices > 0) p.maxVertices = static_cast<std::size_t>(prob->max_vertices);
+    p.device = prob->device;
+    if (p.ellMin < 1) throw ConfigError("ellMin must be >= 1");
+    return p;
+}
+}  // namespace
+
+treemg_status tmg_nccl_unique_id(unsigned char* out128) {
+    if (!out128) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        if (!nccl_unique_id(out128)) throw CudaError("NCCL unavailable");
+    });
+}
+
+treemg_status tmg_slabs_create(const tmg_problem* prob, int local, int rank, int world,
+                               const unsigned char* nccl_id, tmg_slabs** out) {
+    if (!prob || !out) return fail(TREEMG_E_USAGE, "null argument");
+    *out = nullptr;
+    auto* h = new tmg_slabs();
+    const treemg_status st = guarded([&] { h->g = std::make_unique<SlabGroup>(problem_from(prob), local, rank, world, nccl_id); });
+    if (st != TREEMG_OK) {
+        delete h;
+        return st;
+    }
+    *out = h;
+    return TREEMG_OK;
+}
+
+void tmg_slabs_destroy(tmg_slabs* h) { delete h; }
+
+treemg_status tmg_slabs_cycle(tmg_slabs* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
+    if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        Policy p = policy_from(pol);
+        if (n < 1) throw ConfigError("sweep counter starts at 1");
+        if (p.bpx) p.hbMask = false;
+        fill_stats(h->g->cycle(p, n), out);
+    });
+}
+
+treemg_status tmg_slabs_get_fine_u(tmg_slabs* h, double* out) {
+    if (!h || !out) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->g->get_fine_u(out); });
+}
+
+treemg_status tmg_slabs_time_cycles(tmg_slabs* h, const tmg_policy* pol, int n0, int count, double* out4) {
+    if (!h || !pol || !out4) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        Policy p = policy_from(pol);
+        if (p.bpx) p.hbMask = false;
+        h->g->time_cycles(p, n0, count, out4);
+    });
+}
+
+treemg_status tmg_slabs_e2e_step(tmg_slabs* h, const tmg_policy* pol, int n, const double* chi, double* out3,
+                                 long long* h2d_bytes) {
+    if (!h || !pol || !chi || !out3) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        Policy p = policy_from(pol);
+        if (p.bpx) p.hbMask = false;
+        h->g->e2e_step(p, n, chi, out3, h2d_bytes);
+    });
+}
+
+treemg_status tmg_slab_plan(int levels, int world, int* out8) {
+    if (!out8) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        const auto plan = slab_plan(levels, world);
+        for (size_t r = 0; r < plan.size(); ++r)
+            for (int k = 0; k < 8; ++k) out8[8 * r + static_cast<size_t>(k)] = plan[r][static_cast<size_t>(k)];
+    });
+}
+
+int tmg_slabs_owned_planes(tmg_slabs* h, int* z0, int* z1) {
+    if (!h || !z0 || !z1) return 0;
+    return h->g->owned_planes(z0, z1);
 }
 
 treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out) {

@@ -3,6 +3,8 @@
 
 #include "fast.cuh"
 
+#include <algorithm>
+
 namespace tmg {
 namespace fast {
 
@@ -58,8 +60,8 @@ __device__ __forceinline__ double2 stage(double2 smooth, double2 w, bool cp, int
 
 // ---- K1f / K1c: top-down correction ----------------------------------------
 template <int P, bool FINE>
-__global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx) {
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+__global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx, unsigned fa, unsigned fb) {
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int idx[P];
         dev::unflat<P>(f, c.n1, idx);
         if (dev::on_boundary<P>(idx, static_cast<int>(c.m))) continue;  // u = sc = 0 stay pinned
@@ -179,10 +181,10 @@ __global__ void __launch_bounds__(256) k_residual_lowdim(ResArgs a) {
 
 // ---- K3r: r_{l-1} = R r_l (separable 1D weights 1/3 2/3 1 2/3 1/3) -----------
 template <int P>
-__global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse) {
+__global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse, unsigned fa, unsigned fb) {
     const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
     const long long sy = fine.n1, sz = static_cast<long long>(fine.n1) * fine.n1;
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < coarse.n; f += gridDim.x * blockDim.x) {
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int W[P];
         dev::unflat<P>(f, coarse.n1, W);
         if (dev::on_boundary<P>(W, static_cast<int>(coarse.m))) continue;
@@ -240,9 +242,9 @@ __global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse) {
 
 // ---- K3c: coarse smoothing on the restricted residual ------------------------
 template <int P>
-__global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a) {
+__global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a, unsigned fa, unsigned fb) {
     const Lvl& c = a.lv;
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int idx[P];
         dev::unflat<P>(f, c.n1, idx);
         if (a.bpx && c.si) {  // si = siNext (cycles.cpp:247); identically zero unless BPX
@@ -269,16 +271,35 @@ constexpr int kZch = 48;
 
 }  // namespace
 
+namespace {
+// plane range [za, zb) of the last axis -> flat index range
+void span(int P, const Lvl& v, int za, int zb, unsigned& fa, unsigned& fb) {
+    if (za < 0) {
+        fa = 0;
+        fb = v.n;
+        return;
+    }
+    unsigned plane = 1;
+    for (int d = 0; d < P - 1; ++d) plane *= v.n1;
+    fa = static_cast<unsigned>(za) * plane;
+    fb = static_cast<unsigned>(std::min<long long>(zb, v.n1)) * plane;
+    if (fb < fa) fb = fa;
+}
+}  // namespace
+
 void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaStream_t s) {
-    if (P == 1) k_topdown<1, true><<<blocks, 256, 0, s>>>(f, pr, bpx);
-    else if (P == 2) k_topdown<2, true><<<blocks, 256, 0, s>>>(f, pr, bpx);
-    else k_topdown<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx);
+    if (P == 1) k_topdown<1, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, f.n);
+    else if (P == 2) k_topdown<2, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, f.n);
+    else k_topdown<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, f.n);
 }
 
-void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cudaStream_t s) {
-    if (P == 1) k_topdown<1, false><<<blocks, 256, 0, s>>>(c, pr, bpx);
-    else if (P == 2) k_topdown<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx);
-    else k_topdown<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx);
+void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cudaStream_t s, int za, int zb) {
+    unsigned fa, fb;
+    span(P, c, za, zb, fa, fb);
+    if (fb <= fa) return;
+    if (P == 1) k_topdown<1, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
+    else if (P == 2) k_topdown<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
+    else k_topdown<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
 }
 
 int residual_fine_blocks(int P, const Lvl& f, int smCount) {
@@ -305,16 +326,23 @@ int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s) {
     return nb;
 }
 
-void restrict_level(int P, const Lvl& fine, const Lvl& coarse, const double*, int blocks, cudaStream_t s) {
-    if (P == 1) k_restrict<1><<<blocks, 256, 0, s>>>(fine, coarse);
-    else if (P == 2) k_restrict<2><<<blocks, 256, 0, s>>>(fine, coarse);
-    else k_restrict<3><<<blocks, 256, 0, s>>>(fine, coarse);
+void restrict_level(int P, const Lvl& fine, const Lvl& coarse, const double*, int blocks, cudaStream_t s, int za,
+                    int zb) {
+    unsigned fa, fb;
+    span(P, coarse, za, zb, fa, fb);
+    if (fb <= fa) return;
+    if (P == 1) k_restrict<1><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb);
+    else if (P == 2) k_restrict<2><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb);
+    else k_restrict<3><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb);
 }
 
-void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s) {
-    if (P == 1) k_smooth_coarse<1><<<blocks, 256, 0, s>>>(a);
-    else if (P == 2) k_smooth_coarse<2><<<blocks, 256, 0, s>>>(a);
-    else k_smooth_coarse<3><<<blocks, 256, 0, s>>>(a);
+void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s, int za, int zb) {
+    unsigned fa, fb;
+    span(P, a.lv, za, zb, fa, fb);
+    if (fb <= fa) return;
+    if (P == 1) k_smooth_coarse<1><<<blocks, 256, 0, s>>>(a, fa, fb);
+    else if (P == 2) k_smooth_coarse<2><<<blocks, 256, 0, s>>>(a, fa, fb);
+    else k_smooth_coarse<3><<<blocks, 256, 0, s>>>(a, fa, fb);
 }
 
 }  // namespace fast

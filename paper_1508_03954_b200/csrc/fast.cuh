@@ -39,16 +39,18 @@ struct ResArgs {
 // Fine level: u += sc + P sc_{L-1} (- P si_{L-1} at non-cPoints, BPX).
 void correct_fine(int P, const dev::Lvl& f, const dev::Lvl& pr, int bpx, int blocks, cudaStream_t s);
 // Coarse level l < L: sc_l += P sc_{l-1} (- P si_{l-1}, BPX).
-void topdown_coarse(int P, const dev::Lvl& c, const dev::Lvl& pr, int bpx, int blocks, cudaStream_t s);
+// (za, zb): plane range of the last axis, za < 0 for the whole level.
+void topdown_coarse(int P, const dev::Lvl& c, const dev::Lvl& pr, int bpx, int blocks, cudaStream_t s, int za = -1,
+                    int zb = -1);
 // Fine residual r = b - H u, norms, sc = omega r / diag, BPX injection; r to lv.rhat.
 // Returns the number of blocks that wrote norm partials.
 int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s);
 int residual_fine_blocks(int P, const dev::Lvl& f, int smCount);
 // r_{l-1} = R r_l on interior coarse vertices (rhat arrays).
 void restrict_level(int P, const dev::Lvl& fine, const dev::Lvl& coarse, const double* weights, int blocks,
-                    cudaStream_t s);
+                    cudaStream_t s, int za = -1, int zb = -1);
 // Coarse smoothing: sc_l = omega r_l / diag, si commit, BPX injection into l-1.
-void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s);
+void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s, int za = -1, int zb = -1);
 
 }  // namespace fast
 }  // namespace tmg

@@ -115,7 +115,8 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int m = a.g.m, mc = a.g.mc;
-    const int x0 = 1 + blockIdx.x * TX, y0 = 1 + blockIdx.y * TY, z0 = 1 + blockIdx.z * a.g.zc;
+    const int bzg = blockIdx.z + a.chunkBase;  // global z-chunk (slabs launch a chunk range)
+    const int x0 = 1 + blockIdx.x * TX, y0 = 1 + blockIdx.y * TY, z0 = 1 + bzg * a.g.zc;
     const int xe = min(x0 + TX, m), ye = min(y0 + TY, m), z1 = min(z0 + a.g.zc, m);
     const int nplanes = z1 - z0 + 2;
     const long long sy = a.n1, sz = static_cast<long long>(a.n1) * a.n1;
@@ -208,9 +209,11 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
     // restriction slots of this tile (xy); z handled by the column accumulators
     const int Xa = x0 / 3, Xb = (xe + 1) / 3, Ya = y0 / 3, Yb = (ye + 1) / 3;
     const int nsx = Xb - Xa + 1, nsy = Yb - Ya + 1;
-    const long long blockLin =
-        blockIdx.x + static_cast<long long>(gridDim.x) * (blockIdx.y + static_cast<long long>(gridDim.y) * blockIdx.z);
-    double2* part = a.partial + blockLin * static_cast<long long>(a.g.sz * SY * SX);
+    // partial layout [bz][zi][by][bx][SY][SX]: one chunk's zi = 0 slots are contiguous
+    const long long tileXY = blockIdx.x + static_cast<long long>(a.g.nbx) * blockIdx.y;
+    const long long tilesXY = static_cast<long long>(a.g.nbx) * a.g.nby;
+    double2* part = a.partial + (static_cast<long long>(bzg) * a.g.sz * tilesXY + tileXY) * (SY * SX);
+    const long long zStride = tilesXY * (SY * SX);
     const int zBase = (z0 - 1) / 3;
     int zLow = zBase;
     const bool slotThread = tid < nsx * nsy;
@@ -235,7 +238,7 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
                 }
                 acc = axpy(wy, row, acc);
             }
-            part[(zi * SY + syi) * SX + sxi] = acc;
+            part[zi * zStride + syi * SX + sxi] = acc;
         }
     };
 
@@ -362,13 +365,16 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
     dev::block_norms(nmax, nsum, a.norms);
 }
 
-__global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc) {
+__global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int za, int zb) {
     const int mc = a.g.mc, m = a.g.m, zc = a.g.zc;
     const unsigned n1c = a.n1c;
-    const unsigned total = n1c * n1c * n1c;
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+    const unsigned long long first = static_cast<unsigned long long>(za) * n1c * n1c;
+    const unsigned long long total = static_cast<unsigned long long>(zb - za) * n1c * n1c;
+    const long long tilesXY = static_cast<long long>(a.g.nbx) * a.g.nby;
+    for (unsigned long long t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const unsigned long long f = first + t;
         const int W0 = static_cast<int>(f % n1c), W1 = static_cast<int>((f / n1c) % n1c),
-                  W2 = static_cast<int>(f / (n1c * n1c));
+                  W2 = static_cast<int>(f / (static_cast<unsigned long long>(n1c) * n1c));
         if (W0 < 1 || W0 > mc - 1 || W1 < 1 || W1 > mc - 1 || W2 < 1 || W2 > mc - 1) continue;
         double2 acc = zero2();
         const int bz0 = (max(1, 3 * W2 - 2) - 1) / zc, bz1 = (min(m - 1, 3 * W2 + 2) - 1) / zc;
@@ -380,8 +386,9 @@ __global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc) {
                 const int yi = W1 - (1 + by * TY) / 3;
                 for (int bx = bx0; bx <= bx1; ++bx) {
                     const int xi = W0 - (1 + bx * TX) / 3;
-                    const long long bl = bx + static_cast<long long>(a.g.nbx) * (by + static_cast<long long>(a.g.nby) * bz);
-                    acc = add(acc, a.partial[((bl * a.g.sz + zi) * SY + yi) * SX + xi]);
+                    const long long tile = bx + static_cast<long long>(a.g.nbx) * by;
+                    acc = add(acc, a.partial[((static_cast<long long>(bz) * a.g.sz + zi) * tilesXY + tile) * (SY * SX) +
+                                             yi * SX + xi]);
                 }
             }
         }
@@ -399,7 +406,7 @@ Geometry geometry(int m, int mc) {
     g.nbx = (inner + TX - 1) / TX;
     g.nby = (inner + TY - 1) / TY;
     const int tiles = g.nbx * g.nby;
-    const int want = std::max(1, (4 * 2 * 148 + tiles - 1) / tiles);
+    const int want = std::max(8, (4 * 2 * 148 + tiles - 1) / tiles);
     g.zc = std::max(3, ((inner + want - 1) / want + 2) / 3 * 3);
     g.nbz = (inner + g.zc - 1) / g.zc;
     g.sz = g.zc / 3 + 2;
@@ -439,11 +446,11 @@ bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind) {
 }
 
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapC,
-            const CUtensorMap& mapI, cudaStream_t s) {
+            const CUtensorMap& mapI, cudaStream_t s, int nchunks) {
     static bool configured[2] = {false, false};
     const bool bpx = a.bpx != 0;
     const size_t smem = smem_bytes(bpx);
-    dim3 grid(a.g.nbx, a.g.nby, a.g.nbz);
+    dim3 grid(a.g.nbx, a.g.nby, nchunks > 0 ? nchunks : a.g.nbz);
     if (bpx) {
         if (!configured[1]) {
             cudaFuncSetAttribute(k_fused3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -459,8 +466,12 @@ void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, con
     }
 }
 
-void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s) {
-    k_combine<<<nblocks, 256, 0, s>>>(a, rCoarse);
+void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s, int za, int zb) {
+    if (za < 0) {
+        za = 0;
+        zb = a.g.mc + 1;
+    }
+    if (zb > za) k_combine<<<nblocks, 256, 0, s>>>(a, rCoarse, za, zb);
 }
 
 }  // namespace fused3

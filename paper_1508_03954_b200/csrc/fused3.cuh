@@ -57,6 +57,7 @@ struct Args {
     Geometry g;
     fast::LevelCoef k;
     int bpx, hb, ellMin, level;
+    int chunkBase;        // first global z-chunk of this launch
 };
 
 Geometry geometry(int m, int mc);
@@ -68,10 +69,12 @@ int blocks(const Geometry& g);
 // kind 0: fine u / sc halo'd tile, 1: fine b tile, 2: two coarse planes.
 bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind);
 
+// nchunks <= 0: all z-chunks (chunkBase must be 0)
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapC,
-            const CUtensorMap& mapI, cudaStream_t s);
-// r_{L-1}(W) = sum of the tile partials covering W, fixed order.
-void combine(const Args& a, double2* rCoarse, int blocks, cudaStream_t s);
+            const CUtensorMap& mapI, cudaStream_t s, int nchunks = 0);
+// r_{L-1}(W) = sum of the tile partials covering W, fixed order; coarse
+// planes [za, zb) (za < 0: all).
+void combine(const Args& a, double2* rCoarse, int blocks, cudaStream_t s, int za = -1, int zb = -1);
 
 }  // namespace fused3
 }  // namespace tmg

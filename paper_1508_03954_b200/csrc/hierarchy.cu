@@ -291,8 +291,8 @@ __global__ void k_norm_final(const double* __restrict__ partials, int nblocks, d
 // Consistent-mass load of the leaf cells (kernels.cpp:69-87), accumulated per
 // vertex in traversal cell order; constant across sweeps on a static grid.
 template <int P>
-__global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, LevelConst k) {
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+__global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, LevelConst k, unsigned fa, unsigned fb) {
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int idx[P];
         unflat<P>(f, c.n1, idx);
         // permutation: boundary axes carry a single cell, any priority works
@@ -761,16 +761,26 @@ struct Hierarchy::Impl {
     }
 
     template <int P>
-    void load_vector() {
+    void load_vector(unsigned fa, unsigned fb) {
         const dev::Lvl& F = lv[L];
-        dev::k_load_vector<P><<<blocks_for(F.n), 256, 0, stream>>>(F, chiNodal, kc[L]);
+        dev::k_load_vector<P><<<blocks_for(fb - fa), 256, 0, stream>>>(F, chiNodal, kc[L], fa, fb);
         TMG_CUDA(cudaGetLastError());
     }
 
-    void load_vector_dispatch() {
-        if (p == 1) load_vector<1>();
-        else if (p == 2) load_vector<2>();
-        else load_vector<3>();
+    // load vector on planes [za, zb) of the last axis (za < 0: everywhere)
+    void load_vector_dispatch(int za = -1, int zb = -1) {
+        const dev::Lvl& F = lv[L];
+        unsigned fa = 0, fb = F.n;
+        if (za >= 0) {
+            unsigned plane = 1;
+            for (int d = 0; d < p - 1; ++d) plane *= F.n1;
+            fa = static_cast<unsigned>(za) * plane;
+            fb = static_cast<unsigned>(std::min<long long>(zb, F.n1)) * plane;
+        }
+        if (fb <= fa) return;
+        if (p == 1) load_vector<1>(fa, fb);
+        else if (p == 2) load_vector<2>(fa, fb);
+        else load_vector<3>(fa, fb);
     }
 
     template <int P>
@@ -1307,3 +1317,4 @@ void Hierarchy::e2e_step(const Policy& pol, int n, const double* hostChi, double
 }
 
 }  // namespace tmg
+#include "slabs.inc"

@@ -7,6 +7,7 @@
 // fastest, complex128 as interleaved double2 (16-byte vector loads/stores).
 #pragma once
 
+#include <array>
 #include <complex>
 #include <cstdint>
 #include <memory>
@@ -105,10 +106,42 @@ class Hierarchy {
     void e2e_step(const Policy& pol, int n, const double* hostChi, double* out3);
 
     struct Impl;
+    Impl* raw() { return impl_.get(); }
 
   private:
     std::unique_ptr<Impl> impl_;
 };
+
+// z-slab decomposition of a 3D fast-precision hierarchy: the
+// fine level and level L-1 are sharded in z, levels <= L-2 are replicated.
+// Either K "virtual" slabs in one process on one device (transfers are
+// device copies -- the test mode) or one slab per process/GPU over NCCL.
+class SlabGroup {
+  public:
+    // ncclId == nullptr: `local` virtual slabs (rank 0, world = local).
+    SlabGroup(const Problem& prob, int local, int rank, int world, const void* ncclId);
+    ~SlabGroup();
+    SlabGroup(const SlabGroup&) = delete;
+    SlabGroup& operator=(const SlabGroup&) = delete;
+
+    SweepStats cycle(const Policy& pol, int n);
+    // Fine-level u of the planes owned by the local slabs, full-lattice layout
+    // (other planes left untouched in `host`).
+    void get_fine_u(double* host);
+    void time_cycles(const Policy& pol, int n0, int count, double* out4);
+    void e2e_step(const Policy& pol, int n, const double* hostChi, double* out3, long long* h2dBytes);
+    int owned_planes(int* z0, int* z1) const;  // of the first local slab
+
+    struct State;
+
+  private:
+    std::unique_ptr<State> st_;
+};
+
+std::vector<std::array<int, 8>> slab_plan(int levels, int world);
+
+// 128-byte NCCL unique id (dlopen'd libnccl); false if NCCL is unavailable.
+bool nccl_unique_id(void* out128);
 
 // Test hook: x / y elementwise on the device with the kernels' __divdc3
 // restatement (per-element divisor constants); host buffers.
