@@ -217,15 +217,9 @@ def main():
     if args.impl == "reference":
         return run_reference_arm(args, w)
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    dist = None
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
+    from paper_1508_03954_b200 import dist as D
+    ctx = D.init()
+    world, rank, local, dist = ctx.world, ctx.rank, ctx.local, ctx.dist
 
     import numpy as np
     import paper_1508_03954_b200 as T
@@ -236,11 +230,7 @@ def main():
                          ("replicas" if world > 1 else "single"))
     pol = T.Policy(kind=w["omega"], omega_s=w["omega_s"], bpx=(w["cycle"] == "td-bpx"))
     if mode == "slabs":
-        uid = T.nccl_unique_id() if rank == 0 else None
-        if dist:
-            box = [uid]
-            dist.broadcast_object_list(box, src=0)
-            uid = box[0]
+        uid = D.broadcast_bytes(ctx, T.nccl_unique_id() if rank == 0 else None)
         h = T.Slabs(w["level"], phi, chi="seeded", rhs_seed=RHS_SEED, rank=rank, world=world, nccl_id=uid,
                     device=local)
         h.time_cycles(pol, 1, args.warmup)
@@ -251,10 +241,7 @@ def main():
         h.time_cycles(pol, 1, args.warmup, flush_l2=False)
 
     def barrier():
-        if dist:
-            dist.barrier()
-            import torch
-            torch.cuda.synchronize()
+        D.barrier(ctx)
 
     barrier()
     with ClockSampler(local) as clk:
@@ -264,11 +251,7 @@ def main():
             out = h.time_cycles(pol, args.warmup + 1, args.steps, flush_l2=False)
     barrier()
     total_ms, fine_ms, launches_per_cycle = float(out[0]), float(out[1]), int(out[3])
-    if dist:
-        import torch
-        t = torch.tensor([total_ms], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = D.reduce_max(ctx, total_ms)
     dof = interior(w)
     ms_per_step = total_ms / args.steps
     copies = 1 if mode == "slabs" else world
@@ -305,11 +288,7 @@ def main():
         else:
             h.e2e_step(pol, args.warmup + args.steps + 1 + i, chi_host)
     e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if dist:
-        import torch
-        t = torch.tensor([e2e_s], device=f"cuda:{local}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = D.reduce_max(ctx, e2e_s)
     e2e = {"value": copies * dof / e2e_s, "unit": "DoF-updates/s", "h2d_bytes_per_step": int(h2d),
            "d2h_bytes_per_step": 24, "note": "per step: H2D of the nodal rhs (16 B/vertex, pinned; slabs: the "
            "rank's planes), device load vector, one cycle, D2H of the three residual norms (wall clock, max over ranks)"}
@@ -340,8 +319,7 @@ def main():
             "gpu_launches": launches_per_cycle * args.steps, "fine_pass_ms": fine_ms,
         }
         print(json.dumps(line))
-    if dist:
-        dist.destroy_process_group()
+    D.finalize(ctx)
     return 0
 
 
