@@ -69,6 +69,25 @@ def algorithmic_bytes(w, precision):
     return 80 * NL + 200 * coarse, 80 * NL
 
 
+def fine_kernel_label(w, precision):
+    if precision == "exact":
+        return "exact fine pass (k_topdown + k_residual_exact + k_restrict_exact)"
+    if w["dim"] == 3:
+        return "fused fine pass k_fused3 (TMA ring: top-down + residual + smooth + z/xy restriction)"
+    return "fine pass (k_topdown + k_residual + k_restrict)"
+
+
+def ncu_traffic(workload: str, precision: str, mode: str):
+    """DRAM bytes per launch of the fine-pass kernel from the committed ncu capture
+    (profiles/traffic.json, written from a `ncu` run of the same workload), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(f"{workload}/{precision}/{mode}")
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -265,9 +284,14 @@ def main():
     peak, peak_kind = peaks()
     achieved = B_fine / (fine_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": None, "kernel": "fine-level pass (K1 top-down + K2 residual/smooth/restrict), "
-                f"{B_fine / 1e9:.2f} GB algorithmic per cycle (80 B per fine vertex)",
+                "traffic": None, "kernel": fine_kernel_label(w, args.precision) +
+                f", {B_fine / 1e9:.2f} GB algorithmic per cycle (80 B per fine vertex)",
                 "peak_kind": peak_kind, "whole_cycle_GBps": B_total / (ms_per_step / 1e3) / 1e9}
+
+    tr = ncu_traffic(args.workload, args.precision, mode) if mode != "slabs" or world == 1 else None
+    if tr:
+        roofline["traffic"] = tr["bytes_per_launch"]
+        roofline["traffic_source"] = tr["source"]
 
     # e2e through the boundary: host rhs (pinned) -> device -> one cycle -> host norms
     n_lat = lattice(w["level"], w["dim"])
