@@ -24,6 +24,9 @@
  *   hb_sweeps = <k>             hierarchical-basis mask for sweeps 1..k, then off
  *   fmg_from = <level>          FMG unfolding from <level> up to `level`
  *   fmg_stage_cap = <n>         sweeps per FMG stage (default max_sweeps)
+ *   sphere_levels = <k>         static adaptive tree (BASELINE cfg4): `level` regular,
+ *                               then k levels refined where the parent cell's centre
+ *                               lies in |x - 1/2|^2 < 0.04; hanging vertices; exact only
  *   norms = device | host       host (exact precision only): |r| downloaded and
  *                               summed on the host in the reference's traversal
  *                               order, so CSV/log bytes match the reference
@@ -65,6 +68,9 @@ typedef struct tmg_problem {
     int precision;                 /* 0 exact, 1 fast */
     long long max_vertices;        /* 0: reference default 8388608 */
     int device;                    /* CUDA device ordinal */
+    int sphere_levels;             /* static adaptive tree: `levels` regular, then this many levels refined
+                                      where the parent cell's centre lies in |x - 1/2|^2 < 0.04 (BASELINE cfg4;
+                                      the cycle then runs the hanging-vertex events cycles.cpp:143-171, 305-321) */
 } tmg_problem;
 
 typedef struct tmg_policy {        /* OmegaPolicy, proj/include/treemg/cycles.hpp:17-24 */
@@ -102,6 +108,21 @@ treemg_status tmg_set_random_initial_guess(tmg_hierarchy* h, unsigned long long 
 treemg_status tmg_set_fine_rhs(tmg_hierarchy* h, const double* chi_nodal);
 /* FNV-1a over (re+0.0, im+0.0) bit patterns of a level field, lattice order */
 unsigned long long tmg_field_hash(tmg_hierarchy* h, int level, const char* field);
+/* adaptive trees: per lattice point of `level` the classification byte
+ * (1 exists, 2 hanging, 4 refined, 8 boundary, 16 cPoint; spacetree.cpp:438-489),
+ * succ (-1 absent) and per cell (lower corner) 1 exists | 2 refined; any
+ * pointer may be NULL.  TREEMG_E_CONFIG on a regular tree. */
+treemg_status tmg_get_flags(tmg_hierarchy* h, int level, unsigned char* flags, signed char* succ,
+                            unsigned char* cells);
+long long tmg_hanging_vertices(const tmg_hierarchy* h);
+/* Host-only (no GPU): the static sphere tree's structure as tmg_get_flags
+ * reports it, plus per vertex the corner index it has in the cell it is
+ * touched last in (0xFF absent) -- the restriction-order table of amr.hpp. */
+treemg_status tmg_sphere_tree(int dim, int base, int sphere_levels, int level, unsigned char* flags,
+                              signed char* succ, unsigned char* cells, unsigned char* finish_corner);
+/* Spacetree::interior_fine_vertex_count (spacetree.cpp:225-231): non-hanging,
+ * non-refined, interior vertices over all levels */
+long long tmg_leaf_vertices(const tmg_hierarchy* h);
 
 /* Timing: runs `count` cycles starting at sweep counter n0 with CUDA events on
  * the hierarchy's stream; out[0] = total ms, out[1] = ms in the fine-level

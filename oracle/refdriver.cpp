@@ -526,6 +526,47 @@ void refd_field(void* h, int level, const char* field, int channel, double* out,
     });
 }
 
+// As refd_field, hanging vertices included: mask 1 = regular, 2 = hanging.
+void refd_field_all(void* h, int level, const char* field, int channel, double* out, unsigned char* mask) {
+    auto* s = static_cast<Session*>(h);
+    const int p = s->tree->dim();
+    const std::size_t n = lattice_size(p, level);
+    std::fill(out, out + 2 * n, 0.0);
+    std::fill(mask, mask + n, 0);
+    s->tree->for_each_vertex_at(level, [&](const Index& idx, Vertex& v) {
+        const std::size_t f = lattice_flat(p, level, idx);
+        const Cplx z = field_of(v.ch[channel], field);
+        out[2 * f] = z.real();
+        out[2 * f + 1] = z.imag();
+        mask[f] = v.hanging ? 2 : 1;
+    });
+}
+
+// Classification per lattice point (1 exists, 2 hanging, 4 refined,
+// 8 boundary, 16 cPoint), succ (-1 absent) and per cell (lower corner)
+// 1 exists | 2 refined -- the encoding of tmg_get_flags.
+void refd_flags(void* h, int level, unsigned char* flags, signed char* succ, unsigned char* cells) {
+    auto* s = static_cast<Session*>(h);
+    const int p = s->tree->dim();
+    const std::size_t n = lattice_size(p, level);
+    std::fill(flags, flags + n, 0);
+    std::fill(succ, succ + n, static_cast<signed char>(-1));
+    std::fill(cells, cells + n, 0);
+    s->tree->for_each_vertex_at(level, [&](const Index& idx, Vertex& v) {
+        const std::size_t f = lattice_flat(p, level, idx);
+        flags[f] = static_cast<unsigned char>(1 | (v.hanging ? 2 : 0) | (v.refined ? 4 : 0) |
+                                              (v.onBoundary ? 8 : 0) | (v.cPoint ? 16 : 0));
+        succ[f] = static_cast<signed char>(v.succ);
+    });
+    s->tree->for_each_cell_at(level, [&](const Index& idx, Cell& c) {
+        cells[lattice_flat(p, level, idx)] = static_cast<unsigned char>(1 | (c.refined ? 2 : 0));
+    });
+}
+
+long long refd_interior_count(void* h) {
+    return static_cast<long long>(static_cast<Session*>(h)->tree->interior_fine_vertex_count());
+}
+
 // Mirrors proj/tests/test_util.hpp:48-65 (set_fine_interior_u): interior
 // lattice order of the finest level, re-injected upward, pipeline reset.
 void refd_set_fine_interior_u(void* h, const double* u) {

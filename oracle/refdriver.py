@@ -69,6 +69,10 @@ def lib():
         L.refd_lattice_size.argtypes = [vp, ip]
         L.refd_field.argtypes = [vp, ip, cp, ip, ctypes.POINTER(dp), ctypes.POINTER(ctypes.c_ubyte)]
         L.refd_set_fine_interior_u.argtypes = [vp, ctypes.POINTER(dp)]
+        L.refd_field_all.argtypes = [vp, ip, cp, ip, ctypes.POINTER(dp), ctypes.POINTER(ctypes.c_ubyte)]
+        L.refd_flags.argtypes = [vp, ip, vp, vp, vp]
+        L.refd_interior_count.restype = ctypes.c_longlong
+        L.refd_interior_count.argtypes = [vp]
         L.refd_field_hash.restype = ctypes.c_ulonglong
         L.refd_field_hash.argtypes = [vp, ip, cp, ip]
         L.refd_vertex_succ.restype = ip
@@ -180,6 +184,28 @@ class RefSession:
                           mask.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte)))
         z = out[0::2] + 1j * out[1::2]
         return (z, mask.astype(bool)) if with_mask else z
+
+    def field_all(self, level: int, name: str, channel: int = 0):
+        """Every vertex of the level incl. hanging ones; mask 1 regular, 2 hanging."""
+        n = self.L.refd_lattice_size(self.h, level)
+        out = np.zeros(2 * n)
+        mask = np.zeros(n, dtype=np.uint8)
+        self.L.refd_field_all(self.h, level, name.encode(), channel,
+                              out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                              mask.ctypes.data_as(ctypes.POINTER(ctypes.c_ubyte)))
+        return out[0::2] + 1j * out[1::2], mask
+
+    def flags(self, level: int):
+        n = self.L.refd_lattice_size(self.h, level)
+        fl = np.zeros(n, np.uint8)
+        sc = np.zeros(n, np.int8)
+        ce = np.zeros(n, np.uint8)
+        self.L.refd_flags(self.h, level, fl.ctypes.data_as(ctypes.c_void_p), sc.ctypes.data_as(ctypes.c_void_p),
+                          ce.ctypes.data_as(ctypes.c_void_p))
+        return fl, sc, ce
+
+    def interior_count(self) -> int:
+        return int(self.L.refd_interior_count(self.h))
 
     def field_hash(self, level: int, name: str, channel: int = 0) -> int:
         return int(self.L.refd_field_hash(self.h, level, name.encode(), channel))

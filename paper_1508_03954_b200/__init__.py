@@ -64,7 +64,8 @@ class _Problem(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int), ("levels", ctypes.c_int), ("ell_min", ctypes.c_int),
                 ("theta", ctypes.c_double), ("phi_re", ctypes.c_double), ("phi_im", ctypes.c_double),
                 ("chi_kind", ctypes.c_int), ("rhs_seed", ctypes.c_ulonglong), ("rhs_sphere", ctypes.c_int),
-                ("precision", ctypes.c_int), ("max_vertices", ctypes.c_longlong), ("device", ctypes.c_int)]
+                ("precision", ctypes.c_int), ("max_vertices", ctypes.c_longlong), ("device", ctypes.c_int),
+                ("sphere_levels", ctypes.c_int)]
 
 
 class _Policy(ctypes.Structure):
@@ -119,6 +120,14 @@ def lib():
         for n in ("tmg_td_add", "tmg_td_bpx"):
             getattr(L, n).restype = ip
             getattr(L, n).argtypes = [vp, ctypes.POINTER(_Policy), ip, ctypes.POINTER(_Stats)]
+        L.tmg_get_flags.restype = ip
+        L.tmg_get_flags.argtypes = [vp, ip, vp, vp, vp]
+        L.tmg_sphere_tree.restype = ip
+        L.tmg_sphere_tree.argtypes = [ip, ip, ip, ip, vp, vp, vp, vp]
+        L.tmg_hanging_vertices.restype = ctypes.c_longlong
+        L.tmg_hanging_vertices.argtypes = [vp]
+        L.tmg_leaf_vertices.restype = ctypes.c_longlong
+        L.tmg_leaf_vertices.argtypes = [vp]
         L.tmg_lattice_size.restype = ctypes.c_longlong
         L.tmg_lattice_size.argtypes = [vp, ip]
         L.tmg_get_field.restype = ip
@@ -245,17 +254,19 @@ class Hierarchy:
 
     def __init__(self, dim: int, levels: int, phi: complex = 0.0, theta_deg: float = 0.0, chi: str = "sin",
                  rhs_seed: int = 12345, rhs_sphere: bool = False, ell_min: int = 1, precision: str = "exact",
-                 max_vertices: int = 0, device: int = 0):
+                 max_vertices: int = 0, device: int = 0, sphere_levels: int = 0):
+        """levels: depth of the regular base tree; sphere_levels > 0 adds that many
+        levels refined inside |x - 1/2|^2 < 0.04 (static adaptive tree, cfg4)."""
         self.L = lib()
         prob = _Problem(dim, levels, ell_min, np.deg2rad(theta_deg) if theta_deg else 0.0,
                         complex(phi).real, complex(phi).imag, CHI_KINDS[chi], rhs_seed, int(rhs_sphere),
-                        1 if precision == "fast" else 0, max_vertices, device)
+                        1 if precision == "fast" else 0, max_vertices, device, sphere_levels)
         if theta_deg:
             prob.theta = theta_deg * np.pi / 180.0  # ProblemSpec::thetaGlobal = deg * M_PI / 180.0
         h = ctypes.c_void_p()
         _check(self.L.tmg_hierarchy_create(ctypes.byref(prob), ctypes.byref(h)))
         self.h = h
-        self.dim, self.levels = dim, levels
+        self.dim, self.levels = dim, levels + sphere_levels
 
     def close(self):
         if getattr(self, "h", None):
@@ -288,6 +299,26 @@ class Hierarchy:
         out = np.zeros(2 * n)
         _check(self.L.tmg_get_field(self.h, level, name.encode(), _pd(out)))
         return out[0::2] + 1j * out[1::2]
+
+    def flags(self, level: int):
+        """Adaptive trees: (flags, succ, cells) per lattice point of `level`
+        (flags 1 exists | 2 hanging | 4 refined | 8 boundary | 16 cPoint;
+        cells 1 exists | 2 refined, indexed by the lower corner)."""
+        n = self.lattice_size(level)
+        fl = np.zeros(n, np.uint8)
+        sc = np.zeros(n, np.int8)
+        ce = np.zeros(n, np.uint8)
+        _check(self.L.tmg_get_flags(self.h, level, fl.ctypes.data_as(ctypes.c_void_p),
+                                    sc.ctypes.data_as(ctypes.c_void_p), ce.ctypes.data_as(ctypes.c_void_p)))
+        return fl, sc, ce
+
+    @property
+    def hanging_vertices(self) -> int:
+        return int(self.L.tmg_hanging_vertices(self.h))
+
+    @property
+    def leaf_vertices(self) -> int:
+        return int(self.L.tmg_leaf_vertices(self.h))
 
     def set_field(self, level: int, name: str, values: np.ndarray):
         buf = np.ascontiguousarray(np.asarray(values, dtype=np.complex128)).view(np.float64).copy()
@@ -400,6 +431,17 @@ def device_divide(x: np.ndarray, y: np.ndarray) -> np.ndarray:
     out = np.zeros_like(x)
     _check(lib().tmg_test_divdc3(_pd(x.view(np.float64)), _pd(y.view(np.float64)), _pd(out.view(np.float64)), len(x)))
     return out
+
+
+def sphere_tree(dim: int, base: int, sphere_levels: int, level: int):
+    """Host-side structure of the static sphere tree (no GPU needed):
+    (flags, succ, cells, finish_corner) per lattice point of `level`."""
+    L = lib()
+    n = (3 ** level + 1) ** dim
+    fl, sc, ce, fc = np.zeros(n, np.uint8), np.zeros(n, np.int8), np.zeros(n, np.uint8), np.zeros(n, np.uint8)
+    ptr = lambda a: a.ctypes.data_as(ctypes.c_void_p)
+    _check(L.tmg_sphere_tree(dim, base, sphere_levels, level, ptr(fl), ptr(sc), ptr(ce), ptr(fc)))
+    return fl, sc, ce, fc
 
 
 def exported_symbols() -> List[str]:

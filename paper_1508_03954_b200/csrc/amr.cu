@@ -1,0 +1,1021 @@
+// Static adaptive spacetree cycle (exact precision).  See amr.hpp for the
+// layout and the ordering rules; the per-vertex semantics follow
+//   touch_first      proj/src/cycles.cpp:102-141
+//   create_hanging   proj/src/cycles.cpp:143-171
+//   enter_cell       proj/src/cycles.cpp:173-220 (residual, diag, leaf loads)
+//   touch_last       proj/src/cycles.cpp:243-303
+//   destroy_hanging  proj/src/cycles.cpp:305-321
+// and the classification of proj/src/spacetree.cpp:438-489.
+
+#include "amr.hpp"
+
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstring>
+
+#include "exact_ops.cuh"
+#include "lattice.cuh"
+
+namespace tmg {
+
+#define AMR_CUDA(call)                                                                          \
+    do {                                                                                        \
+        cudaError_t err_ = (call);                                                              \
+        if (err_ != cudaSuccess) {                                                              \
+            if (err_ == cudaErrorMemoryAllocation)                                              \
+                throw CapacityError(std::string("device memory exhausted: ") + #call);          \
+            throw CudaError(std::string("CUDA error ") + cudaGetErrorString(err_) + " at " + #call); \
+        }                                                                                       \
+    } while (0)
+
+namespace adev {
+
+using namespace dev;
+
+struct ALvl {
+    double2 *u, *sc, *sf, *si, *sinext, *chi, *uhat, *rhat, *r, *nodal;
+    const unsigned char* vflag;
+    const unsigned char* cflag;
+    const unsigned char* estar;
+    const signed char* succ;
+    int lo[3];
+    int n1[3];
+    unsigned n;
+    int m;
+    int level;
+};
+
+struct AResArgs {
+    ALvl lv, par;
+    LevelConst k;
+    double2 wTab[12];  // omega_unmasked(pol, succ, n) for succ = 0..11
+    int ellMin, bpx, hb;
+    double* partials;
+};
+
+template <int P>
+__device__ __forceinline__ void aunflat(unsigned f, const ALvl& c, int* g) {
+#pragma unroll
+    for (int d = 0; d < P; ++d) {
+        g[d] = c.lo[d] + static_cast<int>(f % static_cast<unsigned>(c.n1[d]));
+        f /= static_cast<unsigned>(c.n1[d]);
+    }
+}
+
+// box position of lattice point g, -1 outside the box
+template <int P>
+__device__ __forceinline__ int aflat(const ALvl& c, const int* g) {
+    int f = 0, s = 1;
+#pragma unroll
+    for (int d = 0; d < P; ++d) {
+        const int x = g[d] - c.lo[d];
+        if (x < 0 || x >= c.n1[d]) return -1;
+        f += x * s;
+        s *= c.n1[d];
+    }
+    return f;
+}
+
+// ---- top-down: touch_first / create_hanging ----------------------------------
+template <int P>
+__global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        const unsigned char vf = c.vflag[f];
+        if (!(vf & amr::kExists)) continue;
+        const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging;
+        if (c.level == 0) {  // cycles.cpp:128-133
+            double2 u = xadd(c.u[f], xadd(c.sc[f], c.sf ? c.sf[f] : cz()));
+            if (bnd) u = cz();
+            c.u[f] = u;
+            c.uhat[f] = cz();
+            if (c.sf) c.sf[f] = cz();
+            continue;
+        }
+        int g[P];
+        aunflat<P>(f, c, g);
+        int q[P], rel[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            q[d] = min(g[d] / 3, pr.m - 1);  // parent_stencil, spacetree.cpp:164-174
+            rel[d] = g[d] - 3 * q[d];
+        }
+        double2 cu[1 << P], cs[1 << P], ci[1 << P];
+#pragma unroll
+        for (int e = 0; e < (1 << P); ++e) {
+            int pi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
+            const int pf = aflat<P>(pr, pi);
+            const bool ok = pf >= 0 && (pr.vflag[pf] & amr::kExists);  // find_vertex: null -> 0
+            cu[e] = ok ? pr.u[pf] : cz();
+            cs[e] = ok ? pr.sc[pf] : cz();
+            ci[e] = (bpx && ok) ? pr.si[pf] : cz();
+        }
+        const double2 pu = prolong<P>(cu, rel);
+        const double2 ps = prolong<P>(cs, rel);
+        if (hang) {  // create_hanging
+            double2 u = pu, sc = ps;
+            if (bpx && !cp) sc = xsub(sc, prolong<P>(ci, rel));
+            if (bnd) {
+                u = cz();
+                sc = cz();
+            }
+            c.u[f] = u;
+            c.sc[f] = sc;
+            c.uhat[f] = cz();
+            if (c.sf) c.sf[f] = cz();
+            if (c.si) c.si[f] = cz();
+            if (c.sinext) c.sinext[f] = cz();
+            continue;
+        }
+        double2 sc = xadd(c.sc[f], ps);
+        if (bpx && !cp) sc = xsub(sc, prolong<P>(ci, rel));
+        const double2 sf = c.sf ? c.sf[f] : cz();
+        double2 u = xadd(c.u[f], xadd(sc, sf));
+        double2 uh = xsub(u, pu);
+        if (bnd) {
+            u = cz();
+            uh = cz();
+        }
+        c.u[f] = u;
+        c.sc[f] = sc;
+        c.uhat[f] = uh;
+        if (c.sf) c.sf[f] = cz();
+    }
+}
+
+// ---- chi: leaf loads and restriction in traversal time order ---------------
+template <int P>
+__global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, const double* __restrict__ w5,
+                                                 int restrictOn) {
+    constexpr int NC = 1 << P;
+    constexpr int NT = P == 1 ? 3 : P == 2 ? 9 : 27;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        if (!(c.vflag[f] & amr::kExists)) continue;
+        int g[P];
+        aunflat<P>(f, c, g);
+        const int pid = perm_id<P>(g);
+        double2 acc = cz();
+        for (int i = 0; i < NC; ++i) {
+            const int e = perm_cell(P, pid, i);  // cells around g in Morton order
+            int cell[P];
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                cell[d] = g[d] - 1 + ((e >> d) & 1);
+                ok &= (cell[d] >= 0) & (cell[d] <= c.m - 1);
+            }
+            if (!ok) continue;
+            const int cf = aflat<P>(c, cell);
+            if (cf < 0) continue;
+            const unsigned char cfl = c.cflag[cf];
+            if (!(cfl & amr::kCellExists)) continue;
+            const int a = (~e) & (NC - 1);  // corner of g in the cell
+            if (!(cfl & amr::kCellRefined)) {
+                // leaf: consistent-mass load on entering the cell (kernels.cpp:69-87)
+                double2 acc2 = cz();
+#pragma unroll
+                for (int bb = 0; bb < NC; ++bb) {
+                    int vb[P];
+#pragma unroll
+                    for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
+                    acc2 = xadd(acc2, xscale(k.M[a ^ bb], c.nodal[aflat<P>(c, vb)]));
+                }
+                acc = xadd(acc, xmul(k.massScale, acc2));
+            } else if (restrictOn) {
+                // refined: fine vertices finishing inside this cell, in child order,
+                // then by their corner index in the child (visit_cell's finish loop)
+                for (int t = 0; t < NT; ++t) {
+                    int j[P];
+                    int tt = t;
+#pragma unroll
+                    for (int d = 0; d < P; ++d) {
+                        j[d] = tt % 3;
+                        tt /= 3;
+                    }
+                    for (int ec = 0; ec < NC; ++ec) {
+                        int v[P];
+                        int code = 0, mul = 1;
+                        bool in = true;
+#pragma unroll
+                        for (int d = 0; d < P; ++d) {
+                            v[d] = 3 * cell[d] + j[d] + ((ec >> d) & 1);
+                            const int off = v[d] - 3 * g[d];
+                            in &= (off >= -2) & (off <= 2) & (v[d] >= 1) & (v[d] <= fl.m - 1);
+                            code += (off + 2) * mul;
+                            mul *= 5;
+                        }
+                        if (!in) continue;
+                        const int vf = aflat<P>(fl, v);
+                        if (vf < 0 || fl.estar[vf] != ec) continue;
+                        acc = xadd(acc, xscale(w5[code], fl.rhat[vf]));
+                    }
+                }
+            }
+        }
+        c.chi[f] = acc;
+    }
+}
+
+// sum_b A(a, b) x_b over the corners of one cell, b ascending (kernels.cpp:39-47)
+template <int P>
+__device__ __forceinline__ double2 cell_apply(const double2* __restrict__ x, const ALvl& c, const int* cell, int a,
+                                              const double2 (&A)[8]) {
+    double2 s = cz();
+#pragma unroll
+    for (int bb = 0; bb < (1 << P); ++bb) {
+        int vb[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
+        const double2 prod = xmul(A[a ^ bb], x[aflat<P>(c, vb)]);
+        s = bb == 0 ? prod : xadd(s, prod);
+    }
+    return s;
+}
+
+// ---- residual + touch_last / destroy_hanging --------------------------------
+template <int P>
+__global__ void __launch_bounds__(256) k_amr_residual(AResArgs a) {
+    constexpr int NC = 1 << P;
+    const ALvl& c = a.lv;
+    double nmax = 0.0, nsum = 0.0;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        const unsigned char vf = c.vflag[f];
+        if (!(vf & amr::kExists)) continue;
+        const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging,
+                   refined = vf & amr::kRefined;
+        int g[P];
+        aunflat<P>(f, c, g);
+        const int pid = perm_id<P>(g);
+        double2 r = cz(), rh = cz();
+        bool first = true;
+        for (int i = 0; i < NC; ++i) {
+            const int e = perm_cell(P, pid, i);
+            int cell[P];
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                cell[d] = g[d] - 1 + ((e >> d) & 1);
+                ok &= (cell[d] >= 0) & (cell[d] <= c.m - 1);
+            }
+            if (!ok) continue;
+            const int cf = aflat<P>(c, cell);
+            if (cf < 0 || !(c.cflag[cf] & amr::kCellExists)) continue;
+            const int ca = (~e) & (NC - 1);
+            const double2 sr = cell_apply<P>(c.u, c, cell, ca, a.k.A);
+            const double2 sh = cell_apply<P>(c.uhat, c, cell, ca, a.k.A);
+            if (first) {
+                r = xneg(sr);
+                rh = xneg(sh);
+                first = false;
+            } else {
+                r = xsub(r, sr);
+                rh = xsub(rh, sh);
+            }
+        }
+        const double2 chi = c.chi[f];
+        if (hang) {  // destroy_hanging: only r-hat (plus load) goes down
+            double2 rhat = rh;
+            if (c.level > a.ellMin) rhat = bnd ? cz() : xadd(chi, rh);
+            c.rhat[f] = rhat;
+            if (c.r) c.r[f] = r;
+            continue;
+        }
+        if (bnd) {  // finish_vertex, kernels.cpp:89-100
+            r = cz();
+            rh = cz();
+        } else {
+            r = xadd(chi, r);
+            rh = xadd(chi, rh);
+        }
+        if (c.si) {
+            c.si[f] = c.sinext[f];
+            c.sinext[f] = cz();
+        }
+        if (!refined && !bnd) {
+            const double m2 = r.x * r.x + r.y * r.y;
+            nmax = fmax(nmax, m2);
+            nsum += m2;
+        }
+        if (c.r) c.r[f] = r;
+        c.rhat[f] = rh;
+        if (c.level < a.ellMin) {
+            c.sc[f] = cz();
+            continue;
+        }
+        const double2 smooth = bnd ? cz() : divdc3(r.x, r.y, a.k.div);
+        const double2 wRaw = a.wTab[c.succ[f]];
+        double2 sc;
+        if (a.bpx) {
+            sc = cp ? cz() : xmul(wRaw, smooth);
+        } else {
+            const bool wz = (a.hb && cp) || xzero(wRaw);
+            sc = wz ? cz() : xmul(wRaw, smooth);
+        }
+        c.sc[f] = sc;
+        if (c.level > a.ellMin && cp) {
+            int wi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) wi[d] = g[d] / 3;
+            const int wf = aflat<P>(a.par, wi);
+            if (wf >= 0 && (a.par.vflag[wf] & amr::kExists)) {
+                const double2 sf = c.sf ? c.sf[f] : cz();
+                a.par.sf[wf] = xadd(sf, sc);
+                if (a.bpx) a.par.sinext[wf] = xmul(wRaw, smooth);
+            }
+        }
+    }
+    block_norms(nmax, nsum, a.partials);
+}
+
+// per-level (max, sum) from the block partials of every level
+__global__ void k_amr_norm_final(const double* __restrict__ partials, const int* __restrict__ offs, int nlev,
+                                 double* out) {
+    __shared__ double smax[1024], ssum[1024];
+    for (int l = 0; l < nlev; ++l) {
+        double mx = 0.0, sm = 0.0;
+        for (int i = offs[l] + threadIdx.x; i < offs[l + 1]; i += blockDim.x) {
+            mx = fmax(mx, partials[2 * i]);
+            sm += partials[2 * i + 1];
+        }
+        smax[threadIdx.x] = mx;
+        ssum[threadIdx.x] = sm;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s) {
+                smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+                ssum[threadIdx.x] += ssum[threadIdx.x + s];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            out[2 * l] = smax[0];
+            out[2 * l + 1] = ssum[0];
+        }
+        __syncthreads();
+    }
+}
+
+// ---- setup -------------------------------------------------------------------
+template <int P>
+__global__ void k_amr_seeded(ALvl c, unsigned long long seed, long long scale, long long mkey, int sphere) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        if (!(c.vflag[f] & amr::kExists)) continue;
+        int g[P];
+        aunflat<P>(f, c, g);
+        unsigned long long key = 0;
+        long long s2 = 0;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            const long long fi = static_cast<long long>(g[d]) * scale;
+            key |= static_cast<unsigned long long>(static_cast<unsigned short>(fi)) << (16 * d);
+            const long long t = 2 * fi - mkey;
+            s2 += t * t;
+        }
+        if (sphere && !(25 * s2 < 4 * mkey * mkey)) {
+            c.nodal[f] = cz();
+            continue;
+        }
+        const unsigned long long s = seed ^ key;
+        c.nodal[f] = make_double2(unit_rand(s), unit_rand(s ^ 0x5bf03635ull));
+    }
+}
+
+// set_random_initial_guess, cycles.cpp:812-840: leaves random, boundary 0
+template <int P>
+__global__ void k_amr_random(ALvl c, unsigned long long seed) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        const unsigned char vf = c.vflag[f];
+        if (!(vf & amr::kExists) || (vf & amr::kHanging)) continue;
+        if (vf & amr::kBoundary) {
+            c.u[f] = cz();
+            continue;
+        }
+        if (vf & amr::kRefined) continue;  // injected from the finer level afterwards
+        int g[P];
+        aunflat<P>(f, c, g);
+        unsigned long long key = 0;
+#pragma unroll
+        for (int d = 0; d < P; ++d) key |= static_cast<unsigned long long>(static_cast<unsigned short>(g[d])) << (16 * d);
+        const unsigned long long base = seed ^ (static_cast<unsigned long long>(c.level) << 56) ^ key;
+        c.u[f] = make_double2(unit_rand(base), unit_rand(base ^ 0x5bf03635ull));
+    }
+}
+
+template <int P>
+__global__ void k_amr_inject(ALvl c, ALvl fine) {
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        const unsigned char vf = c.vflag[f];
+        if (!(vf & amr::kExists) || (vf & (amr::kHanging | amr::kBoundary)) || !(vf & amr::kRefined)) continue;
+        int g[P];
+        aunflat<P>(f, c, g);
+        int fi[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) fi[d] = 3 * g[d];
+        const int ff = aflat<P>(fine, fi);
+        c.u[f] = (ff >= 0 && (fine.vflag[ff] & amr::kExists)) ? fine.u[ff] : cz();
+    }
+}
+
+}  // namespace adev
+
+// ============================================================================
+// Host: tree structure
+// ============================================================================
+
+namespace amr {
+namespace {
+
+int pow3(int l) {
+    int r = 1;
+    for (int i = 0; i < l; ++i) r *= 3;
+    return r;
+}
+
+int tz3h(int x) {
+    if (x == 0) return 31;
+    int t = 0;
+    while (x % 3 == 0) {
+        x /= 3;
+        ++t;
+    }
+    return t;
+}
+
+// host twin of dev::perm_id (exact_ops.cuh)
+int perm_id_host(int p, const int* idx) {
+    if (p == 1) return 0;
+    if (p == 2) return tz3h(idx[1]) >= tz3h(idx[0]) ? 0 : 1;
+    const int k0 = tz3h(idx[0]) * 4 + 0, k1 = tz3h(idx[1]) * 4 + 1, k2 = tz3h(idx[2]) * 4 + 2;
+    int pr0, pr1, pr2;
+    if (k0 > k1 && k0 > k2) {
+        pr0 = 0;
+        pr1 = k1 > k2 ? 1 : 2;
+        pr2 = k1 > k2 ? 2 : 1;
+    } else if (k1 > k2) {
+        pr0 = 1;
+        pr1 = k0 > k2 ? 0 : 2;
+        pr2 = k0 > k2 ? 2 : 0;
+    } else {
+        pr0 = 2;
+        pr1 = k0 > k1 ? 0 : 1;
+        pr2 = k0 > k1 ? 1 : 0;
+    }
+    return 2 * pr0 + (pr1 > pr2 ? 1 : 0);
+}
+
+// cell centre in |x - 1/2|^2 < 0.04 (oracle/refdriver.cpp cell_centre_in_sphere)
+bool centre_in_sphere(int p, int level, const int* c) {
+    const long long m = pow3(level);
+    long long s = 0;
+    for (int d = 0; d < p; ++d) {
+        const long long t = 2LL * c[d] + 1 - m;
+        s += t * t;
+    }
+    return 25 * s < 4 * m * m;
+}
+
+long long box_flat(const HostLevel& h, int p, const int* g) {
+    long long f = 0, s = 1;
+    for (int d = 0; d < p; ++d) {
+        const int x = g[d] - h.lo[d];
+        if (x < 0 || x >= h.n1[d]) return -1;
+        f += static_cast<long long>(x) * s;
+        s *= h.n1[d];
+    }
+    return f;
+}
+
+void box_unflat(const HostLevel& h, int p, long long f, int* g) {
+    for (int d = 0; d < p; ++d) {
+        g[d] = h.lo[d] + static_cast<int>(f % h.n1[d]);
+        f /= h.n1[d];
+    }
+}
+
+}  // namespace
+
+std::vector<HostLevel> build_sphere_tree(int p, int base, int L) {
+    std::vector<HostLevel> lv(static_cast<size_t>(L) + 1);
+    for (int l = 0; l <= L; ++l) {
+        HostLevel& h = lv[l];
+        h.level = l;
+        h.m = pow3(l);
+        if (l <= base) {
+            for (int d = 0; d < p; ++d) {
+                h.lo[d] = 0;
+                h.n1[d] = h.m + 1;
+            }
+        } else {
+            const HostLevel& pr = lv[l - 1];
+            int mn[3] = {INT_MAX, INT_MAX, INT_MAX}, mx[3] = {-1, -1, -1};
+            int g[3] = {0, 0, 0};
+            for (long long f = 0; f < pr.n; ++f) {
+                if (!(pr.cflag[f] & kCellRefined)) continue;
+                box_unflat(pr, p, f, g);
+                for (int d = 0; d < p; ++d) {
+                    mn[d] = std::min(mn[d], g[d]);
+                    mx[d] = std::max(mx[d], g[d]);
+                }
+            }
+            if (mx[0] < 0) throw ConfigError("sphere refinement: no cell to refine at level " + std::to_string(l - 1));
+            for (int d = 0; d < p; ++d) {
+                h.lo[d] = 3 * mn[d];
+                h.n1[d] = 3 * (mx[d] + 1) - h.lo[d] + 1;
+            }
+        }
+        h.n = 1;
+        for (int d = 0; d < p; ++d) h.n *= h.n1[d];
+        if (h.n >= (1LL << 31)) throw CapacityError("adaptive level box exceeds 2^31 vertices");
+        h.cflag.assign(static_cast<size_t>(h.n), 0);
+        int g[3] = {0, 0, 0};
+        for (long long f = 0; f < h.n; ++f) {
+            box_unflat(h, p, f, g);
+            bool inDomain = true;
+            for (int d = 0; d < p; ++d) inDomain &= g[d] <= h.m - 1;
+            if (!inDomain) continue;
+            bool exists = true;
+            if (l > base) {
+                int pc[3] = {0, 0, 0};
+                for (int d = 0; d < p; ++d) pc[d] = g[d] / 3;
+                const HostLevel& pr = lv[l - 1];
+                const long long pf = box_flat(pr, p, pc);
+                exists = pf >= 0 && (pr.cflag[pf] & kCellRefined);
+            }
+            if (!exists) continue;
+            const bool refined = l < L && (l < base || centre_in_sphere(p, l, g));
+            h.cflag[f] = static_cast<unsigned char>(kCellExists | (refined ? kCellRefined : 0));
+        }
+        // vertices: classification (spacetree.cpp:438-466) + finish corner
+        h.vflag.assign(static_cast<size_t>(h.n), 0);
+        h.estar.assign(static_cast<size_t>(h.n), 0xFF);
+        h.succ.assign(static_cast<size_t>(h.n), 0);
+        const int nc = 1 << p;
+        for (long long f = 0; f < h.n; ++f) {
+            box_unflat(h, p, f, g);
+            int total = 0, have = 0, refAdj = 0;
+            bool cellOk[8] = {false, false, false, false, false, false, false, false};
+            for (int e = 0; e < nc; ++e) {  // e: cell = g - 1 + e (exact_ops.cuh convention)
+                int c[3] = {0, 0, 0};
+                bool in = true;
+                for (int d = 0; d < p; ++d) {
+                    c[d] = g[d] - 1 + ((e >> d) & 1);
+                    in &= c[d] >= 0 && c[d] <= h.m - 1;
+                }
+                if (!in) continue;
+                ++total;
+                const long long cf = box_flat(h, p, c);
+                if (cf < 0 || !(h.cflag[cf] & kCellExists)) continue;
+                ++have;
+                cellOk[e] = true;
+                if (h.cflag[cf] & kCellRefined) ++refAdj;
+            }
+            if (have == 0) continue;
+            unsigned char fl = kExists;
+            const bool hanging = have < total;
+            if (hanging) fl |= kHanging;
+            if (!hanging && refAdj == have) fl |= kRefined;
+            bool bnd = false, cp = l > 0;
+            for (int d = 0; d < p; ++d) {
+                bnd |= g[d] == 0 || g[d] == h.m;
+                cp &= g[d] % 3 == 0;
+            }
+            if (bnd) fl |= kBoundary;
+            if (cp) fl |= kCPoint;
+            h.vflag[f] = fl;
+            // the latest existing cell around g in traversal (Morton) order
+            const int pid = perm_id_host(p, g);
+            for (int i = nc - 1; i >= 0; --i) {
+                const int e = dev::perm_cell(p, pid, i);
+                if (cellOk[e]) {
+                    h.estar[f] = static_cast<unsigned char>((~e) & (nc - 1));
+                    break;
+                }
+            }
+        }
+    }
+    // succ, finest level first (Spacetree::classify, spacetree.cpp:491-494)
+    for (int l = L; l >= 0; --l) {
+        HostLevel& h = lv[l];
+        int g[3] = {0, 0, 0};
+        for (long long f = 0; f < h.n; ++f) {
+            if (!(h.vflag[f] & kExists) || !(h.vflag[f] & kRefined) || l == L) continue;
+            box_unflat(h, p, f, g);
+            const HostLevel& fh = lv[l + 1];
+            const int mf = fh.m;
+            int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+            for (int d = 0; d < p; ++d) {
+                lo[d] = std::max(0, 3 * g[d] - 3);
+                hi[d] = std::min(mf, 3 * g[d] + 3);
+            }
+            int minSucc = INT_MAX;
+            int w[3] = {0, 0, 0};
+            for (w[2] = p > 2 ? lo[2] : 0; w[2] <= (p > 2 ? hi[2] : 0); ++w[2])
+                for (w[1] = p > 1 ? lo[1] : 0; w[1] <= (p > 1 ? hi[1] : 0); ++w[1])
+                    for (w[0] = lo[0]; w[0] <= hi[0]; ++w[0]) {
+                        const long long wf = box_flat(fh, p, w);
+                        if (wf < 0 || !(fh.vflag[wf] & kExists)) continue;
+                        const int s = (fh.vflag[wf] & kHanging) ? 0 : fh.succ[wf];
+                        minSucc = std::min(minSucc, s);
+                    }
+            h.succ[f] = static_cast<signed char>(minSucc == INT_MAX ? 0 : 1 + minSucc);
+        }
+    }
+    return lv;
+}
+
+}  // namespace amr
+
+// ============================================================================
+// Host: device state and cycle
+// ============================================================================
+
+struct AmrTree::Dev {
+    std::vector<dev::LevelConst> kc;
+    std::vector<adev::ALvl> lv;
+    std::vector<void*> allocations;
+    std::vector<int> normOffs;  // block partial offsets per level
+    double* partials = nullptr;
+    int* dOffs = nullptr;
+    double* dNorm = nullptr;
+    double* hNorm = nullptr;  // pinned, 2 (L+1)
+    double* weights = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+
+    ~Dev() {
+        for (void* p : allocations) cudaFree(p);
+        if (hNorm) cudaFreeHost(hNorm);
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
+    template <class T>
+    T* alloc(size_t count, cudaStream_t s) {
+        void* ptr = nullptr;
+        AMR_CUDA(cudaMalloc(&ptr, std::max<size_t>(1, count) * sizeof(T)));
+        allocations.push_back(ptr);
+        AMR_CUDA(cudaMemsetAsync(ptr, 0, std::max<size_t>(1, count) * sizeof(T), s));
+        return static_cast<T*>(ptr);
+    }
+};
+
+namespace {
+int blocks_for_n(long long n, int smCount) {
+    const long long need = (n + 255) / 256;
+    return static_cast<int>(std::max<long long>(1, std::min<long long>(need, 8LL * smCount)));
+}
+}  // namespace
+
+AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, const std::vector<Cplx>& diagInterior,
+                 cudaStream_t stream, int smCount)
+    : prob_(prob), p_(prob.dim), L_(prob.levels), base_(prob.levels - prob.sphereLevels), stream_(stream),
+      smCount_(smCount), dev_(new Dev()), diag_(diagInterior) {
+    dev_->kc = kc;
+    if (prob.fast) throw UnsupportedConfigError("adaptive trees run in precision = exact only");
+    if (base_ < 1) throw ConfigError("sphere refinement needs a base level >= 1");
+    host_ = amr::build_sphere_tree(p_, base_, L_);
+    for (const amr::HostLevel& h : host_)
+        for (long long f = 0; f < h.n; ++f) {
+            const unsigned char v = h.vflag[f];
+            if (!(v & amr::kExists)) continue;
+            ++existingCount_;
+            if (v & amr::kHanging) ++hangingCount_;
+            else if (!(v & amr::kRefined) && !(v & amr::kBoundary)) ++leafCount_;
+        }
+    if (static_cast<std::size_t>(existingCount_) > prob.maxVertices)
+        throw CapacityError("vertex capacity exceeded (" + std::to_string(prob.maxVertices) + ")");
+    Dev& D = *dev_;
+    D.lv.resize(L_ + 1);
+    const char* dbg = std::getenv("TMG_DEBUG_R");
+    const bool debugR = dbg && dbg[0] == '1';
+    int blocksTotal = 0;
+    D.normOffs.push_back(0);
+    for (int l = 0; l <= L_; ++l) {
+        const amr::HostLevel& h = host_[l];
+        adev::ALvl& a = D.lv[l];
+        a = adev::ALvl{};
+        a.level = l;
+        a.m = h.m;
+        for (int d = 0; d < 3; ++d) {
+            a.lo[d] = h.lo[d];
+            a.n1[d] = h.n1[d];
+        }
+        a.n = static_cast<unsigned>(h.n);
+        const size_t n = static_cast<size_t>(h.n);
+        a.u = D.alloc<double2>(n, stream_);
+        a.sc = D.alloc<double2>(n, stream_);
+        a.chi = D.alloc<double2>(n, stream_);
+        a.uhat = D.alloc<double2>(n, stream_);
+        a.rhat = D.alloc<double2>(n, stream_);
+        if (l < L_) {
+            a.sf = D.alloc<double2>(n, stream_);
+            a.si = D.alloc<double2>(n, stream_);
+            a.sinext = D.alloc<double2>(n, stream_);
+        }
+        if (debugR) a.r = D.alloc<double2>(n, stream_);
+        if (l >= base_) a.nodal = D.alloc<double2>(n, stream_);
+        auto* vflag = D.alloc<unsigned char>(n, stream_);
+        auto* cflag = D.alloc<unsigned char>(n, stream_);
+        auto* estar = D.alloc<unsigned char>(n, stream_);
+        auto* succ = D.alloc<signed char>(n, stream_);
+        AMR_CUDA(cudaMemcpyAsync(vflag, h.vflag.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(cflag, h.cflag.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(estar, h.estar.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(succ, h.succ.data(), n, cudaMemcpyHostToDevice, stream_));
+        a.vflag = vflag;
+        a.cflag = cflag;
+        a.estar = estar;
+        a.succ = succ;
+        blocksTotal += blocks_for_n(h.n, smCount_);
+        D.normOffs.push_back(blocksTotal);
+    }
+    D.partials = D.alloc<double>(2 * static_cast<size_t>(blocksTotal), stream_);
+    D.dOffs = D.alloc<int>(D.normOffs.size(), stream_);
+    AMR_CUDA(cudaMemcpyAsync(D.dOffs, D.normOffs.data(), D.normOffs.size() * sizeof(int), cudaMemcpyHostToDevice,
+                             stream_));
+    D.dNorm = D.alloc<double>(2 * (L_ + 1), stream_);
+    AMR_CUDA(cudaMallocHost(&D.hNorm, 2 * (L_ + 1) * sizeof(double)));
+    {
+        // restriction_weight (cycles.cpp:46-50): per-axis 1/3, 2/3, 1 folded in axis order
+        const int NT = p_ == 1 ? 5 : p_ == 2 ? 25 : 125;
+        const double k1d[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+        std::vector<double> w(NT);
+        for (int code = 0; code < NT; ++code) {
+            double wt = 1.0;
+            int cc = code;
+            for (int d = 0; d < p_; ++d) {
+                wt *= k1d[cc % 5];
+                cc /= 5;
+            }
+            w[code] = wt;
+        }
+        D.weights = D.alloc<double>(NT, stream_);
+        AMR_CUDA(cudaMemcpyAsync(D.weights, w.data(), NT * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    }
+    AMR_CUDA(cudaEventCreate(&D.ev0));
+    AMR_CUDA(cudaEventCreate(&D.ev1));
+    if (p_ == 1) build_rhs<1>();
+    else if (p_ == 2) build_rhs<2>();
+    else build_rhs<3>();
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+}
+
+AmrTree::~AmrTree() = default;
+
+template <int P>
+void AmrTree::build_rhs() {
+    Dev& D = *dev_;
+    for (int l = base_; l <= L_; ++l) {
+        adev::ALvl& a = D.lv[l];
+        const amr::HostLevel& h = host_[l];
+        if (prob_.chi == ChiKind::Seeded) {
+            const int key = prob_.rhsLattice >= 0 ? prob_.rhsLattice : L_;
+            long long scale = 1, mkey = 1;
+            for (int i = 0; i < key - l; ++i) scale *= 3;
+            for (int i = 0; i < key; ++i) mkey *= 3;
+            adev::k_amr_seeded<P><<<blocks_for_n(h.n, smCount_), 256, 0, stream_>>>(a, prob_.rhsSeed, scale, mkey,
+                                                                                    prob_.rhsSphere ? 1 : 0);
+            AMR_CUDA(cudaGetLastError());
+            continue;
+        }
+        // chi_at at x = index * 3^-l (kernels.cpp:72-77, problems.cpp:55-68), glibc sin
+        std::vector<double2> nod(static_cast<size_t>(h.n), make_double2(0.0, 0.0));
+        const double hh = std::pow(3.0, -l);
+        int g[3] = {0, 0, 0};
+        for (long long f = 0; f < h.n; ++f) {
+            if (!(h.vflag[f] & amr::kExists)) continue;
+            long long ff = f;
+            double x[3];
+            for (int d = 0; d < p_; ++d) {
+                g[d] = h.lo[d] + static_cast<int>(ff % h.n1[d]);
+                ff /= h.n1[d];
+                x[d] = g[d] * hh;
+            }
+            double v = 0.0;
+            if (prob_.chi == ChiKind::SinProduct) {
+                v = static_cast<double>(p_) * M_PI * M_PI;
+                for (int d = 0; d < p_; ++d) v *= std::sin(M_PI * x[d]);
+            } else if (prob_.chi == ChiKind::BallIndicator) {
+                double r2 = 0.0;
+                for (int d = 0; d < p_; ++d) r2 += (x[d] - 0.5) * (x[d] - 0.5);
+                v = r2 < 0.01 ? 1.0 : 0.0;
+            }
+            nod[f] = make_double2(v, 0.0);
+        }
+        AMR_CUDA(cudaMemcpyAsync(a.nodal, nod.data(), nod.size() * sizeof(double2), cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaStreamSynchronize(stream_));
+    }
+}
+
+template <int P>
+void AmrTree::run_cycle(const Policy& pol, int n) {
+    Dev& D = *dev_;
+    const int bpx = pol.bpx ? 1 : 0;
+    for (int l = 0; l <= L_; ++l) {
+        const adev::ALvl& pr = l > 0 ? D.lv[l - 1] : D.lv[0];
+        adev::k_amr_topdown<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
+    }
+    adev::AResArgs a{};
+    a.ellMin = prob_.ellMin;
+    a.bpx = bpx;
+    a.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+    for (int s = 0; s < 12; ++s) {
+        const Cplx w = omega_unmasked(pol, s, n);
+        a.wTab[s] = make_double2(w.real(), w.imag());
+    }
+    for (int l = L_; l >= 0; --l) {
+        const int nb = blocks_for_n(D.lv[l].n, smCount_);
+        const adev::ALvl& fine = l < L_ ? D.lv[l + 1] : D.lv[l];
+        adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.kc[l], D.weights,
+                                                     (l < L_ && l + 1 > prob_.ellMin) ? 1 : 0);
+        a.lv = D.lv[l];
+        a.par = l > 0 ? D.lv[l - 1] : D.lv[0];
+        a.k = D.kc[l];
+        a.partials = D.partials + 2 * static_cast<size_t>(D.normOffs[l]);
+        adev::k_amr_residual<P><<<nb, 256, 0, stream_>>>(a);
+    }
+    adev::k_amr_norm_final<<<1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
+    AMR_CUDA(cudaGetLastError());
+}
+
+SweepStats AmrTree::cycle(const Policy& pol, int n) {
+    for (int l = std::max(1, prob_.ellMin); l <= L_; ++l)
+        if (std::abs(diag_[l]) < 1e-300) throw SingularDiagonalError("vanishing operator diagonal (phi*h^2 resonance?)");
+    if (p_ == 1) run_cycle<1>(pol, n);
+    else if (p_ == 2) run_cycle<2>(pol, n);
+    else run_cycle<3>(pol, n);
+    Dev& D = *dev_;
+    AMR_CUDA(cudaMemcpyAsync(D.hNorm, D.dNorm, 2 * (L_ + 1) * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+    double mx = 0.0, eu = 0.0, hn = 0.0;
+    for (int l = 0; l <= L_; ++l) {
+        const double hp = std::pow(std::pow(3.0, -l), p_);
+        mx = std::max(mx, D.hNorm[2 * l]);
+        eu += D.hNorm[2 * l + 1];
+        hn += hp * D.hNorm[2 * l + 1];
+    }
+    SweepStats st;
+    st.maxNorm = std::sqrt(mx);
+    st.euclidNorm = std::sqrt(eu);
+    st.hNorm = std::sqrt(hn);
+    st.updatedFineVertices = leafCount_;
+    return st;
+}
+
+namespace {
+double2* afield(const adev::ALvl& v, const std::string& f) {
+    if (f == "u") return v.u;
+    if (f == "sc") return v.sc;
+    if (f == "sf") return v.sf;
+    if (f == "si") return v.si;
+    if (f == "sinext") return v.sinext;
+    if (f == "chi") return v.chi;
+    if (f == "uhat") return v.uhat;
+    if (f == "rhat") return v.rhat;
+    if (f == "r") return v.r;
+    return nullptr;
+}
+
+long long full_flat(int p, int m, const int* g) {
+    long long f = 0, s = 1;
+    for (int d = 0; d < p; ++d) {
+        f += static_cast<long long>(g[d]) * s;
+        s *= m + 1;
+    }
+    return f;
+}
+}  // namespace
+
+void AmrTree::get_field(int level, const std::string& name, double* host) const {
+    if (level < 0 || level > L_) throw ConfigError("get_field: level out of range");
+    // "<field>@all": hanging vertices included (the harness's refd_field_all)
+    const bool all = name.size() > 4 && name.compare(name.size() - 4, 4, "@all") == 0;
+    const std::string field = all ? name.substr(0, name.size() - 4) : name;
+    const amr::HostLevel& h = host_[level];
+    long long full = 1;
+    for (int d = 0; d < p_; ++d) full *= h.m + 1;
+    std::fill(host, host + 2 * full, 0.0);
+    const double2* ptr = afield(dev_->lv[level], field);
+    if (!ptr) {
+        static const char* known[] = {"sf", "si", "sinext", "r"};
+        for (const char* k : known)
+            if (field == k) return;
+        throw ConfigError("get_field: unknown field '" + field + "'");
+    }
+    std::vector<double2> box(static_cast<size_t>(h.n));
+    AMR_CUDA(cudaMemcpyAsync(box.data(), ptr, box.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+    int g[3] = {0, 0, 0};
+    for (long long f = 0; f < h.n; ++f) {
+        const unsigned char v = h.vflag[f];
+        if (!(v & amr::kExists) || ((v & amr::kHanging) && !all)) continue;
+        amr::box_unflat(h, p_, f, g);
+        const long long ff = full_flat(p_, h.m, g);
+        host[2 * ff] = box[f].x;
+        host[2 * ff + 1] = box[f].y;
+    }
+}
+
+void AmrTree::get_flags(int level, unsigned char* flags, signed char* succ, unsigned char* cells) const {
+    if (level < 0 || level > L_) throw ConfigError("get_flags: level out of range");
+    const amr::HostLevel& h = host_[level];
+    long long full = 1;
+    for (int d = 0; d < p_; ++d) full *= h.m + 1;
+    if (flags) std::fill(flags, flags + full, 0);
+    if (succ) std::fill(succ, succ + full, static_cast<signed char>(-1));
+    if (cells) std::fill(cells, cells + full, 0);
+    int g[3] = {0, 0, 0};
+    for (long long f = 0; f < h.n; ++f) {
+        if (!(h.vflag[f] & amr::kExists) && !h.cflag[f]) continue;
+        amr::box_unflat(h, p_, f, g);
+        const long long ff = full_flat(p_, h.m, g);
+        if (cells) cells[ff] = h.cflag[f];
+        if (!(h.vflag[f] & amr::kExists)) continue;
+        if (flags) flags[ff] = h.vflag[f];
+        if (succ) succ[ff] = h.succ[f];
+    }
+}
+
+std::uint64_t AmrTree::field_hash(int level, const std::string& field) const {
+    // FNV-1a over the full-lattice layout of get_field, streamed plane by plane
+    if (level < 0 || level > L_) throw ConfigError("field_hash: level out of range");
+    const amr::HostLevel& h = host_[level];
+    const double2* ptr = afield(dev_->lv[level], field);
+    std::vector<double2> box(static_cast<size_t>(h.n), make_double2(0.0, 0.0));
+    if (ptr) {
+        AMR_CUDA(cudaMemcpyAsync(box.data(), ptr, box.size() * sizeof(double2), cudaMemcpyDeviceToHost, stream_));
+        AMR_CUDA(cudaStreamSynchronize(stream_));
+    }
+    std::uint64_t hs = 1469598103934665603ull;
+    auto feed = [&](double x) {
+        const double y = x + 0.0;
+        std::uint64_t bits;
+        std::memcpy(&bits, &y, 8);
+        for (int b = 0; b < 8; ++b) {
+            hs ^= (bits >> (8 * b)) & 0xffu;
+            hs *= 1099511628211ull;
+        }
+    };
+    const int n1 = h.m + 1;
+    long long full = 1;
+    for (int d = 0; d < p_; ++d) full *= n1;
+    int g[3] = {0, 0, 0};
+    for (long long f = 0; f < full; ++f) {
+        long long ff = f;
+        for (int d = 0; d < p_; ++d) {
+            g[d] = static_cast<int>(ff % n1);
+            ff /= n1;
+        }
+        const long long bf = amr::box_flat(h, p_, g);
+        double2 v = make_double2(0.0, 0.0);
+        if (bf >= 0 && (h.vflag[bf] & amr::kExists) && !(h.vflag[bf] & amr::kHanging)) v = box[bf];
+        feed(v.x);
+        feed(v.y);
+    }
+    return hs;
+}
+
+void AmrTree::set_random_initial_guess(std::uint64_t seed) {
+    Dev& D = *dev_;
+    for (int l = L_; l >= 0; --l) {
+        const int nb = blocks_for_n(D.lv[l].n, smCount_);
+        if (p_ == 1) adev::k_amr_random<1><<<nb, 256, 0, stream_>>>(D.lv[l], seed);
+        else if (p_ == 2) adev::k_amr_random<2><<<nb, 256, 0, stream_>>>(D.lv[l], seed);
+        else adev::k_amr_random<3><<<nb, 256, 0, stream_>>>(D.lv[l], seed);
+        if (l < L_) {
+            if (p_ == 1) adev::k_amr_inject<1><<<nb, 256, 0, stream_>>>(D.lv[l], D.lv[l + 1]);
+            else if (p_ == 2) adev::k_amr_inject<2><<<nb, 256, 0, stream_>>>(D.lv[l], D.lv[l + 1]);
+            else adev::k_amr_inject<3><<<nb, 256, 0, stream_>>>(D.lv[l], D.lv[l + 1]);
+        }
+    }
+    // reset_pipeline_state, cycles.cpp:843-853
+    for (int l = 0; l <= L_; ++l) {
+        const adev::ALvl& v = D.lv[l];
+        for (double2* ptr : {v.sc, v.sf, v.si, v.sinext, v.uhat})
+            if (ptr) AMR_CUDA(cudaMemsetAsync(ptr, 0, static_cast<size_t>(v.n) * sizeof(double2), stream_));
+    }
+    AMR_CUDA(cudaGetLastError());
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+}
+
+void AmrTree::time_cycles(const Policy& pol, int n0, int count, double* out4) {
+    Dev& D = *dev_;
+    double totalMs = 0.0;
+    for (int i = 0; i < count; ++i) {
+        AMR_CUDA(cudaEventRecord(D.ev0, stream_));
+        if (p_ == 1) run_cycle<1>(pol, n0 + i);
+        else if (p_ == 2) run_cycle<2>(pol, n0 + i);
+        else run_cycle<3>(pol, n0 + i);
+        AMR_CUDA(cudaEventRecord(D.ev1, stream_));
+        AMR_CUDA(cudaEventSynchronize(D.ev1));
+        float ms = 0.f;
+        AMR_CUDA(cudaEventElapsedTime(&ms, D.ev0, D.ev1));
+        totalMs += ms;
+    }
+    out4[0] = totalMs;
+    out4[1] = 0.0;
+    out4[2] = 0.0;
+    out4[3] = static_cast<double>(3 * (L_ + 1) + 1);
+}
+
+}  // namespace tmg

@@ -9,6 +9,7 @@
 
 #include "../../include/treemg.h"
 #include "../../include/treemg_b200.h"
+#include "amr.hpp"
 #include "runner.hpp"
 
 using namespace tmg;
@@ -192,6 +193,8 @@ Problem problem_from(const tmg_problem* prob) {
     p.fast = prob->precision == 1;
     if (prob->max_vertices > 0) p.maxVertices = static_cast<std::size_t>(prob->max_vertices);
     p.device = prob->device;
+    p.sphereLevels = prob->sphere_levels;
+    p.levels += p.sphereLevels;
     if (p.ellMin < 1) throw ConfigError("ellMin must be >= 1");
     return p;
 }
@@ -285,6 +288,8 @@ treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out)
         p.fast = prob->precision == 1;
         if (prob->max_vertices > 0) p.maxVertices = static_cast<std::size_t>(prob->max_vertices);
         p.device = prob->device;
+        p.sphereLevels = prob->sphere_levels;
+        p.levels += p.sphereLevels;
         if (p.ellMin < 1) throw ConfigError("ellMin must be >= 1");
         h->h = std::make_unique<Hierarchy>(p);
     });
@@ -345,6 +350,49 @@ treemg_status tmg_set_fine_rhs(tmg_hierarchy* h, const double* chi) {
     if (!h || !chi) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] { h->h->set_fine_rhs(chi); });
 }
+
+treemg_status tmg_get_flags(tmg_hierarchy* h, int level, unsigned char* flags, signed char* succ,
+                            unsigned char* cells) {
+    if (!h) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        if (!h->h->get_flags(level, flags, succ, cells)) throw ConfigError("get_flags: the tree is regular");
+    });
+}
+
+treemg_status tmg_sphere_tree(int dim, int base, int sphere_levels, int level, unsigned char* flags,
+                              signed char* succ, unsigned char* cells, unsigned char* finish_corner) {
+    return guarded([&] {
+        if (dim < 1 || dim > 3 || base < 1 || sphere_levels < 1 || base + sphere_levels > 9)
+            throw ConfigError("tmg_sphere_tree: bad arguments");
+        const int L = base + sphere_levels;
+        if (level < 0 || level > L) throw ConfigError("tmg_sphere_tree: level out of range");
+        const std::vector<amr::HostLevel> lv = amr::build_sphere_tree(dim, base, L);
+        const amr::HostLevel& h = lv[static_cast<size_t>(level)];
+        long long full = 1;
+        for (int d = 0; d < dim; ++d) full *= h.m + 1;
+        if (flags) std::fill(flags, flags + full, 0);
+        if (succ) std::fill(succ, succ + full, static_cast<signed char>(-1));
+        if (cells) std::fill(cells, cells + full, 0);
+        if (finish_corner) std::fill(finish_corner, finish_corner + full, 0xFF);
+        for (long long f = 0; f < h.n; ++f) {
+            long long ff = f, gf = 0, s = 1;
+            for (int d = 0; d < dim; ++d) {
+                gf += (h.lo[d] + ff % h.n1[d]) * s;
+                ff /= h.n1[d];
+                s *= h.m + 1;
+            }
+            if (cells) cells[gf] = h.cflag[f];
+            if (!(h.vflag[f] & amr::kExists)) continue;
+            if (flags) flags[gf] = h.vflag[f];
+            if (succ) succ[gf] = h.succ[f];
+            if (finish_corner) finish_corner[gf] = h.estar[f];
+        }
+    });
+}
+
+long long tmg_hanging_vertices(const tmg_hierarchy* h) { return h ? h->h->hanging_vertices() : 0; }
+
+long long tmg_leaf_vertices(const tmg_hierarchy* h) { return h ? h->h->interior_fine_vertices() : 0; }
 
 unsigned long long tmg_field_hash(tmg_hierarchy* h, int level, const char* field) {
     unsigned long long v = 0;

@@ -114,6 +114,23 @@ __device__ __forceinline__ double2 divdc3(double a, double b, const DivConst& k)
     return make_double2(x, y);
 }
 
+__device__ __forceinline__ double unit_rand(unsigned long long x) {  // cycles.cpp:802-808
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    x = x ^ (x >> 31);
+    return __dsub_rn(__ddiv_rn(__dmul_rn(2.0, static_cast<double>(x >> 11)), 9007199254740992.0), 1.0);
+}
+
+// Per-level constants of the exact kernels (constant theta and phi).
+struct LevelConst {
+    double2 A[8];   // element operator entry for XOR pattern of (a, b)
+    double M[8];    // reference mass entry for XOR pattern
+    double2 massScale;
+    DivConst div;
+    double2 wRaw;   // omega_unmasked(pol, succ = L - l, n)
+};
+
 // ---- traversal orders ---------------------------------------------------
 //
 // The spacetree traversal (proj/src/spacetree.cpp:394-424) enters the 3^p

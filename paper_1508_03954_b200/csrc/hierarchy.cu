@@ -20,6 +20,7 @@
 #include <string>
 #include <vector>
 
+#include "amr.hpp"
 #include "exact_ops.cuh"
 #include "fast.cuh"
 #include "fused3.cuh"
@@ -39,14 +40,6 @@ namespace tmg {
     } while (0)
 
 namespace dev {
-
-struct LevelConst {
-    double2 A[8];   // element operator entry for XOR pattern of (a, b)
-    double M[8];    // reference mass entry for XOR pattern
-    double2 massScale;
-    DivConst div;
-    double2 wRaw;   // omega_unmasked(pol, succ = L - l, n)
-};
 
 struct ResArgs {
     Lvl lv;
@@ -331,14 +324,6 @@ __global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, Level
     }
 }
 
-__device__ __forceinline__ double unit_rand(unsigned long long x) {  // cycles.cpp:802-808
-    x += 0x9e3779b97f4a7c15ull;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
-    x = x ^ (x >> 31);
-    return __dsub_rn(__ddiv_rn(__dmul_rn(2.0, static_cast<double>(x >> 11)), 9007199254740992.0), 1.0);
-}
-
 // Seeded nodal rhs f(x) keyed on the finest-lattice position,
 // optionally masked to the ball |x - 1/2|^2 < 0.04.
 template <int P>
@@ -577,8 +562,10 @@ struct Hierarchy::Impl {
     CUtensorMap mapB, mapC, mapI;
     fused3::Geometry geo{};
     double2* partial3 = nullptr;
+    std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
 
     ~Impl() {
+        amr.reset();
         for (void* ptr : allocations) cudaFree(ptr);
         if (hNorm) cudaFreeHost(hNorm);
         if (ev0) cudaEventDestroy(ev0);
@@ -978,6 +965,7 @@ struct Hierarchy::Impl {
     }
 
     SweepStats cycle(const Policy& pol, int n, bool timed = false) {
+        if (amr) return amr->cycle(pol, n);
         check_diag();
         run_cycle(pol, n, timed);
         TMG_CUDA(cudaMemcpyAsync(hNorm, dNorm, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -1003,9 +991,10 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     if (prob.dim < 1 || prob.dim > 3) throw UnsupportedConfigError("B200 path: dim must be 1, 2 or 3");
     if (prob.levels < 1) throw ConfigError("build_regular needs levels >= 1");
     if (prob.levels > 9) throw ConfigError("tree depth exceeds supported maximum");
+    if (prob.sphereLevels < 0 || prob.sphereLevels >= prob.levels) throw ConfigError("sphere_levels out of range");
     // build_regular's capacity estimate (spacetree.cpp:53-63)
     std::size_t estimate = 0;
-    for (int l = 0; l <= prob.levels; ++l) {
+    for (int l = 0; l <= prob.levels - prob.sphereLevels; ++l) {
         std::size_t perAxis = static_cast<std::size_t>(pow3i(l)) + 1, n = 1;
         for (int d = 0; d < prob.dim; ++d) n *= perAxis;
         estimate += n;
@@ -1022,6 +1011,12 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     TMG_CUDA(cudaEventCreate(&I.ev1));
     TMG_CUDA(cudaEventCreate(&I.evf0));
     TMG_CUDA(cudaEventCreate(&I.evf1));
+    if (prob.sphereLevels > 0) {
+        if (prob.hostNorms) throw UnsupportedConfigError("norms = host is not available on adaptive trees");
+        I.compute_level_constants();
+        I.amr = std::make_unique<AmrTree>(prob, I.kc, I.diagInterior, I.stream, I.smCount);
+        return;
+    }
     const char* dbg = std::getenv("TMG_DEBUG_R");
     I.debugR = (dbg && dbg[0] == '1') || (prob.hostNorms && !prob.fast);
     I.lv.resize(I.L + 1);
@@ -1073,10 +1068,24 @@ int Hierarchy::levels() const { return impl_->L; }
 
 long long Hierarchy::lattice_size(int level) const {
     if (level < 0 || level > impl_->L) return 0;
+    if (impl_->amr) {
+        long long n = 1;
+        for (int d = 0; d < impl_->p; ++d) n *= pow3i(level) + 1;
+        return n;
+    }
     return impl_->lv[level].n;
 }
 
+bool Hierarchy::get_flags(int level, unsigned char* flags, signed char* succ, unsigned char* cells) const {
+    if (!impl_->amr) return false;
+    impl_->amr->get_flags(level, flags, succ, cells);
+    return true;
+}
+
+long long Hierarchy::hanging_vertices() const { return impl_->amr ? impl_->amr->hanging_vertices() : 0; }
+
 long long Hierarchy::interior_fine_vertices() const {
+    if (impl_->amr) return impl_->amr->leaf_vertices();
     long long n = 1;
     for (int d = 0; d < impl_->p; ++d) n *= pow3i(impl_->L) - 1;
     return n;
@@ -1100,6 +1109,10 @@ double2* field_ptr(const dev::Lvl& v, const std::string& f) {
 void Hierarchy::get_field(int level, const std::string& field, double* host) const {
     Impl& I = *impl_;
     if (level < 0 || level > I.L) throw ConfigError("get_field: level out of range");
+    if (I.amr) {
+        I.amr->get_field(level, field, host);
+        return;
+    }
     const dev::Lvl& v = I.lv[level];
     if (field == "diag") {
         // host-side: per vertex the sum of A_aa over its existing cells
@@ -1137,6 +1150,7 @@ void Hierarchy::get_field(int level, const std::string& field, double* host) con
 }
 
 void Hierarchy::set_field(int level, const std::string& field, const double* host) {
+    if (impl_->amr) throw UnsupportedConfigError("set_field is not available on adaptive trees");
     Impl& I = *impl_;
     if (level < 0 || level > I.L) throw ConfigError("set_field: level out of range");
     const dev::Lvl& v = I.lv[level];
@@ -1166,6 +1180,7 @@ struct HierarchyAccess {
 };
 
 void Hierarchy::set_fine_interior_u(const double* host) {
+    if (impl_->amr) throw UnsupportedConfigError("set_fine_interior_u is not available on adaptive trees");
     Impl& I = *impl_;
     const dev::Lvl& F = I.lv[I.L];
     const long long ni = interior_fine_vertices();
@@ -1185,6 +1200,10 @@ void Hierarchy::set_fine_interior_u(const double* host) {
 
 void Hierarchy::set_random_initial_guess(std::uint64_t seed) {
     Impl& I = *impl_;
+    if (I.amr) {
+        I.amr->set_random_initial_guess(seed);
+        return;
+    }
     const dev::Lvl& F = I.lv[I.L];
     if (I.p == 1) dev::k_random_fine<1><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
     else if (I.p == 2) dev::k_random_fine<2><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
@@ -1197,6 +1216,7 @@ void Hierarchy::set_random_initial_guess(std::uint64_t seed) {
 }
 
 void Hierarchy::set_fine_rhs(const double* hostNodalChi) {
+    if (impl_->amr) throw UnsupportedConfigError("set_fine_rhs is not available on adaptive trees");
     Impl& I = *impl_;
     const dev::Lvl& F = I.lv[I.L];
     TMG_CUDA(cudaMemcpyAsync(I.chiNodal, hostNodalChi, static_cast<size_t>(F.n) * sizeof(double2),
@@ -1206,6 +1226,7 @@ void Hierarchy::set_fine_rhs(const double* hostNodalChi) {
 }
 
 std::uint64_t Hierarchy::field_hash(int level, const std::string& field) const {
+    if (impl_->amr) return impl_->amr->field_hash(level, field);
     const long long n = lattice_size(level);
     std::vector<double> buf(2 * static_cast<size_t>(n));
     get_field(level, field, buf.data());
@@ -1247,6 +1268,7 @@ void test_divdc3(const double* x, const double* y, double* out, long long n) {
 // canonical-parent prolongation used here equals the creating cell's for
 // every vertex (coinciding components are exact copies, transfer.cpp:26-38).
 void Hierarchy::unfold() {
+    if (impl_->amr) throw UnsupportedConfigError("FMG unfolding is not available on adaptive trees");
     Impl& old = *impl_;
     Problem p2 = old.prob;
     p2.levels = old.L + 1;
@@ -1280,6 +1302,10 @@ void Hierarchy::unfold() {
 
 void Hierarchy::time_cycles(const Policy& pol, int n0, int count, bool flushL2, double* out4) {
     Impl& I = *impl_;
+    if (I.amr) {
+        I.amr->time_cycles(pol, n0, count, out4);
+        return;
+    }
     I.check_diag();
     if (flushL2 && !I.flushBuf) {
         I.flushN = (256ull << 20) / sizeof(double4);  // 256 MB > 126 MB L2
@@ -1305,6 +1331,7 @@ void Hierarchy::time_cycles(const Policy& pol, int n0, int count, bool flushL2, 
 }
 
 void Hierarchy::e2e_step(const Policy& pol, int n, const double* hostChi, double* out3) {
+    if (impl_->amr) throw UnsupportedConfigError("e2e_step is not available on adaptive trees");
     Impl& I = *impl_;
     const dev::Lvl& F = I.lv[I.L];
     TMG_CUDA(cudaMemcpyAsync(I.chiNodal, hostChi, static_cast<size_t>(F.n) * sizeof(double2), cudaMemcpyHostToDevice,

@@ -62,6 +62,7 @@ struct Problem {
     int rhsLattice = -1;  // level the seeded rhs is keyed on (-1: levels)
     bool fast = false;    // precision = fast
     bool hostNorms = false;  // norms = host: reference-order sums of |r| on the host (exact mode)
+    int sphereLevels = 0;    // static adaptive tree: levels-sphereLevels regular, refined inside |x-1/2|^2<0.04
     std::size_t maxVertices = 8u * 1024u * 1024u;
     int device = 0;
 };
@@ -88,6 +89,9 @@ class Hierarchy {
     int levels() const;
     long long lattice_size(int level) const;
     long long interior_fine_vertices() const;
+    // adaptive trees: flags byte / succ per lattice point (amr.hpp); false if regular
+    bool get_flags(int level, unsigned char* flags, signed char* succ, unsigned char* cells = nullptr) const;
+    long long hanging_vertices() const;
 
     void get_field(int level, const std::string& field, double* host) const;
     void set_field(int level, const std::string& field, const double* host);
