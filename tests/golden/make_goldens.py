@@ -76,6 +76,18 @@ CONFIGS = {
                       omega="undamped", omega_s=0.6, max_sweeps=80, fmg_stage_cap=80, target_drop=1e-8, **SEEDED),
     "fmg2d_bpx": dict(problem="helmholtz-sin", dim=2, level=4, fmg_from=2, phi="100,50", cycle="td-bpx",
                       omega="undamped", omega_s=0.5, max_sweeps=50, fmg_stage_cap=50, target_drop=1e-6, **SEEDED),
+    # cfg4: static sphere refinement 4 -> 6, f masked to the ball, hb for 25 cycles then additive (SURVEY §8d pin)
+    "cfg4": dict(problem="helmholtz-sin", dim=3, level=4, sphere_levels=2, phi="1600,800", cycle="td-add",
+                 omega="exponential", omega_s=0.6, hb_sweeps=25, rhs_mask="sphere", max_sweeps=50,
+                 target_drop=1e-30, max_vertices=100000000, **SEEDED),
+    # cfg4 at reduced depth (2 -> 4, SURVEY §7.3 item 5 probe size) and 2D adaptive variants
+    "cfg4_small": dict(problem="helmholtz-sin", dim=3, level=2, sphere_levels=2, phi="1600,800", cycle="td-add",
+                       omega="exponential", omega_s=0.6, hb_sweeps=10, rhs_mask="sphere", max_sweeps=20,
+                       target_drop=1e-30, **SEEDED),
+    "amr2d_conv": dict(problem="helmholtz-sin", dim=2, level=3, sphere_levels=2, phi="100,50", cycle="td-add",
+                       omega="undamped", omega_s=0.6, max_sweeps=150, target_drop=1e-8, **SEEDED),
+    "amr2d_bpx": dict(problem="helmholtz-sin", dim=2, level=2, sphere_levels=3, phi="100,50", cycle="td-bpx",
+                      omega="undamped", omega_s=0.5, max_sweeps=40, target_drop=1e-8, **SEEDED),
     "rotated_3d_bpx": dict(problem="helmholtz-sin", dim=3, level=3, phi="2025", theta_deg=35, cycle="td-bpx",
                            omega="transition", max_sweeps=15, target_drop=1e-30),
 }
@@ -107,6 +119,6 @@ def generate(name: str) -> dict:
 
 
 if __name__ == "__main__":
-    for n in sys.argv[1:] or [k for k in CONFIGS if k not in ("cfg2", "cfg3")]:
+    for n in sys.argv[1:] or [k for k in CONFIGS if k not in ("cfg2", "cfg3", "cfg4")]:
         r = generate(n)
         print(n, r["outcome"], r["sweeps"], f"{r['reference_seconds_per_sweep']:.3f}s/sweep", flush=True)
