@@ -16,7 +16,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtreemg_b200.so")
 SOURCES = ["hierarchy.cu", "amr.cu", "fast.cu", "fused3.cu", "runner.cpp", "capi.cpp"]
-HEADERS = ["hierarchy.hpp", "amr.hpp", "exact_ops.cuh", "fast.cuh", "fused3.cuh", "lattice.cuh", "runner.hpp"]
+HEADERS = ["hierarchy.hpp", "amr.hpp", "exact_ops.cuh", "fast.cuh", "fused3.cuh", "lattice.cuh", "runner.hpp",
+           "slabs.inc"]
 
 
 def nvcc_path() -> str:

@@ -269,7 +269,237 @@ __global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a, unsigned fa, u
 
 constexpr int kZch = 48;
 
+// ---- coarse chains: every coarse level of one cycle phase in one launch -----
+//
+// The coarse levels of a cycle are a dependency chain of small passes
+// (top-down l = 1..top, then smoothing + restriction top..1); as separate
+// launches each costs a launch / drain of a few microseconds and dominated
+// the cycle below 243^3.  One cooperative launch runs the whole chain with a
+// grid barrier between levels.  Data produced inside the launch is read with
+// ld.global.cg (L2), never through the non-coherent L1 / read-only path.
+__device__ __forceinline__ double2 ldcg(const double2* p) { return __ldcg(p); }
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const unsigned target = gen + 1;
+        __threadfence();
+        if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+            atomicExch(bar, 0u);
+            __threadfence();
+            atomicExch(bar + 1, target);
+        } else {
+            while (*reinterpret_cast<volatile unsigned*>(bar + 1) != target) __nanosleep(32);
+        }
+        __threadfence();
+    }
+    ++gen;
+    __syncthreads();
+}
+
+template <int P>
+__device__ __forceinline__ double2 prolong_cg(const double2* __restrict__ src, unsigned n1, const int* q,
+                                              const int* rel) {
+    double2 v[1 << P];
+#pragma unroll
+    for (int e = 0; e < (1 << P); ++e) {
+        unsigned f = 0, s = 1;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            f += static_cast<unsigned>(q[d] + ((e >> d) & 1)) * s;
+            s *= n1;
+        }
+        v[e] = ldcg(src + f);
+    }
+#pragma unroll
+    for (int d = 0; d < P; ++d)
+#pragma unroll
+        for (int i = 0; i < (1 << (P - 1 - d)); ++i) v[i] = lerp(v[2 * i], v[2 * i + 1], rel[d]);
+    return v[0];
+}
+
+template <int P>
+__global__ void __launch_bounds__(kChainThreads) k_chain_down(ChainArgs a) {
+    unsigned gen = *reinterpret_cast<volatile unsigned*>(a.bar + 1);
+    const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    for (int l = 1; l <= a.top; ++l) {
+        const Lvl& c = a.lv[l];
+        const Lvl& pr = a.lv[l - 1];
+        for (unsigned f = tid; f < c.n; f += stride) {
+            int idx[P];
+            dev::unflat<P>(f, c.n1, idx);
+            if (dev::on_boundary<P>(idx, static_cast<int>(c.m))) continue;
+            int q[P], rel[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                q[d] = min(idx[d] / 3, static_cast<int>(pr.m) - 1);
+                rel[d] = idx[d] - 3 * q[d];
+            }
+            double2 sc = add(c.sc[f], prolong_cg<P>(pr.sc, pr.n1, q, rel));
+            if (a.bpx && !dev::is_cpoint<P>(idx)) sc = sub(sc, prolong_at<P>(pr.si, pr.n1, q, rel));
+            c.sc[f] = sc;
+        }
+        if (l < a.top) grid_barrier(a.bar, gen);
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void chain_restrict(const Lvl& fine, const Lvl& coarse, unsigned tid, unsigned stride) {
+    const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+    const long long sy = fine.n1, sz = static_cast<long long>(fine.n1) * fine.n1;
+    for (unsigned f = tid; f < coarse.n; f += stride) {
+        int W[P];
+        dev::unflat<P>(f, coarse.n1, W);
+        if (dev::on_boundary<P>(W, static_cast<int>(coarse.m))) continue;
+        long long centre = 0, s = 1;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            centre += 3LL * W[d] * s;
+            s *= fine.n1;
+        }
+        const double2* __restrict__ r = fine.rhat + centre;
+        double2 acc = make_double2(0.0, 0.0);
+        if (P == 1) {
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const double2 v = ldcg(r + (i - 2));
+                acc.x = fma(w[i], v.x, acc.x);
+                acc.y = fma(w[i], v.y, acc.y);
+            }
+        } else if (P == 2) {
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const double2 v = ldcg(r + (j - 2) * sy + (i - 2));
+                    row.x = fma(w[i], v.x, row.x);
+                    row.y = fma(w[i], v.y, row.y);
+                }
+                acc.x = fma(w[j], row.x, acc.x);
+                acc.y = fma(w[j], row.y, acc.y);
+            }
+        } else {
+            double2 pl[5];
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                pl[k] = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) {
+                        const double2 v = ldcg(r + (k - 2) * sz + (j - 2) * sy + (i - 2));
+                        row.x = fma(w[i], v.x, row.x);
+                        row.y = fma(w[i], v.y, row.y);
+                    }
+                    pl[k].x = fma(w[j], row.x, pl[k].x);
+                    pl[k].y = fma(w[j], row.y, pl[k].y);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < 5; ++k) {
+                acc.x = fma(w[k], pl[k].x, acc.x);
+                acc.y = fma(w[k], pl[k].y, acc.y);
+            }
+        }
+        coarse.rhat[f] = acc;
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kChainThreads) k_chain_up(ChainArgs a) {
+    unsigned gen = *reinterpret_cast<volatile unsigned*>(a.bar + 1);
+    const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    if (a.firstRestrict && a.top >= a.ellMin) {
+        chain_restrict<P>(a.fine, a.lv[a.top], tid, stride);
+        grid_barrier(a.bar, gen);
+    }
+    for (int l = a.top; l >= 1; --l) {
+        const Lvl& c = a.lv[l];
+        const Lvl& par = a.lv[l - 1];
+        const LevelCoef& k = a.k[l];
+        for (unsigned f = tid; f < c.n; f += stride) {  // smoothing (k_smooth_coarse)
+            int idx[P];
+            dev::unflat<P>(f, c.n1, idx);
+            if (a.bpx && c.si) {
+                c.si[f] = ldcg(c.sinext + f);
+                c.sinext[f] = make_double2(0.0, 0.0);
+            }
+            if (dev::on_boundary<P>(idx, static_cast<int>(c.m)) || c.level < a.ellMin) {
+                c.sc[f] = make_double2(0.0, 0.0);
+                continue;
+            }
+            const bool cp = dev::is_cpoint<P>(idx);
+            const double2 smooth = mul(ldcg(c.rhat + f), k.invDiag);
+            c.sc[f] = stage(smooth, k.wRaw, cp, a.bpx, a.hb);
+            if (a.bpx && c.level > a.ellMin && cp) {
+                int wi[P];
+#pragma unroll
+                for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+                par.sinext[dev::flat<P>(wi, par.n1)] = mul(k.wRaw, smooth);
+            }
+        }
+        if (l - 1 >= 1 && l - 1 >= a.ellMin) chain_restrict<P>(c, par, tid, stride);  // into l-1, same step
+        if (l > 1) grid_barrier(a.bar, gen);
+    }
+    if (a.normOut && blockIdx.x == 0) {  // K5: fixed-order reduction of the fine pass's block partials
+        __shared__ double smax[kChainThreads], ssum[kChainThreads];
+        double mx = 0.0, sm = 0.0;
+        for (int i = threadIdx.x; i < a.normBlocks; i += blockDim.x) {
+            mx = fmax(mx, a.normPartials[2 * i]);
+            sm += a.normPartials[2 * i + 1];
+        }
+        smax[threadIdx.x] = mx;
+        ssum[threadIdx.x] = sm;
+        __syncthreads();
+        for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+            if (threadIdx.x < s) {
+                smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+                ssum[threadIdx.x] += ssum[threadIdx.x + s];
+            }
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            a.normOut[0] = smax[0];
+            a.normOut[1] = ssum[0];
+        }
+    }
+}
+
 }  // namespace
+
+template <int P>
+static int chain_grid_for(int smCount) {
+    int perSm = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm, k_chain_up<P>, kChainThreads, 0);
+    int perSm2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&perSm2, k_chain_down<P>, kChainThreads, 0);
+    return std::max(1, std::min(std::min(perSm, perSm2), 2)) * smCount;
+}
+
+int chain_grid(int P, int smCount) {
+    if (P == 1) return chain_grid_for<1>(smCount);
+    if (P == 2) return chain_grid_for<2>(smCount);
+    return chain_grid_for<3>(smCount);
+}
+
+void chain_down(int P, const ChainArgs& a, int grid, cudaStream_t s) {
+    if (a.top < 1) return;
+    void* args[] = {const_cast<ChainArgs*>(&a)};
+    const void* fn = P == 1 ? reinterpret_cast<const void*>(k_chain_down<1>)
+                   : P == 2 ? reinterpret_cast<const void*>(k_chain_down<2>)
+                            : reinterpret_cast<const void*>(k_chain_down<3>);
+    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kChainThreads), args, 0, s);
+}
+
+void chain_up(int P, const ChainArgs& a, int grid, cudaStream_t s) {
+    void* args[] = {const_cast<ChainArgs*>(&a)};
+    const void* fn = P == 1 ? reinterpret_cast<const void*>(k_chain_up<1>)
+                   : P == 2 ? reinterpret_cast<const void*>(k_chain_up<2>)
+                            : reinterpret_cast<const void*>(k_chain_up<3>);
+    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kChainThreads), args, 0, s);
+}
 
 namespace {
 // plane range [za, zb) of the last axis -> flat index range

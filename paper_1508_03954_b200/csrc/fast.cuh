@@ -49,6 +49,28 @@ int residual_fine_blocks(int P, const dev::Lvl& f, int smCount);
 // r_{l-1} = R r_l on interior coarse vertices (rhat arrays).
 void restrict_level(int P, const dev::Lvl& fine, const dev::Lvl& coarse, const double* weights, int blocks,
                     cudaStream_t s, int za = -1, int zb = -1);
+// Coarse chains (one cooperative launch per phase, grid barrier between levels):
+//   chain_down: top-down of levels 1..top;
+//   chain_up:   [restrict fine -> top,] then for l = top..1 smoothing of l and
+//               restriction l -> l-1, then the final norm reduction.
+constexpr int kChainThreads = 512;
+constexpr int kMaxChainLevels = 10;
+struct ChainArgs {
+    dev::Lvl lv[kMaxChainLevels];
+    LevelCoef k[kMaxChainLevels];
+    dev::Lvl fine;
+    int top;            // highest coarse level in the chain (L - 1)
+    int firstRestrict;  // restrict fine.rhat into lv[top] first (unfused fine pass)
+    int ellMin, bpx, hb;
+    unsigned* bar;      // grid barrier state: arrivals, generation
+    const double* normPartials;
+    int normBlocks;
+    double* normOut;    // nullptr: no norm reduction
+};
+int chain_grid(int P, int smCount);
+void chain_down(int P, const ChainArgs& a, int grid, cudaStream_t s);
+void chain_up(int P, const ChainArgs& a, int grid, cudaStream_t s);
+
 // Coarse smoothing: sc_l = omega r_l / diag, si commit, BPX injection into l-1.
 void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s, int za = -1, int zb = -1);
 

@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int 
 
 }  // namespace
 
-Geometry geometry(int m, int mc) {
+Geometry geometry(int m, int mc, int parts, int resident) {
     Geometry g{};
     g.m = m;
     g.mc = mc;
@@ -406,9 +406,16 @@ Geometry geometry(int m, int mc) {
     g.nbx = (inner + TX - 1) / TX;
     g.nby = (inner + TY - 1) / TY;
     const int tiles = g.nbx * g.nby;
-    const int want = std::max(8, (4 * 2 * 148 + tiles - 1) / tiles);
-    g.zc = std::max(3, ((inner + want - 1) / want + 2) / 3 * 3);
-    g.nbz = (inner + g.zc - 1) / g.zc;
+    parts = std::max(1, parts);
+    // at least 8 chunks and ~2 waves of blocks (measured best at 243^3 and
+    // 729^3; a finer wave model did not pay), in multiples of `parts`
+    int want = std::max(8, (2 * std::max(1, resident) + tiles - 1) / tiles);
+    want = (want + parts - 1) / parts * parts;
+    for (;; want += parts) {
+        g.zc = std::max(3, ((inner + want - 1) / want + 2) / 3 * 3);
+        g.nbz = (inner + g.zc - 1) / g.zc;
+        if (g.nbz % parts == 0 || g.zc == 3) break;
+    }
     g.sz = g.zc / 3 + 2;
     return g;
 }
@@ -443,6 +450,16 @@ bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind) {
                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
+}
+
+int resident_blocks(int smCount) {
+    // blocks per SM of the non-BPX kernel at its dynamic shared memory size
+    const size_t smem = smem_bytes(false);
+    cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused3<false>, TX * TY, smem) != cudaSuccess || per < 1)
+        per = 3;
+    return per * smCount;
 }
 
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapC,

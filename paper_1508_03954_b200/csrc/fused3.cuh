@@ -60,7 +60,10 @@ struct Args {
     int chunkBase;        // first global z-chunk of this launch
 };
 
-Geometry geometry(int m, int mc);
+// Tile / z-chunk geometry; the chunk count is a multiple of `parts` (z-slabs:
+// every rank gets the same number of chunks) where the lattice allows it.
+Geometry geometry(int m, int mc, int parts = 1, int resident = 3 * 148);
+int resident_blocks(int smCount);  // co-resident k_fused3 blocks on the device
 size_t partial_count(const Geometry& g);
 size_t smem_bytes(bool bpx);
 int blocks(const Geometry& g);

@@ -563,6 +563,9 @@ struct Hierarchy::Impl {
     fused3::Geometry geo{};
     double2* partial3 = nullptr;
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
+    int chainGrid = 0;              // cooperative coarse-chain grid (0: per-level launches)
+    int fusedResident = 3 * 148;
+    unsigned* chainBar = nullptr;
 
     ~Impl() {
         amr.reset();
@@ -819,7 +822,27 @@ struct Hierarchy::Impl {
             a.partials = partials;
             return a;
         };
-        for (int l = 1; l < L; ++l) fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+        const bool useChain = chainGrid > 0 && L - 1 < fast::kMaxChainLevels;
+        fast::ChainArgs ch{};
+        if (useChain) {
+            for (int l = 0; l < L; ++l) {
+                ch.lv[l] = lv[l];
+                ch.k[l] = fc[l];
+                const Cplx w = omega_unmasked(pol, L - l, n);
+                ch.k[l].wRaw = make_double2(w.real(), w.imag());
+            }
+            ch.fine = lv[L];
+            ch.top = L - 1;
+            ch.ellMin = prob.ellMin;
+            ch.bpx = bpx;
+            ch.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+            ch.bar = chainBar;
+            ch.normPartials = partials;
+            ch.normOut = dNorm;
+            fast::chain_down(P, ch, chainGrid, stream);
+        } else {
+            for (int l = 1; l < L; ++l) fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+        }
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
         if (P == 3 && fused) {
             fused3::Args fa{};
@@ -849,12 +872,19 @@ struct Hierarchy::Impl {
             std::swap(F.sc, scAlt);
             std::swap(mapU[0], mapU[1]);
             std::swap(mapS[0], mapS[1]);
-            for (int l = L - 1; l >= 1; --l) {
-                if (l < L - 1 && l >= prob.ellMin)
-                    fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
-                fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+            if (useChain) {
+                ch.lv[L - 1] = lv[L - 1];
+                ch.firstRestrict = 0;
+                ch.normBlocks = fused3::blocks(geo);
+                fast::chain_up(P, ch, chainGrid, stream);
+            } else {
+                for (int l = L - 1; l >= 1; --l) {
+                    if (l < L - 1 && l >= prob.ellMin)
+                        fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
+                    fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+                }
+                dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused3::blocks(geo), dNorm);
             }
-            dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused3::blocks(geo), dNorm);
             TMG_CUDA(cudaGetLastError());
             coarseUStale = true;
             return;
@@ -862,11 +892,17 @@ struct Hierarchy::Impl {
         fast::correct_fine(P, lv[L], lv[L - 1], bpx, blocks_for(lv[L].n), stream);
         const int nb = fast::residual_fine(P, args(L), smCount, stream);
         if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
-        for (int l = L - 1; l >= 1; --l) {
-            if (l >= prob.ellMin) fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
-            fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+        if (useChain) {
+            ch.firstRestrict = 1;
+            ch.normBlocks = nb;
+            fast::chain_up(P, ch, chainGrid, stream);
+        } else {
+            for (int l = L - 1; l >= 1; --l) {
+                if (l >= prob.ellMin) fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
+                fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+            }
+            dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, nb, dNorm);
         }
-        dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, nb, dNorm);
         TMG_CUDA(cudaGetLastError());
         coarseUStale = true;
     }
@@ -898,6 +934,7 @@ struct Hierarchy::Impl {
     }
 
     int launches_per_cycle() const {
+        if (prob.fast && chainGrid > 0) return 4;  // chain_down, fine pass (+combine or +correction), chain_up
         if (prob.fast && fused) return (L - 1) + 2 + std::max(0, L - 2 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1;
         return prob.fast ? (L - 1) + 2 + (L - 1 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1 : 3 * L;
     }
@@ -1022,10 +1059,22 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     I.lv.resize(I.L + 1);
     for (int l = 0; l <= I.L; ++l) I.lv[l] = I.make_level(l, l == I.L);
     I.normBlocks = std::max(I.blocks_for(I.lv[I.L].n), fast::residual_fine_blocks(I.p, I.lv[I.L], I.smCount));
-    if (prob.fast && I.p == 3 && I.L >= 2)
+    if (prob.fast && I.p == 3 && I.L >= 2) {
+        I.fusedResident = fused3::resident_blocks(I.smCount);
         I.normBlocks = std::max(I.normBlocks, fused3::blocks(fused3::geometry(static_cast<int>(I.lv[I.L].m),
-                                                                              static_cast<int>(I.lv[I.L - 1].m))));
+                                                                              static_cast<int>(I.lv[I.L - 1].m),
+                                                                              prob.zParts, I.fusedResident)));
+    }
     I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks));
+    if (prob.fast) {
+        const char* cz = std::getenv("TMG_CHAIN");
+        int coop = 0;
+        TMG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, prob.device));
+        if (coop && !(cz && cz[0] == '0')) {
+            I.chainGrid = fast::chain_grid(I.p, I.smCount);
+            I.chainBar = I.alloc<unsigned>(2);
+        }
+    }
     I.dNorm = I.alloc<double>(2);
     TMG_CUDA(cudaMallocHost(&I.hNorm, 2 * sizeof(double)));
     I.chiNodal = I.alloc<double2>(I.lv[I.L].n);
@@ -1037,7 +1086,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
             const dev::Lvl& F = I.lv[I.L];
             I.uAlt = I.alloc<double2>(F.n);
             I.scAlt = I.alloc<double2>(F.n);
-            I.geo = fused3::geometry(static_cast<int>(F.m), static_cast<int>(I.lv[I.L - 1].m));
+            I.geo = fused3::geometry(static_cast<int>(F.m), static_cast<int>(I.lv[I.L - 1].m), prob.zParts,
+                                     I.fusedResident);
             I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
             const dev::Lvl& C = I.lv[I.L - 1];
             bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0) && fused3::encode_map(&I.mapS[0], F.sc, F.n1, 0) &&

@@ -62,6 +62,7 @@ struct Problem {
     int rhsLattice = -1;  // level the seeded rhs is keyed on (-1: levels)
     bool fast = false;    // precision = fast
     bool hostNorms = false;  // norms = host: reference-order sums of |r| on the host (exact mode)
+    int zParts = 1;          // fused fine pass: z-chunks come in multiples of this (z-slabs)
     int sphereLevels = 0;    // static adaptive tree: levels-sphereLevels regular, refined inside |x-1/2|^2<0.04
     std::size_t maxVertices = 8u * 1024u * 1024u;
     int device = 0;
@@ -142,7 +143,7 @@ class SlabGroup {
     std::unique_ptr<State> st_;
 };
 
-std::vector<std::array<int, 8>> slab_plan(int levels, int world);
+std::vector<std::array<int, 8>> slab_plan(int levels, int world, int resident = 3 * 148);
 
 // 128-byte NCCL unique id (dlopen'd libnccl); false if NCCL is unavailable.
 bool nccl_unique_id(void* out128);
