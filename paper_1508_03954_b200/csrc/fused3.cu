@@ -111,7 +111,8 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
     double2* Vb = ring + STAGES * SE;                           // [2][kV] (+[2][kV] si)
     double2* Pb = Vb + (BPX ? 4 : 2) * kV;                      // [2][kPlane] corrected planes
     double2* tb = Pb + 2 * kPlane;                              // [TY][TX] z-restricted columns
-    uint64_t* bar = reinterpret_cast<uint64_t*>(tb + NT);
+    double2* rb = tb + NT;                                      // [TY][SX] x-restricted rows
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rb + TY * SX);
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int m = a.g.m, mc = a.g.mc;
@@ -242,6 +243,47 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
         }
     };
 
+    // Pipelined xy reduction of a finished coarse plane: the step after tb is
+    // written reduces rows (stage 1, into rb), the next one columns (stage 2,
+    // into the partials); both ride on the steps' own barriers.  Same
+    // arithmetic as flushSlots.  Task i runs on thread NT-1-i, away from the
+    // threads that carry phase-B halo / coarse-row work.
+    const int ti = NT - 1 - tid;
+    auto stage1 = [&]() {
+        if (ti < TY * nsx) {
+            const int fyl = ti / nsx, sx = ti % nsx;
+            if (y0 + fyl < ye) {
+                const int X = Xa + sx;
+                double2 row = zero2();
+#pragma unroll
+                for (int kx = -2; kx <= 2; ++kx) {
+                    const int fx = 3 * X + kx;
+                    if (fx < x0 || fx >= xe) continue;
+                    const double wx = kx == 0 ? 1.0 : (kx == 1 || kx == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
+                    row = axpy(wx, tb[fyl * TX + (fx - x0)], row);
+                }
+                rb[fyl * SX + sx] = row;
+            }
+        }
+    };
+    auto stage2 = [&](int zi) {
+        if (ti < nsx * nsy) {
+            const int sx = ti % nsx, syy = ti / nsx;
+            const int Y = Ya + syy;
+            double2 acc = zero2();
+#pragma unroll
+            for (int ky = -2; ky <= 2; ++ky) {
+                const int fy = 3 * Y + ky;
+                if (fy < y0 || fy >= ye) continue;
+                const double wy = ky == 0 ? 1.0 : (ky == 1 || ky == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
+                acc = axpy(wy, rb[(fy - y0) * SX + sx], acc);
+            }
+            part[zi * zStride + syy * SX + sx] = acc;
+        }
+    };
+    bool pend1 = false, pend2 = false;
+    int zi1 = 0, zi2 = 0;
+
     const long long colBase = x + y * sy;
     const double2* bPtr = a.b + colBase + static_cast<long long>(z0) * sz;
     double2* uPtr = a.uNew + colBase + static_cast<long long>(z0) * sz;
@@ -300,6 +342,15 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
         stage = nstage;
         parity = nparity;
         // ---- phase C ----
+        if (u == 1 && pend1) {
+            stage1();
+            pend1 = false;
+            pend2 = true;
+            zi2 = zi1;
+        } else if (u == 2 && pend2) {
+            stage2(zi2);
+            pend2 = false;
+        }
         const double2* c = P + po;
         const double2 E = add(add(c[-1], c[1]), add(c[-HX], c[HX]));
         const double2 K = add(add(c[-1 - HX], c[1 - HX]), add(c[-1 + HX], c[1 + HX]));
@@ -338,7 +389,8 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
                 tb[ty * TX + tx] = accLo;
                 accLo = accHi;
                 accHi = zero2();
-                flushSlots(zLow - zBase);
+                pend1 = true;
+                zi1 = zLow - zBase;
                 ++zLow;
             }
         }
@@ -355,6 +407,14 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
         step(it + 1, U1{});
         if (it + 2 >= nplanes) break;
         step(it + 2, U2{});
+    }
+    __syncthreads();
+    if (pend1) {  // drain the pipelined reduction
+        stage1();
+        __syncthreads();
+        stage2(zi1);
+    } else if (pend2) {
+        stage2(zi2);
     }
     __syncthreads();
     tb[ty * TX + tx] = accLo;
@@ -428,7 +488,8 @@ int blocks(const Geometry& g) { return g.nbx * g.nby * g.nbz; }
 
 size_t smem_bytes(bool bpx) {
     const int se = bpx ? stage_elems<true>() : stage_elems<false>();
-    return (STAGES * se + (bpx ? 4 : 2) * kV + 2 * kPlane + NT) * sizeof(double2) + STAGES * sizeof(uint64_t);
+    return (STAGES * se + (bpx ? 4 : 2) * kV + 2 * kPlane + NT + TY * SX) * sizeof(double2) +
+           STAGES * sizeof(uint64_t);
 }
 
 bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind) {
