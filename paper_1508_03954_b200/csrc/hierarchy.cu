@@ -564,6 +564,7 @@ struct Hierarchy::Impl {
     double2* partial3 = nullptr;
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
     int chainGrid = 0;              // cooperative coarse-chain grid (0: per-level launches)
+    static constexpr unsigned kChainMaxN = 1u << 16;  // levels below this size join the chain
     int fusedResident = 3 * 148;
     unsigned* chainBar = nullptr;
 
@@ -822,17 +823,21 @@ struct Hierarchy::Impl {
             a.partials = partials;
             return a;
         };
-        const bool useChain = chainGrid > 0 && L - 1 < fast::kMaxChainLevels;
+        // levels 1..top (each below kChainMaxN points) run as one cooperative
+        // chain per phase; bigger levels keep their own full-grid launches
+        int top = L - 1;
+        while (top >= 1 && lv[top].n >= kChainMaxN) --top;
+        const bool useChain = chainGrid > 0 && top >= 1 && top < fast::kMaxChainLevels;
         fast::ChainArgs ch{};
         if (useChain) {
-            for (int l = 0; l < L; ++l) {
+            for (int l = 0; l <= top; ++l) {
                 ch.lv[l] = lv[l];
                 ch.k[l] = fc[l];
                 const Cplx w = omega_unmasked(pol, L - l, n);
                 ch.k[l].wRaw = make_double2(w.real(), w.imag());
             }
-            ch.fine = lv[L];
-            ch.top = L - 1;
+            ch.fine = lv[top + 1];
+            ch.top = top;
             ch.ellMin = prob.ellMin;
             ch.bpx = bpx;
             ch.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
@@ -840,9 +845,9 @@ struct Hierarchy::Impl {
             ch.normPartials = partials;
             ch.normOut = dNorm;
             fast::chain_down(P, ch, chainGrid, stream);
-        } else {
-            for (int l = 1; l < L; ++l) fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
         }
+        for (int l = useChain ? top + 1 : 1; l < L; ++l)
+            fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
         if (P == 3 && fused) {
             fused3::Args fa{};
@@ -872,17 +877,18 @@ struct Hierarchy::Impl {
             std::swap(F.sc, scAlt);
             std::swap(mapU[0], mapU[1]);
             std::swap(mapS[0], mapS[1]);
+            for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
+                if (l < L - 1 && l >= prob.ellMin)
+                    fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
+                fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+            }
             if (useChain) {
-                ch.lv[L - 1] = lv[L - 1];
+                if (top < L - 1 && top >= prob.ellMin)
+                    fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
                 ch.firstRestrict = 0;
                 ch.normBlocks = fused3::blocks(geo);
                 fast::chain_up(P, ch, chainGrid, stream);
             } else {
-                for (int l = L - 1; l >= 1; --l) {
-                    if (l < L - 1 && l >= prob.ellMin)
-                        fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
-                    fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
-                }
                 dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused3::blocks(geo), dNorm);
             }
             TMG_CUDA(cudaGetLastError());
@@ -892,15 +898,15 @@ struct Hierarchy::Impl {
         fast::correct_fine(P, lv[L], lv[L - 1], bpx, blocks_for(lv[L].n), stream);
         const int nb = fast::residual_fine(P, args(L), smCount, stream);
         if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+        for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
+            if (l >= prob.ellMin) fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
+            fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+        }
         if (useChain) {
-            ch.firstRestrict = 1;
+            ch.firstRestrict = 1;  // fine = lv[top + 1] into lv[top]
             ch.normBlocks = nb;
             fast::chain_up(P, ch, chainGrid, stream);
         } else {
-            for (int l = L - 1; l >= 1; --l) {
-                if (l >= prob.ellMin) fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
-                fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
-            }
             dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, nb, dNorm);
         }
         TMG_CUDA(cudaGetLastError());
@@ -934,7 +940,11 @@ struct Hierarchy::Impl {
     }
 
     int launches_per_cycle() const {
-        if (prob.fast && chainGrid > 0) return 4;  // chain_down, fine pass (+combine or +correction), chain_up
+        if (prob.fast && chainGrid > 0) {
+            int top = L - 1, big = 0;
+            while (top >= 1 && lv[top].n >= kChainMaxN) --top, ++big;
+            if (top >= 1) return 2 + 2 + 3 * big + (top < L - 1 ? 1 : 0);  // chains, fine pass(es), big levels
+        }
         if (prob.fast && fused) return (L - 1) + 2 + std::max(0, L - 2 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1;
         return prob.fast ? (L - 1) + 2 + (L - 1 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1 : 3 * L;
     }
