@@ -81,6 +81,79 @@ __global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx, unsigne
     }
 }
 
+// Same update, one thread per parent cell column in x: the three fine points
+// x = 3qx + {0,1,2} share their 2^P parent values, loaded once (P = 2, 3).
+template <int P, bool FINE>
+__global__ void __launch_bounds__(256) k_topdown_tri(Lvl c, Lvl pr, int bpx, unsigned ra, unsigned rb) {
+    const unsigned mcp = pr.m, n1 = c.n1;
+    const int m = static_cast<int>(c.m);
+    const unsigned total = (rb - ra) * mcp;  // rows [ra, rb) of the (P-1)-dim row index
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const unsigned row = ra + t / mcp;
+        const int qx = static_cast<int>(t - (t / mcp) * mcp);
+        int idx[P];
+        unsigned rr = row;
+#pragma unroll
+        for (int d = 1; d < P; ++d) {
+            idx[d] = static_cast<int>(rr % n1);
+            rr /= n1;
+        }
+        bool bnd = false;
+#pragma unroll
+        for (int d = 1; d < P; ++d) bnd |= (idx[d] == 0) | (idx[d] == m);
+        if (bnd) continue;
+        int q[P], rel[P];
+        q[0] = qx;
+#pragma unroll
+        for (int d = 1; d < P; ++d) {
+            q[d] = min(idx[d] / 3, static_cast<int>(mcp) - 1);
+            rel[d] = idx[d] - 3 * q[d];
+        }
+        double2 vs[1 << P], vi[1 << P];
+#pragma unroll
+        for (int e = 0; e < (1 << P); ++e) {
+            unsigned f = 0, s = 1;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                f += static_cast<unsigned>(q[d] + ((e >> d) & 1)) * s;
+                s *= pr.n1;
+            }
+            vs[e] = ld(pr.sc + f);
+            vi[e] = bpx ? ld(pr.si + f) : make_double2(0.0, 0.0);
+        }
+        bool cpr = true;
+#pragma unroll
+        for (int d = 1; d < P; ++d) cpr &= idx[d] % 3 == 0;
+        const unsigned fb = row * n1;
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int x = 3 * qx + k;
+            if (x < 1 || x > m - 1) continue;
+            rel[0] = k;
+            double2 w[1 << P];
+#pragma unroll
+            for (int e = 0; e < (1 << P); ++e) w[e] = vs[e];
+#pragma unroll
+            for (int d = 0; d < P; ++d)
+#pragma unroll
+                for (int i = 0; i < (1 << (P - 1 - d)); ++i) w[i] = lerp(w[2 * i], w[2 * i + 1], rel[d]);
+            const unsigned f = fb + static_cast<unsigned>(x);
+            double2 sc = add(c.sc[f], w[0]);  // k_topdown order: (sc + P sc) - P si
+            if (bpx && !(cpr && k == 0)) {
+#pragma unroll
+                for (int e = 0; e < (1 << P); ++e) w[e] = vi[e];
+#pragma unroll
+                for (int d = 0; d < P; ++d)
+#pragma unroll
+                    for (int i = 0; i < (1 << (P - 1 - d)); ++i) w[i] = lerp(w[2 * i], w[2 * i + 1], rel[d]);
+                sc = sub(sc, w[0]);
+            }
+            if (FINE) c.u[f] = add(c.u[f], sc);
+            else c.sc[f] = sc;
+        }
+    }
+}
+
 // ---- K2f (3D): r = b - H u by z-marching planes -----------------------------
 // Block = 32 x 4 columns (x, y); each thread walks ZCH planes in z, forming per
 // plane the centre / 4-edge / 4-corner sums of its 3x3 neighbourhood so every
@@ -240,6 +313,87 @@ __global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse, unsigned
     }
 }
 
+// ---- 3D row kernels for the big coarse levels ----------------------------------
+// One block per (y, z) row: the four parent rows a row interpolates from (and
+// for the restriction the 25 fine rows a coarse row gathers) are staged in
+// shared memory once, so the per-point work is a handful of lerps instead of
+// eight scattered loads with full index arithmetic.  Same arithmetic order as
+// prolong_at / k_restrict (bitwise equal results).
+constexpr int kRowThreads = 256;
+
+__global__ void __launch_bounds__(kRowThreads) k_topdown3_rows(Lvl c, Lvl pr, int bpx, int zlo) {
+    extern __shared__ double2 rs[];  // [4 (+4 BPX)][pr.n1]
+    const int m = static_cast<int>(c.m), mcp = static_cast<int>(pr.m);
+    const int y = 1 + blockIdx.x, z = zlo + blockIdx.y;
+    const int qy = min(y / 3, mcp - 1), qz = min(z / 3, mcp - 1);
+    const int ry = y - 3 * qy, rz = z - 3 * qz;
+    const unsigned pn1 = pr.n1;
+    const int nsrc = bpx ? 8 : 4;
+    for (int t = threadIdx.x; t < nsrc * static_cast<int>(pn1); t += blockDim.x) {
+        const int r = t / static_cast<int>(pn1), qx = t % static_cast<int>(pn1);
+        const int e = r & 3;
+        const double2* src = r < 4 ? pr.sc : pr.si;
+        rs[t] = ld(src + qx + pn1 * (static_cast<unsigned>(qy + (e & 1)) + pn1 * static_cast<unsigned>(qz + (e >> 1))));
+    }
+    __syncthreads();
+    const bool cpyz = (y % 3 == 0) && (z % 3 == 0);
+    double2* row = c.sc + c.n1 * (static_cast<unsigned>(y) + c.n1 * static_cast<unsigned>(z));
+    for (int x = 1 + threadIdx.x; x <= m - 1; x += blockDim.x) {
+        const int qx = min(x / 3, mcp - 1), rx = x - 3 * qx;
+        auto pro = [&](const double2* R) {
+            const double2 a0 = lerp(R[qx], R[qx + 1], rx);
+            const double2 a1 = lerp(R[pn1 + qx], R[pn1 + qx + 1], rx);
+            const double2 a2 = lerp(R[2 * pn1 + qx], R[2 * pn1 + qx + 1], rx);
+            const double2 a3 = lerp(R[3 * pn1 + qx], R[3 * pn1 + qx + 1], rx);
+            return lerp(lerp(a0, a1, ry), lerp(a2, a3, ry), rz);
+        };
+        double2 sc = add(row[x], pro(rs));
+        if (bpx && !(cpyz && x % 3 == 0)) sc = sub(sc, pro(rs + 4 * pn1));
+        row[x] = sc;
+    }
+}
+
+__global__ void __launch_bounds__(kRowThreads) k_restrict3_rows(Lvl fine, Lvl coarse, int zlo) {
+    extern __shared__ double2 rw[];  // [25][coarse.n1] x-restricted fine rows
+    const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+    const int mc = static_cast<int>(coarse.m);
+    const int W1 = 1 + blockIdx.x, W2 = zlo + blockIdx.y;
+    const unsigned fn1 = fine.n1, cn1 = coarse.n1;
+    const int nW = mc - 1;
+    for (int t = threadIdx.x; t < 25 * nW; t += blockDim.x) {
+        const int jk = t / nW, W0 = 1 + t % nW;
+        const int j = jk % 5, k = jk / 5;
+        const double2* r = fine.rhat + static_cast<long long>(3 * W0) +
+                           fn1 * (static_cast<long long>(3 * W1 + j - 2) + static_cast<long long>(fn1) * (3 * W2 + k - 2));
+        double2 rowv = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int i = 0; i < 5; ++i) {
+            const double2 v = ld(r + (i - 2));
+            rowv.x = fma(w[i], v.x, rowv.x);
+            rowv.y = fma(w[i], v.y, rowv.y);
+        }
+        rw[jk * nW + (W0 - 1)] = rowv;
+    }
+    __syncthreads();
+    double2* out = coarse.rhat + cn1 * (static_cast<unsigned>(W1) + cn1 * static_cast<unsigned>(W2));
+    for (int W0 = 1 + threadIdx.x; W0 <= mc - 1; W0 += blockDim.x) {
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            double2 pl = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                const double2 rowv = rw[(k * 5 + j) * nW + (W0 - 1)];
+                pl.x = fma(w[j], rowv.x, pl.x);
+                pl.y = fma(w[j], rowv.y, pl.y);
+            }
+            acc.x = fma(w[k], pl.x, acc.x);
+            acc.y = fma(w[k], pl.y, acc.y);
+        }
+        out[W0] = acc;
+    }
+}
+
 // ---- K3c: coarse smoothing on the restricted residual ------------------------
 template <int P>
 __global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a, unsigned fa, unsigned fb) {
@@ -343,8 +497,57 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_down(ChainArgs a) {
     }
 }
 
+// 3D: eight lanes per coarse vertex, lanes 0..4 each form one plane's 25-point
+// partial, lane 0 combines them in plane order (the arithmetic of k_restrict),
+// so the latency chain is 25 loads instead of 125 on the small levels.
+__device__ __forceinline__ void chain_restrict3(const Lvl& fine, const Lvl& coarse, unsigned tid, unsigned stride) {
+    const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+    const long long sy = fine.n1, sz = static_cast<long long>(fine.n1) * fine.n1;
+    const unsigned lane = threadIdx.x & 31u, grp = lane >> 3, k = lane & 7u;
+    const unsigned warp = tid >> 5, warps = stride >> 5;
+    for (unsigned base = warp * 4u; base < coarse.n; base += warps * 4u) {
+        const unsigned f = base + grp;
+        int W[3] = {0, 0, 0};
+        bool act = f < coarse.n;
+        if (act) {
+            dev::unflat<3>(f, coarse.n1, W);
+            act = !dev::on_boundary<3>(W, static_cast<int>(coarse.m));
+        }
+        double2 pl = make_double2(0.0, 0.0);
+        if (act && k < 5) {
+            const double2* __restrict__ r =
+                fine.rhat + (3LL * W[0] + sy * (3LL * W[1]) + sz * (3LL * W[2])) + (static_cast<int>(k) - 2) * sz;
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const double2 v = ldcg(r + (j - 2) * sy + (i - 2));
+                    row.x = fma(w[i], v.x, row.x);
+                    row.y = fma(w[i], v.y, row.y);
+                }
+                pl.x = fma(w[j], row.x, pl.x);
+                pl.y = fma(w[j], row.y, pl.y);
+            }
+        }
+        double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+        for (int kk = 0; kk < 5; ++kk) {
+            const double px = __shfl_sync(0xffffffffu, pl.x, (grp << 3) + kk);
+            const double py = __shfl_sync(0xffffffffu, pl.y, (grp << 3) + kk);
+            acc.x = fma(w[kk], px, acc.x);
+            acc.y = fma(w[kk], py, acc.y);
+        }
+        if (act && k == 0) coarse.rhat[f] = acc;
+    }
+}
+
 template <int P>
 __device__ __forceinline__ void chain_restrict(const Lvl& fine, const Lvl& coarse, unsigned tid, unsigned stride) {
+    if (P == 3) {
+        chain_restrict3(fine, coarse, tid, stride);
+        return;
+    }
     const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
     const long long sy = fine.n1, sz = static_cast<long long>(fine.n1) * fine.n1;
     for (unsigned f = tid; f < coarse.n; f += stride) {
@@ -518,12 +721,37 @@ void span(int P, const Lvl& v, int za, int zb, unsigned& fa, unsigned& fb) {
 }  // namespace
 
 void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaStream_t s) {
+    if (P >= 2 && f.m >= 27) {
+        const unsigned rows = f.n / f.n1;
+        if (P == 2) k_topdown_tri<2, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, rows);
+        else k_topdown_tri<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, rows);
+        return;
+    }
     if (P == 1) k_topdown<1, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, f.n);
     else if (P == 2) k_topdown<2, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, f.n);
     else k_topdown<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, f.n);
 }
 
 void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cudaStream_t s, int za, int zb) {
+    if (P >= 2 && c.m >= 81) {  // parent-cell triples (rows [za, zb) of planes for P = 3)
+        unsigned ra = 0, rb = c.n / c.n1;
+        if (za >= 0) {
+            const unsigned perPlane = P == 3 ? c.n1 : 1u;
+            ra = static_cast<unsigned>(za) * perPlane;
+            rb = std::min(rb, static_cast<unsigned>(zb) * perPlane);
+        }
+        if (rb <= ra) return;
+        if (P == 2) k_topdown_tri<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
+        else k_topdown_tri<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
+        return;
+    }
+    if (P == 3 && c.m == 27) {  // row kernel: small levels, where per-thread latency dominated: interior planes of [za, zb)
+        const int zlo = std::max(1, za < 0 ? 1 : za), zhi = std::min(static_cast<int>(c.m), za < 0 ? static_cast<int>(c.m) : zb);
+        if (zhi <= zlo) return;
+        const size_t smem = (bpx ? 8 : 4) * pr.n1 * sizeof(double2);
+        k_topdown3_rows<<<dim3(c.m - 1, zhi - zlo), kRowThreads, smem, s>>>(c, pr, bpx, zlo);
+        return;
+    }
     unsigned fa, fb;
     span(P, c, za, zb, fa, fb);
     if (fb <= fa) return;
@@ -558,6 +786,14 @@ int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s) {
 
 void restrict_level(int P, const Lvl& fine, const Lvl& coarse, const double*, int blocks, cudaStream_t s, int za,
                     int zb) {
+    if (P == 3 && coarse.m == 27) {  // small levels only (big ones are faster grid-stride)
+        const int zlo = std::max(1, za < 0 ? 1 : za);
+        const int zhi = std::min(static_cast<int>(coarse.m), za < 0 ? static_cast<int>(coarse.m) : zb);
+        if (zhi <= zlo) return;
+        const size_t smem = 25 * (coarse.m - 1) * sizeof(double2);
+        k_restrict3_rows<<<dim3(coarse.m - 1, zhi - zlo), kRowThreads, smem, s>>>(fine, coarse, zlo);
+        return;
+    }
     unsigned fa, fb;
     span(P, coarse, za, zb, fa, fb);
     if (fb <= fa) return;

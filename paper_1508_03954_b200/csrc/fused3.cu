@@ -428,13 +428,13 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
 __global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int za, int zb) {
     const int mc = a.g.mc, m = a.g.m, zc = a.g.zc;
     const unsigned n1c = a.n1c;
-    const unsigned long long first = static_cast<unsigned long long>(za) * n1c * n1c;
-    const unsigned long long total = static_cast<unsigned long long>(zb - za) * n1c * n1c;
+    const unsigned first = static_cast<unsigned>(za) * n1c * n1c;  // coarse lattices < 2^32 points
+    const unsigned total = static_cast<unsigned>(zb - za) * n1c * n1c;
     const long long tilesXY = static_cast<long long>(a.g.nbx) * a.g.nby;
-    for (unsigned long long t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-        const unsigned long long f = first + t;
-        const int W0 = static_cast<int>(f % n1c), W1 = static_cast<int>((f / n1c) % n1c),
-                  W2 = static_cast<int>(f / (static_cast<unsigned long long>(n1c) * n1c));
+    for (unsigned t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const unsigned f = first + t;
+        const unsigned fr = f / n1c;
+        const int W0 = static_cast<int>(f - fr * n1c), W1 = static_cast<int>(fr % n1c), W2 = static_cast<int>(fr / n1c);
         if (W0 < 1 || W0 > mc - 1 || W1 < 1 || W1 > mc - 1 || W2 < 1 || W2 > mc - 1) continue;
         double2 acc = zero2();
         const int bz0 = (max(1, 3 * W2 - 2) - 1) / zc, bz1 = (min(m - 1, 3 * W2 + 2) - 1) / zc;

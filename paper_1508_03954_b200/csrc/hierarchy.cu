@@ -588,9 +588,13 @@ struct Hierarchy::Impl {
         return static_cast<T*>(ptr);
     }
 
+    // grid-stride launches: enough blocks that each thread has only a few
+    // points (memory-level parallelism for the bandwidth-bound level passes)
     int blocks_for(unsigned n) const {
         const long long need = (static_cast<long long>(n) + 255) / 256;
-        return static_cast<int>(std::max<long long>(1, std::min<long long>(need, 8LL * smCount)));
+        const char* cap = std::getenv("TMG_GRID_CAP");
+        const long long perSm = cap ? std::max(1, std::atoi(cap)) : 32;
+        return static_cast<int>(std::max<long long>(1, std::min<long long>(need, perSm * smCount)));
     }
 
     dev::Lvl make_level(int l, bool fine) {
