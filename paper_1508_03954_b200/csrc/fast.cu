@@ -4,6 +4,7 @@
 #include "fast.cuh"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace tmg {
 namespace fast {
@@ -720,8 +721,16 @@ void span(int P, const Lvl& v, int za, int zb, unsigned& fa, unsigned& fb) {
 }
 }  // namespace
 
+static int tri_mode() {  // TMG_TRI: bit 0 fine correction, bit 1 coarse top-down (A/B switch)
+    static int v = [] {
+        const char* e = std::getenv("TMG_TRI");
+        return e ? std::atoi(e) : 1;
+    }();
+    return v;
+}
+
 void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaStream_t s) {
-    if (P >= 2 && f.m >= 27) {
+    if (P >= 2 && f.m >= 27 && (tri_mode() & 1)) {
         const unsigned rows = f.n / f.n1;
         if (P == 2) k_topdown_tri<2, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, rows);
         else k_topdown_tri<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, rows);
@@ -733,7 +742,7 @@ void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaS
 }
 
 void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cudaStream_t s, int za, int zb) {
-    if (P >= 2 && c.m >= 81) {  // parent-cell triples (rows [za, zb) of planes for P = 3)
+    if (P >= 2 && c.m >= 81 && (tri_mode() & 2)) {  // parent-cell triples (rows [za, zb) of planes for P = 3)
         unsigned ra = 0, rb = c.n / c.n1;
         if (za >= 0) {
             const unsigned perPlane = P == 3 ? c.n1 : 1u;
