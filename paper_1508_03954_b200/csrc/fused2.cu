@@ -1,0 +1,275 @@
+// Fused fine pass for 2D (see fused2.cuh).
+
+#include "fused2.cuh"
+
+#include <algorithm>
+
+#include "lattice.cuh"
+
+namespace tmg {
+namespace fused2 {
+
+namespace {
+
+__device__ __forceinline__ double2 zero2() { return make_double2(0.0, 0.0); }
+__device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 mac(double2 acc, double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+}
+__device__ __forceinline__ double2 axpy(double w, double2 v, double2 acc) {
+    return make_double2(fma(w, v.x, acc.x), fma(w, v.y, acc.y));
+}
+__device__ __forceinline__ double2 lerpw(double2 c0, double2 c1, double w1) {
+    return make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
+}
+__device__ __forceinline__ double relw(int r) { return r == 1 ? (1.0 / 3.0) : r == 2 ? (2.0 / 3.0) : (r == 3 ? 1.0 : 0.0); }
+__device__ __forceinline__ double2 ldg(const double2* p) { return __ldg(p); }
+
+__device__ __forceinline__ double2 stage_sc(double2 smooth, double2 w, bool cp, int bpx, int hb) {
+    if (bpx) return cp ? zero2() : mul(w, smooth);
+    if ((hb && cp) || (w.x == 0.0 && w.y == 0.0)) return zero2();
+    return mul(w, smooth);
+}
+
+template <bool BPX>
+__global__ void __launch_bounds__(TX) k_fused2(const Args a) {
+    __shared__ double2 Pb[2][TX + 2];          // corrected rows (x halo at 0 and TX+1)
+    __shared__ double2 Vb[BPX ? 4 : 2][CXW];   // y-interpolated coarse rows (sc[, si])
+    __shared__ double2 tb[TX];                 // y-restricted columns
+
+    const int tid = threadIdx.x;
+    const int m = a.g.m, mc = a.g.mc;
+    const int x0 = 1 + blockIdx.x * TX, xe = min(x0 + TX, m);
+    const int y0 = 1 + blockIdx.y * a.g.yc, y1 = min(y0 + a.g.yc, m);
+    const int nrows = y1 - y0 + 2;
+    const long long n1 = a.n1;
+    const int cx0 = (x0 - 1) / 3;
+    const int x = x0 + tid;
+    const bool owned = x < xe;
+
+    // own column: coarse interpolation slot and weight
+    const int qxo = min(x / 3, mc - 1);
+    const int vo = qxo - cx0;
+    const double wxo = relw(x - 3 * qxo);
+    const bool cpx = x % 3 == 0;
+    // halo columns (threads 0 and 1): x0 - 1 and xe
+    const int hx = tid == 0 ? x0 - 1 : xe;
+    const bool haloThread = tid < 2;
+    const bool hin = haloThread && hx >= 1 && hx <= m - 1;
+    const int hq = min(max(hx, 0) / 3, mc - 1);
+    const int hv = hq - cx0;
+    const double hw = relw(hx - 3 * hq);
+    const bool hcpx = hx % 3 == 0;
+    const int hslot = tid == 0 ? 0 : (xe - x0) + 1;
+
+    auto computeV = [&](int yy, int vb) {  // coarse rows of fine row yy, for coarse columns cx0 + tid
+        if (tid >= CXW) return;
+        const int cx = min(cx0 + tid, mc);
+        const int qy = min(max(yy, 0) / 3, mc - 1);
+        const double w1y = relw(yy - 3 * qy);
+        const double2* s = a.scC + cx + static_cast<long long>(a.n1c) * qy;
+        Vb[vb][tid] = lerpw(ldg(s), ldg(s + a.n1c), w1y);
+        if (BPX) {
+            const double2* si = a.siC + cx + static_cast<long long>(a.n1c) * qy;
+            Vb[2 + vb][tid] = lerpw(ldg(si), ldg(si + a.n1c), w1y);
+        }
+    };
+
+    // restriction slots of this strip
+    const int Xa = x0 / 3, Xb = (xe + 1) / 3, nsx = Xb - Xa + 1;
+    const long long strip = blockIdx.x;
+    double2* part = a.partial + (static_cast<long long>(blockIdx.y) * a.g.sy * a.g.nbx + strip) * SXP;
+    const long long zStride = static_cast<long long>(a.g.nbx) * SXP;
+    const int zBase = (y0 - 1) / 3;
+    int zLow = zBase;
+    const int ti = TX - 1 - tid;  // slot tasks run away from the halo / coarse-row threads
+    auto flush = [&](int zi) {
+        if (ti < nsx) {
+            const int X = Xa + ti;
+            double2 acc = zero2();
+#pragma unroll
+            for (int kx = -2; kx <= 2; ++kx) {
+                const int fx = 3 * X + kx;
+                if (fx < x0 || fx >= xe) continue;
+                const double wx = kx == 0 ? 1.0 : (kx == 1 || kx == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
+                acc = axpy(wx, tb[fx - x0], acc);
+            }
+            part[zi * zStride + ti] = acc;
+        }
+    };
+    bool pend = false;
+    int ziPend = 0;
+
+    const double2 k0 = a.k.c[0], k1 = a.k.c[1], k2 = a.k.c[2];
+    const bool zeroSc = a.level < a.ellMin;
+    const bool injectOK = BPX && a.level > a.ellMin && cpx && owned;
+    double nmax = 0.0, nsum = 0.0;
+    double2 accLo = zero2(), accHi = zero2();
+    double2 Aprev = zero2(), Acur = zero2();
+
+    // row yy's inputs, loaded one step ahead
+    auto loadRow = [&](int yy, double2& u, double2& s, double2& hu, double2& hs) {
+        const bool yin = yy >= 1 && yy <= m - 1;
+        u = s = hu = hs = zero2();
+        if (yin && owned) {
+            const long long f = x + n1 * yy;
+            u = ldg(a.u + f);
+            s = ldg(a.sc + f);
+        }
+        if (yin && hin) {
+            const long long f = hx + n1 * yy;
+            hu = ldg(a.u + f);
+            hs = ldg(a.sc + f);
+        }
+    };
+    double2 uN, sN, huN, hsN;
+    loadRow(y0 - 1, uN, sN, huN, hsN);
+    double2 bq = (owned && y0 < y1) ? ldg(a.b + x + n1 * y0) : zero2();
+    computeV(y0 - 1, 0);
+    __syncthreads();
+
+    for (int it = 0; it < nrows; ++it) {
+        const int yy = y0 - 1 + it;
+        const int u3 = it % 3;  // yy % 3 (y0 = 1 mod 3)
+        const bool yin = yy >= 1 && yy <= m - 1;
+        const double2 uC = uN, sC = sN, huC = huN, hsC = hsN;
+        if (it + 1 < nrows) loadRow(yy + 1, uN, sN, huN, hsN);
+        const double2* V = Vb[it & 1];
+        double2* P = Pb[it & 1];
+        // ---- phase B: corrected row yy ----
+        double2 cOwn = zero2();
+        if (yin && owned) {
+            double2 scv = add(sC, lerpw(V[vo], V[vo + 1], wxo));
+            if (BPX && !(cpx && u3 == 0)) scv = sub(scv, lerpw(Vb[2 + (it & 1)][vo], Vb[2 + (it & 1)][vo + 1], wxo));
+            cOwn = add(uC, scv);
+        }
+        if (owned) P[tid + 1] = cOwn;
+        if (haloThread) {
+            double2 c = zero2();
+            if (yin && hin) {
+                double2 scv = add(hsC, lerpw(V[hv], V[hv + 1], hw));
+                if (BPX && !(hcpx && u3 == 0)) scv = sub(scv, lerpw(Vb[2 + (it & 1)][hv], Vb[2 + (it & 1)][hv + 1], hw));
+                c = add(huC, scv);
+            }
+            P[hslot] = c;
+        }
+        if (it + 1 < nrows) computeV(yy + 1, (it + 1) & 1);
+        __syncthreads();
+        // ---- phase C ----
+        if (pend) {
+            flush(ziPend);
+            pend = false;
+        }
+        const double2 E = add(P[tid], P[tid + 2]);
+        double2 T = mul(k1, cOwn);
+        T = mac(T, k2, E);
+        double2 U = mul(k0, cOwn);
+        U = mac(U, k1, E);
+        if (owned && yy >= y0 && yy < y1) a.uNew[x + n1 * yy] = cOwn;
+        if (it >= 2) {
+            const int yr = yy - 1;
+            const int kz = (u3 + 2) % 3;
+            const double2 hu = add(Aprev, T);
+            const double2 r = owned ? sub(bq, hu) : zero2();
+            if (owned && yr + 1 < y1) bq = ldg(a.b + x + n1 * (yr + 1));
+            const double m2 = fma(r.x, r.x, r.y * r.y);
+            nmax = fmax(nmax, m2);
+            nsum += m2;
+            const double2 smooth = mul(r, a.k.invDiag);
+            if (owned)
+                a.scNew[x + n1 * yr] =
+                    zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
+            if (BPX && kz == 0 && injectOK) a.sinextC[x / 3 + static_cast<long long>(a.n1c) * (yr / 3)] = mul(a.k.wRaw, smooth);
+            if (kz == 0) {
+                accLo = add(accLo, r);
+            } else if (kz == 1) {
+                accLo = axpy(2.0 / 3.0, r, accLo);
+                accHi = axpy(1.0 / 3.0, r, accHi);
+            } else {
+                accLo = axpy(1.0 / 3.0, r, accLo);
+                accHi = axpy(2.0 / 3.0, r, accHi);
+                tb[tid] = accLo;
+                accLo = accHi;
+                accHi = zero2();
+                pend = true;  // x-reduction on the next row's barrier
+                ziPend = zLow - zBase;
+                ++zLow;
+            }
+        }
+        Aprev = add(Acur, U);
+        Acur = T;
+    }
+    __syncthreads();
+    if (pend) flush(ziPend);
+    __syncthreads();
+    tb[tid] = accLo;
+    __syncthreads();
+    flush(zLow - zBase);
+    __syncthreads();
+    tb[tid] = accHi;
+    __syncthreads();
+    flush(zLow + 1 - zBase);
+    dev::block_norms(nmax, nsum, a.norms);
+}
+
+__global__ void __launch_bounds__(256) k_combine2(const Args a, double2* rc) {
+    const int mc = a.g.mc, m = a.g.m, yc = a.g.yc;
+    const unsigned n1c = a.n1c;
+    const unsigned total = n1c * n1c;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < total; f += gridDim.x * blockDim.x) {
+        const int W1 = static_cast<int>(f / n1c), W0 = static_cast<int>(f - static_cast<unsigned>(W1) * n1c);
+        if (W0 < 1 || W0 > mc - 1 || W1 < 1 || W1 > mc - 1) continue;
+        const int by0 = (max(1, 3 * W1 - 2) - 1) / yc, by1 = (min(m - 1, 3 * W1 + 2) - 1) / yc;
+        const int bx0 = (max(1, 3 * W0 - 2) - 1) / TX, bx1 = (min(m - 1, 3 * W0 + 2) - 1) / TX;
+        double2 acc = zero2();
+        for (int by = by0; by <= by1; ++by) {
+            const int yi = W1 - (by * yc) / 3;
+            for (int bx = bx0; bx <= bx1; ++bx) {
+                const int xi = W0 - (1 + bx * TX) / 3;
+                acc = add(acc, a.partial[((static_cast<long long>(by) * a.g.sy + yi) * a.g.nbx + bx) * SXP + xi]);
+            }
+        }
+        rc[f] = acc;
+    }
+}
+
+}  // namespace
+
+Geometry geometry(int m, int mc, int smCount) {
+    Geometry g{};
+    g.m = m;
+    g.mc = mc;
+    const int inner = std::max(1, m - 1);
+    g.nbx = (inner + TX - 1) / TX;
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused2<false>, TX, 0) != cudaSuccess || per < 1) per = 4;
+    const int resident = 2 * per * std::max(1, smCount);  // two waves of strips
+    const int want = std::max(1, (resident + g.nbx - 1) / g.nbx);
+    g.yc = std::max(3, ((inner + want - 1) / want + 2) / 3 * 3);
+    g.nby = (inner + g.yc - 1) / g.yc;
+    g.sy = g.yc / 3 + 2;
+    return g;
+}
+
+size_t partial_count(const Geometry& g) { return static_cast<size_t>(g.nby) * g.sy * g.nbx * SXP; }
+
+int blocks(const Geometry& g) { return g.nbx * g.nby; }
+
+void launch(const Args& a, cudaStream_t s) {
+    dim3 grid(a.g.nbx, a.g.nby);
+    if (a.bpx) k_fused2<true><<<grid, TX, 0, s>>>(a);
+    else k_fused2<false><<<grid, TX, 0, s>>>(a);
+}
+
+void combine(const Args& a, double2* rCoarse, cudaStream_t s) {
+    const unsigned total = a.n1c * a.n1c;
+    const unsigned nb = std::max(1u, std::min((total + 255) / 256, 4096u));
+    k_combine2<<<nb, 256, 0, s>>>(a, rCoarse);
+}
+
+}  // namespace fused2
+}  // namespace tmg

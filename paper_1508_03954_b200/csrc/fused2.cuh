@@ -1,0 +1,55 @@
+// Fused fine pass for 2D (fast precision): the 2D counterpart of fused3.
+//
+// One block owns a strip of TX columns and a y-chunk of rows and marches
+// the rows once: correction u + sc + P sc_{L-1} (- P si, BPX) of the row into
+// shared memory, the 9-point operator as two running row accumulators, the
+// residual, norms, Jacobi staging, BPX injection, and the restriction --
+// accumulated along y per column, reduced in x one step later on the next
+// row barrier -- into per-strip partials summed in fixed order by k_combine2.
+// Reads u, sc, b once and writes u, sc once: 80 B per fine vertex instead of
+// the 128 B of the unfused correct / residual / restrict kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fast.cuh"
+
+namespace tmg {
+namespace fused2 {
+
+constexpr int TX = 128;
+constexpr int SXP = TX / 3 + 3;        // restriction slots per strip (upper bound)
+constexpr int CXW = (TX + 1) / 3 + 3;  // coarse columns feeding the strip's prolongation
+
+struct Geometry {
+    int m, mc;    // fine / coarse cells per axis
+    int nbx, nby; // strips in x, row chunks in y
+    int yc;       // rows per chunk (multiple of 3)
+    int sy;       // coarse-row slots per chunk
+};
+
+struct Args {
+    double2* uNew;
+    double2* scNew;
+    const double2* u;
+    const double2* sc;
+    const double2* b;
+    const double2* scC;
+    const double2* siC;
+    double2* sinextC;
+    double2* partial;
+    double* norms;
+    unsigned n1, n1c;
+    Geometry g;
+    fast::LevelCoef k;
+    int bpx, hb, ellMin, level;
+};
+
+Geometry geometry(int m, int mc, int smCount);
+size_t partial_count(const Geometry& g);
+int blocks(const Geometry& g);
+void launch(const Args& a, cudaStream_t s);
+void combine(const Args& a, double2* rCoarse, cudaStream_t s);
+
+}  // namespace fused2
+}  // namespace tmg

@@ -23,6 +23,7 @@
 #include "amr.hpp"
 #include "exact_ops.cuh"
 #include "fast.cuh"
+#include "fused2.cuh"
 #include "fused3.cuh"
 #include "hierarchy.hpp"
 #include "lattice.cuh"
@@ -563,6 +564,9 @@ struct Hierarchy::Impl {
     fused3::Geometry geo{};
     double2* partial3 = nullptr;
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
+    bool fused2on = false;         // 2D fused fine pass (fast precision)
+    fused2::Geometry geo2{};
+    double2* partial2 = nullptr;
     int chainGrid = 0;              // cooperative coarse-chain grid (0: per-level launches)
     static constexpr unsigned kChainMaxN = 1u << 16;  // levels below this size join the chain
     int fusedResident = 3 * 148;
@@ -853,6 +857,52 @@ struct Hierarchy::Impl {
         for (int l = useChain ? top + 1 : 1; l < L; ++l)
             fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
+        if (P == 2 && fused2on) {
+            fused2::Args fa{};
+            dev::Lvl& F = lv[L];
+            fa.uNew = uAlt;
+            fa.scNew = scAlt;
+            fa.u = F.u;
+            fa.sc = F.sc;
+            fa.b = F.chi;
+            fa.scC = lv[L - 1].sc;
+            fa.siC = lv[L - 1].si;
+            fa.sinextC = lv[L - 1].sinext;
+            fa.partial = partial2;
+            fa.norms = partials;
+            fa.n1 = F.n1;
+            fa.n1c = lv[L - 1].n1;
+            fa.g = geo2;
+            fa.k = fc[L];
+            const Cplx w = omega_unmasked(pol, 0, n);
+            fa.k.wRaw = make_double2(w.real(), w.imag());
+            fa.bpx = bpx;
+            fa.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+            fa.ellMin = prob.ellMin;
+            fa.level = L;
+            fused2::launch(fa, stream);
+            if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+            fused2::combine(fa, lv[L - 1].rhat, stream);
+            std::swap(F.u, uAlt);
+            std::swap(F.sc, scAlt);
+            for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
+                if (l < L - 1 && l >= prob.ellMin)
+                    fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
+                fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+            }
+            if (useChain) {
+                if (top < L - 1 && top >= prob.ellMin)
+                    fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
+                ch.firstRestrict = 0;
+                ch.normBlocks = fused2::blocks(geo2);
+                fast::chain_up(P, ch, chainGrid, stream);
+            } else {
+                dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused2::blocks(geo2), dNorm);
+            }
+            TMG_CUDA(cudaGetLastError());
+            coarseUStale = true;
+            return;
+        }
         if (P == 3 && fused) {
             fused3::Args fa{};
             dev::Lvl& F = lv[L];
@@ -1079,7 +1129,20 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
                                                                               static_cast<int>(I.lv[I.L - 1].m),
                                                                               prob.zParts, I.fusedResident)));
     }
+    {
+        const char* f2 = std::getenv("TMG_FUSED2");
+        if (prob.fast && I.p == 2 && I.L >= 3 && !(f2 && f2[0] == '0')) {
+            I.fused2on = true;
+            I.geo2 = fused2::geometry(static_cast<int>(I.lv[I.L].m), static_cast<int>(I.lv[I.L - 1].m), I.smCount);
+            I.normBlocks = std::max(I.normBlocks, fused2::blocks(I.geo2));
+        }
+    }
     I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks));
+    if (I.fused2on) {
+        I.uAlt = I.alloc<double2>(I.lv[I.L].n);
+        I.scAlt = I.alloc<double2>(I.lv[I.L].n);
+        I.partial2 = I.alloc<double2>(fused2::partial_count(I.geo2));
+    }
     if (prob.fast) {
         const char* cz = std::getenv("TMG_CHAIN");
         int coop = 0;
