@@ -172,6 +172,27 @@ __global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, 
             const unsigned char cfl = c.cflag[cf];
             if (!(cfl & amr::kCellExists)) continue;
             const int a = (~e) & (NC - 1);  // corner of g in the cell
+            if ((c.vflag[f] & amr::kRegularChi) && restrictOn) {
+                // regular neighbourhood: fine vertices 3*cell + j in child order
+                for (int t = 0; t < NT; ++t) {
+                    int v[P];
+                    int code = 0, mul = 1;
+                    bool in = true;
+                    int tt = t;
+#pragma unroll
+                    for (int d = 0; d < P; ++d) {
+                        v[d] = 3 * cell[d] + tt % 3;
+                        tt /= 3;
+                        const int off = v[d] - 3 * g[d];
+                        in &= (off >= -2) & (off <= 2) & (v[d] >= 1) & (v[d] <= fl.m - 1);
+                        code += (off + 2) * mul;
+                        mul *= 5;
+                    }
+                    if (!in) continue;
+                    acc = xadd(acc, xscale(w5[code], fl.rhat[aflat<P>(fl, v)]));
+                }
+                continue;
+            }
             if (!(cfl & amr::kCellRefined)) {
                 // leaf: consistent-mass load on entering the cell (kernels.cpp:69-87)
                 double2 acc2 = cz();
@@ -234,6 +255,58 @@ __device__ __forceinline__ double2 cell_apply(const double2* __restrict__ x, con
     return s;
 }
 
+// All 2^P cells around an interior non-hanging vertex exist: the regular
+// exact path's shared-product evaluation (hierarchy.cu element_residual) on the
+// box strides -- the same per-cell corner order and cell order, bit for bit.
+template <int P, int ID>
+__device__ __forceinline__ double2 amr_ordered_sum(const double2 (&S)[1 << P]) {
+    double2 r = xneg(S[perm_cell(P, ID, 0)]);
+#pragma unroll
+    for (int i = 1; i < (1 << P); ++i) r = xsub(r, S[perm_cell(P, ID, i)]);
+    return r;
+}
+
+template <int P>
+__device__ __forceinline__ double2 regular_residual(const double2* __restrict__ x, int f, int sy, int sz,
+                                                    const double2 (&A)[8], int pid) {
+    constexpr int NC = 1 << P;
+    double2 S[NC];
+#pragma unroll
+    for (int j = 0; j < (P == 1 ? 3 : P == 2 ? 9 : 27); ++j) {
+        int del[P];
+        int off = 0, s = 0;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            del[d] = (j / (d == 0 ? 1 : d == 1 ? 3 : 9)) % 3 - 1;
+            off += del[d] * (d == 0 ? 1 : d == 1 ? sy : sz);
+            s |= (del[d] != 0 ? 1 : 0) << d;
+        }
+        const double2 prod = xmul(A[s], __ldg(x + (f + off)));
+#pragma unroll
+        for (int e = 0; e < NC; ++e) {
+            bool use = true;
+            int b = 0;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                const int bd = del[d] - ((e >> d) & 1) + 1;
+                use &= (bd == 0 || bd == 1);
+                b |= (bd & 1) << d;
+            }
+            if (use) S[e] = (b == 0) ? prod : xadd(S[e], prod);
+        }
+    }
+    if (P == 1) return amr_ordered_sum<P, 0>(S);
+    if (P == 2) return pid == 0 ? amr_ordered_sum<P, 0>(S) : amr_ordered_sum<P, (P >= 2 ? 1 : 0)>(S);
+    switch (pid) {
+        case 0: return amr_ordered_sum<P, 0>(S);
+        case 1: return amr_ordered_sum<P, (P >= 3 ? 1 : 0)>(S);
+        case 2: return amr_ordered_sum<P, (P >= 3 ? 2 : 0)>(S);
+        case 3: return amr_ordered_sum<P, (P >= 3 ? 3 : 0)>(S);
+        case 4: return amr_ordered_sum<P, (P >= 3 ? 4 : 0)>(S);
+        default: return amr_ordered_sum<P, (P >= 3 ? 5 : 0)>(S);
+    }
+}
+
 // ---- residual + touch_last / destroy_hanging --------------------------------
 template <int P>
 __global__ void __launch_bounds__(256) k_amr_residual(AResArgs a) {
@@ -250,7 +323,13 @@ __global__ void __launch_bounds__(256) k_amr_residual(AResArgs a) {
         const int pid = perm_id<P>(g);
         double2 r = cz(), rh = cz();
         bool first = true;
-        for (int i = 0; i < NC; ++i) {
+        const bool general = hang || bnd;
+        if (!general) {  // every cell around g exists
+            const int sy = c.n1[0], sz = c.n1[0] * c.n1[1];
+            r = regular_residual<P>(c.u, static_cast<int>(f), sy, sz, a.k.A, pid);
+            rh = regular_residual<P>(c.uhat, static_cast<int>(f), sy, sz, a.k.A, pid);
+        }
+        for (int i = 0; i < NC && general; ++i) {
             const int e = perm_cell(P, pid, i);
             int cell[P];
             bool ok = true;
@@ -625,6 +704,47 @@ std::vector<HostLevel> build_sphere_tree(int p, int base, int L) {
     return lv;
 }
 
+void mark_regular_chi(std::vector<HostLevel>& lv, int p) {
+    const int L = static_cast<int>(lv.size()) - 1;
+    const int nc = 1 << p;
+    for (int l = 0; l < L; ++l) {
+        HostLevel& h = lv[l];
+        const HostLevel& fh = lv[l + 1];
+        int g[3] = {0, 0, 0};
+        for (long long f = 0; f < h.n; ++f) {
+            if (!(h.vflag[f] & kExists)) continue;
+            box_unflat(h, p, f, g);
+            bool reg = true;
+            for (int e = 0; e < nc && reg; ++e) {
+                int c[3] = {0, 0, 0};
+                bool in = true;
+                for (int d = 0; d < p; ++d) {
+                    c[d] = g[d] - 1 + ((e >> d) & 1);
+                    in &= c[d] >= 0 && c[d] <= h.m - 1;
+                }
+                if (!in) continue;
+                const long long cf = box_flat(h, p, c);
+                reg = cf >= 0 && (h.cflag[cf] & kCellExists) && (h.cflag[cf] & kCellRefined);
+            }
+            int v[3] = {0, 0, 0};
+            const int K = p == 1 ? 5 : p == 2 ? 25 : 125;
+            for (int k = 0; k < K && reg; ++k) {
+                int kk = k;
+                bool interior = true;
+                for (int d = 0; d < p; ++d) {
+                    v[d] = 3 * g[d] + kk % 5 - 2;
+                    kk /= 5;
+                    interior &= v[d] >= 1 && v[d] <= fh.m - 1;
+                }
+                if (!interior) continue;
+                const long long vf = box_flat(fh, p, v);
+                reg = vf >= 0 && (fh.vflag[vf] & kExists) && fh.estar[vf] == 0;
+            }
+            if (reg) h.vflag[f] |= kRegularChi;
+        }
+    }
+}
+
 }  // namespace amr
 
 // ============================================================================
@@ -674,6 +794,7 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
     if (prob.fast) throw UnsupportedConfigError("adaptive trees run in precision = exact only");
     if (base_ < 1) throw ConfigError("sphere refinement needs a base level >= 1");
     host_ = amr::build_sphere_tree(p_, base_, L_);
+    amr::mark_regular_chi(host_, p_);
     for (const amr::HostLevel& h : host_)
         for (long long f = 0; f < h.n; ++f) {
             const unsigned char v = h.vflag[f];
@@ -757,6 +878,14 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
     if (p_ == 1) build_rhs<1>();
     else if (p_ == 2) build_rhs<2>();
     else build_rhs<3>();
+    {  // finest level: every cell is a leaf, chi = the load vector in cell order, constant
+        const adev::ALvl& F = D.lv[L_];
+        const int nb = blocks_for_n(F.n, smCount_);
+        if (p_ == 1) adev::k_amr_chi<1><<<nb, 256, 0, stream_>>>(F, F, D.kc[L_], D.weights, 0);
+        else if (p_ == 2) adev::k_amr_chi<2><<<nb, 256, 0, stream_>>>(F, F, D.kc[L_], D.weights, 0);
+        else adev::k_amr_chi<3><<<nb, 256, 0, stream_>>>(F, F, D.kc[L_], D.weights, 0);
+        AMR_CUDA(cudaGetLastError());
+    }
     AMR_CUDA(cudaStreamSynchronize(stream_));
 }
 
@@ -826,8 +955,9 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
     for (int l = L_; l >= 0; --l) {
         const int nb = blocks_for_n(D.lv[l].n, smCount_);
         const adev::ALvl& fine = l < L_ ? D.lv[l + 1] : D.lv[l];
-        adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.kc[l], D.weights,
-                                                     (l < L_ && l + 1 > prob_.ellMin) ? 1 : 0);
+        if (l < L_)  // finest level: chi is the constant load vector (built at setup)
+            adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.kc[l], D.weights,
+                                                         l + 1 > prob_.ellMin ? 1 : 0);
         a.lv = D.lv[l];
         a.par = l > 0 ? D.lv[l - 1] : D.lv[0];
         a.k = D.kc[l];
@@ -931,7 +1061,7 @@ void AmrTree::get_flags(int level, unsigned char* flags, signed char* succ, unsi
         const long long ff = full_flat(p_, h.m, g);
         if (cells) cells[ff] = h.cflag[f];
         if (!(h.vflag[f] & amr::kExists)) continue;
-        if (flags) flags[ff] = h.vflag[f];
+        if (flags) flags[ff] = h.vflag[f] & 31;  // classification bits only
         if (succ) succ[ff] = h.succ[f];
     }
 }

@@ -38,7 +38,7 @@ struct LevelConst;  // exact_ops.cuh
 
 namespace amr {
 
-enum : unsigned char { kExists = 1, kHanging = 2, kRefined = 4, kBoundary = 8, kCPoint = 16 };
+enum : unsigned char { kExists = 1, kHanging = 2, kRefined = 4, kBoundary = 8, kCPoint = 16, kRegularChi = 32 };
 enum : unsigned char { kCellExists = 1, kCellRefined = 2 };
 
 // One level: a box of the (3^l+1)^p lattice, axis 0 fastest.
@@ -59,6 +59,12 @@ struct HostLevel {
 // reference harness's refine_all_leaves(level, sphereOnly), applied to
 // levels base .. L-1 in turn; oracle/refdriver.cpp).
 std::vector<HostLevel> build_sphere_tree(int p, int base, int L);
+
+// kRegularChi: every cell around the vertex is refined and every interior
+// fine vertex within two fine steps is touched last as the lower corner of
+// its own cell (finish corner 0), so chi is the plain restriction in the
+// regular tree's order (no loads, no finish-corner lookups).
+void mark_regular_chi(std::vector<HostLevel>& lv, int p);
 
 }  // namespace amr
 
