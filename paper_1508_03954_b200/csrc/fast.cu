@@ -435,6 +435,11 @@ constexpr int kZch = 48;
 __device__ __forceinline__ double2 ldcg(const double2* p) { return __ldcg(p); }
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
+    if (gridDim.x == 1) {  // single-CTA chain (tiny hierarchies): a block barrier suffices
+        __threadfence_block();
+        __syncthreads();
+        return;
+    }
     __syncthreads();
     if (threadIdx.x == 0) {
         const unsigned target = gen + 1;

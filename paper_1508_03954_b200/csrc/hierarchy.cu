@@ -852,7 +852,7 @@ struct Hierarchy::Impl {
             ch.bar = chainBar;
             ch.normPartials = partials;
             ch.normOut = dNorm;
-            fast::chain_down(P, ch, chainGrid, stream);
+            fast::chain_down(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
         }
         for (int l = useChain ? top + 1 : 1; l < L; ++l)
             fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
@@ -895,7 +895,7 @@ struct Hierarchy::Impl {
                     fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
                 ch.firstRestrict = 0;
                 ch.normBlocks = fused2::blocks(geo2);
-                fast::chain_up(P, ch, chainGrid, stream);
+                fast::chain_up(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
             } else {
                 dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused2::blocks(geo2), dNorm);
             }
@@ -941,7 +941,7 @@ struct Hierarchy::Impl {
                     fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
                 ch.firstRestrict = 0;
                 ch.normBlocks = fused3::blocks(geo);
-                fast::chain_up(P, ch, chainGrid, stream);
+                fast::chain_up(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
             } else {
                 dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused3::blocks(geo), dNorm);
             }
@@ -959,7 +959,7 @@ struct Hierarchy::Impl {
         if (useChain) {
             ch.firstRestrict = 1;  // fine = lv[top + 1] into lv[top]
             ch.normBlocks = nb;
-            fast::chain_up(P, ch, chainGrid, stream);
+            fast::chain_up(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
         } else {
             dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, nb, dNorm);
         }
@@ -991,6 +991,15 @@ struct Hierarchy::Impl {
             else if (p == 2) cycle_exact<2>(pol, n, timed);
             else cycle_exact<3>(pol, n, timed);
         }
+    }
+
+    // a chain whose levels hold few points runs in one CTA (block barriers only)
+    bool chainSmall(int top) const {
+        unsigned long long pts = 0;
+        for (int l = 1; l <= top; ++l) pts += lv[l].n;
+        const char* e = std::getenv("TMG_CHAIN_SMALL");
+        const unsigned long long lim = e ? std::strtoull(e, nullptr, 10) : 0ull;  // measured: grid chains win
+        return pts <= lim;
     }
 
     int launches_per_cycle() const {
