@@ -91,6 +91,17 @@ def ncu_traffic(workload: str, precision: str, mode: str):
         return None
 
 
+def settle(h, pol, D=None, ctx=None, seconds=0.3, **kw):
+    """Untimed cycles for ~`seconds` before the warm-up: brings SM / HBM clocks to
+    their steady state so short timed regions are not measured on a ramp.  The
+    cycle count is agreed over ranks (slab cycles exchange data collectively)."""
+    ms = float(h.time_cycles(pol, 1, 1, **kw)[0])
+    if D is not None and ctx is not None:
+        ms = D.reduce_max(ctx, ms)
+    count = int(min(2000, max(1, seconds * 1e3 / max(ms, 1e-3))))
+    h.time_cycles(pol, 1, count, **kw)
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -115,11 +126,27 @@ class ClockSampler:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
+            # nvidia-smi needs ~0.1-0.5 s to start: wait for its first sample so the
+            # (often short) timed region is actually covered
+            t0 = time.time()
+            while time.time() - t0 < 3.0:
+                self.fh.flush()
+                if os.path.getsize(self.path) > 0:
+                    break
+                time.sleep(0.01)
+            self.start_lines = self._lines()
         except Exception:
             self.proc = None
         return self
+
+    def _lines(self):
+        try:
+            with open(self.path) as f:
+                return sum(1 for _ in f)
+        except Exception:
+            return 0
 
     def __exit__(self, *a):
         if self.proc:
@@ -134,7 +161,10 @@ class ClockSampler:
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         try:
-            for line in open(self.path):
+            lines = open(self.path).read().splitlines()
+            # samples taken while the timed region ran (plus the one just before it)
+            lines = lines[max(0, getattr(self, "start_lines", 1) - 1):]
+            for line in lines:
                 f = [x.strip() for x in line.split(",")]
                 if len(f) < 8:
                     continue
@@ -243,6 +273,7 @@ def run_amr(args, w):
                     rhs_sphere=True, precision="exact", max_vertices=10 ** 10, device=ctx.local,
                     sphere_levels=w["sphere_levels"])
     pol = T.Policy(kind=w["omega"], omega_s=w["omega_s"])
+    settle(h, pol, D, ctx)
     h.time_cycles(pol, 1, args.warmup)
     D.barrier(ctx)
     with ClockSampler(ctx.local) as clk:
@@ -326,11 +357,13 @@ def main():
         uid = D.broadcast_bytes(ctx, T.nccl_unique_id() if rank == 0 else None)
         h = T.Slabs(w["level"], phi, chi="seeded", rhs_seed=RHS_SEED, rank=rank, world=world, nccl_id=uid,
                     device=local)
+        settle(h, pol, D, ctx)
         h.time_cycles(pol, 1, args.warmup)
     else:
         h = T.Hierarchy(w["dim"], w["level"], phi=phi, chi="seeded", rhs_seed=RHS_SEED, precision=args.precision,
                         max_vertices=10 ** 10, device=local)
         # warm-up cycles (untimed), then K timed cycles with CUDA events on the library stream
+        settle(h, pol, D, ctx, flush_l2=False)
         h.time_cycles(pol, 1, args.warmup, flush_l2=False)
 
     def barrier():
