@@ -36,3 +36,44 @@ def test_fast_and_exact_agree_on_a_3d_run(tmg):
         assert abs(a.max_norm - b.max_norm) <= 1e-10 * a.max_norm
     ue, uf = h_e.field(4, "u"), h_f.field(4, "u")
     assert np.abs(ue - uf).max() <= 1e-10 * np.abs(ue).max()
+
+
+def _fields_after(tmg, env, dim, level, phi, cycles, bpx=False):
+    import os
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        h = tmg.Hierarchy(dim, level, phi=phi, chi="seeded", precision="fast", max_vertices=10 ** 10)
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+    pol = tmg.Policy("undamped", 0.5, bpx=True) if bpx else tmg.Policy("exponential", 0.6)
+    norms = []
+    for n in range(1, cycles + 1):
+        st = h.td_bpx(pol, n) if bpx else h.td_add(pol, n)
+        norms.append((st.max_norm, st.euclid_norm, st.h_norm))
+    return np.array(norms), h.field(level, "u")
+
+
+@pytest.mark.parametrize("dim,level,bpx", [(3, 5, False), (3, 4, True), (2, 6, False), (2, 5, True)])
+def test_coarse_chain_bitwise_equals_per_level_launches(tmg, dim, level, bpx):
+    """The cooperative coarse chain (fast.cu k_chain_*) computes the per-level
+    kernels' values in the same order: identical iterates, norms equal up to
+    the final reduction tree."""
+    a_n, a_u = _fields_after(tmg, {"TMG_CHAIN": "1"}, dim, level, 400 + 200j, 5, bpx)
+    b_n, b_u = _fields_after(tmg, {"TMG_CHAIN": "0"}, dim, level, 400 + 200j, 5, bpx)
+    assert np.array_equal(a_u, b_u)
+    np.testing.assert_allclose(a_n, b_n, rtol=1e-13)
+
+
+@pytest.mark.parametrize("level,bpx", [(5, False), (6, True)])
+def test_fused2_matches_unfused_2d(tmg, level, bpx):
+    """2D fused fine pass vs the three-kernel path: same cycle, different
+    rounding (FMA / summation grouping) -- agreement to ~1e-12."""
+    a_n, a_u = _fields_after(tmg, {"TMG_FUSED2": "1"}, 2, level, 100 + 50j, 6, bpx)
+    b_n, b_u = _fields_after(tmg, {"TMG_FUSED2": "0"}, 2, level, 100 + 50j, 6, bpx)
+    np.testing.assert_allclose(a_n, b_n, rtol=1e-11)
+    assert np.max(np.abs(a_u - b_u)) <= 1e-11 * np.max(np.abs(b_u))
