@@ -65,11 +65,22 @@ def lattice(level, dim):
     return (3 ** level + 1) ** dim
 
 
+def fine_bytes_per_vertex(w, precision):
+    """Algorithmic HBM bytes per fine vertex of the fine pass.
+    counts 80 B (u, sc, b read; u, sc written).  The fused fast passes keep the
+    fine state as v = u + sc (fused3.cuh), so the minimum is 64 B (v, b read;
+    v, sc written); the exact pass is not fused (176 B)."""
+    if precision == "exact":
+        return 176
+    return 64 if w["dim"] >= 2 else 128
+
+
 def algorithmic_bytes(w, precision):
-    """B = 80 N_L + 200 sum_{l<L} N_l (complex128 lattice sizes)."""
+    """B = b_f N_L + 200 sum_{l<L} N_l (complex128 lattice sizes)."""
     NL = lattice(w["level"], w["dim"])
     coarse = sum(lattice(l, w["dim"]) for l in range(1, w["level"]))
-    return 80 * NL + 200 * coarse, 80 * NL
+    bf = fine_bytes_per_vertex(w, precision)
+    return bf * NL + 200 * coarse, bf * NL
 
 
 def fine_kernel_label(w, precision):
@@ -385,14 +396,15 @@ def main():
     B_total, B_fine = algorithmic_bytes(w, args.precision)
     if mode == "slabs":  # this rank's share of the fine level
         z0, z1 = h.owned_planes()
-        B_fine = 80 * (z1 - z0) * (3 ** w["level"] + 1) ** 2
+        B_fine = fine_bytes_per_vertex(w, args.precision) * (z1 - z0) * (3 ** w["level"] + 1) ** 2
         B_total = B_total * (z1 - z0) / (3 ** w["level"] - 1)
         launches_per_cycle = 2 * w["level"] + 6
     peak, peak_kind = peaks()
     achieved = B_fine / (fine_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None, "kernel": fine_kernel_label(w, args.precision) +
-                f", {B_fine / 1e9:.2f} GB algorithmic per cycle (80 B per fine vertex)",
+                f", {B_fine / 1e9:.2f} GB algorithmic per cycle "
+                f"({fine_bytes_per_vertex(w, args.precision)} B per fine vertex)",
                 "peak_kind": peak_kind, "whole_cycle_GBps": B_total / (ms_per_step / 1e3) / 1e9}
 
     tr = ncu_traffic(args.workload, args.precision, mode) if mode != "slabs" or world == 1 else None

@@ -111,23 +111,16 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     double2 accLo = zero2(), accHi = zero2();
     double2 Aprev = zero2(), Acur = zero2();
 
-    // row yy's inputs, loaded one step ahead
-    auto loadRow = [&](int yy, double2& u, double2& s, double2& hu, double2& hs) {
+    // row yy's state v = u + sc (fused3.cuh "v-form"), loaded one step ahead
+    auto loadRow = [&](int yy, double2& u, double2& hu) {
         const bool yin = yy >= 1 && yy <= m - 1;
-        u = s = hu = hs = zero2();
-        if (yin && owned) {
-            const long long f = x + n1 * yy;
-            u = ldg(a.u + f);
-            s = ldg(a.sc + f);
-        }
-        if (yin && hin) {
-            const long long f = hx + n1 * yy;
-            hu = ldg(a.u + f);
-            hs = ldg(a.sc + f);
-        }
+        u = hu = zero2();
+        if (yin && owned) u = ldg(a.u + x + n1 * yy);
+        if (yin && hin) hu = ldg(a.u + hx + n1 * yy);
     };
-    double2 uN, sN, huN, hsN;
-    loadRow(y0 - 1, uN, sN, huN, hsN);
+    double2 uN, huN;
+    loadRow(y0 - 1, uN, huN);
+    double2 cPrev = zero2();
     double2 bq = (owned && y0 < y1) ? ldg(a.b + x + n1 * y0) : zero2();
     computeV(y0 - 1, 0);
     __syncthreads();
@@ -136,14 +129,14 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         const int yy = y0 - 1 + it;
         const int u3 = it % 3;  // yy % 3 (y0 = 1 mod 3)
         const bool yin = yy >= 1 && yy <= m - 1;
-        const double2 uC = uN, sC = sN, huC = huN, hsC = hsN;
-        if (it + 1 < nrows) loadRow(yy + 1, uN, sN, huN, hsN);
+        const double2 uC = uN, huC = huN;
+        if (it + 1 < nrows) loadRow(yy + 1, uN, huN);
         const double2* V = Vb[it & 1];
         double2* P = Pb[it & 1];
         // ---- phase B: corrected row yy ----
         double2 cOwn = zero2();
         if (yin && owned) {
-            double2 scv = add(sC, lerpw(V[vo], V[vo + 1], wxo));
+            double2 scv = lerpw(V[vo], V[vo + 1], wxo);
             if (BPX && !(cpx && u3 == 0)) scv = sub(scv, lerpw(Vb[2 + (it & 1)][vo], Vb[2 + (it & 1)][vo + 1], wxo));
             cOwn = add(uC, scv);
         }
@@ -151,7 +144,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         if (haloThread) {
             double2 c = zero2();
             if (yin && hin) {
-                double2 scv = add(hsC, lerpw(V[hv], V[hv + 1], hw));
+                double2 scv = lerpw(V[hv], V[hv + 1], hw);
                 if (BPX && !(hcpx && u3 == 0)) scv = sub(scv, lerpw(Vb[2 + (it & 1)][hv], Vb[2 + (it & 1)][hv + 1], hw));
                 c = add(huC, scv);
             }
@@ -169,7 +162,6 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         T = mac(T, k2, E);
         double2 U = mul(k0, cOwn);
         U = mac(U, k1, E);
-        if (owned && yy >= y0 && yy < y1) a.uNew[x + n1 * yy] = cOwn;
         if (it >= 2) {
             const int yr = yy - 1;
             const int kz = (u3 + 2) % 3;
@@ -180,9 +172,11 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
             nmax = fmax(nmax, m2);
             nsum += m2;
             const double2 smooth = mul(r, a.k.invDiag);
-            if (owned)
-                a.scNew[x + n1 * yr] =
-                    zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
+            const double2 scn = zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
+            if (owned) {
+                a.scNew[x + n1 * yr] = scn;
+                a.uNew[x + n1 * yr] = add(cPrev, scn);  // next state v of row yr
+            }
             if (BPX && kz == 0 && injectOK) a.sinextC[x / 3 + static_cast<long long>(a.n1c) * (yr / 3)] = mul(a.k.wRaw, smooth);
             if (kz == 0) {
                 accLo = add(accLo, r);
@@ -202,6 +196,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         }
         Aprev = add(Acur, U);
         Acur = T;
+        cPrev = cOwn;
     }
     __syncthreads();
     if (pend) flush(ziPend);

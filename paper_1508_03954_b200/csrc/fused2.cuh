@@ -6,8 +6,9 @@
 // residual, norms, Jacobi staging, BPX injection, and the restriction --
 // accumulated along y per column, reduced in x one step later on the next
 // row barrier -- into per-strip partials summed in fixed order by k_combine2.
-// Reads u, sc, b once and writes u, sc once: 80 B per fine vertex instead of
-// the 128 B of the unfused correct / residual / restrict kernels.
+// The finest level keeps v = u + sc (the "v-form" of fused3.cuh): v and b
+// are read once, v and sc written once -- 64 B per fine vertex instead of the
+// 128 B of the unfused correct / residual / restrict kernels.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -29,10 +30,10 @@ struct Geometry {
 };
 
 struct Args {
-    double2* uNew;
-    double2* scNew;
-    const double2* u;
-    const double2* sc;
+    double2* uNew;        // next state v
+    double2* scNew;       // staged correction (write-only, field API)
+    const double2* u;     // state v
+    const double2* sc;    // unused (kept for layout symmetry)
     const double2* b;
     const double2* scC;
     const double2* siC;

@@ -98,8 +98,10 @@ constexpr unsigned kCBytes = CX * CY * 2 * sizeof(double2);
 constexpr int kV = (HY * CX + 7) / 8 * 8;         // z- and y-interpolated coarse rows
 constexpr int NT = TX * TY;
 
+// Stage = the halo'd tile of the fine state v (= u + sc, see fused3.cuh) and
+// the two coarse sc (si) planes it prolongs from.
 template <bool BPX>
-__host__ __device__ constexpr int stage_elems() { return 2 * kPlane + (BPX ? 2 : 1) * kC; }
+__host__ __device__ constexpr int stage_elems() { return kPlane + (BPX ? 2 : 1) * kC; }
 
 template <bool BPX>
 __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
@@ -122,16 +124,15 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
     const int nplanes = z1 - z0 + 2;
     const long long sy = a.n1, sz = static_cast<long long>(a.n1) * a.n1;
     const int cx0 = (x0 - 1) / 3, cy0 = (y0 - 1) / 3;
-    constexpr unsigned stageBytes = 2 * kTileBytes + (BPX ? 2 : 1) * kCBytes;
+    constexpr unsigned stageBytes = kTileBytes + (BPX ? 2 : 1) * kCBytes;
 
     auto issue = [&](int stage, int zz) {
         double2* st = ring + stage * SE;
         const int cz = min(zz / 3, mc - 1);
         mbar_expect_tx(&bar[stage], stageBytes);
         tma_load3(st, &mapU, 2 * (x0 - 1), y0 - 1, zz, &bar[stage]);
-        tma_load3(st + kPlane, &mapS, 2 * (x0 - 1), y0 - 1, zz, &bar[stage]);
-        tma_load3(st + 2 * kPlane, &mapC, 2 * cx0, cy0, cz, &bar[stage]);
-        if (BPX) tma_load3(st + 2 * kPlane + kC, &mapI, 2 * cx0, cy0, cz, &bar[stage]);
+        tma_load3(st + kPlane, &mapC, 2 * cx0, cy0, cz, &bar[stage]);
+        if (BPX) tma_load3(st + kPlane + kC, &mapI, 2 * cx0, cy0, cz, &bar[stage]);
     };
 
     if (tid == 0) {
@@ -192,7 +193,7 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
     auto computeV = [&](int stage, int zz, int vb) {
         const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
         const double w1z = rz == 1 ? (1.0 / 3.0) : rz == 2 ? (2.0 / 3.0) : (rz == 3 ? 1.0 : 0.0);
-        const double2* C = ring + stage * SE + 2 * kPlane;
+        const double2* C = ring + stage * SE + kPlane;
         const double2 a0 = lerpw(C[vcOff], C[vcOff + CX], w1y);
         const double2 a1 = lerpw(C[vcOff + CX * CY], C[vcOff + CX * CY + CX], w1y);
         Vb[vb * kV + vt] = lerpw(a0, a1, w1z);
@@ -312,14 +313,13 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
         mbar_wait(&bar[stage], parity);
         if (hasNext) mbar_wait(&bar[nstage], nparity);
         const bool zin = zz >= 1 && zz <= m - 1;
-        const double2* Ut = ring + stage * SE;
-        const double2* Sc = Ut + kPlane;
+        const double2* Ut = ring + stage * SE;  // fine state v = u + sc of plane zz
         const double2* V = Vb + (it & 1) * kV;
         double2* P = Pb + (it & 1) * kPlane;
         // ---- phase B ----
         double2 cOwn;
         {
-            double2 scv = add(Sc[po], lerpw(V[vo], V[vo + 1], wxo));
+            double2 scv = lerpw(V[vo], V[vo + 1], wxo);
             if (BPX && !(cpxy && u == 0)) {
                 const double2* Vi = Vb + (2 + (it & 1)) * kV;
                 scv = sub(scv, lerpw(Vi[vo], Vi[vo + 1], wxo));
@@ -328,7 +328,7 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
             P[po] = cOwn;
         }
         if (task == 1) {
-            double2 scv = add(Sc[pr], lerpw(V[vr], V[vr + 1], wxr));
+            double2 scv = lerpw(V[vr], V[vr + 1], wxr);
             if (BPX && !(cpr && u == 0)) {
                 const double2* Vi = Vb + (2 + (it & 1)) * kV;
                 scv = sub(scv, lerpw(Vi[vr], Vi[vr + 1], wxr));
@@ -360,8 +360,6 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
         double2 Uo = mul(k0, cOwn);
         Uo = mac(Uo, k1, E);
         Uo = mac(Uo, k2, K);
-        if (owned && zz >= z0 && zz < z1) *uPtr = cOwn;
-        if (zz >= z0) uPtr += sz;
         if (it >= 2) {
             constexpr int kz = (u + 2) % 3;  // plane z = zz - 1
             const double2 hu = add(Aprev, T);
@@ -372,8 +370,15 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
             nmax = fmax(nmax, m2);
             nsum += m2;
             const double2 smooth = mul(r, a.k.invDiag);
-            if (owned) *sPtr = zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpxy && kz == 0, BPX ? 1 : 0, a.hb);
+            const double2 scn = zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpxy && kz == 0, BPX ? 1 : 0, a.hb);
+            if (owned) {
+                *sPtr = scn;
+                // next cycle's state v = u + sc of plane zz - 1 (its corrected u is
+                // still in the other P buffer: rewritten only in the next phase B)
+                *uPtr = add(Pb[((it + 1) & 1) * kPlane + po], scn);
+            }
             sPtr += sz;
+            uPtr += sz;
             if (BPX && kz == 0 && injectOK) {
                 *siPtr = mul(a.k.wRaw, smooth);
                 siPtr += static_cast<long long>(a.n1c) * a.n1c;

@@ -1,22 +1,29 @@
 // Fused fine pass for 3D, precision = fast (K2F in DESIGN.md §3).
 //
 // One kernel does, per fine vertex, everything the cycle needs on the finest
-// level: the top-down correction u += sc + P sc_{L-1} (- P si_{L-1}, BPX),
-// the residual r = b - H u of the corrected iterate, the norm partials, the
-// Jacobi staging sc = omega r / diag, the BPX injection into si_{L-1} and
-// the restriction R r into the coarse residual.  HBM traffic is the
-// algorithmic minimum of SURVEY §8d: u, sc, b read once, u, sc written once
-// (80 B per fine vertex); u and sc are double-buffered so halo reads never
-// race with the owner's writes.
+// level: the top-down correction, the residual r = b - H u of the corrected
+// iterate, the norm partials, the Jacobi staging sc = omega r / diag, the
+// BPX injection into si_{L-1} and the restriction R r into the coarse
+// residual.
 //
-// Structure: 2D tiles (32 x 12 columns) marching in z over a chunk of planes.
-// The halo'd (34 x 14) u_old / sc_old planes arrive by TMA
-// (cp.async.bulk.tensor.3d) into a 4-stage mbarrier ring; the block forms
-// the corrected plane in shared memory, every column keeps its centre /
-// edge / corner plane sums in registers (z-marching), and the restriction is
-// evaluated separably (x, then y, then z accumulators) into per-tile partial
-// sums that a small combine kernel adds in a fixed order, so the coarse
-// residual is deterministic without atomics.
+// Fine state ("v-form"): the finest level keeps v = u + sc, the iterate with
+// its staged Jacobi correction already applied, plus sc itself for the
+// field API (u = v - sc on request).  The reference applies the staged sc at
+// the next touch-first (u += sc + P sc_{L-1}, cycles.cpp:119-122); applying it
+// when it is formed is the same update in a different rounding order, and
+// the next cycle then needs only v:  u' = v + P sc_{L-1} (- P si_{L-1}).
+// HBM traffic per fine vertex: v and b read, v and sc written = 64 B
+// (80 B with the (u, sc) pair).  v is double-buffered so halo reads never
+// race with the owner's writes; sc is write-only.
+//
+// Structure: 2D tiles (32 x 8 columns) marching in z over a chunk of planes.
+// The halo'd (34 x 10) v planes arrive by TMA (cp.async.bulk.tensor.3d) into
+// a 4-stage mbarrier ring; the block forms the corrected plane in shared
+// memory, every column keeps its centre / edge / corner plane sums in
+// registers (z-marching), and the restriction is evaluated separably (x,
+// then y, then z accumulators) into per-tile partial sums that a small
+// combine kernel adds in a fixed order, so the coarse residual is
+// deterministic without atomics.
 #pragma once
 
 #include <cuda.h>
@@ -31,7 +38,10 @@ namespace fused3 {
 #ifndef TMG_FUSED_TY
 #define TMG_FUSED_TY 8
 #endif
-constexpr int TX = 32, TY = TMG_FUSED_TY, STAGES = 4;
+#ifndef TMG_FUSED_STAGES
+#define TMG_FUSED_STAGES 4
+#endif
+constexpr int TX = 32, TY = TMG_FUSED_TY, STAGES = TMG_FUSED_STAGES;
 constexpr int HX = TX + 2, HY = TY + 2;
 constexpr int SX = TX / 3 + 3, SY = TY / 3 + 3;  // restriction slots per tile (upper bounds)
 constexpr int CX = (TX + 1) / 3 + 2, CY = (TY + 1) / 3 + 2;  // coarse tile feeding the prolongation

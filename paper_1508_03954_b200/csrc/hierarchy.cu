@@ -370,7 +370,7 @@ __global__ void k_random_fine(Lvl c, unsigned long long seed) {  // cycles.cpp:8
 
 // u_l(W) = u_{l+1}(3W) on non-boundary vertices (injection consistency).
 template <int P>
-__global__ void k_inject_u(Lvl c, Lvl fine) {
+__global__ void k_inject_u(Lvl c, Lvl fine, int fineVForm) {
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
         int idx[P];
         unflat<P>(f, c.n1, idx);
@@ -378,8 +378,15 @@ __global__ void k_inject_u(Lvl c, Lvl fine) {
         int fi[P];
 #pragma unroll
         for (int d = 0; d < P; ++d) fi[d] = 3 * idx[d];
-        c.u[f] = fine.u[flat<P>(fi, fine.n1)];
+        const unsigned ff = flat<P>(fi, fine.n1);
+        c.u[f] = fineVForm ? make_double2(fine.u[ff].x - fine.sc[ff].x, fine.u[ff].y - fine.sc[ff].y) : fine.u[ff];
     }
+}
+
+// v-form fine level (fused3.cuh): u = v - sc, in place
+__global__ void k_vform_to_u(double2* v, const double2* sc, size_t n) {
+    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        v[i] = make_double2(v[i].x - sc[i].x, v[i].y - sc[i].y);
 }
 
 // Fine interior values (interior lattice order) scattered into the level.
@@ -860,8 +867,8 @@ struct Hierarchy::Impl {
         if (P == 2 && fused2on) {
             fused2::Args fa{};
             dev::Lvl& F = lv[L];
-            fa.uNew = uAlt;
-            fa.scNew = scAlt;
+            fa.uNew = uAlt;   // v-form (fused3.cuh)
+            fa.scNew = F.sc;
             fa.u = F.u;
             fa.sc = F.sc;
             fa.b = F.chi;
@@ -884,7 +891,6 @@ struct Hierarchy::Impl {
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             fused2::combine(fa, lv[L - 1].rhat, stream);
             std::swap(F.u, uAlt);
-            std::swap(F.sc, scAlt);
             for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
                 if (l < L - 1 && l >= prob.ellMin)
                     fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
@@ -906,8 +912,8 @@ struct Hierarchy::Impl {
         if (P == 3 && fused) {
             fused3::Args fa{};
             dev::Lvl& F = lv[L];
-            fa.uNew = uAlt;
-            fa.scNew = scAlt;
+            fa.uNew = uAlt;   // next v (v-form, fused3.cuh)
+            fa.scNew = F.sc;  // write-only
             fa.b = F.chi;
             fa.scC = lv[L - 1].sc;
             fa.siC = lv[L - 1].si;
@@ -928,9 +934,7 @@ struct Hierarchy::Impl {
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream);
             std::swap(F.u, uAlt);
-            std::swap(F.sc, scAlt);
             std::swap(mapU[0], mapU[1]);
-            std::swap(mapS[0], mapS[1]);
             for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
                 if (l < L - 1 && l >= prob.ellMin)
                     fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
@@ -970,8 +974,11 @@ struct Hierarchy::Impl {
     template <int P>
     void inject_coarse_u() {
         for (int l = L - 1; l >= 1; --l)
-            dev::k_inject_u<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], lv[l + 1]);
+            dev::k_inject_u<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], lv[l + 1], l == L - 1 && vForm() ? 1 : 0);
     }
+
+    // the finest level holds v = u + sc (fused fast paths, fused3.cuh)
+    bool vForm() const { return prob.fast && (fused || fused2on); }
 
     void materialize_coarse_u() {
         if (!prob.fast || !coarseUStale) return;
@@ -1149,7 +1156,6 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks));
     if (I.fused2on) {
         I.uAlt = I.alloc<double2>(I.lv[I.L].n);
-        I.scAlt = I.alloc<double2>(I.lv[I.L].n);
         I.partial2 = I.alloc<double2>(fused2::partial_count(I.geo2));
     }
     if (prob.fast) {
@@ -1170,15 +1176,14 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
         const char* fz = std::getenv("TMG_FUSED");
         if (prob.fast && I.p == 3 && I.L >= 2 && !(fz && fz[0] == '0')) {
             const dev::Lvl& F = I.lv[I.L];
-            I.uAlt = I.alloc<double2>(F.n);
-            I.scAlt = I.alloc<double2>(F.n);
+            I.uAlt = I.alloc<double2>(F.n);  // v double buffer; sc is write-only (v-form)
             I.geo = fused3::geometry(static_cast<int>(F.m), static_cast<int>(I.lv[I.L - 1].m), prob.zParts,
                                      I.fusedResident);
             I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
             const dev::Lvl& C = I.lv[I.L - 1];
             bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0) && fused3::encode_map(&I.mapS[0], F.sc, F.n1, 0) &&
                       fused3::encode_map(&I.mapU[1], I.uAlt, F.n1, 0) &&
-                      fused3::encode_map(&I.mapS[1], I.scAlt, F.n1, 0) && fused3::encode_map(&I.mapB, F.chi, F.n1, 1) &&
+                      fused3::encode_map(&I.mapS[1], F.sc, F.n1, 0) && fused3::encode_map(&I.mapB, F.chi, F.n1, 1) &&
                       fused3::encode_map(&I.mapC, C.sc, C.n1, 2) && fused3::encode_map(&I.mapI, C.si, C.n1, 2);
             if (!ok) throw CudaError("cuTensorMapEncodeTiled failed for the fused fine pass");
             I.fused = true;
@@ -1273,6 +1278,17 @@ void Hierarchy::get_field(int level, const std::string& field, double* host) con
         return;
     }
     if (field == "u" && level < I.L) I.materialize_coarse_u();
+    if (field == "u" && level == I.L && I.vForm()) {  // u = v - sc
+        std::vector<double2> sc(v.n);
+        TMG_CUDA(cudaMemcpyAsync(host, v.u, static_cast<size_t>(v.n) * sizeof(double2), cudaMemcpyDeviceToHost, I.stream));
+        TMG_CUDA(cudaMemcpyAsync(sc.data(), v.sc, sc.size() * sizeof(double2), cudaMemcpyDeviceToHost, I.stream));
+        TMG_CUDA(cudaStreamSynchronize(I.stream));
+        for (size_t i = 0; i < sc.size(); ++i) {
+            host[2 * i] -= sc[i].x;
+            host[2 * i + 1] -= sc[i].y;
+        }
+        return;
+    }
     double2* ptr = field_ptr(v, field);
     if (!ptr) {
         if (field == "uhat" || field == "chi" || field == "sf" || field == "si" || field == "sinext" || field == "r") {
@@ -1292,15 +1308,29 @@ void Hierarchy::set_field(int level, const std::string& field, const double* hos
     const dev::Lvl& v = I.lv[level];
     double2* ptr = field_ptr(v, field);
     if (!ptr) throw ConfigError("set_field: unknown field '" + field + "'");
+    if (level == I.L && I.vForm() && (field == "u" || field == "sc")) {
+        // the device keeps v = u + sc on the finest level
+        std::vector<double> u(2 * static_cast<size_t>(v.n)), sc(2 * static_cast<size_t>(v.n));
+        get_field(level, "u", u.data());
+        get_field(level, "sc", sc.data());
+        const double* nu = field == "u" ? host : u.data();
+        const double* ns = field == "sc" ? host : sc.data();
+        std::vector<double> vv(u.size());
+        for (size_t i = 0; i < vv.size(); ++i) vv[i] = nu[i] + ns[i];
+        TMG_CUDA(cudaMemcpyAsync(v.u, vv.data(), vv.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
+        TMG_CUDA(cudaMemcpyAsync(v.sc, ns, vv.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
+        TMG_CUDA(cudaStreamSynchronize(I.stream));
+        return;
+    }
     TMG_CUDA(cudaMemcpyAsync(ptr, host, static_cast<size_t>(v.n) * sizeof(double2), cudaMemcpyHostToDevice, I.stream));
     TMG_CUDA(cudaStreamSynchronize(I.stream));
 }
 
 namespace {
 template <int P>
-void inject_up(Hierarchy::Impl& I) {
+void inject_up(Hierarchy::Impl& I) {  // callers reset sc afterwards: plain u injection
     for (int l = I.L - 1; l >= 1; --l)
-        dev::k_inject_u<P><<<I.blocks_for(I.lv[l].n), 256, 0, I.stream>>>(I.lv[l], I.lv[l + 1]);
+        dev::k_inject_u<P><<<I.blocks_for(I.lv[l].n), 256, 0, I.stream>>>(I.lv[l], I.lv[l + 1], 0);
 }
 }  // namespace
 
@@ -1409,6 +1439,11 @@ void Hierarchy::unfold() {
     Problem p2 = old.prob;
     p2.levels = old.L + 1;
     if (p2.rhsLattice < 0) p2.rhsLattice = p2.levels;
+    if (old.vForm()) {  // the old finest level becomes a coarse level: back to (u, sc)
+        const dev::Lvl& F = old.lv[old.L];
+        dev::k_vform_to_u<<<old.blocks_for(F.n), 256, 0, old.stream>>>(F.u, F.sc, F.n);
+        TMG_CUDA(cudaGetLastError());
+    }
     TMG_CUDA(cudaStreamSynchronize(old.stream));
     Hierarchy deeper(p2);
     Impl& nw = *deeper.impl_;
