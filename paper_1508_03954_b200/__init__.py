@@ -25,7 +25,7 @@ from typing import Dict, List, Optional
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libtreemg_b200.so")
+LIB_PATH = os.environ.get("TMG_LIB") or os.path.join(PKG, "libtreemg_b200.so")  # TMG_LIB: developer A/B of build variants
 
 STATUS = {0: "TREEMG_OK", 1: "TREEMG_E_USAGE", 2: "TREEMG_E_CAPACITY", 3: "TREEMG_E_RUNTIME"}
 OUTCOME = {0: "converged", 1: "budget-exhausted", 2: "diverged"}

@@ -36,25 +36,29 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not _stale():
+def build(force: bool = False, verbose: bool = False, out: str = "", defines=()) -> str:
+    """Compile libtreemg_b200.so for sm_100a.  `out` / `defines` build a
+    variant library elsewhere (developer A/B of compile-time parameters)."""
+    target = out or LIB
+    if not out and not force and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
     cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
            "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-shared", "-Xlinker", "-soname=libtreemg_b200.so",
-           "-I" + os.path.join(ROOT, "include"), "-o", LIB + ".tmp"] + srcs
+           "-I" + os.path.join(ROOT, "include"), "-o", target + ".tmp"] + ["-D" + d for d in defines] + srcs
     # host compiler: the system g++ so libstdc++ is linked dynamically
     if os.path.exists("/usr/bin/g++"):
         cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
-    out = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
-    with open(os.path.join(PKG, "build.log"), "w") as f:
-        f.write(" ".join(cmd) + "\n" + out.stdout + out.stderr)
-    if out.returncode != 0:
-        raise RuntimeError("nvcc build failed:\n" + out.stderr[-6000:])
-    os.replace(LIB + ".tmp", LIB)
+    res = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
+    if not out:
+        with open(os.path.join(PKG, "build.log"), "w") as f:
+            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
+    if res.returncode != 0:
+        raise RuntimeError("nvcc build failed:\n" + res.stderr[-6000:])
+    os.replace(target + ".tmp", target)
     if verbose:
-        print(out.stderr)
-    return LIB
+        print(res.stderr)
+    return target
 
 
 if __name__ == "__main__":
