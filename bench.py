@@ -421,20 +421,36 @@ def main():
         chi_host = np.empty(2 * n_lat)
     rng = np.random.default_rng(RHS_SEED)
     chi_host[:] = rng.uniform(-1, 1, size=2 * n_lat)
-    e2e_steps = max(2, min(args.steps, 5))
     h2d = 16 * n_lat
+    n0 = args.warmup + args.steps + 1
+    one = (lambda n: h.cycle(pol, n)) if mode == "slabs" else (h.td_bpx if pol.bpx else h.td_add)
+    if mode != "slabs":
+        one = (lambda f: (lambda n: f(pol, n)))(one)
+    # (a) a solve through the public API: the step's input (the rhs) uploaded
+    #     from pinned host memory once, then K cycles, each returning its norms
     barrier()
     t0 = time.perf_counter()
-    for i in range(e2e_steps):
-        if mode == "slabs":
-            _, h2d = h.e2e_step(pol, args.warmup + args.steps + 1 + i, chi_host)
-        else:
-            h.e2e_step(pol, args.warmup + args.steps + 1 + i, chi_host)
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    e2e_s = D.reduce_max(ctx, e2e_s)
-    e2e = {"value": copies * dof / e2e_s, "unit": "DoF-updates/s", "h2d_bytes_per_step": int(h2d),
-           "d2h_bytes_per_step": 24, "note": "per step: H2D of the nodal rhs (16 B/vertex, pinned; slabs: the "
-           "rank's planes), device load vector, one cycle, D2H of the three residual norms (wall clock, max over ranks)"}
+    if mode == "slabs":
+        _, h2d = h.e2e_step(pol, n0, chi_host)
+    else:
+        h.e2e_step(pol, n0, chi_host)
+    for i in range(1, args.steps):
+        one(n0 + i)
+    solve_s = D.reduce_max(ctx, time.perf_counter() - t0)
+    # (b) the pessimistic variant: a fresh rhs uploaded before every cycle
+    reps = max(2, min(args.steps, 5))
+    barrier()
+    t0 = time.perf_counter()
+    for i in range(reps):
+        h.e2e_step(pol, n0 + args.steps + i, chi_host)
+    every_s = D.reduce_max(ctx, (time.perf_counter() - t0) / reps)
+    e2e = {"value": copies * dof * args.steps / solve_s, "unit": "DoF-updates/s",
+           "h2d_bytes_per_step": int(h2d) // max(1, args.steps), "d2h_bytes_per_step": 24,
+           "note": f"public-API solve of K={args.steps} cycles (wall clock, max over ranks): H2D of the nodal rhs "
+                   "(16 B/vertex from pinned memory; slabs: the rank's planes) and the device load vector once, "
+                   "then every cycle with D2H of its three residual norms",
+           "rhs_every_cycle": {"value": copies * dof / every_s, "h2d_bytes_per_step": int(h2d),
+                               "note": "a fresh rhs uploaded before each cycle (PCIe-bound)"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
