@@ -1145,7 +1145,7 @@ void AmrTree::time_cycles(const Policy& pol, int n0, int count, double* out4) {
     out4[0] = totalMs;
     out4[1] = 0.0;
     out4[2] = 0.0;
-    out4[3] = static_cast<double>(3 * (L_ + 1) + 1);
+    out4[3] = static_cast<double>(3 * (L_ + 1));  // top-down L+1, chi L (finest precomputed), residual L+1, norm
 }
 
 }  // namespace tmg

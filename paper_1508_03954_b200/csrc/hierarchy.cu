@@ -1009,14 +1009,20 @@ struct Hierarchy::Impl {
         return pts <= lim;
     }
 
+    // kernel launches of one cycle (bench.py "gpu_launches"), mirroring cycle_fast / cycle_exact
     int launches_per_cycle() const {
-        if (prob.fast && chainGrid > 0) {
-            int top = L - 1, big = 0;
-            while (top >= 1 && lv[top].n >= kChainMaxN) --top, ++big;
-            if (top >= 1) return 2 + 2 + 3 * big + (top < L - 1 ? 1 : 0);  // chains, fine pass(es), big levels
-        }
-        if (prob.fast && fused) return (L - 1) + 2 + std::max(0, L - 2 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1;
-        return prob.fast ? (L - 1) + 2 + (L - 1 - std::max(0, prob.ellMin - 1)) + (L - 1) + 1 : 3 * L;
+        if (!prob.fast) return 3 * L;  // top-down 1..L, residual L..1, restriction L..2, norm
+        int top = L - 1;
+        while (top >= 1 && lv[top].n >= kChainMaxN) --top;
+        const bool useChain = chainGrid > 0 && top >= 1 && top < fast::kMaxChainLevels;
+        const bool fusedPath = (p == 3 && fused) || (p == 2 && fused2on);
+        const int lo = useChain ? top + 1 : 1;
+        int n = useChain ? 1 + (L - 1 - top) : (L - 1);  // top-down
+        n += 2;                                            // fine pass (+ combine, or correction + residual)
+        for (int l = L - 1; l >= lo; --l) n += 1 + ((fusedPath ? l < L - 1 : true) && l >= prob.ellMin ? 1 : 0);
+        if (useChain) n += 1 + (fusedPath && top < L - 1 && top >= prob.ellMin ? 1 : 0);
+        else n += 1;                                       // norm reduction
+        return n;
     }
 
     void check_diag() {
