@@ -726,16 +726,8 @@ void span(int P, const Lvl& v, int za, int zb, unsigned& fa, unsigned& fb) {
 }
 }  // namespace
 
-static int tri_mode() {  // TMG_TRI: bit 0 fine correction, bit 1 coarse top-down (A/B switch)
-    static int v = [] {
-        const char* e = std::getenv("TMG_TRI");
-        return e ? std::atoi(e) : 1;
-    }();
-    return v;
-}
-
 void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaStream_t s) {
-    if (P >= 2 && f.m >= 27 && (tri_mode() & 1)) {
+    if (P >= 2 && f.m >= 27) {  // parent-cell triples: 2^P parent loads shared by three points
         const unsigned rows = f.n / f.n1;
         if (P == 2) k_topdown_tri<2, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, rows);
         else k_topdown_tri<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, rows);
@@ -747,18 +739,6 @@ void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaS
 }
 
 void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cudaStream_t s, int za, int zb) {
-    if (P >= 2 && c.m >= 81 && (tri_mode() & 2)) {  // parent-cell triples (rows [za, zb) of planes for P = 3)
-        unsigned ra = 0, rb = c.n / c.n1;
-        if (za >= 0) {
-            const unsigned perPlane = P == 3 ? c.n1 : 1u;
-            ra = static_cast<unsigned>(za) * perPlane;
-            rb = std::min(rb, static_cast<unsigned>(zb) * perPlane);
-        }
-        if (rb <= ra) return;
-        if (P == 2) k_topdown_tri<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
-        else k_topdown_tri<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
-        return;
-    }
     if (P == 3 && c.m == 27) {  // row kernel: small levels, where per-thread latency dominated: interior planes of [za, zb)
         const int zlo = std::max(1, za < 0 ? 1 : za), zhi = std::min(static_cast<int>(c.m), za < 0 ? static_cast<int>(c.m) : zb);
         if (zhi <= zlo) return;

@@ -105,7 +105,7 @@ __host__ __device__ constexpr int stage_elems() { return kPlane + (BPX ? 2 : 1) 
 
 template <bool BPX>
 __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
-    k_fused3(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapS,
+    k_fused3(const __grid_constant__ CUtensorMap mapU,
              const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int SE = stage_elems<BPX>();
@@ -528,7 +528,7 @@ int resident_blocks(int smCount) {
     return per * smCount;
 }
 
-void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapC,
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
             const CUtensorMap& mapI, cudaStream_t s, int nchunks) {
     static bool configured[2] = {false, false};
     const bool bpx = a.bpx != 0;
@@ -539,13 +539,13 @@ void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, con
             cudaFuncSetAttribute(k_fused3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             configured[1] = true;
         }
-        k_fused3<true><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapS, mapC, mapI, a);
+        k_fused3<true><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapC, mapI, a);
     } else {
         if (!configured[0]) {
             cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             configured[0] = true;
         }
-        k_fused3<false><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapS, mapC, mapI, a);
+        k_fused3<false><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapC, mapI, a);
     }
 }
 

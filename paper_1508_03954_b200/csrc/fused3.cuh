@@ -83,7 +83,7 @@ int blocks(const Geometry& g);
 bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind);
 
 // nchunks <= 0: all z-chunks (chunkBase must be 0)
-void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapS, const CUtensorMap& mapC,
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
             const CUtensorMap& mapI, cudaStream_t s, int nchunks = 0);
 // r_{L-1}(W) = sum of the tile partials covering W, fixed order; coarse
 // planes [za, zb) (za < 0: all).

@@ -565,9 +565,8 @@ struct Hierarchy::Impl {
     // fused 3D fine pass (fast precision): double-buffered fine u / sc
     bool fused = false;
     double2* uAlt = nullptr;
-    double2* scAlt = nullptr;
-    CUtensorMap mapU[2], mapS[2];  // [0]: current buffers, [1]: alternates
-    CUtensorMap mapB, mapC, mapI;
+    CUtensorMap mapU[2];  // v: [0] current buffer, [1] alternate
+    CUtensorMap mapC, mapI;  // coarse sc / si planes (L-1)
     fused3::Geometry geo{};
     double2* partial3 = nullptr;
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
@@ -859,7 +858,7 @@ struct Hierarchy::Impl {
             ch.bar = chainBar;
             ch.normPartials = partials;
             ch.normOut = dNorm;
-            fast::chain_down(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
+            fast::chain_down(P, ch, chainGrid, stream);
         }
         for (int l = useChain ? top + 1 : 1; l < L; ++l)
             fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
@@ -901,7 +900,7 @@ struct Hierarchy::Impl {
                     fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
                 ch.firstRestrict = 0;
                 ch.normBlocks = fused2::blocks(geo2);
-                fast::chain_up(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
+                fast::chain_up(P, ch, chainGrid, stream);
             } else {
                 dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused2::blocks(geo2), dNorm);
             }
@@ -930,7 +929,7 @@ struct Hierarchy::Impl {
             fa.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
             fa.ellMin = prob.ellMin;
             fa.level = L;
-            fused3::launch(fa, mapU[0], mapS[0], mapC, mapI, stream);
+            fused3::launch(fa, mapU[0], mapC, mapI, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream);
             std::swap(F.u, uAlt);
@@ -945,7 +944,7 @@ struct Hierarchy::Impl {
                     fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
                 ch.firstRestrict = 0;
                 ch.normBlocks = fused3::blocks(geo);
-                fast::chain_up(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
+                fast::chain_up(P, ch, chainGrid, stream);
             } else {
                 dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused3::blocks(geo), dNorm);
             }
@@ -963,7 +962,7 @@ struct Hierarchy::Impl {
         if (useChain) {
             ch.firstRestrict = 1;  // fine = lv[top + 1] into lv[top]
             ch.normBlocks = nb;
-            fast::chain_up(P, ch, chainSmall(top) ? 1 : chainGrid, stream);
+            fast::chain_up(P, ch, chainGrid, stream);
         } else {
             dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, nb, dNorm);
         }
@@ -998,15 +997,6 @@ struct Hierarchy::Impl {
             else if (p == 2) cycle_exact<2>(pol, n, timed);
             else cycle_exact<3>(pol, n, timed);
         }
-    }
-
-    // a chain whose levels hold few points runs in one CTA (block barriers only)
-    bool chainSmall(int top) const {
-        unsigned long long pts = 0;
-        for (int l = 1; l <= top; ++l) pts += lv[l].n;
-        const char* e = std::getenv("TMG_CHAIN_SMALL");
-        const unsigned long long lim = e ? std::strtoull(e, nullptr, 10) : 0ull;  // measured: grid chains win
-        return pts <= lim;
     }
 
     // kernel launches of one cycle (bench.py "gpu_launches"), mirroring cycle_fast / cycle_exact
@@ -1187,9 +1177,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
                                      I.fusedResident);
             I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
             const dev::Lvl& C = I.lv[I.L - 1];
-            bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0) && fused3::encode_map(&I.mapS[0], F.sc, F.n1, 0) &&
+            bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0) &&
                       fused3::encode_map(&I.mapU[1], I.uAlt, F.n1, 0) &&
-                      fused3::encode_map(&I.mapS[1], F.sc, F.n1, 0) && fused3::encode_map(&I.mapB, F.chi, F.n1, 1) &&
                       fused3::encode_map(&I.mapC, C.sc, C.n1, 2) && fused3::encode_map(&I.mapI, C.si, C.n1, 2);
             if (!ok) throw CudaError("cuTensorMapEncodeTiled failed for the fused fine pass");
             I.fused = true;
