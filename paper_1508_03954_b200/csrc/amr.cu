@@ -39,6 +39,8 @@ struct ALvl {
     const unsigned char* cflag;
     const unsigned char* estar;
     const signed char* succ;
+    const unsigned* list;  // existing vertices: interior non-hanging first, then the rest
+    unsigned nlist;
     int lo[3];
     int n1[3];
     unsigned n;
@@ -80,7 +82,8 @@ __device__ __forceinline__ int aflat(const ALvl& c, const int* g) {
 // ---- top-down: touch_first / create_hanging ----------------------------------
 template <int P>
 __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
+        const unsigned f = c.list[i];
         const unsigned char vf = c.vflag[f];
         if (!(vf & amr::kExists)) continue;
         const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging;
@@ -100,23 +103,28 @@ __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
             q[d] = min(g[d] / 3, pr.m - 1);  // parent_stencil, spacetree.cpp:164-174
             rel[d] = g[d] - 3 * q[d];
         }
-        double2 cu[1 << P], cs[1 << P], ci[1 << P];
+        // parent corners (find_vertex: absent -> 0); one field at a time keeps
+        // the register footprint small
+        int pfs[1 << P];
 #pragma unroll
         for (int e = 0; e < (1 << P); ++e) {
             int pi[P];
 #pragma unroll
             for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
             const int pf = aflat<P>(pr, pi);
-            const bool ok = pf >= 0 && (pr.vflag[pf] & amr::kExists);  // find_vertex: null -> 0
-            cu[e] = ok ? pr.u[pf] : cz();
-            cs[e] = ok ? pr.sc[pf] : cz();
-            ci[e] = (bpx && ok) ? pr.si[pf] : cz();
+            pfs[e] = (pf >= 0 && (pr.vflag[pf] & amr::kExists)) ? pf : -1;
         }
-        const double2 pu = prolong<P>(cu, rel);
-        const double2 ps = prolong<P>(cs, rel);
+        auto parent_prolong = [&](const double2* src) {
+            double2 v[1 << P];
+#pragma unroll
+            for (int e = 0; e < (1 << P); ++e) v[e] = pfs[e] >= 0 ? src[pfs[e]] : cz();
+            return prolong<P>(v, rel);
+        };
+        const double2 pu = parent_prolong(pr.u);
+        const double2 ps = parent_prolong(pr.sc);
         if (hang) {  // create_hanging
             double2 u = pu, sc = ps;
-            if (bpx && !cp) sc = xsub(sc, prolong<P>(ci, rel));
+            if (bpx && !cp) sc = xsub(sc, parent_prolong(pr.si));
             if (bnd) {
                 u = cz();
                 sc = cz();
@@ -130,7 +138,7 @@ __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
             continue;
         }
         double2 sc = xadd(c.sc[f], ps);
-        if (bpx && !cp) sc = xsub(sc, prolong<P>(ci, rel));
+        if (bpx && !cp) sc = xsub(sc, parent_prolong(pr.si));
         const double2 sf = c.sf ? c.sf[f] : cz();
         double2 u = xadd(c.u[f], xadd(sc, sf));
         double2 uh = xsub(u, pu);
@@ -151,7 +159,8 @@ __global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, 
                                                  int restrictOn) {
     constexpr int NC = 1 << P;
     constexpr int NT = P == 1 ? 3 : P == 2 ? 9 : 27;
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
+        const unsigned f = c.list[i];
         if (!(c.vflag[f] & amr::kExists)) continue;
         int g[P];
         aunflat<P>(f, c, g);
@@ -309,11 +318,15 @@ __device__ __forceinline__ double2 regular_residual(const double2* __restrict__ 
 
 // ---- residual + touch_last / destroy_hanging --------------------------------
 template <int P>
-__global__ void __launch_bounds__(256) k_amr_residual(AResArgs a) {
+#ifndef TMG_AMR_RES_MINB
+#define TMG_AMR_RES_MINB 3
+#endif
+__global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs a) {
     constexpr int NC = 1 << P;
     const ALvl& c = a.lv;
     double nmax = 0.0, nsum = 0.0;
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
+        const unsigned f = c.list[i];
         const unsigned char vf = c.vflag[f];
         if (!(vf & amr::kExists)) continue;
         const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging,
@@ -782,7 +795,7 @@ struct AmrTree::Dev {
 namespace {
 int blocks_for_n(long long n, int smCount) {
     const long long need = (n + 255) / 256;
-    return static_cast<int>(std::max<long long>(1, std::min<long long>(need, 8LL * smCount)));
+    return static_cast<int>(std::max<long long>(1, std::min<long long>(need, 32LL * smCount)));
 }
 }  // namespace
 
@@ -847,6 +860,22 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
         a.cflag = cflag;
         a.estar = estar;
         a.succ = succ;
+        {  // compacted vertex list: warps see uniform work (regular vertices first)
+            std::vector<unsigned> lst;
+            lst.reserve(static_cast<size_t>(h.n));
+            for (int pass = 0; pass < 2; ++pass)
+                for (long long f = 0; f < h.n; ++f) {
+                    const unsigned char v = h.vflag[f];
+                    if (!(v & amr::kExists)) continue;
+                    const bool regular = !(v & (amr::kHanging | amr::kBoundary));
+                    if (regular == (pass == 0)) lst.push_back(static_cast<unsigned>(f));
+                }
+            auto* dl = D.alloc<unsigned>(lst.size(), stream_);
+            AMR_CUDA(cudaMemcpyAsync(dl, lst.data(), lst.size() * sizeof(unsigned), cudaMemcpyHostToDevice, stream_));
+            AMR_CUDA(cudaStreamSynchronize(stream_));
+            a.list = dl;
+            a.nlist = static_cast<unsigned>(lst.size());
+        }
         blocksTotal += blocks_for_n(h.n, smCount_);
         D.normOffs.push_back(blocksTotal);
     }
@@ -942,7 +971,7 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
     const int bpx = pol.bpx ? 1 : 0;
     for (int l = 0; l <= L_; ++l) {
         const adev::ALvl& pr = l > 0 ? D.lv[l - 1] : D.lv[0];
-        adev::k_amr_topdown<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
+        adev::k_amr_topdown<P><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
     }
     adev::AResArgs a{};
     a.ellMin = prob_.ellMin;
@@ -953,7 +982,7 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
         a.wTab[s] = make_double2(w.real(), w.imag());
     }
     for (int l = L_; l >= 0; --l) {
-        const int nb = blocks_for_n(D.lv[l].n, smCount_);
+        const int nb = blocks_for_n(D.lv[l].nlist, smCount_);
         const adev::ALvl& fine = l < L_ ? D.lv[l + 1] : D.lv[l];
         if (l < L_)  // finest level: chi is the constant load vector (built at setup)
             adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.kc[l], D.weights,
