@@ -104,7 +104,7 @@ template <bool BPX>
 __host__ __device__ constexpr int stage_elems() { return kPlane + (BPX ? 2 : 1) * kC; }
 
 template <bool BPX>
-__global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
+__global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     k_fused3(const __grid_constant__ CUtensorMap mapU,
              const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
     extern __shared__ __align__(128) unsigned char smem[];
@@ -430,7 +430,8 @@ __global__ void __launch_bounds__(NT, (TY <= 8 ? 3 : 2))
     dev::block_norms(nmax, nsum, a.norms);
 }
 
-__global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int za, int zb) {
+template <bool SMOOTH>
+__global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int za, int zb, const fast::ResArgs sa) {
     const int mc = a.g.mc, m = a.g.m, zc = a.g.zc;
     const unsigned n1c = a.n1c;
     const unsigned first = static_cast<unsigned>(za) * n1c * n1c;  // coarse lattices < 2^32 points
@@ -458,6 +459,22 @@ __global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int 
             }
         }
         rc[f] = acc;
+        if (SMOOTH) {  // level L-1 smoothing (k_smooth_coarse) on the value just formed
+            const dev::Lvl& cl = sa.lv;
+            if (sa.bpx && cl.si) {
+                cl.si[f] = cl.sinext[f];
+                cl.sinext[f] = zero2();
+            }
+            if (cl.level < sa.ellMin) {
+                cl.sc[f] = zero2();
+                continue;
+            }
+            const bool cp = (W0 % 3 == 0) && (W1 % 3 == 0) && (W2 % 3 == 0);
+            const double2 smooth = mul(acc, sa.k.invDiag);
+            cl.sc[f] = stage_sc(smooth, sa.k.wRaw, cp, sa.bpx, sa.hb);
+            if (sa.bpx && cl.level > sa.ellMin && cp)
+                sa.par.sinext[(W0 / 3) + sa.par.n1 * ((W1 / 3) + sa.par.n1 * (W2 / 3))] = mul(sa.k.wRaw, smooth);
+        }
     }
 }
 
@@ -549,12 +566,15 @@ void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
     }
 }
 
-void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s, int za, int zb) {
+void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s, int za, int zb,
+             const fast::ResArgs* smooth) {
     if (za < 0) {
         za = 0;
         zb = a.g.mc + 1;
     }
-    if (zb > za) k_combine<<<nblocks, 256, 0, s>>>(a, rCoarse, za, zb);
+    if (zb <= za) return;
+    if (smooth) k_combine<true><<<nblocks, 256, 0, s>>>(a, rCoarse, za, zb, *smooth);
+    else k_combine<false><<<nblocks, 256, 0, s>>>(a, rCoarse, za, zb, fast::ResArgs{});
 }
 
 }  // namespace fused3

@@ -87,7 +87,10 @@ void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
             const CUtensorMap& mapI, cudaStream_t s, int nchunks = 0);
 // r_{L-1}(W) = sum of the tile partials covering W, fixed order; coarse
 // planes [za, zb) (za < 0: all).
-void combine(const Args& a, double2* rCoarse, int blocks, cudaStream_t s, int za = -1, int zb = -1);
+// smooth != nullptr: also the level L-1 smoothing of fast::smooth_coarse on the
+// interior points (boundary sc / si stay zero), saving its re-read of r.
+void combine(const Args& a, double2* rCoarse, int blocks, cudaStream_t s, int za = -1, int zb = -1,
+             const fast::ResArgs* smooth = nullptr);
 
 }  // namespace fused3
 }  // namespace tmg

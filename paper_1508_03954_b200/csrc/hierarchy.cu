@@ -574,7 +574,10 @@ struct Hierarchy::Impl {
     fused2::Geometry geo2{};
     double2* partial2 = nullptr;
     int chainGrid = 0;              // cooperative coarse-chain grid (0: per-level launches)
-    static constexpr unsigned kChainMaxN = 1u << 16;  // levels below this size join the chain
+#ifndef TMG_CHAIN_MAXN
+#define TMG_CHAIN_MAXN (1u << 16)
+#endif
+    static constexpr unsigned kChainMaxN = TMG_CHAIN_MAXN;  // levels below this size join the chain
     int fusedResident = 3 * 148;
     unsigned* chainBar = nullptr;
 
@@ -931,13 +934,15 @@ struct Hierarchy::Impl {
             fa.level = L;
             fused3::launch(fa, mapU[0], mapC, mapI, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
-            fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream);
+            const int lo = useChain ? top + 1 : 1;
+            const fast::ResArgs sL = args(L - 1);
+            fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream, -1, -1, lo <= L - 1 ? &sL : nullptr);
             std::swap(F.u, uAlt);
             std::swap(mapU[0], mapU[1]);
-            for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
+            for (int l = L - 1; l >= lo; --l) {
                 if (l < L - 1 && l >= prob.ellMin)
                     fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
-                fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
+                if (l < L - 1) fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);  // L-1: in the combine
             }
             if (useChain) {
                 if (top < L - 1 && top >= prob.ellMin)
@@ -1009,7 +1014,8 @@ struct Hierarchy::Impl {
         const int lo = useChain ? top + 1 : 1;
         int n = useChain ? 1 + (L - 1 - top) : (L - 1);  // top-down
         n += 2;                                            // fine pass (+ combine, or correction + residual)
-        for (int l = L - 1; l >= lo; --l) n += 1 + ((fusedPath ? l < L - 1 : true) && l >= prob.ellMin ? 1 : 0);
+        for (int l = L - 1; l >= lo; --l)
+            n += (p == 3 && fused && l == L - 1 ? 0 : 1) + ((fusedPath ? l < L - 1 : true) && l >= prob.ellMin ? 1 : 0);
         if (useChain) n += 1 + (fusedPath && top < L - 1 && top >= prob.ellMin ? 1 : 0);
         else n += 1;                                       // norm reduction
         return n;
