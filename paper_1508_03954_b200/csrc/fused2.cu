@@ -118,8 +118,9 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         if (yin && owned) u = ldg(a.u + x + n1 * yy);
         if (yin && hin) hu = ldg(a.u + hx + n1 * yy);
     };
-    double2 uN, huN;
+    double2 uN, huN, uN2, huN2;  // rows yy + 1 and yy + 2 in flight
     loadRow(y0 - 1, uN, huN);
+    loadRow(y0, uN2, huN2);
     double2 cPrev = zero2();
     double2 bq = (owned && y0 < y1) ? ldg(a.b + x + n1 * y0) : zero2();
     computeV(y0 - 1, 0);
@@ -130,7 +131,9 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         const int u3 = it % 3;  // yy % 3 (y0 = 1 mod 3)
         const bool yin = yy >= 1 && yy <= m - 1;
         const double2 uC = uN, huC = huN;
-        if (it + 1 < nrows) loadRow(yy + 1, uN, huN);
+        uN = uN2;
+        huN = huN2;
+        if (it + 2 < nrows) loadRow(yy + 2, uN2, huN2);
         const double2* V = Vb[it & 1];
         double2* P = Pb[it & 1];
         // ---- phase B: corrected row yy ----
