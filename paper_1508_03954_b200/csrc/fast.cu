@@ -434,8 +434,12 @@ constexpr int kZch = 48;
 // ld.global.cg (L2), never through the non-coherent L1 / read-only path.
 __device__ __forceinline__ double2 ldcg(const double2* p) { return __ldcg(p); }
 
-__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen) {
-    if (gridDim.x == 1) {  // single-CTA chain (tiny hierarchies): a block barrier suffices
+__device__ __forceinline__ void grid_barrier(unsigned* bar, unsigned& gen, int cluster) {
+    if (cluster) {  // the whole chain is one thread-block cluster: hardware cluster barrier
+        asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+        return;
+    }
+    if (gridDim.x == 1) {  // single-CTA chain: a block barrier suffices
         __threadfence_block();
         __syncthreads();
         return;
@@ -499,7 +503,7 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_down(ChainArgs a) {
             if (a.bpx && !dev::is_cpoint<P>(idx)) sc = sub(sc, prolong_at<P>(pr.si, pr.n1, q, rel));
             c.sc[f] = sc;
         }
-        if (l < a.top) grid_barrier(a.bar, gen);
+        if (l < a.top) grid_barrier(a.bar, gen, a.cluster);
     }
 }
 
@@ -622,7 +626,7 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_up(ChainArgs a) {
     const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
     if (a.firstRestrict && a.top >= a.ellMin) {
         chain_restrict<P>(a.fine, a.lv[a.top], tid, stride);
-        grid_barrier(a.bar, gen);
+        grid_barrier(a.bar, gen, a.cluster);
     }
     for (int l = a.top; l >= 1; --l) {
         const Lvl& c = a.lv[l];
@@ -650,7 +654,7 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_up(ChainArgs a) {
             }
         }
         if (l - 1 >= 1 && l - 1 >= a.ellMin) chain_restrict<P>(c, par, tid, stride);  // into l-1, same step
-        if (l > 1) grid_barrier(a.bar, gen);
+        if (l > 1) grid_barrier(a.bar, gen, a.cluster);
     }
     if (a.normOut && blockIdx.x == 0) {  // K5: fixed-order reduction of the fine pass's block partials
         __shared__ double smax[kChainThreads], ssum[kChainThreads];
@@ -693,21 +697,60 @@ int chain_grid(int P, int smCount) {
     return chain_grid_for<3>(smCount);
 }
 
+namespace {
+template <class K>
+void launch_chain(K kernel, const ChainArgs& a, int grid, cudaStream_t s) {
+    if (a.cluster) {  // one cluster of `grid` CTAs (<= 16), hardware barriers
+        cudaFuncSetAttribute(kernel, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);  // per kernel
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kChainThreads);
+        cfg.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = grid;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        cudaLaunchKernelEx(&cfg, kernel, a);
+        return;
+    }
+    void* args[] = {const_cast<ChainArgs*>(&a)};
+    cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(kernel), dim3(grid), dim3(kChainThreads), args, 0, s);
+}
+}  // namespace
+
 void chain_down(int P, const ChainArgs& a, int grid, cudaStream_t s) {
     if (a.top < 1) return;
-    void* args[] = {const_cast<ChainArgs*>(&a)};
-    const void* fn = P == 1 ? reinterpret_cast<const void*>(k_chain_down<1>)
-                   : P == 2 ? reinterpret_cast<const void*>(k_chain_down<2>)
-                            : reinterpret_cast<const void*>(k_chain_down<3>);
-    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kChainThreads), args, 0, s);
+    if (P == 1) launch_chain(k_chain_down<1>, a, grid, s);
+    else if (P == 2) launch_chain(k_chain_down<2>, a, grid, s);
+    else launch_chain(k_chain_down<3>, a, grid, s);
 }
 
 void chain_up(int P, const ChainArgs& a, int grid, cudaStream_t s) {
-    void* args[] = {const_cast<ChainArgs*>(&a)};
-    const void* fn = P == 1 ? reinterpret_cast<const void*>(k_chain_up<1>)
-                   : P == 2 ? reinterpret_cast<const void*>(k_chain_up<2>)
-                            : reinterpret_cast<const void*>(k_chain_up<3>);
-    cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(kChainThreads), args, 0, s);
+    if (P == 1) launch_chain(k_chain_up<1>, a, grid, s);
+    else if (P == 2) launch_chain(k_chain_up<2>, a, grid, s);
+    else launch_chain(k_chain_up<3>, a, grid, s);
+}
+
+int chain_cluster_size() {
+    // the largest cluster the chain kernels can run as (16 needs the non-portable opt-in)
+    cudaFuncSetAttribute(k_chain_up<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(16);
+    cfg.blockDim = dim3(kChainThreads);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 16;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_chain_up<3>, &cfg) == cudaSuccess && n >= 1) return 16;
+    cudaGetLastError();
+    return 8;
 }
 
 namespace {

@@ -66,8 +66,10 @@ struct ChainArgs {
     const double* normPartials;
     int normBlocks;
     double* normOut;    // nullptr: no norm reduction
+    int cluster;        // 1: launched as one thread-block cluster (hardware cluster barriers)
 };
 int chain_grid(int P, int smCount);
+int chain_cluster_size();
 void chain_down(int P, const ChainArgs& a, int grid, cudaStream_t s);
 void chain_up(int P, const ChainArgs& a, int grid, cudaStream_t s);
 

@@ -579,6 +579,8 @@ struct Hierarchy::Impl {
 #endif
     static constexpr unsigned kChainMaxN = TMG_CHAIN_MAXN;  // levels below this size join the chain
     int fusedResident = 3 * 148;
+    int clusterSize = 0;  // CTAs of a chain cluster (0: grid chains only)
+    static constexpr unsigned long long kClusterMaxPts = 1ull << 18;
     unsigned* chainBar = nullptr;
 
     ~Impl() {
@@ -861,7 +863,12 @@ struct Hierarchy::Impl {
             ch.bar = chainBar;
             ch.normPartials = partials;
             ch.normOut = dNorm;
-            fast::chain_down(P, ch, chainGrid, stream);
+            {  // small chains run as one thread-block cluster (hardware barriers, no atomics)
+                unsigned long long pts = 0;
+                for (int l = 1; l <= top; ++l) pts += lv[l].n;
+                ch.cluster = (clusterSize > 0 && pts <= kClusterMaxPts) ? 1 : 0;
+            }
+            fast::chain_down(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
         }
         for (int l = useChain ? top + 1 : 1; l < L; ++l)
             fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
@@ -903,7 +910,7 @@ struct Hierarchy::Impl {
                     fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
                 ch.firstRestrict = 0;
                 ch.normBlocks = fused2::blocks(geo2);
-                fast::chain_up(P, ch, chainGrid, stream);
+                fast::chain_up(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
             } else {
                 dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused2::blocks(geo2), dNorm);
             }
@@ -949,7 +956,7 @@ struct Hierarchy::Impl {
                     fast::restrict_level(P, lv[top + 1], lv[top], nullptr, blocks_for(lv[top].n), stream);
                 ch.firstRestrict = 0;
                 ch.normBlocks = fused3::blocks(geo);
-                fast::chain_up(P, ch, chainGrid, stream);
+                fast::chain_up(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
             } else {
                 dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, fused3::blocks(geo), dNorm);
             }
@@ -967,7 +974,7 @@ struct Hierarchy::Impl {
         if (useChain) {
             ch.firstRestrict = 1;  // fine = lv[top + 1] into lv[top]
             ch.normBlocks = nb;
-            fast::chain_up(P, ch, chainGrid, stream);
+            fast::chain_up(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
         } else {
             dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, nb, dNorm);
         }
@@ -1167,6 +1174,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
         if (coop && !(cz && cz[0] == '0')) {
             I.chainGrid = fast::chain_grid(I.p, I.smCount);
             I.chainBar = I.alloc<unsigned>(2);
+            const char* cl = std::getenv("TMG_CHAIN_CLUSTER");
+            if (!(cl && cl[0] == '0')) I.clusterSize = fast::chain_cluster_size();
         }
     }
     I.dNorm = I.alloc<double>(2);
