@@ -13,6 +13,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <thread>
 
 #include "exact_ops.cuh"
 #include "lattice.cuh"
@@ -525,6 +526,24 @@ int pow3(int l) {
     return r;
 }
 
+// fn(begin, end) over [0, n) on the host's cores (the setup loops write only
+// their own element)
+template <class F>
+void parallel_for(long long n, F&& fn) {
+    const unsigned hw = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    if (n < 65536 || hw == 1) {
+        fn(0LL, n);
+        return;
+    }
+    std::vector<std::thread> ts;
+    const long long chunk = (n + hw - 1) / hw;
+    for (unsigned t = 0; t < hw; ++t) {
+        const long long a = static_cast<long long>(t) * chunk, b = std::min(n, a + chunk);
+        if (a < b) ts.emplace_back([&fn, a, b] { fn(a, b); });
+    }
+    for (auto& t : ts) t.join();
+}
+
 int tz3h(int x) {
     if (x == 0) return 31;
     int t = 0;
@@ -621,8 +640,9 @@ std::vector<HostLevel> build_sphere_tree(int p, int base, int L) {
         for (int d = 0; d < p; ++d) h.n *= h.n1[d];
         if (h.n >= (1LL << 31)) throw CapacityError("adaptive level box exceeds 2^31 vertices");
         h.cflag.assign(static_cast<size_t>(h.n), 0);
+        parallel_for(h.n, [&](long long fa, long long fb) {
         int g[3] = {0, 0, 0};
-        for (long long f = 0; f < h.n; ++f) {
+        for (long long f = fa; f < fb; ++f) {
             box_unflat(h, p, f, g);
             bool inDomain = true;
             for (int d = 0; d < p; ++d) inDomain &= g[d] <= h.m - 1;
@@ -639,12 +659,15 @@ std::vector<HostLevel> build_sphere_tree(int p, int base, int L) {
             const bool refined = l < L && (l < base || centre_in_sphere(p, l, g));
             h.cflag[f] = static_cast<unsigned char>(kCellExists | (refined ? kCellRefined : 0));
         }
+        });
         // vertices: classification (spacetree.cpp:438-466) + finish corner
         h.vflag.assign(static_cast<size_t>(h.n), 0);
         h.estar.assign(static_cast<size_t>(h.n), 0xFF);
         h.succ.assign(static_cast<size_t>(h.n), 0);
         const int nc = 1 << p;
-        for (long long f = 0; f < h.n; ++f) {
+        parallel_for(h.n, [&](long long fa, long long fb) {
+        int g[3] = {0, 0, 0};
+        for (long long f = fa; f < fb; ++f) {
             box_unflat(h, p, f, g);
             int total = 0, have = 0, refAdj = 0;
             bool cellOk[8] = {false, false, false, false, false, false, false, false};
@@ -686,13 +709,16 @@ std::vector<HostLevel> build_sphere_tree(int p, int base, int L) {
                 }
             }
         }
+        });
     }
     // succ, finest level first (Spacetree::classify, spacetree.cpp:491-494)
     for (int l = L; l >= 0; --l) {
         HostLevel& h = lv[l];
+        if (l == L) continue;
+        parallel_for(h.n, [&](long long fa, long long fb) {
         int g[3] = {0, 0, 0};
-        for (long long f = 0; f < h.n; ++f) {
-            if (!(h.vflag[f] & kExists) || !(h.vflag[f] & kRefined) || l == L) continue;
+        for (long long f = fa; f < fb; ++f) {
+            if (!(h.vflag[f] & kExists) || !(h.vflag[f] & kRefined)) continue;
             box_unflat(h, p, f, g);
             const HostLevel& fh = lv[l + 1];
             const int mf = fh.m;
@@ -713,6 +739,7 @@ std::vector<HostLevel> build_sphere_tree(int p, int base, int L) {
                     }
             h.succ[f] = static_cast<signed char>(minSucc == INT_MAX ? 0 : 1 + minSucc);
         }
+        });
     }
     return lv;
 }
@@ -723,8 +750,9 @@ void mark_regular_chi(std::vector<HostLevel>& lv, int p) {
     for (int l = 0; l < L; ++l) {
         HostLevel& h = lv[l];
         const HostLevel& fh = lv[l + 1];
+        parallel_for(h.n, [&](long long fa, long long fb) {
         int g[3] = {0, 0, 0};
-        for (long long f = 0; f < h.n; ++f) {
+        for (long long f = fa; f < fb; ++f) {
             if (!(h.vflag[f] & kExists)) continue;
             box_unflat(h, p, f, g);
             bool reg = true;
@@ -755,6 +783,7 @@ void mark_regular_chi(std::vector<HostLevel>& lv, int p) {
             }
             if (reg) h.vflag[f] |= kRegularChi;
         }
+        });
     }
 }
 
