@@ -215,6 +215,61 @@ __global__ void __launch_bounds__(TX* TY) k_residual3(ResArgs a, int zch) {
     dev::block_norms(nmax, nsum, a.partials);
 }
 
+// ---- fast load vector: b = ms (M x M x M) f, the assembled consistent mass
+// matrix as a separable 1/6 2/3 1/6 stencil per axis (kernels.cpp:69-87 summed
+// over the cells around each vertex; interior vertices only, the boundary ones
+// are pinned).  z-marching like k_residual3: 32 B of HBM per vertex.
+__global__ void __launch_bounds__(TX* TY) k_load3(Lvl F, const double2* __restrict__ f, double2 ms, int zlo,
+                                                  int zhi, int zch) {
+    const int m = static_cast<int>(F.m);
+    const long long sy = F.n1, sz = static_cast<long long>(F.n1) * F.n1;
+    const int x = blockIdx.x * TX + threadIdx.x + 1;
+    const int y = blockIdx.y * TY + threadIdx.y + 1;
+    const int z0 = zlo + blockIdx.z * zch;
+    const int z1 = min(z0 + zch, zhi);
+    if (x > m - 1 || y > m - 1 || z0 >= z1) return;
+    const long long base = x + y * sy;
+    const double wc = 4.0 / 9.0, we = 1.0 / 9.0, wk = 1.0 / 36.0;  // (2/3)^2, (2/3)(1/6), (1/6)^2
+    auto plane = [&](int z) {
+        const double2* p = f + base + z * sz;
+        const double2 C = ld(p);
+        const double2 E = add(add(ld(p - 1), ld(p + 1)), add(ld(p - sy), ld(p + sy)));
+        const double2 K = add(add(ld(p - 1 - sy), ld(p + 1 - sy)), add(ld(p - 1 + sy), ld(p + 1 + sy)));
+        return make_double2(fma(wc, C.x, fma(we, E.x, wk * K.x)), fma(wc, C.y, fma(we, E.y, wk * K.y)));
+    };
+    double2 Sm = plane(z0 - 1), S0 = plane(z0);
+    for (int z = z0; z < z1; ++z) {
+        const double2 Sp = plane(z + 1);
+        const double2 S = make_double2(fma(2.0 / 3.0, S0.x, (Sm.x + Sp.x) / 6.0), fma(2.0 / 3.0, S0.y, (Sm.y + Sp.y) / 6.0));
+        F.chi[base + z * sz] = mul(ms, S);
+        Sm = S0;
+        S0 = Sp;
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(256) k_load_lowdim(Lvl F, const double2* __restrict__ f, double2 ms) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < F.n; i += gridDim.x * blockDim.x) {
+        int idx[P];
+        dev::unflat<P>(i, F.n1, idx);
+        if (dev::on_boundary<P>(idx, static_cast<int>(F.m))) continue;
+        double2 S;
+        if (P == 1) {
+            S = make_double2(fma(2.0 / 3.0, f[i].x, (f[i - 1].x + f[i + 1].x) / 6.0),
+                             fma(2.0 / 3.0, f[i].y, (f[i - 1].y + f[i + 1].y) / 6.0));
+        } else {
+            const long long sy = F.n1;
+            const double2* p = f + i;
+            const double2 C = ld(p);
+            const double2 E = add(add(ld(p - 1), ld(p + 1)), add(ld(p - sy), ld(p + sy)));
+            const double2 K = add(add(ld(p - 1 - sy), ld(p + 1 - sy)), add(ld(p - 1 + sy), ld(p + 1 + sy)));
+            const double wc = 4.0 / 9.0, we = 1.0 / 9.0, wk = 1.0 / 36.0;
+            S = make_double2(fma(wc, C.x, fma(we, E.x, wk * K.x)), fma(wc, C.y, fma(we, E.y, wk * K.y)));
+        }
+        F.chi[i] = mul(ms, S);
+    }
+}
+
 // ---- K2f (1D / 2D): thread per vertex ---------------------------------------
 template <int P>
 __global__ void __launch_bounds__(256) k_residual_lowdim(ResArgs a) {
@@ -795,6 +850,20 @@ void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cud
     if (P == 1) k_topdown<1, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
     else if (P == 2) k_topdown<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
     else k_topdown<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
+}
+
+void load_vector(int P, const Lvl& F, const double2* f, double2 ms, int blocks, cudaStream_t s, int za, int zb) {
+    if (P == 3) {
+        const int m = static_cast<int>(F.m);
+        const int zlo = std::max(1, za < 0 ? 1 : za), zhi = std::min(m, za < 0 ? m : zb);
+        if (zhi <= zlo) return;
+        dim3 grid((m - 1 + TX - 1) / TX, (m - 1 + TY - 1) / TY, (zhi - zlo + kZch - 1) / kZch);
+        k_load3<<<grid, dim3(TX, TY), 0, s>>>(F, f, ms, zlo, zhi, kZch);
+    } else if (P == 2) {
+        k_load_lowdim<2><<<blocks, 256, 0, s>>>(F, f, ms);
+    } else {
+        k_load_lowdim<1><<<blocks, 256, 0, s>>>(F, f, ms);
+    }
 }
 
 int residual_fine_blocks(int P, const Lvl& f, int smCount) {

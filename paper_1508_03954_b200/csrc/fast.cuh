@@ -42,6 +42,10 @@ void correct_fine(int P, const dev::Lvl& f, const dev::Lvl& pr, int bpx, int blo
 // (za, zb): plane range of the last axis, za < 0 for the whole level.
 void topdown_coarse(int P, const dev::Lvl& c, const dev::Lvl& pr, int bpx, int blocks, cudaStream_t s, int za = -1,
                     int zb = -1);
+// Load vector b = massScale (M x..x M) f on the interior of the finest level
+// (planes [za, zb) of the last axis in 3D; za < 0: all).
+void load_vector(int P, const dev::Lvl& F, const double2* f, double2 ms, int blocks, cudaStream_t s, int za = -1,
+                 int zb = -1);
 // Fine residual r = b - H u, norms, sc = omega r / diag, BPX injection; r to lv.rhat.
 // Returns the number of blocks that wrote norm partials.
 int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s);

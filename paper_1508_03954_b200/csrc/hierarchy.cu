@@ -780,6 +780,11 @@ struct Hierarchy::Impl {
     // load vector on planes [za, zb) of the last axis (za < 0: everywhere)
     void load_vector_dispatch(int za = -1, int zb = -1) {
         const dev::Lvl& F = lv[L];
+        if (prob.fast) {  // separable assembled mass stencil (rounding differs from the cell-by-cell sum)
+            fast::load_vector(p, F, chiNodal, kc[L].massScale, blocks_for(F.n), stream, za, zb);
+            TMG_CUDA(cudaGetLastError());
+            return;
+        }
         unsigned fa = 0, fb = F.n;
         if (za >= 0) {
             unsigned plane = 1;
