@@ -65,31 +65,23 @@ __global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx) {
             q[d] = min(idx[d] / 3, static_cast<int>(pr.m) - 1);
             rel[d] = idx[d] - 3 * q[d];
         }
-        double2 cu[1 << P], cs[1 << P];
-#pragma unroll
-        for (int e = 0; e < (1 << P); ++e) {
-            int pi[P];
-#pragma unroll
-            for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
-            const unsigned pf = flat<P>(pi, pr.n1);
-            cu[e] = pr.u[pf];
-            cs[e] = pr.sc[pf];
-        }
-        double2 sc = xadd(c.sc[f], prolong<P>(cs, rel));
-        if (bpx && !is_cpoint<P>(idx)) {
-            double2 ci[1 << P];
+        // one field at a time (register footprint): P sc, P si (BPX), P u
+        auto parent_prolong = [&](const double2* src) {
+            double2 v[1 << P];
 #pragma unroll
             for (int e = 0; e < (1 << P); ++e) {
                 int pi[P];
 #pragma unroll
                 for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
-                ci[e] = pr.si[flat<P>(pi, pr.n1)];
+                v[e] = src[flat<P>(pi, pr.n1)];
             }
-            sc = xsub(sc, prolong<P>(ci, rel));
-        }
+            return prolong<P>(v, rel);
+        };
+        double2 sc = xadd(c.sc[f], parent_prolong(pr.sc));
+        if (bpx && !is_cpoint<P>(idx)) sc = xsub(sc, parent_prolong(pr.si));
         const double2 sf = c.sf ? c.sf[f] : cz();
         double2 u = xadd(c.u[f], xadd(sc, sf));
-        double2 uh = xsub(u, prolong<P>(cu, rel));
+        double2 uh = xsub(u, parent_prolong(pr.u));
         if (on_boundary<P>(idx, static_cast<int>(c.m))) {
             u = cz();
             uh = cz();
@@ -163,8 +155,11 @@ __device__ __forceinline__ double2 element_residual(const double2* __restrict__ 
 }
 
 // ---- K2/K3: residual + Jacobi staging + injections (enterCell/touchLast) --
+#ifndef TMG_EXACT_RES_MINB
+#define TMG_EXACT_RES_MINB 3
+#endif
 template <int P>
-__global__ void __launch_bounds__(256) k_residual_exact(ResArgs a) {
+__global__ void __launch_bounds__(256, TMG_EXACT_RES_MINB) k_residual_exact(ResArgs a) {
     const Lvl& c = a.lv;
     double nmax = 0.0, nsum = 0.0;
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
