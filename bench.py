@@ -398,7 +398,7 @@ def main():
         z0, z1 = h.owned_planes()
         B_fine = fine_bytes_per_vertex(w, args.precision) * (z1 - z0) * (3 ** w["level"] + 1) ** 2
         B_total = B_total * (z1 - z0) / (3 ** w["level"] - 1)
-        launches_per_cycle = 2 * w["level"] + 6
+        launches_per_cycle = int(out[3]) or (2 * w["level"] + 6)
     peak, peak_kind = peaks()
     achieved = B_fine / (fine_ms / 1e3) / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -844,30 +844,11 @@ struct Hierarchy::Impl {
         };
         // levels 1..top (each below kChainMaxN points) run as one cooperative
         // chain per phase; bigger levels keep their own full-grid launches
-        int top = L - 1;
-        while (top >= 1 && lv[top].n >= kChainMaxN) --top;
-        const bool useChain = chainGrid > 0 && top >= 1 && top < fast::kMaxChainLevels;
+        const int top = chain_top(L - 1);
+        const bool useChain = top >= 1;
         fast::ChainArgs ch{};
         if (useChain) {
-            for (int l = 0; l <= top; ++l) {
-                ch.lv[l] = lv[l];
-                ch.k[l] = fc[l];
-                const Cplx w = omega_unmasked(pol, L - l, n);
-                ch.k[l].wRaw = make_double2(w.real(), w.imag());
-            }
-            ch.fine = lv[top + 1];
-            ch.top = top;
-            ch.ellMin = prob.ellMin;
-            ch.bpx = bpx;
-            ch.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
-            ch.bar = chainBar;
-            ch.normPartials = partials;
-            ch.normOut = dNorm;
-            {  // small chains run as one thread-block cluster (hardware barriers, no atomics)
-                unsigned long long pts = 0;
-                for (int l = 1; l <= top; ++l) pts += lv[l].n;
-                ch.cluster = (clusterSize > 0 && pts <= kClusterMaxPts) ? 1 : 0;
-            }
+            ch = make_chain(pol, n, top);
             fast::chain_down(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
         }
         for (int l = useChain ? top + 1 : 1; l < L; ++l)
@@ -1011,12 +992,41 @@ struct Hierarchy::Impl {
         }
     }
 
+    // highest level <= maxLevel of the coarse chain (every level below kChainMaxN
+    // points joins it); 0 when chains are off
+    int chain_top(int maxLevel) const {
+        int top = maxLevel;
+        while (top >= 1 && lv[top].n >= kChainMaxN) --top;
+        return (chainGrid > 0 && top >= 1 && top < fast::kMaxChainLevels) ? top : 0;
+    }
+
+    fast::ChainArgs make_chain(const Policy& pol, int n, int top) const {
+        fast::ChainArgs ch{};
+        for (int l = 0; l <= top; ++l) {
+            ch.lv[l] = lv[l];
+            ch.k[l] = fc[l];
+            const Cplx w = omega_unmasked(pol, L - l, n);
+            ch.k[l].wRaw = make_double2(w.real(), w.imag());
+        }
+        ch.fine = lv[top + 1];
+        ch.top = top;
+        ch.ellMin = prob.ellMin;
+        ch.bpx = pol.bpx ? 1 : 0;
+        ch.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+        ch.bar = chainBar;
+        ch.normPartials = partials;
+        ch.normOut = dNorm;
+        unsigned long long pts = 0;  // small chains run as one thread-block cluster
+        for (int l = 1; l <= top; ++l) pts += lv[l].n;
+        ch.cluster = (clusterSize > 0 && pts <= kClusterMaxPts) ? 1 : 0;
+        return ch;
+    }
+
     // kernel launches of one cycle (bench.py "gpu_launches"), mirroring cycle_fast / cycle_exact
     int launches_per_cycle() const {
         if (!prob.fast) return 3 * L;  // top-down 1..L, residual L..1, restriction L..2, norm
-        int top = L - 1;
-        while (top >= 1 && lv[top].n >= kChainMaxN) --top;
-        const bool useChain = chainGrid > 0 && top >= 1 && top < fast::kMaxChainLevels;
+        const int top = chain_top(L - 1);
+        const bool useChain = top >= 1;
         const bool fusedPath = (p == 3 && fused) || (p == 2 && fused2on);
         const int lo = useChain ? top + 1 : 1;
         int n = useChain ? 1 + (L - 1 - top) : (L - 1);  // top-down
