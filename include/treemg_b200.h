@@ -94,6 +94,15 @@ void tmg_hierarchy_destroy(tmg_hierarchy* h);
 treemg_status tmg_td_add(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
 treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
 
+/* Verification cycles of a regular tree held in exact storage (precision 0),
+ * each followed by evaluate_residual_norms (cycles.cpp:716-786) into *out:
+ * bu_fas(tree, spec, pol, n) (cycles.cpp:374-603) and
+ * textbook_add(tree, spec, omegaS, omegaCG) (cycles.cpp:605-714).  The
+ * reference sums these in hash-map order, so parity is a tolerance, not
+ * bit-identity. */
+treemg_status tmg_bu_fas(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
+treemg_status tmg_textbook_add(tmg_hierarchy* h, double omega_s_re, double omega_s_im, double omega_cg_re,
+                               double omega_cg_im, tmg_sweep_stats* out);
 long long tmg_lattice_size(const tmg_hierarchy* h, int level);
 /* field: u chi r rhat uhat diag sc sf si sinext; out: 2*lattice_size doubles */
 treemg_status tmg_get_field(tmg_hierarchy* h, int level, const char* field, double* out);

@@ -47,7 +47,8 @@ EXTENSION_SYMBOLS = [
     "tmg_set_fine_rhs", "tmg_field_hash", "tmg_time_cycles", "tmg_e2e_step", "tmg_last_error",
     "treemg_result_fingerprint", "tmg_test_divdc3", "tmg_nccl_unique_id", "tmg_slabs_create", "tmg_slabs_destroy",
     "tmg_slabs_cycle", "tmg_slabs_get_fine_u", "tmg_slabs_time_cycles", "tmg_slabs_owned_planes", "tmg_slab_plan",
-    "tmg_slabs_e2e_step",
+    "tmg_slabs_e2e_step", "tmg_get_flags", "tmg_hanging_vertices", "tmg_leaf_vertices", "tmg_sphere_tree",
+    "tmg_bu_fas", "tmg_textbook_add",
 ]
 
 _lib = None
@@ -128,6 +129,11 @@ def lib():
         L.tmg_hanging_vertices.argtypes = [vp]
         L.tmg_leaf_vertices.restype = ctypes.c_longlong
         L.tmg_leaf_vertices.argtypes = [vp]
+        L.tmg_bu_fas.restype = ip
+        L.tmg_bu_fas.argtypes = [vp, ctypes.POINTER(_Policy), ip, ctypes.POINTER(_Stats)]
+        L.tmg_textbook_add.restype = ip
+        L.tmg_textbook_add.argtypes = [vp, ctypes.c_double, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                       ctypes.POINTER(_Stats)]
         L.tmg_lattice_size.restype = ctypes.c_longlong
         L.tmg_lattice_size.argtypes = [vp, ip]
         L.tmg_get_field.restype = ip
@@ -290,6 +296,17 @@ class Hierarchy:
 
     def td_bpx(self, pol: Policy, n: int) -> SweepStats:
         return self._sweep(self.L.tmg_td_bpx, pol, n)
+
+    def bu_fas(self, pol: Policy, n: int) -> SweepStats:
+        """bu_fas + evaluate_residual_norms (cycles.cpp:374-603, 716-786); exact storage."""
+        return self._sweep(self.L.tmg_bu_fas, pol, n)
+
+    def textbook_add(self, omega_s: complex, omega_cg: complex) -> SweepStats:
+        """textbook_add + evaluate_residual_norms (cycles.cpp:605-714, 716-786); exact storage."""
+        st = _Stats()
+        _check(self.L.tmg_textbook_add(self.h, complex(omega_s).real, complex(omega_s).imag,
+                                       complex(omega_cg).real, complex(omega_cg).imag, ctypes.byref(st)))
+        return SweepStats(st.max_norm, st.euclid_norm, st.h_norm, st.updated_fine_vertices)
 
     def lattice_size(self, level: int) -> int:
         return self.L.tmg_lattice_size(self.h, level)

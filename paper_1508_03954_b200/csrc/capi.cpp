@@ -324,6 +324,22 @@ treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_swe
     });
 }
 
+treemg_status tmg_bu_fas(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
+    if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        if (n < 1) throw ConfigError("sweep counter starts at 1");
+        fill_stats(h->h->bu_fas(policy_from(pol), n), out);
+    });
+}
+
+treemg_status tmg_textbook_add(tmg_hierarchy* h, double omega_s_re, double omega_s_im, double omega_cg_re,
+                               double omega_cg_im, tmg_sweep_stats* out) {
+    if (!h) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        fill_stats(h->h->textbook_add(Cplx(omega_s_re, omega_s_im), Cplx(omega_cg_re, omega_cg_im)), out);
+    });
+}
+
 long long tmg_lattice_size(const tmg_hierarchy* h, int level) { return h ? h->h->lattice_size(level) : 0; }
 
 treemg_status tmg_get_field(tmg_hierarchy* h, int level, const char* field, double* out) {

@@ -26,6 +26,7 @@
 #include "fused2.cuh"
 #include "fused3.cuh"
 #include "hierarchy.hpp"
+#include "vcycles.cuh"
 #include "lattice.cuh"
 
 namespace tmg {
@@ -565,6 +566,7 @@ struct Hierarchy::Impl {
     fused3::Geometry geo{};
     double2* partial3 = nullptr;
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
+    std::vector<double2*> vcScratch;  // verification cycles: per-level residual
     bool fused2on = false;         // 2D fused fine pass (fast precision)
     fused2::Geometry geo2{};
     double2* partial2 = nullptr;
@@ -1223,6 +1225,65 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
 Hierarchy::~Hierarchy() = default;
 
 SweepStats Hierarchy::cycle(const Policy& pol, int n) { return impl_->cycle(pol, n); }
+
+namespace {
+vc::Ctx vc_ctx(Hierarchy::Impl& I, std::vector<double2*>& scratch) {
+    if (I.amr) throw UnsupportedConfigError("verification cycles run on regular trees (runner.cpp:232)");
+    if (I.prob.fast) throw UnsupportedConfigError("verification cycles need the exact storage (precision = exact)");
+    if (scratch.empty())
+        for (int l = 0; l <= I.L; ++l) scratch.push_back(I.alloc<double2>(I.lv[l].n));
+    vc::Ctx x{};
+    x.lv = I.lv.data();
+    x.L = I.L;
+    x.ellMin = I.prob.ellMin;
+    x.fc = I.fc.data();
+    x.r = scratch.data();
+    x.partials = I.partials;
+    x.dNorm = I.dNorm;
+    x.stream = I.stream;
+    x.smCount = I.smCount;
+    return x;
+}
+
+SweepStats vc_norms(Hierarchy::Impl& I, const vc::Ctx& x) {
+    double out[2];
+    vc::residual_norms(I.p, x, out);
+    SweepStats st;
+    const double hp = std::pow(std::pow(3.0, -I.L), I.p);
+    st.maxNorm = std::sqrt(out[0]);
+    st.euclidNorm = std::sqrt(out[1]);
+    st.hNorm = std::sqrt(hp * out[1]);
+    long long inner = 1;
+    for (int d = 0; d < I.p; ++d) inner *= pow3i(I.L) - 1;
+    st.updatedFineVertices = inner;
+    return st;
+}
+}  // namespace
+
+SweepStats Hierarchy::bu_fas(const Policy& pol, int n) {
+    Impl& I = *impl_;
+    const vc::Ctx x = vc_ctx(I, I.vcScratch);
+    I.check_diag();
+    std::vector<double2> wn(I.L + 1), wc(I.L + 1);
+    for (int l = 0; l <= I.L; ++l) {  // omega_of (cycles.cpp:33-36) with succ = L - l
+        const Cplx w = omega_unmasked(pol, I.L - l, n);
+        wn[l] = make_double2(w.real(), w.imag());
+        wc[l] = pol.hbMask ? make_double2(0.0, 0.0) : wn[l];
+    }
+    vc::bu_fas(I.p, x, wn.data(), wc.data(), pol.bpx ? 1 : 0);
+    TMG_CUDA(cudaGetLastError());
+    I.coarseUStale = false;
+    return vc_norms(I, x);
+}
+
+SweepStats Hierarchy::textbook_add(Cplx omegaS, Cplx omegaCG) {
+    Impl& I = *impl_;
+    const vc::Ctx x = vc_ctx(I, I.vcScratch);
+    I.check_diag();
+    vc::textbook_add(I.p, x, make_double2(omegaS.real(), omegaS.imag()), make_double2(omegaCG.real(), omegaCG.imag()));
+    TMG_CUDA(cudaGetLastError());
+    return vc_norms(I, x);
+}
 
 int Hierarchy::dim() const { return impl_->p; }
 int Hierarchy::levels() const { return impl_->L; }

@@ -85,6 +85,11 @@ class Hierarchy {
 
     // One cycle.  bpx selects td_bpx (hb mask forced off, cycles.cpp:345-354).
     SweepStats cycle(const Policy& pol, int n);
+    // Verification cycles of a regular tree in exact storage (precision = exact),
+    // each followed by evaluate_residual_norms: bu_fas (cycles.cpp:374-603) and
+    // textbook_add (cycles.cpp:605-714).
+    SweepStats bu_fas(const Policy& pol, int n);
+    SweepStats textbook_add(Cplx omegaS, Cplx omegaCG);
 
     int dim() const;
     int levels() const;

@@ -88,6 +88,15 @@ CONFIGS = {
                        omega="undamped", omega_s=0.6, max_sweeps=150, target_drop=1e-8, **SEEDED),
     "amr2d_bpx": dict(problem="helmholtz-sin", dim=2, level=2, sphere_levels=3, phi="100,50", cycle="td-bpx",
                       omega="undamped", omega_s=0.5, max_sweeps=40, target_drop=1e-8, **SEEDED),
+    # verification cycles: bottom-up FAS and textbook additive, regular trees
+    "vc_bufas_2d": dict(problem="helmholtz-sin", dim=2, level=4, phi="100,50", cycle="bu-fas", omega="exponential",
+                        omega_s=0.6, max_sweeps=40, target_drop=1e-8, **SEEDED),
+    "vc_bufas_3d_poisson": dict(problem="poisson-sin", dim=3, level=3, cycle="bu-fas", omega="undamped",
+                                omega_s=0.8, max_sweeps=30, target_drop=1e-8, norm="h"),
+    "vc_textbook_2d": dict(problem="helmholtz-sin", dim=2, level=4, phi="100,50", cycle="textbook", omega_s=0.6,
+                           max_sweeps=40, target_drop=1e-8, **SEEDED),
+    "vc_textbook_3d_cg": dict(problem="helmholtz-sin", dim=3, level=3, phi="400,200", cycle="textbook", omega_s=0.6,
+                              omega_cg=0.9, max_sweeps=25, target_drop=1e-8, **SEEDED),
     "rotated_3d_bpx": dict(problem="helmholtz-sin", dim=3, level=3, phi="2025", theta_deg=35, cycle="td-bpx",
                            omega="transition", max_sweeps=15, target_drop=1e-30),
 }
