@@ -53,7 +53,7 @@ def test_version_and_error_codes(tmg):
     ({"level": "2", "h_max": "0.1", "h_min": "0.01"}, 1),  # level and adaptive bounds conflict
     ({"level": "2", "problem": "nope"}, 1),
     ({"level": "10"}, 1),                                 # kMaxLevel
-    ({"level": "2", "cycle": "bu-fas"}, 1),               # not on the device path
+    ({"level": "2", "cycle": "bu-fas", "sphere_levels": "1"}, 1),  # runner.cpp:232: adaptive needs td-*
     ({"level": "2", "channels": "2"}, 1),
     ({"dim": "4", "level": "2"}, 1),
 ])
