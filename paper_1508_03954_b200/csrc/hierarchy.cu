@@ -236,18 +236,30 @@ __global__ void __launch_bounds__(256) k_restrict_exact(Lvl fine, Lvl coarse, co
         const int pid = perm_id<P>(W);
         double2 acc = cz();
         const int mf = static_cast<int>(fine.m);
-        for (int i = 0; i < NT; ++i) {
-            int code = st[pid * NT + i];
-            int v[P];
-            bool in = true;
+        // loads in batches of (up to) 25 independent addresses, then the ordered
+        // sum: the touch-last order stays sequential, the latency chain does not
+        constexpr int NB = NT < 25 ? NT : 25;
+        for (int i0 = 0; i0 < NT; i0 += NB) {
+            double2 vals[NB];
+            double wts[NB];
 #pragma unroll
-            for (int d = 0; d < P; ++d) {
-                v[d] = 3 * W[d] + (code % 5) - 2;
-                code /= 5;
-                in &= (v[d] >= 1) & (v[d] <= mf - 1);
+            for (int b = 0; b < NB; ++b) {
+                const int c0 = st[pid * NT + i0 + b];
+                int code = c0;
+                int v[P];
+                bool in = true;
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    v[d] = 3 * W[d] + (code % 5) - 2;
+                    code /= 5;
+                    in &= (v[d] >= 1) & (v[d] <= mf - 1);
+                }
+                wts[b] = in ? sw[c0] : 0.0;
+                vals[b] = in ? fine.rhat[flat<P>(v, fine.n1)] : cz();
             }
-            if (!in) continue;
-            acc = xadd(acc, xscale(sw[st[pid * NT + i]], fine.rhat[flat<P>(v, fine.n1)]));
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                if (wts[b] != 0.0) acc = xadd(acc, xscale(wts[b], vals[b]));
         }
         coarse.chi[f] = acc;
     }
