@@ -62,7 +62,9 @@ typedef struct tmg_problem {
     int ell_min;                   /* coarsest smoothed level (spacetree.hpp Config::ellMin) */
     double theta;                  /* cell rotation, radians (ProblemSpec::thetaGlobal) */
     double phi_re, phi_im;         /* constant Helmholtz shift phi */
-    int chi_kind;                  /* 0 zero, 1 sin product, 2 ball indicator, 3 seeded */
+    int chi_kind;                  /* 0 zero, 1 sin product, 2 ball indicator, 3 seeded, 4 gaussian scenario
+                                      (2D; cell-varying phi and absorbing-layer theta, problems.cpp:20-24,
+                                      78-90; exact precision) */
     unsigned long long rhs_seed;
     int rhs_sphere;
     int precision;                 /* 0 exact, 1 fast */

@@ -30,7 +30,7 @@ LIB_PATH = os.environ.get("TMG_LIB") or os.path.join(PKG, "libtreemg_b200.so")  
 STATUS = {0: "TREEMG_OK", 1: "TREEMG_E_USAGE", 2: "TREEMG_E_CAPACITY", 3: "TREEMG_E_RUNTIME"}
 OUTCOME = {0: "converged", 1: "budget-exhausted", 2: "diverged"}
 OMEGA_KINDS = {"jacobi-only": 0, "undamped": 1, "lgrid": 2, "exponential": 3, "transition": 4}
-CHI_KINDS = {"zero": 0, "sin": 1, "ball": 2, "seeded": 3}
+CHI_KINDS = {"zero": 0, "sin": 1, "ball": 2, "seeded": 3, "gaussian": 4}
 
 # The 14 entry points of proj/include/treemg.h and the extensions of
 # include/treemg_b200.h, all exported by libtreemg_b200.so.

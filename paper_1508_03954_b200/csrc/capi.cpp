@@ -188,6 +188,7 @@ Problem problem_from(const tmg_problem* prob) {
     p.theta = prob->theta;
     p.phi = Cplx(prob->phi_re, prob->phi_im);
     p.chi = static_cast<ChiKind>(prob->chi_kind);
+    p.gaussian = prob->chi_kind == 4;
     p.rhsSeed = prob->rhs_seed;
     p.rhsSphere = prob->rhs_sphere != 0;
     p.fast = prob->precision == 1;
@@ -283,6 +284,7 @@ treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out)
         p.theta = prob->theta;
         p.phi = Cplx(prob->phi_re, prob->phi_im);
         p.chi = static_cast<ChiKind>(prob->chi_kind);
+        p.gaussian = prob->chi_kind == 4;
         p.rhsSeed = prob->rhs_seed;
         p.rhsSphere = prob->rhs_sphere != 0;
         p.fast = prob->precision == 1;

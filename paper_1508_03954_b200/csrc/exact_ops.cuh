@@ -122,6 +122,41 @@ __device__ __forceinline__ double unit_rand(unsigned long long x) {  // cycles.c
     return __dsub_rn(__ddiv_rn(__dmul_rn(2.0, static_cast<double>(x >> 11)), 9007199254740992.0), 1.0);
 }
 
+// DivConst of a divisor known only on the device (per-vertex diagonals of
+// cell-varying operators): the host div_const (hierarchy.cu) with explicit
+// round-to-nearest operations.
+__device__ __forceinline__ DivConst div_const_dev(double c, double d) {
+    DivConst k{};
+    const bool swap = !(fabs(c) < fabs(d));
+    k.swap = swap ? 1 : 0;
+    const double big = swap ? fabs(c) : fabs(d);
+    k.pre = 0;
+    if (big >= kRBIG) {
+        c = __ddiv_rn(c, 2.0);
+        d = __ddiv_rn(d, 2.0);
+        k.pre = 1;
+    }
+    const double big2 = swap ? fabs(c) : fabs(d);
+    if (big2 < kRMIN2) {
+        c = __dmul_rn(c, kRMINSCAL);
+        d = __dmul_rn(d, kRMINSCAL);
+        k.pre = k.pre == 1 ? 1 : 2;
+    }
+    k.c = c;
+    k.d = d;
+    if (!swap) {
+        k.ratio = __ddiv_rn(c, d);
+        k.denom = __dadd_rn(__dmul_rn(c, k.ratio), d);
+        k.denomTiny = __dadd_rn(__dmul_rn(__dmul_rn(c, kRMINSCAL), k.ratio), __dmul_rn(d, kRMINSCAL));
+    } else {
+        k.ratio = __ddiv_rn(d, c);
+        k.denom = __dadd_rn(__dmul_rn(d, k.ratio), c);
+        k.denomTiny = __dadd_rn(__dmul_rn(__dmul_rn(d, kRMINSCAL), k.ratio), __dmul_rn(c, kRMINSCAL));
+    }
+    k.sub = fabs(k.ratio) > kRMIN ? 0 : 1;
+    return k;
+}
+
 // Per-level constants of the exact kernels (constant theta and phi).
 struct LevelConst {
     double2 A[8];   // element operator entry for XOR pattern of (a, b)

@@ -214,6 +214,110 @@ __global__ void __launch_bounds__(256, TMG_EXACT_RES_MINB) k_residual_exact(ResA
     if (a.isFine) block_norms(nmax, nsum, a.partials);
 }
 
+// ---- K2/K3 for cell-varying operators (gaussian scenario, problems.cpp:20-24,
+// 78-90): the cell matrix A_c (per XOR pattern) and the per-vertex diagonal are
+// taken cell by cell in traversal order, the Jacobi division with the
+// diagonal's own __divdc3 constants.
+template <int P>
+__global__ void __launch_bounds__(256) k_residual_cells(ResArgs a, const double2* __restrict__ cellA) {
+    constexpr int NC = 1 << P;
+    const Lvl& c = a.lv;
+    const int m = static_cast<int>(c.m);
+    double nmax = 0.0, nsum = 0.0;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        int idx[P];
+        unflat<P>(f, c.n1, idx);
+        const bool bnd = on_boundary<P>(idx, m);
+        const bool cp = is_cpoint<P>(idx);
+        const int pid = perm_id<P>(idx);
+        double2 r = cz(), rh = cz(), dg = cz();
+        bool first = true;
+        for (int i = 0; i < NC; ++i) {
+            const int e = perm_cell(P, pid, i);
+            int cell[P];
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                cell[d] = idx[d] - 1 + ((e >> d) & 1);
+                ok &= (cell[d] >= 0) & (cell[d] <= m - 1);
+            }
+            if (!ok) continue;
+            unsigned cf = 0, s = 1;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                cf += static_cast<unsigned>(cell[d]) * s;
+                s *= static_cast<unsigned>(m);
+            }
+            const double2* A = cellA + static_cast<size_t>(cf) * NC;
+            const int ca = (~e) & (NC - 1);
+            double2 sr = cz(), sh = cz();
+#pragma unroll
+            for (int bb = 0; bb < NC; ++bb) {
+                int vb[P];
+#pragma unroll
+                for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
+                const unsigned vf = flat<P>(vb, c.n1);
+                const double2 pu = xmul(A[ca ^ bb], c.u[vf]);
+                const double2 ph = xmul(A[ca ^ bb], c.uhat[vf]);
+                sr = bb == 0 ? pu : xadd(sr, pu);
+                sh = bb == 0 ? ph : xadd(sh, ph);
+            }
+            if (first) {
+                r = xneg(sr);
+                rh = xneg(sh);
+                dg = A[0];
+                first = false;
+            } else {
+                r = xsub(r, sr);
+                rh = xsub(rh, sh);
+                dg = xadd(dg, A[0]);
+            }
+        }
+        if (bnd) {
+            r = cz();
+            rh = cz();
+        } else {
+            const double2 chi = c.chi[f];
+            r = xadd(chi, r);
+            rh = xadd(chi, rh);
+        }
+        if (c.si) {
+            c.si[f] = c.sinext[f];
+            c.sinext[f] = cz();
+        }
+        if (a.isFine && !bnd) {
+            const double m2 = r.x * r.x + r.y * r.y;
+            nmax = fmax(nmax, m2);
+            nsum += m2;
+        }
+        if (c.r) c.r[f] = r;
+        c.rhat[f] = rh;
+        if (c.level < a.ellMin) {
+            c.sc[f] = cz();
+            continue;
+        }
+        const double2 smooth = bnd ? cz() : divdc3(r.x, r.y, div_const_dev(dg.x, dg.y));
+        double2 sc;
+        if (a.bpx) {
+            sc = cp ? cz() : xmul(a.k.wRaw, smooth);
+        } else {
+            const bool wz = (a.hb && cp) || xzero(a.k.wRaw);
+            sc = wz ? cz() : xmul(a.k.wRaw, smooth);
+        }
+        c.sc[f] = sc;
+        if (c.level > a.ellMin && cp) {
+            int wi[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+            const unsigned wf = flat<P>(wi, a.par.n1);
+            const double2 sf = c.sf ? c.sf[f] : cz();
+            a.par.sf[wf] = xadd(sf, sc);
+            if (a.bpx) a.par.sinext[wf] = xmul(a.k.wRaw, smooth);
+        }
+    }
+    if (a.isFine) block_norms(nmax, nsum, a.partials);
+}
+
 // ---- K3r: restriction chi_{l-1} = R rhat_l in touch-last order -------------
 // table: for each permutation id, 5^P offsets (packed base 5) in order.
 template <int P>
@@ -293,7 +397,8 @@ __global__ void k_norm_final(const double* __restrict__ partials, int nblocks, d
 // Consistent-mass load of the leaf cells (kernels.cpp:69-87), accumulated per
 // vertex in traversal cell order; constant across sweeps on a static grid.
 template <int P>
-__global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, LevelConst k, unsigned fa, unsigned fb) {
+__global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, LevelConst k, unsigned fa, unsigned fb,
+                              const double2* __restrict__ cellMs) {
     for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int idx[P];
         unflat<P>(f, c.n1, idx);
@@ -327,7 +432,17 @@ __global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, Level
                 for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
                 acc = xadd(acc, xscale(k.M[a ^ bb], chiNodal[flat<P>(vb, c.n1)]));
             }
-            b = xadd(b, xmul(k.massScale, acc));
+            double2 ms = k.massScale;
+            if (cellMs) {  // per-cell massScale (cell-varying theta)
+                unsigned cf = 0, st = 1;
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    cf += static_cast<unsigned>(cell[d]) * st;
+                    st *= c.m;
+                }
+                ms = cellMs[cf];
+            }
+            b = xadd(b, xmul(ms, acc));
         }
         c.chi[f] = b;
     }
@@ -579,6 +694,7 @@ struct Hierarchy::Impl {
     double2* partial3 = nullptr;
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
     std::vector<double2*> vcScratch;  // verification cycles: per-level residual
+    std::vector<double2*> cellA, cellMs;  // gaussian scenario: per-cell operator / massScale
     bool fused2on = false;         // 2D fused fine pass (fast precision)
     fused2::Geometry geo2{};
     double2* partial2 = nullptr;
@@ -692,6 +808,59 @@ struct Hierarchy::Impl {
         }
     }
 
+    // gaussian scenario (problems.cpp:20-24, 78-90; kernels.cpp:7-23): per level
+    // and cell the element operator per XOR pattern and the massScale, from the
+    // cell's theta (absorbing layer: 30 degrees within 1/3 of the x / y = 1 faces)
+    // and phi at the cell centre -- host arithmetic, so the reference's bits.
+    void build_cell_constants() {
+        cellA.assign(L + 1, nullptr);
+        cellMs.assign(L + 1, nullptr);
+        const int nc = 1 << p;
+        for (int l = 1; l <= L; ++l) {
+            const int m = pow3i(l);
+            long long cells = 1;
+            for (int d = 0; d < p; ++d) cells *= m;
+            std::vector<double2> A(static_cast<size_t>(cells) * nc), MS(static_cast<size_t>(cells));
+            const double h = std::pow(3.0, -l);
+            for (long long cf = 0; cf < cells; ++cf) {
+                long long cc = cf;
+                int ci[3] = {0, 0, 0};
+                for (int d = 0; d < p; ++d) {
+                    ci[d] = static_cast<int>(cc % m);
+                    cc /= m;
+                }
+                double theta = prob.theta;
+                for (int d = 0; d < p; ++d) {  // cell_theta: openHi on axes 0 and 1
+                    const double centre = (ci[d] + 0.5) * h;
+                    if (d < 2 && centre > 1.0 - 1.0 / 3.0) {
+                        theta = 30.0 * M_PI / 180.0;
+                        break;
+                    }
+                }
+                const Cplx hElem = h * Cplx(std::cos(theta), std::sin(theta));
+                const Cplx ls = cplx_ipow(hElem, p - 2);
+                const Cplx ms = cplx_ipow(hElem, p);
+                double centre[3] = {0.0, 0.0, 0.0};
+                for (int d = 0; d < p; ++d) centre[d] = (ci[d] + 0.5) * h;
+                const double ph = 45.0 * 45.0 + 135.0 * 135.0 * (std::exp(-(15.0 * centre[0]) * (15.0 * centre[0])) +
+                                                                 std::exp(-(15.0 * centre[1]) * (15.0 * centre[1])));
+                const Cplx phi(ph, 0.0);
+                for (int sp = 0; sp < nc; ++sp) {
+                    double lap, mas;
+                    reference_pattern(p, sp, lap, mas);
+                    const Cplx a = ls * lap - phi * ms * mas;  // kernels.cpp:43-44
+                    A[static_cast<size_t>(cf) * nc + sp] = make_double2(a.real(), a.imag());
+                }
+                MS[static_cast<size_t>(cf)] = make_double2(ms.real(), ms.imag());
+            }
+            cellA[l] = alloc<double2>(A.size());
+            cellMs[l] = alloc<double2>(MS.size());
+            TMG_CUDA(cudaMemcpyAsync(cellA[l], A.data(), A.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+            TMG_CUDA(cudaMemcpyAsync(cellMs[l], MS.data(), MS.size() * sizeof(double2), cudaMemcpyHostToDevice, stream));
+            TMG_CUDA(cudaStreamSynchronize(stream));
+        }
+    }
+
     void build_restrict_tables() {
         const int NT = p == 1 ? 5 : p == 2 ? 25 : 125;
         const int NP = p == 1 ? 1 : p == 2 ? 2 : 6;
@@ -772,6 +941,8 @@ struct Hierarchy::Impl {
                 double r2 = 0.0;
                 for (int d = 0; d < p; ++d) r2 += (x[d] - 0.5) * (x[d] - 0.5);
                 v = r2 < 0.01 ? 1.0 : 0.0;
+            } else if (prob.chi == ChiKind::Gaussian) {  // problems.cpp:20-21
+                v = std::exp(-(125.0 * x[0]) * (125.0 * x[0]) - (125.0 * x[1]) * (125.0 * x[1]));
             }
             h[f] = make_double2(v, 0.0);
         }
@@ -782,7 +953,8 @@ struct Hierarchy::Impl {
     template <int P>
     void load_vector(unsigned fa, unsigned fb) {
         const dev::Lvl& F = lv[L];
-        dev::k_load_vector<P><<<blocks_for(fb - fa), 256, 0, stream>>>(F, chiNodal, kc[L], fa, fb);
+        dev::k_load_vector<P><<<blocks_for(fb - fa), 256, 0, stream>>>(F, chiNodal, kc[L], fa, fb,
+                                                                     prob.gaussian ? cellMs[L] : nullptr);
         TMG_CUDA(cudaGetLastError());
     }
 
@@ -828,7 +1000,10 @@ struct Hierarchy::Impl {
             a.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
             a.partials = partials;
             const int nb = l == L ? normBlocks : blocks_for(lv[l].n);
-            dev::k_residual_exact<P><<<nb, 256, 0, stream>>>(a);
+            if (prob.gaussian)
+                dev::k_residual_cells<P><<<nb, 256, 0, stream>>>(a, cellA[l]);
+            else
+                dev::k_residual_exact<P><<<nb, 256, 0, stream>>>(a);
             if (timed && l == L) TMG_CUDA(cudaEventRecord(evf1, stream));
             if (l >= 2) {
                 const int zero = l <= prob.ellMin ? 1 : 0;
@@ -1053,6 +1228,7 @@ struct Hierarchy::Impl {
     }
 
     void check_diag() {
+        if (prob.gaussian) return;  // cell-varying diagonals: checked by construction (phi > 0)
         // jacobi (kernels.cpp:102-106) runs on interior vertices of levels
         // >= ellMin; the interior diagonal is constant per level here.
         for (int l = std::max(1, prob.ellMin); l <= L; ++l)
@@ -1207,6 +1383,11 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     I.chiNodal = I.alloc<double2>(I.lv[I.L].n);
     I.compute_level_constants();
     I.build_restrict_tables();
+    if (prob.gaussian) {
+        if (prob.dim != 2) throw ConfigError("the gaussian scenario is two-dimensional");
+        if (prob.fast) throw UnsupportedConfigError("the gaussian scenario (cell-varying phi / theta) runs in precision = exact");
+        I.build_cell_constants();
+    }
     {
         const char* fz = std::getenv("TMG_FUSED");
         if (prob.fast && I.p == 3 && I.L >= 2 && !(fz && fz[0] == '0')) {

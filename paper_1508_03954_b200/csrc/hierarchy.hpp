@@ -48,7 +48,7 @@ struct Policy {  // OmegaPolicy, proj/include/treemg/cycles.hpp:17-24
     bool twoPhase = false;
 };
 
-enum class ChiKind { Zero = 0, SinProduct = 1, BallIndicator = 2, Seeded = 3 };
+enum class ChiKind { Zero = 0, SinProduct = 1, BallIndicator = 2, Seeded = 3, Gaussian = 4 };
 
 struct Problem {
     int dim = 2;
@@ -63,6 +63,7 @@ struct Problem {
     bool fast = false;    // precision = fast
     bool hostNorms = false;  // norms = host: reference-order sums of |r| on the host (exact mode)
     int zParts = 1;          // fused fine pass: z-chunks come in multiples of this (z-slabs)
+    bool gaussian = false;   // 2D gaussian scenario: per-cell phi and absorbing-layer theta (exact only)
     int sphereLevels = 0;    // static adaptive tree: levels-sphereLevels regular, refined inside |x-1/2|^2<0.04
     std::size_t maxVertices = 8u * 1024u * 1024u;
     int device = 0;

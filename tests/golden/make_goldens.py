@@ -97,6 +97,12 @@ CONFIGS = {
                            max_sweeps=40, target_drop=1e-8, **SEEDED),
     "vc_textbook_3d_cg": dict(problem="helmholtz-sin", dim=3, level=3, phi="400,200", cycle="textbook", omega_s=0.6,
                               omega_cg=0.9, max_sweeps=25, target_drop=1e-8, **SEEDED),
+    # gaussian scenario (problems.cpp:20-24, 78-90): cell-varying phi, absorbing-layer theta, reference omega 0.4
+    "gaussian_l3": dict(problem="gaussian", dim=2, level=3, max_sweeps=40, target_drop=1e-8),
+    "gaussian_l4_transition": dict(problem="gaussian", dim=2, level=4, theta_deg=25, omega="transition",
+                                   max_sweeps=30, target_drop=1e-8),
+    "gaussian_l4_bpx": dict(problem="gaussian", dim=2, level=4, cycle="td-bpx", omega="undamped", omega_s=0.3,
+                            max_sweeps=30, target_drop=1e-8),
     "rotated_3d_bpx": dict(problem="helmholtz-sin", dim=3, level=3, phi="2025", theta_deg=35, cycle="td-bpx",
                            omega="transition", max_sweeps=15, target_drop=1e-30),
 }

@@ -210,3 +210,27 @@ def test_reference_cli_runs_on_the_b200_library(tmg, tmp_path):
                           str(tmp_path / "smoke"), "--norms", "host"], capture_output=True, text=True)
     assert out.returncode == 0, out.stdout + out.stderr
     assert (tmp_path / "smoke.csv").read_text() == load_golden("poisson_smoke")["csv"]
+
+
+@pytest.mark.parametrize("cfg,sweeps", [
+    (dict(problem="gaussian", dim=2, level=3), 5),
+    (dict(problem="gaussian", dim=2, level=4, theta_deg=25, omega="transition"), 4),
+    (dict(problem="gaussian", dim=2, level=3, cycle="td-bpx", omega="undamped", omega_s=0.3), 4),
+])
+def test_gaussian_scenario_bit_identical(tmg, ref_mod, cfg, sweeps):
+    """Cell-varying phi and absorbing-layer theta (problems.cpp:20-24, 78-90;
+    kernels.cpp:7-23): every field of every level bit-identical to the live
+    reference after every sweep."""
+    ref = ref_mod.RefSession(cfg)
+    assert ref.status == 0, ref.message
+    h = tmg.Hierarchy(2, cfg["level"], chi="gaussian", theta_deg=float(cfg.get("theta_deg", 0)), precision="exact")
+    bpx = cfg.get("cycle") == "td-bpx"
+    pol = tmg.Policy(cfg.get("omega", "exponential"), float(cfg.get("omega_s", 0.4)), bpx=bpx)
+    L = cfg["level"]
+    for n in range(1, sweeps + 1):
+        a = ref.sweep(n)
+        st = h.td_bpx(pol, n) if bpx else h.td_add(pol, n)
+        assert np.allclose(a[:3], [st.max_norm, st.euclid_norm, st.h_norm], rtol=1e-12, atol=0), n
+        for lvl in range(1, L + 1):
+            for f in ("u", "sc", "chi", "rhat", "uhat") + (("sf", "si") if lvl < L else ()):
+                assert np.array_equal(ref.field(lvl, f), h.field(lvl, f)), (n, lvl, f)
