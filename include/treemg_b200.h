@@ -50,7 +50,7 @@ treemg_status treemg_result_history_row(const treemg_result* res, int i, double*
 /* wall time of the run's cycle loop in milliseconds */
 double treemg_result_device_ms(const treemg_result* res);
 /* FNV-1a of the final finest-level field ("u" or "sc") bit patterns; needs
- * config key fingerprint = 1, else 0 */
+ * config key fingerprint = 1, else 0; which = "u#<c>" reads channel c's u */
 unsigned long long treemg_result_fingerprint(const treemg_result* res, const char* which);
 
 /* ---- 2. device hierarchy ------------------------------------------------- */
@@ -73,6 +73,9 @@ typedef struct tmg_problem {
     int sphere_levels;             /* static adaptive tree: `levels` regular, then this many levels refined
                                       where the parent cell's centre lies in |x - 1/2|^2 < 0.04 (BASELINE cfg4;
                                       the cycle then runs the hanging-vertex events cycles.cpp:143-171, 305-321) */
+    int channels;                  /* unknowns per vertex, 0 or 1: one (RunConfig::channels, runner.cpp:152;
+                                      > 1 runs in exact precision on regular trees) */
+    double coupling_re, coupling_im; /* A_ij for i != j, mass-weighted (runner.cpp:153-157, kernels.cpp:52-53) */
 } tmg_problem;
 
 typedef struct tmg_policy {        /* OmegaPolicy, proj/include/treemg/cycles.hpp:17-24 */
@@ -95,6 +98,10 @@ void tmg_hierarchy_destroy(tmg_hierarchy* h);
 /* One cycle; n is the 1-based sweep counter (cycles.cpp:336-354). */
 treemg_status tmg_td_add(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
 treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
+/* Per-channel norms of the last td_add / td_bpx sweep (SweepStats::maxNorm[c] etc.,
+   cycles.hpp:27-31): writes min(channels, cap) entries of each non-null array and
+   returns the channel count (0 for a one-channel hierarchy), -1 on a null handle. */
+int tmg_channel_norms(tmg_hierarchy* h, double* max_norm, double* euclid, double* h_norm, int cap);
 
 /* Verification cycles of a regular tree held in exact storage (precision 0),
  * each followed by evaluate_residual_norms (cycles.cpp:716-786) into *out:

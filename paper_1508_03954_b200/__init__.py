@@ -48,7 +48,7 @@ EXTENSION_SYMBOLS = [
     "treemg_result_fingerprint", "tmg_test_divdc3", "tmg_nccl_unique_id", "tmg_slabs_create", "tmg_slabs_destroy",
     "tmg_slabs_cycle", "tmg_slabs_get_fine_u", "tmg_slabs_time_cycles", "tmg_slabs_owned_planes", "tmg_slab_plan",
     "tmg_slabs_e2e_step", "tmg_get_flags", "tmg_hanging_vertices", "tmg_leaf_vertices", "tmg_sphere_tree",
-    "tmg_bu_fas", "tmg_textbook_add",
+    "tmg_bu_fas", "tmg_textbook_add", "tmg_channel_norms",
 ]
 
 _lib = None
@@ -66,7 +66,8 @@ class _Problem(ctypes.Structure):
                 ("theta", ctypes.c_double), ("phi_re", ctypes.c_double), ("phi_im", ctypes.c_double),
                 ("chi_kind", ctypes.c_int), ("rhs_seed", ctypes.c_ulonglong), ("rhs_sphere", ctypes.c_int),
                 ("precision", ctypes.c_int), ("max_vertices", ctypes.c_longlong), ("device", ctypes.c_int),
-                ("sphere_levels", ctypes.c_int)]
+                ("sphere_levels", ctypes.c_int), ("channels", ctypes.c_int),
+                ("coupling_re", ctypes.c_double), ("coupling_im", ctypes.c_double)]
 
 
 class _Policy(ctypes.Structure):
@@ -118,6 +119,8 @@ def lib():
         L.tmg_hierarchy_create.restype = ip
         L.tmg_hierarchy_create.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(vp)]
         L.tmg_hierarchy_destroy.argtypes = [vp]
+        L.tmg_channel_norms.restype = ip
+        L.tmg_channel_norms.argtypes = [vp, pd, pd, pd, ip]
         for n in ("tmg_td_add", "tmg_td_bpx"):
             getattr(L, n).restype = ip
             getattr(L, n).argtypes = [vp, ctypes.POINTER(_Policy), ip, ctypes.POINTER(_Stats)]
@@ -199,6 +202,7 @@ class RunResult:
     device_ms: float = 0.0
     u_hash: int = 0
     sc_hash: int = 0
+    channel_u_hashes: List[int] = field(default_factory=list)  # fingerprint: u of every channel
 
 
 def run(cfg: Dict[str, object], out_prefix: Optional[str] = None) -> RunResult:
@@ -227,7 +231,9 @@ def run(cfg: Dict[str, object], out_prefix: Optional[str] = None) -> RunResult:
             first_norm=L.treemg_result_first_norm(res),
             final_norm={w: L.treemg_result_final_norm(res, w.encode(), -1) for w in ("max", "euclid", "h")},
             history=hist, device_ms=L.treemg_result_device_ms(res),
-            u_hash=L.treemg_result_fingerprint(res, b"u"), sc_hash=L.treemg_result_fingerprint(res, b"sc"))
+            u_hash=L.treemg_result_fingerprint(res, b"u"), sc_hash=L.treemg_result_fingerprint(res, b"sc"),
+            channel_u_hashes=[L.treemg_result_fingerprint(res, f"u#{c}".encode())
+                              for c in range(int(cfg.get("channels", 1)))])
     finally:
         L.treemg_result_free(res)
 
@@ -260,13 +266,18 @@ class Hierarchy:
 
     def __init__(self, dim: int, levels: int, phi: complex = 0.0, theta_deg: float = 0.0, chi: str = "sin",
                  rhs_seed: int = 12345, rhs_sphere: bool = False, ell_min: int = 1, precision: str = "exact",
-                 max_vertices: int = 0, device: int = 0, sphere_levels: int = 0):
+                 max_vertices: int = 0, device: int = 0, sphere_levels: int = 0, channels: int = 1,
+                 coupling: complex = 0.0):
         """levels: depth of the regular base tree; sphere_levels > 0 adds that many
-        levels refined inside |x - 1/2|^2 < 0.04 (static adaptive tree, cfg4)."""
+        levels refined inside |x - 1/2|^2 < 0.04 (static adaptive tree, cfg4).
+        channels > 1: that many unknowns per vertex with the same fields, coupled
+        by A_ij = coupling (i != j) through the mass matrix (runner.cpp:152-157);
+        exact precision, regular trees.  field(level, "u#1") reads channel 1."""
         self.L = lib()
         prob = _Problem(dim, levels, ell_min, np.deg2rad(theta_deg) if theta_deg else 0.0,
                         complex(phi).real, complex(phi).imag, CHI_KINDS[chi], rhs_seed, int(rhs_sphere),
-                        1 if precision == "fast" else 0, max_vertices, device, sphere_levels)
+                        1 if precision == "fast" else 0, max_vertices, device, sphere_levels, channels,
+                        complex(coupling).real, complex(coupling).imag)
         if theta_deg:
             prob.theta = theta_deg * np.pi / 180.0  # ProblemSpec::thetaGlobal = deg * M_PI / 180.0
         h = ctypes.c_void_p()
@@ -296,6 +307,14 @@ class Hierarchy:
 
     def td_bpx(self, pol: Policy, n: int) -> SweepStats:
         return self._sweep(self.L.tmg_td_bpx, pol, n)
+
+    def channel_norms(self):
+        """Per-channel (max, euclid, h) norms of the last td_add / td_bpx sweep
+        (SweepStats per channel, cycles.hpp:27-31); empty for one channel."""
+        cap = 16
+        mx, eu, hn = np.zeros(cap), np.zeros(cap), np.zeros(cap)
+        n = self.L.tmg_channel_norms(self.h, _pd(mx), _pd(eu), _pd(hn), cap)
+        return [(mx[c], eu[c], hn[c]) for c in range(max(n, 0))]
 
     def bu_fas(self, pol: Policy, n: int) -> SweepStats:
         """bu_fas + evaluate_residual_norms (cycles.cpp:374-603, 716-786); exact storage."""

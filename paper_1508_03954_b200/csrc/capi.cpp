@@ -25,6 +25,7 @@ struct treemg_result {
 
 struct tmg_hierarchy {
     std::unique_ptr<Hierarchy> h;
+    SweepStats last;  // per-channel norms of the last sweep (tmg_channel_norms)
 };
 
 struct tmg_slabs {
@@ -140,9 +141,11 @@ double treemg_result_final_norm(const treemg_result* res, const char* which, int
     const SweepRecord& rec = res->res.history.back();
     const bool agg = channel < 0;
     if (!agg && channel >= res->channels) return -1.0;
-    if (std::strcmp(which, "max") == 0) return rec.maxNorm;
-    if (std::strcmp(which, "euclid") == 0) return rec.euclidNorm;
-    if (std::strcmp(which, "h") == 0) return rec.hNorm;
+    const bool one = agg || rec.perChannelMax.empty();  // a single channel is its own aggregate
+    const auto c = static_cast<std::size_t>(channel);
+    if (std::strcmp(which, "max") == 0) return one ? rec.maxNorm : rec.perChannelMax[c];
+    if (std::strcmp(which, "euclid") == 0) return one ? rec.euclidNorm : rec.perChannelEuclid[c];
+    if (std::strcmp(which, "h") == 0) return one ? rec.hNorm : rec.perChannelH[c];
     return -1.0;
 }
 
@@ -171,6 +174,12 @@ unsigned long long treemg_result_fingerprint(const treemg_result* res, const cha
     if (!res || !which) return 0;
     if (std::strcmp(which, "u") == 0) return res->res.uHash;
     if (std::strcmp(which, "sc") == 0) return res->res.scHash;
+    if (std::strncmp(which, "u#", 2) == 0) {  // "u#<c>": channel c's u
+        const int c = std::atoi(which + 2);
+        if (c == 0) return res->res.uHash;
+        if (c >= 1 && static_cast<std::size_t>(c) <= res->res.channelUHash.size())
+            return res->res.channelUHash[static_cast<std::size_t>(c) - 1];
+    }
     return 0;
 }
 
@@ -196,6 +205,8 @@ Problem problem_from(const tmg_problem* prob) {
     p.device = prob->device;
     p.sphereLevels = prob->sphere_levels;
     p.levels += p.sphereLevels;
+    p.channels = prob->channels > 0 ? prob->channels : 1;
+    p.coupling = Cplx(prob->coupling_re, prob->coupling_im);
     if (p.ellMin < 1) throw ConfigError("ellMin must be >= 1");
     return p;
 }
@@ -277,22 +288,7 @@ treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out)
     *out = nullptr;
     auto* h = new tmg_hierarchy();
     const treemg_status st = guarded([&] {
-        Problem p;
-        p.dim = prob->dim;
-        p.levels = prob->levels;
-        p.ellMin = prob->ell_min;
-        p.theta = prob->theta;
-        p.phi = Cplx(prob->phi_re, prob->phi_im);
-        p.chi = static_cast<ChiKind>(prob->chi_kind);
-        p.gaussian = prob->chi_kind == 4;
-        p.rhsSeed = prob->rhs_seed;
-        p.rhsSphere = prob->rhs_sphere != 0;
-        p.fast = prob->precision == 1;
-        if (prob->max_vertices > 0) p.maxVertices = static_cast<std::size_t>(prob->max_vertices);
-        p.device = prob->device;
-        p.sphereLevels = prob->sphere_levels;
-        p.levels += p.sphereLevels;
-        if (p.ellMin < 1) throw ConfigError("ellMin must be >= 1");
+        const Problem p = problem_from(prob);
         h->h = std::make_unique<Hierarchy>(p);
     });
     if (st != TREEMG_OK) {
@@ -311,7 +307,7 @@ treemg_status tmg_td_add(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_swe
         Policy p = policy_from(pol);
         if (p.bpx) throw ConfigError("td_add: policy has bpx set, use td_bpx");  // cycles.cpp:338
         if (n < 1) throw ConfigError("sweep counter starts at 1");
-        fill_stats(h->h->cycle(p, n), out);
+        fill_stats(h->last = h->h->cycle(p, n), out);
     });
 }
 
@@ -322,7 +318,7 @@ treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_swe
         if (n < 1) throw ConfigError("sweep counter starts at 1");
         p.bpx = true;  // cycles.cpp:349-351
         p.hbMask = false;
-        fill_stats(h->h->cycle(p, n), out);
+        fill_stats(h->last = h->h->cycle(p, n), out);
     });
 }
 
@@ -428,6 +424,18 @@ treemg_status tmg_time_cycles(tmg_hierarchy* h, const tmg_policy* pol, int n0, i
 treemg_status tmg_e2e_step(tmg_hierarchy* h, const tmg_policy* pol, int n, const double* chi, double* out3) {
     if (!h || !pol || !chi || !out3) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] { h->h->e2e_step(policy_from(pol), n, chi, out3); });
+}
+
+int tmg_channel_norms(tmg_hierarchy* h, double* maxNorm, double* euclid, double* hNorm, int cap) {
+    if (!h) return -1;
+    const SweepStats& st = h->last;
+    const int n = static_cast<int>(st.chMax.size());
+    for (int c = 0; c < n && c < cap; ++c) {
+        if (maxNorm) maxNorm[c] = st.chMax[c];
+        if (euclid) euclid[c] = st.chEuclid[c];
+        if (hNorm) hNorm[c] = st.chH[c];
+    }
+    return n;
 }
 
 }  // extern "C"

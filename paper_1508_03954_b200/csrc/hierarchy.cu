@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <array>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -155,12 +156,72 @@ __device__ __forceinline__ double2 element_residual(const double2* __restrict__ 
     }
 }
 
+// Multichannel element residual (kernels.cpp:39-59): per cell, the own
+// channel's products over b, then for every other channel j (ascending) the
+// coupling products (A_ij massScale mas(a,b)) x_j,b, all in the cell's corner
+// order; the cells are combined in traversal order as above.
+template <int P>
+__device__ __forceinline__ double2 element_residual_mc(const double2* const* __restrict__ xs, int nch, int own,
+                                                       unsigned f, unsigned n1, const double2 (&A)[8],
+                                                       const double2 (&Mc)[8], int pid) {
+    constexpr int NC = 1 << P;
+    constexpr int NB = P == 1 ? 3 : P == 2 ? 9 : 27;
+    double2 S[NC];
+    for (int pass = -1; pass < nch; ++pass) {  // pass -1: own channel; then j = 0..nch-1, j != own
+        if (pass == own) continue;
+        const double2* __restrict__ x = xs[pass < 0 ? own : pass];
+#pragma unroll
+        for (int j = 0; j < NB; ++j) {
+            int del[P];
+            int off = 0, s = 0, stride = 1;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                del[d] = (j / (d == 0 ? 1 : d == 1 ? 3 : 9)) % 3 - 1;
+                off += del[d] * stride;
+                stride *= static_cast<int>(n1);
+                s |= (del[d] != 0 ? 1 : 0) << d;
+            }
+            const double2 prod = xmul(pass < 0 ? A[s] : Mc[s], __ldg(x + (static_cast<int>(f) + off)));
+#pragma unroll
+            for (int e = 0; e < NC; ++e) {
+                bool use = true;
+                int b = 0;
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    const int bd = del[d] - ((e >> d) & 1) + 1;
+                    use &= (bd == 0 || bd == 1);
+                    b |= (bd & 1) << d;
+                }
+                if (use) S[e] = (pass < 0 && b == 0) ? prod : xadd(S[e], prod);
+            }
+        }
+    }
+    if (P == 1) return ordered_sum<P, 0>(S);
+    if (P == 2) return pid == 0 ? ordered_sum<P, 0>(S) : ordered_sum<P, (P >= 2 ? 1 : 0)>(S);
+    switch (pid) {
+        case 0: return ordered_sum<P, 0>(S);
+        case 1: return ordered_sum<P, (P >= 3 ? 1 : 0)>(S);
+        case 2: return ordered_sum<P, (P >= 3 ? 2 : 0)>(S);
+        case 3: return ordered_sum<P, (P >= 3 ? 3 : 0)>(S);
+        case 4: return ordered_sum<P, (P >= 3 ? 4 : 0)>(S);
+        default: return ordered_sum<P, (P >= 3 ? 5 : 0)>(S);
+    }
+}
+
 // ---- K2/K3: residual + Jacobi staging + injections (enterCell/touchLast) --
 #ifndef TMG_EXACT_RES_MINB
 #define TMG_EXACT_RES_MINB 3
 #endif
-template <int P>
-__global__ void __launch_bounds__(256, TMG_EXACT_RES_MINB) k_residual_exact(ResArgs a) {
+// Coupled channels (ResArgs::mc): the other channels' u / u-hat of this level.
+struct McArgs {
+    const double2* const* u;
+    const double2* const* uhat;
+    int nch, own;
+    double2 Mc[8];  // A_ij massScale mas(pattern)
+};
+
+template <int P, bool MC>
+__global__ void __launch_bounds__(256, TMG_EXACT_RES_MINB) k_residual_exact(ResArgs a, McArgs mc) {
     const Lvl& c = a.lv;
     double nmax = 0.0, nsum = 0.0;
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
@@ -171,8 +232,13 @@ __global__ void __launch_bounds__(256, TMG_EXACT_RES_MINB) k_residual_exact(ResA
         double2 r = cz(), rh = cz();
         if (!bnd) {
             const int pid = perm_id<P>(idx);
-            r = element_residual<P>(c.u, f, c.n1, a.k.A, pid);
-            rh = element_residual<P>(c.uhat, f, c.n1, a.k.A, pid);
+            if (MC) {
+                r = element_residual_mc<P>(mc.u, mc.nch, mc.own, f, c.n1, a.k.A, mc.Mc, pid);
+                rh = element_residual_mc<P>(mc.uhat, mc.nch, mc.own, f, c.n1, a.k.A, mc.Mc, pid);
+            } else {
+                r = element_residual<P>(c.u, f, c.n1, a.k.A, pid);
+                rh = element_residual<P>(c.uhat, f, c.n1, a.k.A, pid);
+            }
             const double2 chi = c.chi[f];
             r = xadd(chi, r);    // finish_vertex, kernels.cpp:96-97
             rh = xadd(chi, rh);
@@ -452,7 +518,7 @@ __global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, Level
 // optionally masked to the ball |x - 1/2|^2 < 0.04.
 template <int P>
 __global__ void k_seeded_chi(double2* out, unsigned n, unsigned n1, unsigned long long seed, int scale, long long mkey,
-                             int sphere) {
+                             int sphere, int channel) {
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
         int idx[P];
         unflat<P>(f, n1, idx);
@@ -469,13 +535,13 @@ __global__ void k_seeded_chi(double2* out, unsigned n, unsigned n1, unsigned lon
             out[f] = cz();
             continue;
         }
-        const unsigned long long s = seed ^ key;
+        const unsigned long long s = seed ^ (static_cast<unsigned long long>(channel) << 48) ^ key;
         out[f] = make_double2(unit_rand(s), unit_rand(s ^ 0x5bf03635ull));
     }
 }
 
 template <int P>
-__global__ void k_random_fine(Lvl c, unsigned long long seed) {  // cycles.cpp:812-840
+__global__ void k_random_fine(Lvl c, unsigned long long seed, int channel = 0) {  // cycles.cpp:812-840
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
         int idx[P];
         unflat<P>(f, c.n1, idx);
@@ -486,7 +552,8 @@ __global__ void k_random_fine(Lvl c, unsigned long long seed) {  // cycles.cpp:8
         unsigned long long key = 0;
 #pragma unroll
         for (int d = 0; d < P; ++d) key |= static_cast<unsigned long long>(static_cast<unsigned short>(idx[d])) << (16 * d);
-        const unsigned long long base = seed ^ (static_cast<unsigned long long>(c.level) << 56) ^ key;
+        const unsigned long long base = seed ^ (static_cast<unsigned long long>(c.level) << 56) ^
+                                        (static_cast<unsigned long long>(channel) << 48) ^ key;
         c.u[f] = make_double2(unit_rand(base), unit_rand(base ^ 0x5bf03635ull));
     }
 }
@@ -695,6 +762,9 @@ struct Hierarchy::Impl {
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
     std::vector<double2*> vcScratch;  // verification cycles: per-level residual
     std::vector<double2*> cellA, cellMs;  // gaussian scenario: per-cell operator / massScale
+    std::vector<std::vector<dev::Lvl>> chanLv;  // channels 1.. (exact storage)
+    std::vector<const double2**> chanU, chanUh;  // per level: device arrays of every channel's u / u-hat
+    std::vector<std::array<double2, 8>> couplingM;  // per level: A_ij massScale mas(pattern)
     bool fused2on = false;         // 2D fused fine pass (fast precision)
     fused2::Geometry geo2{};
     double2* partial2 = nullptr;
@@ -909,13 +979,13 @@ struct Hierarchy::Impl {
     }
 
     template <int P>
-    void build_rhs_seeded() {
+    void build_rhs_seeded(int ch = 0) {  // channel ch keyed as oracle/refdriver.cpp seeded_f
         const dev::Lvl& F = lv[L];
         const int key = prob.rhsLattice >= 0 ? prob.rhsLattice : L;
         const int scale = pow3i(key - L);
         dev::k_seeded_chi<P><<<blocks_for(F.n), 256, 0, stream>>>(chiNodal, F.n, F.n1, prob.rhsSeed, scale,
                                                                   static_cast<long long>(pow3i(key)),
-                                                                  prob.rhsSphere ? 1 : 0);
+                                                                  prob.rhsSphere ? 1 : 0, ch);
         TMG_CUDA(cudaGetLastError());
     }
 
@@ -951,15 +1021,15 @@ struct Hierarchy::Impl {
     }
 
     template <int P>
-    void load_vector(unsigned fa, unsigned fb) {
-        const dev::Lvl& F = lv[L];
+    void load_vector(unsigned fa, unsigned fb, int ch) {
+        const dev::Lvl F = level(ch, L);
         dev::k_load_vector<P><<<blocks_for(fb - fa), 256, 0, stream>>>(F, chiNodal, kc[L], fa, fb,
                                                                      prob.gaussian ? cellMs[L] : nullptr);
         TMG_CUDA(cudaGetLastError());
     }
 
     // load vector on planes [za, zb) of the last axis (za < 0: everywhere)
-    void load_vector_dispatch(int za = -1, int zb = -1) {
+    void load_vector_dispatch(int za = -1, int zb = -1, int ch = 0) {
         const dev::Lvl& F = lv[L];
         if (prob.fast) {  // separable assembled mass stencil (rounding differs from the cell-by-cell sum)
             fast::load_vector(p, F, chiNodal, kc[L].massScale, blocks_for(F.n), stream, za, zb);
@@ -974,46 +1044,66 @@ struct Hierarchy::Impl {
             fb = static_cast<unsigned>(std::min<long long>(zb, F.n1)) * plane;
         }
         if (fb <= fa) return;
-        if (p == 1) load_vector<1>(fa, fb);
-        else if (p == 2) load_vector<2>(fa, fb);
-        else load_vector<3>(fa, fb);
+        if (p == 1) load_vector<1>(fa, fb, ch);
+        else if (p == 2) load_vector<2>(fa, fb, ch);
+        else load_vector<3>(fa, fb, ch);
     }
 
     template <int P>
     void cycle_exact(const Policy& pol, int n, bool timed) {
-        // top-down (levels 1..L; level 0 holds only zero boundary corners)
+        const int nch = prob.channels;
+        const bool coupled = nch > 1 && prob.coupling != Cplx(0.0);
+        // top-down (levels 1..L; level 0 holds only zero boundary corners); channels are independent here
         for (int l = 1; l <= L; ++l) {
             if (timed && l == L) TMG_CUDA(cudaEventRecord(evf0, stream));
-            dev::k_topdown<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], lv[l - 1], pol.bpx ? 1 : 0);
+            for (int ch = 0; ch < nch; ++ch)
+                dev::k_topdown<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(level(ch, l), level(ch, l - 1),
+                                                                          pol.bpx ? 1 : 0);
         }
         for (int l = L; l >= 1; --l) {
-            dev::ResArgs a{};
-            a.lv = lv[l];
-            a.par = lv[l - 1];
-            a.k = kc[l];
-            a.k.wRaw = make_double2(0.0, 0.0);
-            const Cplx w = omega_unmasked(pol, L - l, n);
-            a.k.wRaw = make_double2(w.real(), w.imag());
-            a.ellMin = prob.ellMin;
-            a.isFine = l == L ? 1 : 0;
-            a.bpx = pol.bpx ? 1 : 0;
-            a.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
-            a.partials = partials;
-            const int nb = l == L ? normBlocks : blocks_for(lv[l].n);
-            if (prob.gaussian)
-                dev::k_residual_cells<P><<<nb, 256, 0, stream>>>(a, cellA[l]);
-            else
-                dev::k_residual_exact<P><<<nb, 256, 0, stream>>>(a);
+            for (int ch = 0; ch < nch; ++ch) {
+                dev::ResArgs a{};
+                a.lv = level(ch, l);
+                a.par = level(ch, l - 1);
+                a.k = kc[l];
+                const Cplx w = omega_unmasked(pol, L - l, n);
+                a.k.wRaw = make_double2(w.real(), w.imag());
+                a.ellMin = prob.ellMin;
+                a.isFine = l == L ? 1 : 0;
+                a.bpx = pol.bpx ? 1 : 0;
+                a.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+                a.partials = partials + 2 * static_cast<size_t>(normBlocks) * ch;
+                const int nb = l == L ? normBlocks : blocks_for(lv[l].n);
+                if (prob.gaussian) {
+                    dev::k_residual_cells<P><<<nb, 256, 0, stream>>>(a, cellA[l]);
+                } else if (coupled) {
+                    dev::McArgs mc{};
+                    mc.u = chanU[l];
+                    mc.uhat = chanUh[l];
+                    mc.nch = nch;
+                    mc.own = ch;
+                    for (int sp = 0; sp < (1 << p); ++sp) mc.Mc[sp] = couplingM[l][sp];
+                    dev::k_residual_exact<P, true><<<nb, 256, 0, stream>>>(a, mc);
+                } else {
+                    dev::k_residual_exact<P, false><<<nb, 256, 0, stream>>>(a, dev::McArgs{});
+                }
+            }
             if (timed && l == L) TMG_CUDA(cudaEventRecord(evf1, stream));
             if (l >= 2) {
                 const int zero = l <= prob.ellMin ? 1 : 0;
-                dev::k_restrict_exact<P><<<blocks_for(lv[l - 1].n), 256, 0, stream>>>(
-                    lv[l], lv[l - 1], restrictTable, restrictWeights, zero);
+                for (int ch = 0; ch < nch; ++ch)
+                    dev::k_restrict_exact<P><<<blocks_for(lv[l - 1].n), 256, 0, stream>>>(
+                        level(ch, l), level(ch, l - 1), restrictTable, restrictWeights, zero);
             }
         }
-        dev::k_norm_final<<<1, 1024, 0, stream>>>(partials, normBlocks, dNorm);
+        for (int ch = 0; ch < nch; ++ch)
+            dev::k_norm_final<<<1, 1024, 0, stream>>>(partials + 2 * static_cast<size_t>(normBlocks) * ch, normBlocks,
+                                                      dNorm + 2 * ch);
         TMG_CUDA(cudaGetLastError());
     }
+
+    // channel ch's arrays of level l (channel 0: lv)
+    dev::Lvl level(int ch, int l) const { return ch == 0 ? lv[l] : chanLv[ch - 1][l]; }
 
     template <int P>
     void cycle_fast(const Policy& pol, int n, bool timed) {
@@ -1294,13 +1384,30 @@ struct Hierarchy::Impl {
         if (amr) return amr->cycle(pol, n);
         check_diag();
         run_cycle(pol, n, timed);
-        TMG_CUDA(cudaMemcpyAsync(hNorm, dNorm, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+        const int nch = prob.channels;
+        TMG_CUDA(cudaMemcpyAsync(hNorm, dNorm, 2 * sizeof(double) * nch, cudaMemcpyDeviceToHost, stream));
         TMG_CUDA(cudaStreamSynchronize(stream));
         SweepStats st;
         const double hp = std::pow(std::pow(3.0, -L), p);
         st.maxNorm = std::sqrt(hNorm[0]);
         st.euclidNorm = std::sqrt(hNorm[1]);
         st.hNorm = std::sqrt(hp * hNorm[1]);
+        if (nch > 1) {  // per channel, aggregated as runner.cpp:68-77 (max; l2 over channels)
+            double mx = 0.0, se = 0.0, sh = 0.0;
+            for (int ch = 0; ch < nch; ++ch) {
+                const double cm = std::sqrt(hNorm[2 * ch]), ce = std::sqrt(hNorm[2 * ch + 1]),
+                             chh = std::sqrt(hp * hNorm[2 * ch + 1]);
+                st.chMax.push_back(cm);
+                st.chEuclid.push_back(ce);
+                st.chH.push_back(chh);
+                mx = std::max(mx, cm);
+                se += ce * ce;
+                sh += chh * chh;
+            }
+            st.maxNorm = mx;
+            st.euclidNorm = std::sqrt(se);
+            st.hNorm = std::sqrt(sh);
+        }
         long long inner = 1;
         for (int d = 0; d < p; ++d) inner *= pow3i(L) - 1;
         st.updatedFineVertices = inner;
@@ -1318,6 +1425,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     if (prob.levels < 1) throw ConfigError("build_regular needs levels >= 1");
     if (prob.levels > 9) throw ConfigError("tree depth exceeds supported maximum");
     if (prob.sphereLevels < 0 || prob.sphereLevels >= prob.levels) throw ConfigError("sphere_levels out of range");
+    if (prob.channels > 1 && (prob.sphereLevels > 0 || prob.hostNorms))
+        throw UnsupportedConfigError("B200 path: several channels run on regular trees with device norms");
     // build_regular's capacity estimate (spacetree.cpp:53-63)
     std::size_t estimate = 0;
     for (int l = 0; l <= prob.levels - prob.sphereLevels; ++l) {
@@ -1362,7 +1471,16 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
             I.normBlocks = std::max(I.normBlocks, fused2::blocks(I.geo2));
         }
     }
-    I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks));
+    if (prob.channels < 1 || prob.channels > 16) throw ConfigError("channels must lie in [1, 16]");
+    if (prob.channels > 1) {
+        if (prob.fast) throw UnsupportedConfigError("B200 path: several channels run in precision = exact");
+        for (int ch = 1; ch < prob.channels; ++ch) {
+            std::vector<dev::Lvl> v(I.L + 1);
+            for (int l = 0; l <= I.L; ++l) v[l] = I.make_level(l, l == I.L);
+            I.chanLv.push_back(v);
+        }
+    }
+    I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks) * prob.channels);
     if (I.fused2on) {
         I.uAlt = I.alloc<double2>(I.lv[I.L].n);
         I.partial2 = I.alloc<double2>(fused2::partial_count(I.geo2));
@@ -1378,8 +1496,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
             if (!(cl && cl[0] == '0')) I.clusterSize = fast::chain_cluster_size();
         }
     }
-    I.dNorm = I.alloc<double>(2);
-    TMG_CUDA(cudaMallocHost(&I.hNorm, 2 * sizeof(double)));
+    I.dNorm = I.alloc<double>(2 * static_cast<size_t>(prob.channels));
+    TMG_CUDA(cudaMallocHost(&I.hNorm, 2 * sizeof(double) * prob.channels));
     I.chiNodal = I.alloc<double2>(I.lv[I.L].n);
     I.compute_level_constants();
     I.build_restrict_tables();
@@ -1405,13 +1523,48 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
         }
     }
     if (prob.chi == ChiKind::Seeded) {
-        if (I.p == 1) I.build_rhs_seeded<1>();
-        else if (I.p == 2) I.build_rhs_seeded<2>();
-        else I.build_rhs_seeded<3>();
+        // the seeded rhs keys every channel apart (oracle/refdriver.cpp seeded_f: seed ^ c << 48);
+        // channel 0 last so chiNodal keeps its values
+        for (int ch = prob.channels - 1; ch >= 0; --ch) {
+            if (I.p == 1) I.build_rhs_seeded<1>(ch);
+            else if (I.p == 2) I.build_rhs_seeded<2>(ch);
+            else I.build_rhs_seeded<3>(ch);
+            I.load_vector_dispatch(-1, -1, ch);
+        }
     } else {
         I.build_rhs_analytic();
+        I.load_vector_dispatch();
+        // every channel carries the same fields (runner.cpp:152): same load vector
+        for (int ch = 1; ch < prob.channels; ++ch)
+            TMG_CUDA(cudaMemcpyAsync(I.chanLv[ch - 1][I.L].chi, I.lv[I.L].chi,
+                                     static_cast<size_t>(I.lv[I.L].n) * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                     I.stream));
     }
-    I.load_vector_dispatch();
+    if (prob.channels > 1) {
+        I.chanU.assign(I.L + 1, nullptr);
+        I.chanUh.assign(I.L + 1, nullptr);
+        I.couplingM.assign(I.L + 1, std::array<double2, 8>{});
+        for (int l = 0; l <= I.L; ++l) {
+            std::vector<const double2*> pu(prob.channels), ph(prob.channels);
+            for (int ch = 0; ch < prob.channels; ++ch) {
+                pu[ch] = I.level(ch, l).u;
+                ph[ch] = I.level(ch, l).uhat;
+            }
+            auto** du = I.alloc<const double2*>(prob.channels);
+            auto** dh = I.alloc<const double2*>(prob.channels);
+            TMG_CUDA(cudaMemcpyAsync(du, pu.data(), pu.size() * sizeof(void*), cudaMemcpyHostToDevice, I.stream));
+            TMG_CUDA(cudaMemcpyAsync(dh, ph.data(), ph.size() * sizeof(void*), cudaMemcpyHostToDevice, I.stream));
+            I.chanU[l] = du;
+            I.chanUh[l] = dh;
+            const Cplx aij = prob.coupling * I.massScale[l];  // kernels.cpp:52-53
+            for (int sp = 0; sp < (1 << I.p); ++sp) {
+                double lap, mas;
+                reference_pattern(I.p, sp, lap, mas);
+                const Cplx mcpl = aij * mas;
+                I.couplingM[l][sp] = make_double2(mcpl.real(), mcpl.imag());
+            }
+        }
+    }
     TMG_CUDA(cudaStreamSynchronize(I.stream));
 }
 
@@ -1521,14 +1674,22 @@ double2* field_ptr(const dev::Lvl& v, const std::string& f) {
 }
 }  // namespace
 
-void Hierarchy::get_field(int level, const std::string& field, double* host) const {
+void Hierarchy::get_field(int level, const std::string& name, double* host) const {
     Impl& I = *impl_;
     if (level < 0 || level > I.L) throw ConfigError("get_field: level out of range");
     if (I.amr) {
-        I.amr->get_field(level, field, host);
+        I.amr->get_field(level, name, host);
         return;
     }
-    const dev::Lvl& v = I.lv[level];
+    // "<field>#<channel>": another channel's arrays (channels > 1)
+    int ch = 0;
+    std::string field = name;
+    if (const auto hash = name.find('#'); hash != std::string::npos) {
+        ch = std::stoi(name.substr(hash + 1));
+        field = name.substr(0, hash);
+        if (ch < 0 || ch >= I.prob.channels) throw ConfigError("get_field: channel out of range");
+    }
+    const dev::Lvl v = I.level(ch, level);
     if (field == "diag") {
         // host-side: per vertex the sum of A_aa over its existing cells
         const Cplx a = I.diagInterior[level] / static_cast<double>(1 << I.p);
@@ -1602,20 +1763,21 @@ void Hierarchy::set_field(int level, const std::string& field, const double* hos
 
 namespace {
 template <int P>
-void inject_up(Hierarchy::Impl& I) {  // callers reset sc afterwards: plain u injection
+void inject_up(Hierarchy::Impl& I, int ch = 0) {  // callers reset sc afterwards: plain u injection
     for (int l = I.L - 1; l >= 1; --l)
-        dev::k_inject_u<P><<<I.blocks_for(I.lv[l].n), 256, 0, I.stream>>>(I.lv[l], I.lv[l + 1], 0);
+        dev::k_inject_u<P><<<I.blocks_for(I.lv[l].n), 256, 0, I.stream>>>(I.level(ch, l), I.level(ch, l + 1), 0);
 }
 }  // namespace
 
 struct HierarchyAccess {
-    static void reset_pipeline(Hierarchy::Impl& I) {
-        for (int l = 0; l <= I.L; ++l) {
-            const dev::Lvl& v = I.lv[l];
-            const size_t bytes = static_cast<size_t>(v.n) * sizeof(double2);
-            for (double2* ptr : {v.sc, v.sf, v.si, v.sinext, v.uhat})
-                if (ptr) TMG_CUDA(cudaMemsetAsync(ptr, 0, bytes, I.stream));
-        }
+    static void reset_pipeline(Hierarchy::Impl& I) {  // reset_pipeline_state, cycles.cpp:843-853
+        for (int ch = 0; ch < I.prob.channels; ++ch)
+            for (int l = 0; l <= I.L; ++l) {
+                const dev::Lvl v = I.level(ch, l);
+                const size_t bytes = static_cast<size_t>(v.n) * sizeof(double2);
+                for (double2* ptr : {v.sc, v.sf, v.si, v.sinext, v.uhat})
+                    if (ptr) TMG_CUDA(cudaMemsetAsync(ptr, 0, bytes, I.stream));
+            }
     }
 };
 
@@ -1644,13 +1806,15 @@ void Hierarchy::set_random_initial_guess(std::uint64_t seed) {
         I.amr->set_random_initial_guess(seed);
         return;
     }
-    const dev::Lvl& F = I.lv[I.L];
-    if (I.p == 1) dev::k_random_fine<1><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
-    else if (I.p == 2) dev::k_random_fine<2><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
-    else dev::k_random_fine<3><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed);
-    if (I.p == 1) inject_up<1>(I);
-    else if (I.p == 2) inject_up<2>(I);
-    else inject_up<3>(I);
+    for (int ch = 0; ch < I.prob.channels; ++ch) {
+        const dev::Lvl F = I.level(ch, I.L);
+        if (I.p == 1) dev::k_random_fine<1><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed, ch);
+        else if (I.p == 2) dev::k_random_fine<2><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed, ch);
+        else dev::k_random_fine<3><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed, ch);
+        if (I.p == 1) inject_up<1>(I, ch);
+        else if (I.p == 2) inject_up<2>(I, ch);
+        else inject_up<3>(I, ch);
+    }
     HierarchyAccess::reset_pipeline(I);
     TMG_CUDA(cudaStreamSynchronize(I.stream));
 }
@@ -1662,6 +1826,10 @@ void Hierarchy::set_fine_rhs(const double* hostNodalChi) {
     TMG_CUDA(cudaMemcpyAsync(I.chiNodal, hostNodalChi, static_cast<size_t>(F.n) * sizeof(double2),
                              cudaMemcpyHostToDevice, I.stream));
     I.load_vector_dispatch();
+    for (int ch = 1; ch < I.prob.channels; ++ch)  // same fields on every channel (runner.cpp:152)
+        TMG_CUDA(cudaMemcpyAsync(I.chanLv[ch - 1][I.L].chi, I.lv[I.L].chi,
+                                 static_cast<size_t>(I.lv[I.L].n) * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                 I.stream));
     TMG_CUDA(cudaStreamSynchronize(I.stream));
 }
 

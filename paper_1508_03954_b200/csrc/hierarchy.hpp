@@ -64,14 +64,17 @@ struct Problem {
     bool hostNorms = false;  // norms = host: reference-order sums of |r| on the host (exact mode)
     int zParts = 1;          // fused fine pass: z-chunks come in multiples of this (z-slabs)
     bool gaussian = false;   // 2D gaussian scenario: per-cell phi and absorbing-layer theta (exact only)
+    int channels = 1;        // unknowns per vertex (kernels.cpp:33-66; exact precision for > 1)
+    Cplx coupling = Cplx(0.0);  // A_ij for i != j (runner.cpp:152-157)
     int sphereLevels = 0;    // static adaptive tree: levels-sphereLevels regular, refined inside |x-1/2|^2<0.04
     std::size_t maxVertices = 8u * 1024u * 1024u;
     int device = 0;
 };
 
-struct SweepStats {  // SweepStats, cycles.hpp:37-45 (one channel)
-    double maxNorm = 0.0, euclidNorm = 0.0, hNorm = 0.0;
+struct SweepStats {  // SweepStats, cycles.hpp:37-45
+    double maxNorm = 0.0, euclidNorm = 0.0, hNorm = 0.0;  // aggregated over channels (runner.cpp:68-77)
     long long updatedFineVertices = 0;
+    std::vector<double> chMax, chEuclid, chH;  // per channel (channels > 1)
 };
 
 // omega_unmasked, proj/src/cycles.cpp:11-31 (host, same libstdc++ arithmetic)

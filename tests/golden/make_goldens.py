@@ -105,6 +105,17 @@ CONFIGS = {
                             max_sweeps=30, target_drop=1e-8),
     "rotated_3d_bpx": dict(problem="helmholtz-sin", dim=3, level=3, phi="2025", theta_deg=35, cycle="td-bpx",
                            omega="transition", max_sweeps=15, target_drop=1e-30),
+    # several channels: test_runner.cpp:120-155 cases, and coupled / random-start variants
+    "mc2_identical": dict(problem="helmholtz-sin", phi="-1000", dim=2, level=2, channels=2, max_sweeps=10,
+                          target_drop=1e-30),
+    "mc2_coupled_2d": dict(problem="helmholtz-sin", dim=2, level=4, phi="100,50", channels=2, coupling="30,10",
+                           cycle="td-add", omega="undamped", omega_s=0.6, max_sweeps=40, target_drop=1e-8,
+                           **SEEDED),
+    "mc3_coupled_3d_bpx": dict(problem="helmholtz-sin", dim=3, level=3, phi="400,200", channels=3,
+                               coupling="-20,5", cycle="td-bpx", omega="undamped", omega_s=0.5, max_sweeps=25,
+                               target_drop=1e-8, **SEEDED),
+    "mc2_random_2d": dict(problem="poisson-sin", dim=2, level=3, channels=2, coupling="4,0", initial="random",
+                          seed=7, omega="exponential", omega_s=0.8, max_sweeps=30, target_drop=1e-8, norm="h"),
 }
 
 
@@ -124,6 +135,7 @@ def generate(name: str) -> dict:
         csv=s.csv(), log=s.log(),
         u_hash=f"{s.field_hash(L, 'u'):016x}", sc_hash=f"{s.field_hash(L, 'sc'):016x}",
         coarse_u_hash=f"{s.field_hash(L - 1, 'u'):016x}" if L >= 1 else "",
+        channel_u_hashes=[f"{s.field_hash(L, 'u', c):016x}" for c in range(int(cfg.get("channels", 1)))],
         reference_seconds_per_sweep=float(secs.mean()) if len(secs) else 0.0,
         reference_build_seconds=build_s, host=platform.node(), cpu=platform.processor() or platform.machine(),
         generator="tests/golden/make_goldens.py via oracle/_ref (unmodified reference sources)",

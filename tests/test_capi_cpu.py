@@ -54,7 +54,8 @@ def test_version_and_error_codes(tmg):
     ({"level": "2", "problem": "nope"}, 1),
     ({"level": "10"}, 1),                                 # kMaxLevel
     ({"level": "2", "cycle": "bu-fas", "sphere_levels": "1"}, 1),  # runner.cpp:232: adaptive needs td-*
-    ({"level": "2", "channels": "2"}, 1),
+    ({"level": "2", "channels": "2", "precision": "fast"}, 1),
+    ({"level": "2", "channels": "2", "sphere_levels": "1"}, 1),
     ({"dim": "4", "level": "2"}, 1),
 ])
 def test_run_config_errors_without_gpu(tmg, kv, status):
