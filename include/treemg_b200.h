@@ -76,6 +76,10 @@ typedef struct tmg_problem {
     int channels;                  /* unknowns per vertex, 0 or 1: one (RunConfig::channels, runner.cpp:152;
                                       > 1 runs in exact precision on regular trees) */
     double coupling_re, coupling_im; /* A_ij for i != j, mass-weighted (runner.cpp:153-157, kernels.cpp:52-53) */
+    double h_max, h_min;           /* both > 0: dynamic adaptivity (the runner's h_max / h_min, runner.cpp:206-366):
+                                      `levels` is ignored, the tree starts regular at max(ell_min,
+                                      level_for_h(h_max)) and tmg_mark after a sweep marks cells that the next
+                                      sweep refines / erases; exact precision */
 } tmg_problem;
 
 typedef struct tmg_policy {        /* OmegaPolicy, proj/include/treemg/cycles.hpp:17-24 */
@@ -102,6 +106,15 @@ treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_swe
    cycles.hpp:27-31): writes min(channels, cap) entries of each non-null array and
    returns the channel count (0 for a one-channel hierarchy), -1 on a null handle. */
 int tmg_channel_norms(tmg_hierarchy* h, double* max_norm, double* euclid, double* h_norm, int cap);
+/* Dynamic adaptivity: mark (amr.cpp:61-222) on the device after a td_add / td_bpx.
+ * out9: refinedCells, erasedCells of the last sweep, then MarkStats (amr.hpp:19-27)
+ * refineVertices, eraseVertices, refineCells, eraseCells, vetoConvergence, vetoHMin, vetoHMax. */
+treemg_status tmg_mark(tmg_hierarchy* h, long long* out9);
+/* current depth of the tree (grows under dynamic adaptivity) */
+int tmg_levels(const tmg_hierarchy* h);
+/* overwrite the pending marks of every existing cell of `level` (full lattice,
+ * lower corner: 4 refineMark, 8 eraseMark), e.g. to replay externally chosen marks */
+treemg_status tmg_set_cell_marks(tmg_hierarchy* h, int level, const unsigned char* cells);
 
 /* Verification cycles of a regular tree held in exact storage (precision 0),
  * each followed by evaluate_residual_norms (cycles.cpp:716-786) into *out:
@@ -138,6 +151,30 @@ long long tmg_hanging_vertices(const tmg_hierarchy* h);
  * touched last in (0xFF absent) -- the restriction-order table of amr.hpp. */
 treemg_status tmg_sphere_tree(int dim, int base, int sphere_levels, int level, unsigned char* flags,
                               signed char* succ, unsigned char* cells, unsigned char* finish_corner);
+/* Host-only (no GPU): the structural replay of dynamic adaptivity (dyn.hpp).
+ * A tree built as build_regular(start) (spacetree.cpp:48-76); cell marks
+ * (full-lattice, lower corner; 4 refineMark, 8 eraseMark) are applied by
+ * tmg_dyn_sweep exactly as one td_add / td_bpx traversal with applyMarks does
+ * (refine on descent cycles.cpp:174-180, erase on backtracking :222-241),
+ * followed by classify().  out4: refinedCells, erasedCells, touch-last
+ * updates of unrefined interior vertices, vertices with a special pattern. */
+typedef struct tmg_dyn tmg_dyn;
+treemg_status tmg_dyn_create(int dim, int start, int max_level, int ell_min, double h_min, long long max_vertices,
+                             tmg_dyn** out);
+void tmg_dyn_destroy(tmg_dyn* h);
+int tmg_dyn_depth(const tmg_dyn* h);
+long long tmg_dyn_interior_count(const tmg_dyn* h);
+treemg_status tmg_dyn_set_cell_marks(tmg_dyn* h, int level, const unsigned char* cells);
+treemg_status tmg_dyn_sweep(tmg_dyn* h, long long* out4);
+/* flags: 1 exists | 2 hanging | 4 refined | 8 boundary | 16 cPoint; succ (-1 absent);
+ * cells: 1 exists | 2 refined | 4 refineMark | 8 eraseMark (full lattices) */
+treemg_status tmg_dyn_flags(tmg_dyn* h, int level, unsigned char* flags, signed char* succ, unsigned char* cells);
+/* The per-vertex tables of the last sweep: role (dyn.hpp kS*), first finish
+ * corner, finish / skipped cells as bit masks over cell = v - 1 + bits(e),
+ * succ at the touch-last finish, and the cells visited (1) / refined on entry (2). */
+treemg_status tmg_dyn_sweep_tables(tmg_dyn* h, int level, unsigned char* role, unsigned char* finish_corner,
+                                   unsigned char* finish_cells, unsigned char* skip_cells, signed char* succ,
+                                   unsigned char* cells);
 /* Spacetree::interior_fine_vertex_count (spacetree.cpp:225-231): non-hanging,
  * non-refined, interior vertices over all levels */
 long long tmg_leaf_vertices(const tmg_hierarchy* h);

@@ -30,6 +30,7 @@
 #include <string>
 #include <vector>
 
+#include "treemg/amr.hpp"
 #include "treemg/cycles.hpp"
 #include "treemg/elemops.hpp"
 #include "treemg/kernels.hpp"
@@ -161,6 +162,11 @@ struct Session {
     int fmgStageCap = 0;
     bool checkLemma1 = false;
     int finalLevel = 0;
+    // dynamic adaptivity (h_max / h_min, runner.cpp:206-366): marks after every sweep
+    bool adaptive = false;
+    AmrConfig amr;
+    MarkStats lastMark;
+    int lastRefined = 0, lastErased = 0;
 
     // run results
     int status = 0;  // 0 ok, 1 usage, 2 capacity, 3 runtime
@@ -229,9 +235,13 @@ void setup(Session& s, const std::string& text) {
     }
     s.cfg.validate();
     s.spec = problem_of(s.cfg);
-    if (s.cfg.fixedLevel == 0) throw UnsupportedConfigError("oracle driver: fixed-level runs only");
-    s.finalLevel = s.cfg.fixedLevel + s.sphereLevels;
-    const int start = s.fmgFrom > 0 ? s.fmgFrom : s.cfg.fixedLevel;
+    s.adaptive = s.cfg.fixedLevel == 0;
+    if (s.adaptive && (s.sphereLevels > 0 || s.fmgFrom > 0))
+        throw UnsupportedConfigError("oracle driver: h_max/h_min runs take no sphere_levels / fmg_from");
+    s.finalLevel = s.adaptive ? reference_level_of(s.cfg) : s.cfg.fixedLevel + s.sphereLevels;
+    const int start = s.adaptive ? start_level_of(s.cfg) : s.fmgFrom > 0 ? s.fmgFrom : s.cfg.fixedLevel;
+    s.amr.hMax = s.cfg.hMax;  // runner.cpp:228-230
+    s.amr.hMin = s.cfg.hMin;
     s.rhs.lmax = s.finalLevel;
     g_rhs = s.rhs;
     Spacetree::Config tcfg;
@@ -261,6 +271,8 @@ SweepStats one_sweep(Session& s, int n) {
     if (s.hbSweeps >= 0) pol.hbMask = n <= s.hbSweeps;
     SweepOptions opt;
     opt.checkLemma1 = s.checkLemma1;
+    opt.applyMarks = s.adaptive;  // runner.cpp:256-258
+    opt.hMinRefine = s.cfg.hMin;
     switch (s.cfg.cycle) {
         case CycleKind::TdAdd: return td_add(*s.tree, s.spec, pol, n, opt);
         case CycleKind::TdBPX: return td_bpx(*s.tree, s.spec, pol, n, opt);
@@ -363,6 +375,13 @@ void run_loop(Session& s) {
             break;
         }
         const bool converged = stageFirst < 1e-300 || current <= cfg.targetResidualDrop * stageFirst;
+        if (s.adaptive) {  // runner.cpp:350-358
+            s.lastMark = mark(*s.tree, s.amr);
+            const MarkStats& m = s.lastMark;
+            log << "sweep " << n << ": refined=" << stats.refinedCells << " erased=" << stats.erasedCells
+                << " marks(refine=" << m.refineCells << ", erase=" << m.eraseCells << ", veto_conv=" << m.vetoConvergence
+                << ", veto_hmin=" << m.vetoHMin << ", veto_hmax=" << m.vetoHMax << ")\n";
+        }
         const bool lastStage = !fmg || s.tree->depth() >= cfg.fixedLevel;
         if (lastStage) {
             if (converged) {
@@ -421,6 +440,7 @@ Cplx field_of(const ChannelState& ch, const char* f) {
     if (!std::strcmp(f, "sf")) return ch.sf;
     if (!std::strcmp(f, "si")) return ch.si;
     if (!std::strcmp(f, "sinext")) return ch.siNext;
+    if (!std::strcmp(f, "s")) return Cplx(ch.s, 0.0);
     return Cplx(std::nan(""), std::nan(""));
 }
 
@@ -499,6 +519,11 @@ int refd_sweep(void* h, int n, double* out) {
             out[2] = aggregate_l2(st.hNorm);
             out[3] = static_cast<double>(st.updatedFineVertices);
             out[4] = st.lemma1MaxError;
+        }
+        if (s->adaptive) {
+            s->lastRefined = st.refinedCells;
+            s->lastErased = st.erasedCells;
+            s->lastMark = mark(*s->tree, s->amr);
         }
     });
 }
@@ -615,6 +640,42 @@ unsigned long long refd_field_hash(void* h, int level, const char* field, int ch
         }
     }
     return hsh;
+}
+
+// Dynamic adaptivity: refinedCells, erasedCells of the last refd_sweep and the
+// MarkStats of the mark() that followed it (amr.hpp:19-27).
+void refd_mark_stats(void* h, long long* out9) {
+    auto* s = static_cast<Session*>(h);
+    const MarkStats& m = s->lastMark;
+    const long long v[9] = {s->lastRefined, s->lastErased,
+                            static_cast<long long>(m.refineVertices), static_cast<long long>(m.eraseVertices),
+                            static_cast<long long>(m.refineCells), static_cast<long long>(m.eraseCells),
+                            static_cast<long long>(m.vetoConvergence), static_cast<long long>(m.vetoHMin),
+                            static_cast<long long>(m.vetoHMax)};
+    std::copy(v, v + 9, out9);
+}
+
+// Per cell (lower corner, full lattice): 1 exists | 2 refined | 4 refineMark | 8 eraseMark.
+void refd_cell_marks(void* h, int level, unsigned char* cells) {
+    auto* s = static_cast<Session*>(h);
+    const int p = s->tree->dim();
+    std::fill(cells, cells + lattice_size(p, level), 0);
+    if (level > s->tree->depth()) return;
+    s->tree->for_each_cell_at(level, [&](const Index& idx, Cell& c) {
+        cells[lattice_flat(p, level, idx)] = static_cast<unsigned char>(1 | (c.refined ? 2 : 0) |
+                                                                        (c.refineMark ? 4 : 0) | (c.eraseMark ? 8 : 0));
+    });
+}
+
+// Overwrites the pending marks of every existing cell (4 refineMark, 8 eraseMark).
+void refd_set_cell_marks(void* h, int level, const unsigned char* cells) {
+    auto* s = static_cast<Session*>(h);
+    const int p = s->tree->dim();
+    s->tree->for_each_cell_at(level, [&](const Index& idx, Cell& c) {
+        const unsigned char m = cells[lattice_flat(p, level, idx)];
+        c.refineMark = (m & 4) != 0;
+        c.eraseMark = (m & 8) != 0;
+    });
 }
 
 // Regular-grid classification summary used to pin the per-level omega tables.

@@ -78,6 +78,9 @@ def lib():
         L.refd_vertex_succ.restype = ip
         L.refd_vertex_succ.argtypes = [vp, ip, ctypes.POINTER(ip)]
         L.refd_omega.argtypes = [ip, dp, dp, ip, ip, ip, ip, ip, ip, ip, ip, ctypes.POINTER(dp)]
+        L.refd_mark_stats.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+        L.refd_cell_marks.argtypes = [vp, ip, vp]
+        L.refd_set_cell_marks.argtypes = [vp, ip, vp]
         # the reference's own C-ABI (proj/src/capi.cpp), unmodified
         L.treemg_config_new.restype = vp
         L.treemg_config_free.argtypes = [vp]
@@ -203,6 +206,27 @@ class RefSession:
         self.L.refd_flags(self.h, level, fl.ctypes.data_as(ctypes.c_void_p), sc.ctypes.data_as(ctypes.c_void_p),
                           ce.ctypes.data_as(ctypes.c_void_p))
         return fl, sc, ce
+
+    MARK_KEYS = ("refined", "erased", "refine_vertices", "erase_vertices", "refine_cells", "erase_cells",
+                 "veto_conv", "veto_hmin", "veto_hmax")
+
+    def mark_stats(self) -> dict:
+        """h_max/h_min sessions: refined/erased cells of the last sweep() and the
+        MarkStats of the mark() that followed it."""
+        buf = (ctypes.c_longlong * 9)()
+        self.L.refd_mark_stats(self.h, buf)
+        return dict(zip(self.MARK_KEYS, list(buf)))
+
+    def cell_marks(self, level: int) -> np.ndarray:
+        """Per cell (lower corner): 1 exists | 2 refined | 4 refineMark | 8 eraseMark."""
+        n = self.L.refd_lattice_size(self.h, level)
+        ce = np.zeros(n, np.uint8)
+        self.L.refd_cell_marks(self.h, level, ce.ctypes.data_as(ctypes.c_void_p))
+        return ce
+
+    def set_cell_marks(self, level: int, cells: np.ndarray):
+        c = np.ascontiguousarray(cells, np.uint8)
+        self.L.refd_set_cell_marks(self.h, level, c.ctypes.data_as(ctypes.c_void_p))
 
     def interior_count(self) -> int:
         return int(self.L.refd_interior_count(self.h))

@@ -48,7 +48,9 @@ EXTENSION_SYMBOLS = [
     "treemg_result_fingerprint", "tmg_test_divdc3", "tmg_nccl_unique_id", "tmg_slabs_create", "tmg_slabs_destroy",
     "tmg_slabs_cycle", "tmg_slabs_get_fine_u", "tmg_slabs_time_cycles", "tmg_slabs_owned_planes", "tmg_slab_plan",
     "tmg_slabs_e2e_step", "tmg_get_flags", "tmg_hanging_vertices", "tmg_leaf_vertices", "tmg_sphere_tree",
-    "tmg_bu_fas", "tmg_textbook_add", "tmg_channel_norms",
+    "tmg_bu_fas", "tmg_textbook_add", "tmg_channel_norms", "tmg_dyn_create", "tmg_dyn_destroy", "tmg_dyn_depth",
+    "tmg_dyn_interior_count", "tmg_dyn_set_cell_marks", "tmg_dyn_sweep", "tmg_dyn_flags", "tmg_dyn_sweep_tables",
+    "tmg_mark", "tmg_levels", "tmg_set_cell_marks",
 ]
 
 _lib = None
@@ -67,7 +69,8 @@ class _Problem(ctypes.Structure):
                 ("chi_kind", ctypes.c_int), ("rhs_seed", ctypes.c_ulonglong), ("rhs_sphere", ctypes.c_int),
                 ("precision", ctypes.c_int), ("max_vertices", ctypes.c_longlong), ("device", ctypes.c_int),
                 ("sphere_levels", ctypes.c_int), ("channels", ctypes.c_int),
-                ("coupling_re", ctypes.c_double), ("coupling_im", ctypes.c_double)]
+                ("coupling_re", ctypes.c_double), ("coupling_im", ctypes.c_double),
+                ("h_max", ctypes.c_double), ("h_min", ctypes.c_double)]
 
 
 class _Policy(ctypes.Structure):
@@ -119,6 +122,27 @@ def lib():
         L.tmg_hierarchy_create.restype = ip
         L.tmg_hierarchy_create.argtypes = [ctypes.POINTER(_Problem), ctypes.POINTER(vp)]
         L.tmg_hierarchy_destroy.argtypes = [vp]
+        L.tmg_dyn_create.restype = ip
+        L.tmg_dyn_create.argtypes = [ip, ip, ip, ip, dp, ctypes.c_longlong, ctypes.POINTER(vp)]
+        L.tmg_dyn_destroy.argtypes = [vp]
+        L.tmg_dyn_depth.restype = ip
+        L.tmg_dyn_depth.argtypes = [vp]
+        L.tmg_dyn_interior_count.restype = ctypes.c_longlong
+        L.tmg_dyn_interior_count.argtypes = [vp]
+        L.tmg_dyn_set_cell_marks.restype = ip
+        L.tmg_dyn_set_cell_marks.argtypes = [vp, ip, vp]
+        L.tmg_dyn_sweep.restype = ip
+        L.tmg_dyn_sweep.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+        L.tmg_dyn_flags.restype = ip
+        L.tmg_dyn_flags.argtypes = [vp, ip, vp, vp, vp]
+        L.tmg_dyn_sweep_tables.restype = ip
+        L.tmg_dyn_sweep_tables.argtypes = [vp, ip, vp, vp, vp, vp, vp, vp]
+        L.tmg_mark.restype = ip
+        L.tmg_mark.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+        L.tmg_set_cell_marks.restype = ip
+        L.tmg_set_cell_marks.argtypes = [vp, ip, vp]
+        L.tmg_levels.restype = ip
+        L.tmg_levels.argtypes = [vp]
         L.tmg_channel_norms.restype = ip
         L.tmg_channel_norms.argtypes = [vp, pd, pd, pd, ip]
         for n in ("tmg_td_add", "tmg_td_bpx"):
@@ -267,7 +291,7 @@ class Hierarchy:
     def __init__(self, dim: int, levels: int, phi: complex = 0.0, theta_deg: float = 0.0, chi: str = "sin",
                  rhs_seed: int = 12345, rhs_sphere: bool = False, ell_min: int = 1, precision: str = "exact",
                  max_vertices: int = 0, device: int = 0, sphere_levels: int = 0, channels: int = 1,
-                 coupling: complex = 0.0):
+                 coupling: complex = 0.0, h_max: float = 0.0, h_min: float = 0.0):
         """levels: depth of the regular base tree; sphere_levels > 0 adds that many
         levels refined inside |x - 1/2|^2 < 0.04 (static adaptive tree, cfg4).
         channels > 1: that many unknowns per vertex with the same fields, coupled
@@ -277,13 +301,16 @@ class Hierarchy:
         prob = _Problem(dim, levels, ell_min, np.deg2rad(theta_deg) if theta_deg else 0.0,
                         complex(phi).real, complex(phi).imag, CHI_KINDS[chi], rhs_seed, int(rhs_sphere),
                         1 if precision == "fast" else 0, max_vertices, device, sphere_levels, channels,
-                        complex(coupling).real, complex(coupling).imag)
+                        complex(coupling).real, complex(coupling).imag, h_max, h_min)
         if theta_deg:
             prob.theta = theta_deg * np.pi / 180.0  # ProblemSpec::thetaGlobal = deg * M_PI / 180.0
         h = ctypes.c_void_p()
         _check(self.L.tmg_hierarchy_create(ctypes.byref(prob), ctypes.byref(h)))
         self.h = h
         self.dim, self.levels = dim, levels + sphere_levels
+        self.dynamic = h_max > 0 and h_min > 0
+        if self.dynamic:
+            self.levels = self.L.tmg_levels(self.h)
 
     def close(self):
         if getattr(self, "h", None):
@@ -307,6 +334,25 @@ class Hierarchy:
 
     def td_bpx(self, pol: Policy, n: int) -> SweepStats:
         return self._sweep(self.L.tmg_td_bpx, pol, n)
+
+    MARK_KEYS = ("refined", "erased", "refine_vertices", "erase_vertices", "refine_cells", "erase_cells",
+                 "veto_conv", "veto_hmin", "veto_hmax")
+
+    def mark(self) -> dict:
+        """Dynamic adaptivity: mark on the device after a sweep (amr.cpp:61-222);
+        refined / erased are the structural edits of that sweep."""
+        out = (ctypes.c_longlong * 9)()
+        _check(self.L.tmg_mark(self.h, out))
+        self.levels = self.L.tmg_levels(self.h)
+        return dict(zip(self.MARK_KEYS, list(out)))
+
+    def depth(self) -> int:
+        return self.L.tmg_levels(self.h)
+
+    def set_cell_marks(self, level: int, cells: np.ndarray):
+        """Overwrite the pending cell marks of `level` (4 refine, 8 erase per lattice cell)."""
+        c = np.ascontiguousarray(cells, np.uint8)
+        _check(self.L.tmg_set_cell_marks(self.h, level, c.ctypes.data_as(ctypes.c_void_p)))
 
     def channel_norms(self):
         """Per-channel (max, euclid, h) norms of the last td_add / td_bpx sweep
@@ -467,6 +513,61 @@ def device_divide(x: np.ndarray, y: np.ndarray) -> np.ndarray:
     out = np.zeros_like(x)
     _check(lib().tmg_test_divdc3(_pd(x.view(np.float64)), _pd(y.view(np.float64)), _pd(out.view(np.float64)), len(x)))
     return out
+
+
+class DynStructure:
+    """Host-only structural replay of dynamic adaptivity (tmg_dyn_*, dyn.hpp):
+    the tree a td_add / td_bpx traversal with applyMarks leaves behind."""
+
+    def __init__(self, dim: int, start: int, max_level: int, ell_min: int = 1, h_min: float = 1e-3,
+                 max_vertices: int = 0):
+        self.L = lib()
+        h = ctypes.c_void_p()
+        _check(self.L.tmg_dyn_create(dim, start, max_level, ell_min, h_min, max_vertices, ctypes.byref(h)))
+        self.h, self.dim = h, dim
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.L.tmg_dyn_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def depth(self) -> int:
+        return self.L.tmg_dyn_depth(self.h)
+
+    def interior_count(self) -> int:
+        return int(self.L.tmg_dyn_interior_count(self.h))
+
+    def _n(self, level: int) -> int:
+        return (3 ** level + 1) ** self.dim
+
+    def set_cell_marks(self, level: int, cells: np.ndarray):
+        c = np.ascontiguousarray(cells, np.uint8)
+        _check(self.L.tmg_dyn_set_cell_marks(self.h, level, c.ctypes.data_as(ctypes.c_void_p)))
+
+    def sweep(self):
+        out = (ctypes.c_longlong * 4)()
+        _check(self.L.tmg_dyn_sweep(self.h, out))
+        return dict(refined=out[0], erased=out[1], updated=out[2], special=out[3])
+
+    def flags(self, level: int):
+        n = self._n(level)
+        fl, sc, ce = np.zeros(n, np.uint8), np.zeros(n, np.int8), np.zeros(n, np.uint8)
+        _check(self.L.tmg_dyn_flags(self.h, level, fl.ctypes.data_as(ctypes.c_void_p),
+                                    sc.ctypes.data_as(ctypes.c_void_p), ce.ctypes.data_as(ctypes.c_void_p)))
+        return fl, sc, ce
+
+    def sweep_tables(self, level: int):
+        n = self._n(level)
+        arrs = [np.zeros(n, np.uint8) for _ in range(4)] + [np.zeros(n, np.int8), np.zeros(n, np.uint8)]
+        _check(self.L.tmg_dyn_sweep_tables(self.h, level, *[a.ctypes.data_as(ctypes.c_void_p) for a in arrs]))
+        return dict(zip(("role", "finish_corner", "finish_cells", "skip_cells", "succ", "cells"), arrs))
 
 
 def sphere_tree(dim: int, base: int, sphere_levels: int, level: int):

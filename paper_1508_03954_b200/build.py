@@ -15,8 +15,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libtreemg_b200.so")
-SOURCES = ["hierarchy.cu", "amr.cu", "fast.cu", "fused2.cu", "fused3.cu", "vcycles.cu", "runner.cpp", "capi.cpp"]
-HEADERS = ["hierarchy.hpp", "amr.hpp", "exact_ops.cuh", "fast.cuh", "fused2.cuh", "fused3.cuh", "vcycles.cuh", "lattice.cuh", "runner.hpp",
+SOURCES = ["hierarchy.cu", "amr.cu", "fast.cu", "fused2.cu", "fused3.cu", "vcycles.cu", "dyn.cpp", "runner.cpp", "capi.cpp"]
+HEADERS = ["hierarchy.hpp", "amr.hpp", "dyn.hpp", "exact_ops.cuh", "fast.cuh", "fused2.cuh", "fused3.cuh", "vcycles.cuh", "lattice.cuh", "runner.hpp",
            "slabs.inc"]
 
 

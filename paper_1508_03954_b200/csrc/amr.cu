@@ -13,6 +13,7 @@
 #include <climits>
 #include <cmath>
 #include <cstring>
+#include <array>
 #include <thread>
 
 #include "exact_ops.cuh"
@@ -42,6 +43,21 @@ struct ALvl {
     const signed char* succ;
     const unsigned* list;  // existing vertices: interior non-hanging first, then the rest
     unsigned nlist;
+    // dynamic adaptivity (dyn.hpp): sweep tables beyond the static ones, the
+    // classification after the sweep, and the mark pass's per-vertex data
+    double2* dg;                  // accumulated operator diagonal (mark's convergence indicator)
+    const unsigned char* fmask;   // finish cells (bit e: cell = v - 1 + bits(e))
+    const unsigned char* skip;    // cells entered before the vertex was created
+    const int* xoff;              // special vertices: first slot of their finish values in extras
+    double2* extras;              // r-hat at each finish of a special vertex, in traversal order
+    const unsigned* slist;        // special vertices
+    unsigned nslist;
+    const unsigned char* fflag;   // classification after the sweep (amr::k* bits)
+    const unsigned char* fcell;   // cells after the sweep (kCellExists | kCellRefined)
+    double* feat;                 // mark: feature s per candidate
+    double* ind;                  // mark: |r| / |diag|
+    unsigned char* vmark;         // mark: 1 refine, 2 erase, 4 candidate
+    unsigned* cmark;              // mark: per cell, dyn::kRM | dyn::kEM
     int lo[3];
     int n1[3];
     unsigned n;
@@ -53,6 +69,7 @@ struct AResArgs {
     ALvl lv, par;
     LevelConst k;
     double2 wTab[12];  // omega_unmasked(pol, succ, n) for succ = 0..11
+    double2 dgTab[9];  // diag after k cells: ((A_aa + A_aa) + ...) k times (zero_accumulators, then +=)
     int ellMin, bpx, hb;
     double* partials;
 };
@@ -122,6 +139,15 @@ __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
             return prolong<P>(v, rel);
         };
         const double2 pu = parent_prolong(pr.u);
+        if (vf & dyn::kSCreated) {  // create_vertex_if_missing inside the sweep (spacetree.cpp:245-270, 310-318)
+            c.u[f] = pu;
+            c.sc[f] = cz();
+            c.uhat[f] = cz();
+            if (c.sf) c.sf[f] = cz();
+            if (c.si) c.si[f] = cz();
+            if (c.sinext) c.sinext[f] = cz();
+            continue;
+        }
         const double2 ps = parent_prolong(pr.sc);
         if (hang) {  // create_hanging
             double2 u = pu, sc = ps;
@@ -155,6 +181,87 @@ __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
 }
 
 // ---- chi: leaf loads and restriction in traversal time order ---------------
+// r-hat value fine vertex vf restricts from its finish in the child cell where
+// it is corner ec; false if it does not finish there.  A special vertex
+// (dynamic adaptivity) may finish in several cells, in traversal (Morton)
+// order of the cells around it, each with its own value.
+template <int P>
+__device__ __forceinline__ bool fine_finish_value(const ALvl& fl, int vf, int ec, double2& val) {
+    constexpr int NC = 1 << P;
+    if (fl.fmask && (fl.vflag[vf] & dyn::kSSpecial)) {
+        const unsigned char fm = fl.fmask[vf];
+        const int ep = (~ec) & (NC - 1);
+        if (!((fm >> ep) & 1)) return false;
+        int g[P];
+        aunflat<P>(static_cast<unsigned>(vf), fl, g);
+        const int pid = perm_id<P>(g);
+        int k = 0;
+        for (int i = 0; i < NC; ++i) {
+            const int e = perm_cell(P, pid, i);
+            if (e == ep) break;
+            k += (fm >> e) & 1;
+        }
+        val = fl.extras[fl.xoff[vf] + k];
+        return true;
+    }
+    if (fl.estar[vf] != ec) return false;
+    val = fl.rhat[vf];
+    return true;
+}
+
+// chi contribution of one existing cell around g (g is corner a of it):
+// the leaf load on entering it (kernels.cpp:69-87), or, for a cell refined on
+// entry, the restriction of the fine vertices touched last inside it, in
+// child order, then by their corner index in the child (visit_cell's finish loop)
+template <int P>
+__device__ __forceinline__ void cell_chi(double2& acc, const ALvl& c, const ALvl& fl, const LevelConst& k,
+                                         const double* __restrict__ w5, const int* g, const int* cell, int a,
+                                         unsigned char cfl, int restrictOn) {
+    constexpr int NC = 1 << P;
+    constexpr int NT = P == 1 ? 3 : P == 2 ? 9 : 27;
+    if (!(cfl & amr::kCellRefined)) {
+        double2 acc2 = cz();
+#pragma unroll
+        for (int bb = 0; bb < NC; ++bb) {
+            int vb[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
+            acc2 = xadd(acc2, xscale(k.M[a ^ bb], c.nodal[aflat<P>(c, vb)]));
+        }
+        acc = xadd(acc, xmul(k.massScale, acc2));
+        return;
+    }
+    if (!restrictOn) return;
+    for (int t = 0; t < NT; ++t) {
+        int j[P];
+        int tt = t;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            j[d] = tt % 3;
+            tt /= 3;
+        }
+        for (int ec = 0; ec < NC; ++ec) {
+            int v[P];
+            int code = 0, mul = 1;
+            bool in = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                v[d] = 3 * cell[d] + j[d] + ((ec >> d) & 1);
+                const int off = v[d] - 3 * g[d];
+                in &= (off >= -2) & (off <= 2) & (v[d] >= 1) & (v[d] <= fl.m - 1);
+                code += (off + 2) * mul;
+                mul *= 5;
+            }
+            if (!in) continue;
+            const int vf = aflat<P>(fl, v);
+            if (vf < 0) continue;
+            double2 val;
+            if (!fine_finish_value<P>(fl, vf, ec, val)) continue;
+            acc = xadd(acc, xscale(w5[code], val));
+        }
+    }
+}
+
 template <int P>
 __global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, const double* __restrict__ w5,
                                                  int restrictOn) {
@@ -203,47 +310,7 @@ __global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, 
                 }
                 continue;
             }
-            if (!(cfl & amr::kCellRefined)) {
-                // leaf: consistent-mass load on entering the cell (kernels.cpp:69-87)
-                double2 acc2 = cz();
-#pragma unroll
-                for (int bb = 0; bb < NC; ++bb) {
-                    int vb[P];
-#pragma unroll
-                    for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
-                    acc2 = xadd(acc2, xscale(k.M[a ^ bb], c.nodal[aflat<P>(c, vb)]));
-                }
-                acc = xadd(acc, xmul(k.massScale, acc2));
-            } else if (restrictOn) {
-                // refined: fine vertices finishing inside this cell, in child order,
-                // then by their corner index in the child (visit_cell's finish loop)
-                for (int t = 0; t < NT; ++t) {
-                    int j[P];
-                    int tt = t;
-#pragma unroll
-                    for (int d = 0; d < P; ++d) {
-                        j[d] = tt % 3;
-                        tt /= 3;
-                    }
-                    for (int ec = 0; ec < NC; ++ec) {
-                        int v[P];
-                        int code = 0, mul = 1;
-                        bool in = true;
-#pragma unroll
-                        for (int d = 0; d < P; ++d) {
-                            v[d] = 3 * cell[d] + j[d] + ((ec >> d) & 1);
-                            const int off = v[d] - 3 * g[d];
-                            in &= (off >= -2) & (off <= 2) & (v[d] >= 1) & (v[d] <= fl.m - 1);
-                            code += (off + 2) * mul;
-                            mul *= 5;
-                        }
-                        if (!in) continue;
-                        const int vf = aflat<P>(fl, v);
-                        if (vf < 0 || fl.estar[vf] != ec) continue;
-                        acc = xadd(acc, xscale(w5[code], fl.rhat[vf]));
-                    }
-                }
-            }
+            cell_chi<P>(acc, c, fl, k, w5, g, cell, a, cfl, restrictOn);
         }
         c.chi[f] = acc;
     }
@@ -317,6 +384,67 @@ __device__ __forceinline__ double2 regular_residual(const double2* __restrict__ 
     }
 }
 
+// Special vertices of a dynamic sweep (dyn.hpp kSSpecial): created after some
+// adjacent cells were already entered (those never reach it), or finishing
+// more than once (hanging vertices on the rim of blocks refined later in the
+// same traversal: each destroy_hanging, cycles.cpp:305-321, folds chi + r-hat
+// again), or never.  The accumulators run over the cells in traversal order;
+// every finish records its r-hat for the parents' restriction.
+template <int P>
+__global__ void __launch_bounds__(256) k_dyn_special(ALvl c, ALvl fl, LevelConst k, const double* __restrict__ w5,
+                                                     int restrictOn, int ellMin, const double2* __restrict__ dgTab) {
+    constexpr int NC = 1 << P;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nslist; i += gridDim.x * blockDim.x) {
+        const unsigned f = c.slist[i];
+        const unsigned char vf = c.vflag[f];
+        const bool bnd = vf & amr::kBoundary, hang = vf & amr::kHanging;
+        int g[P];
+        aunflat<P>(f, c, g);
+        const int pid = perm_id<P>(g);
+        const unsigned char skip = c.skip[f], fm = c.fmask[f];
+        double2 r = cz(), rh = cz(), chi = cz();
+        bool first = true;
+        int ncell = 0, kfin = 0;
+        for (int ii = 0; ii < NC; ++ii) {
+            const int e = perm_cell(P, pid, ii);
+            int cell[P];
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                cell[d] = g[d] - 1 + ((e >> d) & 1);
+                ok &= (cell[d] >= 0) & (cell[d] <= c.m - 1);
+            }
+            if (!ok || ((skip >> e) & 1)) continue;
+            const int cf = aflat<P>(c, cell);
+            if (cf < 0) continue;
+            const unsigned char cfl = c.cflag[cf];
+            if (!(cfl & amr::kCellExists)) continue;
+            const int ca = (~e) & (NC - 1);
+            const double2 sr = cell_apply<P>(c.u, c, cell, ca, k.A);
+            const double2 sh = cell_apply<P>(c.uhat, c, cell, ca, k.A);
+            if (first) {
+                r = xneg(sr);
+                rh = xneg(sh);
+                first = false;
+            } else {
+                r = xsub(r, sr);
+                rh = xsub(rh, sh);
+            }
+            ++ncell;
+            cell_chi<P>(chi, c, fl, k, w5, g, cell, ca, cfl, restrictOn);
+            if ((fm >> e) & 1) {  // finishes at the end of this cell's visit
+                if (hang && c.level > ellMin) rh = bnd ? cz() : xadd(chi, rh);
+                c.extras[c.xoff[f] + kfin] = rh;
+                ++kfin;
+            }
+        }
+        c.chi[f] = chi;
+        c.rhat[f] = rh;
+        c.r[f] = r;
+        c.dg[f] = ncell > 0 ? dgTab[ncell] : cz();
+    }
+}
+
 // ---- residual + touch_last / destroy_hanging --------------------------------
 template <int P>
 #ifndef TMG_AMR_RES_MINB
@@ -330,6 +458,7 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
         const unsigned f = c.list[i];
         const unsigned char vf = c.vflag[f];
         if (!(vf & amr::kExists)) continue;
+        if (c.slist && (vf & dyn::kSSpecial)) continue;  // k_dyn_special
         const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging,
                    refined = vf & amr::kRefined;
         int g[P];
@@ -337,11 +466,14 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
         const int pid = perm_id<P>(g);
         double2 r = cz(), rh = cz();
         bool first = true;
+        int ncell = NC;
         const bool general = hang || bnd;
         if (!general) {  // every cell around g exists
             const int sy = c.n1[0], sz = c.n1[0] * c.n1[1];
             r = regular_residual<P>(c.u, static_cast<int>(f), sy, sz, a.k.A, pid);
             rh = regular_residual<P>(c.uhat, static_cast<int>(f), sy, sz, a.k.A, pid);
+        } else {
+            ncell = 0;
         }
         for (int i = 0; i < NC && general; ++i) {
             const int e = perm_cell(P, pid, i);
@@ -366,7 +498,9 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
                 r = xsub(r, sr);
                 rh = xsub(rh, sh);
             }
+            ++ncell;
         }
+        if (c.dg) c.dg[f] = ncell > 0 ? a.dgTab[ncell] : cz();
         const double2 chi = c.chi[f];
         if (hang) {  // destroy_hanging: only r-hat (plus load) goes down
             double2 rhat = rh;
@@ -452,9 +586,9 @@ __global__ void k_amr_norm_final(const double* __restrict__ partials, const int*
 
 // ---- setup -------------------------------------------------------------------
 template <int P>
-__global__ void k_amr_seeded(ALvl c, unsigned long long seed, long long scale, long long mkey, int sphere) {
+__global__ void k_amr_seeded(ALvl c, unsigned long long seed, long long scale, long long mkey, int sphere, int all) {
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
-        if (!(c.vflag[f] & amr::kExists)) continue;
+        if (!all && !(c.vflag[f] & amr::kExists)) continue;
         int g[P];
         aunflat<P>(f, c, g);
         unsigned long long key = 0;
@@ -508,6 +642,279 @@ __global__ void k_amr_inject(ALvl c, ALvl fine) {
         for (int d = 0; d < P; ++d) fi[d] = 3 * g[d];
         const int ff = aflat<P>(fine, fi);
         c.u[f] = (ff >= 0 && (fine.vflag[ff] & amr::kExists)) ? fine.u[ff] : cz();
+    }
+}
+
+// ---- dynamic adaptivity: mark (amr.cpp:18-222) ------------------------------
+// |z| as the host's libm computes it (std::abs(complex) -> hypot): glibc's
+// hypot, Borges' algorithm with the non-FMA correction kernel; pinned
+// bit-for-bit against the host libm (tests/test_dyn_structure.py).  Every
+// operation is an explicit round-to-nearest intrinsic (no contraction).
+__device__ __forceinline__ double hypot_kernel(double ax, double ay) {
+    double h = __dsqrt_rn(__dadd_rn(__dmul_rn(ax, ax), __dmul_rn(ay, ay)));
+    double t1, t2;
+    if (h <= 2.0 * ay) {
+        const double delta = __dsub_rn(h, ay);
+        t1 = __dmul_rn(ax, __dsub_rn(2.0 * delta, ax));
+        t2 = __dmul_rn(__dsub_rn(delta, 2.0 * __dsub_rn(ax, ay)), delta);
+    } else {
+        const double delta = __dsub_rn(h, ax);
+        t1 = __dmul_rn(2.0 * delta, __dsub_rn(ax, 2.0 * ay));
+        t2 = __dadd_rn(__dmul_rn(__dsub_rn(4.0 * delta, ay), ay), __dmul_rn(delta, delta));
+    }
+    return __dsub_rn(h, __ddiv_rn(__dadd_rn(t1, t2), 2.0 * h));
+}
+
+__device__ double host_hypot(double x, double y) {
+    x = fabs(x);
+    y = fabs(y);
+    if (isinf(x) || isinf(y)) return INFINITY;
+    if (isnan(x) || isnan(y)) return x + y;
+    const double ax = x < y ? y : x, ay = x < y ? x : y;
+    const double kScale = 0x1p-600, kLarge = 0x1p+511, kTiny = 0x1p-511, kEps = 0x1p-54;
+    if (ax > kLarge) {
+        if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+        return __ddiv_rn(hypot_kernel(__dmul_rn(ax, kScale), __dmul_rn(ay, kScale)), kScale);
+    }
+    if (ay < kTiny) {
+        if (ax >= __ddiv_rn(ay, kEps)) return __dadd_rn(ax, ay);
+        return __dmul_rn(hypot_kernel(__ddiv_rn(ax, kScale), __ddiv_rn(ay, kScale)), kScale);
+    }
+    if (ay <= __dmul_rn(ax, kEps)) return __dadd_rn(ax, ay);
+    return hypot_kernel(ax, ay);
+}
+
+// Spacetree::u_at (spacetree.cpp:191-205): the vertex's u if it exists and is
+// not hanging after the sweep, else the prolongation of u_at on the parent
+// stencil -- the same recursion, evaluated with an explicit frame stack (one
+// frame per level) so the depth never depends on the device call stack
+template <int P>
+__device__ double2 u_at(const ALvl* __restrict__ lvs, int level, const int* idx) {
+    constexpr int NC = 1 << P;
+    struct Frame {
+        int level, e;
+        int q[P], rel[P];
+        double2 v[NC];
+    };
+    auto direct = [&](int l, const int* id, double2& out) -> bool {
+        const ALvl& c = lvs[l];
+        const int f = aflat<P>(c, id);
+        if (f >= 0 && (c.fflag[f] & amr::kExists) && !(c.fflag[f] & amr::kHanging)) {
+            out = c.u[f];
+            return true;
+        }
+        if (l == 0) {
+            out = cz();
+            return true;
+        }
+        return false;
+    };
+    double2 res;
+    if (direct(level, idx, res)) return res;
+    Frame st[10];
+    int sp = 0;
+    auto push = [&](int l, const int* id) {
+        Frame& F = st[sp++];
+        F.level = l;
+        F.e = 0;
+        const int mc = lvs[l - 1].m;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            F.q[d] = min(id[d] / 3, mc - 1);
+            F.rel[d] = id[d] - 3 * F.q[d];
+        }
+    };
+    push(level, idx);
+    while (true) {
+        Frame& F = st[sp - 1];
+        if (F.e == NC) {
+            const double2 val = prolong<P>(F.v, F.rel);
+            if (--sp == 0) return val;
+            Frame& U = st[sp - 1];
+            U.v[U.e++] = val;
+            continue;
+        }
+        int vi[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) vi[d] = F.q[d] + ((F.e >> d) & 1);
+        double2 out;
+        if (direct(F.level - 1, vi, out)) {
+            F.v[F.e++] = out;
+            continue;
+        }
+        push(F.level - 1, vi);
+    }
+}
+
+struct MarkCounters {  // device counters of one mark pass
+    unsigned long long cand, refineV, eraseV, refineC, eraseC, vetoConv, vetoHMin, vetoHMax;
+    unsigned long long sMinBits, sMaxBits;
+};
+
+// candidates: non-hanging, unrefined, interior vertices of levels >= ellMin
+// (amr.cpp:85-90); feature (amr.cpp:18-31) and convergence indicator
+template <int P>
+__global__ void k_dyn_features(const ALvl* __restrict__ lvs, int level, int candOn, MarkCounters* cnt) {
+    const ALvl& c = lvs[level];
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        const unsigned char vf = c.fflag[f];
+        const bool cand =
+            candOn && (vf & amr::kExists) && !(vf & (amr::kHanging | amr::kRefined | amr::kBoundary));
+        c.vmark[f] = cand ? 4 : 0;
+        if (!cand) continue;
+        int g[P];
+        aunflat<P>(f, c, g);
+        const double2 centre = c.u[f];
+        double s = 0.0;
+        for (int d = 0; d < P; ++d) {
+            if (g[d] - 1 < 0 || g[d] + 1 > c.m) continue;
+            int lo[P], hi[P];
+#pragma unroll
+            for (int dd = 0; dd < P; ++dd) {
+                lo[dd] = g[dd];
+                hi[dd] = g[dd];
+            }
+            --lo[d];
+            ++hi[d];
+            const double2 a = u_at<P>(lvs, level, lo), b = u_at<P>(lvs, level, hi);
+            const double2 second = xadd(xsub(a, xscale(2.0, centre)), b);
+            s = fmax(s, host_hypot(second.x, second.y));
+        }
+        const double2 r = c.r[f], dg = c.dg[f];
+        const double ad = host_hypot(dg.x, dg.y);
+        c.feat[f] = s;
+        c.ind[f] = ad > 0.0 ? __ddiv_rn(host_hypot(r.x, r.y), ad) : 0.0;
+        const unsigned long long sb = __double_as_longlong(s);  // s >= 0: bit order is value order
+        atomicMin(&cnt->sMinBits, sb);
+        atomicMax(&cnt->sMaxBits, sb);
+        atomicAdd(&cnt->cand, 1ull);
+    }
+}
+
+__device__ __forceinline__ int mark_bin(double s, double smin, double span, int bins) {
+    const int b = static_cast<int>(__dmul_rn(__ddiv_rn(__dsub_rn(s, smin), span), static_cast<double>(bins)));
+    return min(max(b, 0), bins - 1);
+}
+
+template <int P>
+__global__ void k_dyn_hist(const ALvl* __restrict__ lvs, int level, double smin, double span, int bins,
+                           unsigned long long* hist) {
+    const ALvl& c = lvs[level];
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x)
+        if (c.vmark[f] & 4) atomicAdd(&hist[mark_bin(c.feat[f], smin, span, bins)], 1ull);
+}
+
+// amr.cpp:104-119: top bins refine, bottom bins erase, both vetoed by |r|/|diag|
+template <int P>
+__global__ void k_dyn_classify(const ALvl* __restrict__ lvs, int level, double smin, double span, int bins, int kRef,
+                               int kErase, double veto, MarkCounters* cnt) {
+    const ALvl& c = lvs[level];
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        if (!(c.vmark[f] & 4)) continue;
+        const int b = mark_bin(c.feat[f], smin, span, bins);
+        const bool vetoed = c.ind[f] > veto;
+        if (b >= bins - kRef) {
+            if (vetoed) atomicAdd(&cnt->vetoConv, 1ull);
+            else {
+                c.vmark[f] |= 1;
+                atomicAdd(&cnt->refineV, 1ull);
+            }
+        } else if (b < kErase) {
+            if (vetoed) atomicAdd(&cnt->vetoConv, 1ull);
+            else {
+                c.vmark[f] |= 2;
+                atomicAdd(&cnt->eraseV, 1ull);
+            }
+        }
+    }
+}
+
+// amr.cpp:134-161: every unrefined cell around a refine-marked vertex, above the h floor
+template <int P>
+__global__ void k_dyn_refine_cells(const ALvl* __restrict__ lvs, int level, double h, double hMin,
+                                   MarkCounters* cnt) {
+    const ALvl& c = lvs[level];
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        if (!(c.vmark[f] & 1)) continue;
+        int g[P];
+        aunflat<P>(f, c, g);
+        for (int e = 0; e < (1 << P); ++e) {
+            int ci[P];
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                ci[d] = g[d] - ((e >> d) & 1);
+                ok &= (ci[d] >= 0) & (ci[d] <= c.m - 1);
+            }
+            if (!ok) continue;
+            const int cf = aflat<P>(c, ci);
+            const unsigned char cfl = c.fcell[cf];
+            if (!(cfl & amr::kCellExists) || (cfl & amr::kCellRefined)) continue;
+            if (!(h > hMin)) {
+                atomicAdd(&cnt->vetoHMin, 1ull);
+                continue;
+            }
+            const unsigned old = atomicOr(&c.cmark[cf], static_cast<unsigned>(dyn::kRM));
+            if (!(old & dyn::kRM)) atomicAdd(&cnt->refineC, 1ull);
+        }
+    }
+}
+
+// amr.cpp:163-221: a refined cell with unrefined children erases when every
+// strictly interior child-block vertex is erase-marked and none of the block is
+// refine-marked, unless its h exceeds h_max
+template <int P>
+__global__ void k_dyn_erase_cells(const ALvl* __restrict__ lvs, int level, double h, double hMax, MarkCounters* cnt) {
+    const ALvl& c = lvs[level];
+    const ALvl& fl = lvs[level + 1];
+    constexpr int NB = P == 1 ? 4 : P == 2 ? 16 : 64;
+    constexpr int NT = P == 1 ? 3 : P == 2 ? 9 : 27;
+    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+        const unsigned char cfl = c.fcell[f];
+        if (!(cfl & amr::kCellExists) || !(cfl & amr::kCellRefined)) continue;
+        int g[P];
+        aunflat<P>(f, c, g);
+        int innerTotal = 0, innerMarked = 0;
+        bool anyRefine = false, childRefined = false;
+        for (int t = 0; t < NB; ++t) {
+            int vi[P];
+            bool inner = true;
+            int tt = t;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                const int rel = tt % 4;
+                tt /= 4;
+                vi[d] = 3 * g[d] + rel;
+                inner &= rel == 1 || rel == 2;
+            }
+            const int vf = aflat<P>(fl, vi);
+            if (vf < 0) continue;
+            const unsigned char vm = fl.vmark[vf];
+            if (vm & 1) anyRefine = true;
+            if (!inner) continue;
+            const unsigned char ff = fl.fflag[vf];
+            if (!(ff & amr::kExists) || (ff & (amr::kHanging | amr::kBoundary))) continue;
+            ++innerTotal;
+            if (vm & 2) ++innerMarked;
+        }
+        for (int t = 0; t < NT; ++t) {
+            int ci[P];
+            int tt = t;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                ci[d] = 3 * g[d] + tt % 3;
+                tt /= 3;
+            }
+            const int cf = aflat<P>(fl, ci);
+            if (cf >= 0 && (fl.fcell[cf] & amr::kCellRefined)) childRefined = true;
+        }
+        if (childRefined || anyRefine || innerTotal == 0 || innerMarked != innerTotal) continue;
+        if (h > hMax) {
+            atomicAdd(&cnt->vetoHMax, 1ull);
+            continue;
+        }
+        const unsigned old = atomicOr(&c.cmark[f], static_cast<unsigned>(dyn::kEM));
+        if (!(old & dyn::kEM)) atomicAdd(&cnt->eraseC, 1ull);
     }
 }
 
@@ -804,6 +1211,25 @@ struct AmrTree::Dev {
     double* hNorm = nullptr;  // pinned, 2 (L+1)
     double* weights = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // dynamic adaptivity: writable views of the per-level tables + staging
+    struct DynLevel {
+        unsigned char *vflag = nullptr, *cflag = nullptr, *estar = nullptr, *fmask = nullptr, *skip = nullptr,
+                      *fflag = nullptr, *fcell = nullptr;
+        signed char* succ = nullptr;
+        int* xoff = nullptr;
+        unsigned *list = nullptr, *slist = nullptr, *cmark = nullptr;
+        double2* extras = nullptr;
+        size_t extrasCap = 0;
+    };
+    std::vector<DynLevel> dl;
+    std::vector<std::array<double2, 9>> dgTab;
+    double2* dgDev = nullptr;  // dgTab per level on the device (k_dyn_special)
+    adev::ALvl* dLvs = nullptr;
+    adev::MarkCounters* dCnt = nullptr;
+    unsigned long long* dHist = nullptr;
+    std::vector<unsigned> hList, hSlist, hMark;
+    std::vector<int> hXoff;
+    std::vector<unsigned char> hFlag, hCell;
 
     ~Dev() {
         for (void* p : allocations) cudaFree(p);
@@ -822,6 +1248,19 @@ struct AmrTree::Dev {
 };
 
 namespace {
+// TMG_DYN_CHECK=1: synchronise and check after every dynamic-adaptivity kernel (debugging aid)
+void dyn_check(cudaStream_t s, const char* what, int level) {
+    static const bool on = [] {
+        const char* e = std::getenv("TMG_DYN_CHECK");
+        return e && e[0] == '1';
+    }();
+    if (!on) return;
+    const cudaError_t err = cudaStreamSynchronize(s);
+    if (err != cudaSuccess)
+        throw CudaError(std::string("CUDA error ") + cudaGetErrorString(err) + " after " + what + " at level " +
+                        std::to_string(level));
+}
+
 int blocks_for_n(long long n, int smCount) {
     const long long need = (n + 255) / 256;
     return static_cast<int>(std::max<long long>(1, std::min<long long>(need, 32LL * smCount)));
@@ -834,6 +1273,10 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
       smCount_(smCount), dev_(new Dev()), diag_(diagInterior) {
     dev_->kc = kc;
     if (prob.fast) throw UnsupportedConfigError("adaptive trees run in precision = exact only");
+    if (prob.dynStart > 0) {
+        init_dynamic();
+        return;
+    }
     if (base_ < 1) throw ConfigError("sphere refinement needs a base level >= 1");
     host_ = amr::build_sphere_tree(p_, base_, L_);
     amr::mark_regular_chi(host_, p_);
@@ -914,23 +1357,7 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
                              stream_));
     D.dNorm = D.alloc<double>(2 * (L_ + 1), stream_);
     AMR_CUDA(cudaMallocHost(&D.hNorm, 2 * (L_ + 1) * sizeof(double)));
-    {
-        // restriction_weight (cycles.cpp:46-50): per-axis 1/3, 2/3, 1 folded in axis order
-        const int NT = p_ == 1 ? 5 : p_ == 2 ? 25 : 125;
-        const double k1d[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
-        std::vector<double> w(NT);
-        for (int code = 0; code < NT; ++code) {
-            double wt = 1.0;
-            int cc = code;
-            for (int d = 0; d < p_; ++d) {
-                wt *= k1d[cc % 5];
-                cc /= 5;
-            }
-            w[code] = wt;
-        }
-        D.weights = D.alloc<double>(NT, stream_);
-        AMR_CUDA(cudaMemcpyAsync(D.weights, w.data(), NT * sizeof(double), cudaMemcpyHostToDevice, stream_));
-    }
+    upload_weights();
     AMR_CUDA(cudaEventCreate(&D.ev0));
     AMR_CUDA(cudaEventCreate(&D.ev1));
     if (p_ == 1) build_rhs<1>();
@@ -947,21 +1374,398 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
     AMR_CUDA(cudaStreamSynchronize(stream_));
 }
 
+void AmrTree::upload_weights() {
+    // restriction_weight (cycles.cpp:46-50): per-axis 1/3, 2/3, 1 folded in axis order
+    Dev& D = *dev_;
+    const int NT = p_ == 1 ? 5 : p_ == 2 ? 25 : 125;
+    const double k1d[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+    std::vector<double> w(NT);
+    for (int code = 0; code < NT; ++code) {
+        double wt = 1.0;
+        int cc = code;
+        for (int d = 0; d < p_; ++d) {
+            wt *= k1d[cc % 5];
+            cc /= 5;
+        }
+        w[code] = wt;
+    }
+    D.weights = D.alloc<double>(NT, stream_);
+    AMR_CUDA(cudaMemcpyAsync(D.weights, w.data(), NT * sizeof(double), cudaMemcpyHostToDevice, stream_));
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+}
+
 AmrTree::~AmrTree() = default;
+
+// ---- dynamic adaptivity (h_max / h_min) ---------------------------------------
+// Full-lattice levels 0..reference level; the structure is a dyn::DynTree on
+// the host, replayed once per sweep; the numerics stay on the device.
+void AmrTree::init_dynamic() {
+    Dev& D = *dev_;
+    const int Lmax = prob_.levels;
+    base_ = prob_.dynStart;
+    if (base_ < 1 || base_ > Lmax) throw ConfigError("dynamic adaptivity: bad start level");
+    dyn_ = std::make_unique<dyn::DynTree>(p_, base_, Lmax, prob_.ellMin, prob_.hMin, prob_.maxVertices);
+    L_ = dyn_->depth();
+    host_.assign(static_cast<size_t>(Lmax) + 1, amr::HostLevel{});
+    D.lv.resize(static_cast<size_t>(Lmax) + 1);
+    D.dl.resize(static_cast<size_t>(Lmax) + 1);
+    D.dgTab.resize(static_cast<size_t>(Lmax) + 1);
+    int blocksTotal = 0;
+    D.normOffs.assign(1, 0);
+    for (int l = 0; l <= Lmax; ++l) {
+        const dyn::Level& T = dyn_->level(l);
+        amr::HostLevel& h = host_[l];
+        h.level = l;
+        h.m = T.m;
+        for (int d = 0; d < 3; ++d) {
+            h.lo[d] = 0;
+            h.n1[d] = d < p_ ? T.n1 : 1;
+        }
+        h.n = T.n;
+        h.vflag.assign(static_cast<size_t>(h.n), 0);
+        h.cflag.assign(static_cast<size_t>(h.n), 0);
+        h.estar.assign(static_cast<size_t>(h.n), 0xFF);
+        h.succ.assign(static_cast<size_t>(h.n), 0);
+        adev::ALvl& a = D.lv[l];
+        a = adev::ALvl{};
+        a.level = l;
+        a.m = h.m;
+        for (int d = 0; d < 3; ++d) {
+            a.lo[d] = 0;
+            a.n1[d] = h.n1[d];
+        }
+        a.n = static_cast<unsigned>(h.n);
+        const size_t n = static_cast<size_t>(h.n);
+        a.u = D.alloc<double2>(n, stream_);
+        a.sc = D.alloc<double2>(n, stream_);
+        a.chi = D.alloc<double2>(n, stream_);
+        a.uhat = D.alloc<double2>(n, stream_);
+        a.rhat = D.alloc<double2>(n, stream_);
+        a.sf = D.alloc<double2>(n, stream_);
+        a.si = D.alloc<double2>(n, stream_);
+        a.sinext = D.alloc<double2>(n, stream_);
+        a.r = D.alloc<double2>(n, stream_);
+        a.dg = D.alloc<double2>(n, stream_);
+        a.nodal = D.alloc<double2>(n, stream_);  // any level can hold leaf cells (erase marks)
+        Dev::DynLevel& w = D.dl[l];
+        w.vflag = D.alloc<unsigned char>(n, stream_);
+        w.cflag = D.alloc<unsigned char>(n, stream_);
+        w.estar = D.alloc<unsigned char>(n, stream_);
+        w.fmask = D.alloc<unsigned char>(n, stream_);
+        w.skip = D.alloc<unsigned char>(n, stream_);
+        w.fflag = D.alloc<unsigned char>(n, stream_);
+        w.fcell = D.alloc<unsigned char>(n, stream_);
+        w.succ = D.alloc<signed char>(n, stream_);
+        w.xoff = D.alloc<int>(n, stream_);
+        w.list = D.alloc<unsigned>(n, stream_);
+        w.slist = D.alloc<unsigned>(n, stream_);
+        w.cmark = D.alloc<unsigned>(n, stream_);
+        a.vflag = w.vflag;
+        a.cflag = w.cflag;
+        a.estar = w.estar;
+        a.fmask = w.fmask;
+        a.skip = w.skip;
+        a.fflag = w.fflag;
+        a.fcell = w.fcell;
+        a.succ = w.succ;
+        a.xoff = w.xoff;
+        a.list = w.list;
+        a.slist = w.slist;
+        a.cmark = w.cmark;
+        a.feat = D.alloc<double>(n, stream_);
+        a.ind = D.alloc<double>(n, stream_);
+        a.vmark = D.alloc<unsigned char>(n, stream_);
+        // diag after k cells: zero_accumulators, then diag += A_aa per cell (cycles.cpp:205)
+        const double2 a0 = D.kc[l].A[0];
+        D.dgTab[l][0] = make_double2(0.0, 0.0);
+        Cplx acc(0.0);
+        for (int k = 1; k <= 8; ++k) {
+            acc += Cplx(a0.x, a0.y);
+            D.dgTab[l][k] = make_double2(acc.real(), acc.imag());
+        }
+        blocksTotal += blocks_for_n(h.n, smCount_);
+        D.normOffs.push_back(blocksTotal);
+    }
+    D.partials = D.alloc<double>(2 * static_cast<size_t>(blocksTotal), stream_);
+    D.dOffs = D.alloc<int>(D.normOffs.size(), stream_);
+    AMR_CUDA(cudaMemcpyAsync(D.dOffs, D.normOffs.data(), D.normOffs.size() * sizeof(int), cudaMemcpyHostToDevice,
+                             stream_));
+    D.dNorm = D.alloc<double>(2 * (static_cast<size_t>(Lmax) + 1), stream_);
+    AMR_CUDA(cudaMallocHost(&D.hNorm, 2 * (static_cast<size_t>(Lmax) + 1) * sizeof(double)));
+    D.dLvs = D.alloc<adev::ALvl>(static_cast<size_t>(Lmax) + 1, stream_);
+    D.dgDev = D.alloc<double2>(9 * (static_cast<size_t>(Lmax) + 1), stream_);
+    for (int l = 0; l <= Lmax; ++l)
+        AMR_CUDA(cudaMemcpyAsync(D.dgDev + 9 * l, D.dgTab[l].data(), 9 * sizeof(double2), cudaMemcpyHostToDevice,
+                                 stream_));
+    D.dCnt = D.alloc<adev::MarkCounters>(1, stream_);
+    D.dHist = D.alloc<unsigned long long>(64, stream_);
+    upload_weights();
+    AMR_CUDA(cudaEventCreate(&D.ev0));
+    AMR_CUDA(cudaEventCreate(&D.ev1));
+    // before the first sweep the tables are the regular tree's classification
+    upload_final_flags();
+    for (int l = 0; l <= Lmax; ++l) {
+        Dev::DynLevel& w = D.dl[l];
+        const size_t n = static_cast<size_t>(host_[l].n);
+        AMR_CUDA(cudaMemcpyAsync(w.vflag, w.fflag, n, cudaMemcpyDeviceToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.cflag, w.fcell, n, cudaMemcpyDeviceToDevice, stream_));
+        D.hList.clear();
+        for (long long f = 0; f < host_[l].n; ++f)
+            if (host_[l].vflag[f] & amr::kExists) D.hList.push_back(static_cast<unsigned>(f));
+        AMR_CUDA(cudaMemcpyAsync(w.list, D.hList.data(), D.hList.size() * sizeof(unsigned), cudaMemcpyHostToDevice,
+                                 stream_));
+        AMR_CUDA(cudaStreamSynchronize(stream_));
+        D.lv[l].nlist = static_cast<unsigned>(D.hList.size());
+        D.lv[l].nslist = 0;
+    }
+    if (p_ == 1) build_rhs<1>();
+    else if (p_ == 2) build_rhs<2>();
+    else build_rhs<3>();
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// classification after the sweep -> fflag / fcell (mark) and host_ (field API)
+void AmrTree::upload_final_flags() {
+    Dev& D = *dev_;
+    existingCount_ = hangingCount_ = leafCount_ = 0;
+    for (int l = 0; l <= dyn_->max_level(); ++l) {
+        const dyn::Level& T = dyn_->level(l);
+        amr::HostLevel& h = host_[l];
+        const bool live = l <= dyn_->depth();
+        for (long long f = 0; f < h.n; ++f) {
+            const unsigned char v = live ? static_cast<unsigned char>(T.vtx[f] & 31) : 0;
+            h.vflag[f] = v;
+            h.cflag[f] = live ? static_cast<unsigned char>(T.cell[f] & (dyn::kCE | dyn::kCR)) : 0;
+            h.succ[f] = T.succ[f];
+            if (!(v & amr::kExists)) continue;
+            ++existingCount_;
+            if (v & amr::kHanging) ++hangingCount_;
+            else if (!(v & amr::kRefined) && !(v & amr::kBoundary)) ++leafCount_;
+        }
+        const size_t n = static_cast<size_t>(h.n);
+        AMR_CUDA(cudaMemcpyAsync(D.dl[l].fflag, h.vflag.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(D.dl[l].fcell, h.cflag.data(), n, cudaMemcpyHostToDevice, stream_));
+    }
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// the sweep tables of dyn::DynTree::sweep -> device; vertex lists (regular
+// first), special list and the finish-value slots of the special vertices
+void AmrTree::upload_sweep_tables() {
+    Dev& D = *dev_;
+    L_ = dyn_->depth();
+    for (int l = 0; l <= dyn_->max_level(); ++l) {
+        adev::ALvl& a = D.lv[l];
+        Dev::DynLevel& w = D.dl[l];
+        if (l > L_) {
+            a.nlist = a.nslist = 0;
+            continue;
+        }
+        const dyn::Level& T = dyn_->level(l);
+        const size_t n = static_cast<size_t>(T.n);
+        AMR_CUDA(cudaMemcpyAsync(w.vflag, T.sflag.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.cflag, T.scell.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.estar, T.sestar.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.succ, T.ssucc.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.fmask, T.sfmask.data(), n, cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.skip, T.sskip.data(), n, cudaMemcpyHostToDevice, stream_));
+        D.hList.clear();
+        D.hSlist.clear();
+        D.hXoff.assign(n, 0);
+        size_t slots = 0;
+        for (int pass = 0; pass < 2; ++pass)
+            for (size_t f = 0; f < n; ++f) {
+                const unsigned char v = T.sflag[f];
+                if (!(v & dyn::kSE)) continue;
+                const bool regular = !(v & (dyn::kSH | dyn::kSB | dyn::kSSpecial));
+                if (regular == (pass == 0)) D.hList.push_back(static_cast<unsigned>(f));
+                if (pass == 0 && (v & dyn::kSSpecial)) {
+                    D.hSlist.push_back(static_cast<unsigned>(f));
+                    D.hXoff[f] = static_cast<int>(slots);
+                    slots += static_cast<size_t>(__builtin_popcount(T.sfmask[f]));
+                }
+            }
+        if (slots > w.extrasCap) {
+            if (w.extras) AMR_CUDA(cudaFree(w.extras));
+            w.extrasCap = std::max<size_t>(slots, 2 * w.extrasCap);
+            AMR_CUDA(cudaMalloc(&w.extras, w.extrasCap * sizeof(double2)));
+        }
+        a.extras = w.extras;
+        AMR_CUDA(cudaMemcpyAsync(w.list, D.hList.data(), D.hList.size() * sizeof(unsigned), cudaMemcpyHostToDevice,
+                                 stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.slist, D.hSlist.data(), D.hSlist.size() * sizeof(unsigned),
+                                 cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.xoff, D.hXoff.data(), n * sizeof(int), cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaStreamSynchronize(stream_));  // the staging vectors are reused per level
+        a.nlist = static_cast<unsigned>(D.hList.size());
+        a.nslist = static_cast<unsigned>(D.hSlist.size());
+    }
+}
+
+template <int P>
+void AmrTree::run_cycle_dyn(const Policy& pol, int n) {
+    Dev& D = *dev_;
+    const int bpx = pol.bpx ? 1 : 0;
+    for (int l = 0; l <= L_; ++l) {
+        const adev::ALvl& pr = l > 0 ? D.lv[l - 1] : D.lv[0];
+        if (D.lv[l].nlist)
+            adev::k_amr_topdown<P><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
+        dyn_check(stream_, "k_amr_topdown", l);
+    }
+    AMR_CUDA(cudaMemsetAsync(D.partials, 0, 2 * sizeof(double) * static_cast<size_t>(D.normOffs.back()), stream_));
+    adev::AResArgs a{};
+    a.ellMin = prob_.ellMin;
+    a.bpx = bpx;
+    a.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+    for (int s = 0; s < 12; ++s) {
+        const Cplx w = omega_unmasked(pol, s, n);
+        a.wTab[s] = make_double2(w.real(), w.imag());
+    }
+    for (int l = L_; l >= 0; --l) {
+        const adev::ALvl& c = D.lv[l];
+        if (!c.nlist) continue;
+        const int nb = blocks_for_n(c.nlist, smCount_);
+        const adev::ALvl& fine = l < L_ ? D.lv[l + 1] : D.lv[l];
+        const int restrictOn = (l < L_ && l + 1 > prob_.ellMin) ? 1 : 0;
+        adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(c, fine, D.kc[l], D.weights, restrictOn);
+        dyn_check(stream_, "k_amr_chi", l);
+        if (c.nslist) {
+            adev::k_dyn_special<P><<<blocks_for_n(c.nslist, smCount_), 256, 0, stream_>>>(
+                c, fine, D.kc[l], D.weights, restrictOn, prob_.ellMin, D.dgDev + 9 * l);
+            dyn_check(stream_, "k_dyn_special", l);
+        }
+        a.lv = c;
+        a.par = l > 0 ? D.lv[l - 1] : D.lv[0];
+        a.k = D.kc[l];
+        for (int k = 0; k < 9; ++k) a.dgTab[k] = D.dgTab[l][k];
+        a.partials = D.partials + 2 * static_cast<size_t>(D.normOffs[l]);
+        adev::k_amr_residual<P><<<nb, 256, 0, stream_>>>(a);
+        dyn_check(stream_, "k_amr_residual", l);
+    }
+    adev::k_amr_norm_final<<<1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
+    AMR_CUDA(cudaGetLastError());
+}
+
+namespace {
+// select_bins, amr.cpp:43-59
+int select_bins(const std::vector<unsigned long long>& hist, unsigned long long total, double goal, bool fromTop) {
+    const int bins = static_cast<int>(hist.size());
+    int best = 0;
+    double bestDist = goal;
+    unsigned long long cum = 0;
+    for (int k = 1; k <= bins; ++k) {
+        const int b = fromTop ? bins - k : k - 1;
+        cum += hist[static_cast<size_t>(b)];
+        const double dist = std::abs(static_cast<double>(cum) / static_cast<double>(total) - goal);
+        if (dist < bestDist - 1e-15) {
+            bestDist = dist;
+            best = k;
+        }
+    }
+    return best;
+}
+}  // namespace
+
+template <int P>
+AmrMarkStats AmrTree::mark_dyn() {
+    Dev& D = *dev_;
+    // AmrConfig defaults (amr.hpp:7-15) with the run's h_max / h_min
+    constexpr int kBins = 20;
+    constexpr double kRefineFraction = 0.10, kEraseFraction = 0.02, kVeto = 1e-2;
+    adev::MarkCounters zero{};
+    zero.sMinBits = ~0ull;
+    AMR_CUDA(cudaMemcpyAsync(D.dCnt, &zero, sizeof(zero), cudaMemcpyHostToDevice, stream_));
+    AMR_CUDA(cudaMemcpyAsync(D.dLvs, D.lv.data(), D.lv.size() * sizeof(adev::ALvl), cudaMemcpyHostToDevice, stream_));
+    for (int l = 0; l <= L_; ++l)
+        adev::k_dyn_features<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(
+            D.dLvs, l, l >= prob_.ellMin ? 1 : 0, D.dCnt);
+    dyn_check(stream_, "k_dyn_features", L_);
+    adev::MarkCounters cnt{};
+    AMR_CUDA(cudaMemcpyAsync(&cnt, D.dCnt, sizeof(cnt), cudaMemcpyDeviceToHost, stream_));
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+    if (cnt.cand > 0) {
+        double smin, smax;
+        std::memcpy(&smin, &cnt.sMinBits, 8);
+        std::memcpy(&smax, &cnt.sMaxBits, 8);
+        const double span = smax - smin;
+        if (span > 0.0) {
+            AMR_CUDA(cudaMemsetAsync(D.dHist, 0, kBins * sizeof(unsigned long long), stream_));
+            for (int l = 0; l <= L_; ++l)
+                adev::k_dyn_hist<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(D.dLvs, l, smin, span,
+                                                                                          kBins, D.dHist);
+            std::vector<unsigned long long> hist(kBins);
+            AMR_CUDA(cudaMemcpyAsync(hist.data(), D.dHist, kBins * sizeof(unsigned long long), cudaMemcpyDeviceToHost,
+                                     stream_));
+            AMR_CUDA(cudaStreamSynchronize(stream_));
+            const int kRef = select_bins(hist, cnt.cand, kRefineFraction, true);
+            const int kErase = select_bins(hist, cnt.cand, kEraseFraction, false);
+            for (int l = 0; l <= L_; ++l)
+                adev::k_dyn_classify<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(
+                    D.dLvs, l, smin, span, kBins, kRef, kErase, kVeto, D.dCnt);
+        }
+    }
+    for (int l = 0; l <= L_; ++l) {
+        AMR_CUDA(cudaMemsetAsync(D.dl[l].cmark, 0, static_cast<size_t>(D.lv[l].n) * sizeof(unsigned), stream_));
+        adev::k_dyn_refine_cells<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(
+            D.dLvs, l, std::pow(3.0, -l), prob_.hMin, D.dCnt);
+        dyn_check(stream_, "k_dyn_refine_cells", l);
+    }
+    for (int l = std::max(0, prob_.ellMin); l < L_; ++l)
+        adev::k_dyn_erase_cells<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(
+            D.dLvs, l, std::pow(3.0, -l), prob_.hMax, D.dCnt);
+    dyn_check(stream_, "k_dyn_erase_cells", L_);
+    AMR_CUDA(cudaGetLastError());
+    AMR_CUDA(cudaMemcpyAsync(&cnt, D.dCnt, sizeof(cnt), cudaMemcpyDeviceToHost, stream_));
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+    for (int l = 0; l <= L_; ++l) {  // the cell marks take effect in the next traversal
+        dyn::Level& T = dyn_->level(l);
+        D.hMark.resize(static_cast<size_t>(T.n));
+        AMR_CUDA(cudaMemcpy(D.hMark.data(), D.dl[l].cmark, D.hMark.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
+        for (long long f = 0; f < T.n; ++f)
+            if (T.cell[f] & dyn::kCE) T.cell[f] = static_cast<unsigned char>(T.cell[f] | (D.hMark[f] & (dyn::kRM | dyn::kEM)));
+    }
+    AmrMarkStats st;
+    st.refineVertices = static_cast<long long>(cnt.refineV);
+    st.eraseVertices = static_cast<long long>(cnt.eraseV);
+    st.refineCells = static_cast<long long>(cnt.refineC);
+    st.eraseCells = static_cast<long long>(cnt.eraseC);
+    st.vetoConvergence = static_cast<long long>(cnt.vetoConv);
+    st.vetoHMin = static_cast<long long>(cnt.vetoHMin);
+    st.vetoHMax = static_cast<long long>(cnt.vetoHMax);
+    return st;
+}
+
+void AmrTree::set_cell_marks(int level, const unsigned char* cells) {
+    if (!dyn_) throw UnsupportedConfigError("set_cell_marks: the tree is not dynamically adaptive (h_max / h_min)");
+    if (level < 0 || level > dyn_->max_level()) throw ConfigError("set_cell_marks: level out of range");
+    dyn::Level& T = dyn_->level(level);
+    const unsigned char mk = dyn::kRM | dyn::kEM;
+    for (long long f = 0; f < T.n; ++f)
+        if (T.cell[f] & dyn::kCE) T.cell[f] = static_cast<unsigned char>((T.cell[f] & ~mk) | (cells[f] & mk));
+}
+
+AmrMarkStats AmrTree::mark() {
+    if (!dyn_) throw UnsupportedConfigError("mark: the tree is not dynamically adaptive (h_max / h_min)");
+    if (p_ == 1) return mark_dyn<1>();
+    if (p_ == 2) return mark_dyn<2>();
+    return mark_dyn<3>();
+}
 
 template <int P>
 void AmrTree::build_rhs() {
     Dev& D = *dev_;
-    for (int l = base_; l <= L_; ++l) {
+    const int top = static_cast<int>(host_.size()) - 1;  // static: L_; dynamic: the reference level
+    for (int l = dyn_ ? 0 : base_; l <= top; ++l) {
         adev::ALvl& a = D.lv[l];
         const amr::HostLevel& h = host_[l];
         if (prob_.chi == ChiKind::Seeded) {
-            const int key = prob_.rhsLattice >= 0 ? prob_.rhsLattice : L_;
+            const int key = prob_.rhsLattice >= 0 ? prob_.rhsLattice : top;
             long long scale = 1, mkey = 1;
             for (int i = 0; i < key - l; ++i) scale *= 3;
             for (int i = 0; i < key; ++i) mkey *= 3;
             adev::k_amr_seeded<P><<<blocks_for_n(h.n, smCount_), 256, 0, stream_>>>(a, prob_.rhsSeed, scale, mkey,
-                                                                                    prob_.rhsSphere ? 1 : 0);
+                                                                                    prob_.rhsSphere ? 1 : 0,
+                                                                                    dyn_ ? 1 : 0);
             AMR_CUDA(cudaGetLastError());
             continue;
         }
@@ -970,7 +1774,7 @@ void AmrTree::build_rhs() {
         const double hh = std::pow(3.0, -l);
         int g[3] = {0, 0, 0};
         for (long long f = 0; f < h.n; ++f) {
-            if (!(h.vflag[f] & amr::kExists)) continue;
+            if (!dyn_ && !(h.vflag[f] & amr::kExists)) continue;
             long long ff = f;
             double x[3];
             for (int d = 0; d < p_; ++d) {
@@ -1027,9 +1831,18 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
 }
 
 SweepStats AmrTree::cycle(const Policy& pol, int n) {
+    if (dyn_) {
+        lastCounts_ = dyn_->sweep();  // the traversal's structural edits, replayed on the host
+        upload_sweep_tables();
+    }
     for (int l = std::max(1, prob_.ellMin); l <= L_; ++l)
         if (std::abs(diag_[l]) < 1e-300) throw SingularDiagonalError("vanishing operator diagonal (phi*h^2 resonance?)");
-    if (p_ == 1) run_cycle<1>(pol, n);
+    if (dyn_) {
+        if (p_ == 1) run_cycle_dyn<1>(pol, n);
+        else if (p_ == 2) run_cycle_dyn<2>(pol, n);
+        else run_cycle_dyn<3>(pol, n);
+        upload_final_flags();
+    } else if (p_ == 1) run_cycle<1>(pol, n);
     else if (p_ == 2) run_cycle<2>(pol, n);
     else run_cycle<3>(pol, n);
     Dev& D = *dev_;
@@ -1047,6 +1860,11 @@ SweepStats AmrTree::cycle(const Policy& pol, int n) {
     st.euclidNorm = std::sqrt(eu);
     st.hNorm = std::sqrt(hn);
     st.updatedFineVertices = leafCount_;
+    if (dyn_) {
+        st.updatedFineVertices = lastCounts_.updatedFineVertices;
+        st.refinedCells = lastCounts_.refinedCells;
+        st.erasedCells = lastCounts_.erasedCells;
+    }
     return st;
 }
 

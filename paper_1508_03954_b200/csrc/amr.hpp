@@ -28,6 +28,7 @@
 #include <string>
 #include <vector>
 
+#include "dyn.hpp"
 #include "hierarchy.hpp"
 
 namespace tmg {
@@ -75,6 +76,11 @@ class AmrTree {
     ~AmrTree();
 
     SweepStats cycle(const Policy& pol, int n);
+    // dynamic adaptivity (prob.dynStart > 0): MarkStats of amr.cpp:61-222 on the device
+    AmrMarkStats mark();
+    bool dynamic() const { return dyn_ != nullptr; }
+    // overwrite the pending cell marks of `level` (4 refineMark, 8 eraseMark per lattice cell)
+    void set_cell_marks(int level, const unsigned char* cells);
     int levels() const { return L_; }
     long long leaf_vertices() const { return leafCount_; }
     long long existing_vertices() const { return existingCount_; }
@@ -96,6 +102,15 @@ class AmrTree {
     template <int P>
     void run_cycle(const Policy& pol, int n);
     template <int P>
+    void run_cycle_dyn(const Policy& pol, int n);
+    template <int P>
+    AmrMarkStats mark_dyn();
+    void init_dynamic();
+    void upload_weights();
+    void upload_sweep_tables();
+    void upload_final_flags();
+    void refresh_counts();
+    template <int P>
     void build_rhs();
 
     Problem prob_;
@@ -103,6 +118,8 @@ class AmrTree {
     cudaStream_t stream_;
     int smCount_;
     std::vector<amr::HostLevel> host_;
+    std::unique_ptr<dyn::DynTree> dyn_;  // dynamic adaptivity: the structure, replayed per sweep
+    dyn::SweepCounts lastCounts_;
     std::unique_ptr<Dev> dev_;  // device arrays + the per-level exact constants
     std::vector<Cplx> diag_;
     long long leafCount_ = 0, existingCount_ = 0, hangingCount_ = 0;

@@ -10,6 +10,7 @@
 #include "../../include/treemg.h"
 #include "../../include/treemg_b200.h"
 #include "amr.hpp"
+#include "dyn.hpp"
 #include "runner.hpp"
 
 using namespace tmg;
@@ -207,6 +208,20 @@ Problem problem_from(const tmg_problem* prob) {
     p.levels += p.sphereLevels;
     p.channels = prob->channels > 0 ? prob->channels : 1;
     p.coupling = Cplx(prob->coupling_re, prob->coupling_im);
+    if (prob->h_max > 0.0 || prob->h_min > 0.0) {  // dynamic adaptivity: levels from h_max / h_min
+        RunConfig rc;
+        rc.fixedLevel = 0;
+        rc.hMax = prob->h_max;
+        rc.hMin = prob->h_min;
+        rc.ellMin = prob->ell_min;
+        if (!(rc.hMax > 0.0 && rc.hMin > 0.0 && rc.hMin <= rc.hMax))
+            throw ConfigError("adaptive runs need 0 < h_min <= h_max");
+        p.dynStart = start_level_of(rc);
+        p.levels = std::max(p.dynStart, std::min(reference_level_of(rc), 9));
+        p.hMax = rc.hMax;
+        p.hMin = rc.hMin;
+        p.rhsLattice = reference_level_of(rc);
+    }
     if (p.ellMin < 1) throw ConfigError("ellMin must be >= 1");
     return p;
 }
@@ -404,6 +419,88 @@ treemg_status tmg_sphere_tree(int dim, int base, int sphere_levels, int level, u
     });
 }
 
+struct tmg_dyn {
+    std::unique_ptr<dyn::DynTree> t;
+};
+
+treemg_status tmg_dyn_create(int dim, int start, int max_level, int ell_min, double h_min, long long max_vertices,
+                             tmg_dyn** out) {
+    if (!out) return fail(TREEMG_E_USAGE, "null argument");
+    *out = nullptr;
+    auto* h = new tmg_dyn();
+    const treemg_status st = guarded([&] {
+        h->t = std::make_unique<dyn::DynTree>(dim, start, max_level, ell_min, h_min,
+                                              static_cast<std::size_t>(max_vertices > 0 ? max_vertices : 8388608));
+    });
+    if (st != TREEMG_OK) {
+        delete h;
+        return st;
+    }
+    *out = h;
+    return TREEMG_OK;
+}
+
+void tmg_dyn_destroy(tmg_dyn* h) { delete h; }
+
+int tmg_dyn_depth(const tmg_dyn* h) { return h ? h->t->depth() : -1; }
+
+long long tmg_dyn_interior_count(const tmg_dyn* h) { return h ? h->t->interior_fine_vertex_count() : -1; }
+
+treemg_status tmg_dyn_set_cell_marks(tmg_dyn* h, int level, const unsigned char* cells) {
+    if (!h || !cells) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        if (level < 0 || level > h->t->max_level()) throw ConfigError("tmg_dyn_set_cell_marks: level out of range");
+        dyn::Level& L = h->t->level(level);
+        const unsigned char mk = dyn::kRM | dyn::kEM;
+        for (long long f = 0; f < L.n; ++f)
+            L.cell[f] = static_cast<unsigned char>((L.cell[f] & ~mk) | ((L.cell[f] & dyn::kCE) ? (cells[f] & mk) : 0));
+    });
+}
+
+treemg_status tmg_dyn_sweep(tmg_dyn* h, long long* out4) {
+    if (!h) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        const dyn::SweepCounts c = h->t->sweep();
+        if (out4) {
+            out4[0] = c.refinedCells;
+            out4[1] = c.erasedCells;
+            out4[2] = c.updatedFineVertices;
+            out4[3] = c.specialVertices;
+        }
+    });
+}
+
+treemg_status tmg_dyn_flags(tmg_dyn* h, int level, unsigned char* flags, signed char* succ, unsigned char* cells) {
+    if (!h) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        if (level < 0 || level > h->t->max_level()) throw ConfigError("tmg_dyn_flags: level out of range");
+        const dyn::Level& L = h->t->level(level);
+        for (long long f = 0; f < L.n; ++f) {
+            const bool ex = level <= h->t->depth() && (L.vtx[f] & dyn::kVE);
+            if (flags) flags[f] = ex ? L.vtx[f] : 0;
+            if (succ) succ[f] = ex ? L.succ[f] : static_cast<signed char>(-1);
+            if (cells) cells[f] = level <= h->t->depth() ? L.cell[f] : 0;
+        }
+    });
+}
+
+treemg_status tmg_dyn_sweep_tables(tmg_dyn* h, int level, unsigned char* role, unsigned char* finish_corner,
+                                   unsigned char* finish_cells, unsigned char* skip_cells, signed char* succ,
+                                   unsigned char* cells) {
+    if (!h) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        if (level < 0 || level > h->t->max_level()) throw ConfigError("tmg_dyn_sweep_tables: level out of range");
+        const dyn::Level& L = h->t->level(level);
+        const size_t n = static_cast<size_t>(L.n);
+        if (role) std::copy(L.sflag.begin(), L.sflag.end(), role);
+        if (finish_corner) std::copy(L.sestar.begin(), L.sestar.end(), finish_corner);
+        if (finish_cells) std::copy(L.sfmask.begin(), L.sfmask.end(), finish_cells);
+        if (skip_cells) std::copy(L.sskip.begin(), L.sskip.end(), skip_cells);
+        if (succ) std::copy(L.ssucc.begin(), L.ssucc.end(), succ);
+        if (cells) std::copy(L.scell.begin(), L.scell.begin() + static_cast<long long>(n), cells);
+    });
+}
+
 long long tmg_hanging_vertices(const tmg_hierarchy* h) { return h ? h->h->hanging_vertices() : 0; }
 
 long long tmg_leaf_vertices(const tmg_hierarchy* h) { return h ? h->h->interior_fine_vertices() : 0; }
@@ -424,6 +521,25 @@ treemg_status tmg_time_cycles(tmg_hierarchy* h, const tmg_policy* pol, int n0, i
 treemg_status tmg_e2e_step(tmg_hierarchy* h, const tmg_policy* pol, int n, const double* chi, double* out3) {
     if (!h || !pol || !chi || !out3) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] { h->h->e2e_step(policy_from(pol), n, chi, out3); });
+}
+
+treemg_status tmg_mark(tmg_hierarchy* h, long long* out9) {
+    if (!h) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        const AmrMarkStats m = h->h->mark();
+        if (out9) {
+            const long long v[9] = {h->last.refinedCells, h->last.erasedCells, m.refineVertices, m.eraseVertices,
+                                    m.refineCells, m.eraseCells, m.vetoConvergence, m.vetoHMin, m.vetoHMax};
+            std::copy(v, v + 9, out9);
+        }
+    });
+}
+
+int tmg_levels(const tmg_hierarchy* h) { return h ? h->h->levels() : -1; }
+
+treemg_status tmg_set_cell_marks(tmg_hierarchy* h, int level, const unsigned char* cells) {
+    if (!h || !cells) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { h->h->set_cell_marks(level, cells); });
 }
 
 int tmg_channel_norms(tmg_hierarchy* h, double* maxNorm, double* euclid, double* hNorm, int cap) {

@@ -1425,11 +1425,12 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     if (prob.levels < 1) throw ConfigError("build_regular needs levels >= 1");
     if (prob.levels > 9) throw ConfigError("tree depth exceeds supported maximum");
     if (prob.sphereLevels < 0 || prob.sphereLevels >= prob.levels) throw ConfigError("sphere_levels out of range");
-    if (prob.channels > 1 && (prob.sphereLevels > 0 || prob.hostNorms))
+    if (prob.channels > 1 && (prob.sphereLevels > 0 || prob.dynStart > 0 || prob.hostNorms))
         throw UnsupportedConfigError("B200 path: several channels run on regular trees with device norms");
     // build_regular's capacity estimate (spacetree.cpp:53-63)
     std::size_t estimate = 0;
-    for (int l = 0; l <= prob.levels - prob.sphereLevels; ++l) {
+    const int regularTop = prob.dynStart > 0 ? prob.dynStart : prob.levels - prob.sphereLevels;
+    for (int l = 0; l <= regularTop; ++l) {
         std::size_t perAxis = static_cast<std::size_t>(pow3i(l)) + 1, n = 1;
         for (int d = 0; d < prob.dim; ++d) n *= perAxis;
         estimate += n;
@@ -1446,7 +1447,7 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     TMG_CUDA(cudaEventCreate(&I.ev1));
     TMG_CUDA(cudaEventCreate(&I.evf0));
     TMG_CUDA(cudaEventCreate(&I.evf1));
-    if (prob.sphereLevels > 0) {
+    if (prob.sphereLevels > 0 || prob.dynStart > 0) {
         if (prob.hostNorms) throw UnsupportedConfigError("norms = host is not available on adaptive trees");
         I.compute_level_constants();
         I.amr = std::make_unique<AmrTree>(prob, I.kc, I.diagInterior, I.stream, I.smCount);
@@ -1632,7 +1633,17 @@ SweepStats Hierarchy::textbook_add(Cplx omegaS, Cplx omegaCG) {
 }
 
 int Hierarchy::dim() const { return impl_->p; }
-int Hierarchy::levels() const { return impl_->L; }
+int Hierarchy::levels() const { return impl_->amr ? impl_->amr->levels() : impl_->L; }
+
+void Hierarchy::set_cell_marks(int level, const unsigned char* cells) {
+    if (!impl_->amr) throw UnsupportedConfigError("set_cell_marks: the tree is not dynamically adaptive");
+    impl_->amr->set_cell_marks(level, cells);
+}
+
+AmrMarkStats Hierarchy::mark() {
+    if (!impl_->amr) throw UnsupportedConfigError("mark: the tree is not dynamically adaptive (h_max / h_min)");
+    return impl_->amr->mark();
+}
 
 long long Hierarchy::lattice_size(int level) const {
     if (level < 0 || level > impl_->L) return 0;

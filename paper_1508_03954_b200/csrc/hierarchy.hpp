@@ -67,6 +67,10 @@ struct Problem {
     int channels = 1;        // unknowns per vertex (kernels.cpp:33-66; exact precision for > 1)
     Cplx coupling = Cplx(0.0);  // A_ij for i != j (runner.cpp:152-157)
     int sphereLevels = 0;    // static adaptive tree: levels-sphereLevels regular, refined inside |x-1/2|^2<0.04
+    // dynamic adaptivity (h_max / h_min runs, runner.cpp:206-366): dynStart > 0 builds the regular
+    // tree of that depth; levels is the reference level (level_for_h(h_min)), the deepest refinement
+    int dynStart = 0;
+    double hMax = 0.0, hMin = 0.0;
     std::size_t maxVertices = 8u * 1024u * 1024u;
     int device = 0;
 };
@@ -74,7 +78,13 @@ struct Problem {
 struct SweepStats {  // SweepStats, cycles.hpp:37-45
     double maxNorm = 0.0, euclidNorm = 0.0, hNorm = 0.0;  // aggregated over channels (runner.cpp:68-77)
     long long updatedFineVertices = 0;
+    int refinedCells = 0, erasedCells = 0;  // dynamic adaptivity: structural edits of the sweep
     std::vector<double> chMax, chEuclid, chH;  // per channel (channels > 1)
+};
+
+struct AmrMarkStats {  // MarkStats, amr.hpp:19-27
+    long long refineVertices = 0, eraseVertices = 0, refineCells = 0, eraseCells = 0;
+    long long vetoConvergence = 0, vetoHMin = 0, vetoHMax = 0;
 };
 
 // omega_unmasked, proj/src/cycles.cpp:11-31 (host, same libstdc++ arithmetic)
@@ -95,8 +105,14 @@ class Hierarchy {
     SweepStats bu_fas(const Policy& pol, int n);
     SweepStats textbook_add(Cplx omegaS, Cplx omegaCG);
 
+    // Dynamic adaptivity: mark (amr.cpp:61-222) on the device after a sweep; the
+    // marks take effect in the next cycle (refine on descent, erase on backtracking).
+    AmrMarkStats mark();
+    // overwrite the pending cell marks of a dynamically adaptive tree (4 refine, 8 erase per lattice cell)
+    void set_cell_marks(int level, const unsigned char* cells);
+
     int dim() const;
-    int levels() const;
+    int levels() const;  // current depth (grows under dynamic adaptivity)
     long long lattice_size(int level) const;
     long long interior_fine_vertices() const;
     // adaptive trees: flags byte / succ per lattice point (amr.hpp); false if regular
