@@ -222,6 +222,9 @@ treemg_status tmg_slab_plan(int levels, int world, int* out8);
 /* Test hook: out = x / y elementwise (interleaved complex, host buffers) on
  * the device with the kernels' restatement of libgcc __divdc3. */
 treemg_status tmg_test_divdc3(const double* x, const double* y, double* out, long long n);
+/* Test hook: the device's restatement of the host libm hypot (glibc, Borges' algorithm with
+ * the non-FMA correction) that the dynamic-adaptivity features use for std::abs(complex). */
+treemg_status tmg_test_hypot(const double* x, const double* y, double* out, long long n);
 
 #ifdef __cplusplus
 }

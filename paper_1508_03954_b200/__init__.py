@@ -45,7 +45,7 @@ EXTENSION_SYMBOLS = [
     "tmg_hierarchy_create", "tmg_hierarchy_destroy", "tmg_td_add", "tmg_td_bpx", "tmg_lattice_size",
     "tmg_get_field", "tmg_set_field", "tmg_set_fine_interior_u", "tmg_set_random_initial_guess",
     "tmg_set_fine_rhs", "tmg_field_hash", "tmg_time_cycles", "tmg_e2e_step", "tmg_last_error",
-    "treemg_result_fingerprint", "tmg_test_divdc3", "tmg_nccl_unique_id", "tmg_slabs_create", "tmg_slabs_destroy",
+    "treemg_result_fingerprint", "tmg_test_divdc3", "tmg_test_hypot", "tmg_nccl_unique_id", "tmg_slabs_create", "tmg_slabs_destroy",
     "tmg_slabs_cycle", "tmg_slabs_get_fine_u", "tmg_slabs_time_cycles", "tmg_slabs_owned_planes", "tmg_slab_plan",
     "tmg_slabs_e2e_step", "tmg_get_flags", "tmg_hanging_vertices", "tmg_leaf_vertices", "tmg_sphere_tree",
     "tmg_bu_fas", "tmg_textbook_add", "tmg_channel_norms", "tmg_dyn_create", "tmg_dyn_destroy", "tmg_dyn_depth",
@@ -179,6 +179,8 @@ def lib():
         L.tmg_time_cycles.argtypes = [vp, ctypes.POINTER(_Policy), ip, ip, ip, pd]
         L.treemg_result_fingerprint.restype = ctypes.c_ulonglong
         L.treemg_result_fingerprint.argtypes = [vp, cp]
+        L.tmg_test_hypot.restype = ip
+        L.tmg_test_hypot.argtypes = [pd, pd, pd, ctypes.c_longlong]
         L.tmg_test_divdc3.restype = ip
         L.tmg_test_divdc3.argtypes = [pd, pd, pd, ctypes.c_longlong]
         L.tmg_nccl_unique_id.restype = ip
@@ -512,6 +514,15 @@ def device_divide(x: np.ndarray, y: np.ndarray) -> np.ndarray:
     y = np.ascontiguousarray(y, dtype=np.complex128)
     out = np.zeros_like(x)
     _check(lib().tmg_test_divdc3(_pd(x.view(np.float64)), _pd(y.view(np.float64)), _pd(out.view(np.float64)), len(x)))
+    return out
+
+
+def device_hypot(x: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """hypot(x, y) on the device with the mark pass's libm restatement (test hook)."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    out = np.zeros_like(x)
+    _check(lib().tmg_test_hypot(_pd(x), _pd(y), _pd(out), len(x)))
     return out
 
 

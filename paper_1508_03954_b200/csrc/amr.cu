@@ -918,7 +918,28 @@ __global__ void k_dyn_erase_cells(const ALvl* __restrict__ lvs, int level, doubl
     }
 }
 
+__global__ void k_test_hypot(const double* x, const double* y, double* out, long long n) {
+    for (long long i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = host_hypot(x[i], y[i]);
+}
+
 }  // namespace adev
+
+void test_hypot(const double* x, const double* y, double* out, long long n) {
+    double *dx = nullptr, *dy = nullptr, *dout = nullptr;
+    const size_t bytes = static_cast<size_t>(std::max<long long>(n, 1)) * sizeof(double);
+    AMR_CUDA(cudaMalloc(&dx, bytes));
+    AMR_CUDA(cudaMalloc(&dy, bytes));
+    AMR_CUDA(cudaMalloc(&dout, bytes));
+    AMR_CUDA(cudaMemcpy(dx, x, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice));
+    AMR_CUDA(cudaMemcpy(dy, y, static_cast<size_t>(n) * sizeof(double), cudaMemcpyHostToDevice));
+    adev::k_test_hypot<<<256, 256>>>(dx, dy, dout, n);
+    AMR_CUDA(cudaGetLastError());
+    AMR_CUDA(cudaMemcpy(out, dout, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToHost));
+    cudaFree(dx);
+    cudaFree(dy);
+    cudaFree(dout);
+}
 
 // ============================================================================
 // Host: tree structure

@@ -184,6 +184,11 @@ unsigned long long treemg_result_fingerprint(const treemg_result* res, const cha
     return 0;
 }
 
+treemg_status tmg_test_hypot(const double* x, const double* y, double* out, long long n) {
+    if (!x || !y || !out || n < 0) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] { test_hypot(x, y, out, n); });
+}
+
 treemg_status tmg_test_divdc3(const double* x, const double* y, double* out, long long n) {
     if (!x || !y || !out || n < 0) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] { test_divdc3(x, y, out, n); });

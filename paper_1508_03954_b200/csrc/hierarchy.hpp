@@ -176,5 +176,7 @@ bool nccl_unique_id(void* out128);
 // Test hook: x / y elementwise on the device with the kernels' __divdc3
 // restatement (per-element divisor constants); host buffers.
 void test_divdc3(const double* x, const double* y, double* out, long long n);
+// |x + iy| on the device as the host libm's hypot computes it (dynamic adaptivity's mark features)
+void test_hypot(const double* x, const double* y, double* out, long long n);
 
 }  // namespace tmg

@@ -116,6 +116,19 @@ CONFIGS = {
                                target_drop=1e-8, **SEEDED),
     "mc2_random_2d": dict(problem="poisson-sin", dim=2, level=3, channels=2, coupling="4,0", initial="random",
                           seed=7, omega="exponential", omega_s=0.8, max_sweeps=30, target_drop=1e-8, norm="h"),
+    # dynamic adaptivity: h_max / h_min runs, marks after every sweep
+    "dyn_h2d": dict(problem="helmholtz-sin", dim=2, phi="100,50", h_max=0.04, h_min=0.004, cycle="td-add",
+                    omega="undamped", omega_s=0.6, max_sweeps=14, target_drop=1e-8),
+    "dyn_p2d_bpx": dict(problem="poisson-sin", dim=2, h_max=0.04, h_min=0.002, cycle="td-bpx", omega="undamped",
+                        omega_s=0.5, max_sweeps=12, target_drop=1e-8),
+    "dyn_p3d": dict(problem="poisson-sin", dim=3, h_max=0.12, h_min=0.013, cycle="td-add", omega="undamped",
+                    omega_s=0.6, max_sweeps=12, target_drop=1e-8),
+    "dyn_b2d_seeded": dict(problem="helmholtz-ball", dim=2, h_max=0.12, h_min=0.0014, theta_deg=20,
+                           omega="exponential", omega_s=0.8, max_sweeps=12, target_drop=1e-8, rhs="seeded",
+                           rhs_seed=99),
+    # proj/tests/test_amr.cpp:172-190 (adaptive runs are deterministic)
+    "dyn_p2d_transition": dict(problem="poisson-sin", dim=2, cycle="td-add", omega="transition", h_max=1.0 / 9.0,
+                               h_min=1.0 / 81.0, max_sweeps=12, target_drop=1e-30),
 }
 
 
