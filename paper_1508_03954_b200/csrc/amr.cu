@@ -14,6 +14,8 @@
 #include <cmath>
 #include <cstring>
 #include <array>
+#include <chrono>
+#include <cstdio>
 #include <thread>
 
 #include "exact_ops.cuh"
@@ -1417,6 +1419,32 @@ void AmrTree::upload_weights() {
 
 AmrTree::~AmrTree() = default;
 
+namespace {
+// TMG_DYN_PROFILE=1: per-sweep wall-clock breakdown of dynamic adaptivity on stderr
+struct DynProfile {
+    bool on = false;
+    std::chrono::steady_clock::time_point t;
+    DynProfile() {
+        const char* e = std::getenv("TMG_DYN_PROFILE");
+        on = e && e[0] == '1';
+    }
+    void start() {
+        if (on) t = std::chrono::steady_clock::now();
+    }
+    void lap(const char* what) {
+        if (!on) return;
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, " %s %.2fms", what, std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+DynProfile& dyn_profile() {
+    static DynProfile p;
+    return p;
+}
+}  // namespace
+
+
 // ---- dynamic adaptivity (h_max / h_min) ---------------------------------------
 // Full-lattice levels 0..reference level; the structure is a dyn::DynTree on
 // the host, replayed once per sweep; the numerics stay on the device.
@@ -1767,9 +1795,12 @@ void AmrTree::set_cell_marks(int level, const unsigned char* cells) {
 
 AmrMarkStats AmrTree::mark() {
     if (!dyn_) throw UnsupportedConfigError("mark: the tree is not dynamically adaptive (h_max / h_min)");
-    if (p_ == 1) return mark_dyn<1>();
-    if (p_ == 2) return mark_dyn<2>();
-    return mark_dyn<3>();
+    DynProfile& prof = dyn_profile();
+    prof.start();
+    const AmrMarkStats st = p_ == 1 ? mark_dyn<1>() : p_ == 2 ? mark_dyn<2>() : mark_dyn<3>();
+    prof.lap("mark");
+    if (prof.on) std::fprintf(stderr, " | depth %d specials %lld\n", L_, lastCounts_.specialVertices);
+    return st;
 }
 
 template <int P>
@@ -1852,9 +1883,13 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
 }
 
 SweepStats AmrTree::cycle(const Policy& pol, int n) {
+    DynProfile& prof = dyn_profile();
     if (dyn_) {
+        prof.start();
         lastCounts_ = dyn_->sweep();  // the traversal's structural edits, replayed on the host
+        prof.lap("replay");
         upload_sweep_tables();
+        prof.lap("tables");
     }
     for (int l = std::max(1, prob_.ellMin); l <= L_; ++l)
         if (std::abs(diag_[l]) < 1e-300) throw SingularDiagonalError("vanishing operator diagonal (phi*h^2 resonance?)");
@@ -1862,7 +1897,10 @@ SweepStats AmrTree::cycle(const Policy& pol, int n) {
         if (p_ == 1) run_cycle_dyn<1>(pol, n);
         else if (p_ == 2) run_cycle_dyn<2>(pol, n);
         else run_cycle_dyn<3>(pol, n);
+        if (prof.on) AMR_CUDA(cudaStreamSynchronize(stream_));
+        prof.lap("device");
         upload_final_flags();
+        prof.lap("final");
     } else if (p_ == 1) run_cycle<1>(pol, n);
     else if (p_ == 2) run_cycle<2>(pol, n);
     else run_cycle<3>(pol, n);

@@ -3,6 +3,9 @@
 #include "dyn.hpp"
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <cmath>
 #include <string>
@@ -34,7 +37,14 @@ DynTree::DynTree(int dim, int start, int maxLevel, int ellMin, double hMinRefine
         L.m = pow3i(l);
         L.n1 = L.m + 1;
         L.n = 1;
-        for (int d = 0; d < p_; ++d) L.n *= L.n1;
+        for (int d = 0; d < p_; ++d) {
+            L.stride[d] = L.n;
+            L.n *= L.n1;
+        }
+        for (int e = 0; e < (1 << p_); ++e) {
+            L.off[e] = 0;
+            for (int d = 0; d < p_; ++d) L.off[e] += bit(e, d) ? L.stride[d] : 0;
+        }
         if (L.n >= (1LL << 31)) throw CapacityError("dynamic adaptivity: level lattice exceeds 2^31 points");
         const size_t n = static_cast<size_t>(L.n);
         L.cell.assign(n, 0);
@@ -44,6 +54,7 @@ DynTree::DynTree(int dim, int start, int maxLevel, int ellMin, double hMinRefine
         L.entered.assign(n, 0);
         L.done.assign(n, 0);
         L.expected.assign(n, 0);
+        L.stale.assign(n, 0);
         L.sflag.assign(n, 0);
         L.scell.assign(n, 0);
         L.sestar.assign(n, 0xFF);
@@ -126,27 +137,70 @@ void DynTree::ensure_level(int l) {
     depth_ = std::max(depth_, l);
 }
 
-// refresh_classification, spacetree.cpp:438-489
-void DynTree::refresh(int l, const int* v) {
+// existing cells around lattice point v (cells v - bits(e)), and how many of them are refined
+int DynTree::adjacent_cells(int l, long long f, const int* v, int* refinedAdj) const {
+    const Level& L = lv_[l];
+    int low = 0;  // axes on which v has no lower neighbour cell
+    for (int d = 0; d < p_; ++d) low |= (v[d] == 0) << d;
+    int have = 0, ref = 0;
+    for (int e = 0; e < (1 << p_); ++e) {
+        if (e & low) continue;
+        const unsigned char c = L.cell[static_cast<size_t>(f - L.off[e])];  // upper-rim cells are never set
+        if (c & kCE) {
+            ++have;
+            ref += (c & kCR) ? 1 : 0;
+        }
+    }
+    if (refinedAdj) *refinedAdj = ref;
+    return have;
+}
+
+void DynTree::mark_stale(int l, const int* v) {
     Level& L = lv_[l];
-    const long long f = flat(l, v);
-    unsigned char fl = L.vtx[f] & kVE;
+    long long f = 0;
+    for (int d = 0; d < p_; ++d) {
+        if (v[d] < 0 || v[d] > L.m) return;
+        f += v[d] * L.stride[d];
+    }
+    if (!L.stale[f]) {
+        L.stale[f] = 1;
+        L.staleList.push_back(f);
+    }
+}
+
+void DynTree::stale_parents(int l, const int* v) {
+    if (l < 1) return;
+    const Level& C = lv_[l - 1];
+    int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    for (int d = 0; d < p_; ++d) {  // W with |3 W - v| <= 3 on every axis
+        lo[d] = std::max(0, (v[d] - 1) / 3);
+        hi[d] = std::min(C.m, (v[d] + 3) / 3);
+    }
+    int w[3] = {0, 0, 0};
+    for (w[2] = lo[2]; w[2] <= hi[2]; ++w[2])
+        for (w[1] = lo[1]; w[1] <= hi[1]; ++w[1])
+            for (w[0] = lo[0]; w[0] <= hi[0]; ++w[0]) mark_stale(l - 1, w);
+}
+
+// refresh_classification, spacetree.cpp:438-489
+bool DynTree::refresh(int l, const int* v) {
+    Level& L = lv_[l];
+    long long f = 0;
     bool bnd = false, cp = l > 0;
     for (int d = 0; d < p_; ++d) {
+        f += v[d] * L.stride[d];
         bnd |= v[d] == 0 || v[d] == L.m;
         cp &= v[d] % 3 == 0;
     }
+    L.stale[f] = 0;
+    const unsigned char oldFl = L.vtx[f];
+    const signed char oldSucc = L.succ[f];
+    unsigned char fl = L.vtx[f] & kVE;
     if (bnd) fl |= kVB;
     if (cp) fl |= kVC;
     const int total = indomain_adjacent(l, v);
-    int have = 0, refinedAdj = 0;
-    for (int e = 0; e < (1 << p_); ++e) {
-        int c[3] = {0, 0, 0};
-        for (int d = 0; d < p_; ++d) c[d] = v[d] - bit(e, d);
-        if (!has_cell(l, c)) continue;
-        ++have;
-        if (L.cell[static_cast<size_t>(flat(l, c))] & kCR) ++refinedAdj;
-    }
+    int refinedAdj = 0;
+    const int have = l <= depth_ ? adjacent_cells(l, f, v, &refinedAdj) : 0;
     const bool hanging = have < total;
     const bool refined = !hanging && refinedAdj == have;
     if (hanging) fl |= kVH;
@@ -154,7 +208,8 @@ void DynTree::refresh(int l, const int* v) {
     L.vtx[f] = fl;
     if (!refined) {
         L.succ[f] = 0;
-        return;
+        if (fl != oldFl || oldSucc != 0) stale_parents(l, v);
+        return fl != oldFl || oldSucc != 0;
     }
     int minSucc = INT_MAX;
     if (l + 1 <= depth_) {
@@ -164,17 +219,41 @@ void DynTree::refresh(int l, const int* v) {
             lo[d] = std::max(0, 3 * v[d] - 3);
             hi[d] = std::min(F.m, 3 * v[d] + 3);
         }
-        int w[3] = {0, 0, 0};
-        for (w[2] = p_ > 2 ? lo[2] : 0; w[2] <= (p_ > 2 ? hi[2] : 0); ++w[2])
-            for (w[1] = p_ > 1 ? lo[1] : 0; w[1] <= (p_ > 1 ? hi[1] : 0); ++w[1])
-                for (w[0] = lo[0]; w[0] <= hi[0]; ++w[0]) {
-                    const long long wf = flat(l + 1, w);
-                    const unsigned char fv = F.vtx[wf];
+        for (int z = p_ > 2 ? lo[2] : 0; z <= (p_ > 2 ? hi[2] : 0); ++z)
+            for (int y = p_ > 1 ? lo[1] : 0; y <= (p_ > 1 ? hi[1] : 0); ++y) {
+                const long long row = z * F.stride[2] + y * F.stride[1];
+                for (int x = lo[0]; x <= hi[0]; ++x) {
+                    const long long wf = row + x;
+                    const unsigned char fv = F.vtx[static_cast<size_t>(wf)];
                     if (!(fv & kVE)) continue;
-                    minSucc = std::min(minSucc, (fv & kVH) ? 0 : static_cast<int>(F.succ[wf]));
+                    minSucc = std::min(minSucc, (fv & kVH) ? 0 : static_cast<int>(F.succ[static_cast<size_t>(wf)]));
                 }
+            }
     }
     L.succ[f] = static_cast<signed char>(minSucc == INT_MAX ? 0 : 1 + minSucc);
+    const bool changed = fl != oldFl || L.succ[f] != oldSucc;
+    if (changed) stale_parents(l, v);
+    return changed;
+}
+
+// classify() restricted to the vertices whose inputs changed, finest level
+// first so that succ changes propagate upwards (same result as classify())
+void DynTree::classify_stale() {
+    int g[3] = {0, 0, 0};
+    for (int l = static_cast<int>(lv_.size()) - 1; l >= 0; --l) {
+        Level& L = lv_[l];
+        for (size_t i = 0; i < L.staleList.size(); ++i) {
+            const long long f = L.staleList[i];
+            if (!L.stale[f]) continue;
+            if (!(L.vtx[f] & kVE) || l > depth_) {
+                L.stale[f] = 0;
+                continue;
+            }
+            unflat(l, f, g);
+            refresh(l, g);
+        }
+        L.staleList.clear();
+    }
 }
 
 void DynTree::classify() {
@@ -203,31 +282,29 @@ long long DynTree::interior_fine_vertex_count() const {
 }
 
 // touch_vertex, spacetree.cpp:367-380
-void DynTree::touch(int l, const int* v) {
+void DynTree::touch(int l, long long f, const int* v) {
     Level& L = lv_[l];
-    const long long f = flat(l, v);
     if (L.epoch[f] == epoch_) return;
     L.epoch[f] = epoch_;
     L.done[f] = 0;
-    L.expected[f] = static_cast<unsigned char>(existing_adjacent(l, v));
+    L.expected[f] = static_cast<unsigned char>(adjacent_cells(l, f, v, nullptr));
     const bool hangNow = L.expected[f] < indomain_adjacent(l, v);
     L.sflag[f] = static_cast<unsigned char>(kSE | (hangNow ? kSH : 0) | (L.vtx[f] & (kVB | kVC)));
 }
 
 // finish_vertex_visit, spacetree.cpp:382-392, and the classification refresh
-// of touch_last (cycles.cpp:245) for the touch-last role
-void DynTree::finish(int l, const int* v, int corner, const int* cell) {
+// of touch_last (cycles.cpp:245) for the touch-last role; v is corner `corner`
+// of the cell being left
+void DynTree::finish(int l, long long f, const int* v, int corner) {
     Level& L = lv_[l];
-    const long long f = flat(l, v);
     ++L.done[f];
     if (L.done[f] != L.expected[f]) return;
-    int ce = 0;  // cell convention of exact_ops.cuh: cell = v - 1 + bits(ce)
-    for (int d = 0; d < p_; ++d) ce |= (cell[d] - v[d] + 1) << d;
+    const int ce = (~corner) & ((1 << p_) - 1);  // cell convention of exact_ops.cuh: cell = v - 1 + bits(ce)
     if (L.sfmask[f] == 0) L.sestar[f] = static_cast<unsigned char>(corner);
     else L.sflag[f] |= kSSpecial;  // finishes more than once
     L.sfmask[f] |= static_cast<unsigned char>(1u << ce);
     if (L.sflag[f] & kSH) return;  // destroy_hanging
-    if (dirty_) refresh(l, v);
+    if (dirty_ && L.stale[f]) refresh(l, v);  // unchanged inputs: the stored classification is current
     const unsigned char vf = L.vtx[f];
     if (vf & kVR) L.sflag[f] |= kSR;
     L.ssucc[f] = L.succ[f];
@@ -247,6 +324,11 @@ void DynTree::refine(int l, const int* c) {
     }
     check_capacity(static_cast<std::size_t>(blockVerts));
     P.cell[static_cast<size_t>(flat(l, c))] |= kCR;
+    for (int e = 0; e < (1 << p_); ++e) {  // the cell's corners see one more refined cell
+        int w[3] = {0, 0, 0};
+        for (int d = 0; d < p_; ++d) w[d] = c[d] + bit(e, d);
+        mark_stale(l, w);
+    }
     for (int t = 0; t < blockCells; ++t) {
         int ci[3] = {0, 0, 0}, tt = t;
         for (int d = 0; d < p_; ++d) {
@@ -263,6 +345,7 @@ void DynTree::refine(int l, const int* c) {
             tt /= 4;
         }
         const long long f = flat(l + 1, vi);
+        mark_stale(l + 1, vi);  // new adjacent cells
         if (!(F.vtx[f] & kVE)) {  // create_vertex_if_missing, spacetree.cpp:245-270
             if (F.epoch[f] == epoch_)
                 // it lived earlier in this traversal (touched, then deleted by an erase): two
@@ -279,6 +362,7 @@ void DynTree::refine(int l, const int* c) {
             F.expected[f] = static_cast<unsigned char>(existing_adjacent(l + 1, vi));
             const bool hangNow = F.expected[f] < indomain_adjacent(l + 1, vi);
             refresh(l + 1, vi);
+            stale_parents(l + 1, vi);  // a new vertex in the coarser vertices' succ scans
             F.sflag[f] = static_cast<unsigned char>(kSE | kSCreated | (hangNow ? kSH : 0) | (F.vtx[f] & (kVB | kVC)));
             // adjacent cells already entered in this traversal never reach it
             unsigned char skip = 0;
@@ -318,6 +402,11 @@ void DynTree::erase(int l, const int* c) {
         F.cell[cf] = 0;
     }
     lv_[l].cell[static_cast<size_t>(flat(l, c))] &= static_cast<unsigned char>(~kCR);
+    for (int e = 0; e < (1 << p_); ++e) {
+        int w[3] = {0, 0, 0};
+        for (int d = 0; d < p_; ++d) w[d] = c[d] + bit(e, d);
+        mark_stale(l, w);
+    }
     for (int t = 0; t < blockVerts; ++t) {
         int vi[3] = {0, 0, 0}, tt = t;
         for (int d = 0; d < p_; ++d) {
@@ -325,9 +414,11 @@ void DynTree::erase(int l, const int* c) {
             tt /= 4;
         }
         const size_t f = static_cast<size_t>(flat(l + 1, vi));
+        mark_stale(l + 1, vi);
         if (existing_adjacent(l + 1, vi) == 0 && (F.vtx[f] & kVE)) {
             F.vtx[f] = 0;
             --total_;
+            stale_parents(l + 1, vi);
         }
     }
     dirty_ = true;
@@ -337,13 +428,15 @@ void DynTree::erase(int l, const int* c) {
 // enter_cell's refine mark (cycles.cpp:174-180), leave_cell's erase (:222-241)
 void DynTree::visit(int l, const int* c) {
     const int nc = 1 << p_;
+    Level& L = lv_[l];
+    long long cfl = 0;
+    for (int d = 0; d < p_; ++d) cfl += c[d] * L.stride[d];
+    const size_t cf = static_cast<size_t>(cfl);
     int v[3] = {0, 0, 0};
     for (int e = 0; e < nc; ++e) {
         for (int d = 0; d < p_; ++d) v[d] = c[d] + bit(e, d);
-        touch(l, v);
+        touch(l, cfl + L.off[e], v);
     }
-    Level& L = lv_[l];
-    const size_t cf = static_cast<size_t>(flat(l, c));
     L.entered[cf] = epoch_;
     if (L.cell[cf] & kRM) {
         L.cell[cf] &= static_cast<unsigned char>(~kRM);
@@ -389,11 +482,22 @@ void DynTree::visit(int l, const int* c) {
     }
     for (int e = 0; e < nc; ++e) {
         for (int d = 0; d < p_; ++d) v[d] = c[d] + bit(e, d);
-        finish(l, v, e, c);
+        finish(l, cfl + L.off[e], v, e);
     }
 }
 
 SweepCounts DynTree::sweep() {
+    static const bool prof = [] {
+        const char* e = std::getenv("TMG_DYN_PROFILE");
+        return e && e[0] == '1';
+    }();
+    auto t0 = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!prof) return;
+        const auto t1 = std::chrono::steady_clock::now();
+        std::fprintf(stderr, " [%s %.1fms]", what, std::chrono::duration<double, std::milli>(t1 - t0).count());
+        t0 = t1;
+    };
     ++epoch_;
     dirty_ = false;
     counts_ = SweepCounts{};
@@ -405,8 +509,10 @@ SweepCounts DynTree::sweep() {
         std::fill(L.sskip.begin(), L.sskip.end(), 0);
         std::fill(L.ssucc.begin(), L.ssucc.end(), 0);
     }
+    lap("reset");
     const int zero[3] = {0, 0, 0};
     visit(0, zero);
+    lap("dfs");
     for (int l = 0; l <= depth_; ++l) {
         Level& L = lv_[l];
         for (long long f = 0; f < L.n; ++f) {
@@ -416,10 +522,12 @@ SweepCounts DynTree::sweep() {
             if (s & kSSpecial) ++counts_.specialVertices;
         }
     }
-    if (dirty_) {  // TdSweep::run, cycles.cpp:89-92
-        classify();
+    lap("scan");
+    if (dirty_) {  // TdSweep::run, cycles.cpp:89-92 (classify(), over the vertices it can change)
+        classify_stale();
         dirty_ = false;
     }
+    lap("classify");
     return counts_;
 }
 

@@ -39,12 +39,17 @@ struct Level {
     int m = 1;          // 3^l cells per axis
     int n1 = 2;         // 3^l + 1 lattice points per axis
     long long n = 0;    // n1^p
+    long long stride[3] = {1, 1, 1};
+    long long off[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // lattice offset of corner e: sum_d bit(e, d) stride[d]
     // persistent structure (cells indexed by their lower corner)
     std::vector<unsigned char> cell, vtx;
     std::vector<signed char> succ;
     // traversal bookkeeping (spacetree.cpp:367-436)
     std::vector<std::uint32_t> epoch, entered;
     std::vector<unsigned char> done, expected;
+    // classification inputs changed since the vertex was last classified
+    std::vector<unsigned char> stale;
+    std::vector<long long> staleList;
     // sweep tables
     std::vector<unsigned char> sflag, scell, sestar, sfmask, sskip;
     std::vector<signed char> ssucc;
@@ -83,11 +88,15 @@ class DynTree {
 
   private:
     void visit(int l, const int* c);
-    void touch(int l, const int* v);
-    void finish(int l, const int* v, int corner, const int* cell);
+    void touch(int l, long long f, const int* v);
+    void finish(int l, long long f, const int* v, int corner);
+    int adjacent_cells(int l, long long f, const int* v, int* refinedAdj) const;
     void refine(int l, const int* c);
     void erase(int l, const int* c);
-    void refresh(int l, const int* v);
+    bool refresh(int l, const int* v);  // true if the classification changed
+    void mark_stale(int l, const int* v);
+    void stale_parents(int l, const int* v);  // coarser vertices whose succ scan sees v
+    void classify_stale();
     int existing_adjacent(int l, const int* v) const;
     int indomain_adjacent(int l, const int* v) const;
     bool has_cell(int l, const int* c) const;
