@@ -115,6 +115,12 @@ int tmg_levels(const tmg_hierarchy* h);
 /* overwrite the pending marks of every existing cell of `level` (full lattice,
  * lower corner: 4 refineMark, 8 eraseMark), e.g. to replay externally chosen marks */
 treemg_status tmg_set_cell_marks(tmg_hierarchy* h, int level, const unsigned char* cells);
+/* dynamic adaptivity: cumulative wall-clock ms of the host traversal replay, the sweep-table
+ * upload, the device sweep, the final-classification upload and mark (all sweeps so far);
+ * out6[5]: kernels launched */
+treemg_status tmg_dyn_phase_ms(const tmg_hierarchy* h, double* out6);
+/* adaptive trees: stored vertices, hanging ones included */
+long long tmg_existing_vertices(const tmg_hierarchy* h);
 
 /* Verification cycles of a regular tree held in exact storage (precision 0),
  * each followed by evaluate_residual_norms (cycles.cpp:716-786) into *out:

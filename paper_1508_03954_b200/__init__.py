@@ -50,7 +50,7 @@ EXTENSION_SYMBOLS = [
     "tmg_slabs_e2e_step", "tmg_get_flags", "tmg_hanging_vertices", "tmg_leaf_vertices", "tmg_sphere_tree",
     "tmg_bu_fas", "tmg_textbook_add", "tmg_channel_norms", "tmg_dyn_create", "tmg_dyn_destroy", "tmg_dyn_depth",
     "tmg_dyn_interior_count", "tmg_dyn_set_cell_marks", "tmg_dyn_sweep", "tmg_dyn_flags", "tmg_dyn_sweep_tables",
-    "tmg_mark", "tmg_levels", "tmg_set_cell_marks",
+    "tmg_mark", "tmg_levels", "tmg_set_cell_marks", "tmg_dyn_phase_ms", "tmg_existing_vertices",
 ]
 
 _lib = None
@@ -139,6 +139,10 @@ def lib():
         L.tmg_dyn_sweep_tables.argtypes = [vp, ip, vp, vp, vp, vp, vp, vp]
         L.tmg_mark.restype = ip
         L.tmg_mark.argtypes = [vp, ctypes.POINTER(ctypes.c_longlong)]
+        L.tmg_dyn_phase_ms.restype = ip
+        L.tmg_dyn_phase_ms.argtypes = [vp, pd]
+        L.tmg_existing_vertices.restype = ctypes.c_longlong
+        L.tmg_existing_vertices.argtypes = [vp]
         L.tmg_set_cell_marks.restype = ip
         L.tmg_set_cell_marks.argtypes = [vp, ip, vp]
         L.tmg_levels.restype = ip
@@ -350,6 +354,16 @@ class Hierarchy:
 
     def depth(self) -> int:
         return self.L.tmg_levels(self.h)
+
+    def dyn_phase_ms(self) -> dict:
+        """Cumulative ms: host replay, table upload, device sweep, final upload, mark."""
+        out = np.zeros(6)
+        _check(self.L.tmg_dyn_phase_ms(self.h, _pd(out)))
+        return dict(zip(("replay", "tables", "device", "final", "mark", "launches"), out.tolist()))
+
+    @property
+    def existing_vertices(self) -> int:
+        return int(self.L.tmg_existing_vertices(self.h))
 
     def set_cell_marks(self, level: int, cells: np.ndarray):
         """Overwrite the pending cell marks of `level` (4 refine, 8 erase per lattice cell)."""

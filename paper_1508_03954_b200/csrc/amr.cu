@@ -1428,14 +1428,13 @@ struct DynProfile {
         const char* e = std::getenv("TMG_DYN_PROFILE");
         on = e && e[0] == '1';
     }
-    void start() {
-        if (on) t = std::chrono::steady_clock::now();
-    }
-    void lap(const char* what) {
-        if (!on) return;
+    void start() { t = std::chrono::steady_clock::now(); }
+    double lap(const char* what) {  // ms since the last lap (always measured; printed with TMG_DYN_PROFILE=1)
         const auto now = std::chrono::steady_clock::now();
-        std::fprintf(stderr, " %s %.2fms", what, std::chrono::duration<double, std::milli>(now - t).count());
+        const double ms = std::chrono::duration<double, std::milli>(now - t).count();
+        if (on) std::fprintf(stderr, " %s %.2fms", what, ms);
         t = now;
+        return ms;
     }
 };
 DynProfile& dyn_profile() {
@@ -1657,8 +1656,10 @@ void AmrTree::run_cycle_dyn(const Policy& pol, int n) {
     const int bpx = pol.bpx ? 1 : 0;
     for (int l = 0; l <= L_; ++l) {
         const adev::ALvl& pr = l > 0 ? D.lv[l - 1] : D.lv[0];
-        if (D.lv[l].nlist)
+        if (D.lv[l].nlist) {
             adev::k_amr_topdown<P><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
+            phaseMs_[5] += 1;
+        }
         dyn_check(stream_, "k_amr_topdown", l);
     }
     AMR_CUDA(cudaMemsetAsync(D.partials, 0, 2 * sizeof(double) * static_cast<size_t>(D.normOffs.back()), stream_));
@@ -1677,6 +1678,7 @@ void AmrTree::run_cycle_dyn(const Policy& pol, int n) {
         const adev::ALvl& fine = l < L_ ? D.lv[l + 1] : D.lv[l];
         const int restrictOn = (l < L_ && l + 1 > prob_.ellMin) ? 1 : 0;
         adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(c, fine, D.kc[l], D.weights, restrictOn);
+        phaseMs_[5] += c.nslist ? 3 : 2;  // chi, special, residual
         dyn_check(stream_, "k_amr_chi", l);
         if (c.nslist) {
             adev::k_dyn_special<P><<<blocks_for_n(c.nslist, smCount_), 256, 0, stream_>>>(
@@ -1692,6 +1694,7 @@ void AmrTree::run_cycle_dyn(const Policy& pol, int n) {
         dyn_check(stream_, "k_amr_residual", l);
     }
     adev::k_amr_norm_final<<<1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
+    phaseMs_[5] += 1;
     AMR_CUDA(cudaGetLastError());
 }
 
@@ -1766,6 +1769,8 @@ AmrMarkStats AmrTree::mark_dyn() {
     AMR_CUDA(cudaGetLastError());
     AMR_CUDA(cudaMemcpyAsync(&cnt, D.dCnt, sizeof(cnt), cudaMemcpyDeviceToHost, stream_));
     AMR_CUDA(cudaStreamSynchronize(stream_));
+    // features, refine translation per level, erase translation per level (+ histogram and classify)
+    phaseMs_[5] += 2 * (L_ + 1) + std::max(0, L_ - std::max(0, prob_.ellMin)) + (cnt.cand ? 2 * (L_ + 1) : 0);
     for (int l = 0; l <= L_; ++l) {  // the cell marks take effect in the next traversal
         dyn::Level& T = dyn_->level(l);
         D.hMark.resize(static_cast<size_t>(T.n));
@@ -1798,7 +1803,7 @@ AmrMarkStats AmrTree::mark() {
     DynProfile& prof = dyn_profile();
     prof.start();
     const AmrMarkStats st = p_ == 1 ? mark_dyn<1>() : p_ == 2 ? mark_dyn<2>() : mark_dyn<3>();
-    prof.lap("mark");
+    phaseMs_[4] += prof.lap("mark");
     if (prof.on) std::fprintf(stderr, " | depth %d specials %lld\n", L_, lastCounts_.specialVertices);
     return st;
 }
@@ -1887,9 +1892,9 @@ SweepStats AmrTree::cycle(const Policy& pol, int n) {
     if (dyn_) {
         prof.start();
         lastCounts_ = dyn_->sweep();  // the traversal's structural edits, replayed on the host
-        prof.lap("replay");
+        phaseMs_[0] += prof.lap("replay");
         upload_sweep_tables();
-        prof.lap("tables");
+        phaseMs_[1] += prof.lap("tables");
     }
     for (int l = std::max(1, prob_.ellMin); l <= L_; ++l)
         if (std::abs(diag_[l]) < 1e-300) throw SingularDiagonalError("vanishing operator diagonal (phi*h^2 resonance?)");
@@ -1897,10 +1902,10 @@ SweepStats AmrTree::cycle(const Policy& pol, int n) {
         if (p_ == 1) run_cycle_dyn<1>(pol, n);
         else if (p_ == 2) run_cycle_dyn<2>(pol, n);
         else run_cycle_dyn<3>(pol, n);
-        if (prof.on) AMR_CUDA(cudaStreamSynchronize(stream_));
-        prof.lap("device");
+        AMR_CUDA(cudaStreamSynchronize(stream_));  // the norms are read right after anyway
+        phaseMs_[2] += prof.lap("device");
         upload_final_flags();
-        prof.lap("final");
+        phaseMs_[3] += prof.lap("final");
     } else if (p_ == 1) run_cycle<1>(pol, n);
     else if (p_ == 2) run_cycle<2>(pol, n);
     else run_cycle<3>(pol, n);

@@ -79,6 +79,9 @@ class AmrTree {
     // dynamic adaptivity (prob.dynStart > 0): MarkStats of amr.cpp:61-222 on the device
     AmrMarkStats mark();
     bool dynamic() const { return dyn_ != nullptr; }
+    // cumulative wall-clock ms of the dynamic phases: host replay, table upload, device sweep,
+    // final-classification upload, mark (device + mark download); [5] kernels launched
+    const double* phase_ms() const { return phaseMs_; }
     // overwrite the pending cell marks of `level` (4 refineMark, 8 eraseMark per lattice cell)
     void set_cell_marks(int level, const unsigned char* cells);
     int levels() const { return L_; }
@@ -120,6 +123,7 @@ class AmrTree {
     std::vector<amr::HostLevel> host_;
     std::unique_ptr<dyn::DynTree> dyn_;  // dynamic adaptivity: the structure, replayed per sweep
     dyn::SweepCounts lastCounts_;
+    double phaseMs_[6] = {0, 0, 0, 0, 0, 0};  // + [5]: kernels launched
     std::unique_ptr<Dev> dev_;  // device arrays + the per-level exact constants
     std::vector<Cplx> diag_;
     long long leafCount_ = 0, existingCount_ = 0, hangingCount_ = 0;

@@ -542,6 +542,14 @@ treemg_status tmg_mark(tmg_hierarchy* h, long long* out9) {
 
 int tmg_levels(const tmg_hierarchy* h) { return h ? h->h->levels() : -1; }
 
+treemg_status tmg_dyn_phase_ms(const tmg_hierarchy* h, double* out6) {
+    if (!h || !out6) return fail(TREEMG_E_USAGE, "null argument");
+    h->h->dyn_phase_ms(out6);
+    return TREEMG_OK;
+}
+
+long long tmg_existing_vertices(const tmg_hierarchy* h) { return h ? h->h->existing_vertices() : 0; }
+
 treemg_status tmg_set_cell_marks(tmg_hierarchy* h, int level, const unsigned char* cells) {
     if (!h || !cells) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] { h->h->set_cell_marks(level, cells); });

@@ -1640,6 +1640,14 @@ void Hierarchy::set_cell_marks(int level, const unsigned char* cells) {
     impl_->amr->set_cell_marks(level, cells);
 }
 
+void Hierarchy::dyn_phase_ms(double* out6) const {
+    for (int i = 0; i < 6; ++i) out6[i] = 0.0;
+    if (!impl_->amr || !impl_->amr->dynamic()) return;
+    for (int i = 0; i < 6; ++i) out6[i] = impl_->amr->phase_ms()[i];
+}
+
+long long Hierarchy::existing_vertices() const { return impl_->amr ? impl_->amr->existing_vertices() : 0; }
+
 AmrMarkStats Hierarchy::mark() {
     if (!impl_->amr) throw UnsupportedConfigError("mark: the tree is not dynamically adaptive (h_max / h_min)");
     return impl_->amr->mark();

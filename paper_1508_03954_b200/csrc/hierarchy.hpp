@@ -110,6 +110,10 @@ class Hierarchy {
     AmrMarkStats mark();
     // overwrite the pending cell marks of a dynamically adaptive tree (4 refine, 8 erase per lattice cell)
     void set_cell_marks(int level, const unsigned char* cells);
+    // dynamic adaptivity: cumulative ms of host replay, table upload, device sweep, final upload, mark;
+    // out6[5]: kernels launched
+    void dyn_phase_ms(double* out6) const;
+    long long existing_vertices() const;  // adaptive trees: stored vertices (hanging included)
 
     int dim() const;
     int levels() const;  // current depth (grows under dynamic adaptivity)
