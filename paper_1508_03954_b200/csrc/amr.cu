@@ -60,6 +60,8 @@ struct ALvl {
     double* ind;                  // mark: |r| / |diag|
     unsigned char* vmark;         // mark: 1 refine, 2 erase, 4 candidate
     unsigned* cmark;              // mark: per cell, dyn::kRM | dyn::kEM
+    unsigned* mlist;              // mark: cells whose mark flipped (cell | kind << 31), for the host
+    unsigned* mcount;
     int lo[3];
     int n1[3];
     unsigned n;
@@ -857,7 +859,10 @@ __global__ void k_dyn_refine_cells(const ALvl* __restrict__ lvs, int level, doub
                 continue;
             }
             const unsigned old = atomicOr(&c.cmark[cf], static_cast<unsigned>(dyn::kRM));
-            if (!(old & dyn::kRM)) atomicAdd(&cnt->refineC, 1ull);
+            if (!(old & dyn::kRM)) {
+                atomicAdd(&cnt->refineC, 1ull);
+                c.mlist[atomicAdd(c.mcount, 1u)] = static_cast<unsigned>(cf);
+            }
         }
     }
 }
@@ -916,8 +921,52 @@ __global__ void k_dyn_erase_cells(const ALvl* __restrict__ lvs, int level, doubl
             continue;
         }
         const unsigned old = atomicOr(&c.cmark[f], static_cast<unsigned>(dyn::kEM));
-        if (!(old & dyn::kEM)) atomicAdd(&cnt->eraseC, 1ull);
+        if (!(old & dyn::kEM)) {
+            atomicAdd(&cnt->eraseC, 1ull);
+            c.mlist[atomicAdd(c.mcount, 1u)] = f | 0x80000000u;
+        }
     }
+}
+
+// sweep-table maintenance: clear the previous sweep's entries, scatter the new ones
+struct SweepRec {
+    unsigned f;
+    unsigned char flag, estar, fmask, skip;
+    signed char succ;
+    unsigned char pad[3];
+    int xoff;
+};
+
+__global__ void k_dyn_clear(unsigned char* vflag, unsigned char* estar, const unsigned* prev, unsigned n) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        vflag[prev[i]] = 0;
+        estar[prev[i]] = 0xFF;
+    }
+}
+
+__global__ void k_dyn_scatter(const SweepRec* __restrict__ rec, unsigned n, unsigned char* vflag, unsigned char* estar,
+                              unsigned char* fmask, unsigned char* skip, signed char* succ, int* xoff) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const SweepRec r = rec[i];
+        vflag[r.f] = r.flag;
+        estar[r.f] = r.estar;
+        fmask[r.f] = r.fmask;
+        skip[r.f] = r.skip;
+        succ[r.f] = r.succ;
+        xoff[r.f] = r.xoff;
+    }
+}
+
+// dst[idx[i]] = val[i] (val null: 0)
+__global__ void k_scatter_bytes(const unsigned* __restrict__ idx, const unsigned char* __restrict__ val, unsigned n,
+                                unsigned char* dst) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[idx[i]] = val ? val[i] : 0;
+}
+
+__global__ void k_clear_marks(const unsigned* __restrict__ mlist, unsigned n, unsigned* cmark) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        cmark[mlist[i] & 0x7FFFFFFFu] = 0;
 }
 
 __global__ void k_test_hypot(const double* x, const double* y, double* out, long long n) {
@@ -1240,10 +1289,20 @@ struct AmrTree::Dev {
                       *fflag = nullptr, *fcell = nullptr;
         signed char* succ = nullptr;
         int* xoff = nullptr;
-        unsigned *list = nullptr, *slist = nullptr, *cmark = nullptr;
+        unsigned *list = nullptr, *slist = nullptr, *cmark = nullptr, *mlist = nullptr;
         double2* extras = nullptr;
         size_t extrasCap = 0;
+        // incremental uploads: sweep records, visited cells (kept: the next sweep clears them),
+        // changed final vertex / cell bytes; host staging per level
+        adev::SweepRec* rec = nullptr;
+        unsigned *cidx = nullptr, *fidx = nullptr, *fcidx = nullptr;
+        unsigned char *cval = nullptr, *fval = nullptr, *fcval = nullptr;
+        unsigned ncells = 0;
+        std::vector<adev::SweepRec> hRec;
+        std::vector<unsigned> hList, hSlist, hCidx, hFidx, hFcidx, hMark;
+        std::vector<unsigned char> hCval, hFval, hFcval;
     };
+    unsigned* dMcount = nullptr;
     std::vector<DynLevel> dl;
     std::vector<std::array<double2, 9>> dgTab;
     double2* dgDev = nullptr;  // dgTab per level on the device (k_dyn_special)
@@ -1508,6 +1567,14 @@ void AmrTree::init_dynamic() {
         w.list = D.alloc<unsigned>(n, stream_);
         w.slist = D.alloc<unsigned>(n, stream_);
         w.cmark = D.alloc<unsigned>(n, stream_);
+        w.mlist = D.alloc<unsigned>(n, stream_);
+        w.rec = D.alloc<adev::SweepRec>(n, stream_);
+        w.cidx = D.alloc<unsigned>(n, stream_);
+        w.fidx = D.alloc<unsigned>(n, stream_);
+        w.fcidx = D.alloc<unsigned>(n, stream_);
+        w.cval = D.alloc<unsigned char>(n, stream_);
+        w.fval = D.alloc<unsigned char>(n, stream_);
+        w.fcval = D.alloc<unsigned char>(n, stream_);
         a.vflag = w.vflag;
         a.cflag = w.cflag;
         a.estar = w.estar;
@@ -1520,6 +1587,7 @@ void AmrTree::init_dynamic() {
         a.list = w.list;
         a.slist = w.slist;
         a.cmark = w.cmark;
+        a.mlist = w.mlist;
         a.feat = D.alloc<double>(n, stream_);
         a.ind = D.alloc<double>(n, stream_);
         a.vmark = D.alloc<unsigned char>(n, stream_);
@@ -1541,6 +1609,8 @@ void AmrTree::init_dynamic() {
     D.dNorm = D.alloc<double>(2 * (static_cast<size_t>(Lmax) + 1), stream_);
     AMR_CUDA(cudaMallocHost(&D.hNorm, 2 * (static_cast<size_t>(Lmax) + 1) * sizeof(double)));
     D.dLvs = D.alloc<adev::ALvl>(static_cast<size_t>(Lmax) + 1, stream_);
+    D.dMcount = D.alloc<unsigned>(static_cast<size_t>(Lmax) + 1, stream_);
+    for (int l = 0; l <= Lmax; ++l) D.lv[l].mcount = D.dMcount + l;
     D.dgDev = D.alloc<double2>(9 * (static_cast<size_t>(Lmax) + 1), stream_);
     for (int l = 0; l <= Lmax; ++l)
         AMR_CUDA(cudaMemcpyAsync(D.dgDev + 9 * l, D.dgTab[l].data(), 9 * sizeof(double2), cudaMemcpyHostToDevice,
@@ -1551,7 +1621,7 @@ void AmrTree::init_dynamic() {
     AMR_CUDA(cudaEventCreate(&D.ev0));
     AMR_CUDA(cudaEventCreate(&D.ev1));
     // before the first sweep the tables are the regular tree's classification
-    upload_final_flags();
+    upload_final_flags_full();
     for (int l = 0; l <= Lmax; ++l) {
         Dev::DynLevel& w = D.dl[l];
         const size_t n = static_cast<size_t>(host_[l].n);
@@ -1562,9 +1632,15 @@ void AmrTree::init_dynamic() {
             if (host_[l].vflag[f] & amr::kExists) D.hList.push_back(static_cast<unsigned>(f));
         AMR_CUDA(cudaMemcpyAsync(w.list, D.hList.data(), D.hList.size() * sizeof(unsigned), cudaMemcpyHostToDevice,
                                  stream_));
+        w.hCidx.clear();  // the cells set in cflag, so that the first sweep clears them
+        for (long long f = 0; f < host_[l].n; ++f)
+            if (host_[l].cflag[f] & amr::kCellExists) w.hCidx.push_back(static_cast<unsigned>(f));
+        AMR_CUDA(cudaMemcpyAsync(w.cidx, w.hCidx.data(), w.hCidx.size() * sizeof(unsigned), cudaMemcpyHostToDevice,
+                                 stream_));
         AMR_CUDA(cudaStreamSynchronize(stream_));
         D.lv[l].nlist = static_cast<unsigned>(D.hList.size());
         D.lv[l].nslist = 0;
+        w.ncells = static_cast<unsigned>(w.hCidx.size());
     }
     if (p_ == 1) build_rhs<1>();
     else if (p_ == 2) build_rhs<2>();
@@ -1572,8 +1648,8 @@ void AmrTree::init_dynamic() {
     AMR_CUDA(cudaStreamSynchronize(stream_));
 }
 
-// classification after the sweep -> fflag / fcell (mark) and host_ (field API)
-void AmrTree::upload_final_flags() {
+// classification after the sweep -> fflag / fcell (mark) and host_ (field API), in full
+void AmrTree::upload_final_flags_full() {
     Dev& D = *dev_;
     existingCount_ = hangingCount_ = leafCount_ = 0;
     for (int l = 0; l <= dyn_->max_level(); ++l) {
@@ -1595,59 +1671,137 @@ void AmrTree::upload_final_flags() {
         AMR_CUDA(cudaMemcpyAsync(D.dl[l].fcell, h.cflag.data(), n, cudaMemcpyHostToDevice, stream_));
     }
     AMR_CUDA(cudaStreamSynchronize(stream_));
+    dyn_->clear_notes();
 }
 
-// the sweep tables of dyn::DynTree::sweep -> device; vertex lists (regular
-// first), special list and the finish-value slots of the special vertices
+// ... and after a sweep: only the vertices / cells the sweep may have changed
+void AmrTree::upload_final_flags() {
+    Dev& D = *dev_;
+    auto counts = [](unsigned char v, long long& ex, long long& hg, long long& lf) {
+        if (!(v & amr::kExists)) return;
+        ++ex;
+        if (v & amr::kHanging) ++hg;
+        else if (!(v & amr::kRefined) && !(v & amr::kBoundary)) ++lf;
+    };
+    for (int l = 0; l <= dyn_->depth(); ++l) {
+        const dyn::Level& T = dyn_->level(l);
+        amr::HostLevel& h = host_[l];
+        Dev::DynLevel& w = D.dl[l];
+        w.hFidx.clear();
+        w.hFval.clear();
+        w.hFcidx.clear();
+        w.hFcval.clear();
+        for (long long f : T.vtxNoted) {
+            const unsigned char nv = static_cast<unsigned char>(T.vtx[f] & 31), ov = h.vflag[f];
+            h.succ[f] = T.succ[f];
+            if (nv == ov) continue;
+            long long e0 = 0, g0 = 0, f0 = 0, e1 = 0, g1 = 0, f1 = 0;
+            counts(ov, e0, g0, f0);
+            counts(nv, e1, g1, f1);
+            existingCount_ += e1 - e0;
+            hangingCount_ += g1 - g0;
+            leafCount_ += f1 - f0;
+            h.vflag[f] = nv;
+            w.hFidx.push_back(static_cast<unsigned>(f));
+            w.hFval.push_back(nv);
+        }
+        for (long long f : T.cellNoted) {
+            const unsigned char nc = static_cast<unsigned char>(T.cell[f] & (dyn::kCE | dyn::kCR));
+            if (nc == h.cflag[f]) continue;
+            h.cflag[f] = nc;
+            w.hFcidx.push_back(static_cast<unsigned>(f));
+            w.hFcval.push_back(nc);
+        }
+        const unsigned nv = static_cast<unsigned>(w.hFidx.size()), ncl = static_cast<unsigned>(w.hFcidx.size());
+        if (nv) {
+            AMR_CUDA(cudaMemcpyAsync(w.fidx, w.hFidx.data(), nv * sizeof(unsigned), cudaMemcpyHostToDevice, stream_));
+            AMR_CUDA(cudaMemcpyAsync(w.fval, w.hFval.data(), nv, cudaMemcpyHostToDevice, stream_));
+            adev::k_scatter_bytes<<<blocks_for_n(nv, smCount_), 256, 0, stream_>>>(w.fidx, w.fval, nv, w.fflag);
+        }
+        if (ncl) {
+            AMR_CUDA(cudaMemcpyAsync(w.fcidx, w.hFcidx.data(), ncl * sizeof(unsigned), cudaMemcpyHostToDevice,
+                                     stream_));
+            AMR_CUDA(cudaMemcpyAsync(w.fcval, w.hFcval.data(), ncl, cudaMemcpyHostToDevice, stream_));
+            adev::k_scatter_bytes<<<blocks_for_n(ncl, smCount_), 256, 0, stream_>>>(w.fcidx, w.fcval, ncl, w.fcell);
+        }
+    }
+    AMR_CUDA(cudaGetLastError());
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+    dyn_->clear_notes();
+}
+
+// the sweep tables of dyn::DynTree::sweep -> device, proportional to the
+// sweep: the previous sweep's entries are cleared, the new records scattered;
+// vertex lists (regular first), special list, finish-value slots
 void AmrTree::upload_sweep_tables() {
     Dev& D = *dev_;
     L_ = dyn_->depth();
     for (int l = 0; l <= dyn_->max_level(); ++l) {
         adev::ALvl& a = D.lv[l];
         Dev::DynLevel& w = D.dl[l];
+        if (a.nlist) adev::k_dyn_clear<<<blocks_for_n(a.nlist, smCount_), 256, 0, stream_>>>(w.vflag, w.estar, w.list,
+                                                                                            a.nlist);
+        if (w.ncells) adev::k_scatter_bytes<<<blocks_for_n(w.ncells, smCount_), 256, 0, stream_>>>(w.cidx, nullptr,
+                                                                                                  w.ncells, w.cflag);
         if (l > L_) {
             a.nlist = a.nslist = 0;
+            w.ncells = 0;
             continue;
         }
         const dyn::Level& T = dyn_->level(l);
-        const size_t n = static_cast<size_t>(T.n);
-        AMR_CUDA(cudaMemcpyAsync(w.vflag, T.sflag.data(), n, cudaMemcpyHostToDevice, stream_));
-        AMR_CUDA(cudaMemcpyAsync(w.cflag, T.scell.data(), n, cudaMemcpyHostToDevice, stream_));
-        AMR_CUDA(cudaMemcpyAsync(w.estar, T.sestar.data(), n, cudaMemcpyHostToDevice, stream_));
-        AMR_CUDA(cudaMemcpyAsync(w.succ, T.ssucc.data(), n, cudaMemcpyHostToDevice, stream_));
-        AMR_CUDA(cudaMemcpyAsync(w.fmask, T.sfmask.data(), n, cudaMemcpyHostToDevice, stream_));
-        AMR_CUDA(cudaMemcpyAsync(w.skip, T.sskip.data(), n, cudaMemcpyHostToDevice, stream_));
-        D.hList.clear();
-        D.hSlist.clear();
-        D.hXoff.assign(n, 0);
-        size_t slots = 0;
-        for (int pass = 0; pass < 2; ++pass)
-            for (size_t f = 0; f < n; ++f) {
-                const unsigned char v = T.sflag[f];
-                if (!(v & dyn::kSE)) continue;
-                const bool regular = !(v & (dyn::kSH | dyn::kSB | dyn::kSSpecial));
-                if (regular == (pass == 0)) D.hList.push_back(static_cast<unsigned>(f));
-                if (pass == 0 && (v & dyn::kSSpecial)) {
-                    D.hSlist.push_back(static_cast<unsigned>(f));
-                    D.hXoff[f] = static_cast<int>(slots);
-                    slots += static_cast<size_t>(__builtin_popcount(T.sfmask[f]));
-                }
+        w.hRec.clear();
+        w.hList.clear();
+        w.hSlist.clear();
+        int slots = 0;
+        std::vector<unsigned>& irregular = w.hFidx;  // scratch: non-regular vertices, listed after the regular ones
+        irregular.clear();
+        for (long long f : T.sweepList) {
+            const unsigned char v = T.sflag[f];
+            adev::SweepRec r{};
+            r.f = static_cast<unsigned>(f);
+            r.flag = v;
+            r.estar = T.sestar[f];
+            r.fmask = T.sfmask[f];
+            r.skip = T.sskip[f];
+            r.succ = T.ssucc[f];
+            r.xoff = 0;
+            if (v & dyn::kSSpecial) {
+                w.hSlist.push_back(r.f);
+                r.xoff = slots;
+                slots += __builtin_popcount(T.sfmask[f]);
             }
-        if (slots > w.extrasCap) {
+            w.hRec.push_back(r);
+            if (v & (dyn::kSH | dyn::kSB | dyn::kSSpecial)) irregular.push_back(r.f);
+            else w.hList.push_back(r.f);
+        }
+        w.hList.insert(w.hList.end(), irregular.begin(), irregular.end());
+        w.hCidx.assign(T.cellList.begin(), T.cellList.end());
+        w.hCval.resize(w.hCidx.size());
+        for (size_t i = 0; i < w.hCidx.size(); ++i) w.hCval[i] = T.scell[w.hCidx[i]];
+        if (static_cast<size_t>(slots) > w.extrasCap) {
             if (w.extras) AMR_CUDA(cudaFree(w.extras));
-            w.extrasCap = std::max<size_t>(slots, 2 * w.extrasCap);
+            w.extrasCap = std::max<size_t>(static_cast<size_t>(slots), 2 * w.extrasCap);
             AMR_CUDA(cudaMalloc(&w.extras, w.extrasCap * sizeof(double2)));
         }
         a.extras = w.extras;
-        AMR_CUDA(cudaMemcpyAsync(w.list, D.hList.data(), D.hList.size() * sizeof(unsigned), cudaMemcpyHostToDevice,
+        const unsigned nrec = static_cast<unsigned>(w.hRec.size()), ncl = static_cast<unsigned>(w.hCidx.size());
+        AMR_CUDA(cudaMemcpyAsync(w.rec, w.hRec.data(), nrec * sizeof(adev::SweepRec), cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.list, w.hList.data(), w.hList.size() * sizeof(unsigned), cudaMemcpyHostToDevice,
                                  stream_));
-        AMR_CUDA(cudaMemcpyAsync(w.slist, D.hSlist.data(), D.hSlist.size() * sizeof(unsigned),
+        AMR_CUDA(cudaMemcpyAsync(w.slist, w.hSlist.data(), w.hSlist.size() * sizeof(unsigned),
                                  cudaMemcpyHostToDevice, stream_));
-        AMR_CUDA(cudaMemcpyAsync(w.xoff, D.hXoff.data(), n * sizeof(int), cudaMemcpyHostToDevice, stream_));
-        AMR_CUDA(cudaStreamSynchronize(stream_));  // the staging vectors are reused per level
-        a.nlist = static_cast<unsigned>(D.hList.size());
-        a.nslist = static_cast<unsigned>(D.hSlist.size());
+        AMR_CUDA(cudaMemcpyAsync(w.cidx, w.hCidx.data(), ncl * sizeof(unsigned), cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(w.cval, w.hCval.data(), ncl, cudaMemcpyHostToDevice, stream_));
+        if (nrec)
+            adev::k_dyn_scatter<<<blocks_for_n(nrec, smCount_), 256, 0, stream_>>>(w.rec, nrec, w.vflag, w.estar,
+                                                                                 w.fmask, w.skip, w.succ, w.xoff);
+        if (ncl) adev::k_scatter_bytes<<<blocks_for_n(ncl, smCount_), 256, 0, stream_>>>(w.cidx, w.cval, ncl, w.cflag);
+        a.nlist = static_cast<unsigned>(w.hList.size());
+        a.nslist = static_cast<unsigned>(w.hSlist.size());
+        w.ncells = ncl;
     }
+    AMR_CUDA(cudaGetLastError());
+    AMR_CUDA(cudaStreamSynchronize(stream_));  // staging vectors are rebuilt next sweep
 }
 
 template <int P>
@@ -1756,8 +1910,8 @@ AmrMarkStats AmrTree::mark_dyn() {
                     D.dLvs, l, smin, span, kBins, kRef, kErase, kVeto, D.dCnt);
         }
     }
+    AMR_CUDA(cudaMemsetAsync(D.dMcount, 0, D.lv.size() * sizeof(unsigned), stream_));
     for (int l = 0; l <= L_; ++l) {
-        AMR_CUDA(cudaMemsetAsync(D.dl[l].cmark, 0, static_cast<size_t>(D.lv[l].n) * sizeof(unsigned), stream_));
         adev::k_dyn_refine_cells<P><<<blocks_for_n(D.lv[l].n, smCount_), 256, 0, stream_>>>(
             D.dLvs, l, std::pow(3.0, -l), prob_.hMin, D.dCnt);
         dyn_check(stream_, "k_dyn_refine_cells", l);
@@ -1771,13 +1925,22 @@ AmrMarkStats AmrTree::mark_dyn() {
     AMR_CUDA(cudaStreamSynchronize(stream_));
     // features, refine translation per level, erase translation per level (+ histogram and classify)
     phaseMs_[5] += 2 * (L_ + 1) + std::max(0, L_ - std::max(0, prob_.ellMin)) + (cnt.cand ? 2 * (L_ + 1) : 0);
+    std::vector<unsigned> mcount(D.lv.size());
+    AMR_CUDA(cudaMemcpy(mcount.data(), D.dMcount, mcount.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
     for (int l = 0; l <= L_; ++l) {  // the cell marks take effect in the next traversal
+        if (!mcount[l]) continue;
         dyn::Level& T = dyn_->level(l);
-        D.hMark.resize(static_cast<size_t>(T.n));
-        AMR_CUDA(cudaMemcpy(D.hMark.data(), D.dl[l].cmark, D.hMark.size() * sizeof(unsigned), cudaMemcpyDeviceToHost));
-        for (long long f = 0; f < T.n; ++f)
-            if (T.cell[f] & dyn::kCE) T.cell[f] = static_cast<unsigned char>(T.cell[f] | (D.hMark[f] & (dyn::kRM | dyn::kEM)));
+        Dev::DynLevel& w = D.dl[l];
+        w.hMark.resize(mcount[l]);
+        AMR_CUDA(cudaMemcpy(w.hMark.data(), w.mlist, mcount[l] * sizeof(unsigned), cudaMemcpyDeviceToHost));
+        for (unsigned e : w.hMark) {
+            const long long f = e & 0x7FFFFFFFu;
+            if (T.cell[f] & dyn::kCE)
+                T.cell[f] = static_cast<unsigned char>(T.cell[f] | ((e >> 31) ? dyn::kEM : dyn::kRM));
+        }
+        adev::k_clear_marks<<<blocks_for_n(mcount[l], smCount_), 256, 0, stream_>>>(w.mlist, mcount[l], w.cmark);
     }
+    AMR_CUDA(cudaGetLastError());
     AmrMarkStats st;
     st.refineVertices = static_cast<long long>(cnt.refineV);
     st.eraseVertices = static_cast<long long>(cnt.eraseV);

@@ -112,6 +112,7 @@ class AmrTree {
     void upload_weights();
     void upload_sweep_tables();
     void upload_final_flags();
+    void upload_final_flags_full();
     void refresh_counts();
     template <int P>
     void build_rhs();

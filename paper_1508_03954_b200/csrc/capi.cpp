@@ -466,6 +466,7 @@ treemg_status tmg_dyn_sweep(tmg_dyn* h, long long* out4) {
     if (!h) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
         const dyn::SweepCounts c = h->t->sweep();
+        h->t->clear_notes();
         if (out4) {
             out4[0] = c.refinedCells;
             out4[1] = c.erasedCells;

@@ -55,6 +55,8 @@ DynTree::DynTree(int dim, int start, int maxLevel, int ellMin, double hMinRefine
         L.done.assign(n, 0);
         L.expected.assign(n, 0);
         L.stale.assign(n, 0);
+        L.vtxOld.assign(n, 0);
+        L.noted.assign(n, 0);
         L.sflag.assign(n, 0);
         L.scell.assign(n, 0);
         L.sestar.assign(n, 0xFF);
@@ -155,6 +157,28 @@ int DynTree::adjacent_cells(int l, long long f, const int* v, int* refinedAdj) c
     return have;
 }
 
+void DynTree::note_vtx(Level& L, long long f) {
+    if (L.noted[f] & 1) return;
+    L.noted[f] |= 1;
+    L.vtxOld[f] = L.vtx[f];
+    L.vtxNoted.push_back(f);
+}
+
+void DynTree::note_cell(Level& L, long long f) {
+    if (L.noted[f] & 2) return;
+    L.noted[f] |= 2;
+    L.cellNoted.push_back(f);
+}
+
+void DynTree::clear_notes() {
+    for (Level& L : lv_) {
+        for (long long f : L.vtxNoted) L.noted[f] &= static_cast<unsigned char>(~1);
+        for (long long f : L.cellNoted) L.noted[f] &= static_cast<unsigned char>(~2);
+        L.vtxNoted.clear();
+        L.cellNoted.clear();
+    }
+}
+
 void DynTree::mark_stale(int l, const int* v) {
     Level& L = lv_[l];
     long long f = 0;
@@ -193,6 +217,7 @@ bool DynTree::refresh(int l, const int* v) {
         cp &= v[d] % 3 == 0;
     }
     L.stale[f] = 0;
+    note_vtx(L, f);
     const unsigned char oldFl = L.vtx[f];
     const signed char oldSucc = L.succ[f];
     unsigned char fl = L.vtx[f] & kVE;
@@ -286,6 +311,7 @@ void DynTree::touch(int l, long long f, const int* v) {
     Level& L = lv_[l];
     if (L.epoch[f] == epoch_) return;
     L.epoch[f] = epoch_;
+    L.sweepList.push_back(f);
     L.done[f] = 0;
     L.expected[f] = static_cast<unsigned char>(adjacent_cells(l, f, v, nullptr));
     const bool hangNow = L.expected[f] < indomain_adjacent(l, v);
@@ -323,6 +349,7 @@ void DynTree::refine(int l, const int* c) {
         blockVerts *= 4;
     }
     check_capacity(static_cast<std::size_t>(blockVerts));
+    note_cell(P, flat(l, c));
     P.cell[static_cast<size_t>(flat(l, c))] |= kCR;
     for (int e = 0; e < (1 << p_); ++e) {  // the cell's corners see one more refined cell
         int w[3] = {0, 0, 0};
@@ -335,6 +362,7 @@ void DynTree::refine(int l, const int* c) {
             ci[d] = 3 * c[d] + tt % 3;
             tt /= 3;
         }
+        note_cell(F, flat(l + 1, ci));
         F.cell[static_cast<size_t>(flat(l + 1, ci))] = kCE;
     }
     for (int t = 0; t < blockVerts; ++t) {
@@ -354,10 +382,12 @@ void DynTree::refine(int l, const int* c) {
                     "B200 path: a vertex erased and re-created within one traversal (an erase next to a later "
                     "refinement) is not supported");
             check_capacity(1);
+            note_vtx(F, f);
             F.vtx[f] = kVE;
             F.succ[f] = 0;
             ++total_;
             F.epoch[f] = epoch_;
+            F.sweepList.push_back(f);
             F.done[f] = 0;
             F.expected[f] = static_cast<unsigned char>(existing_adjacent(l + 1, vi));
             const bool hangNow = F.expected[f] < indomain_adjacent(l + 1, vi);
@@ -399,8 +429,10 @@ void DynTree::erase(int l, const int* c) {
         }
         const size_t cf = static_cast<size_t>(flat(l + 1, ci));
         if (F.cell[cf] & kCR) erase(l + 1, ci);
+        note_cell(F, static_cast<long long>(cf));
         F.cell[cf] = 0;
     }
+    note_cell(lv_[l], flat(l, c));
     lv_[l].cell[static_cast<size_t>(flat(l, c))] &= static_cast<unsigned char>(~kCR);
     for (int e = 0; e < (1 << p_); ++e) {
         int w[3] = {0, 0, 0};
@@ -416,6 +448,7 @@ void DynTree::erase(int l, const int* c) {
         const size_t f = static_cast<size_t>(flat(l + 1, vi));
         mark_stale(l + 1, vi);
         if (existing_adjacent(l + 1, vi) == 0 && (F.vtx[f] & kVE)) {
+            note_vtx(F, static_cast<long long>(f));
             F.vtx[f] = 0;
             --total_;
             stale_parents(l + 1, vi);
@@ -432,6 +465,7 @@ void DynTree::visit(int l, const int* c) {
     long long cfl = 0;
     for (int d = 0; d < p_; ++d) cfl += c[d] * L.stride[d];
     const size_t cf = static_cast<size_t>(cfl);
+    L.cellList.push_back(cfl);
     int v[3] = {0, 0, 0};
     for (int e = 0; e < nc; ++e) {
         for (int d = 0; d < p_; ++d) v[d] = c[d] + bit(e, d);
@@ -501,13 +535,17 @@ SweepCounts DynTree::sweep() {
     ++epoch_;
     dirty_ = false;
     counts_ = SweepCounts{};
-    for (Level& L : lv_) {
-        std::fill(L.sflag.begin(), L.sflag.end(), 0);
-        std::fill(L.scell.begin(), L.scell.end(), 0);
-        std::fill(L.sestar.begin(), L.sestar.end(), 0xFF);
-        std::fill(L.sfmask.begin(), L.sfmask.end(), 0);
-        std::fill(L.sskip.begin(), L.sskip.end(), 0);
-        std::fill(L.ssucc.begin(), L.ssucc.end(), 0);
+    for (Level& L : lv_) {  // reset the previous sweep's table entries
+        for (long long f : L.sweepList) {
+            L.sflag[f] = 0;
+            L.sestar[f] = 0xFF;
+            L.sfmask[f] = 0;
+            L.sskip[f] = 0;
+            L.ssucc[f] = 0;
+        }
+        for (long long f : L.cellList) L.scell[f] = 0;
+        L.sweepList.clear();
+        L.cellList.clear();
     }
     lap("reset");
     const int zero[3] = {0, 0, 0};
@@ -515,9 +553,8 @@ SweepCounts DynTree::sweep() {
     lap("dfs");
     for (int l = 0; l <= depth_; ++l) {
         Level& L = lv_[l];
-        for (long long f = 0; f < L.n; ++f) {
+        for (long long f : L.sweepList) {
             unsigned char& s = L.sflag[f];
-            if (!(s & kSE)) continue;
             if (L.sfmask[f] == 0) s |= kSSpecial;  // never finishes
             if (s & kSSpecial) ++counts_.specialVertices;
         }

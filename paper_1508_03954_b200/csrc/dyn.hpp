@@ -50,6 +50,11 @@ struct Level {
     // classification inputs changed since the vertex was last classified
     std::vector<unsigned char> stale;
     std::vector<long long> staleList;
+    // what the last sweep touched: its vertices and cells (sweep tables), and the
+    // vertices / cells whose persistent structure it may have changed (with the
+    // vertex byte before the sweep) -- so uploads and resets are proportional to it
+    std::vector<long long> sweepList, cellList, vtxNoted, cellNoted;
+    std::vector<unsigned char> vtxOld, noted;  // noted: 1 vertex, 2 cell
     // sweep tables
     std::vector<unsigned char> sflag, scell, sestar, sfmask, sskip;
     std::vector<signed char> ssucc;
@@ -97,6 +102,14 @@ class DynTree {
     void mark_stale(int l, const int* v);
     void stale_parents(int l, const int* v);  // coarser vertices whose succ scan sees v
     void classify_stale();
+    void note_vtx(Level& L, long long f);
+    void note_cell(Level& L, long long f);
+
+  public:
+    // forget the noted changes (after the caller consumed them)
+    void clear_notes();
+
+  private:
     int existing_adjacent(int l, const int* v) const;
     int indomain_adjacent(int l, const int* v) const;
     bool has_cell(int l, const int* c) const;
