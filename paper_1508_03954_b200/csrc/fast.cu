@@ -308,9 +308,34 @@ __global__ void __launch_bounds__(256) k_residual_lowdim(ResArgs a) {
     dev::block_norms(nmax, nsum, a.partials);
 }
 
-// ---- K3r: r_{l-1} = R r_l (separable 1D weights 1/3 2/3 1 2/3 1/3) -----------
+// k_smooth_coarse's update of one interior point on its just-restricted residual
+// (the restriction kernels' fold; boundary sc / si stay zero)
 template <int P>
-__global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse, unsigned fa, unsigned fb) {
+__device__ __forceinline__ void smooth_interior(const ResArgs& a, unsigned f, const int* idx, double2 r) {
+    const Lvl& c = a.lv;
+    if (a.bpx && c.si) {
+        c.si[f] = c.sinext[f];
+        c.sinext[f] = make_double2(0.0, 0.0);
+    }
+    if (c.level < a.ellMin) {
+        c.sc[f] = make_double2(0.0, 0.0);
+        return;
+    }
+    const bool cp = dev::is_cpoint<P>(idx);
+    const double2 smooth = mul(r, a.k.invDiag);
+    c.sc[f] = stage(smooth, a.k.wRaw, cp, a.bpx, a.hb);
+    if (a.bpx && c.level > a.ellMin && cp) {
+        int wi[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+        a.par.sinext[dev::flat<P>(wi, a.par.n1)] = mul(a.k.wRaw, smooth);
+    }
+}
+
+// ---- K3r: r_{l-1} = R r_l (separable 1D weights 1/3 2/3 1 2/3 1/3) -----------
+// SMOOTH: also the coarse level's smoothing on the value just formed.
+template <int P, bool SMOOTH = false>
+__global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse, unsigned fa, unsigned fb, const ResArgs sa) {
     const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
     const long long sy = fine.n1, sz = static_cast<long long>(fine.n1) * fine.n1;
     for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
@@ -366,6 +391,7 @@ __global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse, unsigned
             }
         }
         coarse.rhat[f] = acc;
+        if (SMOOTH) smooth_interior<P>(sa, f, W, acc);
     }
 }
 
@@ -409,7 +435,8 @@ __global__ void __launch_bounds__(kRowThreads) k_topdown3_rows(Lvl c, Lvl pr, in
     }
 }
 
-__global__ void __launch_bounds__(kRowThreads) k_restrict3_rows(Lvl fine, Lvl coarse, int zlo) {
+template <bool SMOOTH = false>
+__global__ void __launch_bounds__(kRowThreads) k_restrict3_rows(Lvl fine, Lvl coarse, int zlo, const ResArgs sa) {
     extern __shared__ double2 rw[];  // [25][coarse.n1] x-restricted fine rows
     const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
     const int mc = static_cast<int>(coarse.m);
@@ -447,6 +474,10 @@ __global__ void __launch_bounds__(kRowThreads) k_restrict3_rows(Lvl fine, Lvl co
             acc.y = fma(w[k], pl.y, acc.y);
         }
         out[W0] = acc;
+        if (SMOOTH) {
+            const int W[3] = {W0, W1, W2};
+            smooth_interior<3>(sa, static_cast<unsigned>(W0) + cn1 * (static_cast<unsigned>(W1) + cn1 * static_cast<unsigned>(W2)), W, acc);
+        }
     }
 }
 
@@ -478,6 +509,181 @@ __global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a, unsigned fa, u
 }
 
 constexpr int kZch = 48;
+
+// ---- pyramid top-down (see fast.cuh) ---------------------------------------
+// Threads (32, 8); the tile of level T is 32 x 8 x bz points (P = 3) or
+// 32 x 8 bz (P = 2).  Box of level l-1 feeding box [lo, hi] of level l:
+// [min(lo/3, m-1), min(hi/3, m-1) + 1] per axis (q = min(idx/3, m-1), q + 1).
+constexpr int kPyrTX = 32, kPyrTY = 8, kPyrK = 4;  // kPyrK points per thread
+
+// lerp for rel in {0, 1, 2} (interior points; rel = 3 only on the top boundary),
+// branch-free, bit-identical to lerp()
+__device__ __forceinline__ double2 lerp012(double2 c0, double2 c1, int rel) {
+    const double w1 = rel == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
+    const double2 v = make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
+    return rel == 0 ? c0 : v;
+}
+
+// P-linear prolongation from a box in shared memory (strides s1 = sz0, s2 = sz0 * sz1)
+template <int P>
+__device__ __forceinline__ double2 prolong_box(const double2* box, int s1, int s2, const int* q, const int* rel) {
+    const double2* b = box + q[0] + s1 * q[1] + (P == 3 ? s2 * q[2] : 0);
+    double2 v[1 << P];
+#pragma unroll
+    for (int e = 0; e < (1 << P); ++e) v[e] = b[(e & 1) + ((e >> 1) & 1) * s1 + (P == 3 ? ((e >> 2) & 1) * s2 : 0)];
+#pragma unroll
+    for (int d = 0; d < P; ++d)
+#pragma unroll
+        for (int i = 0; i < (1 << (P - 1 - d)); ++i) v[i] = lerp012(v[2 * i], v[2 * i + 1], rel[d]);
+    return v[0];
+}
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+// Box loops: thread (tx, ty) walks x = tx (boxes are at most 32 wide), y = ty,
+// ty + 8, ..., and (P = 3) every z.
+template <int P>
+__global__ void __launch_bounds__(kPyrTX* kPyrTY) k_topdown_pyr(const PyrArgs a) {
+    extern __shared__ __align__(16) double2 pyr[];
+    __shared__ int blo[kPyrMaxLevels][3], bsz[kPyrMaxLevels][3];
+    __shared__ PyrLevel slv[kPyrMaxLevels];
+    __shared__ int soff[kPyrMaxLevels], scap[kPyrMaxLevels];
+    const int tid = threadIdx.x, tx = tid & (kPyrTX - 1), ty = tid / kPyrTX;
+    const int T = a.T;
+    // per-level parameters into shared memory in one parallel round: a
+    // dynamically indexed kernel parameter is a serialised constant-cache miss
+    if (tid <= T) {
+        slv[tid] = a.lv[tid];
+        soff[tid] = a.off[tid];
+        scap[tid] = a.cap[tid];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int lo[3], hi[3];
+        const int t0 = blockIdx.x % a.nbx, t1 = (blockIdx.x / a.nbx) % a.nby, t2 = blockIdx.x / (a.nbx * a.nby);
+        const int ext[3] = {kPyrTX, P == 3 ? kPyrTY : kPyrTY * kPyrK, kPyrK};
+        const int tl[3] = {t0, t1, t2};
+        for (int d = 0; d < P; ++d) {
+            lo[d] = tl[d] * ext[d];
+            hi[d] = min(lo[d] + ext[d] - 1, slv[T].m);
+            blo[T][d] = lo[d];
+            bsz[T][d] = hi[d] - lo[d] + 1;
+        }
+        for (int l = T - 1; l >= 0; --l) {
+            const int mp = slv[l].m;
+            for (int d = 0; d < P; ++d) {
+                lo[d] = min(lo[d] / 3, mp - 1);
+                hi[d] = min(hi[d] / 3, mp - 1) + 1;
+                blo[l][d] = lo[d];
+                bsz[l][d] = hi[d] - lo[d] + 1;
+            }
+            if (P == 2) blo[l][2] = 0, bsz[l][2] = 1;
+        }
+        if (P == 2) blo[T][2] = 0, bsz[T][2] = 1;
+    }
+    __syncthreads();
+    // (1) this thread's level-T points into registers (in flight during the pyramid)
+    const PyrLevel LT = slv[T];
+    double2 own[kPyrK];
+    unsigned fo[kPyrK];
+    const int gx = blo[T][0] + tx;
+    const bool xin = tx < bsz[T][0] && gx > 0 && gx < LT.m;
+#pragma unroll
+    for (int k = 0; k < kPyrK; ++k) {
+        const int gy = blo[T][1] + ty + (P == 2 ? kPyrTY * k : 0), gz = P == 3 ? blo[T][2] + k : 0;
+        const bool in = xin && gy - blo[T][1] < bsz[T][1] && gy > 0 && gy < LT.m &&
+                        (P == 2 || (k < bsz[T][2] && gz > 0 && gz < LT.m));
+        fo[k] = in ? static_cast<unsigned>(gx) + static_cast<unsigned>(LT.n1) *
+                         (static_cast<unsigned>(gy) + static_cast<unsigned>(LT.n1) * static_cast<unsigned>(gz))
+                   : 0xffffffffu;
+        own[k] = in ? ld(a.scT + fo[k]) : make_double2(0.0, 0.0);
+    }
+    // (2) every ancestor box's sc (and si) into shared memory, all copies in flight at once
+    for (int l = 0; l < T; ++l) {
+        const PyrLevel L = slv[l];
+        const int s0 = bsz[l][0], s1 = bsz[l][1], s2 = bsz[l][2];
+        if (tx >= s0) continue;
+        double2* td = pyr + soff[l];
+        for (int z = 0; z < s2; ++z)
+            for (int y = ty; y < s1; y += kPyrTY) {
+                const unsigned f = static_cast<unsigned>(blo[l][0] + tx) +
+                                   static_cast<unsigned>(L.n1) * (static_cast<unsigned>(blo[l][1] + y) +
+                                                                  static_cast<unsigned>(L.n1) * static_cast<unsigned>(blo[l][2] + z));
+                const int i = tx + s0 * (y + s1 * z);
+                cp_async16(td + i, L.sc + f);
+                if (a.bpx) cp_async16(td + scap[l] + i, L.si + f);
+            }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    // (3) td_l = sc_l + P td_{l-1} (- P si_{l-1}) off the boundary, coarsest first, in place
+    for (int l = 1; l < T; ++l) {
+        const int m = slv[l].m, mp = slv[l - 1].m;
+        const int s0 = bsz[l][0], s1 = bsz[l][1], s2 = bsz[l][2];
+        const int p0 = bsz[l - 1][0], p1 = bsz[l - 1][1];
+        double2* td = pyr + soff[l];
+        const double2* ptd = pyr + soff[l - 1];
+        const int g0 = blo[l][0] + tx;
+        if (tx < s0 && g0 > 0 && g0 < m) {
+            int q[3], rel[3];
+            q[0] = min(g0 / 3, mp - 1);
+            rel[0] = g0 - 3 * q[0];
+            q[0] -= blo[l - 1][0];
+            for (int z = 0; z < s2; ++z) {
+                const int g2 = blo[l][2] + z;
+                if (P == 3) {
+                    if (g2 <= 0 || g2 >= m) continue;
+                    q[2] = min(g2 / 3, mp - 1);
+                    rel[2] = g2 - 3 * q[2];
+                    q[2] -= blo[l - 1][2];
+                }
+                for (int y = ty; y < s1; y += kPyrTY) {
+                    const int g1 = blo[l][1] + y;
+                    if (g1 <= 0 || g1 >= m) continue;
+                    q[1] = min(g1 / 3, mp - 1);
+                    rel[1] = g1 - 3 * q[1];
+                    q[1] -= blo[l - 1][1];
+                    const int i = tx + s0 * (y + s1 * z);
+                    double2 v = add(td[i], prolong_box<P>(ptd, p0, p0 * p1, q, rel));
+                    const bool cp = rel[0] == 0 && rel[1] == 0 && (P == 2 || rel[2] == 0);
+                    if (a.bpx && !cp) v = sub(v, prolong_box<P>(ptd + scap[l - 1], p0, p0 * p1, q, rel));
+                    td[i] = v;
+                }
+            }
+        }
+        __syncthreads();
+    }
+    // (4) level T: the CTA's tile, in place
+    const int mp = slv[T - 1].m;
+    const double2* ptd = pyr + soff[T - 1];
+    const int p0 = bsz[T - 1][0], p1 = bsz[T - 1][1];
+    int q[3], rel[3];
+    q[0] = min(gx / 3, mp - 1);
+    rel[0] = gx - 3 * q[0];
+    q[0] -= blo[T - 1][0];
+#pragma unroll
+    for (int k = 0; k < kPyrK; ++k) {
+        if (fo[k] == 0xffffffffu) continue;
+        const int gy = blo[T][1] + ty + (P == 2 ? kPyrTY * k : 0), gz = P == 3 ? blo[T][2] + k : 0;
+        q[1] = min(gy / 3, mp - 1);
+        rel[1] = gy - 3 * q[1];
+        q[1] -= blo[T - 1][1];
+        if (P == 3) {
+            q[2] = min(gz / 3, mp - 1);
+            rel[2] = gz - 3 * q[2];
+            q[2] -= blo[T - 1][2];
+        }
+        double2 v = add(own[k], prolong_box<P>(ptd, p0, p0 * p1, q, rel));
+        const bool cp = rel[0] == 0 && rel[1] == 0 && (P == 2 || rel[2] == 0);
+        if (a.bpx && !cp) v = sub(v, prolong_box<P>(ptd + scap[T - 1], p0, p0 * p1, q, rel));
+        a.scT[fo[k]] = v;
+    }
+}
+
 
 // ---- coarse chains: every coarse level of one cycle phase in one launch -----
 //
@@ -735,6 +941,308 @@ __global__ void __launch_bounds__(kChainThreads) k_chain_up(ChainArgs a) {
     }
 }
 
+
+// ---- bottom-up helpers -------------------------------------------------------
+template <int P>
+__device__ __forceinline__ void smooth_point(const ChainArgs& a, const Lvl& c, const Lvl& par, const LevelCoef& k,
+                                             unsigned f, double2 rh) {
+    int idx[P];
+    dev::unflat<P>(f, c.n1, idx);
+    if (a.bpx && c.si) {
+        c.si[f] = ldcg(c.sinext + f);
+        c.sinext[f] = make_double2(0.0, 0.0);
+    }
+    if (dev::on_boundary<P>(idx, static_cast<int>(c.m)) || c.level < a.ellMin) {
+        c.sc[f] = make_double2(0.0, 0.0);
+        return;
+    }
+    const bool cp = dev::is_cpoint<P>(idx);
+    const double2 smooth = mul(rh, k.invDiag);
+    c.sc[f] = stage(smooth, k.wRaw, cp, a.bpx, a.hb);
+    if (a.bpx && c.level > a.ellMin && cp) {
+        int wi[P];
+#pragma unroll
+        for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+        par.sinext[dev::flat<P>(wi, par.n1)] = mul(k.wRaw, smooth);
+    }
+}
+
+// R r from a full level lattice in shared memory (chain_restrict's arithmetic)
+template <int P>
+__device__ __forceinline__ double2 restrict_from(const double2* r, unsigned n1) {
+    const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+    const int sy = static_cast<int>(n1), sz = static_cast<int>(n1 * n1);
+    double2 acc = make_double2(0.0, 0.0);
+    if (P == 2) {
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+            double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                const double2 v = r[(j - 2) * sy + (i - 2)];
+                row.x = fma(w[i], v.x, row.x);
+                row.y = fma(w[i], v.y, row.y);
+            }
+            acc.x = fma(w[j], row.x, acc.x);
+            acc.y = fma(w[j], row.y, acc.y);
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            double2 pl = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int j = 0; j < 5; ++j) {
+                double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const double2 v = r[(k - 2) * sz + (j - 2) * sy + (i - 2)];
+                    row.x = fma(w[i], v.x, row.x);
+                    row.y = fma(w[i], v.y, row.y);
+                }
+                pl.x = fma(w[j], row.x, pl.x);
+                pl.y = fma(w[j], row.y, pl.y);
+            }
+            acc.x = fma(w[k], pl.x, acc.x);
+            acc.y = fma(w[k], pl.y, acc.y);
+        }
+    }
+    return acc;
+}
+
+
+// ---- bottom-up chain, cooperative form (see fast.cuh) ------------------------
+// Step l (l = top .. 1): r_l = R r_{l+1} (source a.fine for l = top) and the
+// smoothing of l on the value just formed, one grid barrier per step while
+// the source level is big; once it has at most kUpSingle points the CTA that
+// arrives last at a counter runs the remaining steps alone in shared memory.
+// Same arithmetic as restrict + k_chain_up, bit for bit.
+constexpr unsigned kUpSingle = 1200;
+
+template <int P>
+__device__ __forceinline__ void up_step_multi(const ChainArgs& a, const Lvl& src, const Lvl& c, const Lvl& par,
+                                              const LevelCoef& k, bool restrictIt, unsigned tid, unsigned stride) {
+    if (P == 3) {  // lane groups of 8 per coarse vertex (chain_restrict3), lane 0 smooths
+        const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+        const long long sy = src.n1, sz = static_cast<long long>(src.n1) * src.n1;
+        const unsigned lane = threadIdx.x & 31u, grp = lane >> 3, kk = lane & 7u;
+        const unsigned warp = tid >> 5, warps = stride >> 5;
+        for (unsigned base = warp * 4u; base < c.n; base += warps * 4u) {
+            const unsigned f = base + grp;
+            int W[3] = {0, 0, 0};
+            bool act = f < c.n, interior = false;
+            if (act) {
+                dev::unflat<3>(f, c.n1, W);
+                interior = !dev::on_boundary<3>(W, static_cast<int>(c.m));
+            }
+            double2 pl = make_double2(0.0, 0.0);
+            if (restrictIt && act && interior && kk < 5) {
+                const double2* __restrict__ r =
+                    src.rhat + (3LL * W[0] + sy * (3LL * W[1]) + sz * (3LL * W[2])) + (static_cast<int>(kk) - 2) * sz;
+#pragma unroll
+                for (int j = 0; j < 5; ++j) {
+                    double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) {
+                        const double2 v = ldcg(r + (j - 2) * sy + (i - 2));
+                        row.x = fma(w[i], v.x, row.x);
+                        row.y = fma(w[i], v.y, row.y);
+                    }
+                    pl.x = fma(w[j], row.x, pl.x);
+                    pl.y = fma(w[j], row.y, pl.y);
+                }
+            }
+            double2 acc = make_double2(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 5; ++q) {
+                const double px = __shfl_sync(0xffffffffu, pl.x, (grp << 3) + q);
+                const double py = __shfl_sync(0xffffffffu, pl.y, (grp << 3) + q);
+                acc.x = fma(w[q], px, acc.x);
+                acc.y = fma(w[q], py, acc.y);
+            }
+            if (act && kk == 0) {
+                if (restrictIt && interior) c.rhat[f] = acc;
+                smooth_point<3>(a, c, par, k, f, restrictIt ? acc : make_double2(0.0, 0.0));
+            }
+        }
+    } else {
+        for (unsigned f = tid; f < c.n; f += stride) {
+            int W[P];
+            dev::unflat<P>(f, c.n1, W);
+            double2 acc = make_double2(0.0, 0.0);
+            if (restrictIt && !dev::on_boundary<P>(W, static_cast<int>(c.m))) {
+                unsigned centre = 0, s = 1;
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    centre += 3u * static_cast<unsigned>(W[d]) * s;
+                    s *= src.n1;
+                }
+                const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
+                const double2* __restrict__ r = src.rhat + centre;
+                const long long sy = src.n1;
+                if (P == 1) {
+#pragma unroll
+                    for (int i = 0; i < 5; ++i) {
+                        const double2 v = ldcg(r + (i - 2));
+                        acc.x = fma(w[i], v.x, acc.x);
+                        acc.y = fma(w[i], v.y, acc.y);
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 5; ++j) {
+                        double2 row = make_double2(0.0, 0.0);
+#pragma unroll
+                        for (int i = 0; i < 5; ++i) {
+                            const double2 v = ldcg(r + (j - 2) * sy + (i - 2));
+                            row.x = fma(w[i], v.x, row.x);
+                            row.y = fma(w[i], v.y, row.y);
+                        }
+                        acc.x = fma(w[j], row.x, acc.x);
+                        acc.y = fma(w[j], row.y, acc.y);
+                    }
+                }
+                c.rhat[f] = acc;
+            }
+            smooth_point<P>(a, c, par, k, f, acc);
+        }
+    }
+}
+
+template <int NT>
+__device__ __forceinline__ void chain_norms(const ChainArgs& a) {  // K5 (k_chain_up's tree and order)
+    __shared__ double smax[NT], ssum[NT];
+    double mx = 0.0, sm = 0.0;
+    for (int i = threadIdx.x; i < a.normBlocks; i += NT) {
+        mx = fmax(mx, a.normPartials[2 * i]);
+        sm += a.normPartials[2 * i + 1];
+    }
+    smax[threadIdx.x] = mx;
+    ssum[threadIdx.x] = sm;
+    __syncthreads();
+    for (int s = NT / 2; s > 0; s >>= 1) {
+        if (threadIdx.x < s) {
+            smax[threadIdx.x] = fmax(smax[threadIdx.x], smax[threadIdx.x + s]);
+            ssum[threadIdx.x] += ssum[threadIdx.x + s];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.normOut[0] = smax[0];
+        a.normOut[1] = ssum[0];
+    }
+}
+
+template <int P>
+__global__ void __launch_bounds__(kChainThreads) k_up_coop(const ChainArgs a, unsigned* count) {
+    extern __shared__ __align__(16) double2 us[];  // last CTA: r (and BPX si_next) of the small levels
+    __shared__ unsigned lastFlag;
+    unsigned gen = *reinterpret_cast<volatile unsigned*>(a.bar + 1);
+    const unsigned tid = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    const int top = a.top;
+    // multi-CTA steps
+    int l = top;
+    for (; l >= 1; --l) {
+        const Lvl src = l == top ? a.fine : a.lv[l + 1];
+        if (src.n <= kUpSingle) break;
+        const bool restrictIt = l >= a.ellMin;
+        up_step_multi<P>(a, src, a.lv[l], a.lv[l - 1], a.k[l], restrictIt, tid, stride);
+        if (l > 1) {
+            const Lvl nsrc = a.lv[l];
+            if (nsrc.n > kUpSingle) grid_barrier(a.bar, gen, 0);
+        }
+    }
+    // the remaining steps: the CTA arriving last; norms: the one arriving first.
+    // bar.sync orders the CTA's writes before thread 0's (cumulative) fence + arrival
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned arr = atomicAdd(count, 1u);
+        lastFlag = arr == gridDim.x - 1 ? 1u : arr == 0 ? 2u : 0u;
+        __threadfence();
+    }
+    __syncthreads();
+    if (lastFlag == 2u || (lastFlag == 1u && gridDim.x == 1)) {
+        if (a.normOut) chain_norms<kChainThreads>(a);
+        if (gridDim.x > 1) return;
+    }
+    if (!lastFlag) return;
+    if (l < 1) {
+        if (threadIdx.x == 0) *count = 0u;
+        return;
+    }
+    // shared memory: r of levels l+1 .. 1 (level l+1 = the source of the first step), si_next of l .. 1 (BPX)
+    int offR[kMaxChainLevels + 1], offS[kMaxChainLevels + 1];
+    {
+        int o = 0;
+        for (int j = l + 1; j >= 1; --j) {
+            const unsigned n = j == top + 1 ? a.fine.n : a.lv[j].n;
+            offR[j] = o;
+            o += static_cast<int>(n);
+            if (a.bpx && j <= l) {
+                offS[j] = o;
+                o += static_cast<int>(n);
+            }
+        }
+    }
+    {
+        const Lvl src = l == top ? a.fine : a.lv[l + 1];
+        for (unsigned f = threadIdx.x; f < src.n; f += blockDim.x) cp_async16(us + offR[l + 1] + f, src.rhat + f);
+        if (a.bpx)
+            for (int j = l; j >= 1; --j) {
+                const Lvl c = a.lv[j];
+                if (!c.si) continue;
+                for (unsigned f = threadIdx.x; f < c.n; f += blockDim.x) cp_async16(us + offS[j] + f, c.sinext + f);
+            }
+        asm volatile("cp.async.wait_all;" ::: "memory");
+        __syncthreads();
+    }
+    for (; l >= 1; --l) {
+        const Lvl c = a.lv[l], par = a.lv[l - 1];
+        const unsigned srcN1 = l == top ? a.fine.n1 : a.lv[l + 1].n1;
+        const LevelCoef k = a.k[l];
+        const double2* rsrc = us + offR[l + 1];
+        double2* r = us + offR[l];
+        const bool restrictIt = l >= a.ellMin;
+        for (unsigned f = threadIdx.x; f < c.n; f += blockDim.x) {
+            int idx[P];
+            dev::unflat<P>(f, c.n1, idx);
+            const bool bnd = dev::on_boundary<P>(idx, static_cast<int>(c.m));
+            double2 acc = make_double2(0.0, 0.0);
+            if (restrictIt && !bnd) {
+                unsigned centre = 0, s = 1;
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    centre += 3u * static_cast<unsigned>(idx[d]) * s;
+                    s *= srcN1;
+                }
+                acc = restrict_from<P>(rsrc + centre, srcN1);
+                c.rhat[f] = acc;
+            }
+            r[f] = acc;
+            if (a.bpx && c.si) {
+                c.si[f] = us[offS[l] + f];
+                c.sinext[f] = make_double2(0.0, 0.0);
+            }
+            if (bnd || c.level < a.ellMin) {
+                c.sc[f] = make_double2(0.0, 0.0);
+                continue;
+            }
+            const bool cp = dev::is_cpoint<P>(idx);
+            const double2 smooth = mul(acc, k.invDiag);
+            c.sc[f] = stage(smooth, k.wRaw, cp, a.bpx, a.hb);
+            if (a.bpx && c.level > a.ellMin && cp) {
+                int wi[P];
+#pragma unroll
+                for (int d = 0; d < P; ++d) wi[d] = idx[d] / 3;
+                const unsigned g = dev::flat<P>(wi, par.n1);
+                const double2 v = mul(k.wRaw, smooth);
+                par.sinext[g] = v;
+                if (l - 1 >= 1 && par.si) us[offS[l - 1] + g] = v;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *count = 0u;  // re-arm for the next launch
+}
 }  // namespace
 
 template <int P>
@@ -789,6 +1297,36 @@ void chain_up(int P, const ChainArgs& a, int grid, cudaStream_t s) {
     else launch_chain(k_chain_up<3>, a, grid, s);
 }
 
+
+size_t up_coop_smem(int P, const ChainArgs& a) {
+    int l = a.top;
+    for (; l >= 1; --l) {
+        const unsigned n = l == a.top ? a.fine.n : a.lv[l + 1].n;
+        if (n <= kUpSingle) break;
+    }
+    if (l < 1) return 0;
+    size_t pts = 0;
+    for (int j = l + 1; j >= 1; --j) {
+        const unsigned n = j == a.top + 1 ? a.fine.n : a.lv[j].n;
+        pts += n * ((a.bpx && j <= l) ? 2u : 1u);
+    }
+    (void)P;
+    return pts * sizeof(double2);
+}
+
+void up_coop(int P, const ChainArgs& a, unsigned* count, int smCount, cudaStream_t s) {
+    const size_t smem = up_coop_smem(P, a);
+    void* args[] = {const_cast<ChainArgs*>(&a), &count};
+    const void* k = P == 1 ? reinterpret_cast<const void*>(k_up_coop<1>)
+                    : P == 2 ? reinterpret_cast<const void*>(k_up_coop<2>)
+                             : reinterpret_cast<const void*>(k_up_coop<3>);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    int per = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kChainThreads, smem) != cudaSuccess || per < 1) per = 1;
+    const int grid = std::min(per, 2) * smCount;
+    cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kChainThreads), args, smem, s);
+}
+
 int chain_cluster_size() {
     // the largest cluster the chain kernels can run as (16 needs the non-portable opt-in)
     cudaFuncSetAttribute(k_chain_up<3>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
@@ -836,12 +1374,59 @@ void correct_fine(int P, const Lvl& f, const Lvl& pr, int bpx, int blocks, cudaS
     else k_topdown<3, true><<<blocks, 256, 0, s>>>(f, pr, bpx, 0u, f.n);
 }
 
+size_t pyramid_setup(int P, PyrArgs& a, int T) {
+    const int bz = kPyrK;
+    a.T = T;
+    a.bz = bz;
+    const int n1 = a.lv[T].n1;
+    const int ext[3] = {kPyrTX, P == 3 ? kPyrTY : kPyrTY * bz, bz};
+    a.nbx = (n1 + ext[0] - 1) / ext[0];
+    a.nby = (n1 + ext[1] - 1) / ext[1];
+    // box extents: s_{l-1} <= ceil((s_l - 1) / 3) + 2, at most the level's n1
+    int sz[3] = {ext[0], ext[1], ext[2]};
+    int off = 0;
+    for (int l = T - 1; l >= 0; --l) {
+        int cap = 1;
+        for (int d = 0; d < P; ++d) {
+            sz[d] = std::min((sz[d] - 1 + 2) / 3 + 2, a.lv[l].n1);
+            cap *= sz[d];
+        }
+        a.cap[l] = cap;
+        a.off[l] = off;
+        off += 2 * cap;  // td, si
+    }
+    return static_cast<size_t>(off) * sizeof(double2);
+}
+
+void topdown_pyramid(int P, const PyrArgs& a, size_t smem, cudaStream_t s) {
+    const int n1 = a.lv[a.T].n1;
+    const int nbz = P == 3 ? (n1 + a.bz - 1) / a.bz : 1;
+    const unsigned blocks = static_cast<unsigned>(a.nbx) * a.nby * nbz;
+    if (P == 2) {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_topdown_pyr<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_topdown_pyr<2><<<blocks, kPyrTX * kPyrTY, smem, s>>>(a);
+    } else {
+        if (smem > 48 * 1024) cudaFuncSetAttribute(k_topdown_pyr<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        k_topdown_pyr<3><<<blocks, kPyrTX * kPyrTY, smem, s>>>(a);
+    }
+}
+
 void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cudaStream_t s, int za, int zb) {
     if (P == 3 && c.m == 27) {  // row kernel: small levels, where per-thread latency dominated: interior planes of [za, zb)
         const int zlo = std::max(1, za < 0 ? 1 : za), zhi = std::min(static_cast<int>(c.m), za < 0 ? static_cast<int>(c.m) : zb);
         if (zhi <= zlo) return;
         const size_t smem = (bpx ? 8 : 4) * pr.n1 * sizeof(double2);
         k_topdown3_rows<<<dim3(c.m - 1, zhi - zlo), kRowThreads, smem, s>>>(c, pr, bpx, zlo);
+        return;
+    }
+    const char* tri = std::getenv("TMG_TRI_COARSE");
+    if (P >= 2 && c.m >= 243 && !(tri && tri[0] == '0')) {  // big levels: parent-cell triples (k_topdown_tri)
+        const unsigned plane = P == 3 ? c.n1 : 1u;  // rows per plane of the last axis
+        const unsigned ra = za < 0 ? 0u : static_cast<unsigned>(za) * plane;
+        const unsigned rb = za < 0 ? c.n / c.n1 : std::min<unsigned>(static_cast<unsigned>(zb) * plane, c.n / c.n1);
+        if (rb <= ra) return;
+        if (P == 2) k_topdown_tri<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
+        else k_topdown_tri<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
         return;
     }
     unsigned fa, fb;
@@ -891,21 +1476,29 @@ int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s) {
 }
 
 void restrict_level(int P, const Lvl& fine, const Lvl& coarse, const double*, int blocks, cudaStream_t s, int za,
-                    int zb) {
+                    int zb, const ResArgs* smooth) {
+    const ResArgs sa = smooth ? *smooth : ResArgs{};
     if (P == 3 && coarse.m == 27) {  // small levels only (big ones are faster grid-stride)
         const int zlo = std::max(1, za < 0 ? 1 : za);
         const int zhi = std::min(static_cast<int>(coarse.m), za < 0 ? static_cast<int>(coarse.m) : zb);
         if (zhi <= zlo) return;
         const size_t smem = 25 * (coarse.m - 1) * sizeof(double2);
-        k_restrict3_rows<<<dim3(coarse.m - 1, zhi - zlo), kRowThreads, smem, s>>>(fine, coarse, zlo);
+        if (smooth) k_restrict3_rows<true><<<dim3(coarse.m - 1, zhi - zlo), kRowThreads, smem, s>>>(fine, coarse, zlo, sa);
+        else k_restrict3_rows<false><<<dim3(coarse.m - 1, zhi - zlo), kRowThreads, smem, s>>>(fine, coarse, zlo, sa);
         return;
     }
     unsigned fa, fb;
     span(P, coarse, za, zb, fa, fb);
     if (fb <= fa) return;
-    if (P == 1) k_restrict<1><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb);
-    else if (P == 2) k_restrict<2><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb);
-    else k_restrict<3><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb);
+    if (smooth) {
+        if (P == 1) k_restrict<1, true><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
+        else if (P == 2) k_restrict<2, true><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
+        else k_restrict<3, true><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
+        return;
+    }
+    if (P == 1) k_restrict<1><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
+    else if (P == 2) k_restrict<2><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
+    else k_restrict<3><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
 }
 
 void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s, int za, int zb) {

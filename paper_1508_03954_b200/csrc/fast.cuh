@@ -51,8 +51,10 @@ void load_vector(int P, const dev::Lvl& F, const double2* f, double2 ms, int blo
 int residual_fine(int P, const ResArgs& a, int smCount, cudaStream_t s);
 int residual_fine_blocks(int P, const dev::Lvl& f, int smCount);
 // r_{l-1} = R r_l on interior coarse vertices (rhat arrays).
+// smooth != nullptr: also the coarse level's smoothing (smooth_coarse) on the
+// interior points, on the value just formed.
 void restrict_level(int P, const dev::Lvl& fine, const dev::Lvl& coarse, const double* weights, int blocks,
-                    cudaStream_t s, int za = -1, int zb = -1);
+                    cudaStream_t s, int za = -1, int zb = -1, const ResArgs* smooth = nullptr);
 // Coarse chains (one cooperative launch per phase, grid barrier between levels):
 //   chain_down: top-down of levels 1..top;
 //   chain_up:   [restrict fine -> top,] then for l = top..1 smoothing of l and
@@ -76,6 +78,38 @@ int chain_grid(int P, int smCount);
 int chain_cluster_size();
 void chain_down(int P, const ChainArgs& a, int grid, cudaStream_t s);
 void chain_up(int P, const ChainArgs& a, int grid, cudaStream_t s);
+// The whole bottom-up below the level a.fine (its r complete and smoothed):
+// for l = top .. 1 restriction into l fused with the smoothing of l, grid
+// barriers between big steps, the small steps on the last CTA (cooperative
+// launch, up to two CTAs per SM; count: zeroed counter, re-armed by the kernel).
+size_t up_coop_smem(int P, const ChainArgs& a);
+void up_coop(int P, const ChainArgs& a, unsigned* count, int smCount, cudaStream_t s);
+
+// Every coarse top-down of one cycle in one launch without a grid-wide
+// barrier ("pyramid"): each CTA owns a box of level T and rebuilds in shared
+// memory the ancestor boxes (levels T-1 .. 0) its prolongation needs, each
+// from the one above it; only level T is written (the intermediate levels'
+// top-down values are transients: the bottom-up overwrites their sc).  Same
+// arithmetic as chain_down + topdown_coarse, bit for bit.  P = 2, 3.
+constexpr int kPyrMaxLevels = 16;
+struct PyrLevel {
+    const double2* sc;
+    const double2* si;
+    int m, n1;
+};
+struct PyrArgs {
+    PyrLevel lv[kPyrMaxLevels];
+    double2* scT;         // level T sc, updated in place
+    int T, bpx;
+    int bz;               // points per thread (tile extent along the last axis / rows / 8)
+    int nbx, nby;         // tiles along axes 0, 1
+    int off[kPyrMaxLevels];  // shared-memory offset (double2) of level l's box (td, then si)
+    int cap[kPyrMaxLevels];  // box capacity (points) of level l
+};
+// Builds the launch geometry for level T of the given levels (sc / si / m / n1
+// of levels 0..T); returns the dynamic shared memory bytes.
+size_t pyramid_setup(int P, PyrArgs& a, int T);
+void topdown_pyramid(int P, const PyrArgs& a, size_t smem, cudaStream_t s);
 
 // Coarse smoothing: sc_l = omega r_l / diag, si commit, BPX injection into l-1.
 void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s, int za = -1, int zb = -1);

@@ -214,7 +214,8 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     dev::block_norms(nmax, nsum, a.norms);
 }
 
-__global__ void __launch_bounds__(256) k_combine2(const Args a, double2* rc) {
+template <bool SMOOTH>
+__global__ void __launch_bounds__(256) k_combine2(const Args a, double2* rc, const fast::ResArgs sa) {
     const int mc = a.g.mc, m = a.g.m, yc = a.g.yc;
     const unsigned n1c = a.n1c;
     const unsigned total = n1c * n1c;
@@ -232,6 +233,22 @@ __global__ void __launch_bounds__(256) k_combine2(const Args a, double2* rc) {
             }
         }
         rc[f] = acc;
+        if (SMOOTH) {  // level L-1 smoothing (k_smooth_coarse) on the value just formed (fused3::k_combine<true>)
+            const dev::Lvl& cl = sa.lv;
+            if (sa.bpx && cl.si) {
+                cl.si[f] = cl.sinext[f];
+                cl.sinext[f] = zero2();
+            }
+            if (cl.level < sa.ellMin) {
+                cl.sc[f] = zero2();
+                continue;
+            }
+            const bool cp = (W0 % 3 == 0) && (W1 % 3 == 0);
+            const double2 smooth = mul(acc, sa.k.invDiag);
+            cl.sc[f] = stage_sc(smooth, sa.k.wRaw, cp, sa.bpx, sa.hb);
+            if (sa.bpx && cl.level > sa.ellMin && cp)
+                sa.par.sinext[(W0 / 3) + sa.par.n1 * (W1 / 3)] = mul(sa.k.wRaw, smooth);
+        }
     }
 }
 
@@ -263,10 +280,11 @@ void launch(const Args& a, cudaStream_t s) {
     else k_fused2<false><<<grid, TX, 0, s>>>(a);
 }
 
-void combine(const Args& a, double2* rCoarse, cudaStream_t s) {
+void combine(const Args& a, double2* rCoarse, cudaStream_t s, const fast::ResArgs* smooth) {
     const unsigned total = a.n1c * a.n1c;
     const unsigned nb = std::max(1u, std::min((total + 255) / 256, 4096u));
-    k_combine2<<<nb, 256, 0, s>>>(a, rCoarse);
+    if (smooth) k_combine2<true><<<nb, 256, 0, s>>>(a, rCoarse, *smooth);
+    else k_combine2<false><<<nb, 256, 0, s>>>(a, rCoarse, fast::ResArgs{});
 }
 
 }  // namespace fused2

@@ -50,7 +50,9 @@ Geometry geometry(int m, int mc, int smCount);
 size_t partial_count(const Geometry& g);
 int blocks(const Geometry& g);
 void launch(const Args& a, cudaStream_t s);
-void combine(const Args& a, double2* rCoarse, cudaStream_t s);
+// smooth != nullptr: also the level L-1 smoothing (fast::smooth_coarse) on the
+// interior points, as fused3::combine
+void combine(const Args& a, double2* rCoarse, cudaStream_t s, const fast::ResArgs* smooth = nullptr);
 
 }  // namespace fused2
 }  // namespace tmg

@@ -5,6 +5,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdint>
 #include <type_traits>
 
@@ -492,6 +493,7 @@ Geometry geometry(int m, int mc, int parts, int resident) {
     // at least 8 chunks and ~2 waves of blocks (measured best at 243^3 and
     // 729^3; a finer wave model did not pay), in multiples of `parts`
     int want = std::max(8, (2 * std::max(1, resident) + tiles - 1) / tiles);
+    if (const char* e = std::getenv("TMG_ZCHUNKS")) want = std::max(1, std::atoi(e));  // developer A/B
     want = (want + parts - 1) / parts * parts;
     for (;; want += parts) {
         g.zc = std::max(3, ((inner + want - 1) / want + 2) / 3 * 3);

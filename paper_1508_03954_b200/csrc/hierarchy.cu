@@ -1126,12 +1126,14 @@ struct Hierarchy::Impl {
         const int top = chain_top(L - 1);
         const bool useChain = top >= 1;
         fast::ChainArgs ch{};
-        if (useChain) {
-            ch = make_chain(pol, n, top);
-            fast::chain_down(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
+        if (useChain) ch = make_chain(pol, n, top);
+        if (use_pyramid()) {
+            topdown_all(bpx);
+        } else {
+            if (useChain) fast::chain_down(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
+            for (int l = useChain ? top + 1 : 1; l < L; ++l)
+                fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
         }
-        for (int l = useChain ? top + 1 : 1; l < L; ++l)
-            fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
         if (P == 2 && fused2on) {
             fused2::Args fa{};
@@ -1158,6 +1160,15 @@ struct Hierarchy::Impl {
             fa.level = L;
             fused2::launch(fa, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+            if (use_up()) {  // combine + level L-1 smoothing, then the whole bottom-up in one launch
+                const fast::ResArgs sL = args(L - 1);
+                fused2::combine(fa, lv[L - 1].rhat, stream, &sL);
+                std::swap(F.u, uAlt);
+                up_all(pol, n, fused2::blocks(geo2));
+                TMG_CUDA(cudaGetLastError());
+                coarseUStale = true;
+                return;
+            }
             fused2::combine(fa, lv[L - 1].rhat, stream);
             std::swap(F.u, uAlt);
             for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
@@ -1203,9 +1214,16 @@ struct Hierarchy::Impl {
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             const int lo = useChain ? top + 1 : 1;
             const fast::ResArgs sL = args(L - 1);
-            fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream, -1, -1, lo <= L - 1 ? &sL : nullptr);
+            fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream, -1, -1,
+                            (use_up() || lo <= L - 1) ? &sL : nullptr);
             std::swap(F.u, uAlt);
             std::swap(mapU[0], mapU[1]);
+            if (use_up()) {
+                up_all(pol, n, fused3::blocks(geo));
+                TMG_CUDA(cudaGetLastError());
+                coarseUStale = true;
+                return;
+            }
             for (int l = L - 1; l >= lo; --l) {
                 if (l < L - 1 && l >= prob.ellMin)
                     fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
@@ -1271,6 +1289,64 @@ struct Hierarchy::Impl {
         }
     }
 
+    // bottom-up below level L-1 (r_{L-1} complete and smoothed) as one cooperative launch
+    // (levels above the chain top S: restriction + smoothing kernels; S-1 .. 1:
+    // fast::up_coop, which restricts out of S)
+    bool use_up() const {
+        const char* e = std::getenv("TMG_UP");  // developer A/B (read per call: tests flip it in-process)
+        return !(e && e[0] == '0') && chainBar && (p == 2 || p == 3) && chain_top(L - 1) >= 2;
+    }
+    void up_all(const Policy& pol, int n, int normBlocks) {
+        const int S = chain_top(L - 1);
+        for (int l = L - 2; l >= S; --l) {
+            fast::ResArgs sl{};
+            sl.lv = lv[l];
+            sl.par = lv[l - 1];
+            sl.k = fc[l];
+            const Cplx w = omega_unmasked(pol, L - l, n);
+            sl.k.wRaw = make_double2(w.real(), w.imag());
+            sl.ellMin = prob.ellMin;
+            sl.bpx = pol.bpx ? 1 : 0;
+            sl.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
+            sl.partials = partials;
+            if (l >= prob.ellMin) fast::restrict_level(p, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream, -1, -1, &sl);
+            else fast::smooth_coarse(p, sl, blocks_for(lv[l].n), stream);
+        }
+        fast::ChainArgs ch = make_chain(pol, n, S - 1);  // fine = level S
+        ch.firstRestrict = 1;
+        ch.normBlocks = normBlocks;
+        fast::up_coop(p, ch, chainBar + 2, smCount, stream);
+    }
+
+    // coarse top-down of levels 1..L-1 as one pyramid launch (fast::topdown_pyramid)
+    bool use_pyramid() const {
+        const char* e = std::getenv("TMG_PYR");  // developer A/B (read per call: tests flip it in-process)
+        const bool off = e && e[0] == '0';
+        return !off && (p == 2 || p == 3) && L >= 2 && L - 1 < fast::kPyrMaxLevels;
+    }
+    // pyramid up to the highest level below kPyrMaxN points, per-level launches above it
+    static constexpr unsigned kPyrMaxN = 1u << 21;
+    int pyramid_top() const {
+        int T = L - 1;
+        while (T > 1 && lv[T].n > kPyrMaxN) --T;
+        return T;
+    }
+    void topdown_all(int bpx) {
+        fast::PyrArgs a{};
+        const int T = pyramid_top();
+        for (int l = 0; l <= T; ++l) {
+            a.lv[l].sc = lv[l].sc;
+            a.lv[l].si = lv[l].si ? lv[l].si : lv[l].sc;  // si is read only under BPX
+            a.lv[l].m = static_cast<int>(lv[l].m);
+            a.lv[l].n1 = static_cast<int>(lv[l].n1);
+        }
+        a.scT = lv[T].sc;
+        a.bpx = bpx;
+        const size_t smem = fast::pyramid_setup(p, a, T);
+        fast::topdown_pyramid(p, a, smem, stream);
+        for (int l = T + 1; l < L; ++l) fast::topdown_coarse(p, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+    }
+
     // highest level <= maxLevel of the coarse chain (every level below kChainMaxN
     // points joins it); 0 when chains are off
     int chain_top(int maxLevel) const {
@@ -1308,8 +1384,9 @@ struct Hierarchy::Impl {
         const bool useChain = top >= 1;
         const bool fusedPath = (p == 3 && fused) || (p == 2 && fused2on);
         const int lo = useChain ? top + 1 : 1;
-        int n = useChain ? 1 + (L - 1 - top) : (L - 1);  // top-down
+        int n = use_pyramid() ? 1 + (L - 1 - pyramid_top()) : useChain ? 1 + (L - 1 - top) : (L - 1);  // top-down
         n += 2;                                            // fine pass (+ combine, or correction + residual)
+        if (fusedPath && use_up()) return n + (L - 1 - top) + 1;  // restrict + smooth above the chain top, up_coop
         for (int l = L - 1; l >= lo; --l)
             n += (p == 3 && fused && l == L - 1 ? 0 : 1) + ((fusedPath ? l < L - 1 : true) && l >= prob.ellMin ? 1 : 0);
         if (useChain) n += 1 + (fusedPath && top < L - 1 && top >= prob.ellMin ? 1 : 0);
@@ -1492,7 +1569,7 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
         TMG_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, prob.device));
         if (coop && !(cz && cz[0] == '0')) {
             I.chainGrid = fast::chain_grid(I.p, I.smCount);
-            I.chainBar = I.alloc<unsigned>(2);
+            I.chainBar = I.alloc<unsigned>(3);  // grid barrier (2) + up_coop's last-CTA counter
             const char* cl = std::getenv("TMG_CHAIN_CLUSTER");
             if (!(cl && cl[0] == '0')) I.clusterSize = fast::chain_cluster_size();
         }
