@@ -35,11 +35,29 @@ __device__ __forceinline__ double2 stage_sc(double2 smooth, double2 w, bool cp, 
     return mul(w, smooth);
 }
 
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src)
+                 : "memory");
+}
+
+// 16-byte cp.async; zero-fills the destination when !valid (src-size 0)
+__device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool valid) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+                 "l"(src), "r"(valid ? 16 : 0)
+                 : "memory");
+}
+
+constexpr int kRing = 4;  // rows in flight
+
 template <bool BPX>
 __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     __shared__ double2 Pb[2][TX + 2];          // corrected rows (x halo at 0 and TX+1)
     __shared__ double2 Vb[BPX ? 4 : 2][CXW];   // y-interpolated coarse rows (sc[, si])
     __shared__ double2 tb[TX];                 // y-restricted columns
+    extern __shared__ __align__(16) double2 Cs[];  // the strip's coarse rows [BPX ? 2 : 1][nq][CXW], staged once
+    __shared__ __align__(16) double2 Ru[kRing][TX + 2];  // row ring: v (own columns + x halo)
+    __shared__ __align__(16) double2 Rb[kRing][TX];      // row ring: b
 
     const int tid = threadIdx.x;
     const int m = a.g.m, mc = a.g.mc;
@@ -66,17 +84,26 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     const bool hcpx = hx % 3 == 0;
     const int hslot = tid == 0 ? 0 : (xe - x0) + 1;
 
+    // coarse rows [qlo, qhi] feeding fine rows y0-1 .. y1, staged once (cp.async)
+    const int qlo = min(max(y0 - 1, 0) / 3, mc - 1), qhi = min(y1 / 3, mc - 1) + 1;
+    const int nq = qhi - qlo + 1;
+    if (tid < CXW) {
+        const int cx = min(cx0 + tid, mc);
+        for (int r = 0; r < nq; ++r) {
+            const long long g = cx + static_cast<long long>(a.n1c) * (qlo + r);
+            cp_async16(Cs + r * CXW + tid, a.scC + g);
+            if (BPX) cp_async16(Cs + (nq + r) * CXW + tid, a.siC + g);
+        }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
     auto computeV = [&](int yy, int vb) {  // coarse rows of fine row yy, for coarse columns cx0 + tid
         if (tid >= CXW) return;
-        const int cx = min(cx0 + tid, mc);
         const int qy = min(max(yy, 0) / 3, mc - 1);
         const double w1y = relw(yy - 3 * qy);
-        const double2* s = a.scC + cx + static_cast<long long>(a.n1c) * qy;
-        Vb[vb][tid] = lerpw(ldg(s), ldg(s + a.n1c), w1y);
-        if (BPX) {
-            const double2* si = a.siC + cx + static_cast<long long>(a.n1c) * qy;
-            Vb[2 + vb][tid] = lerpw(ldg(si), ldg(si + a.n1c), w1y);
-        }
+        const double2* c = Cs + (qy - qlo) * CXW + tid;
+        Vb[vb][tid] = lerpw(c[0], c[CXW], w1y);
+        if (BPX) Vb[2 + vb][tid] = lerpw(c[nq * CXW], c[(nq + 1) * CXW], w1y);
     };
 
     // restriction slots of this strip
@@ -111,18 +138,24 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     double2 accLo = zero2(), accHi = zero2();
     double2 Aprev = zero2(), Acur = zero2();
 
-    // row yy's state v = u + sc (fused3.cuh "v-form"), loaded one step ahead
-    auto loadRow = [&](int yy, double2& u, double2& hu) {
+    // Row ring: row yy's state v = u + sc (fused3.cuh "v-form") and its load
+    // vector b, copied (cp.async, zero-filled off the domain) kRing - 1 rows
+    // ahead into slot (yy - y0 + 1) % kRing; every thread reads back only
+    // what it copied itself, so the ring needs no barrier.
+    auto issueRow = [&](int it2) {
+        const int yy = y0 - 1 + it2, slot = it2 % kRing;
         const bool yin = yy >= 1 && yy <= m - 1;
-        u = hu = zero2();
-        if (yin && owned) u = ldg(a.u + x + n1 * yy);
-        if (yin && hin) hu = ldg(a.u + hx + n1 * yy);
+        const long long row = n1 * (yin ? yy : 1);
+        if (owned) {  // (a column past the strip end would collide with the halo slot)
+            cp_async16z(&Ru[slot][tid + 1], a.u + x + row, yin);
+            cp_async16z(&Rb[slot][tid], a.b + x + row, yy >= y0 && yy < y1);
+        }
+        if (haloThread) cp_async16z(&Ru[slot][hslot], a.u + (hin ? hx : x0) + row, yin && hin);
+        asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    double2 uN, huN, uN2, huN2;  // rows yy + 1 and yy + 2 in flight
-    loadRow(y0 - 1, uN, huN);
-    loadRow(y0, uN2, huN2);
+    for (int i = 0; i < kRing - 1; ++i) issueRow(i);  // empty groups past the chunk keep the count uniform
     double2 cPrev = zero2();
-    double2 bq = (owned && y0 < y1) ? ldg(a.b + x + n1 * y0) : zero2();
+    double2 bq = zero2();
     computeV(y0 - 1, 0);
     __syncthreads();
 
@@ -130,10 +163,12 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         const int yy = y0 - 1 + it;
         const int u3 = it % 3;  // yy % 3 (y0 = 1 mod 3)
         const bool yin = yy >= 1 && yy <= m - 1;
-        const double2 uC = uN, huC = huN;
-        uN = uN2;
-        huN = huN2;
-        if (it + 2 < nrows) loadRow(yy + 2, uN2, huN2);
+        asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 2) : "memory");  // row yy landed
+        const double2 uC = Ru[it % kRing][tid + 1];
+        const double2 huC = haloThread ? Ru[it % kRing][hslot] : zero2();
+        if (it >= 2) bq = Rb[(it - 1) % kRing][tid];  // b of row yy - 1 (the residual row)
+        if (it + kRing - 1 < nrows) issueRow(it + kRing - 1);  // into the slot of row yy - 1
+        else asm volatile("cp.async.commit_group;" ::: "memory");
         const double2* V = Vb[it & 1];
         double2* P = Pb[it & 1];
         // ---- phase B: corrected row yy ----
@@ -170,7 +205,6 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
             const int kz = (u3 + 2) % 3;
             const double2 hu = add(Aprev, T);
             const double2 r = owned ? sub(bq, hu) : zero2();
-            if (owned && yr + 1 < y1) bq = ldg(a.b + x + n1 * (yr + 1));
             const double m2 = fma(r.x, r.x, r.y * r.y);
             nmax = fmax(nmax, m2);
             nsum += m2;
@@ -264,7 +298,7 @@ Geometry geometry(int m, int mc, int smCount) {
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused2<false>, TX, 0) != cudaSuccess || per < 1) per = 4;
     const int resident = 2 * per * std::max(1, smCount);  // two waves of strips
     const int want = std::max(1, (resident + g.nbx - 1) / g.nbx);
-    g.yc = std::max(3, ((inner + want - 1) / want + 2) / 3 * 3);
+    g.yc = std::min(kMaxYc, std::max(3, ((inner + want - 1) / want + 2) / 3 * 3));  // cap: staged coarse rows
     g.nby = (inner + g.yc - 1) / g.yc;
     g.sy = g.yc / 3 + 2;
     return g;
@@ -274,10 +308,22 @@ size_t partial_count(const Geometry& g) { return static_cast<size_t>(g.nby) * g.
 
 int blocks(const Geometry& g) { return g.nbx * g.nby; }
 
+size_t smem_bytes(const Geometry& g, bool bpx) {
+    const int nq = g.yc / 3 + 3;  // coarse rows feeding yc + 2 fine rows
+    return static_cast<size_t>(bpx ? 2 : 1) * nq * CXW * sizeof(double2);
+}
+
 void launch(const Args& a, cudaStream_t s) {
     dim3 grid(a.g.nbx, a.g.nby);
-    if (a.bpx) k_fused2<true><<<grid, TX, 0, s>>>(a);
-    else k_fused2<false><<<grid, TX, 0, s>>>(a);
+    const size_t smem = smem_bytes(a.g, a.bpx != 0);
+    static bool configured = false;  // static + dynamic shared memory may pass 48 KB (BPX, long chunks)
+    if (!configured) {
+        cudaFuncSetAttribute(k_fused2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        cudaFuncSetAttribute(k_fused2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+        configured = true;
+    }
+    if (a.bpx) k_fused2<true><<<grid, TX, smem, s>>>(a);
+    else k_fused2<false><<<grid, TX, smem, s>>>(a);
 }
 
 void combine(const Args& a, double2* rCoarse, cudaStream_t s, const fast::ResArgs* smooth) {

@@ -21,6 +21,7 @@ namespace fused2 {
 constexpr int TX = 128;
 constexpr int SXP = TX / 3 + 3;        // restriction slots per strip (upper bound)
 constexpr int CXW = (TX + 1) / 3 + 3;  // coarse columns feeding the strip's prolongation
+constexpr int kMaxYc = 48;             // rows per chunk cap (the chunk's coarse rows are staged in shared memory)
 
 struct Geometry {
     int m, mc;    // fine / coarse cells per axis
