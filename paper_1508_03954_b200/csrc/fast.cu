@@ -1013,10 +1013,14 @@ __device__ __forceinline__ double2 restrict_from(const double2* r, unsigned n1) 
 // ---- bottom-up chain, cooperative form (see fast.cuh) ------------------------
 // Step l (l = top .. 1): r_l = R r_{l+1} (source a.fine for l = top) and the
 // smoothing of l on the value just formed, one grid barrier per step while
-// the source level is big; once it has at most kUpSingle points the CTA that
+// the source level is big; once it has at most up_single<P>() points the CTA that
 // arrives last at a counter runs the remaining steps alone in shared memory.
 // Same arithmetic as restrict + k_chain_up, bit for bit.
-constexpr unsigned kUpSingle = 1200;
+#ifndef TMG_UP_SINGLE2
+#define TMG_UP_SINGLE2 8000
+#endif
+template <int P>
+__host__ __device__ constexpr unsigned up_single() { return P == 2 ? TMG_UP_SINGLE2 : 1200; }  // last-CTA source size (shared memory)
 
 template <int P>
 __device__ __forceinline__ void up_step_multi(const ChainArgs& a, const Lvl& src, const Lvl& c, const Lvl& par,
@@ -1142,12 +1146,12 @@ __global__ void __launch_bounds__(kChainThreads) k_up_coop(const ChainArgs a, un
     int l = top;
     for (; l >= 1; --l) {
         const Lvl src = l == top ? a.fine : a.lv[l + 1];
-        if (src.n <= kUpSingle) break;
+        if (src.n <= up_single<P>()) break;
         const bool restrictIt = l >= a.ellMin;
         up_step_multi<P>(a, src, a.lv[l], a.lv[l - 1], a.k[l], restrictIt, tid, stride);
         if (l > 1) {
             const Lvl nsrc = a.lv[l];
-            if (nsrc.n > kUpSingle) grid_barrier(a.bar, gen, 0);
+            if (nsrc.n > up_single<P>()) grid_barrier(a.bar, gen, 0);
         }
     }
     // the remaining steps: the CTA arriving last; norms: the one arriving first.
@@ -1299,10 +1303,11 @@ void chain_up(int P, const ChainArgs& a, int grid, cudaStream_t s) {
 
 
 size_t up_coop_smem(int P, const ChainArgs& a) {
+    const unsigned single = P == 2 ? up_single<2>() : up_single<3>();
     int l = a.top;
     for (; l >= 1; --l) {
         const unsigned n = l == a.top ? a.fine.n : a.lv[l + 1].n;
-        if (n <= kUpSingle) break;
+        if (n <= single) break;
     }
     if (l < 1) return 0;
     size_t pts = 0;

@@ -27,7 +27,6 @@ __device__ __forceinline__ double2 lerpw(double2 c0, double2 c1, double w1) {
     return make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
 }
 __device__ __forceinline__ double relw(int r) { return r == 1 ? (1.0 / 3.0) : r == 2 ? (2.0 / 3.0) : (r == 3 ? 1.0 : 0.0); }
-__device__ __forceinline__ double2 ldg(const double2* p) { return __ldg(p); }
 
 __device__ __forceinline__ double2 stage_sc(double2 smooth, double2 w, bool cp, int bpx, int hb) {
     if (bpx) return cp ? zero2() : mul(w, smooth);
@@ -55,9 +54,10 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     __shared__ double2 Pb[2][TX + 2];          // corrected rows (x halo at 0 and TX+1)
     __shared__ double2 Vb[BPX ? 4 : 2][CXW];   // y-interpolated coarse rows (sc[, si])
     __shared__ double2 tb[TX];                 // y-restricted columns
-    extern __shared__ __align__(16) double2 Cs[];  // the strip's coarse rows [BPX ? 2 : 1][nq][CXW], staged once
-    __shared__ __align__(16) double2 Ru[kRing][TX + 2];  // row ring: v (own columns + x halo)
-    __shared__ __align__(16) double2 Rb[kRing][TX];      // row ring: b
+    extern __shared__ __align__(16) double2 dyn[];
+    auto Ru = reinterpret_cast<double2(*)[TX + 2]>(dyn);                    // row ring: v (own columns + x halo)
+    auto Rb = reinterpret_cast<double2(*)[TX]>(dyn + kRing * (TX + 2));      // row ring: b
+    double2* Cs = dyn + kRing * (2 * TX + 2);  // the strip's coarse rows [BPX ? 2 : 1][nq][CXW], staged once
 
     const int tid = threadIdx.x;
     const int m = a.g.m, mc = a.g.mc;
@@ -310,7 +310,7 @@ int blocks(const Geometry& g) { return g.nbx * g.nby; }
 
 size_t smem_bytes(const Geometry& g, bool bpx) {
     const int nq = g.yc / 3 + 3;  // coarse rows feeding yc + 2 fine rows
-    return static_cast<size_t>(bpx ? 2 : 1) * nq * CXW * sizeof(double2);
+    return (static_cast<size_t>(kRing) * (2 * TX + 2) + static_cast<size_t>(bpx ? 2 : 1) * nq * CXW) * sizeof(double2);
 }
 
 void launch(const Args& a, cudaStream_t s) {

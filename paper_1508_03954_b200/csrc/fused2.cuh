@@ -18,7 +18,10 @@
 namespace tmg {
 namespace fused2 {
 
-constexpr int TX = 128;
+#ifndef TMG_F2_TX
+#define TMG_F2_TX 128
+#endif
+constexpr int TX = TMG_F2_TX;  // strip width (threads per block)
 constexpr int SXP = TX / 3 + 3;        // restriction slots per strip (upper bound)
 constexpr int CXW = (TX + 1) / 3 + 3;  // coarse columns feeding the strip's prolongation
 constexpr int kMaxYc = 48;             // rows per chunk cap (the chunk's coarse rows are staged in shared memory)
