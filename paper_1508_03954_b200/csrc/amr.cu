@@ -236,6 +236,66 @@ __device__ __forceinline__ void cell_chi(double2& acc, const ALvl& c, const ALvl
         return;
     }
     if (!restrictOn) return;
+    if (!fl.fmask) {
+        // static tree (no special vertices): the 3^P fine vertices of this cell
+        // inside g's restriction window (w = v - 3 cell in [wlo, wlo + 2] per axis)
+        // have their finish corners loaded once, packed 4 bits each (15: absent /
+        // off the domain); then (child t, corner ec) ascending as below, touching
+        // only the pairs whose vertex lies in the window
+        int wlo[3] = {0, 0, 0};
+#pragma unroll
+        for (int d = 0; d < P; ++d) wlo[d] = cell[d] == g[d] - 1 ? 1 : 0;
+        constexpr int NW = P == 1 ? 3 : P == 2 ? 9 : 27;
+        unsigned long long pk[2] = {0ull, 0ull};
+        int vfw[NW];
+#pragma unroll
+        for (int pw = 0; pw < NW; ++pw) {
+            int v[P];
+            int rr = pw;
+            bool in = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                v[d] = 3 * cell[d] + wlo[d] + rr % 3;
+                rr /= 3;
+                in &= (v[d] >= 1) & (v[d] <= fl.m - 1);
+            }
+            const int vf = in ? aflat<P>(fl, v) : -1;
+            vfw[pw] = vf;
+            const unsigned e = vf >= 0 ? static_cast<unsigned>(fl.estar[vf]) & 15u : 15u;
+            pk[pw >> 4] |= static_cast<unsigned long long>(e) << (4 * (pw & 15));
+        }
+        for (int t = 0; t < NT; ++t) {
+            int j[P];
+            int tt = t;
+            unsigned must0 = 0, must1 = 0;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                j[d] = tt % 3;
+                tt /= 3;
+                const int dj = j[d] - wlo[d];  // i_d = dj + ec_d must lie in [0, 2]
+                if (dj < 0) must1 |= 1u << d;
+                if (dj > 1) must0 |= 1u << d;
+            }
+            const unsigned freeb = ~(must0 | must1) & static_cast<unsigned>(NC - 1);
+            unsigned sub = 0;
+            do {  // ec = must1 | sub, ascending
+                const int ec = static_cast<int>(must1 | sub);
+                int pw = 0, mul = 1, code = 0, cm = 1;
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    const int bit = (ec >> d) & 1;
+                    pw += (j[d] - wlo[d] + bit) * mul;
+                    mul *= 3;
+                    code += (3 * cell[d] + j[d] + bit - 3 * g[d] + 2) * cm;
+                    cm *= 5;
+                }
+                const unsigned e = static_cast<unsigned>(pk[pw >> 4] >> (4 * (pw & 15))) & 15u;
+                if (e == static_cast<unsigned>(ec)) acc = xadd(acc, xscale(w5[code], fl.rhat[vfw[pw]]));
+                sub = (sub - freeb) & freeb;
+            } while (sub);
+        }
+        return;
+    }
     for (int t = 0; t < NT; ++t) {
         int j[P];
         int tt = t;
@@ -294,23 +354,40 @@ __global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, 
             if (!(cfl & amr::kCellExists)) continue;
             const int a = (~e) & (NC - 1);  // corner of g in the cell
             if ((c.vflag[f] & amr::kRegularChi) && restrictOn) {
-                // regular neighbourhood: fine vertices 3*cell + j in child order
-                for (int t = 0; t < NT; ++t) {
-                    int v[P];
-                    int code = 0, mul = 1;
-                    bool in = true;
-                    int tt = t;
+                // regular neighbourhood: fine vertices 3*cell + j in child order (t = j0 + 3 j1 + 9 j2),
+                // loaded a batch of 3^min(P,2) at a time so the loads are in flight together; the
+                // sum keeps the child order
+                constexpr int NB = P == 1 ? 3 : 9;  // batch: one j_{P-1} slice (P = 3) / everything
+                int gc[3] = {0, 0, 0};
 #pragma unroll
-                    for (int d = 0; d < P; ++d) {
-                        v[d] = 3 * cell[d] + tt % 3;
-                        tt /= 3;
-                        const int off = v[d] - 3 * g[d];
-                        in &= (off >= -2) & (off <= 2) & (v[d] >= 1) & (v[d] <= fl.m - 1);
-                        code += (off + 2) * mul;
-                        mul *= 5;
+                for (int d = 0; d < P; ++d) gc[d] = 3 * g[d];
+                const int sy = P >= 2 ? fl.n1[0] : 0, sz = P == 3 ? fl.n1[0] * fl.n1[1] : 0;
+                const int centre = aflat<P>(fl, gc);
+#pragma unroll 1
+                for (int t0 = 0; t0 < NT; t0 += NB) {
+                    double2 val[NB];
+                    double wt[NB];
+                    bool act[NB];
+#pragma unroll
+                    for (int q = 0; q < NB; ++q) {
+                        int tt = t0 + q, off[3] = {0, 0, 0}, code = 0, mul = 1;
+                        bool in = true;
+#pragma unroll
+                        for (int d = 0; d < P; ++d) {
+                            const int vd = 3 * cell[d] + tt % 3;
+                            tt /= 3;
+                            off[d] = vd - gc[d];
+                            in &= (off[d] >= -2) & (off[d] <= 2) & (vd >= 1) & (vd <= fl.m - 1);
+                            code += (off[d] + 2) * mul;
+                            mul *= 5;
+                        }
+                        act[q] = in;
+                        val[q] = in ? __ldg(fl.rhat + (centre + off[0] + sy * off[1] + sz * off[2])) : cz();
+                        wt[q] = in ? __ldg(w5 + code) : 0.0;
                     }
-                    if (!in) continue;
-                    acc = xadd(acc, xscale(w5[code], fl.rhat[aflat<P>(fl, v)]));
+#pragma unroll
+                    for (int q = 0; q < NB; ++q)
+                        if (act[q]) acc = xadd(acc, xscale(wt[q], val[q]));
                 }
                 continue;
             }
