@@ -397,6 +397,189 @@ __global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, 
     }
 }
 
+
+// ---- chi gather lists (static trees) -----------------------------------------
+// The chi walk of k_amr_chi visits the same fine vertices and leaf cells in the
+// same order every cycle on a static tree.  k_amr_chi_list replays it once at
+// setup and records, per vertex, its terms in order: (fine box index << 7 |
+// weight code) for a restriction term, (k << 7 | 127) for its k-th leaf-load term,
+// whose value (massScale * sum M nodal) is stored aside -- nodal is constant.
+// Storage is warp-interleaved (term k of list position i at base[i >> 5] +
+// 32 k + (i & 31)), so the per-cycle k_amr_chi_gather reads it coalesced and
+// adds the terms in the recorded order: the same xadd / xscale sequence as
+// k_amr_chi, bit for bit.
+struct ChiList {
+    int* cnt;               // terms per list position (-1: vertex absent)
+    int* lcnt;              // leaf terms per list position
+    const long long* base;  // per warp group: first term slot
+    const long long* lbase; // per warp group: first leaf-value slot
+    unsigned* ent;
+    double2* leaf;
+};
+constexpr unsigned kLeafCode = 127;  // restriction weight codes are 0 .. 5^P - 1
+
+template <int P, bool WRITE>
+__global__ void __launch_bounds__(256) k_amr_chi_list(ALvl c, ALvl fl, LevelConst k, int restrictOn, ChiList L) {
+    constexpr int NC = 1 << P;
+    constexpr int NT = P == 1 ? 3 : P == 2 ? 9 : 27;
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
+        const unsigned f = c.list[i];
+        if (!(c.vflag[f] & amr::kExists)) {
+            if (!WRITE) L.cnt[i] = -1, L.lcnt[i] = 0;
+            continue;
+        }
+        int n = 0, nl = 0;
+        const long long eb = WRITE ? L.base[i >> 5] + (i & 31) : 0, lb = WRITE ? L.lbase[i >> 5] + (i & 31) : 0;
+        auto term = [&](int vf, int code) {
+            if (WRITE) L.ent[eb + 32LL * n] = (static_cast<unsigned>(vf) << 7) | static_cast<unsigned>(code);
+            ++n;
+        };
+        auto leafTerm = [&](double2 v) {
+            if (WRITE) {
+                L.leaf[lb + 32LL * nl] = v;
+                L.ent[eb + 32LL * n] = (static_cast<unsigned>(nl) << 7) | kLeafCode;
+            }
+            ++n;
+            ++nl;
+        };
+        int g[P];
+        aunflat<P>(f, c, g);
+        const int pid = perm_id<P>(g);
+        for (int ic = 0; ic < NC; ++ic) {
+            const int e = perm_cell(P, pid, ic);
+            int cell[P];
+            bool ok = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                cell[d] = g[d] - 1 + ((e >> d) & 1);
+                ok &= (cell[d] >= 0) & (cell[d] <= c.m - 1);
+            }
+            if (!ok) continue;
+            const int cf = aflat<P>(c, cell);
+            if (cf < 0) continue;
+            const unsigned char cfl = c.cflag[cf];
+            if (!(cfl & amr::kCellExists)) continue;
+            const int a = (~e) & (NC - 1);
+            if ((c.vflag[f] & amr::kRegularChi) && restrictOn) {
+                for (int t = 0; t < NT; ++t) {
+                    int v[P], tt = t, code = 0, mul = 1;
+                    bool in = true;
+#pragma unroll
+                    for (int d = 0; d < P; ++d) {
+                        v[d] = 3 * cell[d] + tt % 3;
+                        tt /= 3;
+                        const int off = v[d] - 3 * g[d];
+                        in &= (off >= -2) & (off <= 2) & (v[d] >= 1) & (v[d] <= fl.m - 1);
+                        code += (off + 2) * mul;
+                        mul *= 5;
+                    }
+                    if (in) term(aflat<P>(fl, v), code);
+                }
+                continue;
+            }
+            if (!(cfl & amr::kCellRefined)) {  // leaf load (cell_chi)
+                double2 acc2 = cz();
+#pragma unroll
+                for (int bb = 0; bb < NC; ++bb) {
+                    int vb[P];
+#pragma unroll
+                    for (int d = 0; d < P; ++d) vb[d] = cell[d] + ((bb >> d) & 1);
+                    acc2 = xadd(acc2, xscale(k.M[a ^ bb], c.nodal[aflat<P>(c, vb)]));
+                }
+                leafTerm(xmul(k.massScale, acc2));
+                continue;
+            }
+            if (!restrictOn) continue;
+            for (int t = 0; t < NT; ++t) {  // cell_chi's refined cell: (child, corner) ascending
+                int j[P], tt = t;
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    j[d] = tt % 3;
+                    tt /= 3;
+                }
+                for (int ec = 0; ec < NC; ++ec) {
+                    int v[P], code = 0, mul = 1;
+                    bool in = true;
+#pragma unroll
+                    for (int d = 0; d < P; ++d) {
+                        v[d] = 3 * cell[d] + j[d] + ((ec >> d) & 1);
+                        const int off = v[d] - 3 * g[d];
+                        in &= (off >= -2) & (off <= 2) & (v[d] >= 1) & (v[d] <= fl.m - 1);
+                        code += (off + 2) * mul;
+                        mul *= 5;
+                    }
+                    if (!in) continue;
+                    const int vf = aflat<P>(fl, v);
+                    if (vf < 0 || fl.estar[vf] != ec) continue;
+                    term(vf, code);
+                }
+            }
+        }
+        if (!WRITE) {
+            L.cnt[i] = n;
+            L.lcnt[i] = nl;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_amr_chi_gather(ALvl c, const double2* __restrict__ frhat,
+                                                        const double* __restrict__ w5, ChiList L) {
+    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
+        const int n = L.cnt[i];
+        if (n < 0) continue;
+        const unsigned* __restrict__ e = L.ent + L.base[i >> 5] + (i & 31);
+        const double2* __restrict__ lv = L.leaf + L.lbase[i >> 5] + (i & 31);
+        double2 acc = cz();
+        constexpr int B = 8;  // terms in flight
+        for (int k0 = 0; k0 < n; k0 += B) {
+            double2 val[B];
+            unsigned code[B];
+#pragma unroll
+            for (int b = 0; b < B; ++b) code[b] = k0 + b < n ? __ldg(e + 32LL * (k0 + b)) : kLeafCode;
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                const unsigned x = code[b];
+                const bool leaf = (x & 127u) == kLeafCode;
+                val[b] = k0 + b >= n ? cz() : leaf ? __ldg(lv + 32LL * (x >> 7)) : xscale(__ldg(w5 + (x & 127u)), __ldg(frhat + (x >> 7)));
+            }
+#pragma unroll
+            for (int b = 0; b < B; ++b) {
+                if (k0 + b >= n) break;
+                acc = xadd(acc, val[b]);
+            }
+        }
+        c.chi[c.list[i]] = acc;
+    }
+}
+
+// small levels: one warp per vertex -- the lanes fetch and scale 32 terms at a
+// time, lane 0 adds them in order
+__global__ void __launch_bounds__(256) k_amr_chi_gather_warp(ALvl c, const double2* __restrict__ frhat,
+                                                             const double* __restrict__ w5, ChiList L) {
+    const unsigned lane = threadIdx.x & 31u;
+    const unsigned warps = (gridDim.x * blockDim.x) >> 5;
+    for (unsigned i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < c.nlist; i += warps) {
+        const int n = L.cnt[i];
+        if (n < 0) continue;
+        const unsigned* __restrict__ e = L.ent + L.base[i >> 5] + (i & 31);
+        const double2* __restrict__ lv = L.leaf + L.lbase[i >> 5] + (i & 31);
+        double2 acc = cz();
+        for (int k0 = 0; k0 < n; k0 += 32) {
+            double2 v = cz();
+            if (k0 + static_cast<int>(lane) < n) {
+                const unsigned x = __ldg(e + 32LL * (k0 + lane));
+                v = (x & 127u) == kLeafCode ? __ldg(lv + 32LL * (x >> 7)) : xscale(__ldg(w5 + (x & 127u)), __ldg(frhat + (x >> 7)));
+            }
+            const int cntk = min(32, n - k0);
+            for (int b = 0; b < cntk; ++b) {
+                const double vx = __shfl_sync(0xffffffffu, v.x, b), vy = __shfl_sync(0xffffffffu, v.y, b);
+                acc = xadd(acc, make_double2(vx, vy));
+            }
+        }
+        if (lane == 0) c.chi[c.list[i]] = acc;
+    }
+}
+
 // sum_b A(a, b) x_b over the corners of one cell, b ascending (kernels.cpp:39-47)
 template <int P>
 __device__ __forceinline__ double2 cell_apply(const double2* __restrict__ x, const ALvl& c, const int* cell, int a,
@@ -1354,6 +1537,7 @@ struct AmrTree::Dev {
     std::vector<adev::ALvl> lv;
     std::vector<void*> allocations;
     std::vector<int> normOffs;  // block partial offsets per level
+    std::vector<adev::ChiList> chiList;  // static trees: per-level chi gather lists (empty: k_amr_chi)
     double* partials = nullptr;
     int* dOffs = nullptr;
     double* dNorm = nullptr;
@@ -1530,7 +1714,62 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
         else adev::k_amr_chi<3><<<nb, 256, 0, stream_>>>(F, F, D.kc[L_], D.weights, 0);
         AMR_CUDA(cudaGetLastError());
     }
+    const char* cl = std::getenv("TMG_CHI_LIST");  // developer A/B
+    if (!(cl && cl[0] == '0')) {
+        if (p_ == 1) build_chi_lists<1>();
+        else if (p_ == 2) build_chi_lists<2>();
+        else build_chi_lists<3>();
+    }
     AMR_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// k_amr_chi_list: count pass, warp-group bases on the host, fill pass (static trees;
+// the leaf terms use nodal, built once by build_rhs)
+template <int P>
+void AmrTree::build_chi_lists() {
+    Dev& D = *dev_;
+    D.chiList.assign(L_ + 1, adev::ChiList{});
+    for (int l = 0; l < L_; ++l) {
+        adev::ALvl& c = D.lv[l];
+        const adev::ALvl& fine = D.lv[l + 1];
+        if (c.nlist == 0 || fine.n >= (1u << 25)) continue;  // (vf << 7) must fit 32 bits
+        const int restrictOn = l + 1 > prob_.ellMin ? 1 : 0;
+        adev::ChiList L{};
+        L.cnt = D.alloc<int>(c.nlist, stream_);
+        L.lcnt = D.alloc<int>(c.nlist, stream_);
+        const int nb = blocks_for_n(c.nlist, smCount_);
+        adev::k_amr_chi_list<P, false><<<nb, 256, 0, stream_>>>(c, fine, D.kc[l], restrictOn, L);
+        AMR_CUDA(cudaGetLastError());
+        std::vector<int> cnt(c.nlist), lcnt(c.nlist);
+        AMR_CUDA(cudaMemcpyAsync(cnt.data(), L.cnt, c.nlist * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        AMR_CUDA(cudaMemcpyAsync(lcnt.data(), L.lcnt, c.nlist * sizeof(int), cudaMemcpyDeviceToHost, stream_));
+        AMR_CUDA(cudaStreamSynchronize(stream_));
+        const size_t groups = (c.nlist + 31) / 32;
+        std::vector<long long> base(groups), lbase(groups);
+        long long tb = 0, lt = 0;
+        for (size_t w = 0; w < groups; ++w) {
+            int mx = 0, lmx = 0;
+            for (size_t i = 32 * w; i < std::min<size_t>(32 * w + 32, c.nlist); ++i) {
+                mx = std::max(mx, cnt[i]);
+                lmx = std::max(lmx, lcnt[i]);
+            }
+            base[w] = tb;
+            lbase[w] = lt;
+            tb += 32LL * mx;
+            lt += 32LL * lmx;
+        }
+        long long* dBase = D.alloc<long long>(groups, stream_);
+        long long* dLbase = D.alloc<long long>(groups, stream_);
+        AMR_CUDA(cudaMemcpyAsync(dBase, base.data(), groups * sizeof(long long), cudaMemcpyHostToDevice, stream_));
+        AMR_CUDA(cudaMemcpyAsync(dLbase, lbase.data(), groups * sizeof(long long), cudaMemcpyHostToDevice, stream_));
+        L.base = dBase;
+        L.lbase = dLbase;
+        L.ent = D.alloc<unsigned>(static_cast<size_t>(std::max<long long>(tb, 1)), stream_);
+        L.leaf = D.alloc<double2>(static_cast<size_t>(std::max<long long>(lt, 1)), stream_);
+        adev::k_amr_chi_list<P, true><<<nb, 256, 0, stream_>>>(c, fine, D.kc[l], restrictOn, L);
+        AMR_CUDA(cudaGetLastError());
+        D.chiList[l] = L;
+    }
 }
 
 void AmrTree::upload_weights() {
@@ -2114,9 +2353,18 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
     for (int l = L_; l >= 0; --l) {
         const int nb = blocks_for_n(D.lv[l].nlist, smCount_);
         const adev::ALvl& fine = l < L_ ? D.lv[l + 1] : D.lv[l];
-        if (l < L_)  // finest level: chi is the constant load vector (built at setup)
-            adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.kc[l], D.weights,
-                                                         l + 1 > prob_.ellMin ? 1 : 0);
+        if (l < L_) {  // finest level: chi is the constant load vector (built at setup)
+            if (!D.chiList.empty() && D.chiList[l].ent) {
+                if (D.lv[l].nlist < 65536u)
+                    adev::k_amr_chi_gather_warp<<<blocks_for_n(32LL * D.lv[l].nlist, smCount_), 256, 0, stream_>>>(
+                        D.lv[l], fine.rhat, D.weights, D.chiList[l]);
+                else
+                    adev::k_amr_chi_gather<<<nb, 256, 0, stream_>>>(D.lv[l], fine.rhat, D.weights, D.chiList[l]);
+            }
+            else
+                adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.kc[l], D.weights,
+                                                             l + 1 > prob_.ellMin ? 1 : 0);
+        }
         a.lv = D.lv[l];
         a.par = l > 0 ? D.lv[l - 1] : D.lv[0];
         a.k = D.kc[l];

@@ -116,6 +116,8 @@ class AmrTree {
     void refresh_counts();
     template <int P>
     void build_rhs();
+    template <int P>
+    void build_chi_lists();
 
     Problem prob_;
     int p_ = 3, L_ = 1, base_ = 0;
