@@ -258,14 +258,19 @@ __global__ void __launch_bounds__(256) k_combine2(const Args a, double2* rc, con
         if (W0 < 1 || W0 > mc - 1 || W1 < 1 || W1 > mc - 1) continue;
         const int by0 = (max(1, 3 * W1 - 2) - 1) / yc, by1 = (min(m - 1, 3 * W1 + 2) - 1) / yc;
         const int bx0 = (max(1, 3 * W0 - 2) - 1) / TX, bx1 = (min(m - 1, 3 * W0 + 2) - 1) / TX;
-        double2 acc = zero2();
-        for (int by = by0; by <= by1; ++by) {
-            const int yi = W1 - (by * yc) / 3;
-            for (int bx = bx0; bx <= bx1; ++bx) {
-                const int xi = W0 - (1 + bx * TX) / 3;
-                acc = add(acc, a.partial[((static_cast<long long>(by) * a.g.sy + yi) * a.g.nbx + bx) * SXP + xi]);
-            }
+        double2 v[4];  // at most two strips / chunks per axis: loaded up front, added in (by, bx) order
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int by = by0 + (q >> 1), bx = bx0 + (q & 1);
+            const int yi = W1 - (by * yc) / 3, xi = W0 - (1 + bx * TX) / 3;
+            v[q] = (by <= by1 && bx <= bx1)
+                       ? __ldcs(a.partial + ((static_cast<long long>(by) * a.g.sy + yi) * a.g.nbx + bx) * SXP + xi)
+                       : zero2();
         }
+        double2 acc = zero2();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            if (by0 + (q >> 1) <= by1 && bx0 + (q & 1) <= bx1) acc = add(acc, v[q]);
         rc[f] = acc;
         if (SMOOTH) {  // level L-1 smoothing (k_smooth_coarse) on the value just formed (fused3::k_combine<true>)
             const dev::Lvl& cl = sa.lv;

@@ -443,21 +443,28 @@ __global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int 
         const unsigned fr = f / n1c;
         const int W0 = static_cast<int>(f - fr * n1c), W1 = static_cast<int>(fr % n1c), W2 = static_cast<int>(fr / n1c);
         if (W0 < 1 || W0 > mc - 1 || W1 < 1 || W1 > mc - 1 || W2 < 1 || W2 > mc - 1) continue;
-        double2 acc = zero2();
+        // the tiles / chunks covering W's stencil: at most two per axis (5 fine
+        // points < TX, TY, zc); all candidate partials are loaded up front, then
+        // added in the (bz, by, bx) order
         const int bz0 = (max(1, 3 * W2 - 2) - 1) / zc, bz1 = (min(m - 1, 3 * W2 + 2) - 1) / zc;
         const int by0 = (max(1, 3 * W1 - 2) - 1) / TY, by1 = (min(m - 1, 3 * W1 + 2) - 1) / TY;
         const int bx0 = (max(1, 3 * W0 - 2) - 1) / TX, bx1 = (min(m - 1, 3 * W0 + 2) - 1) / TX;
-        for (int bz = bz0; bz <= bz1; ++bz) {
-            const int zi = W2 - (bz * zc) / 3;
-            for (int by = by0; by <= by1; ++by) {
-                const int yi = W1 - (1 + by * TY) / 3;
-                for (int bx = bx0; bx <= bx1; ++bx) {
-                    const int xi = W0 - (1 + bx * TX) / 3;
-                    const long long tile = bx + static_cast<long long>(a.g.nbx) * by;
-                    acc = add(acc, a.partial[((static_cast<long long>(bz) * a.g.sz + zi) * tilesXY + tile) * (SY * SX) +
-                                             yi * SX + xi]);
-                }
-            }
+        double2 v[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int bz = bz0 + (q >> 2), by = by0 + ((q >> 1) & 1), bx = bx0 + (q & 1);
+            const bool use = bz <= bz1 && by <= by1 && bx <= bx1;
+            const int zi = W2 - (bz * zc) / 3, yi = W1 - (1 + by * TY) / 3, xi = W0 - (1 + bx * TX) / 3;
+            const long long tile = bx + static_cast<long long>(a.g.nbx) * by;
+            v[q] = use ? __ldcs(a.partial + ((static_cast<long long>(bz) * a.g.sz + zi) * tilesXY + tile) * (SY * SX) +
+                                yi * SX + xi)
+                       : zero2();
+        }
+        double2 acc = zero2();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int bz = bz0 + (q >> 2), by = by0 + ((q >> 1) & 1), bx = bx0 + (q & 1);
+            if (bz <= bz1 && by <= by1 && bx <= bx1) acc = add(acc, v[q]);
         }
         rc[f] = acc;
         if (SMOOTH) {  // level L-1 smoothing (k_smooth_coarse) on the value just formed
