@@ -126,6 +126,12 @@ __global__ void __launch_bounds__(256) k_topdown_tri(Lvl c, Lvl pr, int bpx, uns
 #pragma unroll
         for (int d = 1; d < P; ++d) cpr &= idx[d] % 3 == 0;
         const unsigned fb = row * n1;
+        double2 own[3];  // the three points' current values, loaded before any store
+#pragma unroll
+        for (int k = 0; k < 3; ++k) {
+            const int x = 3 * qx + k;
+            own[k] = (x >= 1 && x <= m - 1) ? ld((FINE ? c.u : c.sc) + fb + static_cast<unsigned>(x)) : make_double2(0.0, 0.0);
+        }
 #pragma unroll
         for (int k = 0; k < 3; ++k) {
             const int x = 3 * qx + k;
@@ -139,7 +145,7 @@ __global__ void __launch_bounds__(256) k_topdown_tri(Lvl c, Lvl pr, int bpx, uns
 #pragma unroll
                 for (int i = 0; i < (1 << (P - 1 - d)); ++i) w[i] = lerp(w[2 * i], w[2 * i + 1], rel[d]);
             const unsigned f = fb + static_cast<unsigned>(x);
-            double2 sc = add(c.sc[f], w[0]);  // k_topdown order: (sc + P sc) - P si
+            double2 sc = add(FINE ? c.sc[f] : own[k], w[0]);  // k_topdown order: (sc + P sc) - P si
             if (bpx && !(cpr && k == 0)) {
 #pragma unroll
                 for (int e = 0; e < (1 << P); ++e) w[e] = vi[e];
@@ -149,7 +155,7 @@ __global__ void __launch_bounds__(256) k_topdown_tri(Lvl c, Lvl pr, int bpx, uns
                     for (int i = 0; i < (1 << (P - 1 - d)); ++i) w[i] = lerp(w[2 * i], w[2 * i + 1], rel[d]);
                 sc = sub(sc, w[0]);
             }
-            if (FINE) c.u[f] = add(c.u[f], sc);
+            if (FINE) c.u[f] = add(own[k], sc);
             else c.sc[f] = sc;
         }
     }
