@@ -63,12 +63,13 @@ __device__ __forceinline__ bool is_cpoint(const int* idx) {
 }
 
 // proj/src/transfer.cpp:20-40, one axis fold: exact copies at rel 0 / 3.
+// Branch-free (rel varies across the lanes of a warp): the blend is formed
+// always and the exact copies selected, so the result is the same bits.
 __device__ __forceinline__ double2 lerp_rel(double2 c0, double2 c1, int rel) {
-    if (rel == 0) return c0;
-    if (rel == 3) return c1;
     const double w0 = rel == 1 ? (2.0 / 3.0) : (1.0 / 3.0);
     const double w1 = rel == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
-    return xadd(xscale(w0, c0), xscale(w1, c1));
+    const double2 r = xadd(xscale(w0, c0), xscale(w1, c1));
+    return rel == 0 ? c0 : rel == 3 ? c1 : r;
 }
 
 template <int P>
