@@ -1325,7 +1325,10 @@ struct Hierarchy::Impl {
         return !off && (p == 2 || p == 3) && L >= 2 && L - 1 < fast::kPyrMaxLevels;
     }
     // pyramid up to the highest level below kPyrMaxN points, per-level launches above it
-    static constexpr unsigned kPyrMaxN = 1u << 21;
+#ifndef TMG_PYR_MAXN
+#define TMG_PYR_MAXN (1u << 21)
+#endif
+    static constexpr unsigned kPyrMaxN = TMG_PYR_MAXN;
     int pyramid_top() const {
         int T = L - 1;
         while (T > 1 && lv[T].n > kPyrMaxN) --T;
