@@ -824,7 +824,7 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
 __global__ void k_amr_norm_final(const double* __restrict__ partials, const int* __restrict__ offs, int nlev,
                                  double* out) {
     __shared__ double smax[1024], ssum[1024];
-    for (int l = 0; l < nlev; ++l) {
+    for (int l = blockIdx.x; l < nlev; l += gridDim.x) {  // one block per level (same tree per level)
         double mx = 0.0, sm = 0.0;
         for (int i = offs[l] + threadIdx.x; i < offs[l + 1]; i += blockDim.x) {
             mx = fmax(mx, partials[2 * i]);
@@ -2163,7 +2163,7 @@ void AmrTree::run_cycle_dyn(const Policy& pol, int n) {
         adev::k_amr_residual<P><<<nb, 256, 0, stream_>>>(a);
         dyn_check(stream_, "k_amr_residual", l);
     }
-    adev::k_amr_norm_final<<<1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
+    adev::k_amr_norm_final<<<L_ + 1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
     phaseMs_[5] += 1;
     AMR_CUDA(cudaGetLastError());
 }
@@ -2371,7 +2371,7 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
         a.partials = D.partials + 2 * static_cast<size_t>(D.normOffs[l]);
         adev::k_amr_residual<P><<<nb, 256, 0, stream_>>>(a);
     }
-    adev::k_amr_norm_final<<<1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
+    adev::k_amr_norm_final<<<L_ + 1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
     AMR_CUDA(cudaGetLastError());
 }
 
