@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     extern __shared__ __align__(16) double2 dyn[];
     auto Ru = reinterpret_cast<double2(*)[TX + 2]>(dyn);                    // row ring: v (own columns + x halo)
     auto Rb = reinterpret_cast<double2(*)[TX]>(dyn + kRing * (TX + 2));      // row ring: b
-    double2* Cs = dyn + kRing * (2 * TX + 2);  // the strip's coarse rows [BPX ? 2 : 1][nq][CXW], staged once
+    double2* Cs = dyn + kRing * (2 * TX + 2);  // coarse-row ring: sc [4][CXW] (+ si [4][CXW])
 
     const int tid = threadIdx.x;
     const int m = a.g.m, mc = a.g.mc;
@@ -84,26 +84,31 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     const bool hcpx = hx % 3 == 0;
     const int hslot = tid == 0 ? 0 : (xe - x0) + 1;
 
-    // coarse rows [qlo, qhi] feeding fine rows y0-1 .. y1, staged once (cp.async)
-    const int qlo = min(max(y0 - 1, 0) / 3, mc - 1), qhi = min(y1 / 3, mc - 1) + 1;
-    const int nq = qhi - qlo + 1;
-    if (tid < CXW) {
-        const int cx = min(cx0 + tid, mc);
-        for (int r = 0; r < nq; ++r) {
-            const long long g = cx + static_cast<long long>(a.n1c) * (qlo + r);
-            cp_async16(Cs + r * CXW + tid, a.scC + g);
-            if (BPX) cp_async16(Cs + (nq + r) * CXW + tid, a.siC + g);
+    // coarse rows feeding the strip (sc[, si]) through a 4-slot ring (slot q % 4):
+    // rows q(y0-1) and +1 up front, then coarse row Q + 1 rides with fine row
+    // 3Q - 1's ring group, so it has landed when computeV(3Q) runs (one row later)
+    const int cxo = min(cx0 + tid, mc);
+    auto issueCoarse = [&](int q) {
+        if (tid < CXW && q <= mc) {
+            const long long g = cxo + static_cast<long long>(a.n1c) * q;
+            cp_async16(Cs + (q & 3) * CXW + tid, a.scC + g);
+            if (BPX) cp_async16(Cs + (4 + (q & 3)) * CXW + tid, a.siC + g);
         }
+    };
+    {
+        const int q0 = min(max(y0 - 1, 0) / 3, mc - 1);
+        issueCoarse(q0);
+        issueCoarse(q0 + 1);
+        asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
-    __syncthreads();
     auto computeV = [&](int yy, int vb) {  // coarse rows of fine row yy, for coarse columns cx0 + tid
         if (tid >= CXW) return;
         const int qy = min(max(yy, 0) / 3, mc - 1);
         const double w1y = relw(yy - 3 * qy);
-        const double2* c = Cs + (qy - qlo) * CXW + tid;
-        Vb[vb][tid] = lerpw(c[0], c[CXW], w1y);
-        if (BPX) Vb[2 + vb][tid] = lerpw(c[nq * CXW], c[(nq + 1) * CXW], w1y);
+        const double2* c0 = Cs + (qy & 3) * CXW + tid;
+        const double2* c1 = Cs + ((qy + 1) & 3) * CXW + tid;
+        Vb[vb][tid] = lerpw(c0[0], c1[0], w1y);
+        if (BPX) Vb[2 + vb][tid] = lerpw(c0[4 * CXW], c1[4 * CXW], w1y);
     };
 
     // restriction slots of this strip
@@ -151,6 +156,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
             cp_async16z(&Rb[slot][tid], a.b + x + row, yy >= y0 && yy < y1);
         }
         if (haloThread) cp_async16z(&Ru[slot][hslot], a.u + (hin ? hx : x0) + row, yin && hin);
+        if (yy >= 2 && yy % 3 == 2 && (yy + 1) / 3 < mc) issueCoarse((yy + 1) / 3 + 1);  // needed from fine row yy + 1
         asm volatile("cp.async.commit_group;" ::: "memory");
     };
     for (int i = 0; i < kRing - 1; ++i) issueRow(i);  // empty groups past the chunk keep the count uniform
@@ -314,8 +320,8 @@ size_t partial_count(const Geometry& g) { return static_cast<size_t>(g.nby) * g.
 int blocks(const Geometry& g) { return g.nbx * g.nby; }
 
 size_t smem_bytes(const Geometry& g, bool bpx) {
-    const int nq = g.yc / 3 + 3;  // coarse rows feeding yc + 2 fine rows
-    return (static_cast<size_t>(kRing) * (2 * TX + 2) + static_cast<size_t>(bpx ? 2 : 1) * nq * CXW) * sizeof(double2);
+    (void)g;
+    return (static_cast<size_t>(kRing) * (2 * TX + 2) + static_cast<size_t>(bpx ? 8 : 4) * CXW) * sizeof(double2);
 }
 
 void launch(const Args& a, cudaStream_t s) {
