@@ -1337,7 +1337,11 @@ void up_coop(int P, const ChainArgs& a, unsigned* count, int smCount, cudaStream
     if (smem > 48 * 1024) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, kChainThreads, smem) != cudaSuccess || per < 1) per = 1;
-    const int grid = std::min(per, 2) * smCount;
+    // as many CTAs as the first (biggest) multi-CTA step has work for: fewer CTAs
+    // contend less for the level parameters and arrive sooner at the counter
+    const long long work = static_cast<long long>(a.lv[a.top].n) * (P == 3 ? 8 : 1);
+    const int grid = static_cast<int>(std::max<long long>(
+        1, std::min<long long>(std::min(per, 2) * smCount, (work + kChainThreads - 1) / kChainThreads)));
     cudaLaunchCooperativeKernel(k, dim3(grid), dim3(kChainThreads), args, smem, s);
 }
 
