@@ -102,7 +102,7 @@ __device__ __forceinline__ int aflat(const ALvl& c, const int* g) {
 }
 
 // ---- top-down: touch_first / create_hanging ----------------------------------
-template <int P>
+template <int P, bool STATIC = false>
 __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
         const unsigned f = c.list[i];
@@ -128,13 +128,20 @@ __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
         // parent corners (find_vertex: absent -> 0); one field at a time keeps
         // the register footprint small
         int pfs[1 << P];
+        if (STATIC && (vf & amr::kParentsAll)) {  // every parent corner exists: box strides
+            const int p0 = aflat<P>(pr, q);
+            const int s1 = P >= 2 ? pr.n1[0] : 0, s2 = P == 3 ? pr.n1[0] * pr.n1[1] : 0;
 #pragma unroll
-        for (int e = 0; e < (1 << P); ++e) {
-            int pi[P];
+            for (int e = 0; e < (1 << P); ++e) pfs[e] = p0 + (e & 1) + ((e >> 1) & 1) * s1 + ((e >> 2) & 1) * s2;
+        } else {
 #pragma unroll
-            for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
-            const int pf = aflat<P>(pr, pi);
-            pfs[e] = (pf >= 0 && (pr.vflag[pf] & amr::kExists)) ? pf : -1;
+            for (int e = 0; e < (1 << P); ++e) {
+                int pi[P];
+#pragma unroll
+                for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
+                const int pf = aflat<P>(pr, pi);
+                pfs[e] = (pf >= 0 && (pr.vflag[pf] & amr::kExists)) ? pf : -1;
+            }
         }
         auto parent_prolong = [&](const double2* src) {
             double2 v[1 << P];
@@ -143,7 +150,7 @@ __global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
             return prolong<P>(v, rel);
         };
         const double2 pu = parent_prolong(pr.u);
-        if (vf & dyn::kSCreated) {  // create_vertex_if_missing inside the sweep (spacetree.cpp:245-270, 310-318)
+        if (!STATIC && (vf & dyn::kSCreated)) {  // create_vertex_if_missing inside the sweep (spacetree.cpp:245-270, 310-318)
             c.u[f] = pu;
             c.sc[f] = cz();
             c.uhat[f] = cz();
@@ -1526,6 +1533,30 @@ void mark_regular_chi(std::vector<HostLevel>& lv, int p) {
     }
 }
 
+void mark_parents_all(std::vector<HostLevel>& lv, int p) {
+    const int L = static_cast<int>(lv.size()) - 1;
+    const int nc = 1 << p;
+    for (int l = 1; l <= L; ++l) {
+        HostLevel& h = lv[l];
+        const HostLevel& pr = lv[l - 1];
+        parallel_for(h.n, [&](long long fa, long long fb) {
+            int g[3] = {0, 0, 0};
+            for (long long f = fa; f < fb; ++f) {
+                if (!(h.vflag[f] & kExists)) continue;
+                box_unflat(h, p, f, g);
+                bool all = true;
+                for (int e = 0; e < nc && all; ++e) {
+                    int pi[3] = {0, 0, 0};
+                    for (int d = 0; d < p; ++d) pi[d] = std::min(g[d] / 3, pr.m - 1) + ((e >> d) & 1);
+                    const long long pf = box_flat(pr, p, pi);
+                    all = pf >= 0 && (pr.vflag[pf] & kExists);
+                }
+                if (all) h.vflag[f] |= kParentsAll;
+            }
+        });
+    }
+}
+
 }  // namespace amr
 
 // ============================================================================
@@ -1623,6 +1654,7 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
     if (base_ < 1) throw ConfigError("sphere refinement needs a base level >= 1");
     host_ = amr::build_sphere_tree(p_, base_, L_);
     amr::mark_regular_chi(host_, p_);
+    amr::mark_parents_all(host_, p_);
     for (const amr::HostLevel& h : host_)
         for (long long f = 0; f < h.n; ++f) {
             const unsigned char v = h.vflag[f];
@@ -2340,7 +2372,7 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
     const int bpx = pol.bpx ? 1 : 0;
     for (int l = 0; l <= L_; ++l) {
         const adev::ALvl& pr = l > 0 ? D.lv[l - 1] : D.lv[0];
-        adev::k_amr_topdown<P><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
+        adev::k_amr_topdown<P, true><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
     }
     adev::AResArgs a{};
     a.ellMin = prob_.ellMin;

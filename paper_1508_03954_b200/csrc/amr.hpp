@@ -39,7 +39,8 @@ struct LevelConst;  // exact_ops.cuh
 
 namespace amr {
 
-enum : unsigned char { kExists = 1, kHanging = 2, kRefined = 4, kBoundary = 8, kCPoint = 16, kRegularChi = 32 };
+enum : unsigned char { kExists = 1, kHanging = 2, kRefined = 4, kBoundary = 8, kCPoint = 16, kRegularChi = 32,
+                       kParentsAll = 64 /* static trees only (dynamic trees: dyn::kSCreated) */ };
 enum : unsigned char { kCellExists = 1, kCellRefined = 2 };
 
 // One level: a box of the (3^l+1)^p lattice, axis 0 fastest.
@@ -66,6 +67,9 @@ std::vector<HostLevel> build_sphere_tree(int p, int base, int L);
 // its own cell (finish corner 0), so chi is the plain restriction in the
 // regular tree's order (no loads, no finish-corner lookups).
 void mark_regular_chi(std::vector<HostLevel>& lv, int p);
+// kParentsAll: all 2^p corners of the vertex's parent cell (parent_stencil) exist,
+// so the top-down prolongation needs no existence look-ups (static trees)
+void mark_parents_all(std::vector<HostLevel>& lv, int p);
 
 }  // namespace amr
 
