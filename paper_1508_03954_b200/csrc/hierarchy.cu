@@ -1292,13 +1292,17 @@ struct Hierarchy::Impl {
     // bottom-up below level L-1 (r_{L-1} complete and smoothed) as one cooperative launch
     // (levels above the chain top S: restriction + smoothing kernels; S-1 .. 1:
     // fast::up_coop, which restricts out of S)
-    bool use_up() const {
+    bool use_up() const { return use_up_from(L - 1); }
+    bool use_up_from(int from) const {
         const char* e = std::getenv("TMG_UP");  // developer A/B (read per call: tests flip it in-process)
-        return !(e && e[0] == '0') && chainBar && (p == 2 || p == 3) && chain_top(L - 1) >= 2;
+        return !(e && e[0] == '0') && chainBar && (p == 2 || p == 3) && from >= 2 && chain_top(from) >= 2;
     }
-    void up_all(const Policy& pol, int n, int normBlocks) {
-        const int S = chain_top(L - 1);
-        for (int l = L - 2; l >= S; --l) {
+    // from: the level whose r is complete and smoothed (L-1 after the combine; the
+    // slab path's replicated top L-2); norms = false: up_coop reduces no norms
+    void up_all(const Policy& pol, int n, int normBlocks, int from = -1, bool norms = true) {
+        if (from < 0) from = L - 1;
+        const int S = chain_top(from);
+        for (int l = from - 1; l >= S; --l) {
             fast::ResArgs sl{};
             sl.lv = lv[l];
             sl.par = lv[l - 1];
@@ -1315,6 +1319,7 @@ struct Hierarchy::Impl {
         fast::ChainArgs ch = make_chain(pol, n, S - 1);  // fine = level S
         ch.firstRestrict = 1;
         ch.normBlocks = normBlocks;
+        if (!norms) ch.normOut = nullptr;
         fast::up_coop(p, ch, chainBar + 2, smCount, stream);
     }
 
@@ -1334,9 +1339,12 @@ struct Hierarchy::Impl {
         while (T > 1 && lv[T].n > kPyrMaxN) --T;
         return T;
     }
-    void topdown_all(int bpx) {
+    // levels 1 .. last-1 (default: every coarse level); the slab path passes
+    // last = L-1 (level L-1 is sharded and done per plane range)
+    void topdown_all(int bpx, int last = -1) {
+        if (last < 0) last = L;
         fast::PyrArgs a{};
-        const int T = pyramid_top();
+        const int T = std::min(pyramid_top(), last - 1);
         for (int l = 0; l <= T; ++l) {
             a.lv[l].sc = lv[l].sc;
             a.lv[l].si = lv[l].si ? lv[l].si : lv[l].sc;  // si is read only under BPX
@@ -1347,7 +1355,7 @@ struct Hierarchy::Impl {
         a.bpx = bpx;
         const size_t smem = fast::pyramid_setup(p, a, T);
         fast::topdown_pyramid(p, a, smem, stream);
-        for (int l = T + 1; l < L; ++l) fast::topdown_coarse(p, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+        for (int l = T + 1; l < last; ++l) fast::topdown_coarse(p, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
     }
 
     // highest level <= maxLevel of the coarse chain (every level below kChainMaxN
