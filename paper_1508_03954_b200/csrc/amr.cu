@@ -1614,7 +1614,9 @@ struct AmrTree::Dev {
     template <class T>
     T* alloc(size_t count, cudaStream_t s) {
         void* ptr = nullptr;
-        AMR_CUDA(cudaMalloc(&ptr, std::max<size_t>(1, count) * sizeof(T)));
+        // stream-ordered allocation: a hundred-odd level arrays at setup, each a
+        // cudaMalloc otherwise (freed with cudaFree in ~Dev, which is allowed)
+        AMR_CUDA(cudaMallocAsync(&ptr, std::max<size_t>(1, count) * sizeof(T), s));
         allocations.push_back(ptr);
         AMR_CUDA(cudaMemsetAsync(ptr, 0, std::max<size_t>(1, count) * sizeof(T), s));
         return static_cast<T*>(ptr);
@@ -1652,9 +1654,21 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
         return;
     }
     if (base_ < 1) throw ConfigError("sphere refinement needs a base level >= 1");
+    const char* sp = std::getenv("TMG_AMR_PROFILE");  // setup phase times on stderr
+    const bool prof = sp && sp[0] == '1';
+    auto tp = std::chrono::steady_clock::now();
+    auto lap = [&](const char* what) {
+        if (!prof) return;
+        AMR_CUDA(cudaStreamSynchronize(stream_));
+        const auto t = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "amr setup %-14s %8.1f ms\n", what, std::chrono::duration<double, std::milli>(t - tp).count());
+        tp = t;
+    };
     host_ = amr::build_sphere_tree(p_, base_, L_);
+    lap("tree");
     amr::mark_regular_chi(host_, p_);
     amr::mark_parents_all(host_, p_);
+    lap("marks");
     for (const amr::HostLevel& h : host_)
         for (long long f = 0; f < h.n; ++f) {
             const unsigned char v = h.vflag[f];
@@ -1707,16 +1721,50 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
         a.cflag = cflag;
         a.estar = estar;
         a.succ = succ;
-        {  // compacted vertex list: warps see uniform work (regular vertices first)
-            std::vector<unsigned> lst;
-            lst.reserve(static_cast<size_t>(h.n));
-            for (int pass = 0; pass < 2; ++pass)
-                for (long long f = 0; f < h.n; ++f) {
+        {  // compacted vertex list: warps see uniform work (regular vertices first);
+           // chunked count / prefix / fill on the host's cores, same order as a serial scan
+            const int nt = static_cast<int>(std::max(1u, std::min(64u, std::thread::hardware_concurrency())));
+            const long long chunk = (h.n + nt - 1) / nt;
+            std::vector<long long> nreg(nt, 0), nirr(nt, 0);
+            auto scan = [&](int t, unsigned* out, long long offReg, long long offIrr) {
+                const long long fa = t * chunk, fb = std::min(h.n, fa + chunk);
+                long long r = 0, q = 0;
+                for (long long f = fa; f < fb; ++f) {
                     const unsigned char v = h.vflag[f];
                     if (!(v & amr::kExists)) continue;
                     const bool regular = !(v & (amr::kHanging | amr::kBoundary));
-                    if (regular == (pass == 0)) lst.push_back(static_cast<unsigned>(f));
+                    if (out) {
+                        if (regular) out[offReg + r] = static_cast<unsigned>(f);
+                        else out[offIrr + q] = static_cast<unsigned>(f);
+                    }
+                    (regular ? r : q) += 1;
                 }
+                if (!out) {
+                    nreg[t] = r;
+                    nirr[t] = q;
+                }
+            };
+            {
+                std::vector<std::thread> th;
+                for (int t = 0; t < nt; ++t) th.emplace_back(scan, t, nullptr, 0, 0);
+                for (auto& x : th) x.join();
+            }
+            long long totReg = 0, totIrr = 0;
+            for (int t = 0; t < nt; ++t) {
+                totReg += nreg[t];
+                totIrr += nirr[t];
+            }
+            std::vector<unsigned> lst(static_cast<size_t>(totReg + totIrr));
+            {
+                std::vector<std::thread> th;
+                long long oR = 0, oI = totReg;
+                for (int t = 0; t < nt; ++t) {
+                    th.emplace_back(scan, t, lst.data(), oR, oI);
+                    oR += nreg[t];
+                    oI += nirr[t];
+                }
+                for (auto& x : th) x.join();
+            }
             auto* dl = D.alloc<unsigned>(lst.size(), stream_);
             AMR_CUDA(cudaMemcpyAsync(dl, lst.data(), lst.size() * sizeof(unsigned), cudaMemcpyHostToDevice, stream_));
             AMR_CUDA(cudaStreamSynchronize(stream_));
@@ -1735,9 +1783,11 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
     upload_weights();
     AMR_CUDA(cudaEventCreate(&D.ev0));
     AMR_CUDA(cudaEventCreate(&D.ev1));
+    lap("alloc+upload");
     if (p_ == 1) build_rhs<1>();
     else if (p_ == 2) build_rhs<2>();
     else build_rhs<3>();
+    lap("rhs");
     {  // finest level: every cell is a leaf, chi = the load vector in cell order, constant
         const adev::ALvl& F = D.lv[L_];
         const int nb = blocks_for_n(F.n, smCount_);
@@ -1752,6 +1802,7 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
         else if (p_ == 2) build_chi_lists<2>();
         else build_chi_lists<3>();
     }
+    lap("chi lists");
     AMR_CUDA(cudaStreamSynchronize(stream_));
 }
 
