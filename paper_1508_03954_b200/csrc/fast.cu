@@ -62,6 +62,7 @@ __device__ __forceinline__ double2 stage(double2 smooth, double2 w, bool cp, int
 // ---- K1f / K1c: top-down correction ----------------------------------------
 template <int P, bool FINE>
 __global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx, unsigned fa, unsigned fb) {
+    dev::griddep_wait();
     for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int idx[P];
         dev::unflat<P>(f, c.n1, idx);
@@ -86,6 +87,7 @@ __global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx, unsigne
 // x = 3qx + {0,1,2} share their 2^P parent values, loaded once (P = 2, 3).
 template <int P, bool FINE>
 __global__ void __launch_bounds__(256) k_topdown_tri(Lvl c, Lvl pr, int bpx, unsigned ra, unsigned rb) {
+    dev::griddep_wait();
     const unsigned mcp = pr.m, n1 = c.n1;
     const int m = static_cast<int>(c.m);
     const unsigned total = (rb - ra) * mcp;  // rows [ra, rb) of the (P-1)-dim row index
@@ -342,6 +344,7 @@ __device__ __forceinline__ void smooth_interior(const ResArgs& a, unsigned f, co
 // SMOOTH: also the coarse level's smoothing on the value just formed.
 template <int P, bool SMOOTH = false>
 __global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse, unsigned fa, unsigned fb, const ResArgs sa) {
+    dev::griddep_wait();
     const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
     const long long sy = fine.n1, sz = static_cast<long long>(fine.n1) * fine.n1;
     for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
@@ -410,6 +413,7 @@ __global__ void __launch_bounds__(256) k_restrict(Lvl fine, Lvl coarse, unsigned
 constexpr int kRowThreads = 256;
 
 __global__ void __launch_bounds__(kRowThreads) k_topdown3_rows(Lvl c, Lvl pr, int bpx, int zlo) {
+    dev::griddep_wait();
     extern __shared__ double2 rs[];  // [4 (+4 BPX)][pr.n1]
     const int m = static_cast<int>(c.m), mcp = static_cast<int>(pr.m);
     const int y = 1 + blockIdx.x, z = zlo + blockIdx.y;
@@ -443,6 +447,7 @@ __global__ void __launch_bounds__(kRowThreads) k_topdown3_rows(Lvl c, Lvl pr, in
 
 template <bool SMOOTH = false>
 __global__ void __launch_bounds__(kRowThreads) k_restrict3_rows(Lvl fine, Lvl coarse, int zlo, const ResArgs sa) {
+    dev::griddep_wait();
     extern __shared__ double2 rw[];  // [25][coarse.n1] x-restricted fine rows
     const double w[5] = {1.0 / 3.0, 2.0 / 3.0, 1.0, 2.0 / 3.0, 1.0 / 3.0};
     const int mc = static_cast<int>(coarse.m);
@@ -490,6 +495,7 @@ __global__ void __launch_bounds__(kRowThreads) k_restrict3_rows(Lvl fine, Lvl co
 // ---- K3c: coarse smoothing on the restricted residual ------------------------
 template <int P>
 __global__ void __launch_bounds__(256) k_smooth_coarse(ResArgs a, unsigned fa, unsigned fb) {
+    dev::griddep_wait();
     const Lvl& c = a.lv;
     for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int idx[P];
@@ -557,6 +563,7 @@ __device__ __forceinline__ void cp_async16(void* dst, const void* src) {
 // ty + 8, ..., and (P = 3) every z.
 template <int P>
 __global__ void __launch_bounds__(kPyrTX* kPyrTY) k_topdown_pyr(const PyrArgs a) {
+    dev::griddep_wait();
     extern __shared__ __align__(16) double2 pyr[];
     __shared__ int blo[kPyrMaxLevels][3], bsz[kPyrMaxLevels][3];
     __shared__ PyrLevel slv[kPyrMaxLevels];
@@ -1146,6 +1153,7 @@ __device__ __forceinline__ void chain_norms(const ChainArgs& a) {  // K5 (k_chai
 
 template <int P>
 __global__ void __launch_bounds__(kChainThreads) k_up_coop(const ChainArgs a, unsigned* count) {
+    dev::griddep_wait();
     extern __shared__ __align__(16) double2 us[];  // last CTA: r (and BPX si_next) of the small levels
     __shared__ unsigned lastFlag;
     unsigned gen = *reinterpret_cast<volatile unsigned*>(a.bar + 1);
@@ -1422,10 +1430,10 @@ void topdown_pyramid(int P, const PyrArgs& a, size_t smem, cudaStream_t s) {
     const unsigned blocks = static_cast<unsigned>(a.nbx) * a.nby * nbz;
     if (P == 2) {
         if (smem > 48 * 1024) cudaFuncSetAttribute(k_topdown_pyr<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_topdown_pyr<2><<<blocks, kPyrTX * kPyrTY, smem, s>>>(a);
+        dev::launch_k(k_topdown_pyr<2>, dim3(blocks), dim3(kPyrTX * kPyrTY), smem, s, a);
     } else {
         if (smem > 48 * 1024) cudaFuncSetAttribute(k_topdown_pyr<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        k_topdown_pyr<3><<<blocks, kPyrTX * kPyrTY, smem, s>>>(a);
+        dev::launch_k(k_topdown_pyr<3>, dim3(blocks), dim3(kPyrTX * kPyrTY), smem, s, a);
     }
 }
 
@@ -1434,7 +1442,7 @@ void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cud
         const int zlo = std::max(1, za < 0 ? 1 : za), zhi = std::min(static_cast<int>(c.m), za < 0 ? static_cast<int>(c.m) : zb);
         if (zhi <= zlo) return;
         const size_t smem = (bpx ? 8 : 4) * pr.n1 * sizeof(double2);
-        k_topdown3_rows<<<dim3(c.m - 1, zhi - zlo), kRowThreads, smem, s>>>(c, pr, bpx, zlo);
+        dev::launch_k(k_topdown3_rows, dim3(c.m - 1, zhi - zlo), dim3(kRowThreads), smem, s, c, pr, bpx, zlo);
         return;
     }
     const char* tri = std::getenv("TMG_TRI_COARSE");
@@ -1443,16 +1451,16 @@ void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cud
         const unsigned ra = za < 0 ? 0u : static_cast<unsigned>(za) * plane;
         const unsigned rb = za < 0 ? c.n / c.n1 : std::min<unsigned>(static_cast<unsigned>(zb) * plane, c.n / c.n1);
         if (rb <= ra) return;
-        if (P == 2) k_topdown_tri<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
-        else k_topdown_tri<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx, ra, rb);
+        if (P == 2) dev::launch_k(k_topdown_tri<2, false>, dim3(blocks), dim3(256), 0, s, c, pr, bpx, ra, rb);
+        else dev::launch_k(k_topdown_tri<3, false>, dim3(blocks), dim3(256), 0, s, c, pr, bpx, ra, rb);
         return;
     }
     unsigned fa, fb;
     span(P, c, za, zb, fa, fb);
     if (fb <= fa) return;
     if (P == 1) k_topdown<1, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
-    else if (P == 2) k_topdown<2, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
-    else k_topdown<3, false><<<blocks, 256, 0, s>>>(c, pr, bpx, fa, fb);
+    else if (P == 2) dev::launch_k(k_topdown<2, false>, dim3(blocks), dim3(256), 0, s, c, pr, bpx, fa, fb);
+    else dev::launch_k(k_topdown<3, false>, dim3(blocks), dim3(256), 0, s, c, pr, bpx, fa, fb);
 }
 
 void load_vector(int P, const Lvl& F, const double2* f, double2 ms, int blocks, cudaStream_t s, int za, int zb) {
@@ -1501,31 +1509,31 @@ void restrict_level(int P, const Lvl& fine, const Lvl& coarse, const double*, in
         const int zhi = std::min(static_cast<int>(coarse.m), za < 0 ? static_cast<int>(coarse.m) : zb);
         if (zhi <= zlo) return;
         const size_t smem = 25 * (coarse.m - 1) * sizeof(double2);
-        if (smooth) k_restrict3_rows<true><<<dim3(coarse.m - 1, zhi - zlo), kRowThreads, smem, s>>>(fine, coarse, zlo, sa);
-        else k_restrict3_rows<false><<<dim3(coarse.m - 1, zhi - zlo), kRowThreads, smem, s>>>(fine, coarse, zlo, sa);
+        if (smooth) dev::launch_k(k_restrict3_rows<true>, dim3(coarse.m - 1, zhi - zlo), dim3(kRowThreads), smem, s, fine, coarse, zlo, sa);
+        else dev::launch_k(k_restrict3_rows<false>, dim3(coarse.m - 1, zhi - zlo), dim3(kRowThreads), smem, s, fine, coarse, zlo, sa);
         return;
     }
     unsigned fa, fb;
     span(P, coarse, za, zb, fa, fb);
     if (fb <= fa) return;
     if (smooth) {
-        if (P == 1) k_restrict<1, true><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
-        else if (P == 2) k_restrict<2, true><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
-        else k_restrict<3, true><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
+        if (P == 1) dev::launch_k(k_restrict<1, true>, dim3(blocks), dim3(256), 0, s, fine, coarse, fa, fb, sa);
+        else if (P == 2) dev::launch_k(k_restrict<2, true>, dim3(blocks), dim3(256), 0, s, fine, coarse, fa, fb, sa);
+        else dev::launch_k(k_restrict<3, true>, dim3(blocks), dim3(256), 0, s, fine, coarse, fa, fb, sa);
         return;
     }
-    if (P == 1) k_restrict<1><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
-    else if (P == 2) k_restrict<2><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
-    else k_restrict<3><<<blocks, 256, 0, s>>>(fine, coarse, fa, fb, sa);
+    if (P == 1) dev::launch_k(k_restrict<1>, dim3(blocks), dim3(256), 0, s, fine, coarse, fa, fb, sa);
+    else if (P == 2) dev::launch_k(k_restrict<2>, dim3(blocks), dim3(256), 0, s, fine, coarse, fa, fb, sa);
+    else dev::launch_k(k_restrict<3>, dim3(blocks), dim3(256), 0, s, fine, coarse, fa, fb, sa);
 }
 
 void smooth_coarse(int P, const ResArgs& a, int blocks, cudaStream_t s, int za, int zb) {
     unsigned fa, fb;
     span(P, a.lv, za, zb, fa, fb);
     if (fb <= fa) return;
-    if (P == 1) k_smooth_coarse<1><<<blocks, 256, 0, s>>>(a, fa, fb);
-    else if (P == 2) k_smooth_coarse<2><<<blocks, 256, 0, s>>>(a, fa, fb);
-    else k_smooth_coarse<3><<<blocks, 256, 0, s>>>(a, fa, fb);
+    if (P == 1) dev::launch_k(k_smooth_coarse<1>, dim3(blocks), dim3(256), 0, s, a, fa, fb);
+    else if (P == 2) dev::launch_k(k_smooth_coarse<2>, dim3(blocks), dim3(256), 0, s, a, fa, fb);
+    else dev::launch_k(k_smooth_coarse<3>, dim3(blocks), dim3(256), 0, s, a, fa, fb);
 }
 
 }  // namespace fast

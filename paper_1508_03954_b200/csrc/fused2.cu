@@ -51,6 +51,7 @@ constexpr int kRing = 4;  // rows in flight
 
 template <bool BPX>
 __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
+    dev::griddep_wait();
     __shared__ double2 Pb[2][TX + 2];          // corrected rows (x halo at 0 and TX+1)
     __shared__ double2 Vb[BPX ? 4 : 2][CXW];   // y-interpolated coarse rows (sc[, si])
     __shared__ double2 tb[TX];                 // y-restricted columns
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
 
 template <bool SMOOTH>
 __global__ void __launch_bounds__(256) k_combine2(const Args a, double2* rc, const fast::ResArgs sa) {
+    dev::griddep_wait();
     const int mc = a.g.mc, m = a.g.m, yc = a.g.yc;
     const unsigned n1c = a.n1c;
     const unsigned total = n1c * n1c;
@@ -333,15 +335,15 @@ void launch(const Args& a, cudaStream_t s) {
         cudaFuncSetAttribute(k_fused2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
         configured = true;
     }
-    if (a.bpx) k_fused2<true><<<grid, TX, smem, s>>>(a);
-    else k_fused2<false><<<grid, TX, smem, s>>>(a);
+    if (a.bpx) dev::launch_k(k_fused2<true>, grid, dim3(TX), smem, s, a);
+    else dev::launch_k(k_fused2<false>, grid, dim3(TX), smem, s, a);
 }
 
 void combine(const Args& a, double2* rCoarse, cudaStream_t s, const fast::ResArgs* smooth) {
     const unsigned total = a.n1c * a.n1c;
     const unsigned nb = std::max(1u, std::min((total + 255) / 256, 4096u));
-    if (smooth) k_combine2<true><<<nb, 256, 0, s>>>(a, rCoarse, *smooth);
-    else k_combine2<false><<<nb, 256, 0, s>>>(a, rCoarse, fast::ResArgs{});
+    if (smooth) dev::launch_k(k_combine2<true>, dim3(nb), dim3(256), 0, s, a, rCoarse, *smooth);
+    else dev::launch_k(k_combine2<false>, dim3(nb), dim3(256), 0, s, a, rCoarse, fast::ResArgs{});
 }
 
 }  // namespace fused2

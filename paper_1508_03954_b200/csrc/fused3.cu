@@ -108,6 +108,7 @@ template <bool BPX>
 __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     k_fused3(const __grid_constant__ CUtensorMap mapU,
              const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
+    dev::griddep_wait();
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int SE = stage_elems<BPX>();
     double2* ring = reinterpret_cast<double2*>(smem);          // STAGES x {U, S, C[, I]}
@@ -433,6 +434,7 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
 
 template <bool SMOOTH>
 __global__ void __launch_bounds__(256) k_combine(const Args a, double2* rc, int za, int zb, const fast::ResArgs sa) {
+    dev::griddep_wait();
     const int mc = a.g.mc, m = a.g.m, zc = a.g.zc;
     const unsigned n1c = a.n1c;
     const unsigned first = static_cast<unsigned>(za) * n1c * n1c;  // coarse lattices < 2^32 points
@@ -565,13 +567,13 @@ void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
             cudaFuncSetAttribute(k_fused3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             configured[1] = true;
         }
-        k_fused3<true><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapC, mapI, a);
+        dev::launch_k(k_fused3<true>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
     } else {
         if (!configured[0]) {
             cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
             configured[0] = true;
         }
-        k_fused3<false><<<grid, dim3(TX, TY), smem, s>>>(mapU, mapC, mapI, a);
+        dev::launch_k(k_fused3<false>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
     }
 }
 
@@ -582,8 +584,8 @@ void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s, int z
         zb = a.g.mc + 1;
     }
     if (zb <= za) return;
-    if (smooth) k_combine<true><<<nblocks, 256, 0, s>>>(a, rCoarse, za, zb, *smooth);
-    else k_combine<false><<<nblocks, 256, 0, s>>>(a, rCoarse, za, zb, fast::ResArgs{});
+    if (smooth) dev::launch_k(k_combine<true>, dim3(nblocks), dim3(256), 0, s, a, rCoarse, za, zb, *smooth);
+    else dev::launch_k(k_combine<false>, dim3(nblocks), dim3(256), 0, s, a, rCoarse, za, zb, fast::ResArgs{});
 }
 
 }  // namespace fused3

@@ -7,8 +7,41 @@
 
 #include "exact_ops.cuh"
 
+#include <cstdlib>
+#include <utility>
+
 namespace tmg {
 namespace dev {
+
+// Programmatic dependent launch: kernels launched with launch_k may be
+// dispatched while their predecessor in the stream drains; each such kernel
+// starts with griddep_wait(), which returns once the predecessor grid has
+// completed and its memory is visible (a no-op for ordinary launches).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+    const char* e = std::getenv("TMG_PDL");  // developer A/B (read per launch)
+    return !(e && e[0] == '0');
+}
+
+template <class... KArgs, class... Args>
+inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    if (!pdl_enabled()) {
+        kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 struct Lvl {
     double2* u;
