@@ -2,8 +2,8 @@
 the pyramid top-down (fast::topdown_pyramid vs chain_down + topdown_coarse,
 TMG_PYR=0), the bottom-up below level L-1 (fast::up_coop and the smoothing
 folded into the restriction kernels vs restrict / smooth launches + the
-cluster chain, TMG_UP=0) and the parent-triple top-down of big coarse levels
-(TMG_TRI_COARSE=0).  Bitwise equal iterates and norms,
+cluster chain, TMG_UP=0), the parent-triple top-down of big coarse levels
+(TMG_TRI_COARSE=0) and programmatic dependent launch (TMG_PDL=0).  Bitwise equal iterates and norms,
 2D and 3D, additive / BPX / hb / ell_min, several tile-boundary alignments."""
 import os
 
@@ -21,7 +21,7 @@ CASES = [
 
 
 def _run(tmg, dim, level, phi, kind, new, cycles=4):
-    os.environ["TMG_PYR"] = os.environ["TMG_UP"] = os.environ["TMG_TRI_COARSE"] = "1" if new else "0"
+    os.environ["TMG_PYR"] = os.environ["TMG_UP"] = os.environ["TMG_TRI_COARSE"] = os.environ["TMG_PDL"] = "1" if new else "0"
     try:
         pol = {"add": tmg.Policy("exponential", 0.6), "bpx": tmg.Policy("undamped", 0.5, bpx=True),
                "bpx2": tmg.Policy("undamped", 0.5, bpx=True), "lgrid": tmg.Policy("lgrid", 0.6, lgrid=1),
@@ -37,6 +37,7 @@ def _run(tmg, dim, level, phi, kind, new, cycles=4):
         os.environ.pop("TMG_PYR", None)
         os.environ.pop("TMG_UP", None)
         os.environ.pop("TMG_TRI_COARSE", None)
+        os.environ.pop("TMG_PDL", None)
 
 
 @pytest.mark.parametrize("dim,level,phi,kind", CASES)
