@@ -40,6 +40,11 @@ CONFIGS = {
     # cfg3: 3D depth 5, k=20, exponential 0.6, 50 cycles (vertex cap raised)
     "cfg3": dict(problem="helmholtz-sin", dim=3, level=5, phi="400,200", cycle="td-add", omega="exponential",
                  omega_s=0.6, max_sweeps=50, target_drop=1e-30, max_vertices=40000000, **SEEDED),
+    # the headline workload itself (cfg5's final level, 729^3, k=80): the first 2 cycles (about 130 GB of host
+    # RAM and ~15 min per sweep on one core -- generated on the GPU host, tests/golden/make_head_golden.sh)
+    "cfg5_l6_head": dict(problem="helmholtz-sin", dim=3, level=6, phi="6400,3200", cycle="td-add",
+                         omega="exponential", omega_s=0.6, max_sweeps=2, target_drop=1e-30, max_vertices=500000000,
+                         **SEEDED),
     # cfg3 operator at 81^3 (fast to regenerate; used by the CPU suite's oracle pin)
     "cfg3_l4": dict(problem="helmholtz-sin", dim=3, level=4, phi="400,200", cycle="td-add", omega="exponential",
                     omega_s=0.6, max_sweeps=12, target_drop=1e-30, **SEEDED),
@@ -159,6 +164,6 @@ def generate(name: str) -> dict:
 
 
 if __name__ == "__main__":
-    for n in sys.argv[1:] or [k for k in CONFIGS if k not in ("cfg2", "cfg3", "cfg4")]:
+    for n in sys.argv[1:] or [k for k in CONFIGS if k not in ("cfg2", "cfg3", "cfg4", "cfg5_l6_head")]:
         r = generate(n)
         print(n, r["outcome"], r["sweeps"], f"{r['reference_seconds_per_sweep']:.3f}s/sweep", flush=True)
