@@ -10,6 +10,6 @@ set -e
 cd "$(dirname "$0")/../.."
 mkdir -p gpurun_out
 ulimit -v 185000000
-/usr/bin/time -v python tests/golden/make_goldens.py cfg5_l6_head > gpurun_out/head_golden.log 2>&1 || true
-cp tests/golden/cfg5_l6_head.json gpurun_out/ 2>/dev/null || true
+python tests/golden/make_goldens.py cfg5_l6_head > gpurun_out/head_golden.log 2>&1 || true
+free -g >> gpurun_out/head_golden.log; cp tests/golden/cfg5_l6_head.json gpurun_out/ 2>/dev/null || true
 tail -30 gpurun_out/head_golden.log
