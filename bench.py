@@ -22,9 +22,13 @@ DoF x cycles / max-over-ranks device time.  2D workloads run one replica
 per GPU ("scaling": "weak").  --mode replicas forces replicas.
 
 --impl reference: the reference CPU implementation (oracle/_ref, built from
-the unmodified reference sources) on the host cores -- one independent
-single-threaded reference process per core on an 81^3 sample of the same
-operator (the reference has no intra-solve parallelism), rank 0 only.
+the unmodified reference sources) on the host cores -- one single-threaded
+reference process per core (the reference has no intra-solve parallelism;
+capped by host RAM), rank 0 only.  The sample is the workload itself where
+the reference can hold it in a few minutes (2D, 243^3) and otherwise the
+243^3 tree with the workload's operator (cfg5: its own FMG stage 5; 729^3
+needs ~130 GB and ~15 min per sweep); the line's cpu_baseline.sample says
+which.  `config` is the workload, identical in both arms.
 """
 from __future__ import annotations
 
@@ -61,6 +65,17 @@ WORKLOADS = {
 RHS_SEED = 12345
 
 
+def workload_config(name, w):
+    """The `config` object of the JSON line: the workload only, identical in the
+    B200 arm and the reference arm (run settings are top-level keys)."""
+    if w.get("sphere_levels") or w.get("dynamic"):
+        return {"workload": name, "desc": w["desc"]}
+    n_lat = lattice(w["level"], w["dim"])
+    return {"workload": name, "desc": w["desc"], "dim": w["dim"], "level": w["level"],
+            "interior_dof": interior(w), "cycle": w["cycle"],
+            "l2": f"inputs larger than L2 (fine level arrays of {16 * n_lat / 1e9:.2f} GB each); no flush"}
+
+
 def interior(w):
     return (3 ** w["level"] - 1) ** w["dim"]
 
@@ -70,10 +85,17 @@ def lattice(level, dim):
 
 
 def fine_bytes_per_vertex(w, precision):
-    """Algorithmic HBM bytes per fine vertex of the fine pass.
-    counts 80 B (u, sc, b read; u, sc written).  The fused fast passes keep the
-    fine state as v = u + sc (fused3.cuh), so the minimum is 64 B (v, b read;
-    v, sc written); the exact pass is not fused (176 B)."""
+    """Algorithmic HBM bytes per fine vertex of the fine pass, SURVEY §8(d):
+    80 B (u, sc, b read; u, sc written) -- the basis of roofline.achieved.  The
+    fused fast passes move less for the same work (v-form, fused3.cuh:
+    v, b read, v, sc written = 64 B); the exact pass is not fused (176 B)."""
+    if precision == "exact":
+        return 176
+    return 80 if w["dim"] >= 2 else 128
+
+
+def moved_bytes_per_vertex(w, precision):
+    """Bytes per fine vertex the implementation's fine pass actually has to move."""
     if precision == "exact":
         return 176
     return 64 if w["dim"] >= 2 else 128
@@ -199,55 +221,89 @@ class ClockSampler:
 
 # --------------------------------------------------------------------------
 # reference CPU arm
-def _ref_worker(args):
-    w, steps, warmup, q = args
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
-    import refdriver as R
-    cfg = dict(problem="helmholtz-sin", dim=w["dim"], level=w["sample_level"],
+def _ref_cfg(w, level):
+    cfg = dict(problem="helmholtz-sin", dim=w["dim"], level=level,
                phi=f"{w['k'] ** 2},{0.5 * w['k'] ** 2}", cycle=w["cycle"], omega=w["omega"],
                omega_s=w["omega_s"], max_sweeps=10 ** 6, target_drop=1e-300, rhs="seeded", rhs_seed=RHS_SEED,
                max_vertices=10 ** 9)
     if w.get("sphere_levels"):
         cfg.update(sphere_levels=w["sphere_levels"], rhs_mask="sphere")
-    s = R.RefSession(cfg)
+    return cfg
+
+
+def _ref_worker(args):
+    w, level, sweeps, warmup, bar, q = args
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import refdriver as R
+    s = R.RefSession(_ref_cfg(w, level))
     for n in range(1, warmup + 1):
         s.sweep(n)
-    times = []
-    for n in range(warmup + 1, warmup + steps + 1):
-        t0 = time.perf_counter()
+    bar.wait()  # every process starts its timed sweeps together
+    for n in range(warmup + 1, warmup + sweeps + 1):
         s.sweep(n)
-        times.append(time.perf_counter() - t0)
-    q.put(times)
+    q.put(1)
 
 
-def reference_sample(w, steps, warmup, procs):
-    """Time `procs` independent reference processes on a bounded sample."""
-    ws = dict(w)
-    ws["sample_level"] = (3 if w.get("sphere_levels") else 4) if w["dim"] == 3 else min(w["level"], 6)
-    ctx = mp.get_context("spawn")
-    q = ctx.Queue()
-    ps = [ctx.Process(target=_ref_worker, args=((ws, steps, warmup, q),)) for _ in range(procs)]
-    for p in ps:
-        p.start()
-    res = [q.get() for _ in ps]
-    for p in ps:
-        p.join()
-    dof = (3 ** ws["sample_level"] - 1) ** w["dim"]
+def sample_level(w):
+    """The reference sample of a workload.  3D regular: the 243^3 tree with the
+    workload's operator (for cfg5 that is its own FMG stage 5; the reference's
+    per-DoF rate does not depend on the size: 4.0e5 at 81^3, 4.2e5 at
+    243^3, while 729^3 needs ~130 GB and ~15 min per sweep on one core).  2D and
+    the adaptive tree: the workload itself (levels <= 7) or its base 3."""
+    if w.get("sphere_levels"):
+        return 3
+    if w["dim"] == 3:
+        return min(w["level"], 5)
+    return min(w["level"], 7)
+
+
+def host_ram_gb():
+    try:
+        return os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES") / 1e9
+    except (ValueError, OSError):
+        return 16.0
+
+
+def reference_sample(w, sweeps, warmup, procs):
+    """`procs` concurrent single-threaded reference processes (the reference has
+    no intra-solve parallelism), each `warmup` untimed + `sweeps` timed cycles of
+    the sample; value = all timed DoF-updates / wall time of the timed region
+    (from the barrier all processes pass after their warm-up to the last finish)."""
+    level = sample_level(w)
+    dof = (3 ** level - 1) ** w["dim"]
     if w.get("sphere_levels"):
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import refdriver as R
-        s = R.RefSession(dict(problem="helmholtz-sin", dim=w["dim"], level=ws["sample_level"],
+        s = R.RefSession(dict(problem="helmholtz-sin", dim=w["dim"], level=level,
                               sphere_levels=w["sphere_levels"], max_vertices=10 ** 9))
         dof = s.interior_count()
-    per_step = [max(r[i] for r in res) for i in range(steps)]  # all processes finish a step
-    total = sum(per_step)
-    value = procs * dof * steps / total
-    what = (f"the level-{ws['sample_level']} + {w['sphere_levels']} sphere-refined sub-problem ({dof} leaf DoF)"
+        s.close()
+    # ~350 B of reference RSS per DoF (BASELINE.md §2: 4.87 GB at 243^3)
+    procs = max(1, min(procs, int(0.7 * host_ram_gb() / max(350e-9 * dof, 1e-3))))
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    bar = ctx.Barrier(procs + 1)
+    ps = [ctx.Process(target=_ref_worker, args=((w, level, sweeps, warmup, bar, q),)) for _ in range(procs)]
+    for p in ps:
+        p.start()
+    bar.wait()
+    t0 = time.perf_counter()
+    for _ in ps:
+        q.get()
+    wall = time.perf_counter() - t0
+    for p in ps:
+        p.join()
+    value = procs * dof * sweeps / wall
+    cells = f"{3 ** level}^{w['dim']}"
+    what = (f"the level-{level} + {w['sphere_levels']} sphere-refined tree ({dof} leaf DoF)"
             if w.get("sphere_levels") else
-            f"the level-{ws['sample_level']} sub-problem ({3 ** ws['sample_level']}^{w['dim']} cells, {dof} DoF)")
-    sample = (f"{procs} independent single-threaded reference processes, each {steps} timed cycles (+{warmup} warm-up) "
-              f"of the same operator on {what}")
-    return value, total / steps, sample
+            f"the {cells} tree ({dof} DoF) with the workload's operator" +
+            ("" if level == w["level"] else f" (the workload is {3 ** w['level']}^{w['dim']}; {cells} is "
+                                              f"{'its FMG stage ' + str(level) if w['dim'] == 3 else 'a sub-problem'})"))
+    sample = (f"{procs} concurrent single-threaded reference processes (oracle/_ref, unmodified reference sources), "
+              f"each {warmup} untimed + {sweeps} timed td cycles on {what}; value = {procs * sweeps} timed cycles x "
+              f"DoF / wall time of the timed region")
+    return value, wall / sweeps, sample, procs
 
 
 def level_for_h(h):  # runner.cpp:165-174
@@ -293,7 +349,7 @@ def run_reference_arm(args, w):
             "impl": "reference", "n_gpus": args.gpus, "steps": min(args.steps, 16), "warmup": 0,
             "ms_per_step": sec * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "complex128 (f64)", "data": "synthetic (analytic sin rhs)",
-            "config": {"workload": args.workload, "desc": w["desc"], "precision": "reference"},
+            "config": workload_config(args.workload, w), "precision": "reference",
             "cpu_baseline": {"value": value, "unit": "DoF-updates/s", "cores": 1, "kind": "reference", "sample": sample},
             "e2e": {"value": value, "unit": "DoF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
         return 0
@@ -305,13 +361,16 @@ def run_reference_arm(args, w):
     if not os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libtreemg_ref.so")):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtreemg_ref.so not built"}))
         return 0
-    value, sec_per_step, sample = reference_sample(w, args.steps, args.warmup, procs)
+    # every process the same number of timed cycles: the K steps spread over the cores
+    sweeps = max(1, -(-args.steps // procs))
+    value, sec_per_cycle, sample, procs = reference_sample(w, sweeps, 1, procs)
     line = {
         "metric": "complex DoF-updates/s per additive MG cycle", "value": value, "unit": "DoF-updates/s",
         "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": sec_per_step * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "ms_per_step": interior(w) / value * 1e3 if not w.get("sphere_levels") else sec_per_cycle * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "complex128 (f64)", "data": "synthetic (seeded uniform complex rhs, SURVEY §8d)",
-        "config": {"workload": args.workload, "desc": w["desc"], "precision": "reference"},
+        "config": workload_config(args.workload, w), "precision": "reference (bit-exact complex128)",
         "cpu_baseline": {"value": value, "unit": "DoF-updates/s", "cores": procs, "kind": "reference",
                          "sample": sample},
         "e2e": {"value": value, "unit": "DoF-updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -346,7 +405,7 @@ def run_amr(args, w):
     achieved = B / (total_ms / args.steps / 1e3) / 1e9
     cpu = None
     if ctx.rank == 0 and ctx.world == 1 and not args.no_cpu_baseline:
-        v, _, sample = reference_sample(w, 3, 1, 1)
+        v, _, sample, _ = reference_sample(w, 3, 1, 1)
         cpu = {"value": v, "unit": "DoF-updates/s", "cores": 1, "kind": "reference", "sample": sample}
     # e2e through the public C-ABI: treemg_run of the same configuration (setup + cycles + norms to the host)
     t0 = time.perf_counter()
@@ -527,10 +586,17 @@ def main():
                 f"({fine_bytes_per_vertex(w, args.precision)} B per fine vertex)",
                 "peak_kind": peak_kind, "whole_cycle_GBps": B_total / (ms_per_step / 1e3) / 1e9}
 
+    moved = moved_bytes_per_vertex(w, args.precision)
+    roofline["basis"] = (f"SURVEY §8(d) algorithmic bytes: {fine_bytes_per_vertex(w, args.precision)} B per fine "
+                         f"lattice vertex x {B_fine // fine_bytes_per_vertex(w, args.precision)} vertices per launch")
+    roofline["frac_moved_basis"] = roofline["frac"] * moved / fine_bytes_per_vertex(w, args.precision)
+    roofline["moved_bytes_per_vertex"] = moved
     tr = ncu_traffic(args.workload, args.precision, mode) if mode != "slabs" or world == 1 else None
     if tr:
         roofline["traffic"] = tr["bytes_per_launch"]
         roofline["traffic_source"] = tr["source"]
+        # the kernel's actual DRAM bytes (ncu) over its live event-timed duration
+        roofline["frac_dram_actual"] = tr["bytes_per_launch"] / (fine_ms / 1e3) / 1e9 / peak
 
     # e2e through the boundary: host rhs (pinned) -> device -> one cycle -> host norms
     n_lat = lattice(w["level"], w["dim"])
@@ -575,7 +641,8 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, sps, sample = reference_sample(w, 4, 1, 1)
+            # one cycle of the 243^3 sample (~35 s of CPU work; 3D) without warm-up
+            v, sps, sample, _ = reference_sample(w, 1, 0, 1)
             cpu = {"value": v, "unit": "DoF-updates/s", "cores": 1, "kind": "reference", "sample": sample}
         except Exception as exc:  # reported, never silently replaced
             cpu = {"value": None, "unit": "DoF-updates/s", "cores": 1, "kind": "reference",
@@ -588,12 +655,9 @@ def main():
             "higher_is_better": True, "scaling": "strong" if mode == "slabs" else "weak", "vs_baseline": None,
             "dtype": "complex128 (f64)",
             "data": "synthetic (seeded uniform complex rhs, SURVEY §8d)",
-            "config": {"workload": args.workload, "desc": w["desc"], "dim": w["dim"], "level": w["level"],
-                       "interior_dof": dof, "precision": args.precision, "cycle": w["cycle"],
-                       "l2": "inputs larger than L2 (fine level arrays of "
-                             f"{16 * n_lat / 1e9:.2f} GB each); no flush",
-                       "parallelism": {"slabs": f"z-slabs x{world} (NCCL)", "replicas": f"replicas x{world}",
-                                       "single": "single GPU"}[mode]},
+            "config": workload_config(args.workload, w), "precision": args.precision,
+            "parallelism": {"slabs": f"z-slabs x{world} (NCCL)", "replicas": f"replicas x{world}",
+                            "single": "single GPU"}[mode],
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
             "gpu_launches": launches_per_cycle * args.steps, "fine_pass_ms": fine_ms,
         }

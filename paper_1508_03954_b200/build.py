@@ -37,27 +37,49 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str = "", defines=()) -> str:
-    """Compile libtreemg_b200.so for sm_100a.  `out` / `defines` build a
-    variant library elsewhere (developer A/B of compile-time parameters)."""
+    """Compile libtreemg_b200.so for sm_100a (one nvcc per source file in
+    parallel, then one link).  `out` / `defines` build a variant library
+    elsewhere (developer A/B of compile-time parameters)."""
+    import concurrent.futures as cf
+    import tempfile
     target = out or LIB
     if not out and not force and not _stale():
         return LIB
     srcs = [os.path.join(CSRC, f) for f in SOURCES if os.path.exists(os.path.join(CSRC, f))]
-    cmd = [nvcc_path(), "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-           "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-shared", "-Xlinker", "-soname=libtreemg_b200.so",
-           "-I" + os.path.join(ROOT, "include"), "-o", target + ".tmp"] + ["-D" + d for d in defines] + srcs
+    base = [nvcc_path()]
     # host compiler: the system g++ so libstdc++ is linked dynamically
     if os.path.exists("/usr/bin/g++"):
-        cmd[1:1] = ["-ccbin", "/usr/bin/g++"]
-    res = subprocess.run(cmd, capture_output=True, text=True, cwd=ROOT)
+        base += ["-ccbin", "/usr/bin/g++"]
+    flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
+             "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
+    flags += ["-D" + d for d in defines]
+    tmp = tempfile.mkdtemp(prefix="tmg_build_")
+    objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in srcs]
+
+    def compile_one(i):
+        return subprocess.run(base + flags + ["-c", srcs[i], "-o", objs[i]], capture_output=True, text=True, cwd=ROOT)
+
+    with cf.ThreadPoolExecutor(max_workers=min(len(srcs), os.cpu_count() or 4)) as ex:
+        results = list(ex.map(compile_one, range(len(srcs))))
+    log = ""
+    for src, res in zip(srcs, results):
+        log += f"== {os.path.basename(src)}\n" + res.stdout + res.stderr
+    link = base + ["-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-Xlinker", "-soname=libtreemg_b200.so",
+                   "-o", target + ".tmp"] + objs
+    ok = all(r.returncode == 0 for r in results)
+    if ok:
+        lres = subprocess.run(link, capture_output=True, text=True, cwd=ROOT)
+        log += lres.stdout + lres.stderr
+        ok = lres.returncode == 0
     if not out:
         with open(os.path.join(PKG, "build.log"), "w") as f:
-            f.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
-    if res.returncode != 0:
-        raise RuntimeError("nvcc build failed:\n" + res.stderr[-6000:])
+            f.write(" ".join(base + flags) + "\n" + log)
+    shutil.rmtree(tmp, ignore_errors=True)
+    if not ok:
+        raise RuntimeError("nvcc build failed:\n" + log[-6000:])
     os.replace(target + ".tmp", target)
     if verbose:
-        print(res.stderr)
+        print(log)
     return target
 
 

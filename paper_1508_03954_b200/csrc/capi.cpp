@@ -3,6 +3,8 @@
 // thread-local last error, exception -> status mapping; exceptions never
 // cross the boundary.
 
+#include <cuda_runtime.h>
+
 #include <cstring>
 #include <memory>
 #include <string>
@@ -26,16 +28,31 @@ struct treemg_result {
 
 struct tmg_hierarchy {
     std::unique_ptr<Hierarchy> h;
+    int device = 0;
     SweepStats last;  // per-channel norms of the last sweep (tmg_channel_norms)
 };
 
 struct tmg_slabs {
     std::unique_ptr<SlabGroup> g;
+    int device = 0;
 };
 
 namespace {
 
 thread_local std::string g_lastError;
+
+// A handle's kernels run on its own device whatever device is current on the
+// calling thread (treemg.h: a handle may move between threads); restored on exit.
+struct DeviceScope {
+    int prev = -1, want;
+    explicit DeviceScope(int device) : want(device) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != want) cudaSetDevice(want);
+    }
+    ~DeviceScope() {
+        if (prev >= 0 && prev != want) cudaSetDevice(prev);
+    }
+};
 
 treemg_status fail(treemg_status code, const char* what) {
     g_lastError = what ? what : "unknown error";
@@ -244,7 +261,12 @@ treemg_status tmg_slabs_create(const tmg_problem* prob, int local, int rank, int
     if (!prob || !out) return fail(TREEMG_E_USAGE, "null argument");
     *out = nullptr;
     auto* h = new tmg_slabs();
-    const treemg_status st = guarded([&] { h->g = std::make_unique<SlabGroup>(problem_from(prob), local, rank, world, nccl_id); });
+    const treemg_status st = guarded([&] {
+        const Problem p = problem_from(prob);
+        h->device = p.device;
+        const DeviceScope ds(h->device);
+        h->g = std::make_unique<SlabGroup>(p, local, rank, world, nccl_id);
+    });
     if (st != TREEMG_OK) {
         delete h;
         return st;
@@ -253,11 +275,16 @@ treemg_status tmg_slabs_create(const tmg_problem* prob, int local, int rank, int
     return TREEMG_OK;
 }
 
-void tmg_slabs_destroy(tmg_slabs* h) { delete h; }
+void tmg_slabs_destroy(tmg_slabs* h) {
+    if (!h) return;
+    const DeviceScope ds(h->device);
+    delete h;
+}
 
 treemg_status tmg_slabs_cycle(tmg_slabs* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
     if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         Policy p = policy_from(pol);
         if (n < 1) throw ConfigError("sweep counter starts at 1");
         if (p.bpx) p.hbMask = false;
@@ -267,12 +294,14 @@ treemg_status tmg_slabs_cycle(tmg_slabs* h, const tmg_policy* pol, int n, tmg_sw
 
 treemg_status tmg_slabs_get_fine_u(tmg_slabs* h, double* out) {
     if (!h || !out) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->g->get_fine_u(out); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->g->get_fine_u(out); });
 }
 
 treemg_status tmg_slabs_time_cycles(tmg_slabs* h, const tmg_policy* pol, int n0, int count, double* out4) {
     if (!h || !pol || !out4) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         Policy p = policy_from(pol);
         if (p.bpx) p.hbMask = false;
         h->g->time_cycles(p, n0, count, out4);
@@ -283,6 +312,7 @@ treemg_status tmg_slabs_e2e_step(tmg_slabs* h, const tmg_policy* pol, int n, con
                                  long long* h2d_bytes) {
     if (!h || !pol || !chi || !out3) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         Policy p = policy_from(pol);
         if (p.bpx) p.hbMask = false;
         h->g->e2e_step(p, n, chi, out3, h2d_bytes);
@@ -292,7 +322,17 @@ treemg_status tmg_slabs_e2e_step(tmg_slabs* h, const tmg_policy* pol, int n, con
 treemg_status tmg_slab_plan(int levels, int world, int* out8) {
     if (!out8) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
-        const auto plan = slab_plan(levels, world);
+        // the chunking the live device runs (co-resident fused blocks); 3 x 148 without a GPU
+        int ndev = 0, resident = 3 * 148;
+        if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
+            int dev = 0, sms = 148;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            resident = fused3_resident_blocks(sms);
+        } else {
+            cudaGetLastError();
+        }
+        const auto plan = slab_plan(levels, world, resident);
         for (size_t r = 0; r < plan.size(); ++r)
             for (int k = 0; k < 8; ++k) out8[8 * r + static_cast<size_t>(k)] = plan[r][static_cast<size_t>(k)];
     });
@@ -309,6 +349,8 @@ treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out)
     auto* h = new tmg_hierarchy();
     const treemg_status st = guarded([&] {
         const Problem p = problem_from(prob);
+        h->device = p.device;
+        const DeviceScope ds(h->device);
         h->h = std::make_unique<Hierarchy>(p);
     });
     if (st != TREEMG_OK) {
@@ -319,11 +361,16 @@ treemg_status tmg_hierarchy_create(const tmg_problem* prob, tmg_hierarchy** out)
     return TREEMG_OK;
 }
 
-void tmg_hierarchy_destroy(tmg_hierarchy* h) { delete h; }
+void tmg_hierarchy_destroy(tmg_hierarchy* h) {
+    if (!h) return;
+    const DeviceScope ds(h->device);
+    delete h;
+}
 
 treemg_status tmg_td_add(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
     if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         Policy p = policy_from(pol);
         if (p.bpx) throw ConfigError("td_add: policy has bpx set, use td_bpx");  // cycles.cpp:338
         if (n < 1) throw ConfigError("sweep counter starts at 1");
@@ -334,6 +381,7 @@ treemg_status tmg_td_add(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_swe
 treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
     if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         Policy p = policy_from(pol);
         if (n < 1) throw ConfigError("sweep counter starts at 1");
         p.bpx = true;  // cycles.cpp:349-351
@@ -345,6 +393,7 @@ treemg_status tmg_td_bpx(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_swe
 treemg_status tmg_bu_fas(tmg_hierarchy* h, const tmg_policy* pol, int n, tmg_sweep_stats* out) {
     if (!h || !pol) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         if (n < 1) throw ConfigError("sweep counter starts at 1");
         fill_stats(h->h->bu_fas(policy_from(pol), n), out);
     });
@@ -354,6 +403,7 @@ treemg_status tmg_textbook_add(tmg_hierarchy* h, double omega_s_re, double omega
                                double omega_cg_im, tmg_sweep_stats* out) {
     if (!h) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         fill_stats(h->h->textbook_add(Cplx(omega_s_re, omega_s_im), Cplx(omega_cg_re, omega_cg_im)), out);
     });
 }
@@ -362,33 +412,39 @@ long long tmg_lattice_size(const tmg_hierarchy* h, int level) { return h ? h->h-
 
 treemg_status tmg_get_field(tmg_hierarchy* h, int level, const char* field, double* out) {
     if (!h || !field || !out) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->get_field(level, field, out); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->get_field(level, field, out); });
 }
 
 treemg_status tmg_set_field(tmg_hierarchy* h, int level, const char* field, const double* in) {
     if (!h || !field || !in) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->set_field(level, field, in); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->set_field(level, field, in); });
 }
 
 treemg_status tmg_set_fine_interior_u(tmg_hierarchy* h, const double* u) {
     if (!h || !u) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->set_fine_interior_u(u); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->set_fine_interior_u(u); });
 }
 
 treemg_status tmg_set_random_initial_guess(tmg_hierarchy* h, unsigned long long seed) {
     if (!h) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->set_random_initial_guess(seed); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->set_random_initial_guess(seed); });
 }
 
 treemg_status tmg_set_fine_rhs(tmg_hierarchy* h, const double* chi) {
     if (!h || !chi) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->set_fine_rhs(chi); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->set_fine_rhs(chi); });
 }
 
 treemg_status tmg_get_flags(tmg_hierarchy* h, int level, unsigned char* flags, signed char* succ,
                             unsigned char* cells) {
     if (!h) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         if (!h->h->get_flags(level, flags, succ, cells)) throw ConfigError("get_flags: the tree is regular");
     });
 }
@@ -521,17 +577,20 @@ unsigned long long tmg_field_hash(tmg_hierarchy* h, int level, const char* field
 treemg_status tmg_time_cycles(tmg_hierarchy* h, const tmg_policy* pol, int n0, int count, int flush_l2,
                               double* out4) {
     if (!h || !pol || !out4) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->time_cycles(policy_from(pol), n0, count, flush_l2 != 0, out4); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->time_cycles(policy_from(pol), n0, count, flush_l2 != 0, out4); });
 }
 
 treemg_status tmg_e2e_step(tmg_hierarchy* h, const tmg_policy* pol, int n, const double* chi, double* out3) {
     if (!h || !pol || !chi || !out3) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->e2e_step(policy_from(pol), n, chi, out3); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->e2e_step(policy_from(pol), n, chi, out3); });
 }
 
 treemg_status tmg_mark(tmg_hierarchy* h, long long* out9) {
     if (!h) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
+        const DeviceScope ds(h->device);
         const AmrMarkStats m = h->h->mark();
         if (out9) {
             const long long v[9] = {h->last.refinedCells, h->last.erasedCells, m.refineVertices, m.eraseVertices,
@@ -553,7 +612,8 @@ long long tmg_existing_vertices(const tmg_hierarchy* h) { return h ? h->h->exist
 
 treemg_status tmg_set_cell_marks(tmg_hierarchy* h, int level, const unsigned char* cells) {
     if (!h || !cells) return fail(TREEMG_E_USAGE, "null argument");
-    return guarded([&] { h->h->set_cell_marks(level, cells); });
+    return guarded([&] {
+        const DeviceScope ds(h->device); h->h->set_cell_marks(level, cells); });
 }
 
 int tmg_channel_norms(tmg_hierarchy* h, double* maxNorm, double* euclid, double* hNorm, int cap) {

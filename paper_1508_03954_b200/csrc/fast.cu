@@ -1445,8 +1445,7 @@ void topdown_coarse(int P, const Lvl& c, const Lvl& pr, int bpx, int blocks, cud
         dev::launch_k(k_topdown3_rows, dim3(c.m - 1, zhi - zlo), dim3(kRowThreads), smem, s, c, pr, bpx, zlo);
         return;
     }
-    const char* tri = std::getenv("TMG_TRI_COARSE");
-    if (P >= 2 && c.m >= 243 && !(tri && tri[0] == '0')) {  // big levels: parent-cell triples (k_topdown_tri)
+    if (P >= 2 && c.m >= 243 && dev::switches().triCoarse) {  // big levels: parent-cell triples (k_topdown_tri)
         const unsigned plane = P == 3 ? c.n1 : 1u;  // rows per plane of the last axis
         const unsigned ra = za < 0 ? 0u : static_cast<unsigned>(za) * plane;
         const unsigned rb = za < 0 ? c.n / c.n1 : std::min<unsigned>(static_cast<unsigned>(zb) * plane, c.n / c.n1);

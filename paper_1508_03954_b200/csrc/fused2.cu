@@ -329,12 +329,10 @@ size_t smem_bytes(const Geometry& g, bool bpx) {
 void launch(const Args& a, cudaStream_t s) {
     dim3 grid(a.g.nbx, a.g.nby);
     const size_t smem = smem_bytes(a.g, a.bpx != 0);
-    static bool configured = false;  // static + dynamic shared memory may pass 48 KB (BPX, long chunks)
-    if (!configured) {
-        cudaFuncSetAttribute(k_fused2<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        cudaFuncSetAttribute(k_fused2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
-        configured = true;
-    }
+    // static + dynamic shared memory may pass 48 KB (BPX, long chunks); a per-device
+    // attribute, so set on every launch (host-side call)
+    cudaFuncSetAttribute(a.bpx ? k_fused2<true> : k_fused2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         96 * 1024);
     if (a.bpx) dev::launch_k(k_fused2<true>, grid, dim3(TX), smem, s, a);
     else dev::launch_k(k_fused2<false>, grid, dim3(TX), smem, s, a);
 }

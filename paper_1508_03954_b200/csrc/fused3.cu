@@ -502,7 +502,7 @@ Geometry geometry(int m, int mc, int parts, int resident) {
     // at least 8 chunks and ~2 waves of blocks (measured best at 243^3 and
     // 729^3; a finer wave model did not pay), in multiples of `parts`
     int want = std::max(8, (2 * std::max(1, resident) + tiles - 1) / tiles);
-    if (const char* e = std::getenv("TMG_ZCHUNKS")) want = std::max(1, std::atoi(e));  // developer A/B
+    if (dev::switches().zchunks > 0) want = dev::switches().zchunks;  // developer A/B
     want = (want + parts - 1) / parts * parts;
     for (;; want += parts) {
         g.zc = std::max(3, ((inner + want - 1) / want + 2) / 3 * 3);
@@ -558,21 +558,16 @@ int resident_blocks(int smCount) {
 
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
             const CUtensorMap& mapI, cudaStream_t s, int nchunks) {
-    static bool configured[2] = {false, false};
+    // the shared-memory limit is a per-device function attribute: set it on every
+    // launch (a host-side call, no device work) so a second device is configured too
     const bool bpx = a.bpx != 0;
     const size_t smem = smem_bytes(bpx);
     dim3 grid(a.g.nbx, a.g.nby, nchunks > 0 ? nchunks : a.g.nbz);
     if (bpx) {
-        if (!configured[1]) {
-            cudaFuncSetAttribute(k_fused3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            configured[1] = true;
-        }
+        cudaFuncSetAttribute(k_fused3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         dev::launch_k(k_fused3<true>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
     } else {
-        if (!configured[0]) {
-            cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-            configured[0] = true;
-        }
+        cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         dev::launch_k(k_fused3<false>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
     }
 }

@@ -802,8 +802,7 @@ struct Hierarchy::Impl {
     // points (memory-level parallelism for the bandwidth-bound level passes)
     int blocks_for(unsigned n) const {
         const long long need = (static_cast<long long>(n) + 255) / 256;
-        const char* cap = std::getenv("TMG_GRID_CAP");
-        const long long perSm = cap ? std::max(1, std::atoi(cap)) : 32;
+        const long long perSm = dev::switches().gridCap;
         return static_cast<int>(std::max<long long>(1, std::min<long long>(need, perSm * smCount)));
     }
 
@@ -1294,8 +1293,7 @@ struct Hierarchy::Impl {
     // fast::up_coop, which restricts out of S)
     bool use_up() const { return use_up_from(L - 1); }
     bool use_up_from(int from) const {
-        const char* e = std::getenv("TMG_UP");  // developer A/B (read per call: tests flip it in-process)
-        return !(e && e[0] == '0') && chainBar && (p == 2 || p == 3) && from >= 2 && chain_top(from) >= 2;
+        return dev::switches().up && chainBar && (p == 2 || p == 3) && from >= 2 && chain_top(from) >= 2;
     }
     // from: the level whose r is complete and smoothed (L-1 after the combine; the
     // slab path's replicated top L-2); norms = false: up_coop reduces no norms
@@ -1325,9 +1323,7 @@ struct Hierarchy::Impl {
 
     // coarse top-down of levels 1..L-1 as one pyramid launch (fast::topdown_pyramid)
     bool use_pyramid() const {
-        const char* e = std::getenv("TMG_PYR");  // developer A/B (read per call: tests flip it in-process)
-        const bool off = e && e[0] == '0';
-        return !off && (p == 2 || p == 3) && L >= 2 && L - 1 < fast::kPyrMaxLevels;
+        return dev::switches().pyr && (p == 2 || p == 3) && L >= 2 && L - 1 < fast::kPyrMaxLevels;
     }
     // pyramid up to the highest level below kPyrMaxN points, per-level launches above it
 #ifndef TMG_PYR_MAXN
@@ -1506,6 +1502,7 @@ struct Hierarchy::Impl {
 
 Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     Impl& I = *impl_;
+    dev::refresh_switches();  // developer A/B environment, read here, not on the launch path
     I.prob = prob;
     I.p = prob.dim;
     I.L = prob.levels;
@@ -1957,6 +1954,8 @@ std::uint64_t Hierarchy::field_hash(int level, const std::string& field) const {
     }
     return h;
 }
+
+int fused3_resident_blocks(int smCount) { return fused3::resident_blocks(smCount); }
 
 void test_divdc3(const double* x, const double* y, double* out, long long n) {
     std::vector<dev::DivConst> k(static_cast<size_t>(n));

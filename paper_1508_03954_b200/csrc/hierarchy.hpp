@@ -173,6 +173,8 @@ class SlabGroup {
 };
 
 std::vector<std::array<int, 8>> slab_plan(int levels, int world, int resident = 3 * 148);
+// co-resident blocks of the 3D fused fine pass on the current device (the chunking input of slab_plan)
+int fused3_resident_blocks(int smCount);
 
 // 128-byte NCCL unique id (dlopen'd libnccl); false if NCCL is unavailable.
 bool nccl_unique_id(void* out128);

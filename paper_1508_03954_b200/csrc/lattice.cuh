@@ -7,6 +7,7 @@
 
 #include "exact_ops.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 #include <utility>
 
@@ -19,10 +20,38 @@ namespace dev {
 // completed and its memory is visible (a no-op for ordinary launches).
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-inline bool pdl_enabled() {
-    const char* e = std::getenv("TMG_PDL");  // developer A/B (read per launch)
-    return !(e && e[0] == '0');
+// Developer A/B switches (environment), snapshotted when a
+// hierarchy is constructed (refresh_switches) instead of being read on the
+// launch path.  Every switch selects an older, bit-identical implementation.
+struct Switches {
+    bool pdl = true;        // TMG_PDL=0: ordinary launches
+    bool triCoarse = true;  // TMG_TRI_COARSE=0: one thread per point for big coarse top-downs
+    bool up = true;         // TMG_UP=0: restrict / smooth launches + cluster chain
+    bool pyr = true;        // TMG_PYR=0: per-level top-down launches
+    int gridCap = 32;       // TMG_GRID_CAP: blocks per SM of grid-stride launches
+    int zchunks = 0;        // TMG_ZCHUNKS: z-chunk count of the 3D fused pass (0: automatic)
+};
+inline Switches& switches() {
+    static Switches s;
+    return s;
 }
+inline void refresh_switches() {
+    auto on = [](const char* name) {
+        const char* e = std::getenv(name);
+        return !(e && e[0] == '0');
+    };
+    Switches& s = switches();
+    s.pdl = on("TMG_PDL");
+    s.triCoarse = on("TMG_TRI_COARSE");
+    s.up = on("TMG_UP");
+    s.pyr = on("TMG_PYR");
+    const char* cap = std::getenv("TMG_GRID_CAP");
+    s.gridCap = cap ? std::max(1, std::atoi(cap)) : 32;
+    const char* zc = std::getenv("TMG_ZCHUNKS");
+    s.zchunks = zc ? std::max(1, std::atoi(zc)) : 0;
+}
+
+inline bool pdl_enabled() { return switches().pdl; }
 
 template <class... KArgs, class... Args>
 inline void launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
