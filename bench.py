@@ -91,6 +91,8 @@ def fine_bytes_per_vertex(w, precision):
     v, b read, v, sc written = 64 B); the exact pass is not fused (176 B)."""
     if precision == "exact":
         return 176
+    if precision == "fast-complex64":  # SURVEY §8(d): complex64 halves B
+        return 40
     return 80 if w["dim"] >= 2 else 128
 
 
@@ -98,6 +100,8 @@ def moved_bytes_per_vertex(w, precision):
     """Bytes per fine vertex the implementation's fine pass actually has to move."""
     if precision == "exact":
         return 176
+    if precision == "fast-complex64":
+        return 32
     return 64 if w["dim"] >= 2 else 128
 
 
@@ -113,8 +117,10 @@ def fine_kernel_label(w, precision):
     if precision == "exact":
         return "exact fine pass (k_topdown + k_residual_exact + k_restrict_exact)"
     if w["dim"] == 3:
-        return "fused fine pass k_fused3 (TMA ring: top-down + residual + smooth + z/xy restriction)"
-    return "fine pass (k_topdown + k_residual + k_restrict)"
+        return ("fused fine pass k_fused3<complex64> (TMA ring: top-down + residual + smooth + z/xy restriction)"
+                if precision == "fast-complex64" else
+                "fused fine pass k_fused3 (TMA ring: top-down + residual + smooth + z/xy restriction)")
+    return "fused fine pass k_fused2 (row-marching strips: top-down + residual + smooth + restriction)"
 
 
 def ncu_traffic(workload: str, precision: str, mode: str):
@@ -517,8 +523,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--workload", default="cfg5", choices=list(WORKLOADS))
-    ap.add_argument("--precision", default=os.environ.get("TMG_PRECISION", "fast"), choices=["fast", "exact"])
+    ap.add_argument("--precision", default=os.environ.get("TMG_PRECISION", "fast"),
+                    choices=["fast", "exact", "fast-complex64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="developer A/B: skip the end-to-end leg")
     ap.add_argument("--mode", default=None, choices=["single", "slabs", "replicas"])
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
@@ -598,45 +606,47 @@ def main():
         # the kernel's actual DRAM bytes (ncu) over its live event-timed duration
         roofline["frac_dram_actual"] = tr["bytes_per_launch"] / (fine_ms / 1e3) / 1e9 / peak
 
-    # e2e through the boundary: host rhs (pinned) -> device -> one cycle -> host norms
-    n_lat = lattice(w["level"], w["dim"])
-    try:
-        import torch
-        chi_host = torch.empty(2 * n_lat, dtype=torch.float64, pin_memory=True).numpy()
-    except Exception:
-        chi_host = np.empty(2 * n_lat)
-    rng = np.random.default_rng(RHS_SEED)
-    chi_host[:] = rng.uniform(-1, 1, size=2 * n_lat)
-    h2d = 16 * n_lat
-    n0 = args.warmup + args.steps + 1
-    one = (lambda n: h.cycle(pol, n)) if mode == "slabs" else (h.td_bpx if pol.bpx else h.td_add)
-    if mode != "slabs":
-        one = (lambda f: (lambda n: f(pol, n)))(one)
-    # (a) a solve through the public API: the step's input (the rhs) uploaded
-    #     from pinned host memory once, then K cycles, each returning its norms
-    barrier()
-    t0 = time.perf_counter()
-    if mode == "slabs":
-        _, h2d = h.e2e_step(pol, n0, chi_host)
-    else:
-        h.e2e_step(pol, n0, chi_host)
-    for i in range(1, args.steps):
-        one(n0 + i)
-    solve_s = D.reduce_max(ctx, time.perf_counter() - t0)
-    # (b) the pessimistic variant: a fresh rhs uploaded before every cycle
-    reps = max(2, min(args.steps, 5))
-    barrier()
-    t0 = time.perf_counter()
-    for i in range(reps):
-        h.e2e_step(pol, n0 + args.steps + i, chi_host)
-    every_s = D.reduce_max(ctx, (time.perf_counter() - t0) / reps)
-    e2e = {"value": copies * dof * args.steps / solve_s, "unit": "DoF-updates/s",
-           "h2d_bytes_per_step": int(h2d) // max(1, args.steps), "d2h_bytes_per_step": 24,
-           "note": f"public-API solve of K={args.steps} cycles (wall clock, max over ranks): H2D of the nodal rhs "
-                   "(16 B/vertex from pinned memory; slabs: the rank's planes) and the device load vector once, "
-                   "then every cycle with D2H of its three residual norms",
-           "rhs_every_cycle": {"value": copies * dof / every_s, "h2d_bytes_per_step": int(h2d),
-                               "note": "a fresh rhs uploaded before each cycle (PCIe-bound)"}}
+    e2e = None
+    if not args.no_e2e:  # developer A/B runs skip the end-to-end leg
+        # e2e through the boundary: host rhs (pinned) -> device -> one cycle -> host norms
+        n_lat = lattice(w["level"], w["dim"])
+        try:
+            import torch
+            chi_host = torch.empty(2 * n_lat, dtype=torch.float64, pin_memory=True).numpy()
+        except Exception:
+            chi_host = np.empty(2 * n_lat)
+        rng = np.random.default_rng(RHS_SEED)
+        chi_host[:] = rng.uniform(-1, 1, size=2 * n_lat)
+        h2d = 16 * n_lat
+        n0 = args.warmup + args.steps + 1
+        one = (lambda n: h.cycle(pol, n)) if mode == "slabs" else (h.td_bpx if pol.bpx else h.td_add)
+        if mode != "slabs":
+            one = (lambda f: (lambda n: f(pol, n)))(one)
+        # (a) a solve through the public API: the step's input (the rhs) uploaded
+        #     from pinned host memory once, then K cycles, each returning its norms
+        barrier()
+        t0 = time.perf_counter()
+        if mode == "slabs":
+            _, h2d = h.e2e_step(pol, n0, chi_host)
+        else:
+            h.e2e_step(pol, n0, chi_host)
+        for i in range(1, args.steps):
+            one(n0 + i)
+        solve_s = D.reduce_max(ctx, time.perf_counter() - t0)
+        # (b) the pessimistic variant: a fresh rhs uploaded before every cycle
+        reps = max(2, min(args.steps, 5))
+        barrier()
+        t0 = time.perf_counter()
+        for i in range(reps):
+            h.e2e_step(pol, n0 + args.steps + i, chi_host)
+        every_s = D.reduce_max(ctx, (time.perf_counter() - t0) / reps)
+        e2e = {"value": copies * dof * args.steps / solve_s, "unit": "DoF-updates/s",
+               "h2d_bytes_per_step": int(h2d) // max(1, args.steps), "d2h_bytes_per_step": 24,
+               "note": f"public-API solve of K={args.steps} cycles (wall clock, max over ranks): H2D of the nodal rhs "
+                       "(16 B/vertex from pinned memory; slabs: the rank's planes) and the device load vector once, "
+                       "then every cycle with D2H of its three residual norms",
+               "rhs_every_cycle": {"value": copies * dof / every_s, "h2d_bytes_per_step": int(h2d),
+                                   "note": "a fresh rhs uploaded before each cycle (PCIe-bound)"}}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -653,7 +663,7 @@ def main():
             "metric": "complex DoF-updates/s per additive MG cycle", "value": value, "unit": "DoF-updates/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong" if mode == "slabs" else "weak", "vs_baseline": None,
-            "dtype": "complex128 (f64)",
+            "dtype": "complex64 (f32)" if args.precision == "fast-complex64" else "complex128 (f64)",
             "data": "synthetic (seeded uniform complex rhs, SURVEY §8d)",
             "config": workload_config(args.workload, w), "precision": args.precision,
             "parallelism": {"slabs": f"z-slabs x{world} (NCCL)", "replicas": f"replicas x{world}",

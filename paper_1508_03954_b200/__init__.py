@@ -31,6 +31,7 @@ STATUS = {0: "TREEMG_OK", 1: "TREEMG_E_USAGE", 2: "TREEMG_E_CAPACITY", 3: "TREEM
 OUTCOME = {0: "converged", 1: "budget-exhausted", 2: "diverged"}
 OMEGA_KINDS = {"jacobi-only": 0, "undamped": 1, "lgrid": 2, "exponential": 3, "transition": 4}
 CHI_KINDS = {"zero": 0, "sin": 1, "ball": 2, "seeded": 3, "gaussian": 4}
+PRECISIONS = {"exact": 0, "fast": 1, "fast-complex64": 2}
 
 # The 14 entry points of proj/include/treemg.h and the extensions of
 # include/treemg_b200.h, all exported by libtreemg_b200.so.
@@ -306,7 +307,7 @@ class Hierarchy:
         self.L = lib()
         prob = _Problem(dim, levels, ell_min, np.deg2rad(theta_deg) if theta_deg else 0.0,
                         complex(phi).real, complex(phi).imag, CHI_KINDS[chi], rhs_seed, int(rhs_sphere),
-                        1 if precision == "fast" else 0, max_vertices, device, sphere_levels, channels,
+                        PRECISIONS[precision], max_vertices, device, sphere_levels, channels,
                         complex(coupling).real, complex(coupling).imag, h_max, h_min)
         if theta_deg:
             prob.theta = theta_deg * np.pi / 180.0  # ProblemSpec::thetaGlobal = deg * M_PI / 180.0

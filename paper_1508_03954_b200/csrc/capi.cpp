@@ -223,7 +223,8 @@ Problem problem_from(const tmg_problem* prob) {
     p.gaussian = prob->chi_kind == 4;
     p.rhsSeed = prob->rhs_seed;
     p.rhsSphere = prob->rhs_sphere != 0;
-    p.fast = prob->precision == 1;
+    p.fast = prob->precision == 1 || prob->precision == 2;
+    p.c64 = prob->precision == 2;
     if (prob->max_vertices > 0) p.maxVertices = static_cast<std::size_t>(prob->max_vertices);
     p.device = prob->device;
     p.sphereLevels = prob->sphere_levels;

@@ -14,48 +14,45 @@ namespace fused3 {
 
 namespace {
 
-__device__ __forceinline__ double2 zero2() { return make_double2(0.0, 0.0); }
-__device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 mul(double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 mac(double2 acc, double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
-}
-__device__ __forceinline__ double2 axpy(double w, double2 v, double2 acc) {
-    return make_double2(fma(w, v.x, acc.x), fma(w, v.y, acc.y));
-}
-__device__ __forceinline__ double2 ld(const double2* p) { return __ldg(p); }
+// ---- complex arithmetic on double2 (complex128) and float2 (complex64) ----
+template <class S> struct Cx;
+template <> struct Cx<double> { using T = double2; };
+template <> struct Cx<float> { using T = float2; };
 
-__device__ __forceinline__ double2 lerp(double2 c0, double2 c1, int rel) {
-    if (rel == 0) return c0;
-    if (rel == 3) return c1;
-    const double w1 = rel == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
-    return make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
+__device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ float2 mk(float x, float y) { return make_float2(x, y); }
+template <class C> __device__ __forceinline__ C zero();
+template <> __device__ __forceinline__ double2 zero<double2>() { return make_double2(0.0, 0.0); }
+template <> __device__ __forceinline__ float2 zero<float2>() { return make_float2(0.f, 0.f); }
+__device__ __forceinline__ double2 zero2() { return zero<double2>(); }
+template <class C> __device__ __forceinline__ C add(C a, C b) { return mk(a.x + b.x, a.y + b.y); }
+template <class C> __device__ __forceinline__ C sub(C a, C b) { return mk(a.x - b.x, a.y - b.y); }
+template <class C> __device__ __forceinline__ C mul(C a, C b) {
+    return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
-
-// trilinear prolongation from the coarse lattice (transfer.cpp:20-40 order)
-__device__ __forceinline__ double2 prolong3(const double2* __restrict__ src, unsigned n1c, int mc, int x, int y,
-                                            int z) {
-    const int qx = min(x / 3, mc - 1), qy = min(y / 3, mc - 1), qz = min(z / 3, mc - 1);
-    const int rx = x - 3 * qx, ry = y - 3 * qy, rz = z - 3 * qz;
-    const double2* p = src + qx + static_cast<long long>(n1c) * (qy + static_cast<long long>(n1c) * qz);
-    const long long sy = n1c, sz = static_cast<long long>(n1c) * n1c;
-    const double2 a = lerp(ld(p), ld(p + 1), rx);
-    const double2 b = lerp(ld(p + sy), ld(p + sy + 1), rx);
-    const double2 c = lerp(ld(p + sz), ld(p + sz + 1), rx);
-    const double2 d = lerp(ld(p + sz + sy), ld(p + sz + sy + 1), rx);
-    return lerp(lerp(a, b, ry), lerp(c, d, ry), rz);
+template <class C> __device__ __forceinline__ C mac(C acc, C a, C b) {
+    return mk(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
 }
-
-__device__ __forceinline__ double2 lerpw(double2 c0, double2 c1, double w1) {
-    return make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
+template <class C, class S> __device__ __forceinline__ C axpy(S w, C v, C acc) {
+    return mk(fma(w, v.x, acc.x), fma(w, v.y, acc.y));
+}
+template <class C, class S> __device__ __forceinline__ C lerpw(C c0, C c1, S w1) {
+    return mk(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
+}
+template <class C> __device__ __forceinline__ C ld(const C* p) { return __ldg(p); }
+// complex128 <-> the kernel's complex type
+__device__ __forceinline__ double2 to_c(double2 v, double2) { return v; }
+__device__ __forceinline__ float2 to_c(double2 v, float2) { return make_float2(static_cast<float>(v.x), static_cast<float>(v.y)); }
+__device__ __forceinline__ double2 to_d(double2 v) { return v; }
+__device__ __forceinline__ double2 to_d(float2 v) { return make_double2(v.x, v.y); }
+template <class S> __device__ __forceinline__ S third(int num) {  // num / 3 in the kernel's precision
+    return static_cast<S>(num == 1 ? (1.0 / 3.0) : num == 2 ? (2.0 / 3.0) : num == 3 ? 1.0 : 0.0);
 }
 
-__device__ __forceinline__ double2 stage_sc(double2 smooth, double2 w, bool cp, int bpx, int hb) {
-    if (bpx) return cp ? zero2() : mul(w, smooth);
-    if ((hb && cp) || (w.x == 0.0 && w.y == 0.0)) return zero2();
+template <class C>
+__device__ __forceinline__ C stage_sc(C smooth, C w, bool cp, int bpx, int hb) {
+    if (bpx) return cp ? zero<C>() : mul(w, smooth);
+    if ((hb && cp) || (w.x == 0 && w.y == 0)) return zero<C>();
     return mul(w, smooth);
 }
 
@@ -92,31 +89,43 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
         : "memory");
 }
 
-constexpr int kPlane = (HX * HY + 7) / 8 * 8;  // stage strides: TMA destinations are 128-byte aligned
-constexpr unsigned kTileBytes = HX * HY * sizeof(double2);
-constexpr int kC = (CX * CY * 2 + 7) / 8 * 8;     // two coarse planes (box {2*CX, CY, 2})
-constexpr unsigned kCBytes = CX * CY * 2 * sizeof(double2);
-constexpr int kV = (HY * CX + 7) / 8 * 8;         // z- and y-interpolated coarse rows
+// Shared-memory carve-up (bytes; every TMA destination 128-byte aligned).
+// C = the kernel's complex type (16 B complex128 or 8 B complex64).
+template <class C>
+struct Smem {
+    static constexpr int kPlane = (HX * HY * static_cast<int>(sizeof(C)) + 127) / 128 * 128;  // halo'd fine tile
+    static constexpr unsigned kTileBytes = HX * HY * sizeof(C);
+    static constexpr int kC = (CX * CY * 2 * 16 + 127) / 128 * 128;  // two complex128 coarse planes
+    static constexpr unsigned kCBytes = CX * CY * 2 * sizeof(double2);
+    static constexpr int kV = (HY * CX + 7) / 8 * 8;  // z- and y-interpolated coarse rows (elements of C)
+    static constexpr int kP = (HX * HY + 7) / 8 * 8;  // corrected plane (elements of C)
+    template <bool BPX>
+    __host__ __device__ static constexpr int stage() { return kPlane + (BPX ? 2 : 1) * kC; }
+    template <bool BPX>
+    __host__ __device__ static constexpr size_t bytes() {
+        return STAGES * stage<BPX>() + ((BPX ? 4 : 2) * kV + 2 * kP + TX * TY + TY * SX) * sizeof(C) +
+               STAGES * sizeof(uint64_t);
+    }
+};
 constexpr int NT = TX * TY;
 
-// Stage = the halo'd tile of the fine state v (= u + sc, see fused3.cuh) and
-// the two coarse sc (si) planes it prolongs from.
-template <bool BPX>
-__host__ __device__ constexpr int stage_elems() { return kPlane + (BPX ? 2 : 1) * kC; }
-
-template <bool BPX>
+template <bool BPX, class S>
 __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     k_fused3(const __grid_constant__ CUtensorMap mapU,
              const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
+    using C = typename Cx<S>::T;
+    using M = Smem<C>;
     dev::griddep_wait();
     extern __shared__ __align__(128) unsigned char smem[];
-    constexpr int SE = stage_elems<BPX>();
-    double2* ring = reinterpret_cast<double2*>(smem);          // STAGES x {U, S, C[, I]}
-    double2* Vb = ring + STAGES * SE;                           // [2][kV] (+[2][kV] si)
-    double2* Pb = Vb + (BPX ? 4 : 2) * kV;                      // [2][kPlane] corrected planes
-    double2* tb = Pb + 2 * kPlane;                              // [TY][TX] z-restricted columns
-    double2* rb = tb + NT;                                      // [TY][SX] x-restricted rows
+    constexpr int SB = M::template stage<BPX>();                 // stage stride, bytes
+    unsigned char* ring = smem;                                  // STAGES x {v tile, coarse sc[, si]}
+    C* Vb = reinterpret_cast<C*>(smem + STAGES * SB);            // [2][kV] (+[2][kV] si)
+    C* Pb = Vb + (BPX ? 4 : 2) * M::kV;                          // [2][kP] corrected planes
+    C* tb = Pb + 2 * M::kP;                                      // [TY][TX] z-restricted columns
+    C* rb = tb + NT;                                             // [TY][SX] x-restricted rows
     uint64_t* bar = reinterpret_cast<uint64_t*>(rb + TY * SX);
+    auto tile = [&](int st) { return reinterpret_cast<const C*>(ring + st * SB); };
+    auto coarse = [&](int st) { return reinterpret_cast<const double2*>(ring + st * SB + M::kPlane); };
 
     const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
     const int m = a.g.m, mc = a.g.mc;
@@ -126,15 +135,16 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     const int nplanes = z1 - z0 + 2;
     const long long sy = a.n1, sz = static_cast<long long>(a.n1) * a.n1;
     const int cx0 = (x0 - 1) / 3, cy0 = (y0 - 1) / 3;
-    constexpr unsigned stageBytes = kTileBytes + (BPX ? 2 : 1) * kCBytes;
+    constexpr unsigned stageBytes = M::kTileBytes + (BPX ? 2 : 1) * M::kCBytes;
+    constexpr int xScale = sizeof(C) / sizeof(S);  // tensor-map x coordinates count scalars
 
     auto issue = [&](int stage, int zz) {
-        double2* st = ring + stage * SE;
+        unsigned char* st = ring + stage * SB;
         const int cz = min(zz / 3, mc - 1);
         mbar_expect_tx(&bar[stage], stageBytes);
-        tma_load3(st, &mapU, 2 * (x0 - 1), y0 - 1, zz, &bar[stage]);
-        tma_load3(st + kPlane, &mapC, 2 * cx0, cy0, cz, &bar[stage]);
-        if (BPX) tma_load3(st + kPlane + kC, &mapI, 2 * cx0, cy0, cz, &bar[stage]);
+        tma_load3(st, &mapU, xScale * (x0 - 1), y0 - 1, zz, &bar[stage]);
+        tma_load3(st + M::kPlane, &mapC, 2 * cx0, cy0, cz, &bar[stage]);
+        if (BPX) tma_load3(st + M::kPlane + M::kC, &mapI, 2 * cx0, cy0, cz, &bar[stage]);
     };
 
     if (tid == 0) {
@@ -155,16 +165,15 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     const bool cpxy = (x % 3 == 0) && (y % 3 == 0);
     const int po = (ty + 1) * HX + (tx + 1);
     int vo;
-    double wxo;
+    S wxo;
     {
         const int qx = min(x / 3, mc - 1);
         vo = (ty + 1) * CX + (qx - cx0);
-        const int rx = x - 3 * qx;
-        wxo = rx == 1 ? (1.0 / 3.0) : rx == 2 ? (2.0 / 3.0) : (rx == 3 ? 1.0 : 0.0);
+        wxo = third<S>(x - 3 * qx);
     }
     const int task = tid < RING ? 1 : (tid < RING + HY * CX ? 2 : 0);  // warp-uniform except one warp
     int pr = 0, vr = 0;
-    double wxr = 0.0;
+    S wxr = 0;
     bool pinr = false, cpr = false;
     int vcOff = 0;
     double w1y = 0.0;
@@ -179,36 +188,35 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
         const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
         pinr = gx >= 1 && gx <= m - 1 && gy >= 1 && gy <= m - 1;
         const int qx = min(max(gx, 0) / 3, mc - 1);
-        const int rx = gx - 3 * qx;
         pr = ly * HX + lx;
         vr = ly * CX + (qx - cx0);
-        wxr = rx == 1 ? (1.0 / 3.0) : rx == 2 ? (2.0 / 3.0) : (rx == 3 ? 1.0 : 0.0);
+        wxr = third<S>(gx - 3 * qx);
         cpr = (gx % 3 == 0) && (gy % 3 == 0);
     } else if (task == 2) {
         const int ly = vt / CX, ci = vt % CX;
         const int gy = y0 - 1 + ly;
         const int qy = min(max(gy, 0) / 3, mc - 1);
-        const int ry = gy - 3 * qy;
         vcOff = (qy - cy0) * CX + ci;
-        w1y = ry == 1 ? (1.0 / 3.0) : ry == 2 ? (2.0 / 3.0) : (ry == 3 ? 1.0 : 0.0);
+        w1y = third<double>(gy - 3 * qy);
     }
+    // the coarse (complex128) correction interpolated in y and z, stored in the kernel's precision
     auto computeV = [&](int stage, int zz, int vb) {
         const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
-        const double w1z = rz == 1 ? (1.0 / 3.0) : rz == 2 ? (2.0 / 3.0) : (rz == 3 ? 1.0 : 0.0);
-        const double2* C = ring + stage * SE + kPlane;
-        const double2 a0 = lerpw(C[vcOff], C[vcOff + CX], w1y);
-        const double2 a1 = lerpw(C[vcOff + CX * CY], C[vcOff + CX * CY + CX], w1y);
-        Vb[vb * kV + vt] = lerpw(a0, a1, w1z);
+        const double w1z = third<double>(rz);
+        const double2* Cc = coarse(stage);
+        const double2 a0 = lerpw(Cc[vcOff], Cc[vcOff + CX], w1y);
+        const double2 a1 = lerpw(Cc[vcOff + CX * CY], Cc[vcOff + CX * CY + CX], w1y);
+        Vb[vb * M::kV + vt] = to_c(lerpw(a0, a1, w1z), C{});
         if (BPX) {
-            const double2* I = C + kC;
+            const double2* I = Cc + M::kC / 16;
             const double2 b0 = lerpw(I[vcOff], I[vcOff + CX], w1y);
             const double2 b1 = lerpw(I[vcOff + CX * CY], I[vcOff + CX * CY + CX], w1y);
-            Vb[(2 + vb) * kV + vt] = lerpw(b0, b1, w1z);
+            Vb[(2 + vb) * M::kV + vt] = to_c(lerpw(b0, b1, w1z), C{});
         }
     };
 
     double nmax = 0.0, nsum = 0.0;
-    double2 accLo = zero2(), accHi = zero2();
+    C accLo = zero<C>(), accHi = zero<C>();
 
     // restriction slots of this tile (xy); z handled by the column accumulators
     const int Xa = x0 / 3, Xb = (xe + 1) / 3, Ya = y0 / 3, Yb = (ye + 1) / 3;
@@ -222,27 +230,26 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     int zLow = zBase;
     const bool slotThread = tid < nsx * nsy;
     const int sxi = slotThread ? tid % nsx : 0, syi = slotThread ? tid / nsx : 0;
+    auto wk = [](int k) { return static_cast<S>(k == 0 ? 1.0 : (k == 1 || k == -1) ? (2.0 / 3.0) : (1.0 / 3.0)); };
     auto flushSlots = [&](int zi) {
         __syncthreads();
         if (slotThread) {
             const int X = Xa + sxi, Y = Ya + syi;
-            double2 acc = zero2();
+            C acc = zero<C>();
 #pragma unroll
             for (int ky = -2; ky <= 2; ++ky) {
                 const int fy = 3 * Y + ky;
                 if (fy < y0 || fy >= ye) continue;
-                const double wy = ky == 0 ? 1.0 : (ky == 1 || ky == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
-                double2 row = zero2();
+                C row = zero<C>();
 #pragma unroll
                 for (int kx = -2; kx <= 2; ++kx) {
                     const int fx = 3 * X + kx;
                     if (fx < x0 || fx >= xe) continue;
-                    const double wx = kx == 0 ? 1.0 : (kx == 1 || kx == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
-                    row = axpy(wx, tb[(fy - y0) * TX + (fx - x0)], row);
+                    row = axpy(wk(kx), tb[(fy - y0) * TX + (fx - x0)], row);
                 }
-                acc = axpy(wy, row, acc);
+                acc = axpy(wk(ky), row, acc);
             }
-            part[zi * zStride + syi * SX + sxi] = acc;
+            part[zi * zStride + syi * SX + sxi] = to_d(acc);
         }
     };
 
@@ -252,18 +259,18 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     // arithmetic as flushSlots.  Task i runs on thread NT-1-i, away from the
     // threads that carry phase-B halo / coarse-row work.
     const int ti = NT - 1 - tid;
+    const int s1y = nsx > 0 ? ti / nsx : 0, s1x = ti - s1y * nsx;  // stage-1 task (row, slot) / stage-2 (sy, sx)
     auto stage1 = [&]() {
         if (ti < TY * nsx) {
-            const int fyl = ti / nsx, sx = ti % nsx;
+            const int fyl = s1y, sx = s1x;
             if (y0 + fyl < ye) {
                 const int X = Xa + sx;
-                double2 row = zero2();
+                C row = zero<C>();
 #pragma unroll
                 for (int kx = -2; kx <= 2; ++kx) {
                     const int fx = 3 * X + kx;
                     if (fx < x0 || fx >= xe) continue;
-                    const double wx = kx == 0 ? 1.0 : (kx == 1 || kx == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
-                    row = axpy(wx, tb[fyl * TX + (fx - x0)], row);
+                    row = axpy(wk(kx), tb[fyl * TX + (fx - x0)], row);
                 }
                 rb[fyl * SX + sx] = row;
             }
@@ -271,38 +278,38 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
     };
     auto stage2 = [&](int zi) {
         if (ti < nsx * nsy) {
-            const int sx = ti % nsx, syy = ti / nsx;
+            const int sx = s1x, syy = s1y;
             const int Y = Ya + syy;
-            double2 acc = zero2();
+            C acc = zero<C>();
 #pragma unroll
             for (int ky = -2; ky <= 2; ++ky) {
                 const int fy = 3 * Y + ky;
                 if (fy < y0 || fy >= ye) continue;
-                const double wy = ky == 0 ? 1.0 : (ky == 1 || ky == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
-                acc = axpy(wy, rb[(fy - y0) * SX + sx], acc);
+                acc = axpy(wk(ky), rb[(fy - y0) * SX + sx], acc);
             }
-            part[zi * zStride + syy * SX + sx] = acc;
+            part[zi * zStride + syy * SX + sx] = to_d(acc);
         }
     };
     bool pend1 = false, pend2 = false;
     int zi1 = 0, zi2 = 0;
 
     const long long colBase = x + y * sy;
-    const double2* bPtr = a.b + colBase + static_cast<long long>(z0) * sz;
-    double2* uPtr = a.uNew + colBase + static_cast<long long>(z0) * sz;
-    double2* sPtr = a.scNew + colBase + static_cast<long long>(z0) * sz;
+    const C* bPtr = static_cast<const C*>(a.b) + colBase + static_cast<long long>(z0) * sz;
+    C* uPtr = static_cast<C*>(a.uNew) + colBase + static_cast<long long>(z0) * sz;
+    C* sPtr = static_cast<C*>(a.scNew) + colBase + static_cast<long long>(z0) * sz;
     double2* siPtr = a.sinextC + (x / 3) + a.n1c * (static_cast<long long>(y / 3) + static_cast<long long>(a.n1c) * ((z0 + 2) / 3));
-    double2 bq0 = (owned && z0 < z1) ? ld(bPtr) : zero2();
+    C bq0 = (owned && z0 < z1) ? ld(bPtr) : zero<C>();
     const bool zeroSc = a.level < a.ellMin;
     const bool injectOK = BPX && a.level > a.ellMin && cpxy && owned;
-    const double2 k0 = a.k.c[0], k1 = a.k.c[1], k2 = a.k.c[2], k3 = a.k.c[3];
+    const C k0 = to_c(a.k.c[0], C{}), k1 = to_c(a.k.c[1], C{}), k2 = to_c(a.k.c[2], C{}), k3 = to_c(a.k.c[3], C{});
+    const C invDiag = to_c(a.k.invDiag, C{}), wRaw = to_c(a.k.wRaw, C{});
 
     mbar_wait(&bar[0], 0);
     if (task == 2) computeV(0, z0 - 1, 0);
     __syncthreads();
 
     // running stencil accumulators: Aprev = H u at plane p-1 minus its plane-p terms, Acur = plane p's so far
-    double2 Aprev = zero2(), Acur = zero2();
+    C Aprev = zero<C>(), Acur = zero<C>();
     int stage = 0;
     unsigned parity = 0;
 
@@ -315,27 +322,27 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
         mbar_wait(&bar[stage], parity);
         if (hasNext) mbar_wait(&bar[nstage], nparity);
         const bool zin = zz >= 1 && zz <= m - 1;
-        const double2* Ut = ring + stage * SE;  // fine state v = u + sc of plane zz
-        const double2* V = Vb + (it & 1) * kV;
-        double2* P = Pb + (it & 1) * kPlane;
+        const C* Ut = tile(stage);  // fine state v = u + sc of plane zz
+        const C* V = Vb + (it & 1) * M::kV;
+        C* P = Pb + (it & 1) * M::kP;
         // ---- phase B ----
-        double2 cOwn;
+        C cOwn;
         {
-            double2 scv = lerpw(V[vo], V[vo + 1], wxo);
+            C scv = lerpw(V[vo], V[vo + 1], wxo);
             if (BPX && !(cpxy && u == 0)) {
-                const double2* Vi = Vb + (2 + (it & 1)) * kV;
+                const C* Vi = Vb + (2 + (it & 1)) * M::kV;
                 scv = sub(scv, lerpw(Vi[vo], Vi[vo + 1], wxo));
             }
-            cOwn = (zin && owned) ? add(Ut[po], scv) : zero2();
+            cOwn = (zin && owned) ? add(Ut[po], scv) : zero<C>();
             P[po] = cOwn;
         }
         if (task == 1) {
-            double2 scv = lerpw(V[vr], V[vr + 1], wxr);
+            C scv = lerpw(V[vr], V[vr + 1], wxr);
             if (BPX && !(cpr && u == 0)) {
-                const double2* Vi = Vb + (2 + (it & 1)) * kV;
+                const C* Vi = Vb + (2 + (it & 1)) * M::kV;
                 scv = sub(scv, lerpw(Vi[vr], Vi[vr + 1], wxr));
             }
-            P[pr] = (zin && pinr) ? add(Ut[pr], scv) : zero2();
+            P[pr] = (zin && pinr) ? add(Ut[pr], scv) : zero<C>();
         } else if (task == 2 && hasNext) {
             computeV(nstage, zz + 1, (it + 1) & 1);
         }
@@ -353,49 +360,51 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
             stage2(zi2);
             pend2 = false;
         }
-        const double2* c = P + po;
-        const double2 E = add(add(c[-1], c[1]), add(c[-HX], c[HX]));
-        const double2 K = add(add(c[-1 - HX], c[1 - HX]), add(c[-1 + HX], c[1 + HX]));
-        double2 T = mul(k1, cOwn);
+        const C* c = P + po;
+        const C E = add(add(c[-1], c[1]), add(c[-HX], c[HX]));
+        const C K = add(add(c[-1 - HX], c[1 - HX]), add(c[-1 + HX], c[1 + HX]));
+        C T = mul(k1, cOwn);
         T = mac(T, k2, E);
         T = mac(T, k3, K);
-        double2 Uo = mul(k0, cOwn);
+        C Uo = mul(k0, cOwn);
         Uo = mac(Uo, k1, E);
         Uo = mac(Uo, k2, K);
         if (it >= 2) {
             constexpr int kz = (u + 2) % 3;  // plane z = zz - 1
-            const double2 hu = add(Aprev, T);
-            const double2 r = owned ? sub(bq0, hu) : zero2();
+            const C hu = add(Aprev, T);
+            const C r = owned ? sub(bq0, hu) : zero<C>();
             bPtr += sz;
             if (owned && zz < z1) bq0 = ld(bPtr);
-            const double m2 = fma(r.x, r.x, r.y * r.y);
-            nmax = fmax(nmax, m2);
-            nsum += m2;
-            const double2 smooth = mul(r, a.k.invDiag);
-            const double2 scn = zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpxy && kz == 0, BPX ? 1 : 0, a.hb);
+            const S m2 = fma(r.x, r.x, r.y * r.y);
+            nmax = fmax(nmax, static_cast<double>(m2));
+            nsum += static_cast<double>(m2);
+            const C smooth = mul(r, invDiag);
+            const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpxy && kz == 0, BPX ? 1 : 0, a.hb);
             if (owned) {
+#ifndef TMG_NO_SC_STORE  // timing experiment only: the fine sc is not written
                 *sPtr = scn;
+#endif
                 // next cycle's state v = u + sc of plane zz - 1 (its corrected u is
                 // still in the other P buffer: rewritten only in the next phase B)
-                *uPtr = add(Pb[((it + 1) & 1) * kPlane + po], scn);
+                *uPtr = add(Pb[((it + 1) & 1) * M::kP + po], scn);
             }
             sPtr += sz;
             uPtr += sz;
             if (BPX && kz == 0 && injectOK) {
-                *siPtr = mul(a.k.wRaw, smooth);
+                *siPtr = to_d(mul(wRaw, smooth));
                 siPtr += static_cast<long long>(a.n1c) * a.n1c;
             }
             if (kz == 0) {
                 accLo = add(accLo, r);
             } else if (kz == 1) {
-                accLo = axpy(2.0 / 3.0, r, accLo);
-                accHi = axpy(1.0 / 3.0, r, accHi);
+                accLo = axpy(static_cast<S>(2.0 / 3.0), r, accLo);
+                accHi = axpy(static_cast<S>(1.0 / 3.0), r, accHi);
             } else {
-                accLo = axpy(1.0 / 3.0, r, accLo);
-                accHi = axpy(2.0 / 3.0, r, accHi);
+                accLo = axpy(static_cast<S>(1.0 / 3.0), r, accLo);
+                accHi = axpy(static_cast<S>(2.0 / 3.0), r, accHi);
                 tb[ty * TX + tx] = accLo;
                 accLo = accHi;
-                accHi = zero2();
+                accHi = zero<C>();
                 pend1 = true;
                 zi1 = zLow - zBase;
                 ++zLow;
@@ -519,13 +528,12 @@ size_t partial_count(const Geometry& g) {
 
 int blocks(const Geometry& g) { return g.nbx * g.nby * g.nbz; }
 
-size_t smem_bytes(bool bpx) {
-    const int se = bpx ? stage_elems<true>() : stage_elems<false>();
-    return (STAGES * se + (bpx ? 4 : 2) * kV + 2 * kPlane + NT + TY * SX) * sizeof(double2) +
-           STAGES * sizeof(uint64_t);
+size_t smem_bytes(bool bpx, bool c64) {
+    if (c64) return bpx ? Smem<float2>::bytes<true>() : Smem<float2>::bytes<false>();
+    return bpx ? Smem<double2>::bytes<true>() : Smem<double2>::bytes<false>();
 }
 
-bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind) {
+bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64) {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -535,40 +543,52 @@ bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind) {
             return false;
         fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(ptr);
     }
+    const bool f32 = c64 && kind != 2;  // coarse planes stay complex128
+    const cuuint64_t es = f32 ? 4 : 8;
     const cuuint64_t dims[3] = {2ull * n1, n1, n1};
-    const cuuint64_t strides[2] = {16ull * n1, 16ull * n1 * n1};
+    const cuuint64_t strides[2] = {2 * es * n1, 2 * es * n1 * n1};
     const cuuint32_t box[3] = {kind == 0 ? 2u * HX : kind == 1 ? 2u * TX : 2u * CX,
                                static_cast<cuuint32_t>(kind == 0 ? HY : kind == 1 ? TY : CY), kind == 2 ? 2u : 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
-    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double2*>(base), dims, strides, box,
-                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                          const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
 }
 
 int resident_blocks(int smCount) {
-    // blocks per SM of the non-BPX kernel at its dynamic shared memory size
+    // blocks per SM of the non-BPX complex128 kernel at its dynamic shared memory size
     const size_t smem = smem_bytes(false);
-    cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaFuncSetAttribute(k_fused3<false, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused3<false>, TX * TY, smem) != cudaSuccess || per < 1)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused3<false, double>, TX * TY, smem) != cudaSuccess ||
+        per < 1)
         per = 3;
     return per * smCount;
 }
 
-void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
-            const CUtensorMap& mapI, cudaStream_t s, int nchunks) {
+namespace {
+template <bool BPX, class S>
+void launch_one(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC, const CUtensorMap& mapI,
+                cudaStream_t s, dim3 grid) {
     // the shared-memory limit is a per-device function attribute: set it on every
     // launch (a host-side call, no device work) so a second device is configured too
-    const bool bpx = a.bpx != 0;
-    const size_t smem = smem_bytes(bpx);
-    dim3 grid(a.g.nbx, a.g.nby, nchunks > 0 ? nchunks : a.g.nbz);
-    if (bpx) {
-        cudaFuncSetAttribute(k_fused3<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        dev::launch_k(k_fused3<true>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
+    const size_t smem = smem_bytes(BPX, sizeof(S) == 4);
+    cudaFuncSetAttribute(k_fused3<BPX, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dev::launch_k(k_fused3<BPX, S>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
+}
+}  // namespace
+
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
+            const CUtensorMap& mapI, cudaStream_t s, int nchunks) {
+    const dim3 grid(a.g.nbx, a.g.nby, nchunks > 0 ? nchunks : a.g.nbz);
+    if (a.c64) {
+        if (a.bpx) launch_one<true, float>(a, mapU, mapC, mapI, s, grid);
+        else launch_one<false, float>(a, mapU, mapC, mapI, s, grid);
     } else {
-        cudaFuncSetAttribute(k_fused3<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        dev::launch_k(k_fused3<false>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
+        if (a.bpx) launch_one<true, double>(a, mapU, mapC, mapI, s, grid);
+        else launch_one<false, double>(a, mapU, mapC, mapI, s, grid);
     }
 }
 

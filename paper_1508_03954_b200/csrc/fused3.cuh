@@ -54,10 +54,12 @@ struct Geometry {
     int sz;     // z slots per chunk
 };
 
+// Fine-level arrays are double2 (complex128) or float2 (precision =
+// fast-complex64, the kernel instantiated with S = float): untyped here.
 struct Args {
-    double2* uNew;
-    double2* scNew;
-    const double2* b;
+    void* uNew;
+    void* scNew;
+    const void* b;
     const double2* scC;   // coarse sc (after the coarse top-down)
     const double2* siC;   // coarse si (BPX)
     double2* sinextC;     // coarse si next (BPX injection)
@@ -68,6 +70,7 @@ struct Args {
     fast::LevelCoef k;
     int bpx, hb, ellMin, level;
     int chunkBase;        // first global z-chunk of this launch
+    int c64;              // fine level in complex64 (float2) storage and arithmetic
 };
 
 // Tile / z-chunk geometry; the chunk count is a multiple of `parts` (z-slabs:
@@ -75,12 +78,13 @@ struct Args {
 Geometry geometry(int m, int mc, int parts = 1, int resident = 3 * 148);
 int resident_blocks(int smCount);  // co-resident k_fused3 blocks on the device
 size_t partial_count(const Geometry& g);
-size_t smem_bytes(bool bpx);
+size_t smem_bytes(bool bpx, bool c64 = false);
 int blocks(const Geometry& g);
 
-// TMA descriptor for one lattice array (double2 viewed as float64 pairs).
+// TMA descriptor for one lattice array (double2 viewed as float64 pairs, or
+// float2 as float32 pairs when c64).
 // kind 0: fine u / sc halo'd tile, 1: fine b tile, 2: two coarse planes.
-bool encode_map(CUtensorMap* map, const double2* base, unsigned n1, int kind);
+bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64 = false);
 
 // nchunks <= 0: all z-chunks (chunkBase must be 0)
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,

@@ -573,6 +573,22 @@ __global__ void k_inject_u(Lvl c, Lvl fine, int fineVForm) {
     }
 }
 
+// complex64 fine level (precision = fast-complex64): conversions to / from complex128
+__global__ void k_f2d(const float2* __restrict__ in, double2* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = make_double2(in[i].x, in[i].y);
+}
+__global__ void k_d2f(const double2* __restrict__ in, float2* __restrict__ out, size_t n) {
+    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = make_float2(static_cast<float>(in[i].x), static_cast<float>(in[i].y));
+}
+// u = v - sc of a complex64 v-form fine level, as complex128
+__global__ void k_vform_f2d(const float2* __restrict__ v, const float2* __restrict__ sc, double2* __restrict__ out,
+                            size_t n) {
+    for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        out[i] = make_double2(static_cast<double>(v[i].x) - sc[i].x, static_cast<double>(v[i].y) - sc[i].y);
+}
+
 // v-form fine level (fused3.cuh): u = v - sc, in place
 __global__ void k_vform_to_u(double2* v, const double2* sc, size_t n) {
     for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -774,6 +790,21 @@ struct Hierarchy::Impl {
 #endif
     static constexpr unsigned kChainMaxN = TMG_CHAIN_MAXN;  // levels below this size join the chain
     int fusedResident = 3 * 148;
+    bool fineFused = false;  // the fine level runs a fused pass (decided before allocation)
+    // bytes per fine-level element: complex64 storage (precision = fast-complex64) or complex128
+    size_t fine_elem() const { return prob.c64 ? sizeof(float2) : sizeof(double2); }
+    // a transient complex128 array of the fine lattice (complex64 conversions)
+    struct Tmp {
+        double2* p = nullptr;
+        ~Tmp() {
+            if (p) cudaFree(p);
+        }
+    };
+    double2* tmp_fine(Tmp& t) {
+        TMG_CUDA(cudaMalloc(&t.p, static_cast<size_t>(lv[L].n) * sizeof(double2)));
+        TMG_CUDA(cudaMemsetAsync(t.p, 0, static_cast<size_t>(lv[L].n) * sizeof(double2), stream));
+        return t.p;
+    }
     int clusterSize = 0;  // CTAs of a chain cluster (0: grid chains only)
     static constexpr unsigned long long kClusterMaxPts = 1ull << 18;
     unsigned* chainBar = nullptr;
@@ -815,9 +846,16 @@ struct Hierarchy::Impl {
         for (int d = 0; d < p; ++d) n *= v.n1;
         if (n >= (1ull << 32)) throw CapacityError("level lattice exceeds 2^32 vertices");
         v.n = static_cast<unsigned>(n);
+        if (fine && prob.c64) {  // complex64 storage (float2) behind the double2 pointers: fused3 / conversions only
+            v.u = reinterpret_cast<double2*>(alloc<float2>(n));
+            v.sc = reinterpret_cast<double2*>(alloc<float2>(n));
+            v.chi = reinterpret_cast<double2*>(alloc<float2>(n));
+            return v;
+        }
         v.u = alloc<double2>(n);
         v.sc = alloc<double2>(n);
-        v.rhat = alloc<double2>(n);
+        // the fused fine passes keep the fine residual in registers: no fine r-hat
+        if (!(fine && fineFused)) v.rhat = alloc<double2>(n);
         if (!prob.fast) {  // exact: the full FAS state of cycles.cpp
             v.chi = alloc<double2>(n);
             v.uhat = alloc<double2>(n);
@@ -1030,6 +1068,16 @@ struct Hierarchy::Impl {
     // load vector on planes [za, zb) of the last axis (za < 0: everywhere)
     void load_vector_dispatch(int za = -1, int zb = -1, int ch = 0) {
         const dev::Lvl& F = lv[L];
+        if (prob.fast && prob.c64) {  // complex128 load vector, stored as complex64
+            Tmp t;
+            dev::Lvl Fd = F;
+            Fd.chi = tmp_fine(t);
+            fast::load_vector(p, Fd, chiNodal, kc[L].massScale, blocks_for(F.n), stream, za, zb);
+            dev::k_d2f<<<blocks_for(F.n), 256, 0, stream>>>(Fd.chi, reinterpret_cast<float2*>(F.chi), F.n);
+            TMG_CUDA(cudaGetLastError());
+            TMG_CUDA(cudaStreamSynchronize(stream));
+            return;
+        }
         if (prob.fast) {  // separable assembled mass stencil (rounding differs from the cell-by-cell sum)
             fast::load_vector(p, F, chiNodal, kc[L].massScale, blocks_for(F.n), stream, za, zb);
             TMG_CUDA(cudaGetLastError());
@@ -1209,6 +1257,7 @@ struct Hierarchy::Impl {
             fa.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
             fa.ellMin = prob.ellMin;
             fa.level = L;
+            fa.c64 = prob.c64 ? 1 : 0;
             fused3::launch(fa, mapU[0], mapC, mapI, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             const int lo = useChain ? top + 1 : 1;
@@ -1261,8 +1310,20 @@ struct Hierarchy::Impl {
 
     template <int P>
     void inject_coarse_u() {
-        for (int l = L - 1; l >= 1; --l)
+        Tmp t;
+        for (int l = L - 1; l >= 1; --l) {
+            if (l == L - 1 && prob.c64) {  // u = v - sc of the complex64 fine level, as complex128
+                dev::Lvl Fd = lv[L];
+                Fd.u = tmp_fine(t);
+                dev::k_vform_f2d<<<blocks_for(Fd.n), 256, 0, stream>>>(reinterpret_cast<const float2*>(lv[L].u),
+                                                                       reinterpret_cast<const float2*>(lv[L].sc),
+                                                                       Fd.u, Fd.n);
+                dev::k_inject_u<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], Fd, 0);
+                continue;
+            }
             dev::k_inject_u<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], lv[l + 1], l == L - 1 && vForm() ? 1 : 0);
+        }
+        TMG_CUDA(cudaStreamSynchronize(stream));
     }
 
     // the finest level holds v = u + sc (fused fast paths, fused3.cuh)
@@ -1540,6 +1601,17 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     }
     const char* dbg = std::getenv("TMG_DEBUG_R");
     I.debugR = (dbg && dbg[0] == '1') || (prob.hostNorms && !prob.fast);
+    {
+        const char* f3 = std::getenv("TMG_FUSED");
+        const char* f2 = std::getenv("TMG_FUSED2");
+        I.fineFused = prob.fast && ((I.p == 3 && I.L >= 2 && !(f3 && f3[0] == '0')) ||
+                                    (I.p == 2 && I.L >= 3 && !(f2 && f2[0] == '0')));
+    }
+    if (prob.c64) {
+        if (!prob.fast) throw ConfigError("complex64 storage is a fast-precision mode");
+        if (I.p != 3 || !I.fineFused || prob.channels > 1 || prob.gaussian)
+            throw UnsupportedConfigError("precision = fast-complex64 runs the 3D fused fine pass (dim = 3, one channel)");
+    }
     I.lv.resize(I.L + 1);
     for (int l = 0; l <= I.L; ++l) I.lv[l] = I.make_level(l, l == I.L);
     I.normBlocks = std::max(I.blocks_for(I.lv[I.L].n), fast::residual_fine_blocks(I.p, I.lv[I.L], I.smCount));
@@ -1596,13 +1668,14 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
         const char* fz = std::getenv("TMG_FUSED");
         if (prob.fast && I.p == 3 && I.L >= 2 && !(fz && fz[0] == '0')) {
             const dev::Lvl& F = I.lv[I.L];
-            I.uAlt = I.alloc<double2>(F.n);  // v double buffer; sc is write-only (v-form)
+            // v double buffer; sc is write-only (v-form)
+            I.uAlt = prob.c64 ? reinterpret_cast<double2*>(I.alloc<float2>(F.n)) : I.alloc<double2>(F.n);
             I.geo = fused3::geometry(static_cast<int>(F.m), static_cast<int>(I.lv[I.L - 1].m), prob.zParts,
                                      I.fusedResident);
             I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
             const dev::Lvl& C = I.lv[I.L - 1];
-            bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0) &&
-                      fused3::encode_map(&I.mapU[1], I.uAlt, F.n1, 0) &&
+            bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0, prob.c64) &&
+                      fused3::encode_map(&I.mapU[1], I.uAlt, F.n1, 0, prob.c64) &&
                       fused3::encode_map(&I.mapC, C.sc, C.n1, 2) && fused3::encode_map(&I.mapI, C.si, C.n1, 2);
             if (!ok) throw CudaError("cuTensorMapEncodeTiled failed for the fused fine pass");
             I.fused = true;
@@ -1817,6 +1890,21 @@ void Hierarchy::get_field(int level, const std::string& name, double* host) cons
         return;
     }
     if (field == "u" && level < I.L) I.materialize_coarse_u();
+    if (level == I.L && I.prob.c64 && (field == "u" || field == "sc" || field == "chi")) {  // complex64 storage
+        std::vector<float2> a(v.n), b;
+        TMG_CUDA(cudaMemcpyAsync(a.data(), field == "chi" ? v.chi : field == "sc" ? v.sc : v.u,
+                                 a.size() * sizeof(float2), cudaMemcpyDeviceToHost, I.stream));
+        if (field == "u") {  // u = v - sc
+            b.resize(v.n);
+            TMG_CUDA(cudaMemcpyAsync(b.data(), v.sc, b.size() * sizeof(float2), cudaMemcpyDeviceToHost, I.stream));
+        }
+        TMG_CUDA(cudaStreamSynchronize(I.stream));
+        for (size_t i = 0; i < a.size(); ++i) {
+            host[2 * i] = static_cast<double>(a[i].x) - (b.empty() ? 0.0 : static_cast<double>(b[i].x));
+            host[2 * i + 1] = static_cast<double>(a[i].y) - (b.empty() ? 0.0 : static_cast<double>(b[i].y));
+        }
+        return;
+    }
     if (field == "u" && level == I.L && I.vForm()) {  // u = v - sc
         std::vector<double2> sc(v.n);
         TMG_CUDA(cudaMemcpyAsync(host, v.u, static_cast<size_t>(v.n) * sizeof(double2), cudaMemcpyDeviceToHost, I.stream));
@@ -1830,7 +1918,8 @@ void Hierarchy::get_field(int level, const std::string& name, double* host) cons
     }
     double2* ptr = field_ptr(v, field);
     if (!ptr) {
-        if (field == "uhat" || field == "chi" || field == "sf" || field == "si" || field == "sinext" || field == "r") {
+        if (field == "uhat" || field == "chi" || field == "sf" || field == "si" || field == "sinext" || field == "r" ||
+            field == "rhat") {
             std::fill(host, host + 2 * static_cast<size_t>(v.n), 0.0);
             return;
         }
@@ -1856,20 +1945,48 @@ void Hierarchy::set_field(int level, const std::string& field, const double* hos
         const double* ns = field == "sc" ? host : sc.data();
         std::vector<double> vv(u.size());
         for (size_t i = 0; i < vv.size(); ++i) vv[i] = nu[i] + ns[i];
+        if (I.prob.c64) {  // complex64 storage
+            std::vector<float> fv(vv.size()), fs(vv.size());
+            for (size_t i = 0; i < vv.size(); ++i) {
+                fv[i] = static_cast<float>(vv[i]);
+                fs[i] = static_cast<float>(ns[i]);
+            }
+            TMG_CUDA(cudaMemcpyAsync(v.u, fv.data(), fv.size() * sizeof(float), cudaMemcpyHostToDevice, I.stream));
+            TMG_CUDA(cudaMemcpyAsync(v.sc, fs.data(), fs.size() * sizeof(float), cudaMemcpyHostToDevice, I.stream));
+            TMG_CUDA(cudaStreamSynchronize(I.stream));
+            return;
+        }
         TMG_CUDA(cudaMemcpyAsync(v.u, vv.data(), vv.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
         TMG_CUDA(cudaMemcpyAsync(v.sc, ns, vv.size() * sizeof(double), cudaMemcpyHostToDevice, I.stream));
         TMG_CUDA(cudaStreamSynchronize(I.stream));
         return;
     }
+    if (level == I.L && I.prob.c64) throw UnsupportedConfigError("set_field: complex64 fine level holds u / sc only");
     TMG_CUDA(cudaMemcpyAsync(ptr, host, static_cast<size_t>(v.n) * sizeof(double2), cudaMemcpyHostToDevice, I.stream));
     TMG_CUDA(cudaStreamSynchronize(I.stream));
 }
 
 namespace {
+// callers reset sc afterwards: plain u injection; fineD: the fine level's u as
+// complex128 (complex64 storage) instead of the level itself
 template <int P>
-void inject_up(Hierarchy::Impl& I, int ch = 0) {  // callers reset sc afterwards: plain u injection
+void inject_up(Hierarchy::Impl& I, int ch = 0, const dev::Lvl* fineD = nullptr) {
     for (int l = I.L - 1; l >= 1; --l)
-        dev::k_inject_u<P><<<I.blocks_for(I.lv[l].n), 256, 0, I.stream>>>(I.level(ch, l), I.level(ch, l + 1), 0);
+        dev::k_inject_u<P><<<I.blocks_for(I.lv[l].n), 256, 0, I.stream>>>(
+            I.level(ch, l), (l == I.L - 1 && fineD) ? *fineD : I.level(ch, l + 1), 0);
+}
+
+// complex64 fine level: a complex128 stand-in whose u is written by the caller,
+// then stored as complex64 (store_fine_u) and injected from (inject_up's fineD)
+dev::Lvl c64_stage(Hierarchy::Impl& I, Hierarchy::Impl::Tmp& t) {
+    dev::Lvl Fd = I.lv[I.L];
+    Fd.u = I.tmp_fine(t);
+    return Fd;
+}
+void store_fine_u(Hierarchy::Impl& I, const dev::Lvl& Fd) {
+    const dev::Lvl& F = I.lv[I.L];
+    dev::k_d2f<<<I.blocks_for(F.n), 256, 0, I.stream>>>(Fd.u, reinterpret_cast<float2*>(F.u), F.n);
+    TMG_CUDA(cudaGetLastError());
 }
 }  // namespace
 
@@ -1878,7 +1995,7 @@ struct HierarchyAccess {
         for (int ch = 0; ch < I.prob.channels; ++ch)
             for (int l = 0; l <= I.L; ++l) {
                 const dev::Lvl v = I.level(ch, l);
-                const size_t bytes = static_cast<size_t>(v.n) * sizeof(double2);
+                const size_t bytes = static_cast<size_t>(v.n) * (l == I.L ? I.fine_elem() : sizeof(double2));
                 for (double2* ptr : {v.sc, v.sf, v.si, v.sinext, v.uhat})
                     if (ptr) TMG_CUDA(cudaMemsetAsync(ptr, 0, bytes, I.stream));
             }
@@ -1888,7 +2005,9 @@ struct HierarchyAccess {
 void Hierarchy::set_fine_interior_u(const double* host) {
     if (impl_->amr) throw UnsupportedConfigError("set_fine_interior_u is not available on adaptive trees");
     Impl& I = *impl_;
-    const dev::Lvl& F = I.lv[I.L];
+    Impl::Tmp t;
+    const dev::Lvl F = I.prob.c64 ? c64_stage(I, t) : I.lv[I.L];
+    const dev::Lvl* fineD = I.prob.c64 ? &F : nullptr;
     const long long ni = interior_fine_vertices();
     double2* tmp = nullptr;
     TMG_CUDA(cudaMalloc(&tmp, static_cast<size_t>(ni) * sizeof(double2)));
@@ -1896,9 +2015,10 @@ void Hierarchy::set_fine_interior_u(const double* host) {
     if (I.p == 1) dev::k_scatter_interior<1><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, tmp);
     else if (I.p == 2) dev::k_scatter_interior<2><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, tmp);
     else dev::k_scatter_interior<3><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, tmp);
-    if (I.p == 1) inject_up<1>(I);
-    else if (I.p == 2) inject_up<2>(I);
-    else inject_up<3>(I);
+    if (fineD) store_fine_u(I, F);
+    if (I.p == 1) inject_up<1>(I, 0, fineD);
+    else if (I.p == 2) inject_up<2>(I, 0, fineD);
+    else inject_up<3>(I, 0, fineD);
     HierarchyAccess::reset_pipeline(I);
     TMG_CUDA(cudaStreamSynchronize(I.stream));
     cudaFree(tmp);
@@ -1911,13 +2031,17 @@ void Hierarchy::set_random_initial_guess(std::uint64_t seed) {
         return;
     }
     for (int ch = 0; ch < I.prob.channels; ++ch) {
-        const dev::Lvl F = I.level(ch, I.L);
+        Impl::Tmp t;
+        const dev::Lvl F = I.prob.c64 ? c64_stage(I, t) : I.level(ch, I.L);
+        const dev::Lvl* fineD = I.prob.c64 ? &F : nullptr;
         if (I.p == 1) dev::k_random_fine<1><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed, ch);
         else if (I.p == 2) dev::k_random_fine<2><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed, ch);
         else dev::k_random_fine<3><<<I.blocks_for(F.n), 256, 0, I.stream>>>(F, seed, ch);
-        if (I.p == 1) inject_up<1>(I, ch);
-        else if (I.p == 2) inject_up<2>(I, ch);
-        else inject_up<3>(I, ch);
+        if (fineD) store_fine_u(I, F);
+        if (I.p == 1) inject_up<1>(I, ch, fineD);
+        else if (I.p == 2) inject_up<2>(I, ch, fineD);
+        else inject_up<3>(I, ch, fineD);
+        TMG_CUDA(cudaStreamSynchronize(I.stream));
     }
     HierarchyAccess::reset_pipeline(I);
     TMG_CUDA(cudaStreamSynchronize(I.stream));
@@ -1983,6 +2107,7 @@ void test_divdc3(const double* x, const double* y, double* out, long long n) {
 // every vertex (coinciding components are exact copies, transfer.cpp:26-38).
 void Hierarchy::unfold() {
     if (impl_->amr) throw UnsupportedConfigError("FMG unfolding is not available on adaptive trees");
+    if (impl_->prob.c64) throw UnsupportedConfigError("FMG unfolding runs in complex128 (precision = fast | exact)");
     Impl& old = *impl_;
     Problem p2 = old.prob;
     p2.levels = old.L + 1;
