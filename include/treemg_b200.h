@@ -36,6 +36,10 @@
  *                               order, so CSV/log bytes match the reference
  *   fingerprint = 0 | 1         hash the final fine u / sc (treemg_result_fingerprint)
  *   device = <ordinal>          CUDA device
+ *   gpus = <n>                  n > 1: the finest level as n z-slabs over the GPUs
+ *                               device .. device+n-1 of this process (3D, fast;
+ *                               with fmg_from: at the last unfolding); bitwise
+ *                               identical iterates to gpus = 1
  */
 
 #ifndef TREEMG_B200_H
@@ -208,14 +212,21 @@ const char* tmg_last_error(void);
  * fused fine pass), coarser levels are replicated; halos, restriction
  * partials and the replicated level's residual move over NCCL (dlopen'd
  * libnccl.so.2), one slab per process/GPU.  With nccl_id == NULL, `local`
- * virtual slabs run in this process on one device with device-copy
- * transfers (the single-GPU test mode of the same code path).  3D, fast
- * precision; iterates are bitwise identical for every slab count. */
+ * slabs run in this process with device-copy transfers: on one device (the
+ * single-GPU test mode of the same code path), or with
+ * tmg_slabs_create_local spread over `devices` GPUs with peer copies over
+ * NVLink (what treemg_run's `gpus` key drives).  Each slab allocates only
+ * its planes (+ halos) of levels L and L-1.  3D, fast precision; iterates
+ * are bitwise identical for every slab count. */
 typedef struct tmg_slabs tmg_slabs;
 treemg_status tmg_nccl_unique_id(unsigned char* out128);
 treemg_status tmg_slabs_create(const tmg_problem* prob, int local, int rank, int world,
                                const unsigned char* nccl_id, tmg_slabs** out);
+treemg_status tmg_slabs_create_local(const tmg_problem* prob, int slabs, int devices, tmg_slabs** out);
 void tmg_slabs_destroy(tmg_slabs* h);
+/* whole-lattice u or sc of any level gathered from the slabs of this process
+ * (bitwise what one GPU's tmg_get_field returns) */
+treemg_status tmg_slabs_get_field(tmg_slabs* h, int level, const char* field, double* out);
 treemg_status tmg_slabs_cycle(tmg_slabs* h, const tmg_policy* pol, int n, tmg_sweep_stats* out);
 /* owned fine planes of the local slabs into a full-lattice host buffer */
 treemg_status tmg_slabs_get_fine_u(tmg_slabs* h, double* out);

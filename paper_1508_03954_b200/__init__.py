@@ -52,6 +52,7 @@ EXTENSION_SYMBOLS = [
     "tmg_bu_fas", "tmg_textbook_add", "tmg_channel_norms", "tmg_dyn_create", "tmg_dyn_destroy", "tmg_dyn_depth",
     "tmg_dyn_interior_count", "tmg_dyn_set_cell_marks", "tmg_dyn_sweep", "tmg_dyn_flags", "tmg_dyn_sweep_tables",
     "tmg_mark", "tmg_levels", "tmg_set_cell_marks", "tmg_dyn_phase_ms", "tmg_existing_vertices",
+    "tmg_slabs_create_local", "tmg_slabs_get_field",
 ]
 
 _lib = None
@@ -193,6 +194,10 @@ def lib():
         L.tmg_slabs_create.restype = ip
         L.tmg_slabs_create.argtypes = [ctypes.POINTER(_Problem), ip, ip, ip, ctypes.c_char_p, ctypes.POINTER(vp)]
         L.tmg_slabs_destroy.argtypes = [vp]
+        L.tmg_slabs_create_local.restype = ip
+        L.tmg_slabs_create_local.argtypes = [ctypes.POINTER(_Problem), ip, ip, ctypes.POINTER(vp)]
+        L.tmg_slabs_get_field.restype = ip
+        L.tmg_slabs_get_field.argtypes = [vp, ip, cp, pd]
         L.tmg_slabs_cycle.restype = ip
         L.tmg_slabs_cycle.argtypes = [vp, ctypes.POINTER(_Policy), ip, ctypes.POINTER(_Stats)]
         L.tmg_slabs_get_fine_u.restype = ip
@@ -471,12 +476,17 @@ class Slabs:
     else one slab for `rank` of `world` over NCCL."""
 
     def __init__(self, levels: int, phi: complex, chi: str = "seeded", rhs_seed: int = 12345, ell_min: int = 1,
-                 local: int = 1, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, device: int = 0):
+                 local: int = 1, rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None, device: int = 0,
+                 devices: int = 1):
+        """devices > 1 (nccl_id None): the `local` slabs spread over that many GPUs of this process."""
         self.L = lib()
         prob = _Problem(3, levels, ell_min, 0.0, complex(phi).real, complex(phi).imag, CHI_KINDS[chi], rhs_seed, 0, 1,
                         10 ** 12, device)
         h = ctypes.c_void_p()
-        _check(self.L.tmg_slabs_create(ctypes.byref(prob), local, rank, world, nccl_id, ctypes.byref(h)))
+        if nccl_id is None:
+            _check(self.L.tmg_slabs_create_local(ctypes.byref(prob), local, devices, ctypes.byref(h)))
+        else:
+            _check(self.L.tmg_slabs_create(ctypes.byref(prob), local, rank, world, nccl_id, ctypes.byref(h)))
         self.h = h
         self.levels = levels
 
@@ -501,6 +511,13 @@ class Slabs:
         n = (3 ** self.levels + 1) ** 3
         out = np.zeros(2 * n)
         _check(self.L.tmg_slabs_get_fine_u(self.h, _pd(out)))
+        return out[0::2] + 1j * out[1::2]
+
+    def field(self, level: int, name: str) -> np.ndarray:
+        """Whole-lattice u / sc of `level` gathered from the slabs (bitwise one GPU's field)."""
+        n = (3 ** level + 1) ** 3
+        out = np.zeros(2 * n)
+        _check(self.L.tmg_slabs_get_field(self.h, level, name.encode(), _pd(out)))
         return out[0::2] + 1j * out[1::2]
 
     def owned_planes(self):

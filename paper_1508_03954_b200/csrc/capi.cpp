@@ -41,18 +41,6 @@ namespace {
 
 thread_local std::string g_lastError;
 
-// A handle's kernels run on its own device whatever device is current on the
-// calling thread (treemg.h: a handle may move between threads); restored on exit.
-struct DeviceScope {
-    int prev = -1, want;
-    explicit DeviceScope(int device) : want(device) {
-        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
-        if (prev != want) cudaSetDevice(want);
-    }
-    ~DeviceScope() {
-        if (prev >= 0 && prev != want) cudaSetDevice(prev);
-    }
-};
 
 treemg_status fail(treemg_status code, const char* what) {
     g_lastError = what ? what : "unknown error";
@@ -274,6 +262,32 @@ treemg_status tmg_slabs_create(const tmg_problem* prob, int local, int rank, int
     }
     *out = h;
     return TREEMG_OK;
+}
+
+treemg_status tmg_slabs_create_local(const tmg_problem* prob, int slabs, int devices, tmg_slabs** out) {
+    if (!prob || !out) return fail(TREEMG_E_USAGE, "null argument");
+    *out = nullptr;
+    auto* h = new tmg_slabs();
+    const treemg_status st = guarded([&] {
+        const Problem p = problem_from(prob);
+        h->device = p.device;
+        const DeviceScope ds(h->device);
+        h->g = std::make_unique<SlabGroup>(p, slabs, 0, slabs, nullptr, devices);
+    });
+    if (st != TREEMG_OK) {
+        delete h;
+        return st;
+    }
+    *out = h;
+    return TREEMG_OK;
+}
+
+treemg_status tmg_slabs_get_field(tmg_slabs* h, int level, const char* field, double* out) {
+    if (!h || !field || !out) return fail(TREEMG_E_USAGE, "null argument");
+    return guarded([&] {
+        const DeviceScope ds(h->device);
+        h->g->get_field(level, field, out);
+    });
 }
 
 void tmg_slabs_destroy(tmg_slabs* h) {

@@ -142,9 +142,9 @@ __global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
         unsigned char* st = ring + stage * SB;
         const int cz = min(zz / 3, mc - 1);
         mbar_expect_tx(&bar[stage], stageBytes);
-        tma_load3(st, &mapU, xScale * (x0 - 1), y0 - 1, zz, &bar[stage]);
-        tma_load3(st + M::kPlane, &mapC, 2 * cx0, cy0, cz, &bar[stage]);
-        if (BPX) tma_load3(st + M::kPlane + M::kC, &mapI, 2 * cx0, cy0, cz, &bar[stage]);
+        tma_load3(st, &mapU, xScale * (x0 - 1), y0 - 1, zz - a.tmaZ0, &bar[stage]);
+        tma_load3(st + M::kPlane, &mapC, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
+        if (BPX) tma_load3(st + M::kPlane + M::kC, &mapI, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
     };
 
     if (tid == 0) {
@@ -533,7 +533,7 @@ size_t smem_bytes(bool bpx, bool c64) {
     return bpx ? Smem<double2>::bytes<true>() : Smem<double2>::bytes<false>();
 }
 
-bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64) {
+bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64, int nz) {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -545,7 +545,7 @@ bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool 
     }
     const bool f32 = c64 && kind != 2;  // coarse planes stay complex128
     const cuuint64_t es = f32 ? 4 : 8;
-    const cuuint64_t dims[3] = {2ull * n1, n1, n1};
+    const cuuint64_t dims[3] = {2ull * n1, n1, nz > 0 ? static_cast<cuuint64_t>(nz) : n1};
     const cuuint64_t strides[2] = {2 * es * n1, 2 * es * n1 * n1};
     const cuuint32_t box[3] = {kind == 0 ? 2u * HX : kind == 1 ? 2u * TX : 2u * CX,
                                static_cast<cuuint32_t>(kind == 0 ? HY : kind == 1 ? TY : CY), kind == 2 ? 2u : 1u};

@@ -71,6 +71,7 @@ struct Args {
     int bpx, hb, ellMin, level;
     int chunkBase;        // first global z-chunk of this launch
     int c64;              // fine level in complex64 (float2) storage and arithmetic
+    int tmaZ0, tmaZ0c;    // first plane of the fine / coarse tensor maps (z-slab members; else 0)
 };
 
 // Tile / z-chunk geometry; the chunk count is a multiple of `parts` (z-slabs:
@@ -84,7 +85,8 @@ int blocks(const Geometry& g);
 // TMA descriptor for one lattice array (double2 viewed as float64 pairs, or
 // float2 as float32 pairs when c64).
 // kind 0: fine u / sc halo'd tile, 1: fine b tile, 2: two coarse planes.
-bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64 = false);
+// nz > 0: the map covers nz planes from `base` (a z-slab's allocated range)
+bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64 = false, int nz = 0);
 
 // nchunks <= 0: all z-chunks (chunkBase must be 0)
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,

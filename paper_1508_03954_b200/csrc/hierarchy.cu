@@ -517,9 +517,9 @@ __global__ void k_load_vector(Lvl c, const double2* __restrict__ chiNodal, Level
 // Seeded nodal rhs f(x) keyed on the finest-lattice position,
 // optionally masked to the ball |x - 1/2|^2 < 0.04.
 template <int P>
-__global__ void k_seeded_chi(double2* out, unsigned n, unsigned n1, unsigned long long seed, int scale, long long mkey,
-                             int sphere, int channel) {
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
+__global__ void k_seeded_chi(double2* out, unsigned fa, unsigned n, unsigned n1, unsigned long long seed, int scale,
+                             long long mkey, int sphere, int channel) {  // flat indices [fa, n)
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < n; f += gridDim.x * blockDim.x) {
         int idx[P];
         unflat<P>(f, n1, idx);
         unsigned long long key = 0;
@@ -614,8 +614,8 @@ __global__ void k_scatter_interior(Lvl c, const double2* __restrict__ in) {
 
 // FMG unfolding: new finest level u = P u_{coarse} (spacetree.cpp:245-270).
 template <int P>
-__global__ void k_prolong_new(Lvl c, Lvl pr) {
-    for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
+__global__ void k_prolong_new(Lvl c, Lvl pr, unsigned fa, unsigned fb) {  // flat indices [fa, fb)
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         int idx[P];
         unflat<P>(f, c.n1, idx);
         int q[P], rel[P];
@@ -791,6 +791,16 @@ struct Hierarchy::Impl {
     static constexpr unsigned kChainMaxN = TMG_CHAIN_MAXN;  // levels below this size join the chain
     int fusedResident = 3 * 148;
     bool fineFused = false;  // the fine level runs a fused pass (decided before allocation)
+    // z-slab member (prob.slabLo >= 0): allocated plane ranges [za, zb) of levels L and L-1
+    int zaF = 0, zbF = 0, zaC = 0, zbC = 0;
+    bool slab() const { return prob.slabLo >= 0; }
+    // the fine lattice's allocated flat index range
+    std::pair<unsigned, unsigned> fine_flat_range() const {
+        const dev::Lvl& F = lv[L];
+        if (!slab()) return {0u, F.n};
+        const unsigned plane = F.n1 * F.n1;
+        return {static_cast<unsigned>(zaF) * plane, static_cast<unsigned>(zbF) * plane};
+    }
     // bytes per fine-level element: complex64 storage (precision = fast-complex64) or complex128
     size_t fine_elem() const { return prob.c64 ? sizeof(float2) : sizeof(double2); }
     // a transient complex128 array of the fine lattice (complex64 conversions)
@@ -828,6 +838,14 @@ struct Hierarchy::Impl {
         TMG_CUDA(cudaMemsetAsync(ptr, 0, count * sizeof(T), stream));
         return static_cast<T*>(ptr);
     }
+    // planes [za, zb) of a level whose planes hold `plane` elements, addressed
+    // with global lattice indices (the returned base is za planes before the
+    // allocation; only indices inside the range are ever touched)
+    template <class T>
+    T* alloc_planes(long long plane, int za, int zb) {
+        T* ptr = alloc<T>(static_cast<size_t>(plane) * static_cast<size_t>(zb - za));
+        return ptr - plane * za;
+    }
 
     // grid-stride launches: enough blocks that each thread has only a few
     // points (memory-level parallelism for the bandwidth-bound level passes)
@@ -846,6 +864,20 @@ struct Hierarchy::Impl {
         for (int d = 0; d < p; ++d) n *= v.n1;
         if (n >= (1ull << 32)) throw CapacityError("level lattice exceeds 2^32 vertices");
         v.n = static_cast<unsigned>(n);
+        if (slab() && l >= L - 1) {  // z-slab member: the plane range of levels L and L-1 only
+            const long long plane = static_cast<long long>(v.n1) * v.n1;
+            const int za = fine ? zaF : zaC, zb = fine ? zbF : zbC;
+            v.u = alloc_planes<double2>(plane, za, zb);
+            v.sc = alloc_planes<double2>(plane, za, zb);
+            if (fine) {
+                v.chi = alloc_planes<double2>(plane, za, zb);
+            } else {
+                v.rhat = alloc_planes<double2>(plane, za, zb);
+                v.si = alloc_planes<double2>(plane, za, zb);
+                v.sinext = alloc_planes<double2>(plane, za, zb);
+            }
+            return v;
+        }
         if (fine && prob.c64) {  // complex64 storage (float2) behind the double2 pointers: fused3 / conversions only
             v.u = reinterpret_cast<double2*>(alloc<float2>(n));
             v.sc = reinterpret_cast<double2*>(alloc<float2>(n));
@@ -1020,9 +1052,10 @@ struct Hierarchy::Impl {
         const dev::Lvl& F = lv[L];
         const int key = prob.rhsLattice >= 0 ? prob.rhsLattice : L;
         const int scale = pow3i(key - L);
-        dev::k_seeded_chi<P><<<blocks_for(F.n), 256, 0, stream>>>(chiNodal, F.n, F.n1, prob.rhsSeed, scale,
-                                                                  static_cast<long long>(pow3i(key)),
-                                                                  prob.rhsSphere ? 1 : 0, ch);
+        const auto [fa, fb] = fine_flat_range();
+        dev::k_seeded_chi<P><<<blocks_for(fb - fa), 256, 0, stream>>>(chiNodal, fa, fb, F.n1, prob.rhsSeed, scale,
+                                                                       static_cast<long long>(pow3i(key)),
+                                                                       prob.rhsSphere ? 1 : 0, ch);
         TMG_CUDA(cudaGetLastError());
     }
 
@@ -1053,7 +1086,9 @@ struct Hierarchy::Impl {
             }
             h[f] = make_double2(v, 0.0);
         }
-        TMG_CUDA(cudaMemcpyAsync(chiNodal, h.data(), F.n * sizeof(double2), cudaMemcpyHostToDevice, stream));
+        const auto [fa, fb] = fine_flat_range();
+        TMG_CUDA(cudaMemcpyAsync(chiNodal + fa, h.data() + fa, (fb - fa) * sizeof(double2), cudaMemcpyHostToDevice,
+                                 stream));
         TMG_CUDA(cudaStreamSynchronize(stream));
     }
 
@@ -1612,6 +1647,16 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
         if (I.p != 3 || !I.fineFused || prob.channels > 1 || prob.gaussian)
             throw UnsupportedConfigError("precision = fast-complex64 runs the 3D fused fine pass (dim = 3, one channel)");
     }
+    if (I.slab()) {
+        if (!prob.fast || I.p != 3 || !I.fineFused || prob.c64 || prob.channels > 1 || I.L < 3)
+            throw UnsupportedConfigError("z-slabs: 3D fast precision (complex128), fused fine pass");
+        const int n1 = pow3i(I.L) + 1, n1c = pow3i(I.L - 1) + 1;
+        const int Zs = (prob.slabLo + 2) / 3, Ze = (prob.slabHi + 2) / 3;
+        I.zaF = std::max(0, prob.slabLo - 1);
+        I.zbF = std::min(n1, prob.slabHi + 1);
+        I.zaC = std::max(0, Zs - 2);
+        I.zbC = std::min(n1c, Ze + 2);
+    }
     I.lv.resize(I.L + 1);
     for (int l = 0; l <= I.L; ++l) I.lv[l] = I.make_level(l, l == I.L);
     I.normBlocks = std::max(I.blocks_for(I.lv[I.L].n), fast::residual_fine_blocks(I.p, I.lv[I.L], I.smCount));
@@ -1656,7 +1701,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     }
     I.dNorm = I.alloc<double>(2 * static_cast<size_t>(prob.channels));
     TMG_CUDA(cudaMallocHost(&I.hNorm, 2 * sizeof(double) * prob.channels));
-    I.chiNodal = I.alloc<double2>(I.lv[I.L].n);
+    I.chiNodal = I.slab() ? I.alloc_planes<double2>(static_cast<long long>(I.lv[I.L].n1) * I.lv[I.L].n1, I.zaF, I.zbF)
+                          : I.alloc<double2>(I.lv[I.L].n);
     I.compute_level_constants();
     I.build_restrict_tables();
     if (prob.gaussian) {
@@ -1669,14 +1715,23 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
         if (prob.fast && I.p == 3 && I.L >= 2 && !(fz && fz[0] == '0')) {
             const dev::Lvl& F = I.lv[I.L];
             // v double buffer; sc is write-only (v-form)
-            I.uAlt = prob.c64 ? reinterpret_cast<double2*>(I.alloc<float2>(F.n)) : I.alloc<double2>(F.n);
+            const long long plane = static_cast<long long>(F.n1) * F.n1;
+            I.uAlt = prob.c64  ? reinterpret_cast<double2*>(I.alloc<float2>(F.n))
+                     : I.slab() ? I.alloc_planes<double2>(plane, I.zaF, I.zbF)
+                                : I.alloc<double2>(F.n);
             I.geo = fused3::geometry(static_cast<int>(F.m), static_cast<int>(I.lv[I.L - 1].m), prob.zParts,
                                      I.fusedResident);
             I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
             const dev::Lvl& C = I.lv[I.L - 1];
-            bool ok = fused3::encode_map(&I.mapU[0], F.u, F.n1, 0, prob.c64) &&
-                      fused3::encode_map(&I.mapU[1], I.uAlt, F.n1, 0, prob.c64) &&
-                      fused3::encode_map(&I.mapC, C.sc, C.n1, 2) && fused3::encode_map(&I.mapI, C.si, C.n1, 2);
+            // slab members: maps over the allocated plane ranges, z coordinates shifted by the kernel
+            const long long planeC = static_cast<long long>(C.n1) * C.n1;
+            const int nzF = I.slab() ? I.zbF - I.zaF : static_cast<int>(F.n1);
+            const int nzC = I.slab() ? I.zbC - I.zaC : static_cast<int>(C.n1);
+            const long long offF = I.slab() ? plane * I.zaF : 0, offC = I.slab() ? planeC * I.zaC : 0;
+            bool ok = fused3::encode_map(&I.mapU[0], F.u + offF, F.n1, 0, prob.c64, nzF) &&
+                      fused3::encode_map(&I.mapU[1], I.uAlt + offF, F.n1, 0, prob.c64, nzF) &&
+                      fused3::encode_map(&I.mapC, C.sc + offC, C.n1, 2, false, nzC) &&
+                      fused3::encode_map(&I.mapI, C.si + offC, C.n1, 2, false, nzC);
             if (!ok) throw CudaError("cuTensorMapEncodeTiled failed for the fused fine pass");
             I.fused = true;
         }
@@ -1688,11 +1743,13 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
             if (I.p == 1) I.build_rhs_seeded<1>(ch);
             else if (I.p == 2) I.build_rhs_seeded<2>(ch);
             else I.build_rhs_seeded<3>(ch);
-            I.load_vector_dispatch(-1, -1, ch);
+            if (I.slab()) I.load_vector_dispatch(prob.slabLo, prob.slabHi, ch);
+            else I.load_vector_dispatch(-1, -1, ch);
         }
     } else {
         I.build_rhs_analytic();
-        I.load_vector_dispatch();
+        if (I.slab()) I.load_vector_dispatch(prob.slabLo, prob.slabHi);
+        else I.load_vector_dispatch();
         // every channel carries the same fields (runner.cpp:152): same load vector
         for (int ch = 1; ch < prob.channels; ++ch)
             TMG_CUDA(cudaMemcpyAsync(I.chanLv[ch - 1][I.L].chi, I.lv[I.L].chi,
@@ -1867,6 +1924,8 @@ void Hierarchy::get_field(int level, const std::string& name, double* host) cons
         if (ch < 0 || ch >= I.prob.channels) throw ConfigError("get_field: channel out of range");
     }
     const dev::Lvl v = I.level(ch, level);
+    if (I.slab() && level >= I.L - 1 && field != "diag")
+        throw UnsupportedConfigError("get_field: a z-slab member holds a plane range of levels L and L-1 (SlabGroup)");
     if (field == "diag") {
         // host-side: per vertex the sum of A_aa over its existing cells
         const Cplx a = I.diagInterior[level] / static_cast<double>(1 << I.p);
@@ -2061,11 +2120,8 @@ void Hierarchy::set_fine_rhs(const double* hostNodalChi) {
     TMG_CUDA(cudaStreamSynchronize(I.stream));
 }
 
-std::uint64_t Hierarchy::field_hash(int level, const std::string& field) const {
-    if (impl_->amr) return impl_->amr->field_hash(level, field);
-    const long long n = lattice_size(level);
-    std::vector<double> buf(2 * static_cast<size_t>(n));
-    get_field(level, field, buf.data());
+// FNV-1a over the bit patterns (sign of zero folded), tests/golden/make_goldens.py
+std::uint64_t fnv_hash(const std::vector<double>& buf) {
     std::uint64_t h = 1469598103934665603ull;
     for (double x : buf) {
         const double y = x + 0.0;
@@ -2079,7 +2135,23 @@ std::uint64_t Hierarchy::field_hash(int level, const std::string& field) const {
     return h;
 }
 
+std::uint64_t Hierarchy::field_hash(int level, const std::string& field) const {
+    if (impl_->amr) return impl_->amr->field_hash(level, field);
+    const long long n = lattice_size(level);
+    std::vector<double> buf(2 * static_cast<size_t>(n));
+    get_field(level, field, buf.data());
+    return fnv_hash(buf);
+}
+
 int fused3_resident_blocks(int smCount) { return fused3::resident_blocks(smCount); }
+
+DeviceScope::DeviceScope(int device) : want(device) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != want) cudaSetDevice(want);
+}
+DeviceScope::~DeviceScope() {
+    if (prev >= 0 && prev != want) cudaSetDevice(prev);
+}
 
 void test_divdc3(const double* x, const double* y, double* out, long long n) {
     std::vector<dev::DivConst> k(static_cast<size_t>(n));
@@ -2135,9 +2207,9 @@ void Hierarchy::unfold() {
         copy(b.sinext, a.sinext);
     }
     const dev::Lvl& F = nw.lv[L + 1];
-    if (nw.p == 1) dev::k_prolong_new<1><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L]);
-    else if (nw.p == 2) dev::k_prolong_new<2><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L]);
-    else dev::k_prolong_new<3><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L]);
+    if (nw.p == 1) dev::k_prolong_new<1><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L], 0u, F.n);
+    else if (nw.p == 2) dev::k_prolong_new<2><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L], 0u, F.n);
+    else dev::k_prolong_new<3><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L], 0u, F.n);
     TMG_CUDA(cudaGetLastError());
     nw.coarseUStale = nw.prob.fast;
     TMG_CUDA(cudaStreamSynchronize(nw.stream));

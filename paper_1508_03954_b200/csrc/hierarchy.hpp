@@ -74,6 +74,10 @@ struct Problem {
     double hMax = 0.0, hMin = 0.0;
     std::size_t maxVertices = 8u * 1024u * 1024u;
     int device = 0;
+    // z-slab member (SlabGroup): the fine-level planes [slabLo, slabHi)
+    // are owned; levels L and L-1 are allocated only over the planes the slab
+    // reads / writes (owned + halos), behind global-index base pointers
+    int slabLo = -1, slabHi = -1;
 };
 
 struct SweepStats {  // SweepStats, cycles.hpp:37-45
@@ -86,6 +90,17 @@ struct SweepStats {  // SweepStats, cycles.hpp:37-45
 struct AmrMarkStats {  // MarkStats, amr.hpp:19-27
     long long refineVertices = 0, eraseVertices = 0, refineCells = 0, eraseCells = 0;
     long long vetoConvergence = 0, vetoHMin = 0, vetoHMax = 0;
+};
+
+// Makes `device` current for its lifetime and restores the caller's device:
+// a handle's kernels run on its own device whatever is current on the calling
+// thread (treemg.h: a handle may move between threads).
+struct DeviceScope {
+    int prev = -1, want;
+    explicit DeviceScope(int device);
+    ~DeviceScope();
+    DeviceScope(const DeviceScope&) = delete;
+    DeviceScope& operator=(const DeviceScope&) = delete;
 };
 
 // omega_unmasked, proj/src/cycles.cpp:11-31 (host, same libstdc++ arithmetic)
@@ -153,8 +168,10 @@ class Hierarchy {
 // device copies -- the test mode) or one slab per process/GPU over NCCL.
 class SlabGroup {
   public:
-    // ncclId == nullptr: `local` virtual slabs (rank 0, world = local).
-    SlabGroup(const Problem& prob, int local, int rank, int world, const void* ncclId);
+    // ncclId == nullptr: `local` slabs in this process (rank 0, world = local),
+    // spread round-robin over `devices` GPUs from prob.device (transfers are
+    // device / peer copies); else one slab for `rank` of `world` over NCCL.
+    SlabGroup(const Problem& prob, int local, int rank, int world, const void* ncclId, int devices = 1);
     ~SlabGroup();
     SlabGroup(const SlabGroup&) = delete;
     SlabGroup& operator=(const SlabGroup&) = delete;
@@ -163,6 +180,17 @@ class SlabGroup {
     // Fine-level u of the planes owned by the local slabs, full-lattice layout
     // (other planes left untouched in `host`).
     void get_fine_u(double* host);
+    // Whole-lattice u / sc of any level gathered from the local slabs (all slabs
+    // local: ncclId == nullptr), bitwise what one GPU's Hierarchy::get_field gives.
+    void get_field(int level, const std::string& field, double* host);
+    std::uint64_t field_hash(int level, const std::string& field);
+    int levels() const;
+    long long interior_fine_vertices() const;
+    // FMG's last unfolding onto slabs: a group one level deeper than `coarse`
+    // (a single-GPU hierarchy at the previous FMG stage, consumed), with that
+    // stage's state and the new finest level p-linearly prolonged on every
+    // slab's planes -- Hierarchy::unfold restricted to the slab ranges.
+    static std::unique_ptr<SlabGroup> unfold_from(Hierarchy& coarse, int local, int devices);
     void time_cycles(const Policy& pol, int n0, int count, double* out4);
     void e2e_step(const Policy& pol, int n, const double* hostChi, double* out3, long long* h2dBytes);
     int owned_planes(int* z0, int* z1) const;  // of the first local slab
