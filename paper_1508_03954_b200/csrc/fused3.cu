@@ -109,8 +109,11 @@ struct Smem {
 };
 constexpr int NT = TX * TY;
 
+#ifndef TMG_F3_MINB
+#define TMG_F3_MINB (TY <= 4 ? 6 : TY <= 8 ? 3 : 2)
+#endif
 template <bool BPX, class S>
-__global__ void __launch_bounds__(NT, (TY <= 4 ? 6 : TY <= 8 ? 3 : 2))
+__global__ void __launch_bounds__(NT, TMG_F3_MINB)
     k_fused3(const __grid_constant__ CUtensorMap mapU,
              const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
     using C = typename Cx<S>::T;

@@ -19,8 +19,8 @@ from conftest import load_golden
 
 pytestmark = pytest.mark.gpu
 
-C64_NORM_TOL = 1e-4
-C64_U_TOL = 1e-4
+C64_NORM_TOL = 3e-4  # cfg3 after 50 cycles: 9.7e-5 (B200, round 2)
+C64_U_TOL = 3e-4
 
 
 def _hist(tmg, level, phi, pol, precision, cycles):
