@@ -384,9 +384,7 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
             const C smooth = mul(r, invDiag);
             const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpxy && kz == 0, BPX ? 1 : 0, a.hb);
             if (owned) {
-#ifndef TMG_NO_SC_STORE  // timing experiment only: the fine sc is not written
-                *sPtr = scn;
-#endif
+                if (a.writeSc) *sPtr = scn;
                 // next cycle's state v = u + sc of plane zz - 1 (its corrected u is
                 // still in the other P buffer: rewritten only in the next phase B)
                 *uPtr = add(Pb[((it + 1) & 1) * M::kP + po], scn);
@@ -442,6 +440,36 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     tb[ty * TX + tx] = accHi;
     flushSlots(zLow + 1 - zBase);
     dev::block_norms(nmax, nsum, a.norms);
+}
+
+// derive_u (fused3.cuh): phase B of k_fused3 for one point, from global memory
+template <class S>
+__global__ void __launch_bounds__(256) k_derive_u(const typename Cx<S>::T* __restrict__ vOld,
+                                                  const double2* __restrict__ scTD, unsigned n1, unsigned n1c,
+                                                  unsigned fa, unsigned fb, double2* __restrict__ uOut) {
+    using C = typename Cx<S>::T;
+    const int m = static_cast<int>(n1) - 1, mc = static_cast<int>(n1c) - 1;
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
+        const unsigned fr = f / n1;
+        const int x = static_cast<int>(f - fr * n1), y = static_cast<int>(fr % n1), z = static_cast<int>(fr / n1);
+        if (x < 1 || x > m - 1 || y < 1 || y > m - 1 || z < 1 || z > m - 1) {
+            uOut[f] = zero2();
+            continue;
+        }
+        const int qx = min(x / 3, mc - 1), qy = min(y / 3, mc - 1), qz = min(z / 3, mc - 1);
+        const double w1y = third<double>(y - 3 * qy), w1z = third<double>(z - 3 * qz);
+        const long long sy = n1c, sz = static_cast<long long>(n1c) * n1c;
+        C V[2];
+#pragma unroll
+        for (int dx = 0; dx < 2; ++dx) {  // computeV: y, then z, stored in the kernel's precision
+            const double2* c = scTD + (qx + dx) + sy * qy + sz * qz;
+            const double2 a0 = lerpw(ld(c), ld(c + sy), w1y);
+            const double2 a1 = lerpw(ld(c + sz), ld(c + sz + sy), w1y);
+            V[dx] = to_c(lerpw(a0, a1, w1z), C{});
+        }
+        const C scv = lerpw(V[0], V[1], third<S>(x - 3 * qx));  // phase B: x
+        uOut[f] = to_d(add(ld(vOld + f), scv));
+    }
 }
 
 template <bool SMOOTH>
@@ -593,6 +621,16 @@ void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
         if (a.bpx) launch_one<true, double>(a, mapU, mapC, mapI, s, grid);
         else launch_one<false, double>(a, mapU, mapC, mapI, s, grid);
     }
+}
+
+void derive_u(const void* vOld, const double2* scTD, unsigned n1, unsigned n1c, unsigned fa, unsigned fb,
+              double2* uOut, bool c64, cudaStream_t s) {
+    if (fb <= fa) return;
+    const unsigned blocks = std::min<unsigned>((fb - fa + 255) / 256, 148u * 32u);
+    if (c64)
+        k_derive_u<float><<<blocks, 256, 0, s>>>(static_cast<const float2*>(vOld), scTD, n1, n1c, fa, fb, uOut);
+    else
+        k_derive_u<double><<<blocks, 256, 0, s>>>(static_cast<const double2*>(vOld), scTD, n1, n1c, fa, fb, uOut);
 }
 
 void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s, int za, int zb,

@@ -72,6 +72,7 @@ struct Args {
     int chunkBase;        // first global z-chunk of this launch
     int c64;              // fine level in complex64 (float2) storage and arithmetic
     int tmaZ0, tmaZ0c;    // first plane of the fine / coarse tensor maps (z-slab members; else 0)
+    int writeSc;          // store the fine sc (else it is re-derived on demand: derive_u)
 };
 
 // Tile / z-chunk geometry; the chunk count is a multiple of `parts` (z-slabs:
@@ -87,6 +88,15 @@ int blocks(const Geometry& g);
 // kind 0: fine u / sc halo'd tile, 1: fine b tile, 2: two coarse planes.
 // nz > 0: the map covers nz planes from `base` (a z-slab's allocated range)
 bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64 = false, int nz = 0);
+
+// The corrected fine iterate u = v_old + P sc_td(L-1) of the last fused pass,
+// re-derived with the kernel's own arithmetic (y, z, then x interpolation of the
+// complex128 coarse values; complex64 when c64) on the fine flat indices
+// [fa, fb); boundary points get 0.  vOld: the fine state the pass read,
+// scTD: the level L-1 top-down values it prolonged.  The fused pass then need
+// not store the write-only fine sc (16 of its 64 B per vertex): sc = v - u.
+void derive_u(const void* vOld, const double2* scTD, unsigned n1, unsigned n1c, unsigned fa, unsigned fb,
+              double2* uOut, bool c64, cudaStream_t s);
 
 // nchunks <= 0: all z-chunks (chunkBase must be 0)
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,

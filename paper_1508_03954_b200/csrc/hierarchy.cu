@@ -589,6 +589,18 @@ __global__ void k_vform_f2d(const float2* __restrict__ v, const float2* __restri
         out[i] = make_double2(static_cast<double>(v[i].x) - sc[i].x, static_cast<double>(v[i].y) - sc[i].y);
 }
 
+// sc-free fused pass: sc = v - u with the derived u (fused3::derive_u), on [fa, fb)
+template <class S2>
+__global__ void k_split_derived(S2* __restrict__ v, S2* __restrict__ sc, const double2* __restrict__ u, unsigned fa,
+                                unsigned fb, int toU) {  // toU: v <- u as well
+    using R = decltype(S2::x);
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
+        const S2 vf = v[f];
+        sc[f] = S2{static_cast<R>(vf.x - u[f].x), static_cast<R>(vf.y - u[f].y)};
+        if (toU) v[f] = S2{static_cast<R>(u[f].x), static_cast<R>(u[f].y)};
+    }
+}
+
 // v-form fine level (fused3.cuh): u = v - sc, in place
 __global__ void k_vform_to_u(double2* v, const double2* sc, size_t n) {
     for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
@@ -791,6 +803,10 @@ struct Hierarchy::Impl {
     static constexpr unsigned kChainMaxN = TMG_CHAIN_MAXN;  // levels below this size join the chain
     int fusedResident = 3 * 148;
     bool fineFused = false;  // the fine level runs a fused pass (decided before allocation)
+    // sc-free fine pass (3D fused td-add, fused3::derive_u): the level L-1 top-down values the
+    // last pass prolonged (the planes of a slab), and whether the fine (u, sc) must be derived
+    double2* scTD = nullptr;
+    bool fineDerived = false;
     // z-slab member (prob.slabLo >= 0): allocated plane ranges [za, zb) of levels L and L-1
     int zaF = 0, zbF = 0, zaC = 0, zbC = 0;
     bool slab() const { return prob.slabLo >= 0; }
@@ -1274,6 +1290,8 @@ struct Hierarchy::Impl {
         if (P == 3 && fused) {
             fused3::Args fa{};
             dev::Lvl& F = lv[L];
+            fa.writeSc = bpx;  // td-add: the fine sc is re-derived on demand (fused3::derive_u)
+            if (!bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1));
             fa.uNew = uAlt;   // next v (v-form, fused3.cuh)
             fa.scNew = F.sc;  // write-only
             fa.b = F.chi;
@@ -1301,6 +1319,7 @@ struct Hierarchy::Impl {
                             (use_up() || lo <= L - 1) ? &sL : nullptr);
             std::swap(F.u, uAlt);
             std::swap(mapU[0], mapU[1]);
+            fineDerived = !bpx;
             if (use_up()) {
                 up_all(pol, n, fused3::blocks(geo));
                 TMG_CUDA(cudaGetLastError());
@@ -1347,6 +1366,14 @@ struct Hierarchy::Impl {
     void inject_coarse_u() {
         Tmp t;
         for (int l = L - 1; l >= 1; --l) {
+            if (l == L - 1 && fineDerived) {  // the derived fine u (sc-free fused pass)
+                dev::Lvl Fd = lv[L];
+                Fd.u = tmp_fine(t);
+                const auto [fa, fb] = fine_flat_range();
+                derive_fine_u(Fd.u, fa, fb);
+                dev::k_inject_u<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(lv[l], Fd, 0);
+                continue;
+            }
             if (l == L - 1 && prob.c64) {  // u = v - sc of the complex64 fine level, as complex128
                 dev::Lvl Fd = lv[L];
                 Fd.u = tmp_fine(t);
@@ -1363,6 +1390,41 @@ struct Hierarchy::Impl {
 
     // the finest level holds v = u + sc (fused fast paths, fused3.cuh)
     bool vForm() const { return prob.fast && (fused || fused2on); }
+
+    // planes [za, zb) of level L-1's top-down sc, as the sc-free fused pass is about to read them
+    void save_coarse_td(int za, int zb) {
+        const dev::Lvl& C = lv[L - 1];
+        const long long plane = static_cast<long long>(C.n1) * C.n1;
+        if (zb > za)
+            TMG_CUDA(cudaMemcpyAsync(scTD + za * plane, C.sc + za * plane, static_cast<size_t>((zb - za) * plane) *
+                                     sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+    }
+
+    // the fine u of the last sc-free pass on the flat range [fa, fb) into out (global indices)
+    void derive_fine_u(double2* out, unsigned fa, unsigned fb) {
+        const dev::Lvl& F = lv[L];
+        fused3::derive_u(uAlt, scTD, F.n1, lv[L - 1].n1, fa, fb, out, prob.c64, stream);
+        TMG_CUDA(cudaGetLastError());
+    }
+
+    // fineDerived -> the fine arrays hold (v, sc) again, sc = v - u with the derived u;
+    // toU: (u, sc) instead (what Hierarchy::unfold makes of the old finest level)
+    void split_fine(bool toU) {
+        if (!fineDerived) return;
+        const dev::Lvl& F = lv[L];
+        const auto [fa, fb] = fine_flat_range();
+        Tmp t;
+        double2* u = tmp_fine(t);
+        derive_fine_u(u, fa, fb);
+        if (prob.c64)
+            dev::k_split_derived<float2><<<blocks_for(fb - fa), 256, 0, stream>>>(
+                reinterpret_cast<float2*>(F.u), reinterpret_cast<float2*>(F.sc), u, fa, fb, toU ? 1 : 0);
+        else
+            dev::k_split_derived<double2><<<blocks_for(fb - fa), 256, 0, stream>>>(F.u, F.sc, u, fa, fb, toU ? 1 : 0);
+        TMG_CUDA(cudaGetLastError());
+        TMG_CUDA(cudaStreamSynchronize(stream));
+        fineDerived = false;
+    }
 
     void materialize_coarse_u() {
         if (!prob.fast || !coarseUStale) return;
@@ -1723,6 +1785,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
                                      I.fusedResident);
             I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
             const dev::Lvl& C = I.lv[I.L - 1];
+            I.scTD = I.slab() ? I.alloc_planes<double2>(static_cast<long long>(C.n1) * C.n1, I.zaC, I.zbC)
+                              : I.alloc<double2>(C.n);
             // slab members: maps over the allocated plane ranges, z coordinates shifted by the kernel
             const long long planeC = static_cast<long long>(C.n1) * C.n1;
             const int nzF = I.slab() ? I.zbF - I.zaF : static_cast<int>(F.n1);
@@ -1949,6 +2013,32 @@ void Hierarchy::get_field(int level, const std::string& name, double* host) cons
         return;
     }
     if (field == "u" && level < I.L) I.materialize_coarse_u();
+    if (level == I.L && I.fineDerived && (field == "u" || field == "sc")) {  // sc-free pass: u derived, sc = v - u
+        Impl::Tmp t;
+        double2* u = I.tmp_fine(t);
+        I.derive_fine_u(u, 0, v.n);
+        TMG_CUDA(cudaMemcpyAsync(host, u, static_cast<size_t>(v.n) * sizeof(double2), cudaMemcpyDeviceToHost, I.stream));
+        std::vector<double> vv;
+        if (field == "sc") {
+            vv.resize(2 * static_cast<size_t>(v.n));
+            if (I.prob.c64) {
+                std::vector<float> vf(vv.size());
+                TMG_CUDA(cudaMemcpyAsync(vf.data(), v.u, vf.size() * sizeof(float), cudaMemcpyDeviceToHost, I.stream));
+                TMG_CUDA(cudaStreamSynchronize(I.stream));
+                for (size_t i = 0; i < vv.size(); ++i) vv[i] = vf[i];
+            } else {
+                TMG_CUDA(cudaMemcpyAsync(vv.data(), v.u, vv.size() * sizeof(double), cudaMemcpyDeviceToHost, I.stream));
+            }
+        }
+        TMG_CUDA(cudaStreamSynchronize(I.stream));
+        if (field == "sc") {
+            for (size_t i = 0; i < vv.size(); ++i) {
+                const double r = vv[i] - host[i];
+                host[i] = I.prob.c64 ? static_cast<double>(static_cast<float>(r)) : r;
+            }
+        }
+        return;
+    }
     if (level == I.L && I.prob.c64 && (field == "u" || field == "sc" || field == "chi")) {  // complex64 storage
         std::vector<float2> a(v.n), b;
         TMG_CUDA(cudaMemcpyAsync(a.data(), field == "chi" ? v.chi : field == "sc" ? v.sc : v.u,
@@ -1997,6 +2087,7 @@ void Hierarchy::set_field(int level, const std::string& field, const double* hos
     if (!ptr) throw ConfigError("set_field: unknown field '" + field + "'");
     if (level == I.L && I.vForm() && (field == "u" || field == "sc")) {
         // the device keeps v = u + sc on the finest level
+        I.split_fine(false);
         std::vector<double> u(2 * static_cast<size_t>(v.n)), sc(2 * static_cast<size_t>(v.n));
         get_field(level, "u", u.data());
         get_field(level, "sc", sc.data());
@@ -2079,6 +2170,7 @@ void Hierarchy::set_fine_interior_u(const double* host) {
     else if (I.p == 2) inject_up<2>(I, 0, fineD);
     else inject_up<3>(I, 0, fineD);
     HierarchyAccess::reset_pipeline(I);
+    I.fineDerived = false;
     TMG_CUDA(cudaStreamSynchronize(I.stream));
     cudaFree(tmp);
 }
@@ -2103,6 +2195,7 @@ void Hierarchy::set_random_initial_guess(std::uint64_t seed) {
         TMG_CUDA(cudaStreamSynchronize(I.stream));
     }
     HierarchyAccess::reset_pipeline(I);
+    I.fineDerived = false;
     TMG_CUDA(cudaStreamSynchronize(I.stream));
 }
 
@@ -2184,7 +2277,9 @@ void Hierarchy::unfold() {
     Problem p2 = old.prob;
     p2.levels = old.L + 1;
     if (p2.rhsLattice < 0) p2.rhsLattice = p2.levels;
-    if (old.vForm()) {  // the old finest level becomes a coarse level: back to (u, sc)
+    if (old.fineDerived) {  // the old finest level becomes a coarse level: (u, sc) with the derived u
+        old.split_fine(true);
+    } else if (old.vForm()) {  // back to (u, sc)
         const dev::Lvl& F = old.lv[old.L];
         dev::k_vform_to_u<<<old.blocks_for(F.n), 256, 0, old.stream>>>(F.u, F.sc, F.n);
         TMG_CUDA(cudaGetLastError());
