@@ -1232,6 +1232,8 @@ struct Hierarchy::Impl {
             for (int l = useChain ? top + 1 : 1; l < L; ++l)
                 fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
         }
+        // sc-free 3D fused pass (td-add): keep the level L-1 top-down values it prolongs (fused3::derive_u)
+        if (P == 3 && fused && !bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1));
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
         if (P == 2 && fused2on) {
             fused2::Args fa{};
@@ -1291,7 +1293,6 @@ struct Hierarchy::Impl {
             fused3::Args fa{};
             dev::Lvl& F = lv[L];
             fa.writeSc = bpx;  // td-add: the fine sc is re-derived on demand (fused3::derive_u)
-            if (!bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1));
             fa.uNew = uAlt;   // next v (v-form, fused3.cuh)
             fa.scNew = F.sc;  // write-only
             fa.b = F.chi;
