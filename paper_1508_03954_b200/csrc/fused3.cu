@@ -107,8 +107,9 @@ struct Smem {
                STAGES * sizeof(uint64_t);
     }
 };
-constexpr int NT = TX * TY;
+constexpr int NT = TX * TYT;  // threads per block
 
+#if TMG_F3_ROWS == 1
 #ifndef TMG_F3_MINB
 #define TMG_F3_MINB (TY <= 4 ? 6 : TY <= 8 ? 3 : 2)
 #endif
@@ -442,6 +443,351 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     dev::block_norms(nmax, nsum, a.norms);
 }
 
+#else  // TMG_F3_ROWS == 2: every thread two tile rows (y, y + 1) of the 32 x 16 tile
+
+#ifndef TMG_F3_MINB
+#define TMG_F3_MINB 2
+#endif
+// Same pass as the one-row kernel with twice the points per thread: the
+// in-plane sums of the two rows share their x-pair sums s_j = c(x-1) + c(x+1)
+// (rows y-1 .. y+2: 10 shared-memory loads for two points instead of 16), the
+// halo ring is 100 / 512 points instead of 84 / 256, and every warp carries
+// two independent points (more latency hiding per issue slot).
+template <bool BPX, class S>
+__global__ void __launch_bounds__(NT, TMG_F3_MINB)
+    k_fused3(const __grid_constant__ CUtensorMap mapU,
+             const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
+    using C = typename Cx<S>::T;
+    using M = Smem<C>;
+    dev::griddep_wait();
+    extern __shared__ __align__(128) unsigned char smem[];
+    constexpr int SB = M::template stage<BPX>();
+    unsigned char* ring = smem;
+    C* Vb = reinterpret_cast<C*>(smem + STAGES * SB);
+    C* Pb = Vb + (BPX ? 4 : 2) * M::kV;
+    C* tb = Pb + 2 * M::kP;                                      // [TY][TX] z-restricted columns
+    C* rb = tb + TX * TY;                                        // [TY][SX] x-restricted rows
+    uint64_t* bar = reinterpret_cast<uint64_t*>(rb + TY * SX);
+    auto tile = [&](int st) { return reinterpret_cast<const C*>(ring + st * SB); };
+    auto coarse = [&](int st) { return reinterpret_cast<const double2*>(ring + st * SB + M::kPlane); };
+
+    const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+    const int m = a.g.m, mc = a.g.mc;
+    const int bzg = blockIdx.z + a.chunkBase;
+    const int x0 = 1 + blockIdx.x * TX, y0 = 1 + blockIdx.y * TY, z0 = 1 + bzg * a.g.zc;
+    const int xe = min(x0 + TX, m), ye = min(y0 + TY, m), z1 = min(z0 + a.g.zc, m);
+    const int nplanes = z1 - z0 + 2;
+    const long long sy = a.n1, sz = static_cast<long long>(a.n1) * a.n1;
+    const int cx0 = (x0 - 1) / 3, cy0 = (y0 - 1) / 3;
+    constexpr unsigned stageBytes = M::kTileBytes + (BPX ? 2 : 1) * M::kCBytes;
+    constexpr int xScale = sizeof(C) / sizeof(S);
+
+    auto issue = [&](int stage, int zz) {
+        unsigned char* st = ring + stage * SB;
+        const int cz = min(zz / 3, mc - 1);
+        mbar_expect_tx(&bar[stage], stageBytes);
+        tma_load3(st, &mapU, xScale * (x0 - 1), y0 - 1, zz - a.tmaZ0, &bar[stage]);
+        tma_load3(st + M::kPlane, &mapC, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
+        if (BPX) tma_load3(st + M::kPlane + M::kC, &mapI, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
+    };
+
+    if (tid == 0) {
+        for (int s = 0; s < STAGES; ++s) mbar_init(&bar[s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (tid == 0)
+        for (int s = 0; s < STAGES && s < nplanes; ++s) issue(s, z0 - 1 + s);
+
+    // ---- per-thread constants ----
+    // Phase B tasks besides the own two points: the NV rows of the z/y-interpolated
+    // coarse plane (threads [0, NV)) and the NRING halo-ring points (threads
+    // [NV, NT) first, then threads [0, ...) a second task).
+    constexpr int NRING = 2 * HX + 2 * TY, NV = HY * CX;
+    static_assert(NV <= NT && NRING <= 2 * NT - NV, "phase-B tasks exceed two per thread");
+    const int x = x0 + tx;
+    const int yr0 = y0 + ROWS * ty;  // the thread's rows yr0, yr0 + 1
+    bool owned[2], cpxy[2];
+    int po[2], vo[2];
+    S wxo;
+    {
+        const int qx = min(x / 3, mc - 1);
+        wxo = third<S>(x - 3 * qx);
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const int y = yr0 + r;
+            owned[r] = x < xe && y < ye;
+            cpxy[r] = (x % 3 == 0) && (y % 3 == 0);
+            po[r] = (ROWS * ty + r + 1) * HX + (tx + 1);
+            vo[r] = (ROWS * ty + r + 1) * CX + (qx - cx0);
+        }
+    }
+    const int rk = tid >= NV ? tid - NV : (tid < NRING - (NT - NV) ? tid + (NT - NV) : -1);  // ring task
+    int pr = 0, vr = 0;
+    S wxr = 0;
+    bool pinr = false, cpr = false;
+    if (rk >= 0) {
+        int lx, ly;
+        if (rk < HX) { lx = rk; ly = 0; }
+        else if (rk < 2 * HX) { lx = rk - HX; ly = HY - 1; }
+        else if (rk < 2 * HX + TY) { lx = 0; ly = 1 + (rk - 2 * HX); }
+        else { lx = HX - 1; ly = 1 + (rk - 2 * HX - TY); }
+        const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
+        pinr = gx >= 1 && gx <= m - 1 && gy >= 1 && gy <= m - 1;
+        const int qx = min(max(gx, 0) / 3, mc - 1);
+        pr = ly * HX + lx;
+        vr = ly * CX + (qx - cx0);
+        wxr = third<S>(gx - 3 * qx);
+        cpr = (gx % 3 == 0) && (gy % 3 == 0);
+    }
+    const bool vtask = tid < NV;
+    int vcOff = 0;
+    double w1y = 0.0;
+    if (vtask) {
+        const int ly = tid / CX, ci = tid % CX;
+        const int gy = y0 - 1 + ly;
+        const int qy = min(max(gy, 0) / 3, mc - 1);
+        vcOff = (qy - cy0) * CX + ci;
+        w1y = third<double>(gy - 3 * qy);
+    }
+    auto computeV = [&](int stage, int zz, int vb) {
+        const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
+        const double w1z = third<double>(rz);
+        const double2* Cc = coarse(stage);
+        const double2 a0 = lerpw(Cc[vcOff], Cc[vcOff + CX], w1y);
+        const double2 a1 = lerpw(Cc[vcOff + CX * CY], Cc[vcOff + CX * CY + CX], w1y);
+        Vb[vb * M::kV + tid] = to_c(lerpw(a0, a1, w1z), C{});
+        if (BPX) {
+            const double2* I = Cc + M::kC / 16;
+            const double2 b0 = lerpw(I[vcOff], I[vcOff + CX], w1y);
+            const double2 b1 = lerpw(I[vcOff + CX * CY], I[vcOff + CX * CY + CX], w1y);
+            Vb[(2 + vb) * M::kV + tid] = to_c(lerpw(b0, b1, w1z), C{});
+        }
+    };
+
+    double nmax = 0.0, nsum = 0.0;
+    C accLo[2] = {zero<C>(), zero<C>()}, accHi[2] = {zero<C>(), zero<C>()};
+
+    const int Xa = x0 / 3, Xb = (xe + 1) / 3, Ya = y0 / 3, Yb = (ye + 1) / 3;
+    const int nsx = Xb - Xa + 1, nsy = Yb - Ya + 1;
+    const long long tileXY = blockIdx.x + static_cast<long long>(a.g.nbx) * blockIdx.y;
+    const long long tilesXY = static_cast<long long>(a.g.nbx) * a.g.nby;
+    double2* part = a.partial + (static_cast<long long>(bzg) * a.g.sz * tilesXY + tileXY) * (SY * SX);
+    const long long zStride = tilesXY * (SY * SX);
+    const int zBase = (z0 - 1) / 3;
+    int zLow = zBase;
+    const bool slotThread = tid < nsx * nsy;
+    const int sxi = slotThread ? tid % nsx : 0, syi = slotThread ? tid / nsx : 0;
+    auto wk = [](int k) { return static_cast<S>(k == 0 ? 1.0 : (k == 1 || k == -1) ? (2.0 / 3.0) : (1.0 / 3.0)); };
+    auto flushSlots = [&](int zi) {
+        __syncthreads();
+        if (slotThread) {
+            const int X = Xa + sxi, Y = Ya + syi;
+            C acc = zero<C>();
+#pragma unroll
+            for (int ky = -2; ky <= 2; ++ky) {
+                const int fy = 3 * Y + ky;
+                if (fy < y0 || fy >= ye) continue;
+                C row = zero<C>();
+#pragma unroll
+                for (int kx = -2; kx <= 2; ++kx) {
+                    const int fx = 3 * X + kx;
+                    if (fx < x0 || fx >= xe) continue;
+                    row = axpy(wk(kx), tb[(fy - y0) * TX + (fx - x0)], row);
+                }
+                acc = axpy(wk(ky), row, acc);
+            }
+            part[zi * zStride + syi * SX + sxi] = to_d(acc);
+        }
+    };
+    const int ti = NT - 1 - tid;
+    const int s1y = ti / nsx, s1x = ti - s1y * nsx;
+    auto stage1 = [&]() {
+        if (ti < TY * nsx && y0 + s1y < ye) {
+            const int X = Xa + s1x;
+            C row = zero<C>();
+#pragma unroll
+            for (int kx = -2; kx <= 2; ++kx) {
+                const int fx = 3 * X + kx;
+                if (fx < x0 || fx >= xe) continue;
+                row = axpy(wk(kx), tb[s1y * TX + (fx - x0)], row);
+            }
+            rb[s1y * SX + s1x] = row;
+        }
+    };
+    auto stage2 = [&](int zi) {
+        if (ti < nsx * nsy) {
+            const int Y = Ya + s1y;
+            C acc = zero<C>();
+#pragma unroll
+            for (int ky = -2; ky <= 2; ++ky) {
+                const int fy = 3 * Y + ky;
+                if (fy < y0 || fy >= ye) continue;
+                acc = axpy(wk(ky), rb[(fy - y0) * SX + s1x], acc);
+            }
+            part[zi * zStride + s1y * SX + s1x] = to_d(acc);
+        }
+    };
+    bool pend1 = false, pend2 = false;
+    int zi1 = 0, zi2 = 0;
+
+    const long long colBase = x + static_cast<long long>(yr0) * sy;  // row 0; row 1 is + sy
+    const C* bPtr = static_cast<const C*>(a.b) + colBase + static_cast<long long>(z0) * sz;
+    C* uPtr = static_cast<C*>(a.uNew) + colBase + static_cast<long long>(z0) * sz;
+    C* sPtr = static_cast<C*>(a.scNew) + colBase + static_cast<long long>(z0) * sz;
+    C bq[2];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) bq[r] = (owned[r] && z0 < z1) ? ld(bPtr + r * sy) : zero<C>();
+    const bool zeroSc = a.level < a.ellMin;
+    const C k0 = to_c(a.k.c[0], C{}), k1 = to_c(a.k.c[1], C{}), k2 = to_c(a.k.c[2], C{}), k3 = to_c(a.k.c[3], C{});
+    const C invDiag = to_c(a.k.invDiag, C{}), wRaw = to_c(a.k.wRaw, C{});
+
+    mbar_wait(&bar[0], 0);
+    if (vtask) computeV(0, z0 - 1, 0);
+    __syncthreads();
+
+    C Aprev[2] = {zero<C>(), zero<C>()}, Acur[2] = {zero<C>(), zero<C>()};
+    int stage = 0;
+    unsigned parity = 0;
+
+    auto step = [&](int it, auto U3) {
+        constexpr int u = decltype(U3)::value;  // zz % 3 == u
+        const int zz = z0 - 1 + it;
+        const bool hasNext = it + 1 < nplanes;
+        const int nstage = stage + 1 == STAGES ? 0 : stage + 1;
+        const unsigned nparity = stage + 1 == STAGES ? parity ^ 1u : parity;
+        mbar_wait(&bar[stage], parity);
+        if (hasNext) mbar_wait(&bar[nstage], nparity);
+        const bool zin = zz >= 1 && zz <= m - 1;
+        const C* Ut = tile(stage);
+        const C* V = Vb + (it & 1) * M::kV;
+        C* P = Pb + (it & 1) * M::kP;
+        // ---- phase B ----
+        C cOwn[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            C scv = lerpw(V[vo[r]], V[vo[r] + 1], wxo);
+            if (BPX && !(cpxy[r] && u == 0)) {
+                const C* Vi = Vb + (2 + (it & 1)) * M::kV;
+                scv = sub(scv, lerpw(Vi[vo[r]], Vi[vo[r] + 1], wxo));
+            }
+            cOwn[r] = (zin && owned[r]) ? add(Ut[po[r]], scv) : zero<C>();
+            P[po[r]] = cOwn[r];
+        }
+        if (rk >= 0) {
+            C scv = lerpw(V[vr], V[vr + 1], wxr);
+            if (BPX && !(cpr && u == 0)) {
+                const C* Vi = Vb + (2 + (it & 1)) * M::kV;
+                scv = sub(scv, lerpw(Vi[vr], Vi[vr + 1], wxr));
+            }
+            P[pr] = (zin && pinr) ? add(Ut[pr], scv) : zero<C>();
+        }
+        if (vtask && hasNext) computeV(nstage, zz + 1, (it + 1) & 1);
+        __syncthreads();
+        if (tid == 0 && it + STAGES < nplanes) issue(stage, zz + STAGES);
+        stage = nstage;
+        parity = nparity;
+        // ---- phase C ----
+        if (u == 1 && pend1) {
+            stage1();
+            pend1 = false;
+            pend2 = true;
+            zi2 = zi1;
+        } else if (u == 2 && pend2) {
+            stage2(zi2);
+            pend2 = false;
+        }
+        // rows y-1 .. y+2 around the thread's two points: x-pair sums s_j, centres
+        const C* c = P + ROWS * ty * HX + tx;  // row y-1, column x-1
+        C sj[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sj[j] = add(c[j * HX], c[j * HX + 2]);
+        const C mTop = c[1], mBot = c[3 * HX + 1];
+        const C E[2] = {add(sj[1], add(mTop, cOwn[1])), add(sj[2], add(cOwn[0], mBot))};
+        const C K[2] = {add(sj[0], sj[2]), add(sj[1], sj[3])};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            C T = mul(k1, cOwn[r]);
+            T = mac(T, k2, E[r]);
+            T = mac(T, k3, K[r]);
+            C Uo = mul(k0, cOwn[r]);
+            Uo = mac(Uo, k1, E[r]);
+            Uo = mac(Uo, k2, K[r]);
+            if (it >= 2) {
+                constexpr int kz = (u + 2) % 3;  // plane z = zz - 1
+                const C hu = add(Aprev[r], T);
+                const C res = owned[r] ? sub(bq[r], hu) : zero<C>();
+                if (owned[r] && zz < z1) bq[r] = ld(bPtr + sz + r * sy);
+                const S m2 = fma(res.x, res.x, res.y * res.y);
+                nmax = fmax(nmax, static_cast<double>(m2));
+                nsum += static_cast<double>(m2);
+                const C smooth = mul(res, invDiag);
+                const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpxy[r] && kz == 0, BPX ? 1 : 0, a.hb);
+                if (owned[r]) {
+                    if (a.writeSc) sPtr[r * sy] = scn;
+                    uPtr[r * sy] = add(Pb[((it + 1) & 1) * M::kP + po[r]], scn);
+                }
+                if (BPX && kz == 0 && a.level > a.ellMin && cpxy[r] && owned[r])
+                    a.sinextC[(x / 3) + a.n1c * (static_cast<long long>((yr0 + r) / 3) +
+                                                 static_cast<long long>(a.n1c) * ((zz - 1) / 3))] =
+                        to_d(mul(wRaw, smooth));
+                if (kz == 0) {
+                    accLo[r] = add(accLo[r], res);
+                } else if (kz == 1) {
+                    accLo[r] = axpy(static_cast<S>(2.0 / 3.0), res, accLo[r]);
+                    accHi[r] = axpy(static_cast<S>(1.0 / 3.0), res, accHi[r]);
+                } else {
+                    accLo[r] = axpy(static_cast<S>(1.0 / 3.0), res, accLo[r]);
+                    accHi[r] = axpy(static_cast<S>(2.0 / 3.0), res, accHi[r]);
+                    tb[(ROWS * ty + r) * TX + tx] = accLo[r];
+                    accLo[r] = accHi[r];
+                    accHi[r] = zero<C>();
+                }
+            }
+            Aprev[r] = add(Acur[r], Uo);
+            Acur[r] = T;
+        }
+        if (it >= 2) {
+            bPtr += sz;
+            sPtr += sz;
+            uPtr += sz;
+            if ((u + 2) % 3 == 2) {
+                pend1 = true;
+                zi1 = zLow - zBase;
+                ++zLow;
+            }
+        }
+    };
+    using U0 = std::integral_constant<int, 0>;
+    using U1 = std::integral_constant<int, 1>;
+    using U2 = std::integral_constant<int, 2>;
+    for (int it = 0; it < nplanes; it += 3) {
+        step(it, U0{});
+        if (it + 1 >= nplanes) break;
+        step(it + 1, U1{});
+        if (it + 2 >= nplanes) break;
+        step(it + 2, U2{});
+    }
+    __syncthreads();
+    if (pend1) {
+        stage1();
+        __syncthreads();
+        stage2(zi1);
+    } else if (pend2) {
+        stage2(zi2);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 2; ++r) tb[(ROWS * ty + r) * TX + tx] = accLo[r];
+    flushSlots(zLow - zBase);
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 2; ++r) tb[(ROWS * ty + r) * TX + tx] = accHi[r];
+    flushSlots(zLow + 1 - zBase);
+    dev::block_norms(nmax, nsum, a.norms);
+}
+#endif  // TMG_F3_ROWS
+
 // derive_u (fused3.cuh): phase B of k_fused3 for one point, from global memory
 template <class S>
 __global__ void __launch_bounds__(256) k_derive_u(const typename Cx<S>::T* __restrict__ vOld,
@@ -593,7 +939,7 @@ int resident_blocks(int smCount) {
     const size_t smem = smem_bytes(false);
     cudaFuncSetAttribute(k_fused3<false, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused3<false, double>, TX * TY, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused3<false, double>, NT, smem) != cudaSuccess ||
         per < 1)
         per = 3;
     return per * smCount;
@@ -607,7 +953,7 @@ void launch_one(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
     // launch (a host-side call, no device work) so a second device is configured too
     const size_t smem = smem_bytes(BPX, sizeof(S) == 4);
     cudaFuncSetAttribute(k_fused3<BPX, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    dev::launch_k(k_fused3<BPX, S>, grid, dim3(TX, TY), smem, s, mapU, mapC, mapI, a);
+    dev::launch_k(k_fused3<BPX, S>, grid, dim3(TX, TYT), smem, s, mapU, mapC, mapI, a);
 }
 }  // namespace
 

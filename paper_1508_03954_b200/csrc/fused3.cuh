@@ -41,7 +41,12 @@ namespace fused3 {
 #ifndef TMG_FUSED_STAGES
 #define TMG_FUSED_STAGES 4
 #endif
-constexpr int TX = 32, TY = TMG_FUSED_TY, STAGES = TMG_FUSED_STAGES;
+#ifndef TMG_F3_ROWS
+#define TMG_F3_ROWS 1
+#endif
+// TYT thread rows per block, each thread ROWS tile rows: TY = TYT * ROWS rows of points
+constexpr int ROWS = TMG_F3_ROWS, TYT = TMG_FUSED_TY;
+constexpr int TX = 32, TY = TYT * ROWS, STAGES = TMG_FUSED_STAGES;
 constexpr int HX = TX + 2, HY = TY + 2;
 constexpr int SX = TX / 3 + 3, SY = TY / 3 + 3;  // restriction slots per tile (upper bounds)
 constexpr int CX = (TX + 1) / 3 + 2, CY = (TY + 1) / 3 + 2;  // coarse tile feeding the prolongation
