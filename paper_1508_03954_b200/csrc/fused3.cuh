@@ -49,7 +49,9 @@ constexpr int ROWS = TMG_F3_ROWS, TYT = TMG_FUSED_TY;
 constexpr int TX = 32, TY = TYT * ROWS, STAGES = TMG_FUSED_STAGES;
 constexpr int HX = TX + 2, HY = TY + 2;
 constexpr int SX = TX / 3 + 3, SY = TY / 3 + 3;  // restriction slots per tile (upper bounds)
-constexpr int CX = (TX + 1) / 3 + 2, CY = (TY + 1) / 3 + 2;  // coarse tile feeding the prolongation
+// coarse tile feeding the prolongation: parents floor((o-1)/3) .. floor((o+T)/3) + 1 of a tile
+// [o, o+T) plus halo, for any tile origin o (T = TX or TY; 13 x 5 for 32 x 8, 13 x 8 for 32 x 16)
+constexpr int CX = (TX + 3) / 3 + 2, CY = (TY + 3) / 3 + 2;
 
 struct Geometry {
     int m;      // fine cells per axis (3^L)
