@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
             const double2 smooth = mul(r, a.k.invDiag);
             const double2 scn = zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
             if (owned) {
-                a.scNew[x + n1 * yr] = scn;
+                if (a.writeSc) a.scNew[x + n1 * yr] = scn;
                 a.uNew[x + n1 * yr] = add(cPrev, scn);  // next state v of row yr
             }
             if (BPX && kz == 0 && injectOK) a.sinextC[x / 3 + static_cast<long long>(a.n1c) * (yr / 3)] = mul(a.k.wRaw, smooth);
@@ -253,6 +253,31 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     __syncthreads();
     flush(zLow + 1 - zBase);
     dev::block_norms(nmax, nsum, a.norms);
+}
+
+// derive_u: k_fused2's phase B for one point, from global memory
+__global__ void __launch_bounds__(256) k_derive_u2(const double2* __restrict__ vOld, const double2* __restrict__ scTD,
+                                                   const double2* __restrict__ siTD, unsigned n1, unsigned n1c,
+                                                   unsigned fa, unsigned fb, double2* __restrict__ uOut) {
+    const int m = static_cast<int>(n1) - 1, mc = static_cast<int>(n1c) - 1;
+    for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
+        const int y = static_cast<int>(f / n1), x = static_cast<int>(f - static_cast<unsigned>(y) * n1);
+        if (x < 1 || x > m - 1 || y < 1 || y > m - 1) {
+            uOut[f] = zero2();
+            continue;
+        }
+        const int qx = min(x / 3, mc - 1), qy = min(y / 3, mc - 1);
+        const double w1y = relw(y - 3 * qy), wx = relw(x - 3 * qx);
+        auto prolong = [&](const double2* src) {  // computeV (y), then x
+            const double2* c = src + qx + static_cast<long long>(n1c) * qy;
+            const double2 v0 = lerpw(__ldg(c), __ldg(c + n1c), w1y);
+            const double2 v1 = lerpw(__ldg(c + 1), __ldg(c + 1 + n1c), w1y);
+            return lerpw(v0, v1, wx);
+        };
+        double2 scv = prolong(scTD);
+        if (siTD && !(x % 3 == 0 && y % 3 == 0)) scv = sub(scv, prolong(siTD));
+        uOut[f] = add(__ldg(vOld + f), scv);
+    }
 }
 
 template <bool SMOOTH>
@@ -324,6 +349,13 @@ int blocks(const Geometry& g) { return g.nbx * g.nby; }
 size_t smem_bytes(const Geometry& g, bool bpx) {
     (void)g;
     return (static_cast<size_t>(kRing) * (2 * TX + 2) + static_cast<size_t>(bpx ? 8 : 4) * CXW) * sizeof(double2);
+}
+
+void derive_u(const double2* vOld, const double2* scTD, const double2* siTD, unsigned n1, unsigned n1c, unsigned fa,
+              unsigned fb, double2* uOut, cudaStream_t s) {
+    if (fb <= fa) return;
+    const unsigned blocks = std::min<unsigned>((fb - fa + 255) / 256, 148u * 32u);
+    k_derive_u2<<<blocks, 256, 0, s>>>(vOld, scTD, siTD, n1, n1c, fa, fb, uOut);
 }
 
 void launch(const Args& a, cudaStream_t s) {

@@ -791,8 +791,9 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
 // derive_u (fused3.cuh): phase B of k_fused3 for one point, from global memory
 template <class S>
 __global__ void __launch_bounds__(256) k_derive_u(const typename Cx<S>::T* __restrict__ vOld,
-                                                  const double2* __restrict__ scTD, unsigned n1, unsigned n1c,
-                                                  unsigned fa, unsigned fb, double2* __restrict__ uOut) {
+                                                  const double2* __restrict__ scTD, const double2* __restrict__ siTD,
+                                                  unsigned n1, unsigned n1c, unsigned fa, unsigned fb,
+                                                  double2* __restrict__ uOut) {
     using C = typename Cx<S>::T;
     const int m = static_cast<int>(n1) - 1, mc = static_cast<int>(n1c) - 1;
     for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
@@ -805,15 +806,20 @@ __global__ void __launch_bounds__(256) k_derive_u(const typename Cx<S>::T* __res
         const int qx = min(x / 3, mc - 1), qy = min(y / 3, mc - 1), qz = min(z / 3, mc - 1);
         const double w1y = third<double>(y - 3 * qy), w1z = third<double>(z - 3 * qz);
         const long long sy = n1c, sz = static_cast<long long>(n1c) * n1c;
-        C V[2];
+        auto prolong = [&](const double2* src) {  // computeV (y, then z, in the kernel's precision), then x
+            C V[2];
 #pragma unroll
-        for (int dx = 0; dx < 2; ++dx) {  // computeV: y, then z, stored in the kernel's precision
-            const double2* c = scTD + (qx + dx) + sy * qy + sz * qz;
-            const double2 a0 = lerpw(ld(c), ld(c + sy), w1y);
-            const double2 a1 = lerpw(ld(c + sz), ld(c + sz + sy), w1y);
-            V[dx] = to_c(lerpw(a0, a1, w1z), C{});
-        }
-        const C scv = lerpw(V[0], V[1], third<S>(x - 3 * qx));  // phase B: x
+            for (int dx = 0; dx < 2; ++dx) {
+                const double2* c = src + (qx + dx) + sy * qy + sz * qz;
+                const double2 a0 = lerpw(ld(c), ld(c + sy), w1y);
+                const double2 a1 = lerpw(ld(c + sz), ld(c + sz + sy), w1y);
+                V[dx] = to_c(lerpw(a0, a1, w1z), C{});
+            }
+            return lerpw(V[0], V[1], third<S>(x - 3 * qx));
+        };
+        C scv = prolong(scTD);
+        // td-bpx: minus P si off the cPoints (phase B's `BPX && !(cpxy && u == 0)`)
+        if (siTD && !(x % 3 == 0 && y % 3 == 0 && z % 3 == 0)) scv = sub(scv, prolong(siTD));
         uOut[f] = to_d(add(ld(vOld + f), scv));
     }
 }
@@ -969,14 +975,15 @@ void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
     }
 }
 
-void derive_u(const void* vOld, const double2* scTD, unsigned n1, unsigned n1c, unsigned fa, unsigned fb,
-              double2* uOut, bool c64, cudaStream_t s) {
+void derive_u(const void* vOld, const double2* scTD, const double2* siTD, unsigned n1, unsigned n1c, unsigned fa,
+              unsigned fb, double2* uOut, bool c64, cudaStream_t s) {
     if (fb <= fa) return;
     const unsigned blocks = std::min<unsigned>((fb - fa + 255) / 256, 148u * 32u);
     if (c64)
-        k_derive_u<float><<<blocks, 256, 0, s>>>(static_cast<const float2*>(vOld), scTD, n1, n1c, fa, fb, uOut);
+        k_derive_u<float><<<blocks, 256, 0, s>>>(static_cast<const float2*>(vOld), scTD, siTD, n1, n1c, fa, fb, uOut);
     else
-        k_derive_u<double><<<blocks, 256, 0, s>>>(static_cast<const double2*>(vOld), scTD, n1, n1c, fa, fb, uOut);
+        k_derive_u<double><<<blocks, 256, 0, s>>>(static_cast<const double2*>(vOld), scTD, siTD, n1, n1c, fa, fb,
+                                                  uOut);
 }
 
 void combine(const Args& a, double2* rCoarse, int nblocks, cudaStream_t s, int za, int zb,

@@ -96,14 +96,15 @@ int blocks(const Geometry& g);
 // nz > 0: the map covers nz planes from `base` (a z-slab's allocated range)
 bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64 = false, int nz = 0);
 
-// The corrected fine iterate u = v_old + P sc_td(L-1) of the last fused pass,
-// re-derived with the kernel's own arithmetic (y, z, then x interpolation of the
-// complex128 coarse values; complex64 when c64) on the fine flat indices
-// [fa, fb); boundary points get 0.  vOld: the fine state the pass read,
-// scTD: the level L-1 top-down values it prolonged.  The fused pass then need
-// not store the write-only fine sc (16 of its 64 B per vertex): sc = v - u.
-void derive_u(const void* vOld, const double2* scTD, unsigned n1, unsigned n1c, unsigned fa, unsigned fb,
-              double2* uOut, bool c64, cudaStream_t s);
+// The corrected fine iterate u = v_old + P sc_td(L-1) (- P si(L-1) off the
+// cPoints, td-bpx) of the last fused pass, re-derived with the kernel's own
+// arithmetic (y, z, then x interpolation of the complex128 coarse values;
+// complex64 when c64) on the fine flat indices [fa, fb); boundary points get
+// 0.  vOld: the fine state the pass read, scTD / siTD: the level L-1 values it
+// prolonged (siTD null: td-add).  The fused pass then need not store the
+// write-only fine sc (16 of its 64 B per vertex): sc = v - u.
+void derive_u(const void* vOld, const double2* scTD, const double2* siTD, unsigned n1, unsigned n1c, unsigned fa,
+              unsigned fb, double2* uOut, bool c64, cudaStream_t s);
 
 // nchunks <= 0: all z-chunks (chunkBase must be 0)
 void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,

@@ -806,7 +806,8 @@ struct Hierarchy::Impl {
     // sc-free fine pass (3D fused td-add, fused3::derive_u): the level L-1 top-down values the
     // last pass prolonged (the planes of a slab), and whether the fine (u, sc) must be derived
     double2* scTD = nullptr;
-    bool fineDerived = false;
+    double2* siTD = nullptr;  // td-bpx: level L-1 si as the pass read it
+    bool fineDerived = false, derivedBpx = false;
     // z-slab member (prob.slabLo >= 0): allocated plane ranges [za, zb) of levels L and L-1
     int zaF = 0, zbF = 0, zaC = 0, zbC = 0;
     bool slab() const { return prob.slabLo >= 0; }
@@ -1232,8 +1233,8 @@ struct Hierarchy::Impl {
             for (int l = useChain ? top + 1 : 1; l < L; ++l)
                 fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
         }
-        // sc-free 3D fused pass (td-add): keep the level L-1 top-down values it prolongs (fused3::derive_u)
-        if (P == 3 && fused && !bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1));
+        // sc-free fused passes: keep the level L-1 values they prolong (fused3::derive_u)
+        if ((P == 3 && fused) || (P == 2 && fused2on)) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), bpx);
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
         if (P == 2 && fused2on) {
             fused2::Args fa{};
@@ -1258,12 +1259,15 @@ struct Hierarchy::Impl {
             fa.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
             fa.ellMin = prob.ellMin;
             fa.level = L;
+            fa.writeSc = 0;  // re-derived on demand (fused2::derive_u)
             fused2::launch(fa, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             if (use_up()) {  // combine + level L-1 smoothing, then the whole bottom-up in one launch
                 const fast::ResArgs sL = args(L - 1);
                 fused2::combine(fa, lv[L - 1].rhat, stream, &sL);
                 std::swap(F.u, uAlt);
+                fineDerived = true;
+                derivedBpx = bpx;
                 up_all(pol, n, fused2::blocks(geo2));
                 TMG_CUDA(cudaGetLastError());
                 coarseUStale = true;
@@ -1271,6 +1275,8 @@ struct Hierarchy::Impl {
             }
             fused2::combine(fa, lv[L - 1].rhat, stream);
             std::swap(F.u, uAlt);
+            fineDerived = true;
+            derivedBpx = bpx;
             for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
                 if (l < L - 1 && l >= prob.ellMin)
                     fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
@@ -1292,7 +1298,7 @@ struct Hierarchy::Impl {
         if (P == 3 && fused) {
             fused3::Args fa{};
             dev::Lvl& F = lv[L];
-            fa.writeSc = bpx;  // td-add: the fine sc is re-derived on demand (fused3::derive_u)
+            fa.writeSc = 0;  // the fine sc is re-derived on demand (fused3::derive_u)
             fa.uNew = uAlt;   // next v (v-form, fused3.cuh)
             fa.scNew = F.sc;  // write-only
             fa.b = F.chi;
@@ -1320,7 +1326,8 @@ struct Hierarchy::Impl {
                             (use_up() || lo <= L - 1) ? &sL : nullptr);
             std::swap(F.u, uAlt);
             std::swap(mapU[0], mapU[1]);
-            fineDerived = !bpx;
+            fineDerived = true;
+            derivedBpx = bpx;
             if (use_up()) {
                 up_all(pol, n, fused3::blocks(geo));
                 TMG_CUDA(cudaGetLastError());
@@ -1393,18 +1400,23 @@ struct Hierarchy::Impl {
     bool vForm() const { return prob.fast && (fused || fused2on); }
 
     // planes [za, zb) of level L-1's top-down sc, as the sc-free fused pass is about to read them
-    void save_coarse_td(int za, int zb) {
+    // planes (2D: rows) [za, zb) of level L-1's top-down sc (and si, td-bpx), as the
+    // sc-free fused pass is about to read them
+    void save_coarse_td(int za, int zb, bool bpx) {
         const dev::Lvl& C = lv[L - 1];
-        const long long plane = static_cast<long long>(C.n1) * C.n1;
-        if (zb > za)
-            TMG_CUDA(cudaMemcpyAsync(scTD + za * plane, C.sc + za * plane, static_cast<size_t>((zb - za) * plane) *
-                                     sizeof(double2), cudaMemcpyDeviceToDevice, stream));
+        const long long plane = p == 3 ? static_cast<long long>(C.n1) * C.n1 : C.n1;
+        const size_t bytes = static_cast<size_t>((zb - za) * plane) * sizeof(double2);
+        if (zb <= za) return;
+        TMG_CUDA(cudaMemcpyAsync(scTD + za * plane, C.sc + za * plane, bytes, cudaMemcpyDeviceToDevice, stream));
+        if (bpx) TMG_CUDA(cudaMemcpyAsync(siTD + za * plane, C.si + za * plane, bytes, cudaMemcpyDeviceToDevice, stream));
     }
 
     // the fine u of the last sc-free pass on the flat range [fa, fb) into out (global indices)
     void derive_fine_u(double2* out, unsigned fa, unsigned fb) {
         const dev::Lvl& F = lv[L];
-        fused3::derive_u(uAlt, scTD, F.n1, lv[L - 1].n1, fa, fb, out, prob.c64, stream);
+        const double2* si = derivedBpx ? siTD : nullptr;
+        if (p == 2) fused2::derive_u(uAlt, scTD, si, F.n1, lv[L - 1].n1, fa, fb, out, stream);
+        else fused3::derive_u(uAlt, scTD, si, F.n1, lv[L - 1].n1, fa, fb, out, prob.c64, stream);
         TMG_CUDA(cudaGetLastError());
     }
 
@@ -1750,6 +1762,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     if (I.fused2on) {
         I.uAlt = I.alloc<double2>(I.lv[I.L].n);
         I.partial2 = I.alloc<double2>(fused2::partial_count(I.geo2));
+        I.scTD = I.alloc<double2>(I.lv[I.L - 1].n);
+        I.siTD = I.alloc<double2>(I.lv[I.L - 1].n);
     }
     if (prob.fast) {
         const char* cz = std::getenv("TMG_CHAIN");
@@ -1787,6 +1801,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
             I.partial3 = I.alloc<double2>(fused3::partial_count(I.geo));
             const dev::Lvl& C = I.lv[I.L - 1];
             I.scTD = I.slab() ? I.alloc_planes<double2>(static_cast<long long>(C.n1) * C.n1, I.zaC, I.zbC)
+                              : I.alloc<double2>(C.n);
+            I.siTD = I.slab() ? I.alloc_planes<double2>(static_cast<long long>(C.n1) * C.n1, I.zaC, I.zbC)
                               : I.alloc<double2>(C.n);
             // slab members: maps over the allocated plane ranges, z coordinates shifted by the kernel
             const long long planeC = static_cast<long long>(C.n1) * C.n1;
