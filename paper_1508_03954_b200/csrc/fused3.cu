@@ -504,7 +504,8 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     // coarse plane (threads [0, NV)) and the NRING halo-ring points (threads
     // [NV, NT) first, then threads [0, ...) a second task).
     constexpr int NRING = 2 * HX + 2 * TY, NV = HY * CX;
-    static_assert(NV <= NT && NRING <= 2 * NT - NV, "phase-B tasks exceed two per thread");
+    static_assert(NV + NRING <= 2 * NT, "phase-B tasks exceed two per thread");
+    static_assert(NV <= NT || NV + NRING <= 2 * NT, "coarse-row tasks");
     const int x = x0 + tx;
     const int yr0 = y0 + ROWS * ty;  // the thread's rows yr0, yr0 + 1
     bool owned[2], cpxy[2];
@@ -522,7 +523,10 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
             vo[r] = (ROWS * ty + r + 1) * CX + (qx - cx0);
         }
     }
-    const int rk = tid >= NV ? tid - NV : (tid < NRING - (NT - NV) ? tid + (NT - NV) : -1);  // ring task
+    // task slots k = tid and tid + NT of [0, NV + NRING): k < NV a coarse row, else ring point k - NV
+    const int kb = tid + NT;
+    const int rk = tid >= NV ? tid - NV : (kb >= NV && kb < NV + NRING ? kb - NV : -1);  // ring task
+    const int vk2 = (NV > NT && kb < NV) ? kb : -1;  // a second coarse-row task (small blocks)
     int pr = 0, vr = 0;
     S wxr = 0;
     bool pinr = false, cpr = false;
@@ -541,27 +545,35 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
         cpr = (gx % 3 == 0) && (gy % 3 == 0);
     }
     const bool vtask = tid < NV;
-    int vcOff = 0;
-    double w1y = 0.0;
-    if (vtask) {
-        const int ly = tid / CX, ci = tid % CX;
+    int vcOff[2] = {0, 0};
+    double w1y[2] = {0.0, 0.0};
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int k = j == 0 ? tid : vk2;
+        if (k < 0 || (j == 0 && !vtask)) continue;
+        const int ly = k / CX, ci = k % CX;
         const int gy = y0 - 1 + ly;
         const int qy = min(max(gy, 0) / 3, mc - 1);
-        vcOff = (qy - cy0) * CX + ci;
-        w1y = third<double>(gy - 3 * qy);
+        vcOff[j] = (qy - cy0) * CX + ci;
+        w1y[j] = third<double>(gy - 3 * qy);
     }
     auto computeV = [&](int stage, int zz, int vb) {
         const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
         const double w1z = third<double>(rz);
         const double2* Cc = coarse(stage);
-        const double2 a0 = lerpw(Cc[vcOff], Cc[vcOff + CX], w1y);
-        const double2 a1 = lerpw(Cc[vcOff + CX * CY], Cc[vcOff + CX * CY + CX], w1y);
-        Vb[vb * M::kV + tid] = to_c(lerpw(a0, a1, w1z), C{});
-        if (BPX) {
-            const double2* I = Cc + M::kC / 16;
-            const double2 b0 = lerpw(I[vcOff], I[vcOff + CX], w1y);
-            const double2 b1 = lerpw(I[vcOff + CX * CY], I[vcOff + CX * CY + CX], w1y);
-            Vb[(2 + vb) * M::kV + tid] = to_c(lerpw(b0, b1, w1z), C{});
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            if (j == 0 ? !vtask : vk2 < 0) continue;
+            const int o = vcOff[j], slot = j == 0 ? tid : vk2;
+            const double2 a0 = lerpw(Cc[o], Cc[o + CX], w1y[j]);
+            const double2 a1 = lerpw(Cc[o + CX * CY], Cc[o + CX * CY + CX], w1y[j]);
+            Vb[vb * M::kV + slot] = to_c(lerpw(a0, a1, w1z), C{});
+            if (BPX) {
+                const double2* I = Cc + M::kC / 16;
+                const double2 b0 = lerpw(I[o], I[o + CX], w1y[j]);
+                const double2 b1 = lerpw(I[o + CX * CY], I[o + CX * CY + CX], w1y[j]);
+                Vb[(2 + vb) * M::kV + slot] = to_c(lerpw(b0, b1, w1z), C{});
+            }
         }
     };
 
@@ -643,7 +655,7 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     const C invDiag = to_c(a.k.invDiag, C{}), wRaw = to_c(a.k.wRaw, C{});
 
     mbar_wait(&bar[0], 0);
-    if (vtask) computeV(0, z0 - 1, 0);
+    computeV(0, z0 - 1, 0);
     __syncthreads();
 
     C Aprev[2] = {zero<C>(), zero<C>()}, Acur[2] = {zero<C>(), zero<C>()};
@@ -682,7 +694,7 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
             }
             P[pr] = (zin && pinr) ? add(Ut[pr], scv) : zero<C>();
         }
-        if (vtask && hasNext) computeV(nstage, zz + 1, (it + 1) & 1);
+        if (hasNext) computeV(nstage, zz + 1, (it + 1) & 1);
         __syncthreads();
         if (tid == 0 && it + STAGES < nplanes) issue(stage, zz + STAGES);
         stage = nstage;
