@@ -87,8 +87,8 @@ def lattice(level, dim):
 def fine_bytes_per_vertex(w, precision):
     """Algorithmic HBM bytes per fine vertex of the fine pass, SURVEY §8(d):
     80 B (u, sc, b read; u, sc written) -- the basis of roofline.achieved.  The
-    fused fast passes move less for the same work (v-form, fused3.cuh:
-    v, b read, v, sc written = 64 B); the exact pass is not fused (176 B)."""
+    fused fast passes move less for the same work (v-form, fused3.cuh: v, b
+    read, v written = 48 B); the exact pass is not fused (176 B)."""
     if precision == "exact":
         return 176
     if precision == "fast-complex64":  # SURVEY §8(d): complex64 halves B
@@ -97,12 +97,14 @@ def fine_bytes_per_vertex(w, precision):
 
 
 def moved_bytes_per_vertex(w, precision):
-    """Bytes per fine vertex the implementation's fine pass actually has to move."""
+    """Bytes per fine vertex the implementation's fine pass actually has to move:
+    the fused passes read v and b and write v (v-form, the write-only fine sc is
+    re-derived on demand: fused3.cuh derive_u) -- 48 B, 24 B in complex64."""
     if precision == "exact":
         return 176
     if precision == "fast-complex64":
-        return 32
-    return 64 if w["dim"] >= 2 else 128
+        return 24
+    return 48 if w["dim"] >= 2 else 128
 
 
 def algorithmic_bytes(w, precision):

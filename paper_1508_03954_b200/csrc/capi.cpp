@@ -337,8 +337,8 @@ treemg_status tmg_slabs_e2e_step(tmg_slabs* h, const tmg_policy* pol, int n, con
 treemg_status tmg_slab_plan(int levels, int world, int* out8) {
     if (!out8) return fail(TREEMG_E_USAGE, "null argument");
     return guarded([&] {
-        // the chunking the live device runs (co-resident fused blocks); 3 x 148 without a GPU
-        int ndev = 0, resident = 3 * 148;
+        // the chunking the live device runs (co-resident fused blocks); 4 x 148 without a GPU
+        int ndev = 0, resident = 4 * 148;
         if (cudaGetDeviceCount(&ndev) == cudaSuccess && ndev > 0) {
             int dev = 0, sms = 148;
             cudaGetDevice(&dev);

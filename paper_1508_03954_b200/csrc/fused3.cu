@@ -446,7 +446,7 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
 #else  // TMG_F3_ROWS == 2: every thread two tile rows (y, y + 1) of the 32 x 16 tile
 
 #ifndef TMG_F3_MINB
-#define TMG_F3_MINB 2
+#define TMG_F3_MINB (TYT <= 4 ? 4 : 2)
 #endif
 // Same pass as the one-row kernel with twice the points per thread: the
 // in-plane sums of the two rows share their x-pair sums s_j = c(x-1) + c(x+1)

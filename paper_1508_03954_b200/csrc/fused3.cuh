@@ -35,14 +35,18 @@
 namespace tmg {
 namespace fused3 {
 
+// thread rows per block (TMG_FUSED_TY) x rows per thread (TMG_F3_ROWS): the
+// default 4 x 2 = a 32 x 8 tile on 128 threads, 4 blocks per SM (measured
+// against 8 x 1 on 256 threads, the round-1 kernel: -4 % fine-pass time at
+// 729^3, -3 % at 243^3; 8 x 2 = 32 x 16: -6 % / +3 %)
 #ifndef TMG_FUSED_TY
-#define TMG_FUSED_TY 8
+#define TMG_FUSED_TY 4
 #endif
 #ifndef TMG_FUSED_STAGES
 #define TMG_FUSED_STAGES 4
 #endif
 #ifndef TMG_F3_ROWS
-#define TMG_F3_ROWS 1
+#define TMG_F3_ROWS 2
 #endif
 // TYT thread rows per block, each thread ROWS tile rows: TY = TYT * ROWS rows of points
 constexpr int ROWS = TMG_F3_ROWS, TYT = TMG_FUSED_TY;
@@ -84,7 +88,7 @@ struct Args {
 
 // Tile / z-chunk geometry; the chunk count is a multiple of `parts` (z-slabs:
 // every rank gets the same number of chunks) where the lattice allows it.
-Geometry geometry(int m, int mc, int parts = 1, int resident = 3 * 148);
+Geometry geometry(int m, int mc, int parts = 1, int resident = 4 * 148);
 int resident_blocks(int smCount);  // co-resident k_fused3 blocks on the device
 size_t partial_count(const Geometry& g);
 size_t smem_bytes(bool bpx, bool c64 = false);

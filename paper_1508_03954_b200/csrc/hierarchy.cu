@@ -801,7 +801,7 @@ struct Hierarchy::Impl {
 #define TMG_CHAIN_MAXN (1u << 16)
 #endif
     static constexpr unsigned kChainMaxN = TMG_CHAIN_MAXN;  // levels below this size join the chain
-    int fusedResident = 3 * 148;
+    int fusedResident = 4 * 148;  // replaced by fused3::resident_blocks at construction
     bool fineFused = false;  // the fine level runs a fused pass (decided before allocation)
     // sc-free fine pass (3D fused td-add, fused3::derive_u): the level L-1 top-down values the
     // last pass prolonged (the planes of a slab), and whether the fine (u, sc) must be derived

@@ -201,7 +201,7 @@ class SlabGroup {
     std::unique_ptr<State> st_;
 };
 
-std::vector<std::array<int, 8>> slab_plan(int levels, int world, int resident = 3 * 148);
+std::vector<std::array<int, 8>> slab_plan(int levels, int world, int resident = 4 * 148);
 // co-resident blocks of the 3D fused fine pass on the current device (the chunking input of slab_plan)
 int fused3_resident_blocks(int smCount);
 
