@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx, unsigne
         if (FINE) {
             c.u[f] = add(c.u[f], sc);  // sf is identically zero on the finest level
         } else {
-            c.sc[f] = sc;
+            (c.scOut ? c.scOut : c.sc)[f] = sc;
         }
     }
 }
@@ -158,7 +158,7 @@ __global__ void __launch_bounds__(256) k_topdown_tri(Lvl c, Lvl pr, int bpx, uns
                 sc = sub(sc, w[0]);
             }
             if (FINE) c.u[f] = add(own[k], sc);
-            else c.sc[f] = sc;
+            else (c.scOut ? c.scOut : c.sc)[f] = sc;
         }
     }
 }
@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(kRowThreads) k_topdown3_rows(Lvl c, Lvl pr, in
     }
     __syncthreads();
     const bool cpyz = (y % 3 == 0) && (z % 3 == 0);
-    double2* row = c.sc + c.n1 * (static_cast<unsigned>(y) + c.n1 * static_cast<unsigned>(z));
+    const size_t rowOff = c.n1 * (static_cast<unsigned>(y) + c.n1 * static_cast<unsigned>(z));
+    const double2* row = c.sc + rowOff;
+    double2* out = (c.scOut ? c.scOut : c.sc) + rowOff;
     for (int x = 1 + threadIdx.x; x <= m - 1; x += blockDim.x) {
         const int qx = min(x / 3, mcp - 1), rx = x - 3 * qx;
         auto pro = [&](const double2* R) {
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(kRowThreads) k_topdown3_rows(Lvl c, Lvl pr, in
         };
         double2 sc = add(row[x], pro(rs));
         if (bpx && !(cpyz && x % 3 == 0)) sc = sub(sc, pro(rs + 4 * pn1));
-        row[x] = sc;
+        out[x] = sc;
     }
 }
 
@@ -616,7 +618,7 @@ __global__ void __launch_bounds__(kPyrTX* kPyrTY) k_topdown_pyr(const PyrArgs a)
         fo[k] = in ? static_cast<unsigned>(gx) + static_cast<unsigned>(LT.n1) *
                          (static_cast<unsigned>(gy) + static_cast<unsigned>(LT.n1) * static_cast<unsigned>(gz))
                    : 0xffffffffu;
-        own[k] = in ? ld(a.scT + fo[k]) : make_double2(0.0, 0.0);
+        own[k] = in ? ld(a.scTin + fo[k]) : make_double2(0.0, 0.0);
     }
     // (2) every ancestor box's sc (and si) into shared memory, all copies in flight at once
     for (int l = 0; l < T; ++l) {

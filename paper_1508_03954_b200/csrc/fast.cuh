@@ -99,7 +99,8 @@ struct PyrLevel {
 };
 struct PyrArgs {
     PyrLevel lv[kPyrMaxLevels];
-    double2* scT;         // level T sc, updated in place
+    double2* scT;         // level T top-down output (== scTin: in place)
+    const double2* scTin; // level T staged sc
     int T, bpx;
     int bz;               // points per thread (tile extent along the last axis / rows / 8)
     int nbx, nby;         // tiles along axes 0, 1

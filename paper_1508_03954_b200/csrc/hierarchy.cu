@@ -1226,15 +1226,22 @@ struct Hierarchy::Impl {
         const bool useChain = top >= 1;
         fast::ChainArgs ch{};
         if (useChain) ch = make_chain(pol, n, top);
+        // the fused passes read level L-1's top-down values from scTD (written there
+        // directly; the staged sc stays in place), and td-bpx's si from siTD:
+        // both are what fused3::derive_u / fused2::derive_u re-read later
+        const bool toTD = (P == 3 && fused) || (P == 2 && fused2on);
         if (use_pyramid()) {
-            topdown_all(bpx);
+            topdown_all(bpx, -1, toTD ? scTD : nullptr);
         } else {
             if (useChain) fast::chain_down(P, ch, ch.cluster ? clusterSize : chainGrid, stream);
-            for (int l = useChain ? top + 1 : 1; l < L; ++l)
-                fast::topdown_coarse(P, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+            for (int l = useChain ? top + 1 : 1; l < L; ++l) {
+                dev::Lvl c = lv[l];
+                if (l == L - 1 && toTD) c.scOut = scTD;
+                fast::topdown_coarse(P, c, lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+            }
+            if (toTD && useChain && top == L - 1) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), false, true);
         }
-        // sc-free fused passes: keep the level L-1 values they prolong (fused3::derive_u)
-        if ((P == 3 && fused) || (P == 2 && fused2on)) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), bpx);
+        if (toTD && bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), true, false);
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
         if (P == 2 && fused2on) {
             fused2::Args fa{};
@@ -1244,7 +1251,7 @@ struct Hierarchy::Impl {
             fa.u = F.u;
             fa.sc = F.sc;
             fa.b = F.chi;
-            fa.scC = lv[L - 1].sc;
+            fa.scC = scTD;  // level L-1 top-down values
             fa.siC = lv[L - 1].si;
             fa.sinextC = lv[L - 1].sinext;
             fa.partial = partial2;
@@ -1302,7 +1309,7 @@ struct Hierarchy::Impl {
             fa.uNew = uAlt;   // next v (v-form, fused3.cuh)
             fa.scNew = F.sc;  // write-only
             fa.b = F.chi;
-            fa.scC = lv[L - 1].sc;
+            fa.scC = scTD;  // level L-1 top-down values (read through mapC)
             fa.siC = lv[L - 1].si;
             fa.sinextC = lv[L - 1].sinext;
             fa.partial = partial3;
@@ -1400,15 +1407,16 @@ struct Hierarchy::Impl {
     bool vForm() const { return prob.fast && (fused || fused2on); }
 
     // planes [za, zb) of level L-1's top-down sc, as the sc-free fused pass is about to read them
-    // planes (2D: rows) [za, zb) of level L-1's top-down sc (and si, td-bpx), as the
-    // sc-free fused pass is about to read them
-    void save_coarse_td(int za, int zb, bool bpx) {
+    // planes (2D: rows) [za, zb) of level L-1's si (td-bpx) and / or top-down sc as
+    // the sc-free fused pass is about to read them (sc: only where the top-down
+    // ran in place -- the coarse chains)
+    void save_coarse_td(int za, int zb, bool si, bool sc) {
         const dev::Lvl& C = lv[L - 1];
         const long long plane = p == 3 ? static_cast<long long>(C.n1) * C.n1 : C.n1;
         const size_t bytes = static_cast<size_t>((zb - za) * plane) * sizeof(double2);
         if (zb <= za) return;
-        TMG_CUDA(cudaMemcpyAsync(scTD + za * plane, C.sc + za * plane, bytes, cudaMemcpyDeviceToDevice, stream));
-        if (bpx) TMG_CUDA(cudaMemcpyAsync(siTD + za * plane, C.si + za * plane, bytes, cudaMemcpyDeviceToDevice, stream));
+        if (sc) TMG_CUDA(cudaMemcpyAsync(scTD + za * plane, C.sc + za * plane, bytes, cudaMemcpyDeviceToDevice, stream));
+        if (si) TMG_CUDA(cudaMemcpyAsync(siTD + za * plane, C.si + za * plane, bytes, cudaMemcpyDeviceToDevice, stream));
     }
 
     // the fine u of the last sc-free pass on the flat range [fa, fb) into out (global indices)
@@ -1508,7 +1516,9 @@ struct Hierarchy::Impl {
     }
     // levels 1 .. last-1 (default: every coarse level); the slab path passes
     // last = L-1 (level L-1 is sharded and done per plane range)
-    void topdown_all(int bpx, int last = -1) {
+    // outL1: level L-1's top-down values go there instead of in place (the fused
+    // passes read them from scTD: the staged sc stays, nothing to save)
+    void topdown_all(int bpx, int last = -1, double2* outL1 = nullptr) {
         if (last < 0) last = L;
         fast::PyrArgs a{};
         const int T = std::min(pyramid_top(), last - 1);
@@ -1518,11 +1528,16 @@ struct Hierarchy::Impl {
             a.lv[l].m = static_cast<int>(lv[l].m);
             a.lv[l].n1 = static_cast<int>(lv[l].n1);
         }
-        a.scT = lv[T].sc;
+        a.scTin = lv[T].sc;
+        a.scT = (T == L - 1 && outL1) ? outL1 : lv[T].sc;
         a.bpx = bpx;
         const size_t smem = fast::pyramid_setup(p, a, T);
         fast::topdown_pyramid(p, a, smem, stream);
-        for (int l = T + 1; l < last; ++l) fast::topdown_coarse(p, lv[l], lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+        for (int l = T + 1; l < last; ++l) {
+            dev::Lvl c = lv[l];
+            if (l == L - 1) c.scOut = outL1;
+            fast::topdown_coarse(p, c, lv[l - 1], bpx, blocks_for(lv[l].n), stream);
+        }
     }
 
     // highest level <= maxLevel of the coarse chain (every level below kChainMaxN
@@ -1811,7 +1826,7 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
             const long long offF = I.slab() ? plane * I.zaF : 0, offC = I.slab() ? planeC * I.zaC : 0;
             bool ok = fused3::encode_map(&I.mapU[0], F.u + offF, F.n1, 0, prob.c64, nzF) &&
                       fused3::encode_map(&I.mapU[1], I.uAlt + offF, F.n1, 0, prob.c64, nzF) &&
-                      fused3::encode_map(&I.mapC, C.sc + offC, C.n1, 2, false, nzC) &&
+                      fused3::encode_map(&I.mapC, I.scTD + offC, C.n1, 2, false, nzC) &&
                       fused3::encode_map(&I.mapI, C.si + offC, C.n1, 2, false, nzC);
             if (!ok) throw CudaError("cuTensorMapEncodeTiled failed for the fused fine pass");
             I.fused = true;

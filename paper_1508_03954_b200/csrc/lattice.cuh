@@ -82,6 +82,7 @@ struct Lvl {
     double2* uhat;
     double2* rhat;
     double2* r;  // optional debug copy of the residual
+    double2* scOut;  // coarse top-down output (null: in place into sc; the fused passes' level L-1)
     unsigned m;   // 3^l
     unsigned n1;  // 3^l + 1
     unsigned n;   // (3^l+1)^p
