@@ -1239,9 +1239,9 @@ struct Hierarchy::Impl {
                 if (l == L - 1 && toTD) c.scOut = scTD;
                 fast::topdown_coarse(P, c, lv[l - 1], bpx, blocks_for(lv[l].n), stream);
             }
-            if (toTD && useChain && top == L - 1) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), false, true);
+            if (toTD && useChain && top == L - 1) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), false, true);  // in place
         }
-        if (toTD && bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), true, false);
+        if (P == 3 && fused && bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), true, false);
         if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
         if (P == 2 && fused2on) {
             fused2::Args fa{};
@@ -1266,15 +1266,15 @@ struct Hierarchy::Impl {
             fa.hb = (pol.hbMask && !pol.bpx) ? 1 : 0;
             fa.ellMin = prob.ellMin;
             fa.level = L;
-            fa.writeSc = 0;  // re-derived on demand (fused2::derive_u)
+            // the 2D pass is bound by its per-row barrier, not by HBM: it keeps the
+            // stored fine sc (no derive, no si copy for td-bpx)
+            fa.writeSc = 1;
             fused2::launch(fa, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             if (use_up()) {  // combine + level L-1 smoothing, then the whole bottom-up in one launch
                 const fast::ResArgs sL = args(L - 1);
                 fused2::combine(fa, lv[L - 1].rhat, stream, &sL);
                 std::swap(F.u, uAlt);
-                fineDerived = true;
-                derivedBpx = bpx;
                 up_all(pol, n, fused2::blocks(geo2));
                 TMG_CUDA(cudaGetLastError());
                 coarseUStale = true;
@@ -1282,8 +1282,6 @@ struct Hierarchy::Impl {
             }
             fused2::combine(fa, lv[L - 1].rhat, stream);
             std::swap(F.u, uAlt);
-            fineDerived = true;
-            derivedBpx = bpx;
             for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
                 if (l < L - 1 && l >= prob.ellMin)
                     fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
