@@ -89,36 +89,48 @@ __device__ __forceinline__ void tma_load3(void* dst, const CUtensorMap* map, int
         : "memory");
 }
 
+// Kernel shape: R rows of points per thread (fused3.cuh).
+template <int R>
+struct Cfg {
+    static constexpr int TYT = TY / R;                 // thread rows
+    static constexpr int NT = TX * TYT;                // threads per block
+    static constexpr int STAGES = R == 2 ? 3 : 4;      // ring depth (R = 2 stages carry a b tile too)
+    static constexpr int MINB = R == 2 ? 4 : 3;        // blocks per SM
+    static_assert(TY % R == 0, "tile height");
+};
+
 // Shared-memory carve-up (bytes; every TMA destination 128-byte aligned).
 // C = the kernel's complex type (16 B complex128 or 8 B complex64).
-template <class C>
+template <class C, int R>
 struct Smem {
+    static constexpr int STAGES = Cfg<R>::STAGES;
     static constexpr int kPlane = (HX * HY * static_cast<int>(sizeof(C)) + 127) / 128 * 128;  // halo'd fine tile
     static constexpr unsigned kTileBytes = HX * HY * sizeof(C);
     static constexpr int kC = (CX * CY * 2 * 16 + 127) / 128 * 128;  // two complex128 coarse planes
     static constexpr unsigned kCBytes = CX * CY * 2 * sizeof(double2);
     static constexpr int kV = (HY * CX + 7) / 8 * 8;  // z- and y-interpolated coarse rows (elements of C)
     static constexpr int kP = (HX * HY + 7) / 8 * 8;  // corrected plane (elements of C)
+    // R = 2: the b tile of the plane the step's residual is for (32 x TY, no halo), TMA'd with the stage
+    static constexpr int kBt = R == 2 ? (TX * TY * static_cast<int>(sizeof(C)) + 127) / 128 * 128 : 0;
+    static constexpr unsigned kBtBytes = R == 2 ? TX * TY * sizeof(C) : 0;
     template <bool BPX>
-    __host__ __device__ static constexpr int stage() { return kPlane + (BPX ? 2 : 1) * kC; }
+    __host__ __device__ static constexpr int stage() { return kPlane + (BPX ? 2 : 1) * kC + kBt; }
     template <bool BPX>
     __host__ __device__ static constexpr size_t bytes() {
         return STAGES * stage<BPX>() + ((BPX ? 4 : 2) * kV + 2 * kP + TX * TY + TY * SX) * sizeof(C) +
                STAGES * sizeof(uint64_t);
     }
 };
-constexpr int NT = TX * TYT;  // threads per block
 
-#if TMG_F3_ROWS == 1
-#ifndef TMG_F3_MINB
-#define TMG_F3_MINB (TY <= 4 ? 6 : TY <= 8 ? 3 : 2)
-#endif
+// One point per thread (the round-1 shape; the complex64 kernel).
 template <bool BPX, class S>
-__global__ void __launch_bounds__(NT, TMG_F3_MINB)
-    k_fused3(const __grid_constant__ CUtensorMap mapU,
-             const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
+__global__ void __launch_bounds__(Cfg<1>::NT, Cfg<1>::MINB)
+    k_fused3_r1(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapC,
+                const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapB, const Args a) {
     using C = typename Cx<S>::T;
-    using M = Smem<C>;
+    using M = Smem<C, 1>;
+    constexpr int NT = Cfg<1>::NT, STAGES = Cfg<1>::STAGES;
+    (void)mapB;
     dev::griddep_wait();
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int SB = M::template stage<BPX>();                 // stage stride, bytes
@@ -443,22 +455,19 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     dev::block_norms(nmax, nsum, a.norms);
 }
 
-#else  // TMG_F3_ROWS == 2: every thread two tile rows (y, y + 1) of the 32 x 16 tile
-
-#ifndef TMG_F3_MINB
-#define TMG_F3_MINB (TYT <= 4 ? 4 : 2)
-#endif
+// Two rows per thread (rows y, y + 1 of the 32 x TY tile; the complex128 kernel).
 // Same pass as the one-row kernel with twice the points per thread: the
 // in-plane sums of the two rows share their x-pair sums s_j = c(x-1) + c(x+1)
 // (rows y-1 .. y+2: 10 shared-memory loads for two points instead of 16), the
 // halo ring is 100 / 512 points instead of 84 / 256, and every warp carries
 // two independent points (more latency hiding per issue slot).
 template <bool BPX, class S>
-__global__ void __launch_bounds__(NT, TMG_F3_MINB)
-    k_fused3(const __grid_constant__ CUtensorMap mapU,
-             const __grid_constant__ CUtensorMap mapC, const __grid_constant__ CUtensorMap mapI, const Args a) {
+__global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
+    k_fused3_r2(const __grid_constant__ CUtensorMap mapU, const __grid_constant__ CUtensorMap mapC,
+                const __grid_constant__ CUtensorMap mapI, const __grid_constant__ CUtensorMap mapB, const Args a) {
     using C = typename Cx<S>::T;
-    using M = Smem<C>;
+    using M = Smem<C, 2>;
+    constexpr int NT = Cfg<2>::NT, STAGES = Cfg<2>::STAGES, ROWS = 2;
     dev::griddep_wait();
     extern __shared__ __align__(128) unsigned char smem[];
     constexpr int SB = M::template stage<BPX>();
@@ -479,9 +488,12 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     const int nplanes = z1 - z0 + 2;
     const long long sy = a.n1, sz = static_cast<long long>(a.n1) * a.n1;
     const int cx0 = (x0 - 1) / 3, cy0 = (y0 - 1) / 3;
-    constexpr unsigned stageBytes = M::kTileBytes + (BPX ? 2 : 1) * M::kCBytes;
+    constexpr unsigned stageBytes = M::kTileBytes + (BPX ? 2 : 1) * M::kCBytes + M::kBtBytes;
     constexpr int xScale = sizeof(C) / sizeof(S);
+    constexpr int kBtOff = M::kPlane + (BPX ? 2 : 1) * M::kC;
 
+    // stage of plane zz: the halo'd v tile, the coarse planes, and b of plane zz - 1
+    // (the plane this step's residual is for; out-of-range planes land as zeros)
     auto issue = [&](int stage, int zz) {
         unsigned char* st = ring + stage * SB;
         const int cz = min(zz / 3, mc - 1);
@@ -489,6 +501,7 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
         tma_load3(st, &mapU, xScale * (x0 - 1), y0 - 1, zz - a.tmaZ0, &bar[stage]);
         tma_load3(st + M::kPlane, &mapC, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
         if (BPX) tma_load3(st + M::kPlane + M::kC, &mapI, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
+        tma_load3(st + kBtOff, &mapB, xScale * x0, y0, zz - 1 - a.tmaZ0, &bar[stage]);
     };
 
     if (tid == 0) {
@@ -644,12 +657,9 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     int zi1 = 0, zi2 = 0;
 
     const long long colBase = x + static_cast<long long>(yr0) * sy;  // row 0; row 1 is + sy
-    const C* bPtr = static_cast<const C*>(a.b) + colBase + static_cast<long long>(z0) * sz;
     C* uPtr = static_cast<C*>(a.uNew) + colBase + static_cast<long long>(z0) * sz;
     C* sPtr = static_cast<C*>(a.scNew) + colBase + static_cast<long long>(z0) * sz;
-    C bq[2];
-#pragma unroll
-    for (int r = 0; r < 2; ++r) bq[r] = (owned[r] && z0 < z1) ? ld(bPtr + r * sy) : zero<C>();
+    C bq[2];  // b of the step's residual plane, from the stage's b tile
     const bool zeroSc = a.level < a.ellMin;
     const C k0 = to_c(a.k.c[0], C{}), k1 = to_c(a.k.c[1], C{}), k2 = to_c(a.k.c[2], C{}), k3 = to_c(a.k.c[3], C{});
     const C invDiag = to_c(a.k.invDiag, C{}), wRaw = to_c(a.k.wRaw, C{});
@@ -674,6 +684,11 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
         const C* Ut = tile(stage);
         const C* V = Vb + (it & 1) * M::kV;
         C* P = Pb + (it & 1) * M::kP;
+        {  // b of plane zz - 1, read before the stage is refilled
+            const C* Bt = reinterpret_cast<const C*>(ring + stage * SB + kBtOff);
+#pragma unroll
+            for (int r = 0; r < 2; ++r) bq[r] = Bt[(ROWS * ty + r) * TX + tx];
+        }
         // ---- phase B ----
         C cOwn[2];
 #pragma unroll
@@ -729,7 +744,6 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
                 constexpr int kz = (u + 2) % 3;  // plane z = zz - 1
                 const C hu = add(Aprev[r], T);
                 const C res = owned[r] ? sub(bq[r], hu) : zero<C>();
-                if (owned[r] && zz < z1) bq[r] = ld(bPtr + sz + r * sy);
                 const S m2 = fma(res.x, res.x, res.y * res.y);
                 nmax = fmax(nmax, static_cast<double>(m2));
                 nsum += static_cast<double>(m2);
@@ -760,7 +774,6 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
             Acur[r] = T;
         }
         if (it >= 2) {
-            bPtr += sz;
             sPtr += sz;
             uPtr += sz;
             if ((u + 2) % 3 == 2) {
@@ -798,7 +811,6 @@ __global__ void __launch_bounds__(NT, TMG_F3_MINB)
     flushSlots(zLow + 1 - zBase);
     dev::block_norms(nmax, nsum, a.norms);
 }
-#endif  // TMG_F3_ROWS
 
 // derive_u (fused3.cuh): phase B of k_fused3 for one point, from global memory
 template <class S>
@@ -923,9 +935,21 @@ size_t partial_count(const Geometry& g) {
 
 int blocks(const Geometry& g) { return g.nbx * g.nby * g.nbz; }
 
+namespace {
+template <class S>
+constexpr int rows_of() { return sizeof(S) == 4 ? TMG_F3_ROWS_C64 : TMG_F3_ROWS; }
+template <class S, bool BPX>
+constexpr size_t smem_of() {
+    using C = typename Cx<S>::T;
+    return rows_of<S>() == 2 ? Smem<C, 2>::template bytes<BPX>() : Smem<C, 1>::template bytes<BPX>();
+}
+template <bool BPX, class S>
+constexpr auto kernel_of() { return rows_of<S>() == 2 ? k_fused3_r2<BPX, S> : k_fused3_r1<BPX, S>; }
+}  // namespace
+
 size_t smem_bytes(bool bpx, bool c64) {
-    if (c64) return bpx ? Smem<float2>::bytes<true>() : Smem<float2>::bytes<false>();
-    return bpx ? Smem<double2>::bytes<true>() : Smem<double2>::bytes<false>();
+    if (c64) return bpx ? smem_of<float, true>() : smem_of<float, false>();
+    return bpx ? smem_of<double, true>() : smem_of<double, false>();
 }
 
 bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool c64, int nz) {
@@ -955,35 +979,37 @@ bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool 
 int resident_blocks(int smCount) {
     // blocks per SM of the non-BPX complex128 kernel at its dynamic shared memory size
     const size_t smem = smem_bytes(false);
-    cudaFuncSetAttribute(k_fused3<false, double>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    constexpr auto k = kernel_of<false, double>();
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     int per = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused3<false, double>, NT, smem) != cudaSuccess ||
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, Cfg<rows_of<double>()>::NT, smem) != cudaSuccess ||
         per < 1)
-        per = 3;
+        per = Cfg<rows_of<double>()>::MINB;
     return per * smCount;
 }
 
 namespace {
 template <bool BPX, class S>
 void launch_one(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC, const CUtensorMap& mapI,
-                cudaStream_t s, dim3 grid) {
+                const CUtensorMap& mapB, cudaStream_t s, dim3 grid) {
     // the shared-memory limit is a per-device function attribute: set it on every
     // launch (a host-side call, no device work) so a second device is configured too
-    const size_t smem = smem_bytes(BPX, sizeof(S) == 4);
-    cudaFuncSetAttribute(k_fused3<BPX, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    dev::launch_k(k_fused3<BPX, S>, grid, dim3(TX, TYT), smem, s, mapU, mapC, mapI, a);
+    const size_t smem = smem_of<S, BPX>();
+    constexpr auto k = kernel_of<BPX, S>();
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    dev::launch_k(k, grid, dim3(TX, Cfg<rows_of<S>()>::TYT), smem, s, mapU, mapC, mapI, mapB, a);
 }
 }  // namespace
 
-void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
-            const CUtensorMap& mapI, cudaStream_t s, int nchunks) {
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC, const CUtensorMap& mapI,
+            const CUtensorMap& mapB, cudaStream_t s, int nchunks) {
     const dim3 grid(a.g.nbx, a.g.nby, nchunks > 0 ? nchunks : a.g.nbz);
     if (a.c64) {
-        if (a.bpx) launch_one<true, float>(a, mapU, mapC, mapI, s, grid);
-        else launch_one<false, float>(a, mapU, mapC, mapI, s, grid);
+        if (a.bpx) launch_one<true, float>(a, mapU, mapC, mapI, mapB, s, grid);
+        else launch_one<false, float>(a, mapU, mapC, mapI, mapB, s, grid);
     } else {
-        if (a.bpx) launch_one<true, double>(a, mapU, mapC, mapI, s, grid);
-        else launch_one<false, double>(a, mapU, mapC, mapI, s, grid);
+        if (a.bpx) launch_one<true, double>(a, mapU, mapC, mapI, mapB, s, grid);
+        else launch_one<false, double>(a, mapU, mapC, mapI, mapB, s, grid);
     }
 }
 

@@ -35,22 +35,21 @@
 namespace tmg {
 namespace fused3 {
 
-// thread rows per block (TMG_FUSED_TY) x rows per thread (TMG_F3_ROWS): the
-// default 4 x 2 = a 32 x 8 tile on 128 threads, 4 blocks per SM (measured
-// against 8 x 1 on 256 threads, the round-1 kernel: -4 % fine-pass time at
-// 729^3, -3 % at 243^3; 8 x 2 = 32 x 16: -6 % / +3 %)
+// Tiles of 32 x TY points.  Two kernel shapes over the same tiles (fused3.cu
+// Cfg<R>): R = 2 rows per thread on TY / 2 thread rows (128 threads, 4 blocks
+// per SM, b tiles by TMA) and R = 1 (256 threads, 3 blocks per SM).  Measured
+// at 729^3: complex128 R = 2 -4 % fine-pass time against R = 1 (243^3 -3 %),
+// complex64 R = 1 -7 % against R = 2; TMG_F3_ROWS / TMG_F3_ROWS_C64 override.
 #ifndef TMG_FUSED_TY
-#define TMG_FUSED_TY 4
-#endif
-#ifndef TMG_FUSED_STAGES
-#define TMG_FUSED_STAGES 4
+#define TMG_FUSED_TY 8
 #endif
 #ifndef TMG_F3_ROWS
 #define TMG_F3_ROWS 2
 #endif
-// TYT thread rows per block, each thread ROWS tile rows: TY = TYT * ROWS rows of points
-constexpr int ROWS = TMG_F3_ROWS, TYT = TMG_FUSED_TY;
-constexpr int TX = 32, TY = TYT * ROWS, STAGES = TMG_FUSED_STAGES;
+#ifndef TMG_F3_ROWS_C64
+#define TMG_F3_ROWS_C64 1
+#endif
+constexpr int TX = 32, TY = TMG_FUSED_TY;
 constexpr int HX = TX + 2, HY = TY + 2;
 constexpr int SX = TX / 3 + 3, SY = TY / 3 + 3;  // restriction slots per tile (upper bounds)
 // coarse tile feeding the prolongation: parents floor((o-1)/3) .. floor((o+T)/3) + 1 of a tile
@@ -111,8 +110,8 @@ void derive_u(const void* vOld, const double2* scTD, const double2* siTD, unsign
               unsigned fb, double2* uOut, bool c64, cudaStream_t s);
 
 // nchunks <= 0: all z-chunks (chunkBase must be 0)
-void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC,
-            const CUtensorMap& mapI, cudaStream_t s, int nchunks = 0);
+void launch(const Args& a, const CUtensorMap& mapU, const CUtensorMap& mapC, const CUtensorMap& mapI,
+            const CUtensorMap& mapB, cudaStream_t s, int nchunks = 0);
 // r_{L-1}(W) = sum of the tile partials covering W, fixed order; coarse
 // planes [za, zb) (za < 0: all).
 // smooth != nullptr: also the level L-1 smoothing of fast::smooth_coarse on the

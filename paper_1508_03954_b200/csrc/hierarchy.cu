@@ -785,6 +785,7 @@ struct Hierarchy::Impl {
     double2* uAlt = nullptr;
     CUtensorMap mapU[2];  // v: [0] current buffer, [1] alternate
     CUtensorMap mapC, mapI;  // coarse sc / si planes (L-1)
+    CUtensorMap mapB;        // fine load vector b (the fused pass's b tiles)
     fused3::Geometry geo{};
     double2* partial3 = nullptr;
     std::unique_ptr<AmrTree> amr;  // static adaptive tree (prob.sphereLevels > 0)
@@ -1323,7 +1324,7 @@ struct Hierarchy::Impl {
             fa.ellMin = prob.ellMin;
             fa.level = L;
             fa.c64 = prob.c64 ? 1 : 0;
-            fused3::launch(fa, mapU[0], mapC, mapI, stream);
+            fused3::launch(fa, mapU[0], mapC, mapI, mapB, stream);
             if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
             const int lo = useChain ? top + 1 : 1;
             const fast::ResArgs sL = args(L - 1);
@@ -1825,7 +1826,8 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
             bool ok = fused3::encode_map(&I.mapU[0], F.u + offF, F.n1, 0, prob.c64, nzF) &&
                       fused3::encode_map(&I.mapU[1], I.uAlt + offF, F.n1, 0, prob.c64, nzF) &&
                       fused3::encode_map(&I.mapC, I.scTD + offC, C.n1, 2, false, nzC) &&
-                      fused3::encode_map(&I.mapI, C.si + offC, C.n1, 2, false, nzC);
+                      fused3::encode_map(&I.mapI, C.si + offC, C.n1, 2, false, nzC) &&
+                      fused3::encode_map(&I.mapB, F.chi + offF, F.n1, 1, prob.c64, nzF);
             if (!ok) throw CudaError("cuTensorMapEncodeTiled failed for the fused fine pass");
             I.fused = true;
         }
