@@ -522,18 +522,19 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
     const int x = x0 + tx;
     const int yr0 = y0 + ROWS * ty;  // the thread's rows yr0, yr0 + 1
     bool owned[2], cpxy[2];
-    int po[2], vo[2];
+    // row r's corrected-plane / coarse-row slots: po + r * HX, vo + r * CX
+    const int po = (ROWS * ty + 1) * HX + (tx + 1);
+    int vo;
     S wxo;
     {
         const int qx = min(x / 3, mc - 1);
         wxo = third<S>(x - 3 * qx);
+        vo = (ROWS * ty + 1) * CX + (qx - cx0);
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
             const int y = yr0 + r;
             owned[r] = x < xe && y < ye;
             cpxy[r] = (x % 3 == 0) && (y % 3 == 0);
-            po[r] = (ROWS * ty + r + 1) * HX + (tx + 1);
-            vo[r] = (ROWS * ty + r + 1) * CX + (qx - cx0);
         }
     }
     // task slots k = tid and tid + NT of [0, NV + NRING): k < NV a coarse row, else ring point k - NV
@@ -558,35 +559,38 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         cpr = (gx % 3 == 0) && (gy % 3 == 0);
     }
     const bool vtask = tid < NV;
-    int vcOff[2] = {0, 0};
-    double w1y[2] = {0.0, 0.0};
-#pragma unroll
-    for (int j = 0; j < 2; ++j) {
-        const int k = j == 0 ? tid : vk2;
-        if (k < 0 || (j == 0 && !vtask)) continue;
+    // coarse-row task k: offset into the coarse tile and the y weight
+    auto vparams = [&](int k, int& off, double& w) {
         const int ly = k / CX, ci = k % CX;
         const int gy = y0 - 1 + ly;
         const int qy = min(max(gy, 0) / 3, mc - 1);
-        vcOff[j] = (qy - cy0) * CX + ci;
-        w1y[j] = third<double>(gy - 3 * qy);
-    }
+        off = (qy - cy0) * CX + ci;
+        w = third<double>(gy - 3 * qy);
+    };
+    int vcOff = 0;
+    double w1y = 0.0;
+    if (vtask) vparams(tid, vcOff, w1y);
     auto computeV = [&](int stage, int zz, int vb) {
         const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
         const double w1z = third<double>(rz);
         const double2* Cc = coarse(stage);
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-            if (j == 0 ? !vtask : vk2 < 0) continue;
-            const int o = vcOff[j], slot = j == 0 ? tid : vk2;
-            const double2 a0 = lerpw(Cc[o], Cc[o + CX], w1y[j]);
-            const double2 a1 = lerpw(Cc[o + CX * CY], Cc[o + CX * CY + CX], w1y[j]);
+        auto one = [&](int o, double wy, int slot) {
+            const double2 a0 = lerpw(Cc[o], Cc[o + CX], wy);
+            const double2 a1 = lerpw(Cc[o + CX * CY], Cc[o + CX * CY + CX], wy);
             Vb[vb * M::kV + slot] = to_c(lerpw(a0, a1, w1z), C{});
             if (BPX) {
                 const double2* I = Cc + M::kC / 16;
-                const double2 b0 = lerpw(I[o], I[o + CX], w1y[j]);
-                const double2 b1 = lerpw(I[o + CX * CY], I[o + CX * CY + CX], w1y[j]);
+                const double2 b0 = lerpw(I[o], I[o + CX], wy);
+                const double2 b1 = lerpw(I[o + CX * CY], I[o + CX * CY + CX], wy);
                 Vb[(2 + vb) * M::kV + slot] = to_c(lerpw(b0, b1, w1z), C{});
             }
+        };
+        if (vtask) one(vcOff, w1y, tid);
+        if (vk2 >= 0) {  // the few threads with a second coarse-row task: parameters on the fly
+            int o2;
+            double wy2;
+            vparams(vk2, o2, wy2);
+            one(o2, wy2, vk2);
         }
     };
 
@@ -693,13 +697,13 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         C cOwn[2];
 #pragma unroll
         for (int r = 0; r < 2; ++r) {
-            C scv = lerpw(V[vo[r]], V[vo[r] + 1], wxo);
+            C scv = lerpw(V[(vo + r * CX)], V[(vo + r * CX) + 1], wxo);
             if (BPX && !(cpxy[r] && u == 0)) {
                 const C* Vi = Vb + (2 + (it & 1)) * M::kV;
-                scv = sub(scv, lerpw(Vi[vo[r]], Vi[vo[r] + 1], wxo));
+                scv = sub(scv, lerpw(Vi[(vo + r * CX)], Vi[(vo + r * CX) + 1], wxo));
             }
-            cOwn[r] = (zin && owned[r]) ? add(Ut[po[r]], scv) : zero<C>();
-            P[po[r]] = cOwn[r];
+            cOwn[r] = (zin && owned[r]) ? add(Ut[(po + r * HX)], scv) : zero<C>();
+            P[(po + r * HX)] = cOwn[r];
         }
         if (rk >= 0) {
             C scv = lerpw(V[vr], V[vr + 1], wxr);
@@ -714,6 +718,10 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         if (tid == 0 && it + STAGES < nplanes) issue(stage, zz + STAGES);
         stage = nstage;
         parity = nparity;
+        // keep the ring slot a run-time value: with 3 stages and the 3-way unrolled
+        // plane loop the compiler would otherwise specialise every slot address
+        // per step (+ 70 B of register spills)
+        asm volatile("" : "+r"(stage));
         // ---- phase C ----
         if (u == 1 && pend1) {
             stage1();
@@ -751,7 +759,7 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
                 const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpxy[r] && kz == 0, BPX ? 1 : 0, a.hb);
                 if (owned[r]) {
                     if (a.writeSc) sPtr[r * sy] = scn;
-                    uPtr[r * sy] = add(Pb[((it + 1) & 1) * M::kP + po[r]], scn);
+                    uPtr[r * sy] = add(Pb[((it + 1) & 1) * M::kP + (po + r * HX)], scn);
                 }
                 if (BPX && kz == 0 && a.level > a.ellMin && cpxy[r] && owned[r])
                     a.sinextC[(x / 3) + a.n1c * (static_cast<long long>((yr0 + r) / 3) +
