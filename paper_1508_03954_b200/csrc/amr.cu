@@ -101,12 +101,52 @@ __device__ __forceinline__ int aflat(const ALvl& c, const int* g) {
     return f;
 }
 
+// Grid-stride walk over a level's vertex list with the list entry loaded two
+// iterations ahead and the vertex's flags one ahead: the per-vertex chain
+// list -> flags -> data was three dependent memory latencies per iteration.
+struct ListWalk {
+    const unsigned* list;
+    const unsigned char* vflag;
+    unsigned n, stride;
+    unsigned f = 0, fN = 0;  // this / the next iteration's vertex
+    unsigned char vf = 0;    // this iteration's flags
+    __device__ explicit ListWalk(const ALvl& c) : list(c.list), vflag(c.vflag), n(c.nlist), stride(gridDim.x * blockDim.x) {}
+    __device__ unsigned first() {
+        const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+        if (i < n) {
+            f = __ldg(list + i);
+            vf = __ldg(vflag + f);
+        }
+        if (i + stride < n) fN = __ldg(list + i + stride);
+        return i;
+    }
+    // issue the loads of the iterations after i (call once per iteration, before any `continue`)
+    __device__ void prefetch(unsigned i) {
+        const unsigned i1 = i + stride, i2 = i1 + stride;
+        unsigned char vfN = 0;
+        if (i1 < n) vfN = __ldg(vflag + fN);
+        const unsigned fNN = i2 < n ? __ldg(list + i2) : 0u;
+        pendF = fN;
+        pendVf = vfN;
+        fN = fNN;
+    }
+    __device__ unsigned next(unsigned i) {
+        f = pendF;
+        vf = pendVf;
+        return i + stride;
+    }
+    unsigned pendF = 0;
+    unsigned char pendVf = 0;
+};
+
 // ---- top-down: touch_first / create_hanging ----------------------------------
 template <int P, bool STATIC = false>
-__global__ void __launch_bounds__(256) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
-        const unsigned f = c.list[i];
-        const unsigned char vf = c.vflag[f];
+__global__ void __launch_bounds__(256, 3) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
+    ListWalk w(c);
+    for (unsigned i = w.first(); i < c.nlist; i = w.next(i)) {
+        const unsigned f = w.f;
+        const unsigned char vf = w.vf;
+        w.prefetch(i);
         if (!(vf & amr::kExists)) continue;
         const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging;
         if (c.level == 0) {  // cycles.cpp:128-133
@@ -725,9 +765,11 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
     constexpr int NC = 1 << P;
     const ALvl& c = a.lv;
     double nmax = 0.0, nsum = 0.0;
-    for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
-        const unsigned f = c.list[i];
-        const unsigned char vf = c.vflag[f];
+    ListWalk w(c);
+    for (unsigned i = w.first(); i < c.nlist; i = w.next(i)) {
+        const unsigned f = w.f;
+        const unsigned char vf = w.vf;
+        w.prefetch(i);
         if (!(vf & amr::kExists)) continue;
         if (c.slist && (vf & dyn::kSSpecial)) continue;  // k_dyn_special
         const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging,
