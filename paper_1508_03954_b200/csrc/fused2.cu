@@ -3,6 +3,7 @@
 #include "fused2.cuh"
 
 #include <algorithm>
+#include <type_traits>
 
 #include "lattice.cuh"
 
@@ -147,34 +148,54 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     // Row ring: row yy's state v = u + sc (fused3.cuh "v-form") and its load
     // vector b, copied (cp.async, zero-filled off the domain) kRing - 1 rows
     // ahead into slot (yy - y0 + 1) % kRing; every thread reads back only
-    // what it copied itself, so the ring needs no barrier.
-    auto issueRow = [&](int it2) {
-        const int yy = y0 - 1 + it2, slot = it2 % kRing;
+    // what it copied itself, so the ring needs no barrier.  The row loop is
+    // unrolled by three (yy % 3 a compile-time constant, y0 = 1 mod 3) and the
+    // global row addresses advance by pointer.
+    const double2* uIss = a.u + x + n1 * (y0 - 1);  // row of the next issue (it2)
+    const double2* bIss = a.b + x + n1 * (y0 - 1);
+    const double2* hIss = a.u + (hin ? hx : x0) + n1 * (y0 - 1);
+    int issRow = y0 - 1;
+    auto issueRow = [&](int it2, auto U3) {  // U3: (y0 - 1 + it2) % 3
+        constexpr int uu = decltype(U3)::value;
+        const int yy = issRow, slot = it2 & (kRing - 1);
         const bool yin = yy >= 1 && yy <= m - 1;
-        const long long row = n1 * (yin ? yy : 1);
         if (owned) {  // (a column past the strip end would collide with the halo slot)
-            cp_async16z(&Ru[slot][tid + 1], a.u + x + row, yin);
-            cp_async16z(&Rb[slot][tid], a.b + x + row, yy >= y0 && yy < y1);
+            cp_async16z(&Ru[slot][tid + 1], yin ? uIss : a.u, yin);
+            cp_async16z(&Rb[slot][tid], yin ? bIss : a.b, yy >= y0 && yy < y1);
         }
-        if (haloThread) cp_async16z(&Ru[slot][hslot], a.u + (hin ? hx : x0) + row, yin && hin);
-        if (yy >= 2 && yy % 3 == 2 && (yy + 1) / 3 < mc) issueCoarse((yy + 1) / 3 + 1);  // needed from fine row yy + 1
+        if (haloThread) cp_async16z(&Ru[slot][hslot], yin && hin ? hIss : a.u, yin && hin);
+        if (uu == 2 && yy >= 2 && (yy + 1) / 3 < mc) issueCoarse((yy + 1) / 3 + 1);  // needed from fine row yy + 1
         asm volatile("cp.async.commit_group;" ::: "memory");
+        uIss += n1;
+        bIss += n1;
+        hIss += n1;
+        ++issRow;
     };
-    for (int i = 0; i < kRing - 1; ++i) issueRow(i);  // empty groups past the chunk keep the count uniform
+    using U0 = std::integral_constant<int, 0>;
+    using U1 = std::integral_constant<int, 1>;
+    using U2 = std::integral_constant<int, 2>;
+    // empty groups past the chunk keep the count uniform
+    issueRow(0, U0{});
+    issueRow(1, U1{});
+    issueRow(2, U2{});
     double2 cPrev = zero2();
     double2 bq = zero2();
     computeV(y0 - 1, 0);
     __syncthreads();
 
-    for (int it = 0; it < nrows; ++it) {
+    double2* uOut = a.uNew + x + n1 * y0;  // row yy - 1 of the residual steps (it >= 2), advanced by each
+    double2* scOut = a.scNew + x + n1 * y0;
+    const double2 wRaw = a.k.wRaw, invDiag = a.k.invDiag;
+    auto step = [&](int it, auto U3) {
+        constexpr int u3 = decltype(U3)::value;  // yy % 3
+        constexpr int kz = (u3 + 2) % 3;         // (yy - 1) % 3
         const int yy = y0 - 1 + it;
-        const int u3 = it % 3;  // yy % 3 (y0 = 1 mod 3)
         const bool yin = yy >= 1 && yy <= m - 1;
         asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 2) : "memory");  // row yy landed
-        const double2 uC = Ru[it % kRing][tid + 1];
-        const double2 huC = haloThread ? Ru[it % kRing][hslot] : zero2();
-        if (it >= 2) bq = Rb[(it - 1) % kRing][tid];  // b of row yy - 1 (the residual row)
-        if (it + kRing - 1 < nrows) issueRow(it + kRing - 1);  // into the slot of row yy - 1
+        const double2 uC = Ru[it & (kRing - 1)][tid + 1];
+        const double2 huC = haloThread ? Ru[it & (kRing - 1)][hslot] : zero2();
+        if (it >= 2) bq = Rb[(it + kRing - 1) & (kRing - 1)][tid];  // b of row yy - 1 (the residual row)
+        if (it + kRing - 1 < nrows) issueRow(it + kRing - 1, U3);  // into the slot of row yy - 1; same residue
         else asm volatile("cp.async.commit_group;" ::: "memory");
         const double2* V = Vb[it & 1];
         double2* P = Pb[it & 1];
@@ -208,20 +229,19 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         double2 U = mul(k0, cOwn);
         U = mac(U, k1, E);
         if (it >= 2) {
-            const int yr = yy - 1;
-            const int kz = (u3 + 2) % 3;
             const double2 hu = add(Aprev, T);
             const double2 r = owned ? sub(bq, hu) : zero2();
             const double m2 = fma(r.x, r.x, r.y * r.y);
             nmax = fmax(nmax, m2);
             nsum += m2;
-            const double2 smooth = mul(r, a.k.invDiag);
-            const double2 scn = zeroSc ? zero2() : stage_sc(smooth, a.k.wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
+            const double2 smooth = mul(r, invDiag);
+            const double2 scn = zeroSc ? zero2() : stage_sc(smooth, wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
             if (owned) {
-                if (a.writeSc) a.scNew[x + n1 * yr] = scn;
-                a.uNew[x + n1 * yr] = add(cPrev, scn);  // next state v of row yr
+                if (a.writeSc) *scOut = scn;
+                *uOut = add(cPrev, scn);  // next state v of row yy - 1
             }
-            if (BPX && kz == 0 && injectOK) a.sinextC[x / 3 + static_cast<long long>(a.n1c) * (yr / 3)] = mul(a.k.wRaw, smooth);
+            if (BPX && kz == 0 && injectOK)
+                a.sinextC[x / 3 + static_cast<long long>(a.n1c) * ((yy - 1) / 3)] = mul(wRaw, smooth);
             if (kz == 0) {
                 accLo = add(accLo, r);
             } else if (kz == 1) {
@@ -237,10 +257,20 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
                 ziPend = zLow - zBase;
                 ++zLow;
             }
+            uOut += n1;
+            scOut += n1;
         }
         Aprev = add(Acur, U);
         Acur = T;
         cPrev = cOwn;
+    };
+    // yy = y0 - 1 + it and y0 = 1 (mod 3): yy % 3 == it % 3
+    for (int it = 0; it < nrows; it += 3) {
+        step(it, U0{});
+        if (it + 1 >= nrows) break;
+        step(it + 1, U1{});
+        if (it + 2 >= nrows) break;
+        step(it + 2, U2{});
     }
     __syncthreads();
     if (pend) flush(ziPend);
