@@ -49,6 +49,27 @@ __device__ __forceinline__ void cp_async16z(void* dst, const void* src, bool val
 }
 
 constexpr int kRing = 4;  // rows in flight
+constexpr int kHaloT = TX >= 64 ? 32 : 0;   // first of the two halo-column threads
+constexpr int kCvT = TX >= 128 ? 64 : 0;    // first coarse-row thread
+static_assert(kCvT + CXW <= TX, "coarse-row tasks");
+
+__device__ __forceinline__ unsigned su32(const void* p) { return static_cast<unsigned>(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void bulk_row(void* dst, const void* src, unsigned bytes, unsigned long long* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(su32(dst)),
+                 "l"(src), "r"(bytes), "r"(su32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void rbar_wait(unsigned long long* bar, unsigned parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "TMG_RW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra TMG_RW_%=;\n"
+        "}\n" ::"r"(su32(bar)),
+        "r"(parity)
+        : "memory");
+}
 
 template <bool BPX>
 __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
@@ -56,6 +77,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     __shared__ double2 Pb[2][TX + 2];          // corrected rows (x halo at 0 and TX+1)
     __shared__ double2 Vb[BPX ? 4 : 2][CXW];   // y-interpolated coarse rows (sc[, si])
     __shared__ double2 tb[TX];                 // y-restricted columns
+    __shared__ unsigned long long rbar[kRing]; // row ring: one mbarrier per slot (bulk copies)
     extern __shared__ __align__(16) double2 dyn[];
     auto Ru = reinterpret_cast<double2(*)[TX + 2]>(dyn);                    // row ring: v (own columns + x halo)
     auto Rb = reinterpret_cast<double2(*)[TX]>(dyn + kRing * (TX + 2));      // row ring: b
@@ -77,24 +99,28 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     const double wxo = relw(x - 3 * qxo);
     const bool cpx = x % 3 == 0;
     // halo columns (threads 0 and 1): x0 - 1 and xe
-    const int hx = tid == 0 ? x0 - 1 : xe;
-    const bool haloThread = tid < 2;
+    // per-row side tasks spread over the warps (the row barrier waits for the
+    // busiest): halo columns on warp 1, coarse rows on warps 2-3, the bulk-copy
+    // issue on thread 0, the restriction flush on the last threads
+    const int hx = tid == kHaloT ? x0 - 1 : xe;
+    const bool haloThread = tid == kHaloT || tid == kHaloT + 1;
     const bool hin = haloThread && hx >= 1 && hx <= m - 1;
     const int hq = min(max(hx, 0) / 3, mc - 1);
     const int hv = hq - cx0;
     const double hw = relw(hx - 3 * hq);
     const bool hcpx = hx % 3 == 0;
-    const int hslot = tid == 0 ? 0 : (xe - x0) + 1;
+    const int hslot = tid == kHaloT ? 0 : (xe - x0) + 1;
+    const int ct = tid - kCvT;  // coarse-row task: coarse column cx0 + ct
 
     // coarse rows feeding the strip (sc[, si]) through a 4-slot ring (slot q % 4):
     // rows q(y0-1) and +1 up front, then coarse row Q + 1 rides with fine row
     // 3Q - 1's ring group, so it has landed when computeV(3Q) runs (one row later)
-    const int cxo = min(cx0 + tid, mc);
+    const int cxo = min(cx0 + ct, mc);
     auto issueCoarse = [&](int q) {
-        if (tid < CXW && q <= mc) {
+        if (ct >= 0 && ct < CXW && q <= mc) {
             const long long g = cxo + static_cast<long long>(a.n1c) * q;
-            cp_async16(Cs + (q & 3) * CXW + tid, a.scC + g);
-            if (BPX) cp_async16(Cs + (4 + (q & 3)) * CXW + tid, a.siC + g);
+            cp_async16(Cs + (q & 3) * CXW + ct, a.scC + g);
+            if (BPX) cp_async16(Cs + (4 + (q & 3)) * CXW + ct, a.siC + g);
         }
     };
     {
@@ -103,14 +129,14 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         issueCoarse(q0 + 1);
         asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    auto computeV = [&](int yy, int vb) {  // coarse rows of fine row yy, for coarse columns cx0 + tid
-        if (tid >= CXW) return;
+    auto computeV = [&](int yy, int vb) {  // coarse rows of fine row yy, for coarse columns cx0 + ct
+        if (ct < 0 || ct >= CXW) return;
         const int qy = min(max(yy, 0) / 3, mc - 1);
         const double w1y = relw(yy - 3 * qy);
-        const double2* c0 = Cs + (qy & 3) * CXW + tid;
-        const double2* c1 = Cs + ((qy + 1) & 3) * CXW + tid;
-        Vb[vb][tid] = lerpw(c0[0], c1[0], w1y);
-        if (BPX) Vb[2 + vb][tid] = lerpw(c0[4 * CXW], c1[4 * CXW], w1y);
+        const double2* c0 = Cs + (qy & 3) * CXW + ct;
+        const double2* c1 = Cs + ((qy + 1) & 3) * CXW + ct;
+        Vb[vb][ct] = lerpw(c0[0], c1[0], w1y);
+        if (BPX) Vb[2 + vb][ct] = lerpw(c0[4 * CXW], c1[4 * CXW], w1y);
     };
 
     // restriction slots of this strip
@@ -145,39 +171,47 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     double2 accLo = zero2(), accHi = zero2();
     double2 Aprev = zero2(), Acur = zero2();
 
-    // Row ring: row yy's state v = u + sc (fused3.cuh "v-form") and its load
-    // vector b, copied (cp.async, zero-filled off the domain) kRing - 1 rows
-    // ahead into slot (yy - y0 + 1) % kRing; every thread reads back only
-    // what it copied itself, so the ring needs no barrier.  The row loop is
-    // unrolled by three (yy % 3 a compile-time constant, y0 = 1 mod 3) and the
-    // global row addresses advance by pointer.
-    const double2* uIss = a.u + x + n1 * (y0 - 1);  // row of the next issue (it2)
-    const double2* bIss = a.b + x + n1 * (y0 - 1);
-    const double2* hIss = a.u + (hin ? hx : x0) + n1 * (y0 - 1);
-    int issRow = y0 - 1;
-    auto issueRow = [&](int it2, auto U3) {  // U3: (y0 - 1 + it2) % 3
+    // Row ring: row yy's state v = u + sc (fused3.cuh "v-form") over the strip
+    // and its halo columns [x0 - 1, xe], and its load vector b over [x0, xe),
+    // bulk-copied by one thread kRing - 1 rows ahead into slot (yy - y0 + 1) % kRing
+    // (mbarrier per slot); coarse row Q + 1 (sc[, si]) rides with fine row 3Q - 1,
+    // so it has landed when computeV(3Q) runs (one row later).  Rows off the
+    // domain (0, m) are not copied: phase B reads them as zeros.  The row loop is
+    // unrolled by three (yy % 3 a compile-time constant, y0 = 1 mod 3).
+    if (tid == 0) {
+        for (int k = 0; k < kRing; ++k)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(&rbar[k])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    const unsigned uBytes = static_cast<unsigned>(xe - x0 + 2) * 16u, bBytes = static_cast<unsigned>(xe - x0) * 16u;
+    const int cCount = min(CXW, mc + 1 - cx0);
+    auto issueRow = [&](int it2, auto U3) {  // thread 0; U3: (y0 - 1 + it2) % 3
         constexpr int uu = decltype(U3)::value;
-        const int yy = issRow, slot = it2 & (kRing - 1);
-        const bool yin = yy >= 1 && yy <= m - 1;
-        if (owned) {  // (a column past the strip end would collide with the halo slot)
-            cp_async16z(&Ru[slot][tid + 1], yin ? uIss : a.u, yin);
-            cp_async16z(&Rb[slot][tid], yin ? bIss : a.b, yy >= y0 && yy < y1);
+        const int yy = y0 - 1 + it2, slot = it2 & (kRing - 1);
+        const bool yin = yy >= 1 && yy <= m - 1, bin = yy >= y0 && yy < y1;
+        const int q = (yy + 1) / 3 + 1;
+        const bool coarse = uu == 2 && yy >= 2 && (yy + 1) / 3 < mc && q <= mc;  // needed from fine row yy + 1
+        const unsigned cb = coarse ? static_cast<unsigned>(cCount) * 16u : 0u;
+        const unsigned tx = (yin ? uBytes : 0u) + (bin ? bBytes : 0u) + (BPX ? 2u : 1u) * cb;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rbar[slot])), "r"(tx) : "memory");
+        const long long row = n1 * yy;
+        if (yin) bulk_row(&Ru[slot][0], a.u + (x0 - 1) + row, uBytes, &rbar[slot]);
+        if (bin) bulk_row(&Rb[slot][0], a.b + x0 + row, bBytes, &rbar[slot]);
+        if (coarse) {
+            const long long g = cx0 + static_cast<long long>(a.n1c) * q;
+            bulk_row(Cs + (q & 3) * CXW, a.scC + g, cb, &rbar[slot]);
+            if (BPX) bulk_row(Cs + (4 + (q & 3)) * CXW, a.siC + g, cb, &rbar[slot]);
         }
-        if (haloThread) cp_async16z(&Ru[slot][hslot], yin && hin ? hIss : a.u, yin && hin);
-        if (uu == 2 && yy >= 2 && (yy + 1) / 3 < mc) issueCoarse((yy + 1) / 3 + 1);  // needed from fine row yy + 1
-        asm volatile("cp.async.commit_group;" ::: "memory");
-        uIss += n1;
-        bIss += n1;
-        hIss += n1;
-        ++issRow;
     };
     using U0 = std::integral_constant<int, 0>;
     using U1 = std::integral_constant<int, 1>;
     using U2 = std::integral_constant<int, 2>;
-    // empty groups past the chunk keep the count uniform
-    issueRow(0, U0{});
-    issueRow(1, U1{});
-    issueRow(2, U2{});
+    if (tid == 0) {
+        issueRow(0, U0{});
+        if (nrows > 1) issueRow(1, U1{});
+        if (nrows > 2) issueRow(2, U2{});
+    }
     double2 cPrev = zero2();
     double2 bq = zero2();
     computeV(y0 - 1, 0);
@@ -191,12 +225,10 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         constexpr int kz = (u3 + 2) % 3;         // (yy - 1) % 3
         const int yy = y0 - 1 + it;
         const bool yin = yy >= 1 && yy <= m - 1;
-        asm volatile("cp.async.wait_group %0;" ::"n"(kRing - 2) : "memory");  // row yy landed
+        rbar_wait(&rbar[it & (kRing - 1)], static_cast<unsigned>(it / kRing) & 1u);  // row yy landed
         const double2 uC = Ru[it & (kRing - 1)][tid + 1];
         const double2 huC = haloThread ? Ru[it & (kRing - 1)][hslot] : zero2();
         if (it >= 2) bq = Rb[(it + kRing - 1) & (kRing - 1)][tid];  // b of row yy - 1 (the residual row)
-        if (it + kRing - 1 < nrows) issueRow(it + kRing - 1, U3);  // into the slot of row yy - 1; same residue
-        else asm volatile("cp.async.commit_group;" ::: "memory");
         const double2* V = Vb[it & 1];
         double2* P = Pb[it & 1];
         // ---- phase B: corrected row yy ----
@@ -218,6 +250,8 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         }
         if (it + 1 < nrows) computeV(yy + 1, (it + 1) & 1);
         __syncthreads();
+        // every thread has read row yy - 1's slot: refill it with row yy + 3 (same residue)
+        if (tid == 0 && it + kRing - 1 < nrows) issueRow(it + kRing - 1, U3);
         // ---- phase C ----
         if (pend) {
             flush(ziPend);
