@@ -19,7 +19,7 @@ namespace tmg {
 namespace fused2 {
 
 #ifndef TMG_F2_TX
-#define TMG_F2_TX 128
+#define TMG_F2_TX 256
 #endif
 constexpr int TX = TMG_F2_TX;  // strip width (threads per block)
 constexpr int SXP = TX / 3 + 3;        // restriction slots per strip (upper bound)
