@@ -837,7 +837,38 @@ struct Hierarchy::Impl {
     static constexpr unsigned long long kClusterMaxPts = 1ull << 18;
     unsigned* chainBar = nullptr;
 
+    // ---- CUDA graphs of the fast cycle ----
+    // A fast cycle is a handful of launches whose host-side preparation (omega
+    // tables, occupancy queries, argument blocks) and launch latency dominate
+    // the small levels (cfg1: ~4 launches in ~35 us).  When the cycle's
+    // arguments do not depend on n (every omega policy but the n-dependent
+    // transition / two-phase ones), the cycle is captured once per state of the
+    // double-buffered fine level and replayed with one cudaGraphLaunch; the
+    // host-side effects of the captured cycle (buffer swaps, flags) are stored
+    // with the graph and reapplied on every replay.
+    struct CycleGraph {
+        std::string sig;          // pre-state + arguments the capture depends on
+        cudaGraphExec_t exec = nullptr;
+        double2 *fu = nullptr, *ualt = nullptr;  // post-state
+        CUtensorMap mu0, mu1;
+        bool fineDerived = false, coarseUStale = false;
+        int derivedBpx = 0;
+    };
+    std::vector<CycleGraph> graphs;
+    bool graphsBroken = false;  // a capture failed: ordinary launches from then on
+    bool capturing = false;
+    void clear_graphs() {
+        for (CycleGraph& g : graphs)
+            if (g.exec) cudaGraphExecDestroy(g.exec);
+        graphs.clear();
+    }
+    // cudaEventRecord inside a capture must become an event-record node
+    void record(cudaEvent_t ev) {
+        TMG_CUDA(cudaEventRecordWithFlags(ev, stream, capturing ? cudaEventRecordExternal : cudaEventRecordDefault));
+    }
+
     ~Impl() {
+        clear_graphs();
         amr.reset();
         for (void* ptr : allocations) cudaFree(ptr);
         if (hNorm) cudaFreeHost(hNorm);
@@ -1155,7 +1186,7 @@ struct Hierarchy::Impl {
         const bool coupled = nch > 1 && prob.coupling != Cplx(0.0);
         // top-down (levels 1..L; level 0 holds only zero boundary corners); channels are independent here
         for (int l = 1; l <= L; ++l) {
-            if (timed && l == L) TMG_CUDA(cudaEventRecord(evf0, stream));
+            if (timed && l == L) record(evf0);
             for (int ch = 0; ch < nch; ++ch)
                 dev::k_topdown<P><<<blocks_for(lv[l].n), 256, 0, stream>>>(level(ch, l), level(ch, l - 1),
                                                                           pol.bpx ? 1 : 0);
@@ -1188,7 +1219,7 @@ struct Hierarchy::Impl {
                     dev::k_residual_exact<P, false><<<nb, 256, 0, stream>>>(a, dev::McArgs{});
                 }
             }
-            if (timed && l == L) TMG_CUDA(cudaEventRecord(evf1, stream));
+            if (timed && l == L) record(evf1);
             if (l >= 2) {
                 const int zero = l <= prob.ellMin ? 1 : 0;
                 for (int ch = 0; ch < nch; ++ch)
@@ -1243,7 +1274,7 @@ struct Hierarchy::Impl {
             if (toTD && useChain && top == L - 1) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), false, true);  // in place
         }
         if (P == 3 && fused && bpx) save_coarse_td(0, static_cast<int>(lv[L - 1].n1), true, false);
-        if (timed) TMG_CUDA(cudaEventRecord(evf0, stream));
+        if (timed) record(evf0);
         if (P == 2 && fused2on) {
             fused2::Args fa{};
             dev::Lvl& F = lv[L];
@@ -1271,7 +1302,7 @@ struct Hierarchy::Impl {
             // stored fine sc (no derive, no si copy for td-bpx)
             fa.writeSc = 1;
             fused2::launch(fa, stream);
-            if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+            if (timed) record(evf1);
             if (use_up()) {  // combine + level L-1 smoothing, then the whole bottom-up in one launch
                 const fast::ResArgs sL = args(L - 1);
                 fused2::combine(fa, lv[L - 1].rhat, stream, &sL);
@@ -1325,7 +1356,7 @@ struct Hierarchy::Impl {
             fa.level = L;
             fa.c64 = prob.c64 ? 1 : 0;
             fused3::launch(fa, mapU[0], mapC, mapI, mapB, stream);
-            if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+            if (timed) record(evf1);
             const int lo = useChain ? top + 1 : 1;
             const fast::ResArgs sL = args(L - 1);
             fused3::combine(fa, lv[L - 1].rhat, blocks_for(lv[L - 1].n), stream, -1, -1,
@@ -1360,7 +1391,7 @@ struct Hierarchy::Impl {
         }
         fast::correct_fine(P, lv[L], lv[L - 1], bpx, blocks_for(lv[L].n), stream);
         const int nb = fast::residual_fine(P, args(L), smCount, stream);
-        if (timed) TMG_CUDA(cudaEventRecord(evf1, stream));
+        if (timed) record(evf1);
         for (int l = L - 1; l >= (useChain ? top + 1 : 1); --l) {
             if (l >= prob.ellMin) fast::restrict_level(P, lv[l + 1], lv[l], nullptr, blocks_for(lv[l].n), stream);
             fast::smooth_coarse(P, args(l), blocks_for(lv[l].n), stream);
@@ -1454,11 +1485,100 @@ struct Hierarchy::Impl {
         coarseUStale = false;
     }
 
+    void cycle_fast_dispatch(const Policy& pol, int n, bool timed) {
+        if (p == 1) cycle_fast<1>(pol, n, timed);
+        else if (p == 2) cycle_fast<2>(pol, n, timed);
+        else cycle_fast<3>(pol, n, timed);
+    }
+
+    // the cycle's launch arguments as bytes, or "" when they depend on n
+    std::string cycle_signature(const Policy& pol, int n, bool timed) const {
+        std::string sig;
+        auto put = [&](const void* ptr, size_t bytes) { sig.append(static_cast<const char*>(ptr), bytes); };
+        for (int succ = 0; succ <= L; ++succ) {
+            const Cplx w = omega_unmasked(pol, succ, n);
+            if (w != omega_unmasked(pol, succ, n + 1)) return std::string();
+            put(&w, sizeof(w));
+        }
+        const int flags[4] = {pol.bpx ? 1 : 0, pol.hbMask ? 1 : 0, timed ? 1 : 0, prob.ellMin};
+        put(flags, sizeof(flags));
+        put(&lv[L].u, sizeof(double2*));
+        put(&uAlt, sizeof(double2*));
+        return sig;
+    }
+
+    void cycle_fast_graph(const Policy& pol, int n, bool timed) {
+        const std::string sig = dev::switches().graph && !graphsBroken ? cycle_signature(pol, n, timed) : std::string();
+        if (sig.empty()) {
+            cycle_fast_dispatch(pol, n, timed);
+            return;
+        }
+        for (CycleGraph& g : graphs) {
+            if (g.sig != sig) continue;
+            TMG_CUDA(cudaGraphLaunch(g.exec, stream));
+            lv[L].u = g.fu;
+            uAlt = g.ualt;
+            mapU[0] = g.mu0;
+            mapU[1] = g.mu1;
+            fineDerived = g.fineDerived;
+            derivedBpx = g.derivedBpx;
+            coarseUStale = g.coarseUStale;
+            return;
+        }
+        // capture: the host-side state is restored if the capture fails
+        double2 *fu = lv[L].u, *ua = uAlt;
+        const CUtensorMap m0 = mapU[0], m1 = mapU[1];
+        const bool fd = fineDerived, cs = coarseUStale;
+        const int db = derivedBpx;
+        cudaGraph_t graph = nullptr;
+        cudaGraphExec_t exec = nullptr;
+        bool ok = cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+        if (ok) {
+            capturing = true;
+            try {
+                cycle_fast_dispatch(pol, n, timed);
+            } catch (...) {
+                ok = false;
+            }
+            capturing = false;
+            ok = cudaStreamEndCapture(stream, &graph) == cudaSuccess && ok && graph;
+        }
+        if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+        if (graph) cudaGraphDestroy(graph);
+        if (!ok) {
+            (void)cudaGetLastError();
+            graphsBroken = true;
+            lv[L].u = fu;
+            uAlt = ua;
+            mapU[0] = m0;
+            mapU[1] = m1;
+            fineDerived = fd;
+            derivedBpx = db;
+            coarseUStale = cs;
+            cycle_fast_dispatch(pol, n, timed);
+            return;
+        }
+        if (graphs.size() >= 4) {
+            cudaGraphExecDestroy(graphs.front().exec);
+            graphs.erase(graphs.begin());
+        }
+        CycleGraph g;
+        g.sig = sig;
+        g.exec = exec;
+        g.fu = lv[L].u;
+        g.ualt = uAlt;
+        g.mu0 = mapU[0];
+        g.mu1 = mapU[1];
+        g.fineDerived = fineDerived;
+        g.derivedBpx = derivedBpx;
+        g.coarseUStale = coarseUStale;
+        graphs.push_back(g);
+        TMG_CUDA(cudaGraphLaunch(exec, stream));
+    }
+
     void run_cycle(const Policy& pol, int n, bool timed) {
         if (prob.fast) {
-            if (p == 1) cycle_fast<1>(pol, n, timed);
-            else if (p == 2) cycle_fast<2>(pol, n, timed);
-            else cycle_fast<3>(pol, n, timed);
+            cycle_fast_graph(pol, n, timed);
         } else {
             if (p == 1) cycle_exact<1>(pol, n, timed);
             else if (p == 2) cycle_exact<2>(pol, n, timed);

@@ -30,6 +30,7 @@ struct Switches {
     bool pyr = true;        // TMG_PYR=0: per-level top-down launches
     int gridCap = 32;       // TMG_GRID_CAP: blocks per SM of grid-stride launches
     int zchunks = 0;        // TMG_ZCHUNKS: z-chunk count of the 3D fused pass (0: automatic)
+    bool graph = true;      // TMG_GRAPH=0: launch the fast cycle's kernels one by one (no CUDA graph)
 };
 inline Switches& switches() {
     static Switches s;
@@ -49,6 +50,7 @@ inline void refresh_switches() {
     s.gridCap = cap ? std::max(1, std::atoi(cap)) : 32;
     const char* zc = std::getenv("TMG_ZCHUNKS");
     s.zchunks = zc ? std::max(1, std::atoi(zc)) : 0;
+    s.graph = on("TMG_GRAPH");
 }
 
 inline bool pdl_enabled() { return switches().pdl; }
