@@ -54,7 +54,7 @@ WORKLOADS = {
                  desc="3D depth 5 (243^3), k=20, additive MG, exponential omega 0.6"),
     "cfg4": dict(dim=3, level=4, sphere_levels=2, k=40, cycle="td-add", omega="exponential", omega_s=0.6,
                  desc="3D adaptive: depth 4 refined to 6 inside |x-1/2|<0.2 (hanging vertices), k=40, f in the ball, "
-                      "additive MG, exponential omega 0.6, exact precision"),
+                      "additive MG, exponential omega 0.6"),
     "cfg5": dict(dim=3, level=6, k=80, cycle="td-add", omega="exponential", omega_s=0.6,
                  desc="3D depth 6 (729^3), k=80, additive MG, exponential omega 0.6 (cfg5 final FMG level)"),
     # dynamic adaptivity: feature-based refine / erase marks after every sweep
@@ -389,13 +389,16 @@ def run_reference_arm(args, w):
 
 # --------------------------------------------------------------------------
 def run_amr(args, w):
-    """cfg4: the static adaptive tree, exact precision, one GPU (replicas for N > 1)."""
+    """cfg4: the static adaptive tree, one GPU (replicas for N > 1).  precision
+    fast (default): the regular vertices' residual as the assembled stencil in
+    FMAs; exact: every iterate bit-identical to the reference."""
     from paper_1508_03954_b200 import dist as D
     import paper_1508_03954_b200 as T
     ctx = D.init()
     k = w["k"]
+    prec = "exact" if args.precision == "exact" else "fast"
     h = T.Hierarchy(w["dim"], w["level"], phi=complex(k * k, 0.5 * k * k), chi="seeded", rhs_seed=RHS_SEED,
-                    rhs_sphere=True, precision="exact", max_vertices=10 ** 10, device=ctx.local,
+                    rhs_sphere=True, precision=prec, max_vertices=10 ** 10, device=ctx.local,
                     sphere_levels=w["sphere_levels"])
     pol = T.Policy(kind=w["omega"], omega_s=w["omega_s"])
     settle(h, pol, D, ctx)
@@ -420,7 +423,7 @@ def run_amr(args, w):
     r = T.run(dict(problem="helmholtz-sin", dim=w["dim"], level=w["level"], sphere_levels=w["sphere_levels"],
                    phi=f"{k * k},{0.5 * k * k}", omega=w["omega"], omega_s=w["omega_s"], rhs="seeded",
                    rhs_seed=RHS_SEED, rhs_mask="sphere", max_sweeps=args.steps, target_drop=1e-300,
-                   max_vertices=10 ** 10, device=ctx.local))
+                   max_vertices=10 ** 10, device=ctx.local, precision=prec))
     e2e_s = time.perf_counter() - t0
     if ctx.rank == 0:
         line = {
@@ -430,12 +433,14 @@ def run_amr(args, w):
             "data": "synthetic (seeded uniform complex rhs in the ball, SURVEY §8d)",
             "config": {"workload": args.workload, "desc": w["desc"], "leaf_dof": dof,
                        "hanging_vertices": h.hanging_vertices, "existing_vertices": existing,
-                       "precision": "exact", "parallelism": f"replicas x{ctx.world}" if ctx.world > 1 else "single GPU",
+                       "precision": prec, "parallelism": f"replicas x{ctx.world}" if ctx.world > 1 else "single GPU",
                        "l2": "level-6 box arrays of 0.4 GB each (> L2); no flush"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": None, "peak_kind": peak_kind,
-                         "kernel": "whole exact adaptive cycle (k_amr_topdown/chi/residual per level), 176 B per "
-                                   "existing vertex; FP64-issue bound (element-by-element, reference order)"},
+                         "kernel": f"whole {prec} adaptive cycle (k_amr_topdown/chi/residual per level), 176 B per "
+                                   "existing vertex" + ("; FP64-issue bound (element-by-element, reference order)"
+                                                        if prec == "exact" else
+                                                        "; regular vertices' residual as the assembled stencil (FMA)")},
             "cpu_baseline": cpu,
             "e2e": {"value": ctx.world * dof * r.sweeps / e2e_s, "unit": "DoF-updates/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 48, "note": f"treemg_run of {r.sweeps} cycles incl. tree setup "

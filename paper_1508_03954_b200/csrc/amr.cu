@@ -76,6 +76,7 @@ struct AResArgs {
     double2 dgTab[9];  // diag after k cells: ((A_aa + A_aa) + ...) k times (zero_accumulators, then +=)
     int ellMin, bpx, hb;
     double* partials;
+    double2 kAsm[8];  // precision = fast: assembled stencil entry per offset class s, 2^(P - |s|) A[s]
 };
 
 template <int P>
@@ -695,6 +696,29 @@ __device__ __forceinline__ double2 regular_residual(const double2* __restrict__ 
     }
 }
 
+// precision = fast: the same residual as the assembled 3^P-point stencil (the
+// 2^(P - |s|) cells that share the vertex and its neighbour at offset class s
+// each contribute A[s]), complex FMAs in neighbour order -- within rounding of
+// the traversal-order element sums, not bit-identical
+template <int P>
+__device__ __forceinline__ double2 regular_residual_fast(const double2* __restrict__ x, int f, int sy, int sz,
+                                                         const double2 (&K)[8]) {
+    double2 acc = cz();
+#pragma unroll
+    for (int j = 0; j < (P == 1 ? 3 : P == 2 ? 9 : 27); ++j) {
+        int off = 0, s = 0;
+#pragma unroll
+        for (int d = 0; d < P; ++d) {
+            const int del = (j / (d == 0 ? 1 : d == 1 ? 3 : 9)) % 3 - 1;
+            off += del * (d == 0 ? 1 : d == 1 ? sy : sz);
+            s |= (del != 0 ? 1 : 0) << d;
+        }
+        const double2 v = __ldg(x + (f + off));
+        acc = make_double2(fma(K[s].x, v.x, fma(-K[s].y, v.y, acc.x)), fma(K[s].x, v.y, fma(K[s].y, v.x, acc.y)));
+    }
+    return xneg(acc);
+}
+
 // Special vertices of a dynamic sweep (dyn.hpp kSSpecial): created after some
 // adjacent cells were already entered (those never reach it), or finishing
 // more than once (hanging vertices on the rim of blocks refined later in the
@@ -757,10 +781,10 @@ __global__ void __launch_bounds__(256) k_dyn_special(ALvl c, ALvl fl, LevelConst
 }
 
 // ---- residual + touch_last / destroy_hanging --------------------------------
-template <int P>
 #ifndef TMG_AMR_RES_MINB
 #define TMG_AMR_RES_MINB 3
 #endif
+template <int P, bool FAST = false>
 __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs a) {
     constexpr int NC = 1 << P;
     const ALvl& c = a.lv;
@@ -783,8 +807,13 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
         const bool general = hang || bnd;
         if (!general) {  // every cell around g exists
             const int sy = c.n1[0], sz = c.n1[0] * c.n1[1];
-            r = regular_residual<P>(c.u, static_cast<int>(f), sy, sz, a.k.A, pid);
-            rh = regular_residual<P>(c.uhat, static_cast<int>(f), sy, sz, a.k.A, pid);
+            if (FAST) {
+                r = regular_residual_fast<P>(c.u, static_cast<int>(f), sy, sz, a.kAsm);
+                rh = regular_residual_fast<P>(c.uhat, static_cast<int>(f), sy, sz, a.kAsm);
+            } else {
+                r = regular_residual<P>(c.u, static_cast<int>(f), sy, sz, a.k.A, pid);
+                rh = regular_residual<P>(c.uhat, static_cast<int>(f), sy, sz, a.k.A, pid);
+            }
         } else {
             ncell = 0;
         }
@@ -1690,7 +1719,8 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
     : prob_(prob), p_(prob.dim), L_(prob.levels), base_(prob.levels - prob.sphereLevels), stream_(stream),
       smCount_(smCount), dev_(new Dev()), diag_(diagInterior) {
     dev_->kc = kc;
-    if (prob.fast) throw UnsupportedConfigError("adaptive trees run in precision = exact only");
+    if (prob.fast && (prob.dynStart > 0 || prob.c64))
+        throw UnsupportedConfigError("adaptive trees: precision = fast on static (sphere) trees in complex128 only");
     if (prob.dynStart > 0) {
         init_dynamic();
         return;
@@ -2494,7 +2524,15 @@ void AmrTree::run_cycle(const Policy& pol, int n) {
         a.par = l > 0 ? D.lv[l - 1] : D.lv[0];
         a.k = D.kc[l];
         a.partials = D.partials + 2 * static_cast<size_t>(D.normOffs[l]);
-        adev::k_amr_residual<P><<<nb, 256, 0, stream_>>>(a);
+        if (prob_.fast) {
+            for (int s = 0; s < 8; ++s) {
+                const double m = static_cast<double>(1 << (P - __builtin_popcount(static_cast<unsigned>(s) & ((1u << P) - 1))));
+                a.kAsm[s] = make_double2(m * a.k.A[s].x, m * a.k.A[s].y);
+            }
+            adev::k_amr_residual<P, true><<<nb, 256, 0, stream_>>>(a);
+        } else {
+            adev::k_amr_residual<P><<<nb, 256, 0, stream_>>>(a);
+        }
     }
     adev::k_amr_norm_final<<<L_ + 1, 1024, 0, stream_>>>(D.partials, D.dOffs, L_ + 1, D.dNorm);
     AMR_CUDA(cudaGetLastError());

@@ -40,7 +40,7 @@ def hierarchy_for(T, cfg):
     chi = "seeded" if cfg.get("rhs") == "seeded" else ("ball" if cfg["problem"] == "helmholtz-ball" else "sin")
     h = T.Hierarchy(cfg["dim"], cfg["level"], phi=phi, chi=chi, rhs_seed=int(cfg.get("rhs_seed", 12345)),
                     rhs_sphere=cfg.get("rhs_mask") == "sphere", ell_min=int(cfg.get("ell_min", 1)),
-                    precision="exact", max_vertices=10 ** 9, sphere_levels=cfg["sphere_levels"])
+                    precision=cfg.get("precision", "exact"), max_vertices=10 ** 9, sphere_levels=cfg["sphere_levels"])
     if cfg.get("initial") == "random":
         h.set_random_initial_guess(int(cfg.get("seed", 0)))
     pol = T.Policy(kind=cfg.get("omega", "exponential"), omega_s=float(cfg.get("omega_s", 0.8)),
@@ -84,10 +84,13 @@ def test_amr_bit_identical(tmg, name):
                 assert len(bad) == 0, (n, lvl, f, len(bad), bad[:4], zr[bad[:4]], zm[bad[:4]], mr[bad[:4]])
 
 
-def test_amr_rejects_fast_and_fmg(tmg):
+def test_amr_rejects_complex64_and_fmg(tmg):
+    """precision = fast runs on static adaptive trees (test_gpu_amr_fast.py);
+    complex64 storage and FMG unfolding do not."""
     with pytest.raises(Exception):
-        tmg.Hierarchy(3, 2, phi=400 + 200j, chi="seeded", precision="fast", sphere_levels=1)
+        tmg.Hierarchy(3, 2, phi=400 + 200j, chi="seeded", precision="fast-complex64", sphere_levels=1)
     with pytest.raises(Exception):
-        tmg.run(dict(problem="helmholtz-sin", dim=3, level=2, sphere_levels=1, precision="fast", max_sweeps=1))
+        tmg.run(dict(problem="helmholtz-sin", dim=3, level=2, sphere_levels=1, precision="fast-complex64",
+                     max_sweeps=1))
     with pytest.raises(Exception):
         tmg.run(dict(problem="helmholtz-sin", dim=3, level=3, fmg_from=2, sphere_levels=1, max_sweeps=1))
