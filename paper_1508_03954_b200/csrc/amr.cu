@@ -1645,6 +1645,8 @@ struct AmrTree::Dev {
     double* dNorm = nullptr;
     double* hNorm = nullptr;  // pinned, 2 (L+1)
     double* weights = nullptr;
+    std::vector<std::pair<std::string, cudaGraphExec_t>> graphs;  // static-tree cycles (AmrTree::run_cycle)
+    bool graphsBroken = false;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // dynamic adaptivity: writable views of the per-level tables + staging
     struct DynLevel {
@@ -1677,6 +1679,7 @@ struct AmrTree::Dev {
     std::vector<unsigned char> hFlag, hCell;
 
     ~Dev() {
+        for (auto& g : graphs) cudaGraphExecDestroy(g.second);
         for (void* p : allocations) cudaFree(p);
         if (hNorm) cudaFreeHost(hNorm);
         if (ev0) cudaEventDestroy(ev0);
@@ -2489,8 +2492,66 @@ void AmrTree::build_rhs() {
     }
 }
 
+// The static tree's cycle is ~3 (L + 1) small launches; when its arguments do
+// not depend on n (every omega policy but the transition / two-phase ones) it
+// is captured once as a CUDA graph and replayed with one launch (no host-side
+// state changes in a static-tree cycle).  TMG_GRAPH=0: launches.
 template <int P>
 void AmrTree::run_cycle(const Policy& pol, int n) {
+    Dev& D = *dev_;
+    std::string sig;
+    if (dev::switches().graph && !D.graphsBroken) {
+        for (int s = 0; s < 12; ++s) {
+            const Cplx w = omega_unmasked(pol, s, n);
+            if (w != omega_unmasked(pol, s, n + 1)) {
+                sig.clear();
+                break;
+            }
+            sig.append(reinterpret_cast<const char*>(&w), sizeof(w));
+        }
+        if (!sig.empty()) {
+            const int flags[3] = {pol.bpx ? 1 : 0, pol.hbMask ? 1 : 0, prob_.ellMin};
+            sig.append(reinterpret_cast<const char*>(flags), sizeof(flags));
+        }
+    }
+    if (sig.empty()) {
+        run_cycle_launches<P>(pol, n);
+        return;
+    }
+    for (auto& g : D.graphs)
+        if (g.first == sig) {
+            AMR_CUDA(cudaGraphLaunch(g.second, stream_));
+            return;
+        }
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    bool ok = cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+    if (ok) {
+        try {
+            run_cycle_launches<P>(pol, n);
+        } catch (...) {
+            ok = false;
+        }
+        ok = cudaStreamEndCapture(stream_, &graph) == cudaSuccess && ok && graph;
+    }
+    if (ok) ok = cudaGraphInstantiate(&exec, graph, 0) == cudaSuccess;
+    if (graph) cudaGraphDestroy(graph);
+    if (!ok) {
+        (void)cudaGetLastError();
+        D.graphsBroken = true;
+        run_cycle_launches<P>(pol, n);
+        return;
+    }
+    if (D.graphs.size() >= 4) {
+        cudaGraphExecDestroy(D.graphs.front().second);
+        D.graphs.erase(D.graphs.begin());
+    }
+    D.graphs.emplace_back(sig, exec);
+    AMR_CUDA(cudaGraphLaunch(exec, stream_));
+}
+
+template <int P>
+void AmrTree::run_cycle_launches(const Policy& pol, int n) {
     Dev& D = *dev_;
     const int bpx = pol.bpx ? 1 : 0;
     for (int l = 0; l <= L_; ++l) {

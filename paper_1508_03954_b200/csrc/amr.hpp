@@ -109,6 +109,8 @@ class AmrTree {
     template <int P>
     void run_cycle(const Policy& pol, int n);
     template <int P>
+    void run_cycle_launches(const Policy& pol, int n);
+    template <int P>
     void run_cycle_dyn(const Policy& pol, int n);
     template <int P>
     AmrMarkStats mark_dyn();
