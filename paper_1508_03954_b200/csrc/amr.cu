@@ -142,7 +142,10 @@ struct ListWalk {
 
 // ---- top-down: touch_first / create_hanging ----------------------------------
 template <int P, bool STATIC = false>
-__global__ void __launch_bounds__(256, 3) k_amr_topdown(ALvl c, ALvl pr, int bpx) {
+// finestStatic: the finest level of a static tree, where the residual pass
+// restages sc of every non-hanging vertex and no finer top-down reads it -- the
+// top-down's sc is dead there and not stored (the sum still feeds u)
+__global__ void __launch_bounds__(256, 3) k_amr_topdown(ALvl c, ALvl pr, int bpx, int finestStatic = 0) {
     ListWalk w(c);
     for (unsigned i = w.first(); i < c.nlist; i = w.next(i)) {
         const unsigned f = w.f;
@@ -226,7 +229,7 @@ __global__ void __launch_bounds__(256, 3) k_amr_topdown(ALvl c, ALvl pr, int bpx
             uh = cz();
         }
         c.u[f] = u;
-        c.sc[f] = sc;
+        if (!(STATIC && finestStatic)) c.sc[f] = sc;
         c.uhat[f] = uh;
         if (c.sf) c.sf[f] = cz();
     }
@@ -2556,7 +2559,8 @@ void AmrTree::run_cycle_launches(const Policy& pol, int n) {
     const int bpx = pol.bpx ? 1 : 0;
     for (int l = 0; l <= L_; ++l) {
         const adev::ALvl& pr = l > 0 ? D.lv[l - 1] : D.lv[0];
-        adev::k_amr_topdown<P, true><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx);
+        adev::k_amr_topdown<P, true><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx,
+                                                                                               l == L_ ? 1 : 0);
     }
     adev::AResArgs a{};
     a.ellMin = prob_.ellMin;
