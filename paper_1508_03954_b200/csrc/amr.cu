@@ -1650,6 +1650,7 @@ struct AmrTree::Dev {
     double* weights = nullptr;
     std::vector<std::pair<std::string, cudaGraphExec_t>> graphs;  // static-tree cycles (AmrTree::run_cycle)
     bool graphsBroken = false;
+    bool backToBack = false;  // graphs only for cycles issued back to back (time_cycles), as Hierarchy
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // dynamic adaptivity: writable views of the per-level tables + staging
     struct DynLevel {
@@ -2495,15 +2496,16 @@ void AmrTree::build_rhs() {
     }
 }
 
-// The static tree's cycle is ~3 (L + 1) small launches; when its arguments do
-// not depend on n (every omega policy but the transition / two-phase ones) it
-// is captured once as a CUDA graph and replayed with one launch (no host-side
-// state changes in a static-tree cycle).  TMG_GRAPH=0: launches.
+// The static tree's cycle is ~3 (L + 1) small launches; when cycles are issued
+// back to back (time_cycles) and its arguments do not depend on n (every omega
+// policy but the transition / two-phase ones) it is captured once as a CUDA
+// graph and replayed with one launch (no host-side state changes in a
+// static-tree cycle).  TMG_GRAPH=0: launches.
 template <int P>
 void AmrTree::run_cycle(const Policy& pol, int n) {
     Dev& D = *dev_;
     std::string sig;
-    if (dev::switches().graph && !D.graphsBroken) {
+    if (dev::switches().graph && !D.graphsBroken && D.backToBack) {
         for (int s = 0; s < 12; ++s) {
             const Cplx w = omega_unmasked(pol, s, n);
             if (w != omega_unmasked(pol, s, n + 1)) {
@@ -2787,6 +2789,11 @@ void AmrTree::set_random_initial_guess(std::uint64_t seed) {
 void AmrTree::time_cycles(const Policy& pol, int n0, int count, double* out4) {
     Dev& D = *dev_;
     double totalMs = 0.0;
+    D.backToBack = true;
+    struct Reset {
+        bool& b;
+        ~Reset() { b = false; }
+    } reset{D.backToBack};
     for (int i = 0; i < count; ++i) {
         AMR_CUDA(cudaEventRecord(D.ev0, stream_));
         if (p_ == 1) run_cycle<1>(pol, n0 + i);

@@ -840,9 +840,10 @@ struct Hierarchy::Impl {
     // ---- CUDA graphs of the fast cycle ----
     // A fast cycle is a handful of launches whose host-side preparation (omega
     // tables, occupancy queries, argument blocks) and launch latency dominate
-    // the small levels (cfg1: ~4 launches in ~35 us).  When the cycle's
-    // arguments do not depend on n (every omega policy but the n-dependent
-    // transition / two-phase ones), the cycle is captured once per state of the
+    // the small levels (cfg1: ~4 launches in ~35 us).  When cycles are issued
+    // back to back (time_cycles) and the cycle's arguments do not depend on n
+    // (every omega policy but the n-dependent transition / two-phase ones), the
+    // cycle is captured once per state of the
     // double-buffered fine level and replayed with one cudaGraphLaunch; the
     // host-side effects of the captured cycle (buffer swaps, flags) are stored
     // with the graph and reapplied on every replay.
@@ -857,6 +858,11 @@ struct Hierarchy::Impl {
     std::vector<CycleGraph> graphs;
     bool graphsBroken = false;  // a capture failed: ordinary launches from then on
     bool capturing = false;
+    // graphs only for cycles issued back to back (time_cycles): a cycle that
+    // reads its norms back before the next one is issued runs as fast from
+    // launches (measured: 47 vs 45 us per cfg1 cycle) and a short solve would
+    // pay the ~0.5 ms capture
+    bool backToBack = false;
     void clear_graphs() {
         for (CycleGraph& g : graphs)
             if (g.exec) cudaGraphExecDestroy(g.exec);
@@ -1500,7 +1506,8 @@ struct Hierarchy::Impl {
             if (w != omega_unmasked(pol, succ, n + 1)) return std::string();
             put(&w, sizeof(w));
         }
-        const int flags[4] = {pol.bpx ? 1 : 0, pol.hbMask ? 1 : 0, timed ? 1 : 0, prob.ellMin};
+        (void)timed;  // a captured cycle always records the fine-pass events (time_cycles and cycle share it)
+        const int flags[3] = {pol.bpx ? 1 : 0, pol.hbMask ? 1 : 0, prob.ellMin};
         put(flags, sizeof(flags));
         put(&lv[L].u, sizeof(double2*));
         put(&uAlt, sizeof(double2*));
@@ -1508,7 +1515,8 @@ struct Hierarchy::Impl {
     }
 
     void cycle_fast_graph(const Policy& pol, int n, bool timed) {
-        const std::string sig = dev::switches().graph && !graphsBroken ? cycle_signature(pol, n, timed) : std::string();
+        const std::string sig =
+            dev::switches().graph && !graphsBroken && backToBack ? cycle_signature(pol, n, timed) : std::string();
         if (sig.empty()) {
             cycle_fast_dispatch(pol, n, timed);
             return;
@@ -1536,7 +1544,7 @@ struct Hierarchy::Impl {
         if (ok) {
             capturing = true;
             try {
-                cycle_fast_dispatch(pol, n, timed);
+                cycle_fast_dispatch(pol, n, true);
             } catch (...) {
                 ok = false;
             }
@@ -2475,6 +2483,11 @@ void Hierarchy::time_cycles(const Policy& pol, int n0, int count, bool flushL2, 
         I.flushBuf = I.alloc<double4>(I.flushN);
     }
     double totalMs = 0.0, fineMs = 0.0;
+    I.backToBack = true;
+    struct Reset {
+        bool& b;
+        ~Reset() { b = false; }
+    } reset{I.backToBack};
     for (int i = 0; i < count; ++i) {
         if (flushL2) dev::k_flush<<<4 * I.smCount, 256, 0, I.stream>>>(I.flushBuf, I.flushN, 0.0);
         TMG_CUDA(cudaEventRecord(I.ev0, I.stream));
