@@ -30,7 +30,9 @@
  *   fmg_stage_cap = <n>         sweeps per FMG stage (default max_sweeps)
  *   sphere_levels = <k>         static adaptive tree (BASELINE cfg4): `level` regular,
  *                               then k levels refined where the parent cell's centre
- *                               lies in |x - 1/2|^2 < 0.04; hanging vertices; exact only
+ *                               lies in |x - 1/2|^2 < 0.04; hanging vertices; precision
+ *                               exact (bit-identical) or fast (regular vertices' residual
+ *                               as the assembled stencil), not fast-complex64
  *   norms = device | host       host (exact precision only): |r| downloaded and
  *                               summed on the host in the reference's traversal
  *                               order, so CSV/log bytes match the reference
