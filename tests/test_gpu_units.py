@@ -102,3 +102,14 @@ def test_vform_field_api_round_trip(tmg, dim, level):
         b_h.td_add(pol, n)
     b = b_h.td_add(pol, 4)
     assert abs(a.h_norm - b.h_norm) <= 1e-12 * b.h_norm
+
+
+def test_device_memory_exhaustion_is_a_capacity_error(tmg):
+    """A problem past the device's 180 GB (3D depth 7: 10.5 G vertices per fine
+    array) with the vertex cap lifted reports TREEMG_E_CAPACITY through the
+    C-ABI (capi.cpp:28-43's mapping) and leaves the library usable."""
+    with pytest.raises(tmg.TreemgError) as e:
+        tmg.run(dict(problem="helmholtz-sin", dim=3, level=7, precision="fast", max_vertices=10 ** 12, max_sweeps=1))
+    assert e.value.status == 2, e.value
+    r = tmg.run(dict(problem="poisson-sin", dim=2, level=2, max_sweeps=60))
+    assert r.outcome == "converged" and r.sweeps == 28
