@@ -66,6 +66,11 @@ CONFIGS = {
                                       max_sweeps=300),
     "runner_budget_one": dict(problem="poisson-sin", dim=2, level=2, max_sweeps=1, target_drop=1e-30),
     "capi_poisson_l2": dict(problem="poisson-sin", dim=2, level=2, max_sweeps=60),
+    # BASELINE cfg5 exactly as specified (FMG 3 -> 6, k = 80, to a drop of 1e-8 per level): the reference
+    # diverges in its first (27^3) stage, so the golden is cheap
+    "cfg5": dict(problem="helmholtz-sin", dim=3, level=6, fmg_from=3, phi="6400,3200", cycle="td-add",
+                 omega="exponential", omega_s=0.6, max_sweeps=400, target_drop=1e-8, max_vertices=1000000000,
+                 **SEEDED),
     # cfg5 schedule (FMG unfolding) at reduced depth: 3D 2 -> 4 with the cfg5 operator, and converging variants
     "fmg3d_cfg5op": dict(problem="helmholtz-sin", dim=3, level=4, fmg_from=2, phi="6400,3200", cycle="td-add",
                          omega="exponential", omega_s=0.6, max_sweeps=40, fmg_stage_cap=40, target_drop=1e-8,
