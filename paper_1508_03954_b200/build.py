@@ -51,7 +51,7 @@ def build(force: bool = False, verbose: bool = False, out: str = "", defines=())
     if os.path.exists("/usr/bin/g++"):
         base += ["-ccbin", "/usr/bin/g++"]
     flags = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-             "-Xcompiler", "-fPIC,-ffp-contract=off", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
+             "-Xcompiler", "-fPIC,-ffp-contract=off,-fno-semantic-interposition", "-Xptxas", "-v", "-I" + os.path.join(ROOT, "include")]
     flags += ["-D" + d for d in defines]
     tmp = tempfile.mkdtemp(prefix="tmg_build_")
     objs = [os.path.join(tmp, os.path.basename(src) + ".o") for src in srcs]

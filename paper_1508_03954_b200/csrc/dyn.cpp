@@ -467,9 +467,11 @@ void DynTree::visit(int l, const int* c) {
     const size_t cf = static_cast<size_t>(cfl);
     L.cellList.push_back(cfl);
     int v[3] = {0, 0, 0};
-    for (int e = 0; e < nc; ++e) {
+    for (int e = 0; e < nc; ++e) {  // touch_vertex: only a vertex's first touch in this sweep does work
+        const long long f = cfl + L.off[e];
+        if (L.epoch[static_cast<size_t>(f)] == epoch_) continue;
         for (int d = 0; d < p_; ++d) v[d] = c[d] + bit(e, d);
-        touch(l, cfl + L.off[e], v);
+        touch(l, f, v);
     }
     L.entered[cf] = epoch_;
     if (L.cell[cf] & kRM) {
@@ -514,9 +516,14 @@ void DynTree::visit(int l, const int* c) {
             }
         }
     }
-    for (int e = 0; e < nc; ++e) {
+    for (int e = 0; e < nc; ++e) {  // finish_vertex_visit: only the last of the expected visits does work
+        const long long f = cfl + L.off[e];
+        if (static_cast<unsigned char>(L.done[static_cast<size_t>(f)] + 1) != L.expected[static_cast<size_t>(f)]) {
+            ++L.done[static_cast<size_t>(f)];
+            continue;
+        }
         for (int d = 0; d < p_; ++d) v[d] = c[d] + bit(e, d);
-        finish(l, cfl + L.off[e], v, e);
+        finish(l, f, v, e);
     }
 }
 
