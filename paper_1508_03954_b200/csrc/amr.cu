@@ -141,11 +141,14 @@ struct ListWalk {
 };
 
 // ---- top-down: touch_first / create_hanging ----------------------------------
+#ifndef TMG_AMR_TD_MINB
+#define TMG_AMR_TD_MINB 3
+#endif
 template <int P, bool STATIC = false>
 // finestStatic: the finest level of a static tree, where the residual pass
 // restages sc of every non-hanging vertex and no finer top-down reads it -- the
 // top-down's sc is dead there and not stored (the sum still feeds u)
-__global__ void __launch_bounds__(256, 3) k_amr_topdown(ALvl c, ALvl pr, int bpx, int finestStatic = 0) {
+__global__ void __launch_bounds__(256, TMG_AMR_TD_MINB) k_amr_topdown(ALvl c, ALvl pr, int bpx, int finestStatic = 0) {
     ListWalk w(c);
     for (unsigned i = w.first(); i < c.nlist; i = w.next(i)) {
         const unsigned f = w.f;
