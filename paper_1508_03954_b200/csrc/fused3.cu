@@ -187,20 +187,23 @@ __global__ void __launch_bounds__(Cfg<1>::NT, Cfg<1>::MINB)
         vo = (ty + 1) * CX + (qx - cx0);
         wxo = third<S>(x - 3 * qx);
     }
-    const int task = tid < RING ? 1 : (tid < RING + HY * CX ? 2 : 0);  // warp-uniform except one warp
+    // coarse-row tasks take 16 lanes per row from thread VT0 on (bank-conflict-free: see k_fused3_r2)
+    constexpr int VT0 = (RING + 31) / 32 * 32;
+    static_assert(CX <= 16 && VT0 + HY * 16 <= NT, "phase-B task map");
+    const int vs = tid - VT0;
+    const int task = tid < RING ? 1 : ((vs >= 0 && (vs & 15) < CX && (vs >> 4) < HY) ? 2 : 0);
     int pr = 0, vr = 0;
     S wxr = 0;
     bool pinr = false, cpr = false;
     int vcOff = 0;
     double w1y = 0.0;
-    const int vt = tid - RING;
+    const int vt = (vs >> 4) * CX + (vs & 15);
     if (task == 1) {
         const int k = tid;
         int lx, ly;
         if (k < HX) { lx = k; ly = 0; }
         else if (k < 2 * HX) { lx = k - HX; ly = HY - 1; }
-        else if (k < 2 * HX + TY) { lx = 0; ly = 1 + (k - 2 * HX); }
-        else { lx = HX - 1; ly = 1 + (k - 2 * HX - TY); }
+        else { lx = ((k - 2 * HX) & 1) ? HX - 1 : 0; ly = 1 + ((k - 2 * HX) >> 1); }  // halo columns interleaved
         const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
         pinr = gx >= 1 && gx <= m - 1 && gy >= 1 && gy <= m - 1;
         const int qx = min(max(gx, 0) / 3, mc - 1);
@@ -209,7 +212,7 @@ __global__ void __launch_bounds__(Cfg<1>::NT, Cfg<1>::MINB)
         wxr = third<S>(gx - 3 * qx);
         cpr = (gx % 3 == 0) && (gy % 3 == 0);
     } else if (task == 2) {
-        const int ly = vt / CX, ci = vt % CX;
+        const int ly = vs >> 4, ci = vs & 15;
         const int gy = y0 - 1 + ly;
         const int qy = min(max(gy, 0) / 3, mc - 1);
         vcOff = (qy - cy0) * CX + ci;
@@ -513,12 +516,9 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         for (int s = 0; s < STAGES && s < nplanes; ++s) issue(s, z0 - 1 + s);
 
     // ---- per-thread constants ----
-    // Phase B tasks besides the own two points: the NV rows of the z/y-interpolated
-    // coarse plane (threads [0, NV)) and the NRING halo-ring points (threads
-    // [NV, NT) first, then threads [0, ...) a second task).
-    constexpr int NRING = 2 * HX + 2 * TY, NV = HY * CX;
-    static_assert(NV + NRING <= 2 * NT, "phase-B tasks exceed two per thread");
-    static_assert(NV <= NT || NV + NRING <= 2 * NT, "coarse-row tasks");
+    // Phase B tasks besides the own two points: the HY x CX entries of the
+    // z/y-interpolated coarse plane and the NRING halo-ring points (map below).
+    constexpr int NRING = 2 * HX + 2 * TY;
     const int x = x0 + tx;
     const int yr0 = y0 + ROWS * ty;  // the thread's rows yr0, yr0 + 1
     bool owned[2], cpxy[2];
@@ -537,10 +537,18 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
             cpxy[r] = (x % 3 == 0) && (y % 3 == 0);
         }
     }
-    // task slots k = tid and tid + NT of [0, NV + NRING): k < NV a coarse row, else ring point k - NV
-    const int kb = tid + NT;
-    const int rk = tid >= NV ? tid - NV : (kb >= NV && kb < NV + NRING ? kb - NV : -1);  // ring task
-    const int vk2 = (NV > NT && kb < NV) ? kb : -1;  // a second coarse-row task (small blocks)
+    // Bank-conflict-free task map: coarse-row tasks take 16 lanes per row (a
+    // quarter warp never straddles two rows of the same coarse row, whose
+    // elements 8 apart share banks), first the rows [0, NT / 16) on every thread,
+    // the rest on the last warp; ring points on threads [0, NRING), the two halo
+    // columns interleaved (left / right of a row are 33 elements apart: distinct
+    // banks, while the rows of one column are 34 apart: 4 rows wrap the banks).
+    static_assert(CX <= 16 && HY * 16 <= NT + 32 && NRING <= NT, "phase-B task map");
+    const int vly = tid >> 4, vci = tid & 15;
+    const int v2 = tid - (NT - 32);                          // second pass: rows NT / 16 .. on the last warp
+    const int vly2 = (NT + v2) >> 4, vci2 = v2 & 15;
+    const int rk = tid < NRING ? tid : -1;
+    const int vk2 = (v2 >= 0 && vly2 < HY && vci2 < CX) ? vly2 * CX + vci2 : -1;
     int pr = 0, vr = 0;
     S wxr = 0;
     bool pinr = false, cpr = false;
@@ -548,8 +556,7 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         int lx, ly;
         if (rk < HX) { lx = rk; ly = 0; }
         else if (rk < 2 * HX) { lx = rk - HX; ly = HY - 1; }
-        else if (rk < 2 * HX + TY) { lx = 0; ly = 1 + (rk - 2 * HX); }
-        else { lx = HX - 1; ly = 1 + (rk - 2 * HX - TY); }
+        else { lx = ((rk - 2 * HX) & 1) ? HX - 1 : 0; ly = 1 + ((rk - 2 * HX) >> 1); }
         const int gx = x0 - 1 + lx, gy = y0 - 1 + ly;
         pinr = gx >= 1 && gx <= m - 1 && gy >= 1 && gy <= m - 1;
         const int qx = min(max(gx, 0) / 3, mc - 1);
@@ -558,7 +565,7 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         wxr = third<S>(gx - 3 * qx);
         cpr = (gx % 3 == 0) && (gy % 3 == 0);
     }
-    const bool vtask = tid < NV;
+    const bool vtask = vci < CX && vly < HY;
     // coarse-row task k: offset into the coarse tile and the y weight
     auto vparams = [&](int k, int& off, double& w) {
         const int ly = k / CX, ci = k % CX;
@@ -569,7 +576,8 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
     };
     int vcOff = 0;
     double w1y = 0.0;
-    if (vtask) vparams(tid, vcOff, w1y);
+    const int vslot = vly * CX + vci;
+    if (vtask) vparams(vslot, vcOff, w1y);
     auto computeV = [&](int stage, int zz, int vb) {
         const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
         const double w1z = third<double>(rz);
@@ -585,7 +593,7 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
                 Vb[(2 + vb) * M::kV + slot] = to_c(lerpw(b0, b1, w1z), C{});
             }
         };
-        if (vtask) one(vcOff, w1y, tid);
+        if (vtask) one(vcOff, w1y, vslot);
         if (vk2 >= 0) {  // the few threads with a second coarse-row task: parameters on the fly
             int o2;
             double wy2;
