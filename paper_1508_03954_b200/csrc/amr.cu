@@ -463,14 +463,24 @@ __global__ void __launch_bounds__(256) k_amr_chi(ALvl c, ALvl fl, LevelConst k, 
 // adds the terms in the recorded order: the same xadd / xscale sequence as
 // k_amr_chi, bit for bit.
 struct ChiList {
-    int* cnt;               // terms per list position (-1: vertex absent)
+    int* cnt;               // terms per list position (-1: vertex absent, kChiDirect: no stored list)
     int* lcnt;              // leaf terms per list position
     const long long* base;  // per warp group: first term slot
     const long long* lbase; // per warp group: first leaf-value slot
     unsigned* ent;
     double2* leaf;
+    const unsigned char* order;  // direct vertices: weight codes in term order, [perm id][5^P]
+    int direct;                  // record interior kRegularChi vertices as kChiDirect
 };
 constexpr unsigned kLeafCode = 127;  // restriction weight codes are 0 .. 5^P - 1
+// An interior kRegularChi vertex (amr.hpp) has no loads and no finish-corner
+// look-ups: its terms are the 5^P fine vertices 3 g + off, off in [-2, 2]^P, in
+// an order that depends only on its permutation id (cells in perm_cell order,
+// the 3^P lower-corner vertices of each cell lexicographically).  No list is
+// stored for it; k_amr_chi_gather walks the per-id order table instead (the
+// weight code gives the offset: code = sum (off_d + 2) 5^d).  Same terms, same
+// order, same xscale / xadd sequence as the stored list.
+constexpr int kChiDirect = -2;
 
 template <int P, bool WRITE>
 __global__ void __launch_bounds__(256) k_amr_chi_list(ALvl c, ALvl fl, LevelConst k, int restrictOn, ChiList L) {
@@ -499,6 +509,15 @@ __global__ void __launch_bounds__(256) k_amr_chi_list(ALvl c, ALvl fl, LevelCons
         int g[P];
         aunflat<P>(f, c, g);
         const int pid = perm_id<P>(g);
+        if (L.direct && restrictOn && (c.vflag[f] & amr::kRegularChi)) {
+            bool interior = true;
+#pragma unroll
+            for (int d = 0; d < P; ++d) interior &= (g[d] >= 1) & (g[d] <= c.m - 1);
+            if (interior) {  // every term is 3 g + off inside the fine box: walked from the order table
+                if (!WRITE) L.cnt[i] = kChiDirect, L.lcnt[i] = 0;
+                continue;
+            }
+        }
         for (int ic = 0; ic < NC; ++ic) {
             const int e = perm_cell(P, pid, ic);
             int cell[P];
@@ -576,10 +595,37 @@ __global__ void __launch_bounds__(256) k_amr_chi_list(ALvl c, ALvl fl, LevelCons
     }
 }
 
-__global__ void __launch_bounds__(256) k_amr_chi_gather(ALvl c, const double2* __restrict__ frhat,
-                                                        const double* __restrict__ w5, ChiList L) {
+template <int P>
+__global__ void __launch_bounds__(256) k_amr_chi_gather(ALvl c, ALvl fl, const double* __restrict__ w5, ChiList L) {
+    const double2* __restrict__ frhat = fl.rhat;
     for (unsigned i = blockIdx.x * blockDim.x + threadIdx.x; i < c.nlist; i += gridDim.x * blockDim.x) {
         const int n = L.cnt[i];
+        if (n == kChiDirect) {  // interior kRegularChi vertex: the order table instead of a stored list
+            constexpr int K = P == 1 ? 5 : P == 2 ? 25 : 125;
+            const unsigned f = c.list[i];
+            int g[P], v0[P];
+            aunflat<P>(f, c, g);
+            const unsigned char* __restrict__ ord = L.order + perm_id<P>(g) * K;
+#pragma unroll
+            for (int d = 0; d < P; ++d) v0[d] = 3 * g[d];
+            const int fb = aflat<P>(fl, v0);
+            const int sy = P >= 2 ? fl.n1[0] : 0, sz = P >= 3 ? fl.n1[0] * fl.n1[1] : 0;
+            double2 acc = cz();
+            constexpr int B = 5;  // terms in flight (K is a multiple of 5)
+            for (int k0 = 0; k0 < K; k0 += B) {
+                double2 val[B];
+#pragma unroll
+                for (int b = 0; b < B; ++b) {
+                    const int code = ord[k0 + b];
+                    const int off = (code % 5 - 2) + (P >= 2 ? (code / 5 % 5 - 2) * sy : 0) + (P >= 3 ? (code / 25 - 2) * sz : 0);
+                    val[b] = xscale(__ldg(w5 + code), __ldg(frhat + (fb + off)));
+                }
+#pragma unroll
+                for (int b = 0; b < B; ++b) acc = xadd(acc, val[b]);
+            }
+            c.chi[f] = acc;
+            continue;
+        }
         if (n < 0) continue;
         const unsigned* __restrict__ e = L.ent + L.base[i >> 5] + (i & 31);
         const double2* __restrict__ lv = L.leaf + L.lbase[i >> 5] + (i & 31);
@@ -1646,6 +1692,7 @@ struct AmrTree::Dev {
     std::vector<void*> allocations;
     std::vector<int> normOffs;  // block partial offsets per level
     std::vector<adev::ChiList> chiList;  // static trees: per-level chi gather lists (empty: k_amr_chi)
+    const unsigned char* chiOrder = nullptr;  // term order of interior kRegularChi vertices (chi_order_table)
     double* partials = nullptr;
     int* dOffs = nullptr;
     double* dNorm = nullptr;
@@ -1879,6 +1926,8 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
         AMR_CUDA(cudaGetLastError());
     }
     const char* cl = std::getenv("TMG_CHI_LIST");  // developer A/B
+    const char* cd = std::getenv("TMG_CHI_DIRECT");
+    chiDirect_ = !(cd && cd[0] == '0');
     if (!(cl && cl[0] == '0')) {
         if (p_ == 1) build_chi_lists<1>();
         else if (p_ == 2) build_chi_lists<2>();
@@ -1890,6 +1939,41 @@ AmrTree::AmrTree(const Problem& prob, const std::vector<dev::LevelConst>& kc, co
 
 // k_amr_chi_list: count pass, warp-group bases on the host, fill pass (static trees;
 // the leaf terms use nodal, built once by build_rhs)
+// Weight codes of an interior kRegularChi vertex's 5^P terms in traversal order, per
+// permutation id: the loops of k_amr_chi_list's kRegularChi branch with every cell present.
+template <int P>
+const unsigned char* AmrTree::chi_order_table() {
+    Dev& D = *dev_;
+    if (D.chiOrder) return D.chiOrder;
+    constexpr int K = P == 1 ? 5 : P == 2 ? 25 : 125, NC = 1 << P, NT = P == 1 ? 3 : P == 2 ? 9 : 27;
+    constexpr int NID = P == 1 ? 1 : P == 2 ? 2 : 6;
+    std::vector<unsigned char> tab(static_cast<size_t>(NID) * K);
+    for (int pid = 0; pid < NID; ++pid) {
+        int k = 0;
+        for (int ic = 0; ic < NC; ++ic) {
+            const int e = dev::perm_cell(P, pid, ic);
+            for (int t = 0; t < NT; ++t) {
+                int tt = t, code = 0, mul = 1;
+                bool in = true;
+                for (int d = 0; d < P; ++d) {
+                    const int off = 3 * (((e >> d) & 1) - 1) + tt % 3;
+                    tt /= 3;
+                    in = in && off >= -2 && off <= 2;
+                    code += (off + 2) * mul;
+                    mul *= 5;
+                }
+                if (in) tab[static_cast<size_t>(pid) * K + k++] = static_cast<unsigned char>(code);
+            }
+        }
+        if (k != K) throw CudaError("chi order table: term count");
+    }
+    unsigned char* d = D.alloc<unsigned char>(tab.size(), stream_);
+    AMR_CUDA(cudaMemcpyAsync(d, tab.data(), tab.size(), cudaMemcpyHostToDevice, stream_));
+    AMR_CUDA(cudaStreamSynchronize(stream_));
+    D.chiOrder = d;
+    return d;
+}
+
 template <int P>
 void AmrTree::build_chi_lists() {
     Dev& D = *dev_;
@@ -1902,6 +1986,10 @@ void AmrTree::build_chi_lists() {
         adev::ChiList L{};
         L.cnt = D.alloc<int>(c.nlist, stream_);
         L.lcnt = D.alloc<int>(c.nlist, stream_);
+        // thread-per-vertex gathers (k_amr_chi_gather) walk interior kRegularChi vertices from the
+        // order table; the warp-per-vertex gather of small levels keeps stored lists
+        L.direct = (chiDirect_ && c.nlist >= 65536u) ? 1 : 0;
+        L.order = chi_order_table<P>();
         const int nb = blocks_for_n(c.nlist, smCount_);
         adev::k_amr_chi_list<P, false><<<nb, 256, 0, stream_>>>(c, fine, D.kc[l], restrictOn, L);
         AMR_CUDA(cudaGetLastError());
@@ -1915,7 +2003,7 @@ void AmrTree::build_chi_lists() {
         for (size_t w = 0; w < groups; ++w) {
             int mx = 0, lmx = 0;
             for (size_t i = 32 * w; i < std::min<size_t>(32 * w + 32, c.nlist); ++i) {
-                mx = std::max(mx, cnt[i]);
+                mx = std::max(mx, cnt[i]);  // absent (-1) / direct (kChiDirect) positions store nothing
                 lmx = std::max(lmx, lcnt[i]);
             }
             base[w] = tb;
@@ -2584,7 +2672,7 @@ void AmrTree::run_cycle_launches(const Policy& pol, int n) {
                     adev::k_amr_chi_gather_warp<<<blocks_for_n(32LL * D.lv[l].nlist, smCount_), 256, 0, stream_>>>(
                         D.lv[l], fine.rhat, D.weights, D.chiList[l]);
                 else
-                    adev::k_amr_chi_gather<<<nb, 256, 0, stream_>>>(D.lv[l], fine.rhat, D.weights, D.chiList[l]);
+                    adev::k_amr_chi_gather<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.weights, D.chiList[l]);
             }
             else
                 adev::k_amr_chi<P><<<nb, 256, 0, stream_>>>(D.lv[l], fine, D.kc[l], D.weights,

@@ -124,8 +124,11 @@ class AmrTree {
     void build_rhs();
     template <int P>
     void build_chi_lists();
+    template <int P>
+    const unsigned char* chi_order_table();
 
     Problem prob_;
+    bool chiDirect_ = true;  // TMG_CHI_DIRECT=0: stored term lists for every vertex (developer A/B, same bits)
     int p_ = 3, L_ = 1, base_ = 0;
     cudaStream_t stream_;
     int smCount_;

@@ -94,3 +94,37 @@ def test_amr_rejects_complex64_and_fmg(tmg):
                      max_sweeps=1))
     with pytest.raises(Exception):
         tmg.run(dict(problem="helmholtz-sin", dim=3, level=3, fmg_from=2, sphere_levels=1, max_sweeps=1))
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(problem="helmholtz-sin", dim=3, level=4, sphere_levels=2, phi="1600,800", rhs="seeded", rhs_mask="sphere",
+         omega_s=0.6),
+    dict(problem="helmholtz-sin", dim=3, level=4, sphere_levels=2, phi="1600,800", rhs="seeded", cycle="td-bpx",
+         omega="undamped", omega_s=0.5, initial="random", seed=3),
+    dict(problem="helmholtz-sin", dim=2, level=6, sphere_levels=2, phi="10000,5000", rhs="seeded", omega_s=0.6),
+], ids=["cfg4-tree", "cfg4-tree-bpx-random", "2d-base6"])
+def test_direct_chi_gather_bitwise_equal_stored_lists(tmg, cfg):
+    """Levels with >= 65536 listed vertices gather the chi of interior
+    kRegularChi vertices from the per-permutation order table (amr.cu,
+    kChiDirect) instead of a stored term list (TMG_CHI_DIRECT=0): the same terms
+    in the same order, so chi, r-hat, u, u-hat and sc of every level are the
+    same bits (BASELINE cfg4's tree: base 4 + 2 sphere levels; a 2D tree)."""
+    import os
+
+    def run(direct):
+        os.environ["TMG_CHI_DIRECT"] = "1" if direct else "0"
+        try:
+            h, pol = hierarchy_for(tmg, cfg)
+            norms = []
+            for n in range(1, 4):
+                st = h.td_bpx(pol, n) if pol.bpx else h.td_add(pol, n)
+                norms.append((st.max_norm, st.h_norm))
+            return norms, [h.field(l, f) for l in range(h.levels + 1) for f in ("u", "uhat", "sc", "chi", "rhat")]
+        finally:
+            os.environ.pop("TMG_CHI_DIRECT", None)
+
+    na, fa = run(True)
+    nb, fb = run(False)
+    assert na == nb
+    for x, y in zip(fa, fb):
+        assert np.array_equal(x, y)
