@@ -98,13 +98,14 @@ def fine_bytes_per_vertex(w, precision):
 
 def moved_bytes_per_vertex(w, precision):
     """Bytes per fine vertex the implementation's fine pass actually has to move:
-    the fused passes read v and b and write v (v-form, the write-only fine sc is
-    re-derived on demand: fused3.cuh derive_u) -- 48 B, 24 B in complex64."""
+    the fused 3D pass reads v and b and writes v (v-form, the write-only fine sc is
+    re-derived on demand: fused3.cuh derive_u) -- 48 B, 24 B in complex64; the
+    fused 2D pass also stores the fine sc -- 64 B, 32 B in complex64."""
     if precision == "exact":
         return 176
     if precision == "fast-complex64":
-        return 24
-    return 48 if w["dim"] >= 2 else 128
+        return 24 if w["dim"] == 3 else 32
+    return 48 if w["dim"] == 3 else 64 if w["dim"] == 2 else 128
 
 
 def algorithmic_bytes(w, precision):
@@ -122,7 +123,9 @@ def fine_kernel_label(w, precision):
         return ("fused fine pass k_fused3<complex64> (TMA ring: top-down + residual + smooth + z/xy restriction)"
                 if precision == "fast-complex64" else
                 "fused fine pass k_fused3 (TMA ring: top-down + residual + smooth + z/xy restriction)")
-    return "fused fine pass k_fused2 (row-marching strips: top-down + residual + smooth + restriction)"
+    return ("fused fine pass k_fused2<complex64> (row-marching strips: top-down + residual + smooth + restriction)"
+            if precision == "fast-complex64" else
+            "fused fine pass k_fused2 (row-marching strips: top-down + residual + smooth + restriction)")
 
 
 def ncu_traffic(workload: str, precision: str, mode: str):

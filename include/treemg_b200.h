@@ -22,7 +22,7 @@
  *                               exact: bit-identical iterates to the reference
  *                               fast: FMA, correction-form coarse levels
  *                               fast-complex64: fast with the finest level stored
- *                               and computed in complex64 (3D; coarse levels and
+ *                               and computed in complex64 (2D / 3D; coarse levels and
  *                               norm sums complex128 / double)
  *   max_vertices = <n>          vertex cap (reference default 8388608)
  *   hb_sweeps = <k>             hierarchical-basis mask for sweeps 1..k, then off
@@ -77,7 +77,7 @@ typedef struct tmg_problem {
                                       78-90; exact precision) */
     unsigned long long rhs_seed;
     int rhs_sphere;
-    int precision;                 /* 0 exact, 1 fast, 2 fast-complex64 (3D: complex64 fine level) */
+    int precision;                 /* 0 exact, 1 fast, 2 fast-complex64 (2D / 3D: complex64 fine level) */
     long long max_vertices;        /* 0: reference default 8388608 */
     int device;                    /* CUDA device ordinal */
     int sphere_levels;             /* static adaptive tree: `levels` regular, then this many levels refined

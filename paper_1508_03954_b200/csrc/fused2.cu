@@ -12,26 +12,41 @@ namespace fused2 {
 
 namespace {
 
-__device__ __forceinline__ double2 zero2() { return make_double2(0.0, 0.0); }
-__device__ __forceinline__ double2 add(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 sub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-__device__ __forceinline__ double2 mul(double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+// ---- complex arithmetic on double2 (complex128) and float2 (complex64), as fused3.cu ----
+template <class S> struct Cx;
+template <> struct Cx<double> { using T = double2; };
+template <> struct Cx<float> { using T = float2; };
+__device__ __forceinline__ double2 mk(double x, double y) { return make_double2(x, y); }
+__device__ __forceinline__ float2 mk(float x, float y) { return make_float2(x, y); }
+template <class C> __device__ __forceinline__ C zero();
+template <> __device__ __forceinline__ double2 zero<double2>() { return make_double2(0.0, 0.0); }
+template <> __device__ __forceinline__ float2 zero<float2>() { return make_float2(0.f, 0.f); }
+__device__ __forceinline__ double2 zero2() { return zero<double2>(); }
+template <class C> __device__ __forceinline__ C add(C a, C b) { return mk(a.x + b.x, a.y + b.y); }
+template <class C> __device__ __forceinline__ C sub(C a, C b) { return mk(a.x - b.x, a.y - b.y); }
+template <class C> __device__ __forceinline__ C mul(C a, C b) {
+    return mk(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
 }
-__device__ __forceinline__ double2 mac(double2 acc, double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
+template <class C> __device__ __forceinline__ C mac(C acc, C a, C b) {
+    return mk(fma(a.x, b.x, fma(-a.y, b.y, acc.x)), fma(a.x, b.y, fma(a.y, b.x, acc.y)));
 }
-__device__ __forceinline__ double2 axpy(double w, double2 v, double2 acc) {
-    return make_double2(fma(w, v.x, acc.x), fma(w, v.y, acc.y));
+template <class C, class S> __device__ __forceinline__ C axpy(S w, C v, C acc) {
+    return mk(fma(w, v.x, acc.x), fma(w, v.y, acc.y));
 }
-__device__ __forceinline__ double2 lerpw(double2 c0, double2 c1, double w1) {
-    return make_double2(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
+template <class C, class S> __device__ __forceinline__ C lerpw(C c0, C c1, S w1) {
+    return mk(fma(w1, c1.x - c0.x, c0.x), fma(w1, c1.y - c0.y, c0.y));
 }
 __device__ __forceinline__ double relw(int r) { return r == 1 ? (1.0 / 3.0) : r == 2 ? (2.0 / 3.0) : (r == 3 ? 1.0 : 0.0); }
+// complex128 <-> the kernel's complex type
+__device__ __forceinline__ double2 to_c(double2 v, double2) { return v; }
+__device__ __forceinline__ float2 to_c(double2 v, float2) { return make_float2(static_cast<float>(v.x), static_cast<float>(v.y)); }
+__device__ __forceinline__ double2 to_d(double2 v) { return v; }
+__device__ __forceinline__ double2 to_d(float2 v) { return make_double2(v.x, v.y); }
 
-__device__ __forceinline__ double2 stage_sc(double2 smooth, double2 w, bool cp, int bpx, int hb) {
-    if (bpx) return cp ? zero2() : mul(w, smooth);
-    if ((hb && cp) || (w.x == 0.0 && w.y == 0.0)) return zero2();
+template <class C>
+__device__ __forceinline__ C stage_sc(C smooth, C w, bool cp, int bpx, int hb) {
+    if (bpx) return cp ? zero<C>() : mul(w, smooth);
+    if ((hb && cp) || (w.x == 0 && w.y == 0)) return zero<C>();
     return mul(w, smooth);
 }
 
@@ -71,17 +86,25 @@ __device__ __forceinline__ void rbar_wait(unsigned long long* bar, unsigned pari
         : "memory");
 }
 
-template <bool BPX>
+// S = double: complex128; S = float: the finest level stored and computed in
+// complex64 (precision = fast-complex64), coarse values / partials / norms in double.
+// Bulk copies need 16-byte aligned addresses and sizes: x0 - 1 and every row
+// length are even, so complex64 rows of v start aligned; its b rows are copied
+// from x0 - 1 as well (BOFF = 1: one leading element the kernel skips).
+template <bool BPX, class S>
 __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
+    using C = typename Cx<S>::T;
+    constexpr int BOFF = sizeof(C) == 8 ? 1 : 0;
+    constexpr int TXB = TX + 2 * BOFF;
     dev::griddep_wait();
-    __shared__ double2 Pb[2][TX + 2];          // corrected rows (x halo at 0 and TX+1)
-    __shared__ double2 Vb[BPX ? 4 : 2][CXW];   // y-interpolated coarse rows (sc[, si])
-    __shared__ double2 tb[TX];                 // y-restricted columns
+    __shared__ C Pb[2][TX + 2];                // corrected rows (x halo at 0 and TX+1)
+    __shared__ C Vb[BPX ? 4 : 2][CXW];         // y-interpolated coarse rows (sc[, si])
+    __shared__ C tb[TX];                       // y-restricted columns
     __shared__ unsigned long long rbar[kRing]; // row ring: one mbarrier per slot (bulk copies)
-    extern __shared__ __align__(16) double2 dyn[];
-    auto Ru = reinterpret_cast<double2(*)[TX + 2]>(dyn);                    // row ring: v (own columns + x halo)
-    auto Rb = reinterpret_cast<double2(*)[TX]>(dyn + kRing * (TX + 2));      // row ring: b
-    double2* Cs = dyn + kRing * (2 * TX + 2);  // coarse-row ring: sc [4][CXW] (+ si [4][CXW])
+    extern __shared__ __align__(16) unsigned char dynRaw[];
+    auto Ru = reinterpret_cast<C(*)[TX + 2]>(dynRaw);                                        // row ring: v (own columns + x halo)
+    auto Rb = reinterpret_cast<C(*)[TXB]>(dynRaw + kRing * (TX + 2) * sizeof(C));            // row ring: b
+    double2* Cs = reinterpret_cast<double2*>(dynRaw + kRing * (TX + 2 + TXB) * sizeof(C));  // coarse-row ring: sc [4][CXW] (+ si [4][CXW])
 
     const int tid = threadIdx.x;
     const int m = a.g.m, mc = a.g.mc;
@@ -96,7 +119,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     // own column: coarse interpolation slot and weight
     const int qxo = min(x / 3, mc - 1);
     const int vo = qxo - cx0;
-    const double wxo = relw(x - 3 * qxo);
+    const S wxo = static_cast<S>(relw(x - 3 * qxo));
     const bool cpx = x % 3 == 0;
     // halo columns (threads 0 and 1): x0 - 1 and xe
     // per-row side tasks spread over the warps (the row barrier waits for the
@@ -107,7 +130,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     const bool hin = haloThread && hx >= 1 && hx <= m - 1;
     const int hq = min(max(hx, 0) / 3, mc - 1);
     const int hv = hq - cx0;
-    const double hw = relw(hx - 3 * hq);
+    const S hw = static_cast<S>(relw(hx - 3 * hq));
     const bool hcpx = hx % 3 == 0;
     const int hslot = tid == kHaloT ? 0 : (xe - x0) + 1;
     const int ct = tid - kCvT;  // coarse-row task: coarse column cx0 + ct
@@ -135,8 +158,8 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         const double w1y = relw(yy - 3 * qy);
         const double2* c0 = Cs + (qy & 3) * CXW + ct;
         const double2* c1 = Cs + ((qy + 1) & 3) * CXW + ct;
-        Vb[vb][ct] = lerpw(c0[0], c1[0], w1y);
-        if (BPX) Vb[2 + vb][ct] = lerpw(c0[4 * CXW], c1[4 * CXW], w1y);
+        Vb[vb][ct] = to_c(lerpw(c0[0], c1[0], w1y), C{});
+        if (BPX) Vb[2 + vb][ct] = to_c(lerpw(c0[4 * CXW], c1[4 * CXW], w1y), C{});
     };
 
     // restriction slots of this strip
@@ -150,26 +173,26 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     auto flush = [&](int zi) {
         if (ti < nsx) {
             const int X = Xa + ti;
-            double2 acc = zero2();
+            C acc = zero<C>();
 #pragma unroll
             for (int kx = -2; kx <= 2; ++kx) {
                 const int fx = 3 * X + kx;
                 if (fx < x0 || fx >= xe) continue;
-                const double wx = kx == 0 ? 1.0 : (kx == 1 || kx == -1) ? (2.0 / 3.0) : (1.0 / 3.0);
+                const S wx = static_cast<S>(kx == 0 ? 1.0 : (kx == 1 || kx == -1) ? (2.0 / 3.0) : (1.0 / 3.0));
                 acc = axpy(wx, tb[fx - x0], acc);
             }
-            part[zi * zStride + ti] = acc;
+            part[zi * zStride + ti] = to_d(acc);
         }
     };
     bool pend = false;
     int ziPend = 0;
 
-    const double2 k0 = a.k.c[0], k1 = a.k.c[1], k2 = a.k.c[2];
+    const C k0 = to_c(a.k.c[0], C{}), k1 = to_c(a.k.c[1], C{}), k2 = to_c(a.k.c[2], C{});
     const bool zeroSc = a.level < a.ellMin;
     const bool injectOK = BPX && a.level > a.ellMin && cpx && owned;
     double nmax = 0.0, nsum = 0.0;
-    double2 accLo = zero2(), accHi = zero2();
-    double2 Aprev = zero2(), Acur = zero2();
+    C accLo = zero<C>(), accHi = zero<C>();
+    C Aprev = zero<C>(), Acur = zero<C>();
 
     // Row ring: row yy's state v = u + sc (fused3.cuh "v-form") over the strip
     // and its halo columns [x0 - 1, xe], and its load vector b over [x0, xe),
@@ -184,7 +207,10 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-    const unsigned uBytes = static_cast<unsigned>(xe - x0 + 2) * 16u, bBytes = static_cast<unsigned>(xe - x0) * 16u;
+    const unsigned uBytes = static_cast<unsigned>(xe - x0 + 2) * static_cast<unsigned>(sizeof(C)),
+                   bBytes = static_cast<unsigned>(xe - x0 + 2 * BOFF) * static_cast<unsigned>(sizeof(C));
+    const C* gU = static_cast<const C*>(static_cast<const void*>(a.u));
+    const C* gB = static_cast<const C*>(static_cast<const void*>(a.b));
     const int cCount = min(CXW, mc + 1 - cx0);
     auto issueRow = [&](int it2, auto U3) {  // thread 0; U3: (y0 - 1 + it2) % 3
         constexpr int uu = decltype(U3)::value;
@@ -196,8 +222,8 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         const unsigned tx = (yin ? uBytes : 0u) + (bin ? bBytes : 0u) + (BPX ? 2u : 1u) * cb;
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(&rbar[slot])), "r"(tx) : "memory");
         const long long row = n1 * yy;
-        if (yin) bulk_row(&Ru[slot][0], a.u + (x0 - 1) + row, uBytes, &rbar[slot]);
-        if (bin) bulk_row(&Rb[slot][0], a.b + x0 + row, bBytes, &rbar[slot]);
+        if (yin) bulk_row(&Ru[slot][0], gU + (x0 - 1) + row, uBytes, &rbar[slot]);
+        if (bin) bulk_row(&Rb[slot][0], gB + (x0 - BOFF) + row, bBytes, &rbar[slot]);
         if (coarse) {
             const long long g = cx0 + static_cast<long long>(a.n1c) * q;
             bulk_row(Cs + (q & 3) * CXW, a.scC + g, cb, &rbar[slot]);
@@ -212,37 +238,37 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         if (nrows > 1) issueRow(1, U1{});
         if (nrows > 2) issueRow(2, U2{});
     }
-    double2 cPrev = zero2();
-    double2 bq = zero2();
+    C cPrev = zero<C>();
+    C bq = zero<C>();
     computeV(y0 - 1, 0);
     __syncthreads();
 
-    double2* uOut = a.uNew + x + n1 * y0;  // row yy - 1 of the residual steps (it >= 2), advanced by each
-    double2* scOut = a.scNew + x + n1 * y0;
-    const double2 wRaw = a.k.wRaw, invDiag = a.k.invDiag;
+    C* uOut = static_cast<C*>(static_cast<void*>(a.uNew)) + x + n1 * y0;  // row yy - 1 of the residual steps (it >= 2), advanced by each
+    C* scOut = static_cast<C*>(static_cast<void*>(a.scNew)) + x + n1 * y0;
+    const C wRaw = to_c(a.k.wRaw, C{}), invDiag = to_c(a.k.invDiag, C{});
     auto step = [&](int it, auto U3) {
         constexpr int u3 = decltype(U3)::value;  // yy % 3
         constexpr int kz = (u3 + 2) % 3;         // (yy - 1) % 3
         const int yy = y0 - 1 + it;
         const bool yin = yy >= 1 && yy <= m - 1;
         rbar_wait(&rbar[it & (kRing - 1)], static_cast<unsigned>(it / kRing) & 1u);  // row yy landed
-        const double2 uC = Ru[it & (kRing - 1)][tid + 1];
-        const double2 huC = haloThread ? Ru[it & (kRing - 1)][hslot] : zero2();
-        if (it >= 2) bq = Rb[(it + kRing - 1) & (kRing - 1)][tid];  // b of row yy - 1 (the residual row)
-        const double2* V = Vb[it & 1];
-        double2* P = Pb[it & 1];
+        const C uC = Ru[it & (kRing - 1)][tid + 1];
+        const C huC = haloThread ? Ru[it & (kRing - 1)][hslot] : zero<C>();
+        if (it >= 2) bq = Rb[(it + kRing - 1) & (kRing - 1)][tid + BOFF];  // b of row yy - 1 (the residual row)
+        const C* V = Vb[it & 1];
+        C* P = Pb[it & 1];
         // ---- phase B: corrected row yy ----
-        double2 cOwn = zero2();
+        C cOwn = zero<C>();
         if (yin && owned) {
-            double2 scv = lerpw(V[vo], V[vo + 1], wxo);
+            C scv = lerpw(V[vo], V[vo + 1], wxo);
             if (BPX && !(cpx && u3 == 0)) scv = sub(scv, lerpw(Vb[2 + (it & 1)][vo], Vb[2 + (it & 1)][vo + 1], wxo));
             cOwn = add(uC, scv);
         }
         if (owned) P[tid + 1] = cOwn;
         if (haloThread) {
-            double2 c = zero2();
+            C c = zero<C>();
             if (yin && hin) {
-                double2 scv = lerpw(V[hv], V[hv + 1], hw);
+                C scv = lerpw(V[hv], V[hv + 1], hw);
                 if (BPX && !(hcpx && u3 == 0)) scv = sub(scv, lerpw(Vb[2 + (it & 1)][hv], Vb[2 + (it & 1)][hv + 1], hw));
                 c = add(huC, scv);
             }
@@ -257,36 +283,36 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
             flush(ziPend);
             pend = false;
         }
-        const double2 E = add(P[tid], P[tid + 2]);
-        double2 T = mul(k1, cOwn);
+        const C E = add(P[tid], P[tid + 2]);
+        C T = mul(k1, cOwn);
         T = mac(T, k2, E);
-        double2 U = mul(k0, cOwn);
+        C U = mul(k0, cOwn);
         U = mac(U, k1, E);
         if (it >= 2) {
-            const double2 hu = add(Aprev, T);
-            const double2 r = owned ? sub(bq, hu) : zero2();
-            const double m2 = fma(r.x, r.x, r.y * r.y);
-            nmax = fmax(nmax, m2);
-            nsum += m2;
-            const double2 smooth = mul(r, invDiag);
-            const double2 scn = zeroSc ? zero2() : stage_sc(smooth, wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
+            const C hu = add(Aprev, T);
+            const C r = owned ? sub(bq, hu) : zero<C>();
+            const S m2 = fma(r.x, r.x, r.y * r.y);
+            nmax = fmax(nmax, static_cast<double>(m2));
+            nsum += static_cast<double>(m2);
+            const C smooth = mul(r, invDiag);
+            const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);
             if (owned) {
                 if (a.writeSc) *scOut = scn;
                 *uOut = add(cPrev, scn);  // next state v of row yy - 1
             }
             if (BPX && kz == 0 && injectOK)
-                a.sinextC[x / 3 + static_cast<long long>(a.n1c) * ((yy - 1) / 3)] = mul(wRaw, smooth);
+                a.sinextC[x / 3 + static_cast<long long>(a.n1c) * ((yy - 1) / 3)] = to_d(mul(wRaw, smooth));
             if (kz == 0) {
                 accLo = add(accLo, r);
             } else if (kz == 1) {
-                accLo = axpy(2.0 / 3.0, r, accLo);
-                accHi = axpy(1.0 / 3.0, r, accHi);
+                accLo = axpy(static_cast<S>(2.0 / 3.0), r, accLo);
+                accHi = axpy(static_cast<S>(1.0 / 3.0), r, accHi);
             } else {
-                accLo = axpy(1.0 / 3.0, r, accLo);
-                accHi = axpy(2.0 / 3.0, r, accHi);
+                accLo = axpy(static_cast<S>(1.0 / 3.0), r, accLo);
+                accHi = axpy(static_cast<S>(2.0 / 3.0), r, accHi);
                 tb[tid] = accLo;
                 accLo = accHi;
-                accHi = zero2();
+                accHi = zero<C>();
                 pend = true;  // x-reduction on the next row's barrier
                 ziPend = zLow - zBase;
                 ++zLow;
@@ -320,9 +346,12 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
 }
 
 // derive_u: k_fused2's phase B for one point, from global memory
-__global__ void __launch_bounds__(256) k_derive_u2(const double2* __restrict__ vOld, const double2* __restrict__ scTD,
-                                                   const double2* __restrict__ siTD, unsigned n1, unsigned n1c,
-                                                   unsigned fa, unsigned fb, double2* __restrict__ uOut) {
+template <class S>
+__global__ void __launch_bounds__(256) k_derive_u2(const typename Cx<S>::T* __restrict__ vOld,
+                                                   const double2* __restrict__ scTD, const double2* __restrict__ siTD,
+                                                   unsigned n1, unsigned n1c, unsigned fa, unsigned fb,
+                                                   double2* __restrict__ uOut) {
+    using C = typename Cx<S>::T;
     const int m = static_cast<int>(n1) - 1, mc = static_cast<int>(n1c) - 1;
     for (unsigned f = fa + blockIdx.x * blockDim.x + threadIdx.x; f < fb; f += gridDim.x * blockDim.x) {
         const int y = static_cast<int>(f / n1), x = static_cast<int>(f - static_cast<unsigned>(y) * n1);
@@ -331,16 +360,17 @@ __global__ void __launch_bounds__(256) k_derive_u2(const double2* __restrict__ v
             continue;
         }
         const int qx = min(x / 3, mc - 1), qy = min(y / 3, mc - 1);
-        const double w1y = relw(y - 3 * qy), wx = relw(x - 3 * qx);
-        auto prolong = [&](const double2* src) {  // computeV (y), then x
+        const double w1y = relw(y - 3 * qy);
+        const S wx = static_cast<S>(relw(x - 3 * qx));
+        auto prolong = [&](const double2* src) {  // computeV (y, stored in the kernel's precision), then x
             const double2* c = src + qx + static_cast<long long>(n1c) * qy;
-            const double2 v0 = lerpw(__ldg(c), __ldg(c + n1c), w1y);
-            const double2 v1 = lerpw(__ldg(c + 1), __ldg(c + 1 + n1c), w1y);
+            const C v0 = to_c(lerpw(__ldg(c), __ldg(c + n1c), w1y), C{});
+            const C v1 = to_c(lerpw(__ldg(c + 1), __ldg(c + 1 + n1c), w1y), C{});
             return lerpw(v0, v1, wx);
         };
-        double2 scv = prolong(scTD);
+        C scv = prolong(scTD);
         if (siTD && !(x % 3 == 0 && y % 3 == 0)) scv = sub(scv, prolong(siTD));
-        uOut[f] = add(__ldg(vOld + f), scv);
+        uOut[f] = to_d(add(__ldg(vOld + f), scv));
     }
 }
 
@@ -397,7 +427,7 @@ Geometry geometry(int m, int mc, int smCount) {
     const int inner = std::max(1, m - 1);
     g.nbx = (inner + TX - 1) / TX;
     int per = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused2<false>, TX, 0) != cudaSuccess || per < 1) per = 4;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_fused2<false, double>, TX, 0) != cudaSuccess || per < 1) per = 4;
     const int resident = 2 * per * std::max(1, smCount);  // two waves of strips
     const int want = std::max(1, (resident + g.nbx - 1) / g.nbx);
     g.yc = std::min(kMaxYc, std::max(3, ((inner + want - 1) / want + 2) / 3 * 3));  // cap: staged coarse rows
@@ -410,27 +440,41 @@ size_t partial_count(const Geometry& g) { return static_cast<size_t>(g.nby) * g.
 
 int blocks(const Geometry& g) { return g.nbx * g.nby; }
 
-size_t smem_bytes(const Geometry& g, bool bpx) {
+size_t smem_bytes(const Geometry& g, bool bpx, bool c64) {
     (void)g;
-    return (static_cast<size_t>(kRing) * (2 * TX + 2) + static_cast<size_t>(bpx ? 8 : 4) * CXW) * sizeof(double2);
+    const size_t rows = c64 ? static_cast<size_t>(kRing) * (2 * TX + 4) * sizeof(float2)   // v rows + b rows (from x0 - 1)
+                            : static_cast<size_t>(kRing) * (2 * TX + 2) * sizeof(double2);
+    return rows + static_cast<size_t>(bpx ? 8 : 4) * CXW * sizeof(double2);
 }
 
 void derive_u(const double2* vOld, const double2* scTD, const double2* siTD, unsigned n1, unsigned n1c, unsigned fa,
-              unsigned fb, double2* uOut, cudaStream_t s) {
+              unsigned fb, double2* uOut, bool c64, cudaStream_t s) {
     if (fb <= fa) return;
     const unsigned blocks = std::min<unsigned>((fb - fa + 255) / 256, 148u * 32u);
-    k_derive_u2<<<blocks, 256, 0, s>>>(vOld, scTD, siTD, n1, n1c, fa, fb, uOut);
+    if (c64)
+        k_derive_u2<float><<<blocks, 256, 0, s>>>(reinterpret_cast<const float2*>(vOld), scTD, siTD, n1, n1c, fa, fb, uOut);
+    else
+        k_derive_u2<double><<<blocks, 256, 0, s>>>(vOld, scTD, siTD, n1, n1c, fa, fb, uOut);
+}
+
+template <bool BPX, class S>
+static void launch_as(const Args& a, dim3 grid, size_t smem, cudaStream_t s) {
+    // static + dynamic shared memory may pass 48 KB (BPX, long chunks); a per-device
+    // attribute, so set on every launch (host-side call)
+    cudaFuncSetAttribute(k_fused2<BPX, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024);
+    dev::launch_k(k_fused2<BPX, S>, grid, dim3(TX), smem, s, a);
 }
 
 void launch(const Args& a, cudaStream_t s) {
     dim3 grid(a.g.nbx, a.g.nby);
-    const size_t smem = smem_bytes(a.g, a.bpx != 0);
-    // static + dynamic shared memory may pass 48 KB (BPX, long chunks); a per-device
-    // attribute, so set on every launch (host-side call)
-    cudaFuncSetAttribute(a.bpx ? k_fused2<true> : k_fused2<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         96 * 1024);
-    if (a.bpx) dev::launch_k(k_fused2<true>, grid, dim3(TX), smem, s, a);
-    else dev::launch_k(k_fused2<false>, grid, dim3(TX), smem, s, a);
+    const size_t smem = smem_bytes(a.g, a.bpx != 0, a.c64 != 0);
+    if (a.c64) {
+        if (a.bpx) launch_as<true, float>(a, grid, smem, s);
+        else launch_as<false, float>(a, grid, smem, s);
+    } else {
+        if (a.bpx) launch_as<true, double>(a, grid, smem, s);
+        else launch_as<false, double>(a, grid, smem, s);
+    }
 }
 
 void combine(const Args& a, double2* rCoarse, cudaStream_t s, const fast::ResArgs* smooth) {

@@ -49,12 +49,13 @@ struct Args {
     fast::LevelCoef k;
     int bpx, hb, ellMin, level;
     int writeSc;          // store the fine sc (else re-derived on demand: derive_u)
+    int c64;              // u / uNew / scNew / b hold complex64 (float2) behind the double2 pointers
 };
 
 Geometry geometry(int m, int mc, int smCount);
 // fused3::derive_u for the 2D pass (its phase B: y, then x interpolation)
 void derive_u(const double2* vOld, const double2* scTD, const double2* siTD, unsigned n1, unsigned n1c, unsigned fa,
-              unsigned fb, double2* uOut, cudaStream_t s);
+              unsigned fb, double2* uOut, bool c64, cudaStream_t s);
 size_t partial_count(const Geometry& g);
 int blocks(const Geometry& g);
 void launch(const Args& a, cudaStream_t s);

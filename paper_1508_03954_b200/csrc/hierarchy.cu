@@ -1307,6 +1307,7 @@ struct Hierarchy::Impl {
             // the 2D pass is bound by its per-row barrier, not by HBM: it keeps the
             // stored fine sc (no derive, no si copy for td-bpx)
             fa.writeSc = 1;
+            fa.c64 = prob.c64 ? 1 : 0;
             fused2::launch(fa, stream);
             if (timed) record(evf1);
             if (use_up()) {  // combine + level L-1 smoothing, then the whole bottom-up in one launch
@@ -1459,7 +1460,7 @@ struct Hierarchy::Impl {
     void derive_fine_u(double2* out, unsigned fa, unsigned fb) {
         const dev::Lvl& F = lv[L];
         const double2* si = derivedBpx ? siTD : nullptr;
-        if (p == 2) fused2::derive_u(uAlt, scTD, si, F.n1, lv[L - 1].n1, fa, fb, out, stream);
+        if (p == 2) fused2::derive_u(uAlt, scTD, si, F.n1, lv[L - 1].n1, fa, fb, out, prob.c64, stream);
         else fused3::derive_u(uAlt, scTD, si, F.n1, lv[L - 1].n1, fa, fb, out, prob.c64, stream);
         TMG_CUDA(cudaGetLastError());
     }
@@ -1861,8 +1862,10 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     }
     if (prob.c64) {
         if (!prob.fast) throw ConfigError("complex64 storage is a fast-precision mode");
-        if (I.p != 3 || !I.fineFused || prob.channels > 1 || prob.gaussian)
-            throw UnsupportedConfigError("precision = fast-complex64 runs the 3D fused fine pass (dim = 3, one channel)");
+        if ((I.p != 3 && I.p != 2) || !I.fineFused || prob.channels > 1 || prob.gaussian)
+            throw UnsupportedConfigError(
+                "precision = fast-complex64 runs the fused fine passes (dim = 2 with level >= 3, dim = 3 with level >= 2; "
+                "one channel)");
     }
     if (I.slab()) {
         if (!prob.fast || I.p != 3 || !I.fineFused || prob.c64 || prob.channels > 1 || I.L < 3)
@@ -1902,7 +1905,7 @@ Hierarchy::Hierarchy(const Problem& prob) : impl_(new Impl()) {
     }
     I.partials = I.alloc<double>(2 * static_cast<size_t>(I.normBlocks) * prob.channels);
     if (I.fused2on) {
-        I.uAlt = I.alloc<double2>(I.lv[I.L].n);
+        I.uAlt = prob.c64 ? reinterpret_cast<double2*>(I.alloc<float2>(I.lv[I.L].n)) : I.alloc<double2>(I.lv[I.L].n);
         I.partial2 = I.alloc<double2>(fused2::partial_count(I.geo2));
         I.scTD = I.alloc<double2>(I.lv[I.L - 1].n);
         I.siTD = I.alloc<double2>(I.lv[I.L - 1].n);

@@ -61,7 +61,7 @@ struct Problem {
     bool rhsSphere = false;
     int rhsLattice = -1;  // level the seeded rhs is keyed on (-1: levels)
     bool fast = false;    // precision = fast
-    bool c64 = false;     // precision = fast-complex64: fine level in complex64 storage / arithmetic (3D)
+    bool c64 = false;     // precision = fast-complex64: fine level in complex64 storage / arithmetic (2D / 3D fused passes)
     bool hostNorms = false;  // norms = host: reference-order sums of |r| on the host (exact mode)
     int zParts = 1;          // fused fine pass: z-chunks come in multiples of this (z-slabs)
     bool gaussian = false;   // 2D gaussian scenario: per-cell phi and absorbing-layer theta (exact only)
