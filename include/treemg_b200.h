@@ -26,7 +26,8 @@
  *                               norm sums complex128 / double)
  *   max_vertices = <n>          vertex cap (reference default 8388608)
  *   hb_sweeps = <k>             hierarchical-basis mask for sweeps 1..k, then off
- *   fmg_from = <level>          FMG unfolding from <level> up to `level`
+ *   fmg_from = <level>          FMG unfolding from <level> up to `level` (fast-complex64: the
+ *                               stages below `level` run in complex128)
  *   fmg_stage_cap = <n>         sweeps per FMG stage (default max_sweeps)
  *   sphere_levels = <k>         static adaptive tree (BASELINE cfg4): `level` regular,
  *                               then k levels refined where the parent cell's centre

@@ -2433,12 +2433,13 @@ void test_divdc3(const double* x, const double* y, double* out, long long n) {
 // existing levels' u / sc / sf / si, and re-classifies (succ = L+1-l).  The
 // canonical-parent prolongation used here equals the creating cell's for
 // every vertex (coinciding components are exact copies, transfer.cpp:26-38).
-void Hierarchy::unfold() {
+void Hierarchy::unfold(bool toComplex64) {
     if (impl_->amr) throw UnsupportedConfigError("FMG unfolding is not available on adaptive trees");
-    if (impl_->prob.c64) throw UnsupportedConfigError("FMG unfolding runs in complex128 (precision = fast | exact)");
+    if (impl_->prob.c64) throw UnsupportedConfigError("FMG unfolding: only the final level may be complex64");
     Impl& old = *impl_;
     Problem p2 = old.prob;
     p2.levels = old.L + 1;
+    p2.c64 = toComplex64;
     if (p2.rhsLattice < 0) p2.rhsLattice = p2.levels;
     if (old.fineDerived) {  // the old finest level becomes a coarse level: (u, sc) with the derived u
         old.split_fine(true);
@@ -2464,11 +2465,14 @@ void Hierarchy::unfold() {
         copy(b.si, a.si);
         copy(b.sinext, a.sinext);
     }
-    const dev::Lvl& F = nw.lv[L + 1];
+    Impl::Tmp t;
+    // complex64 fine level: prolonged in complex128 into a stand-in, then stored as complex64
+    const dev::Lvl F = nw.prob.c64 ? c64_stage(nw, t) : nw.lv[L + 1];
     if (nw.p == 1) dev::k_prolong_new<1><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L], 0u, F.n);
     else if (nw.p == 2) dev::k_prolong_new<2><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L], 0u, F.n);
     else dev::k_prolong_new<3><<<nw.blocks_for(F.n), 256, 0, nw.stream>>>(F, nw.lv[L], 0u, F.n);
     TMG_CUDA(cudaGetLastError());
+    if (nw.prob.c64) store_fine_u(nw, F);
     nw.coarseUStale = nw.prob.fast;
     TMG_CUDA(cudaStreamSynchronize(nw.stream));
     std::swap(impl_, deeper.impl_);

@@ -149,7 +149,9 @@ class Hierarchy {
     // Adds one uniformly refined level on top (FMG unfolding through
     // refine_cell of every leaf + classify()): the new
     // level's u is p-linearly prolonged, its other payload zero.
-    void unfold();
+    // toComplex64: the new finest level in complex64 (FMG's last unfolding of a precision = fast-complex64 run;
+    // the stages below it run in complex128)
+    void unfold(bool toComplex64 = false);
 
     // Timing helpers (CUDA events on the hierarchy stream).
     void time_cycles(const Policy& pol, int n0, int count, bool flushL2, double* out4);

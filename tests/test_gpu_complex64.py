@@ -130,13 +130,39 @@ def test_complex64_run_matches_golden_outcome(tmg):
 @pytest.mark.parametrize("cfg", [
     dict(problem="helmholtz-sin", dim=1, level=4, phi="100,50"),
     dict(problem="helmholtz-sin", dim=2, level=2, phi="100,50"),
-    dict(problem="helmholtz-sin", dim=3, level=4, fmg_from=2, phi="400,200"),
+    dict(problem="helmholtz-sin", dim=1, level=4, fmg_from=2, phi="100,50"),
     dict(problem="helmholtz-sin", dim=3, level=3, cycle="bu-fas", phi="400,200"),
 ])
 def test_complex64_unsupported_modes_fail_loudly(tmg, cfg):
     with pytest.raises(tmg.TreemgError) as e:
         tmg.run(dict(cfg, precision="fast-complex64", max_sweeps=3))
     assert e.value.status == 1
+
+
+@pytest.mark.parametrize("cfg", [
+    dict(dim=3, level=4, fmg_from=2, phi="400,200", fmg_stage_cap=8, max_sweeps=30),
+    dict(dim=3, level=5, fmg_from=3, phi="400,200", fmg_stage_cap=6, max_sweeps=20),
+    dict(dim=2, level=6, fmg_from=3, phi="10000,5000", cycle="td-bpx", omega="undamped", omega_s=0.5,
+         fmg_stage_cap=6, max_sweeps=30),
+], ids=["3d-2to4", "3d-3to5", "2d-3to6-bpx"])
+def test_complex64_fmg_final_level(tmg, cfg):
+    """FMG with precision = fast-complex64: the stages below the final level
+    run in complex128 (rows bitwise those of precision = fast), the last
+    unfolding prolongs into a complex64 finest level (Hierarchy::unfold(true));
+    its rows within the complex64 gate of the complex128 run, same sweep
+    counts (stages capped so both runs unfold at the same sweeps)."""
+    base = dict(dict(problem="helmholtz-sin", rhs="seeded", rhs_seed=12345, target_drop=1e-30, omega_s=0.6,
+                     max_vertices=10 ** 9), **cfg)
+    a = tmg.run(dict(base, precision="fast"))
+    b = tmg.run(dict(base, precision="fast-complex64"))
+    assert (a.outcome, a.sweeps) == (b.outcome, b.sweeps)
+    assert np.array_equal(a.history[:, :3], b.history[:, :3])
+    lead = (int(cfg["level"]) - int(cfg["fmg_from"])) * int(cfg["fmg_stage_cap"])  # sweeps below the final level
+    assert np.array_equal(a.history[:lead, 3:], b.history[:lead, 3:])
+    rel = np.abs(b.history[lead:, 3:] - a.history[lead:, 3:]) / a.history[lead:, 3:]
+    print(f"FMG {cfg['dim']}D {cfg['fmg_from']} -> {cfg['level']}: complex64 final level vs complex128, "
+          f"{a.sweeps - lead} cycles: max rel {rel.max():.2e}")
+    assert a.sweeps > lead and np.all(rel <= C64_NORM_TOL), rel.max()
 
 
 def test_complex64_field_roundtrip(tmg):
