@@ -828,10 +828,23 @@ struct Hierarchy::Impl {
             if (p) cudaFree(p);
         }
     };
+    // complex64 hierarchies convert on their hot paths (the load vector of every new right-hand
+    // side, field export): they keep one stand-in for the hierarchy's lifetime instead of a
+    // cudaMalloc / cudaFree of the whole lattice per call (6.2 GB at 729^3); complex128
+    // hierarchies (and slab members, which must stay at 1 / N of the memory) allocate transiently
+    double2* tmpFineKept = nullptr;
     double2* tmp_fine(Tmp& t) {
-        TMG_CUDA(cudaMalloc(&t.p, static_cast<size_t>(lv[L].n) * sizeof(double2)));
-        TMG_CUDA(cudaMemsetAsync(t.p, 0, static_cast<size_t>(lv[L].n) * sizeof(double2), stream));
-        return t.p;
+        const size_t bytes = static_cast<size_t>(lv[L].n) * sizeof(double2);
+        double2* p = nullptr;
+        if (prob.c64) {
+            if (!tmpFineKept) tmpFineKept = alloc<double2>(lv[L].n);
+            p = tmpFineKept;
+        } else {
+            TMG_CUDA(cudaMalloc(&t.p, bytes));
+            p = t.p;
+        }
+        TMG_CUDA(cudaMemsetAsync(p, 0, bytes, stream));
+        return p;
     }
     int clusterSize = 0;  // CTAs of a chain cluster (0: grid chains only)
     static constexpr unsigned long long kClusterMaxPts = 1ull << 18;
