@@ -102,6 +102,38 @@ __device__ __forceinline__ int aflat(const ALvl& c, const int* g) {
     return f;
 }
 
+// aunflat with the divisions by the box extents as multiply-high by
+// M = ceil(2^64 / n1) (exact for 32-bit operands; Lemire & Kaser 2019): the two
+// magic numbers are formed once per thread, the per-vertex cost is two
+// 64-bit multiply-highs instead of two 32-bit divisions and remainders.
+template <int P>
+struct FastUnflat {
+    unsigned long long m0 = 0, m1 = 0;
+    unsigned n0 = 1, n1 = 1;
+    int lo[3] = {0, 0, 0};
+    __device__ explicit FastUnflat(const ALvl& c) {
+        n0 = static_cast<unsigned>(c.n1[0]);
+        n1 = P >= 2 ? static_cast<unsigned>(c.n1[1]) : 1u;
+        m0 = n0 > 1 ? ~0ull / n0 + 1ull : 0ull;  // n = 1: quotient is f itself (handled below)
+        m1 = n1 > 1 ? ~0ull / n1 + 1ull : 0ull;
+#pragma unroll
+        for (int d = 0; d < P; ++d) lo[d] = c.lo[d];
+    }
+    __device__ __forceinline__ void operator()(unsigned f, int* g) const {
+        const unsigned q0 = n0 > 1 ? static_cast<unsigned>(__umul64hi(m0, f)) : f;
+        g[0] = lo[0] + static_cast<int>(f - q0 * n0);
+        if (P == 1) return;
+        if (P == 2) {
+            g[1] = lo[1] + static_cast<int>(q0);  // aunflat takes q0 % n1[1]; q0 < n1[1] inside the box
+            return;
+        }
+        const unsigned q1 = n1 > 1 ? static_cast<unsigned>(__umul64hi(m1, q0)) : q0;
+        g[1] = lo[1] + static_cast<int>(q0 - q1 * n1);
+        // the last axis: aunflat takes q1 % n1[2]; q1 < n1[2] for every index inside the box
+        g[2] = lo[2] + static_cast<int>(q1);
+    }
+};
+
 // Grid-stride walk over a level's vertex list with the list entry loaded two
 // iterations ahead and the vertex's flags one ahead: the per-vertex chain
 // list -> flags -> data was three dependent memory latencies per iteration.
@@ -150,12 +182,66 @@ template <int P, bool STATIC = false>
 // top-down's sc is dead there and not stored (the sum still feeds u)
 __global__ void __launch_bounds__(256, TMG_AMR_TD_MINB) k_amr_topdown(ALvl c, ALvl pr, int bpx, int finestStatic = 0) {
     ListWalk w(c);
+    const FastUnflat<P> unflat(c);
     for (unsigned i = w.first(); i < c.nlist; i = w.next(i)) {
         const unsigned f = w.f;
         const unsigned char vf = w.vf;
         w.prefetch(i);
         if (!(vf & amr::kExists)) continue;
         const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging;
+        if (STATIC && c.level > 0 && (vf & amr::kParentsAll) && !hang) {
+            // Static tree, every parent corner present, regular vertex: the same values
+            // and operations as the general path below with less bookkeeping.  The parent
+            // cell is taken as q = g / 3 with rel = g % 3 in {0, 1, 2} (at the upper
+            // boundary the general path's (q - 1, rel 3) names the same corner q as
+            // (q, rel 0)); an axis with rel 0 reads its lower corner twice (stride 0)
+            // and copies it, so the interpolation needs one exact-copy select instead
+            // of two and no existence look-ups.
+            int g[P];
+            unflat(f, g);
+            int q[P], rel[P];
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                q[d] = g[d] / 3;
+                rel[d] = g[d] - 3 * q[d];
+            }
+            const int p0 = aflat<P>(pr, q);
+            const int s0 = rel[0] ? 1 : 0;
+            const int s1 = (P >= 2 && rel[P >= 2 ? 1 : 0]) ? pr.n1[0] : 0;
+            const int s2 = (P == 3 && rel[P == 3 ? 2 : 0]) ? pr.n1[0] * pr.n1[1] : 0;
+            auto prolong012 = [&](const double2* __restrict__ src) {
+                double2 v[1 << P];
+#pragma unroll
+                for (int e = 0; e < (1 << P); ++e)
+                    v[e] = src[p0 + (e & 1) * s0 + ((e >> 1) & 1) * s1 + ((e >> 2) & 1) * s2];
+#pragma unroll
+                for (int d = 0; d < P; ++d) {
+                    const double w0 = rel[d] == 1 ? (2.0 / 3.0) : (1.0 / 3.0);
+                    const double w1 = rel[d] == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
+#pragma unroll
+                    for (int k = 0; k < (1 << (P - 1 - d)); ++k) {
+                        const double2 r = xadd(xscale(w0, v[2 * k]), xscale(w1, v[2 * k + 1]));  // lerp_rel
+                        v[k] = rel[d] == 0 ? v[2 * k] : r;
+                    }
+                }
+                return v[0];
+            };
+            const double2 pu = prolong012(pr.u);
+            double2 sc = xadd(c.sc[f], prolong012(pr.sc));
+            if (bpx && !cp) sc = xsub(sc, prolong012(pr.si));
+            const double2 sf = c.sf ? c.sf[f] : cz();
+            double2 u = xadd(c.u[f], xadd(sc, sf));
+            double2 uh = xsub(u, pu);
+            if (bnd) {
+                u = cz();
+                uh = cz();
+            }
+            c.u[f] = u;
+            if (!finestStatic) c.sc[f] = sc;
+            c.uhat[f] = uh;
+            if (c.sf) c.sf[f] = cz();
+            continue;
+        }
         if (c.level == 0) {  // cycles.cpp:128-133
             double2 u = xadd(c.u[f], xadd(c.sc[f], c.sf ? c.sf[f] : cz()));
             if (bnd) u = cz();
@@ -842,6 +928,7 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
     const ALvl& c = a.lv;
     double nmax = 0.0, nsum = 0.0;
     ListWalk w(c);
+    const FastUnflat<P> unflat(c);
     for (unsigned i = w.first(); i < c.nlist; i = w.next(i)) {
         const unsigned f = w.f;
         const unsigned char vf = w.vf;
@@ -851,7 +938,7 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
         const bool bnd = vf & amr::kBoundary, cp = vf & amr::kCPoint, hang = vf & amr::kHanging,
                    refined = vf & amr::kRefined;
         int g[P];
-        aunflat<P>(f, c, g);
+        unflat(f, g);
         const int pid = perm_id<P>(g);
         double2 r = cz(), rh = cz();
         bool first = true;
