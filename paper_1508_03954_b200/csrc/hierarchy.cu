@@ -58,26 +58,57 @@ struct ResArgs {
 // ---- K1: top-down update (touch_first, cycles.cpp:102-141) ----------------
 template <int P>
 __global__ void __launch_bounds__(256) k_topdown(Lvl c, Lvl pr, int bpx) {
+    // The parent cell is taken as q = idx / 3 with rel = idx % 3 in {0, 1, 2}: at the upper
+    // boundary parent_stencil's (q - 1, rel 3) names the same corner q as (q, rel 0).  An
+    // axis with rel 0 reads its lower corner twice (stride 0) and copies it exactly
+    // (transfer.cpp:20-40), so the interpolation needs one exact-copy select, not two.
+    // The lattice index is split by multiply-high with M = ceil(2^64 / n1) (exact for
+    // 32-bit operands) instead of divisions.  Values and operation order are unchanged.
+    const unsigned n1 = c.n1, pn1 = pr.n1;
+    const unsigned long long M = ~0ull / n1 + 1ull;
     for (unsigned f = blockIdx.x * blockDim.x + threadIdx.x; f < c.n; f += gridDim.x * blockDim.x) {
         int idx[P];
-        unflat<P>(f, c.n1, idx);
-        int q[P], rel[P];
+        {
+            unsigned r = f;
+#pragma unroll
+            for (int d = 0; d + 1 < P; ++d) {
+                const unsigned qd = static_cast<unsigned>(__umul64hi(M, r));
+                idx[d] = static_cast<int>(r - qd * n1);
+                r = qd;
+            }
+            idx[P - 1] = static_cast<int>(r);
+        }
+        int rel[P];
+        unsigned p0 = 0, ps = 1, str[P];
 #pragma unroll
         for (int d = 0; d < P; ++d) {
-            q[d] = min(idx[d] / 3, static_cast<int>(pr.m) - 1);
-            rel[d] = idx[d] - 3 * q[d];
+            const int q = idx[d] / 3;
+            rel[d] = idx[d] - 3 * q;
+            p0 += static_cast<unsigned>(q) * ps;
+            str[d] = rel[d] ? ps : 0u;
+            ps *= pn1;
         }
         // one field at a time (register footprint): P sc, P si (BPX), P u
-        auto parent_prolong = [&](const double2* src) {
+        auto parent_prolong = [&](const double2* __restrict__ src) {
             double2 v[1 << P];
 #pragma unroll
             for (int e = 0; e < (1 << P); ++e) {
-                int pi[P];
+                unsigned o = p0;
 #pragma unroll
-                for (int d = 0; d < P; ++d) pi[d] = q[d] + ((e >> d) & 1);
-                v[e] = src[flat<P>(pi, pr.n1)];
+                for (int d = 0; d < P; ++d) o += ((e >> d) & 1) ? str[d] : 0u;
+                v[e] = src[o];
             }
-            return prolong<P>(v, rel);
+#pragma unroll
+            for (int d = 0; d < P; ++d) {
+                const double w0 = rel[d] == 1 ? (2.0 / 3.0) : (1.0 / 3.0);
+                const double w1 = rel[d] == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
+#pragma unroll
+                for (int k = 0; k < (1 << (P - 1 - d)); ++k) {
+                    const double2 r = xadd(xscale(w0, v[2 * k]), xscale(w1, v[2 * k + 1]));  // lerp_rel
+                    v[k] = rel[d] == 0 ? v[2 * k] : r;
+                }
+            }
+            return v[0];
         };
         double2 sc = xadd(c.sc[f], parent_prolong(pr.sc));
         if (bpx && !is_cpoint<P>(idx)) sc = xsub(sc, parent_prolong(pr.si));
