@@ -939,11 +939,12 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
                    refined = vf & amr::kRefined;
         int g[P];
         unflat(f, g);
-        const int pid = perm_id<P>(g);
         double2 r = cz(), rh = cz();
         bool first = true;
         int ncell = NC;
         const bool general = hang || bnd;
+        // the traversal order of the cells around g: not needed by the assembled stencil
+        const int pid = (FAST && !general) ? 0 : perm_id<P>(g);
         if (!general) {  // every cell around g exists
             const int sy = c.n1[0], sz = c.n1[0] * c.n1[1];
             if (FAST) {
