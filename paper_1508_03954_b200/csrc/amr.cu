@@ -77,6 +77,7 @@ struct AResArgs {
     int ellMin, bpx, hb;
     double* partials;
     double2 kAsm[8];  // precision = fast: assembled stencil entry per offset class s, 2^(P - |s|) A[s]
+    double2 invDiag;  // precision = fast: 1 / (the diagonal after 2^P cells), Jacobi as a complex multiply
 };
 
 template <int P>
@@ -1013,7 +1014,10 @@ __global__ void __launch_bounds__(256, TMG_AMR_RES_MINB) k_amr_residual(AResArgs
             c.sc[f] = cz();
             continue;
         }
-        const double2 smooth = bnd ? cz() : divdc3(r.x, r.y, a.k.div);
+        const double2 smooth =
+            bnd ? cz()
+                : FAST ? make_double2(fma(r.x, a.invDiag.x, -r.y * a.invDiag.y), fma(r.x, a.invDiag.y, r.y * a.invDiag.x))
+                       : divdc3(r.x, r.y, a.k.div);
         const double2 wRaw = a.wTab[c.succ[f]];
         double2 sc;
         if (a.bpx) {
@@ -2775,6 +2779,8 @@ void AmrTree::run_cycle_launches(const Policy& pol, int n) {
                 const double m = static_cast<double>(1 << (P - __builtin_popcount(static_cast<unsigned>(s) & ((1u << P) - 1))));
                 a.kAsm[s] = make_double2(m * a.k.A[s].x, m * a.k.A[s].y);
             }
+            const Cplx inv = Cplx(1.0) / diag_[static_cast<size_t>(l)];  // the interior diagonal kc[l].div divides by
+            a.invDiag = make_double2(inv.real(), inv.imag());
             adev::k_amr_residual<P, true><<<nb, 256, 0, stream_>>>(a);
         } else {
             adev::k_amr_residual<P><<<nb, 256, 0, stream_>>>(a);
