@@ -177,7 +177,9 @@ struct ListWalk {
 #ifndef TMG_AMR_TD_MINB
 #define TMG_AMR_TD_MINB 3
 #endif
-template <int P, bool STATIC = false>
+template <int P, bool STATIC = false, bool FAST = false>
+// FAST (precision = fast on static trees): the regular vertices' interpolation as
+// fma(rel / 3, c1 - c0, c0) -- no exact-copy select (weight 0 copies c0), within rounding
 // finestStatic: the finest level of a static tree, where the residual pass
 // restages sc of every non-hanging vertex and no finer top-down reads it -- the
 // top-down's sc is dead there and not stored (the sum still feeds u)
@@ -221,8 +223,14 @@ __global__ void __launch_bounds__(256, TMG_AMR_TD_MINB) k_amr_topdown(ALvl c, AL
                     const double w1 = rel[d] == 1 ? (1.0 / 3.0) : (2.0 / 3.0);
 #pragma unroll
                     for (int k = 0; k < (1 << (P - 1 - d)); ++k) {
-                        const double2 r = xadd(xscale(w0, v[2 * k]), xscale(w1, v[2 * k + 1]));  // lerp_rel
-                        v[k] = rel[d] == 0 ? v[2 * k] : r;
+                        if (FAST) {
+                            const double wr = rel[d] == 0 ? 0.0 : w1;
+                            v[k] = make_double2(fma(wr, v[2 * k + 1].x - v[2 * k].x, v[2 * k].x),
+                                                fma(wr, v[2 * k + 1].y - v[2 * k].y, v[2 * k].y));
+                        } else {
+                            const double2 r = xadd(xscale(w0, v[2 * k]), xscale(w1, v[2 * k + 1]));  // lerp_rel
+                            v[k] = rel[d] == 0 ? v[2 * k] : r;
+                        }
                     }
                 }
                 return v[0];
@@ -2744,7 +2752,8 @@ void AmrTree::run_cycle_launches(const Policy& pol, int n) {
     const int bpx = pol.bpx ? 1 : 0;
     for (int l = 0; l <= L_; ++l) {
         const adev::ALvl& pr = l > 0 ? D.lv[l - 1] : D.lv[0];
-        adev::k_amr_topdown<P, true><<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx,
+        (prob_.fast ? adev::k_amr_topdown<P, true, true> : adev::k_amr_topdown<P, true, false>)
+            <<<blocks_for_n(D.lv[l].nlist, smCount_), 256, 0, stream_>>>(D.lv[l], pr, bpx,
                                                                                                l == L_ ? 1 : 0);
     }
     adev::AResArgs a{};
