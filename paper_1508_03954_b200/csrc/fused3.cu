@@ -578,9 +578,8 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
     double w1y = 0.0;
     const int vslot = vly * CX + vci;
     if (vtask) vparams(vslot, vcOff, w1y);
-    auto computeV = [&](int stage, int zz, int vb) {
-        const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
-        const double w1z = third<double>(rz);
+    // w1z: the z weight of plane zz between its two coarse planes (the caller knows zz % 3)
+    auto computeV = [&](int stage, double w1z, int vb) {
         const double2* Cc = coarse(stage);
         auto one = [&](int o, double wy, int slot) {
             const double2 a0 = lerpw(Cc[o], Cc[o + CX], wy);
@@ -677,7 +676,10 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
     const C invDiag = to_c(a.k.invDiag, C{}), wRaw = to_c(a.k.wRaw, C{});
 
     mbar_wait(&bar[0], 0);
-    computeV(0, z0 - 1, 0);
+    {
+        const int zf = z0 - 1, cz = min(zf / 3, mc - 1);
+        computeV(0, third<double>(zf - 3 * cz), 0);
+    }
     __syncthreads();
 
     C Aprev[2] = {zero<C>(), zero<C>()}, Acur[2] = {zero<C>(), zero<C>()};
@@ -721,7 +723,9 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
             }
             P[pr] = (zin && pinr) ? add(Ut[pr], scv) : zero<C>();
         }
-        if (hasNext) computeV(nstage, zz + 1, (it + 1) & 1);
+        // plane zz + 1 has residue (u + 1) % 3; the top lattice plane m = 3 mc sits on the
+        // last coarse plane of the clamped pair (weight 1)
+        if (hasNext) computeV(nstage, zz + 1 == m ? 1.0 : third<double>((u + 1) % 3), (it + 1) & 1);
         __syncthreads();
         if (tid == 0 && it + STAGES < nplanes) issue(stage, zz + STAGES);
         stage = nstage;
@@ -761,7 +765,7 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
                 const C hu = add(Aprev[r], T);
                 const C res = owned[r] ? sub(bq[r], hu) : zero<C>();
                 const S m2 = fma(res.x, res.x, res.y * res.y);
-                nmax = fmax(nmax, static_cast<double>(m2));
+                nmax = static_cast<double>(m2) > nmax ? static_cast<double>(m2) : nmax;  // == fmax (a NaN is ignored)
                 nsum += static_cast<double>(m2);
                 const C smooth = mul(res, invDiag);
                 const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpxy[r] && kz == 0, BPX ? 1 : 0, a.hb);
