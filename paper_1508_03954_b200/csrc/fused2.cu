@@ -152,10 +152,11 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
         issueCoarse(q0 + 1);
         asm volatile("cp.async.wait_all;" ::: "memory");
     }
-    auto computeV = [&](int yy, int vb) {  // coarse rows of fine row yy, for coarse columns cx0 + ct
+    // coarse rows of fine row yy, for coarse columns cx0 + ct; w1y: the row's weight between
+    // its two coarse rows (the caller knows yy % 3)
+    auto computeV = [&](int yy, double w1y, int vb) {
         if (ct < 0 || ct >= CXW) return;
         const int qy = min(max(yy, 0) / 3, mc - 1);
-        const double w1y = relw(yy - 3 * qy);
         const double2* c0 = Cs + (qy & 3) * CXW + ct;
         const double2* c1 = Cs + ((qy + 1) & 3) * CXW + ct;
         Vb[vb][ct] = to_c(lerpw(c0[0], c1[0], w1y), C{});
@@ -240,7 +241,10 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
     }
     C cPrev = zero<C>();
     C bq = zero<C>();
-    computeV(y0 - 1, 0);
+    {
+        const int yf = y0 - 1, qf = min(max(yf, 0) / 3, mc - 1);
+        computeV(yf, relw(yf - 3 * qf), 0);
+    }
     __syncthreads();
 
     C* uOut = static_cast<C*>(static_cast<void*>(a.uNew)) + x + n1 * y0;  // row yy - 1 of the residual steps (it >= 2), advanced by each
@@ -274,7 +278,8 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
             }
             P[hslot] = c;
         }
-        if (it + 1 < nrows) computeV(yy + 1, (it + 1) & 1);
+        // row yy + 1 has residue (u3 + 1) % 3; the top lattice row m = 3 mc takes weight 1
+        if (it + 1 < nrows) computeV(yy + 1, yy + 1 == m ? 1.0 : relw((u3 + 1) % 3), (it + 1) & 1);
         __syncthreads();
         // every thread has read row yy - 1's slot: refill it with row yy + 3 (same residue)
         if (tid == 0 && it + kRing - 1 < nrows) issueRow(it + kRing - 1, U3);
@@ -292,7 +297,7 @@ __global__ void __launch_bounds__(TX) k_fused2(const Args a) {
             const C hu = add(Aprev, T);
             const C r = owned ? sub(bq, hu) : zero<C>();
             const S m2 = fma(r.x, r.x, r.y * r.y);
-            nmax = fmax(nmax, static_cast<double>(m2));
+            nmax = static_cast<double>(m2) > nmax ? static_cast<double>(m2) : nmax;  // == fmax (a NaN is ignored)
             nsum += static_cast<double>(m2);
             const C smooth = mul(r, invDiag);
             const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpx && kz == 0, BPX ? 1 : 0, a.hb);

@@ -219,9 +219,8 @@ __global__ void __launch_bounds__(Cfg<1>::NT, Cfg<1>::MINB)
         w1y = third<double>(gy - 3 * qy);
     }
     // the coarse (complex128) correction interpolated in y and z, stored in the kernel's precision
-    auto computeV = [&](int stage, int zz, int vb) {
-        const int cz = min(zz / 3, mc - 1), rz = zz - 3 * cz;
-        const double w1z = third<double>(rz);
+    // w1z: the z weight of plane zz between its two coarse planes (the caller knows zz % 3)
+    auto computeV = [&](int stage, double w1z, int vb) {
         const double2* Cc = coarse(stage);
         const double2 a0 = lerpw(Cc[vcOff], Cc[vcOff + CX], w1y);
         const double2 a1 = lerpw(Cc[vcOff + CX * CY], Cc[vcOff + CX * CY + CX], w1y);
@@ -324,7 +323,10 @@ __global__ void __launch_bounds__(Cfg<1>::NT, Cfg<1>::MINB)
     const C invDiag = to_c(a.k.invDiag, C{}), wRaw = to_c(a.k.wRaw, C{});
 
     mbar_wait(&bar[0], 0);
-    if (task == 2) computeV(0, z0 - 1, 0);
+    if (task == 2) {
+        const int zf = z0 - 1, cz = min(zf / 3, mc - 1);
+        computeV(0, third<double>(zf - 3 * cz), 0);
+    }
     __syncthreads();
 
     // running stencil accumulators: Aprev = H u at plane p-1 minus its plane-p terms, Acur = plane p's so far
@@ -363,7 +365,8 @@ __global__ void __launch_bounds__(Cfg<1>::NT, Cfg<1>::MINB)
             }
             P[pr] = (zin && pinr) ? add(Ut[pr], scv) : zero<C>();
         } else if (task == 2 && hasNext) {
-            computeV(nstage, zz + 1, (it + 1) & 1);
+            // plane zz + 1 has residue (u + 1) % 3; the top lattice plane m = 3 mc takes weight 1
+            computeV(nstage, zz + 1 == m ? 1.0 : third<double>((u + 1) % 3), (it + 1) & 1);
         }
         __syncthreads();
         if (tid == 0 && it + STAGES < nplanes) issue(stage, zz + STAGES);
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(Cfg<1>::NT, Cfg<1>::MINB)
             bPtr += sz;
             if (owned && zz < z1) bq0 = ld(bPtr);
             const S m2 = fma(r.x, r.x, r.y * r.y);
-            nmax = fmax(nmax, static_cast<double>(m2));
+            nmax = static_cast<double>(m2) > nmax ? static_cast<double>(m2) : nmax;  // == fmax (a NaN is ignored)
             nsum += static_cast<double>(m2);
             const C smooth = mul(r, invDiag);
             const C scn = zeroSc ? zero<C>() : stage_sc(smooth, wRaw, cpxy && kz == 0, BPX ? 1 : 0, a.hb);
