@@ -111,8 +111,12 @@ struct Smem {
     static constexpr int kV = (HY * CX + 7) / 8 * 8;  // z- and y-interpolated coarse rows (elements of C)
     static constexpr int kP = (HX * HY + 7) / 8 * 8;  // corrected plane (elements of C)
     // R = 2: the b tile of the plane the step's residual is for (32 x TY, no halo), TMA'd with the stage
-    static constexpr int kBt = R == 2 ? (TX * TY * static_cast<int>(sizeof(C)) + 127) / 128 * 128 : 0;
-    static constexpr unsigned kBtBytes = R == 2 ? TX * TY * sizeof(C) : 0;
+    // complex64: the b tile starts one column early (x0 - 1, even: the TMA box start is then 16-byte
+    // aligned as for complex128) and is two columns wider; the kernel skips the leading column
+    static constexpr int kBOff = sizeof(C) == 8 ? 1 : 0;
+    static constexpr int kBW = TX + 2 * kBOff;  // b tile row length
+    static constexpr int kBt = R == 2 ? (kBW * TY * static_cast<int>(sizeof(C)) + 127) / 128 * 128 : 0;
+    static constexpr unsigned kBtBytes = R == 2 ? kBW * TY * sizeof(C) : 0;
     template <bool BPX>
     __host__ __device__ static constexpr int stage() { return kPlane + (BPX ? 2 : 1) * kC + kBt; }
     template <bool BPX>
@@ -507,7 +511,7 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         tma_load3(st, &mapU, xScale * (x0 - 1), y0 - 1, zz - a.tmaZ0, &bar[stage]);
         tma_load3(st + M::kPlane, &mapC, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
         if (BPX) tma_load3(st + M::kPlane + M::kC, &mapI, 2 * cx0, cy0, cz - a.tmaZ0c, &bar[stage]);
-        tma_load3(st + kBtOff, &mapB, xScale * x0, y0, zz - 1 - a.tmaZ0, &bar[stage]);
+        tma_load3(st + kBtOff, &mapB, xScale * (x0 - M::kBOff), y0, zz - 1 - a.tmaZ0, &bar[stage]);
     };
 
     if (tid == 0) {
@@ -704,7 +708,7 @@ __global__ void __launch_bounds__(Cfg<2>::NT, Cfg<2>::MINB)
         {  // b of plane zz - 1, read before the stage is refilled
             const C* Bt = reinterpret_cast<const C*>(ring + stage * SB + kBtOff);
 #pragma unroll
-            for (int r = 0; r < 2; ++r) bq[r] = Bt[(ROWS * ty + r) * TX + tx];
+            for (int r = 0; r < 2; ++r) bq[r] = Bt[(ROWS * ty + r) * M::kBW + tx + M::kBOff];
         }
         // ---- phase B ----
         C cOwn[2];
@@ -989,7 +993,8 @@ bool encode_map(CUtensorMap* map, const void* base, unsigned n1, int kind, bool 
     const cuuint64_t es = f32 ? 4 : 8;
     const cuuint64_t dims[3] = {2ull * n1, n1, nz > 0 ? static_cast<cuuint64_t>(nz) : n1};
     const cuuint64_t strides[2] = {2 * es * n1, 2 * es * n1 * n1};
-    const cuuint32_t box[3] = {kind == 0 ? 2u * HX : kind == 1 ? 2u * TX : 2u * CX,
+    // kind 1 (b tiles): complex64 boxes are two columns wider (Smem::kBW)
+    const cuuint32_t box[3] = {kind == 0 ? 2u * HX : kind == 1 ? 2u * (TX + (f32 ? 2u : 0u)) : 2u * CX,
                                static_cast<cuuint32_t>(kind == 0 ? HY : kind == 1 ? TY : CY), kind == 2 ? 2u : 1u};
     const cuuint32_t estr[3] = {1u, 1u, 1u};
     const CUresult r = fn(map, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,

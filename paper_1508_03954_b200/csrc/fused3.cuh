@@ -38,8 +38,10 @@ namespace fused3 {
 // Tiles of 32 x TY points.  Two kernel shapes over the same tiles (fused3.cu
 // Cfg<R>): R = 2 rows per thread on TY / 2 thread rows (128 threads, 4 blocks
 // per SM, b tiles by TMA) and R = 1 (256 threads, 3 blocks per SM).  Measured
-// at 729^3: complex128 R = 2 -4 % fine-pass time against R = 1 (243^3 -3 %),
-// complex64 R = 1 -7 % against R = 2; TMG_F3_ROWS / TMG_F3_ROWS_C64 override.
+// at 729^3: complex128 R = 2 -4 % fine-pass time against R = 1 (243^3 -3 %);
+// complex64 R = 2 -7 % against R = 1 since session 4 of round 2 (its b tiles
+// start at the even column x0 - 1: a TMA box must start 16-byte aligned);
+// TMG_F3_ROWS / TMG_F3_ROWS_C64 override.
 #ifndef TMG_FUSED_TY
 #define TMG_FUSED_TY 8
 #endif
@@ -47,7 +49,7 @@ namespace fused3 {
 #define TMG_F3_ROWS 2
 #endif
 #ifndef TMG_F3_ROWS_C64
-#define TMG_F3_ROWS_C64 1
+#define TMG_F3_ROWS_C64 2
 #endif
 constexpr int TX = 32, TY = TMG_FUSED_TY;
 constexpr int HX = TX + 2, HY = TY + 2;
